@@ -1,0 +1,151 @@
+/*
+ * sft.h -- C ABI of the B200 butterfly sparse Fourier transform (libsft.so).
+ *
+ * Computes u_i = sum_j exp(2*pi*i * x_i . k_j / N) f_j          (eq. sfft)
+ * with Ying's butterfly algorithm (§2.2):
+ *   sft_plan   -- step 1, quadtrees/octrees T_X, T_K of non-empty boxes with
+ *                 unit-width leaves, built on the GPU;
+ *   sft_apply  -- step 2 leaf charges, step 3 per-level
+ *                 translations (fig. 1), step 4 final
+ *                 evaluation; all in hand-written sm_100a kernels;
+ *   sft_destroy.
+ *
+ * Conventions:
+ *   - dim in {2,3}; N = 2^L with 2 <= N <= 2^20; p in {5,7,9} (grid points per
+ *     axis).  Points must lie in [0,N]^dim; a point with
+ *     coordinate y belongs to leaf floor(y) (N-1 when y == N).
+ *   - Layouts: x [nx][dim], k [nk][dim] float64 row-major (torch.float64 [n,dim]);
+ *     f [nk], u [nx] complex128 with (re,im) interleaved (torch.complex128).
+ *   - Pointers may be host or device memory (detected with
+ *     cudaPointerGetAttributes).  Host buffers are staged through plan-owned
+ *     device memory inside the call (this is the "e2e" path of bench.py).
+ *   - Ownership: the caller owns x, k, f, u.  sft_plan copies what it needs
+ *     (sorted coordinates), so x and k may be freed after it returns.  The plan
+ *     owns trees, operator tables and the two live level buffers
+ *     until sft_destroy.
+ *   - Streams: all device work of a plan is ordered on opts.stream (a
+ *     cudaStream_t; NULL = legacy default stream).  sft_plan synchronises that
+ *     stream once (to size the level buffers).  sft_apply does not synchronise
+ *     unless f or u is a host pointer.
+ *   - Errors: every call returns an SFT_* status; nothing throws across the ABI;
+ *     a failed sft_plan leaves *out untouched.  sft_last_error() gives a
+ *     thread-local message for the last failure.
+ *   - Semantics: linear in f; f == 0 gives u == 0 exactly; deterministic (no
+ *     floating-point atomics; identical bits run to run and for any world size).
+ *     One plan must not be used by two concurrent sft_apply calls.
+ */
+#ifndef SFT_H_
+#define SFT_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  SFT_OK = 0,
+  SFT_E_ARG = 1,     /* bad dim/N/p/count/pointer/option */
+  SFT_E_DOMAIN = 2,  /* a coordinate is non-finite or outside [0,N] */
+  SFT_E_NOMEM = 3,   /* device or host allocation failed */
+  SFT_E_CUDA = 4,    /* CUDA runtime error (message in sft_last_error) */
+  SFT_E_STATE = 5,   /* call not valid for this plan (e.g. phase order, world size) */
+};
+
+typedef struct sft_plan_s* sft_plan_t;
+
+typedef struct {
+  int precision;      /* 0 = FP64 (the only value supported in this build) */
+  void* stream;       /* cudaStream_t for all device work; NULL = default stream */
+  int rank;           /* this rank's index, 0 <= rank < world */
+  int world;          /* number of ranks sharing the transform; 1 = single GPU */
+  int exchange_level; /* world > 1: level m of the charge exchange; -1 = choose */
+  int split_k;        /* world > 1: T_K subtree level s_K; -1 = choose */
+  int split_x;        /* world > 1: T_X subtree level s_X; -1 = choose */
+} sft_opts;
+
+/* Fill *o with defaults: FP64, NULL stream, rank 0, world 1, automatic levels. */
+void sft_default_opts(sft_opts* o);
+
+/* Step 1: build T_X from targets x and T_K from sources k.
+ * x: [nx][dim] float64, k: [nk][dim] float64 (host or device), nx, nk >= 1.
+ * Returns SFT_E_ARG for bad dim/N/p/counts/NULL pointers, SFT_E_DOMAIN for a
+ * coordinate outside [0,N] or non-finite. */
+int sft_plan(int dim, int64_t N, int p, const double* x, int64_t nx, const double* k, int64_t nk,
+             const sft_opts* opts, sft_plan_t* out);
+
+/* Steps 2-4: u = butterfly(f).  f: [nk] complex128, u: [nx]
+ * complex128, host or device.  Only valid for world == 1 plans. */
+int sft_apply(sft_plan_t plan, const void* f, void* u);
+
+/* NULL is a no-op. */
+int sft_destroy(sft_plan_t plan);
+
+const char* sft_strerror(int status);
+const char* sft_last_error(void);
+
+/* Plan statistics (host memory, caller-allocated).
+ *   counts_x, counts_k: [L+1] non-empty boxes per level of T_X / T_K (or NULL)
+ *   pairs: [L+1] pairs(t) = |T_K level t| * |T_X level L-t| (or NULL)
+ *   info[0..7]: L, p^dim, nx, nk, level-buffer bytes, plan ms (device),
+ *               groups total, translation algorithmic bytes per apply. */
+int sft_plan_stats(sft_plan_t plan, int64_t* counts_x, int64_t* counts_k, int64_t* pairs, double* info);
+
+/* Device time (ms, CUDA events on the plan stream) of the kernels of the last
+ * sft_apply when timing was enabled with sft_set_timing(plan, 1):
+ *   t_ms[0] leaf kernel, t_ms[1] sum of translation kernels, t_ms[2] final
+ *   kernel, t_ms[3] whole apply; per_level_ms [L] translation level t=0..L-1
+ *   (or NULL). */
+int sft_set_timing(sft_plan_t plan, int enable);
+int sft_last_timing(sft_plan_t plan, double* t_ms, double* per_level_ms);
+
+/* ---- multi-GPU (world > 1), SURVEY.md §8(e) ----------------------------
+ * Phase 1 (levels t = L..m) over this rank's T_K subtrees at level s_K,
+ * one all-to-all of the level-m charges, phase 2 (t = m-1..0 and step 4) over
+ * this rank's T_X subtrees at level s_X.  The collective itself is issued by
+ * the caller (torch.distributed over NCCL) between the two calls.
+ *
+ * sft_exchange_counts: send_counts/recv_counts [world] in complex128 elements
+ *   (contiguous per-peer segments in rank order).
+ * sft_apply_phase1(plan, f, sendbuf): f [nk] (all sources); sendbuf device,
+ *   >= sum(send_counts) complex128.
+ * sft_apply_phase2(plan, recvbuf, u): recvbuf device with the peers' segments
+ *   concatenated in rank order; u [nx] is fully overwritten: this rank's
+ *   targets get their values, all others 0 (sum-reduce across ranks to
+ *   assemble; every entry has exactly one non-zero contributor). */
+int sft_exchange_counts(sft_plan_t plan, int64_t* send_counts, int64_t* recv_counts);
+int sft_apply_phase1(sft_plan_t plan, const void* f, void* sendbuf);
+int sft_apply_phase2(sft_plan_t plan, const void* recvbuf, void* u);
+
+/* Partition actually used by a world > 1 plan (host, caller-allocated):
+ * part[0..2] = s_K, s_X, m; then for every rank r: part[3+4r .. 3+4r+3] =
+ * [first, last) T_K box range at level s_K and [first, last) T_X box range at
+ * level s_X owned by r (Morton order, contiguous). */
+int sft_partition_info(sft_plan_t plan, int64_t* part);
+
+/* Host-only partitioner (no GPU needed; sft_plan calls the same routine).
+ * counts_x/counts_k: [L+1] non-empty boxes per level; parent_x/parent_k: [L+1]
+ * pointers, parent_*[l] = [counts[l]] int32 parent index (level l-1) of each
+ * box at level l (entry 0 unused).  force_*: -1 = choose, else use the value.
+ * Chooses (s_K, s_X, m) and contiguous subtree ranges minimising
+ *   max_r phase-1 pairs + max_r phase-2 pairs + 4 * max_r exchanged pairs
+ * (pairs ~ p^d*16 bytes of HBM traffic each; one exchanged pair over NVLink
+ * costs ~4 pairs of HBM time).  out: [3 + 4*world] laid out as in
+ * sft_partition_info; out_cost (may be NULL): [3] the three max terms. */
+int sft_choose_partition(int L, int world, const int64_t* counts_x, const int64_t* counts_k,
+                         const int32_t* const* parent_x, const int32_t* const* parent_k, int force_sk,
+                         int force_sx, int force_m, int64_t* out, int64_t* out_cost);
+
+/* Diagnostics (host only, no GPU): the constant operator tables the kernels
+ * use for grid size p (3 <= p <= 15), built in long double from the
+ * Lagrange / sine-product closed forms:
+ *   V    [2][2][p][p] complex128 interleaved, V[alpha][beta][m][l'];
+ *   invD [p] leaf-weight normalisers 1/prod_{q!=m} sin(pi (m-q)/(p-1)^2).
+ * Either pointer may be NULL. */
+int sft_operator_tables(int p, double* V, double* invD);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SFT_H_ */

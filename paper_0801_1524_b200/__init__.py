@@ -1,0 +1,257 @@
+"""B200-native butterfly sparse Fourier transform (Ying, arXiv 0801.1524).
+
+Thin ctypes binding of ``libsft.so`` (C ABI in ``include/sft.h``).  This
+module only marshals arguments: every step of the transform -- tree build,
+leaf charges, per-level translations, final evaluation -- runs in the
+library's sm_100a kernels.  There is no CPU fallback: if the library is
+missing or no CUDA device is present, calls raise.
+
+    plan = Plan(dim, N, p, x, k)        # sft_plan
+    u = plan.apply(f)                   # sft_apply
+    plan.close()                        # sft_destroy
+
+x [nx, dim] float64, k [nk, dim] float64, f [nk] complex128: torch tensors
+(CUDA or pinned/pageable CPU) or numpy arrays.  Host buffers are staged by the
+library (the end-to-end path).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+__all__ = ["Plan", "lib", "LIB_PATH", "SftError", "operator_tables", "choose_partition", "HEADER_SYMBOLS"]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsft.so")
+HEADER = os.path.join(os.path.dirname(_HERE), "include", "sft.h")
+
+_c_i64p = ctypes.POINTER(ctypes.c_int64)
+_c_dp = ctypes.POINTER(ctypes.c_double)
+
+
+class SftError(RuntimeError):
+    pass
+
+
+class _Opts(ctypes.Structure):
+    _fields_ = [("precision", ctypes.c_int), ("stream", ctypes.c_void_p), ("rank", ctypes.c_int),
+                ("world", ctypes.c_int), ("exchange_level", ctypes.c_int), ("split_k", ctypes.c_int),
+                ("split_x", ctypes.c_int)]
+
+
+_lib = None
+
+
+def _header_symbols():
+    import re
+    txt = open(HEADER).read()
+    return sorted(set(re.findall(r"^\s*(?:int|void|const char\*)\s+(sft_\w+)\s*\(", txt, re.M)))
+
+
+HEADER_SYMBOLS = _header_symbols() if os.path.exists(HEADER) else []
+
+
+def lib():
+    """Load libsft.so (built by ``paper_0801_1524_b200/build.py`` / ``__graft_entry__.build``)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise SftError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    L = ctypes.CDLL(LIB_PATH)
+    vp = ctypes.c_void_p
+    L.sft_default_opts.argtypes = [ctypes.POINTER(_Opts)]
+    L.sft_default_opts.restype = None
+    L.sft_plan.argtypes = [ctypes.c_int, ctypes.c_int64, ctypes.c_int, vp, ctypes.c_int64, vp, ctypes.c_int64,
+                           ctypes.POINTER(_Opts), ctypes.POINTER(vp)]
+    L.sft_apply.argtypes = [vp, vp, vp]
+    L.sft_destroy.argtypes = [vp]
+    L.sft_strerror.argtypes = [ctypes.c_int]
+    L.sft_strerror.restype = ctypes.c_char_p
+    L.sft_last_error.argtypes = []
+    L.sft_last_error.restype = ctypes.c_char_p
+    L.sft_plan_stats.argtypes = [vp, _c_i64p, _c_i64p, _c_i64p, _c_dp]
+    L.sft_set_timing.argtypes = [vp, ctypes.c_int]
+    L.sft_last_timing.argtypes = [vp, _c_dp, _c_dp]
+    L.sft_exchange_counts.argtypes = [vp, _c_i64p, _c_i64p]
+    L.sft_apply_phase1.argtypes = [vp, vp, vp]
+    L.sft_apply_phase2.argtypes = [vp, vp, vp]
+    L.sft_partition_info.argtypes = [vp, _c_i64p]
+    L.sft_choose_partition.argtypes = [ctypes.c_int, ctypes.c_int, _c_i64p, _c_i64p,
+                                       ctypes.POINTER(ctypes.POINTER(ctypes.c_int32)),
+                                       ctypes.POINTER(ctypes.POINTER(ctypes.c_int32)), ctypes.c_int, ctypes.c_int,
+                                       ctypes.c_int, _c_i64p, _c_i64p]
+    L.sft_operator_tables.argtypes = [ctypes.c_int, _c_dp, _c_dp]
+    _lib = L
+    return L
+
+
+def _check(rc):
+    if rc != 0:
+        L = lib()
+        raise SftError(f"{L.sft_strerror(rc).decode()} ({rc}): {L.sft_last_error().decode()}")
+
+
+def _ptr(a, dtype_np, shape_last=None):
+    """Return (pointer, keepalive) for a torch tensor or numpy array, contiguous, right dtype."""
+    try:
+        import torch
+        if isinstance(a, torch.Tensor):
+            want = {np.float64: torch.float64, np.complex128: torch.complex128}[dtype_np]
+            if a.dtype != want or not a.is_contiguous():
+                a = a.to(want).contiguous()
+            return ctypes.c_void_p(a.data_ptr()), a
+    except ImportError:  # pragma: no cover
+        pass
+    a = np.ascontiguousarray(a, dtype=dtype_np)
+    return ctypes.c_void_p(a.ctypes.data), a
+
+
+def _stream_handle(stream):
+    if stream is None:
+        try:
+            import torch
+            if torch.cuda.is_available():
+                return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+        except ImportError:  # pragma: no cover
+            pass
+        return ctypes.c_void_p(0)
+    if isinstance(stream, int):
+        return ctypes.c_void_p(stream)
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+class Plan:
+    """sft_plan / sft_apply / sft_destroy (include/sft.h)."""
+
+    def __init__(self, dim, N, p, x, k, stream=None, rank=0, world=1, exchange_level=-1, split_k=-1, split_x=-1):
+        L = lib()
+        o = _Opts()
+        L.sft_default_opts(ctypes.byref(o))
+        o.stream = _stream_handle(stream)
+        o.rank, o.world = int(rank), int(world)
+        o.exchange_level, o.split_k, o.split_x = int(exchange_level), int(split_k), int(split_x)
+        xp, self._x = _ptr(x, np.float64)
+        kp, self._k = _ptr(k, np.float64)
+        self.dim, self.N, self.p = int(dim), int(N), int(p)
+        self.nx = int(self._x.shape[0]) if len(self._x.shape) else 0
+        self.nk = int(self._k.shape[0]) if len(self._k.shape) else 0
+        self.world, self.rank = int(world), int(rank)
+        self.L = int(N).bit_length() - 1
+        h = ctypes.c_void_p()
+        _check(L.sft_plan(self.dim, self.N, self.p, xp, self.nx, kp, self.nk, ctypes.byref(o), ctypes.byref(h)))
+        self._h = h
+        self._x = self._k = None  # the plan copied what it needs
+
+    # -- single GPU ---------------------------------------------------------
+    def apply(self, f, u=None):
+        """u = butterfly(f).  If ``u`` is None a buffer like ``f`` (device or host) is allocated."""
+        fp, fk = _ptr(f, np.complex128)
+        if u is None:
+            u = self._like(fk, self.nx)
+        up, uk = _ptr(u, np.complex128)
+        _check(lib().sft_apply(self._h, fp, up))
+        return uk
+
+    @staticmethod
+    def _like(ref, n):
+        try:
+            import torch
+            if isinstance(ref, torch.Tensor):
+                return torch.empty(n, dtype=torch.complex128, device=ref.device,
+                                   pin_memory=(ref.device.type == "cpu" and ref.is_pinned()))
+        except ImportError:  # pragma: no cover
+            pass
+        return np.empty(n, dtype=np.complex128)
+
+    # -- multi GPU (see paper_0801_1524_b200.dist) ---------------------------
+    def exchange_counts(self):
+        s = np.zeros(self.world, np.int64)
+        r = np.zeros(self.world, np.int64)
+        _check(lib().sft_exchange_counts(self._h, s.ctypes.data_as(_c_i64p), r.ctypes.data_as(_c_i64p)))
+        return s, r
+
+    def partition(self):
+        out = np.zeros(3 + 4 * self.world, np.int64)
+        _check(lib().sft_partition_info(self._h, out.ctypes.data_as(_c_i64p)))
+        return out
+
+    def apply_phase1(self, f, sendbuf):
+        fp, fk = _ptr(f, np.complex128)
+        sp, _ = _ptr(sendbuf, np.complex128)
+        _check(lib().sft_apply_phase1(self._h, fp, sp))
+
+    def apply_phase2(self, recvbuf, u):
+        rp, _ = _ptr(recvbuf, np.complex128)
+        up, _ = _ptr(u, np.complex128)
+        _check(lib().sft_apply_phase2(self._h, rp, up))
+
+    # -- stats / timing -------------------------------------------------------
+    def stats(self):
+        n = self.L + 1
+        cx = np.zeros(n, np.int64); ck = np.zeros(n, np.int64); pr = np.zeros(n, np.int64)
+        info = np.zeros(8)
+        _check(lib().sft_plan_stats(self._h, cx.ctypes.data_as(_c_i64p), ck.ctypes.data_as(_c_i64p),
+                                    pr.ctypes.data_as(_c_i64p), info.ctypes.data_as(_c_dp)))
+        keys = ["L", "pd", "nx", "nk", "level_buffer_bytes", "plan_ms", "groups", "trans_alg_bytes"]
+        d = dict(zip(keys, info.tolist()))
+        d.update(counts_x=cx, counts_k=ck, pairs=pr)
+        return d
+
+    def set_timing(self, on=True):
+        _check(lib().sft_set_timing(self._h, 1 if on else 0))
+
+    def last_timing(self):
+        t = np.zeros(4); lv = np.zeros(max(self.L, 1))
+        _check(lib().sft_last_timing(self._h, t.ctypes.data_as(_c_dp), lv.ctypes.data_as(_c_dp)))
+        return dict(leaf_ms=t[0], trans_ms=t[1], final_ms=t[2], apply_ms=t[3], level_ms=lv[: self.L])
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().sft_destroy(self._h)
+            self._h = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+
+def operator_tables(p):
+    """Host-only: (V [2,2,p,p] complex128, invD [p]) exactly as uploaded to the GPU."""
+    V = np.zeros(2 * 4 * p * p)
+    invD = np.zeros(p)
+    _check(lib().sft_operator_tables(p, V.ctypes.data_as(_c_dp), invD.ctypes.data_as(_c_dp)))
+    return V.view(np.complex128).reshape(2, 2, p, p), invD
+
+
+def choose_partition(L, world, counts_x, counts_k, parents_x, parents_k, force=(-1, -1, -1)):
+    """Host-only partitioner (sft_choose_partition).  parents_*[l] int32 arrays for l=1..L
+    (index 0 ignored).  Returns (s_K, s_X, m, ranges [world,4], cost [3])."""
+    cx = np.ascontiguousarray(counts_x, np.int64)
+    ck = np.ascontiguousarray(counts_k, np.int64)
+    keep = []
+
+    def parr(ps):
+        arr = (ctypes.POINTER(ctypes.c_int32) * (L + 1))()
+        for l in range(1, L + 1):
+            a = np.ascontiguousarray(ps[l], np.int32)
+            keep.append(a)
+            arr[l] = a.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+        return arr
+
+    out = np.zeros(3 + 4 * world, np.int64)
+    cost = np.zeros(3, np.int64)
+    _check(lib().sft_choose_partition(L, world, cx.ctypes.data_as(_c_i64p), ck.ctypes.data_as(_c_i64p),
+                                      parr(parents_x), parr(parents_k), force[0], force[1], force[2],
+                                      out.ctypes.data_as(_c_i64p), cost.ctypes.data_as(_c_i64p)))
+    return int(out[0]), int(out[1]), int(out[2]), out[3:].reshape(world, 4), cost

@@ -1,0 +1,700 @@
+// api.cu -- the C ABI of include/sft.h: plan / apply / destroy and the
+// multi-GPU phase calls.  Host orchestration only; every arithmetic step of
+// the transform runs in the kernels of tree.cu and kernels.cu.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "sft_internal.cuh"
+
+using namespace sft;
+
+static thread_local std::string g_last_error;
+
+static int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+#define CKR(x)                                                                   \
+  do {                                                                           \
+    cudaError_t e_ = (x);                                                        \
+    if (e_ != cudaSuccess)                                                       \
+      return fail(SFT_E_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_));  \
+  } while (0)
+
+static bool is_device_ptr(const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();  // clear
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+static int64_t ipow64(int b, int e) {
+  int64_t r = 1;
+  while (e-- > 0) r *= b;
+  return r;
+}
+
+extern "C" void sft_default_opts(sft_opts* o) {
+  if (!o) return;
+  o->precision = 0;
+  o->stream = nullptr;
+  o->rank = 0;
+  o->world = 1;
+  o->exchange_level = -1;
+  o->split_k = -1;
+  o->split_x = -1;
+}
+
+extern "C" const char* sft_strerror(int status) {
+  switch (status) {
+    case SFT_OK: return "ok";
+    case SFT_E_ARG: return "invalid argument";
+    case SFT_E_DOMAIN: return "coordinate outside [0,N] or non-finite";
+    case SFT_E_NOMEM: return "out of memory";
+    case SFT_E_CUDA: return "CUDA error";
+    case SFT_E_STATE: return "invalid call for this plan";
+    default: return "unknown status";
+  }
+}
+
+extern "C" const char* sft_last_error(void) { return g_last_error.c_str(); }
+
+// ---------------------------------------------------------------------------
+// ranges of descendants (Morton order keeps every subtree contiguous)
+// ---------------------------------------------------------------------------
+// For boxes [lo, hi) at level s, the descendant range at level l >= s is
+// [first index at l whose ancestor at s is >= lo, ... >= hi).  Computed on the
+// host from parent arrays.
+static void descend_ranges(const std::vector<std::vector<int32_t>>& parent, int s, int64_t lo, int64_t hi, int L,
+                           std::vector<LevelRange>& out) {
+  out.assign(L + 1, LevelRange());
+  out[s].lo = lo;
+  out[s].hi = hi;
+  // ancestor-at-s of each box at deeper levels, level by level
+  std::vector<int32_t> anc_prev, anc;
+  for (int l = s + 1; l <= L; ++l) {
+    const std::vector<int32_t>& par = parent[l];
+    anc.resize(par.size());
+    for (size_t i = 0; i < par.size(); ++i) anc[i] = (l == s + 1) ? par[i] : anc_prev[par[i]];
+    out[l].lo = std::lower_bound(anc.begin(), anc.end(), (int32_t)lo) - anc.begin();
+    out[l].hi = std::lower_bound(anc.begin(), anc.end(), (int32_t)hi) - anc.begin();
+    anc_prev.swap(anc);
+  }
+  for (int l = 0; l < s; ++l) out[l].lo = out[l].hi = 0;  // unused
+}
+
+// ---------------------------------------------------------------------------
+// host partitioner; exposed as sft_choose_partition
+// ---------------------------------------------------------------------------
+// Per-box descendant counts at each level for every box at split level s:
+//   cnt[l][i] = number of descendants at level l of box i (level s).
+static std::vector<std::vector<int64_t>> desc_counts(const std::vector<std::vector<int32_t>>& parent,
+                                                     const std::vector<int64_t>& counts, int s, int L) {
+  std::vector<std::vector<int64_t>> cnt(L + 1, std::vector<int64_t>(counts[s], 0));
+  std::vector<int32_t> anc_prev, anc;
+  for (int64_t i = 0; i < counts[s]; ++i) cnt[s][i] = 1;
+  for (int l = s + 1; l <= L; ++l) {
+    anc.resize(counts[l]);
+    for (int64_t i = 0; i < counts[l]; ++i) {
+      anc[i] = (l == s + 1) ? parent[l][i] : anc_prev[parent[l][i]];
+      cnt[l][anc[i]]++;
+    }
+    anc_prev.swap(anc);
+  }
+  return cnt;
+}
+
+// contiguous split of weights w[0..n) into k chunks minimising the max chunk
+// (binary search on the bottleneck + greedy), returns boundaries [k+1]
+static std::vector<int64_t> linear_partition(const std::vector<int64_t>& w, int k) {
+  const int64_t n = (int64_t)w.size();
+  int64_t lo = 0, hi = 0;
+  for (int64_t v : w) {
+    lo = std::max(lo, v);
+    hi += v;
+  }
+  auto feasible = [&](int64_t cap, std::vector<int64_t>* b) {
+    int used = 1;
+    int64_t cur = 0;
+    if (b) {
+      b->assign(1, 0);
+    }
+    for (int64_t i = 0; i < n; ++i) {
+      if (cur + w[i] > cap) {
+        ++used;
+        cur = 0;
+        if (b) b->push_back(i);
+      }
+      cur += w[i];
+    }
+    return used <= k;
+  };
+  while (lo < hi) {
+    int64_t mid = lo + (hi - lo) / 2;
+    if (feasible(mid, nullptr)) hi = mid; else lo = mid + 1;
+  }
+  std::vector<int64_t> b;
+  feasible(lo, &b);
+  while ((int)b.size() < k) b.push_back(n);  // empty trailing chunks
+  b.push_back(n);
+  return b;
+}
+
+static int choose_partition(int L, int world, const std::vector<int64_t>& cx, const std::vector<int64_t>& ck,
+                            const std::vector<std::vector<int32_t>>& px, const std::vector<std::vector<int32_t>>& pk,
+                            int force_sk, int force_sx, int force_m, Partition& best, int64_t* best_cost) {
+  int64_t best_total = -1;
+  // candidate split levels: forced value, else levels with at least `world`
+  // subtrees and few enough (<= 64 per rank) that the search stays cheap;
+  // fall back to every level if none qualifies
+  auto candidates = [&](const std::vector<int64_t>& c, int force) {
+    std::vector<int> v;
+    if (force >= 0) {
+      if (force <= L) v.push_back(force);
+      return v;
+    }
+    for (int s = 0; s <= L; ++s)
+      if (c[s] >= world && c[s] <= 64 * (int64_t)world) v.push_back(s);
+    if (v.empty())
+      for (int s = 0; s <= L; ++s)
+        if (c[s] <= 64 * (int64_t)world) v.push_back(s);
+    return v;
+  };
+  std::vector<int> cand_k = candidates(ck, force_sk), cand_x = candidates(cx, force_sx);
+  std::vector<std::vector<std::vector<int64_t>>> DK(L + 1), DX(L + 1);
+  for (int s : cand_k) DK[s] = desc_counts(pk, ck, s, L);
+  for (int s : cand_x) DX[s] = desc_counts(px, cx, s, L);
+  // pairs(t) = ck[t] * cx[L-t]
+  for (int sk : cand_k) {
+    const auto& dk = DK[sk];
+    for (int sx : cand_x) {
+      const auto& dx = DX[sx];
+      for (int m = sk; m <= L - sx; ++m) {
+        if (force_m >= 0 && m != force_m) continue;
+        // phase-1 work of T_K box i at sk: sum_{t=m..L} desc_t(i) * cx[L-t]
+        std::vector<int64_t> wk(ck[sk], 0), wx(cx[sx], 0);
+        for (int64_t i = 0; i < ck[sk]; ++i)
+          for (int t = m; t <= L; ++t) wk[i] += dk[t][i] * cx[L - t];
+        // phase-2 work of T_X box i at sx: sum_{t=0..m-1} desc_{L-t}(i) * ck[t] + leaves (final)
+        for (int64_t i = 0; i < cx[sx]; ++i) {
+          for (int t = 0; t < m; ++t) wx[i] += dx[L - t][i] * ck[t];
+          wx[i] += dx[L][i];
+        }
+        auto bk = linear_partition(wk, world);
+        auto bx = linear_partition(wx, world);
+        int64_t max1 = 0, max2 = 0, maxx = 0;
+        // exchange: sender r sends its B(m) rows x (A at L-m not owned by r)
+        std::vector<int64_t> a_own(world, 0);
+        for (int r = 0; r < world; ++r) {
+          int64_t s1 = 0, s2 = 0;
+          for (int64_t i = bk[r]; i < bk[r + 1]; ++i) s1 += wk[i];
+          for (int64_t i = bx[r]; i < bx[r + 1]; ++i) s2 += wx[i];
+          max1 = std::max(max1, s1);
+          max2 = std::max(max2, s2);
+          for (int64_t i = bx[r]; i < bx[r + 1]; ++i) a_own[r] += dx[L - m][i];
+        }
+        for (int r = 0; r < world; ++r) {
+          int64_t nb = 0;
+          for (int64_t i = bk[r]; i < bk[r + 1]; ++i) nb += dk[m][i];
+          int64_t sent = nb * (cx[L - m] - a_own[r]);
+          int64_t recv = a_own[r] * (ck[m] - nb);
+          maxx = std::max(maxx, std::max(sent, recv));
+        }
+        int64_t total = max1 + max2 + 4 * maxx;
+        if (best_total < 0 || total < best_total) {
+          best_total = total;
+          best.sk = sk;
+          best.sx = sx;
+          best.m = m;
+          best.k_lo.assign(bk.begin(), bk.end() - 1);
+          best.k_hi.assign(bk.begin() + 1, bk.end());
+          best.x_lo.assign(bx.begin(), bx.end() - 1);
+          best.x_hi.assign(bx.begin() + 1, bx.end());
+          if (best_cost) {
+            best_cost[0] = max1;
+            best_cost[1] = max2;
+            best_cost[2] = maxx;
+          }
+        }
+      }
+    }
+  }
+  return best_total < 0 ? SFT_E_ARG : SFT_OK;
+}
+
+extern "C" int sft_choose_partition(int L, int world, const int64_t* counts_x, const int64_t* counts_k,
+                                    const int32_t* const* parent_x, const int32_t* const* parent_k, int force_sk,
+                                    int force_sx, int force_m, int64_t* out, int64_t* out_cost) {
+  if (L < 1 || L > 20 || world < 1 || !counts_x || !counts_k || !parent_x || !parent_k || !out)
+    return fail(SFT_E_ARG, "sft_choose_partition: bad arguments");
+  std::vector<int64_t> cx(counts_x, counts_x + L + 1), ck(counts_k, counts_k + L + 1);
+  std::vector<std::vector<int32_t>> px(L + 1), pk(L + 1);
+  for (int l = 1; l <= L; ++l) {
+    px[l].assign(parent_x[l], parent_x[l] + cx[l]);
+    pk[l].assign(parent_k[l], parent_k[l] + ck[l]);
+  }
+  Partition part;
+  int rc = choose_partition(L, world, cx, ck, px, pk, force_sk, force_sx, force_m, part, out_cost);
+  if (rc) return fail(rc, "sft_choose_partition: no feasible (s_K, s_X, m)");
+  out[0] = part.sk;
+  out[1] = part.sx;
+  out[2] = part.m;
+  for (int r = 0; r < world; ++r) {
+    out[3 + 4 * r] = part.k_lo[r];
+    out[4 + 4 * r] = part.k_hi[r];
+    out[5 + 4 * r] = part.x_lo[r];
+    out[6 + 4 * r] = part.x_hi[r];
+  }
+  return SFT_OK;
+}
+
+// ---------------------------------------------------------------------------
+// plan
+// ---------------------------------------------------------------------------
+static void plan_free(sft_plan_s* P) {
+  if (!P) return;
+  cudaStream_t s = P->stream;
+  free_tree(P->X, s);
+  free_tree(P->K, s);
+  for (int i = 0; i < 2; ++i)
+    if (P->buf[i]) cudaFreeAsync(P->buf[i], s);
+  if (P->f_stage) cudaFreeAsync(P->f_stage, s);
+  if (P->u_stage) cudaFreeAsync(P->u_stage, s);
+  if (P->d_err) cudaFreeAsync(P->d_err, s);
+  if (P->d_seg) cudaFreeAsync(P->d_seg, s);
+  for (int i = 0; i < P->ev_created; ++i) cudaEventDestroy(P->ev[i]);
+  cudaStreamSynchronize(s);
+  delete P;
+}
+
+static int supported_p(int d, int p) { return (d == 2 || d == 3) && (p == 5 || p == 7 || p == 9); }
+
+extern "C" int sft_plan(int dim, int64_t N, int p, const double* x, int64_t nx, const double* k, int64_t nk,
+                        const sft_opts* opts, sft_plan_t* out) {
+  if (!out) return fail(SFT_E_ARG, "out is NULL");
+  if (dim != 2 && dim != 3) return fail(SFT_E_ARG, "dim must be 2 or 3");
+  if (N < 2 || N > (1 << 20) || (N & (N - 1))) return fail(SFT_E_ARG, "N must be a power of two in [2, 2^20]");
+  if (!supported_p(dim, p)) return fail(SFT_E_ARG, "p must be 5, 7 or 9");
+  if (nx < 1 || nk < 1 || nx > INT32_MAX || nk > INT32_MAX) return fail(SFT_E_ARG, "point counts must be >= 1");
+  if (!x || !k) return fail(SFT_E_ARG, "x or k is NULL");
+  sft_opts o;
+  sft_default_opts(&o);
+  if (opts) o = *opts;
+  if (o.precision != 0) return fail(SFT_E_ARG, "only precision 0 (FP64) is built");
+  if (o.world < 1 || o.rank < 0 || o.rank >= o.world) return fail(SFT_E_ARG, "bad rank/world");
+
+  sft_plan_s* P = new (std::nothrow) sft_plan_s();
+  if (!P) return fail(SFT_E_NOMEM, "host allocation failed");
+  P->d = dim;
+  P->p = p;
+  P->N = N;
+  int L = 0;
+  while ((int64_t(1) << L) < N) ++L;
+  P->L = L;
+  P->nx = nx;
+  P->nk = nk;
+  P->rank = o.rank;
+  P->world = o.world;
+  P->stream = (cudaStream_t)o.stream;
+  cudaStream_t s = P->stream;
+
+  // stream-ordered allocations: keep freed memory in the pool so plan/destroy
+  // cycles do not go back to the driver
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  }
+  std::string err;
+  P->tab = get_device_tables(p, &err);
+  if (!P->tab) {
+    delete P;
+    return fail(SFT_E_CUDA, err);
+  }
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0, s);
+  auto bail = [&](int code, const std::string& m) {
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    plan_free(P);
+    return fail(code, m);
+  };
+  if (cudaMallocAsync(&P->d_err, sizeof(int), s) != cudaSuccess) return bail(SFT_E_NOMEM, "alloc");
+  cudaMemsetAsync(P->d_err, 0, sizeof(int), s);
+
+  // stage host coordinates
+  const double* xd = x;
+  const double* kd = k;
+  double* xs = nullptr;
+  double* ks = nullptr;
+  if (!is_device_ptr(x)) {
+    if (cudaMallocAsync(&xs, nx * dim * sizeof(double), s) != cudaSuccess) return bail(SFT_E_NOMEM, "alloc x");
+    cudaMemcpyAsync(xs, x, nx * dim * sizeof(double), cudaMemcpyHostToDevice, s);
+    xd = xs;
+  }
+  if (!is_device_ptr(k)) {
+    if (cudaMallocAsync(&ks, nk * dim * sizeof(double), s) != cudaSuccess) return bail(SFT_E_NOMEM, "alloc k");
+    cudaMemcpyAsync(ks, k, nk * dim * sizeof(double), cudaMemcpyHostToDevice, s);
+    kd = ks;
+  }
+  int rc = build_trees(P, xd, kd, &err);
+  if (xs) cudaFreeAsync(xs, s);
+  if (ks) cudaFreeAsync(ks, s);
+  if (rc) return bail(rc, err);
+
+  // level buffers: max over t of (local) pairs(t)
+  const int64_t PD = ipow64(p, dim);
+  if (P->world > 1) {
+    // partition + per-rank ranges; needs parent arrays on the host
+    std::vector<std::vector<int32_t>> px(L + 1), pk(L + 1);
+    for (int l = 1; l <= L; ++l) {
+      px[l].resize(P->X.counts[l]);
+      pk[l].resize(P->K.counts[l]);
+      cudaMemcpyAsync(px[l].data(), P->X.lev[l].parent, px[l].size() * sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+      cudaMemcpyAsync(pk[l].data(), P->K.lev[l].parent, pk[l].size() * sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+    }
+    if (cudaStreamSynchronize(s) != cudaSuccess) return bail(SFT_E_CUDA, "sync");
+    int64_t cost[3];
+    if (choose_partition(L, P->world, P->X.counts, P->K.counts, px, pk, o.split_k, o.split_x, o.exchange_level,
+                         P->part, cost))
+      return bail(SFT_E_ARG, "no feasible partition for the requested split levels");
+    const Partition& pt = P->part;
+    descend_ranges(pk, pt.sk, pt.k_lo[P->rank], pt.k_hi[P->rank], L, P->k_rng);
+    descend_ranges(px, pt.sx, pt.x_lo[P->rank], pt.x_hi[P->rank], L, P->x_rng);
+    // exchange layout at level m: A boundaries at level L-m for every rank
+    const int m = pt.m, W = P->world;
+    std::vector<int64_t> abound(W + 1), nb_of(W);
+    std::vector<LevelRange> tmp;
+    for (int q = 0; q < W; ++q) {
+      descend_ranges(px, pt.sx, pt.x_lo[q], pt.x_hi[q], L, tmp);
+      abound[q] = tmp[L - m].lo;
+      abound[q + 1] = tmp[L - m].hi;
+      descend_ranges(pk, pt.sk, pt.k_lo[q], pt.k_hi[q], L, tmp);
+      nb_of[q] = tmp[m].hi - tmp[m].lo;
+    }
+    const int64_t my_nb = P->k_rng[m].hi - P->k_rng[m].lo;
+    const int64_t my_na = abound[P->rank + 1] - abound[P->rank];
+    P->send_counts.assign(W, 0);
+    P->recv_counts.assign(W, 0);
+    std::vector<int64_t> seg(2 * W + 1, 0);
+    int64_t base = 0;
+    for (int q = 0; q < W; ++q) {
+      seg[q] = abound[q];
+      seg[W + 1 + q] = base;  // pair offset of segment q in the send buffer
+      P->send_counts[q] = my_nb * (abound[q + 1] - abound[q]) * PD;
+      P->recv_counts[q] = nb_of[q] * my_na * PD;
+      base += my_nb * (abound[q + 1] - abound[q]);
+    }
+    seg[W] = abound[W];
+    if (cudaMallocAsync(&P->d_seg, seg.size() * sizeof(int64_t), s) != cudaSuccess) return bail(SFT_E_NOMEM, "seg");
+    cudaMemcpyAsync(P->d_seg, seg.data(), seg.size() * sizeof(int64_t), cudaMemcpyHostToDevice, s);
+    int64_t mx = 0;
+    for (int t = m; t <= L; ++t) mx = std::max(mx, (P->k_rng[t].hi - P->k_rng[t].lo) * P->X.counts[L - t]);
+    for (int t = 0; t <= m; ++t) mx = std::max(mx, P->K.counts[t] * (P->x_rng[L - t].hi - P->x_rng[L - t].lo));
+    P->buf_elems = (size_t)mx * PD;
+  } else {
+    int64_t mx = 0;
+    for (int t = 0; t <= L; ++t) mx = std::max(mx, P->K.counts[t] * P->X.counts[L - t]);
+    P->buf_elems = (size_t)mx * PD;
+    P->k_rng.assign(L + 1, LevelRange());
+    P->x_rng.assign(L + 1, LevelRange());
+    for (int l = 0; l <= L; ++l) {
+      P->k_rng[l].hi = P->K.counts[l];
+      P->x_rng[l].hi = P->X.counts[l];
+    }
+  }
+  for (int i = 0; i < 2; ++i)
+    if (cudaMallocAsync(&P->buf[i], P->buf_elems * sizeof(double2), s) != cudaSuccess)
+      return bail(SFT_E_NOMEM, "level buffer allocation failed");
+  cudaEventRecord(e1, s);
+  if (cudaEventSynchronize(e1) != cudaSuccess) return bail(SFT_E_CUDA, "plan sync failed");
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  P->plan_ms = ms;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaError_t ce = cudaGetLastError();
+  if (ce != cudaSuccess) {
+    plan_free(P);
+    return fail(SFT_E_CUDA, cudaGetErrorString(ce));
+  }
+  *out = P;
+  return SFT_OK;
+}
+
+extern "C" int sft_destroy(sft_plan_t plan) {
+  plan_free(plan);
+  return SFT_OK;
+}
+
+// ---------------------------------------------------------------------------
+// apply
+// ---------------------------------------------------------------------------
+static void tmark(sft_plan_s* P) {
+  if (!P->timing) return;
+  if (P->n_ev < 64) cudaEventRecord(P->ev[P->n_ev++], P->stream);
+}
+
+static LevelDims level_dims(const sft_plan_s* P, int t) {
+  const int L = P->L;
+  LevelDims ld;
+  ld.t = t;
+  ld.cbK = P->K.lev[t].child_begin;
+  ld.mK = P->K.lev[t].child_mask;
+  ld.cbX = P->X.lev[L - t - 1].child_begin;
+  ld.mX = P->X.lev[L - t - 1].child_mask;
+  ld.seg = nullptr;
+  ld.nseg = 0;
+  return ld;
+}
+
+// Phase-1 style level (B restricted to this rank's T_K range, all A).
+static LevelDims level_dims_k(const sft_plan_s* P, int t) {
+  const int L = P->L;
+  LevelDims ld = level_dims(P, t);
+  ld.b_lo = P->k_rng[t].lo;
+  ld.b_hi = P->k_rng[t].hi;
+  ld.ap_lo = 0;
+  ld.ap_hi = P->X.counts[L - t - 1];
+  ld.in_b0 = P->k_rng[t + 1].lo;
+  ld.in_nA = P->X.counts[L - t - 1];
+  ld.in_a0 = 0;
+  ld.out_b0 = P->k_rng[t].lo;
+  ld.out_nA = P->X.counts[L - t];
+  ld.out_a0 = 0;
+  return ld;
+}
+
+// Phase-2 style level (all B, A restricted to this rank's T_X range).
+static LevelDims level_dims_x(const sft_plan_s* P, int t) {
+  const int L = P->L;
+  LevelDims ld = level_dims(P, t);
+  ld.b_lo = 0;
+  ld.b_hi = P->K.counts[t];
+  ld.ap_lo = P->x_rng[L - t - 1].lo;
+  ld.ap_hi = P->x_rng[L - t - 1].hi;
+  ld.in_b0 = 0;
+  ld.in_nA = P->x_rng[L - t - 1].hi - P->x_rng[L - t - 1].lo;
+  ld.in_a0 = P->x_rng[L - t - 1].lo;
+  ld.out_b0 = 0;
+  ld.out_nA = P->x_rng[L - t].hi - P->x_rng[L - t].lo;
+  ld.out_a0 = P->x_rng[L - t].lo;
+  return ld;
+}
+
+static int finish_timing(sft_plan_s* P, int n_levels_first) {
+  if (!P->timing) return SFT_OK;
+  CKR(cudaEventSynchronize(P->ev[P->n_ev - 1]));
+  // events: [0] start, [1] after leaf, [2..] after each level, [n-1] after final
+  float ms;
+  P->level_ms.assign(P->L, 0.0);
+  double trans = 0;
+  cudaEventElapsedTime(&ms, P->ev[0], P->ev[1]);
+  P->last_ms[0] = ms;
+  int nlev = P->n_ev - 3;
+  for (int i = 0; i < nlev; ++i) {
+    cudaEventElapsedTime(&ms, P->ev[1 + i], P->ev[2 + i]);
+    int t = n_levels_first - i;
+    if (t >= 0 && t < P->L) P->level_ms[t] = ms;
+    trans += ms;
+  }
+  P->last_ms[1] = trans;
+  cudaEventElapsedTime(&ms, P->ev[P->n_ev - 2], P->ev[P->n_ev - 1]);
+  P->last_ms[2] = ms;
+  cudaEventElapsedTime(&ms, P->ev[0], P->ev[P->n_ev - 1]);
+  P->last_ms[3] = ms;
+  return SFT_OK;
+}
+
+extern "C" int sft_apply(sft_plan_t P, const void* f, void* u) {
+  if (!P || !f || !u) return fail(SFT_E_ARG, "NULL argument");
+  if (P->world != 1) return fail(SFT_E_STATE, "sft_apply needs a world == 1 plan; use the phase calls");
+  cudaStream_t s = P->stream;
+  const int L = P->L;
+  const double2* fd = (const double2*)f;
+  double2* ud = (double2*)u;
+  const bool f_host = !is_device_ptr(f), u_host = !is_device_ptr(u);
+  if (f_host) {
+    if (!P->f_stage) CKR(cudaMallocAsync(&P->f_stage, P->nk * sizeof(double2), s));
+    CKR(cudaMemcpyAsync(P->f_stage, f, P->nk * sizeof(double2), cudaMemcpyHostToDevice, s));
+    fd = P->f_stage;
+  }
+  if (u_host) {
+    if (!P->u_stage) CKR(cudaMallocAsync(&P->u_stage, P->nx * sizeof(double2), s));
+    ud = P->u_stage;
+  }
+  if (P->timing && P->ev_created < L + 3) {
+    for (int i = P->ev_created; i < L + 3; ++i) cudaEventCreate(&P->ev[i]);
+    P->ev_created = L + 3;
+  }
+  P->n_ev = 0;
+  tmark(P);
+  // step 2: leaf charges, level L buffer
+  CKR(launch_leaf(P, fd, P->buf[L & 1], 0, P->K.counts[L]));
+  tmark(P);
+  // step 3: t = L-1 .. 0
+  for (int t = L - 1; t >= 0; --t) {
+    LevelDims ld = level_dims_k(P, t);
+    CKR(launch_translate(P, ld, P->buf[(t + 1) & 1], P->buf[t & 1]));
+    tmark(P);
+  }
+  // step 4: final evaluation, level 0 buffer [A leaves]
+  CKR(launch_final(P, P->buf[0], ud, 0, P->X.counts[L]));
+  tmark(P);
+  if (u_host) {
+    CKR(cudaMemcpyAsync(u, ud, P->nx * sizeof(double2), cudaMemcpyDeviceToHost, s));
+    CKR(cudaStreamSynchronize(s));
+  }
+  return finish_timing(P, L - 1);
+}
+
+// ---------------------------------------------------------------------------
+// multi-GPU phases
+// ---------------------------------------------------------------------------
+extern "C" int sft_exchange_counts(sft_plan_t P, int64_t* send_counts, int64_t* recv_counts) {
+  if (!P) return fail(SFT_E_ARG, "NULL plan");
+  if (P->world < 2) return fail(SFT_E_STATE, "plan is not multi-rank");
+  for (int q = 0; q < P->world; ++q) {
+    if (send_counts) send_counts[q] = P->send_counts[q];
+    if (recv_counts) recv_counts[q] = P->recv_counts[q];
+  }
+  return SFT_OK;
+}
+
+extern "C" int sft_partition_info(sft_plan_t P, int64_t* part) {
+  if (!P || !part) return fail(SFT_E_ARG, "NULL argument");
+  if (P->world < 2) return fail(SFT_E_STATE, "plan is not multi-rank");
+  part[0] = P->part.sk;
+  part[1] = P->part.sx;
+  part[2] = P->part.m;
+  for (int r = 0; r < P->world; ++r) {
+    part[3 + 4 * r] = P->part.k_lo[r];
+    part[4 + 4 * r] = P->part.k_hi[r];
+    part[5 + 4 * r] = P->part.x_lo[r];
+    part[6 + 4 * r] = P->part.x_hi[r];
+  }
+  return SFT_OK;
+}
+
+extern "C" int sft_apply_phase1(sft_plan_t P, const void* f, void* sendbuf) {
+  if (!P || !f || !sendbuf) return fail(SFT_E_ARG, "NULL argument");
+  if (P->world < 2) return fail(SFT_E_STATE, "plan is not multi-rank");
+  if (!is_device_ptr(sendbuf)) return fail(SFT_E_ARG, "sendbuf must be device memory");
+  cudaStream_t s = P->stream;
+  const int L = P->L, m = P->part.m;
+  const double2* fd = (const double2*)f;
+  if (!is_device_ptr(f)) {
+    if (!P->f_stage) CKR(cudaMallocAsync(&P->f_stage, P->nk * sizeof(double2), s));
+    CKR(cudaMemcpyAsync(P->f_stage, f, P->nk * sizeof(double2), cudaMemcpyHostToDevice, s));
+    fd = P->f_stage;
+  }
+  double2* sb = (double2*)sendbuf;
+  // leaf level: the local leaf range; if m == L the leaf output is the send buffer
+  const LevelRange kl = P->k_rng[L];
+  if (m == L) {
+    // exchange at the leaf level: pairs (A0, B) with the single root A0 of T_X
+    // (s_X = 0), so only its owner's segment is non-empty and starts at 0
+    CKR(launch_leaf(P, fd, sb, kl.lo, kl.hi));
+    return SFT_OK;
+  }
+  CKR(launch_leaf(P, fd, P->buf[L & 1], kl.lo, kl.hi));
+  for (int t = L - 1; t >= m; --t) {
+    LevelDims ld = level_dims_k(P, t);
+    double2* out = P->buf[t & 1];
+    if (t == m) {
+      ld.seg = P->d_seg;
+      ld.nseg = P->world;
+      out = sb;
+    }
+    CKR(launch_translate(P, ld, P->buf[(t + 1) & 1], out));
+  }
+  return SFT_OK;
+}
+
+extern "C" int sft_apply_phase2(sft_plan_t P, const void* recvbuf, void* u) {
+  if (!P || !recvbuf || !u) return fail(SFT_E_ARG, "NULL argument");
+  if (P->world < 2) return fail(SFT_E_STATE, "plan is not multi-rank");
+  if (!is_device_ptr(recvbuf)) return fail(SFT_E_ARG, "recvbuf must be device memory");
+  cudaStream_t s = P->stream;
+  const int L = P->L, m = P->part.m;
+  const bool u_host = !is_device_ptr(u);
+  double2* ud = (double2*)u;
+  if (u_host) {
+    if (!P->u_stage) CKR(cudaMallocAsync(&P->u_stage, P->nx * sizeof(double2), s));
+    ud = P->u_stage;
+  }
+  CKR(launch_zero(ud, P->nx, s));
+  const double2* in = (const double2*)recvbuf;
+  for (int t = m - 1; t >= 0; --t) {
+    LevelDims ld = level_dims_x(P, t);
+    double2* out = P->buf[t & 1];
+    CKR(launch_translate(P, ld, in, out));
+    in = out;
+  }
+  const LevelRange xl = P->x_rng[L];
+  CKR(launch_final(P, in, ud, xl.lo, xl.hi));
+  if (u_host) {
+    CKR(cudaMemcpyAsync(u, ud, P->nx * sizeof(double2), cudaMemcpyDeviceToHost, s));
+    CKR(cudaStreamSynchronize(s));
+  }
+  return SFT_OK;
+}
+
+// ---------------------------------------------------------------------------
+// stats / timing
+// ---------------------------------------------------------------------------
+extern "C" int sft_plan_stats(sft_plan_t P, int64_t* counts_x, int64_t* counts_k, int64_t* pairs, double* info) {
+  if (!P) return fail(SFT_E_ARG, "NULL plan");
+  const int L = P->L;
+  const int64_t PD = ipow64(P->p, P->d);
+  double groups = 0, bytes = 0;
+  for (int l = 0; l <= L; ++l) {
+    if (counts_x) counts_x[l] = P->X.counts[l];
+    if (counts_k) counts_k[l] = P->K.counts[l];
+    if (pairs) pairs[l] = P->K.counts[l] * P->X.counts[L - l];
+  }
+  for (int t = 0; t < L; ++t) {
+    groups += (double)P->K.counts[t] * P->X.counts[L - t - 1];
+    bytes += 16.0 * PD * ((double)P->K.counts[t] * P->X.counts[L - t] + (double)P->K.counts[t + 1] * P->X.counts[L - t - 1]);
+  }
+  if (info) {
+    info[0] = L;
+    info[1] = (double)PD;
+    info[2] = (double)P->nx;
+    info[3] = (double)P->nk;
+    info[4] = 2.0 * P->buf_elems * sizeof(double2);
+    info[5] = P->plan_ms;
+    info[6] = groups;
+    info[7] = bytes;
+  }
+  return SFT_OK;
+}
+
+extern "C" int sft_set_timing(sft_plan_t P, int enable) {
+  if (!P) return fail(SFT_E_ARG, "NULL plan");
+  P->timing = enable != 0;
+  return SFT_OK;
+}
+
+extern "C" int sft_last_timing(sft_plan_t P, double* t_ms, double* per_level_ms) {
+  if (!P) return fail(SFT_E_ARG, "NULL plan");
+  if (t_ms)
+    for (int i = 0; i < 4; ++i) t_ms[i] = P->last_ms[i];
+  if (per_level_ms)
+    for (int t = 0; t < P->L; ++t) per_level_ms[t] = t < (int)P->level_ms.size() ? P->level_ms[t] : 0.0;
+  return SFT_OK;
+}

@@ -1,0 +1,123 @@
+// sft_internal.cuh -- internal structures of libsft (B200 butterfly SFT).
+// Nothing here is shared with oracle/ (test infrastructure).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/sft.h"
+
+namespace sft {
+
+// Box-relative formulation (derived from eq. M1/E1):
+//   g^{AB} = M12 f^{AB} per axis, (M12)_l = e^{2 pi i a l/(p-1)} (a = index of A).
+//   leaf:   g^{A0 B}_m = sum_{k_j in B} f_j prod_axes w_m(k_j - c^B)
+//   level:  g^{AB} = sum_{present B_c} (x)_axes V[alpha_ax][beta_ax] g^{A' B_c}
+//   final:  u(x) = sum_l prod_axes e^{2 pi i (x - c^A) l/(p-1)} g^{A B0}_l
+// V and the leaf constants depend on p only; they are built on the host in
+// long double from the Lagrange / sine-product closed forms (tables.cpp).
+
+constexpr int kMaxDim = 3;
+
+struct TreeLevel {
+  int64_t n = 0;                  // non-empty boxes at this level
+  uint64_t* key = nullptr;        // [n] Morton key of each box (sorted)
+  int32_t* child_begin = nullptr; // [n] first child at level+1 (level < L)
+  uint32_t* child_mask = nullptr; // [n] bit c set <=> child c present (level < L)
+  int32_t* parent = nullptr;      // [n] parent index at level-1 (level > 0)
+};
+
+struct Tree {
+  int d = 0, L = 0;
+  int64_t npts = 0;
+  std::vector<TreeLevel> lev;      // [L+1]
+  std::vector<int64_t> counts;     // host copy of lev[l].n
+  int32_t* first_pt = nullptr;     // [n_leaf+1] CSR of sorted points per leaf
+  int32_t* perm = nullptr;         // [npts] sorted position -> user index
+  double* pts_sorted = nullptr;    // [npts][d]
+  uint64_t* keys_sorted = nullptr; // [npts] leaf Morton keys in sorted order
+};
+
+struct DeviceTables {
+  int p = 0;
+  double2* V = nullptr;       // [2][2][p][p]  V[alpha][beta][m][l']
+  double* leaf_invD = nullptr;  // [p]  1 / prod_{q != m} sin(pi (m-q)/(p-1)^2)
+};
+
+// Host-side long double construction (tables.cpp).
+void build_tables_host(int p, std::vector<double>& V /* 2*4*p*p */, std::vector<double>& invD /* p */);
+const DeviceTables* get_device_tables(int p, std::string* err);
+
+struct Partition {
+  int sk = 0, sx = 0, m = 0;
+  std::vector<int64_t> k_lo, k_hi;  // [world] box ranges at level sk
+  std::vector<int64_t> x_lo, x_hi;  // [world] box ranges at level sx
+};
+
+// Range of boxes at level `lev` that descend from boxes [lo, hi) at level `s`.
+struct LevelRange {
+  int64_t lo = 0, hi = 0;
+};
+
+}  // namespace sft
+
+struct sft_plan_s {
+  int d = 0, p = 0, L = 0;
+  int64_t N = 0, nx = 0, nk = 0;
+  int rank = 0, world = 1;
+  cudaStream_t stream = nullptr;
+  sft::Tree X, K;
+  const sft::DeviceTables* tab = nullptr;
+  // two live level buffers, complex128
+  double2* buf[2] = {nullptr, nullptr};
+  size_t buf_elems = 0;
+  // staging for host pointers
+  double2* f_stage = nullptr;
+  double2* u_stage = nullptr;
+  int* d_err = nullptr;
+  // multi-GPU
+  sft::Partition part;
+  std::vector<sft::LevelRange> k_rng;  // [L+1] this rank's T_K range per level (phase 1)
+  std::vector<sft::LevelRange> x_rng;  // [L+1] this rank's T_X range per level (phase 2)
+  std::vector<int64_t> send_counts, recv_counts;  // [world] complex elements
+  int64_t* d_seg = nullptr;  // device [2*world+1]: a-boundaries at level L-m, send segment bases
+  // timing
+  bool timing = false;
+  cudaEvent_t ev[64];
+  int n_ev = 0;
+  int ev_created = 0;
+  double last_ms[4] = {0, 0, 0, 0};
+  std::vector<double> level_ms;
+  double plan_ms = 0;
+};
+
+namespace sft {
+
+// tree.cu
+int build_trees(sft_plan_s* P, const double* x_dev, const double* k_dev, std::string* err);
+void free_tree(Tree& T, cudaStream_t s);
+
+// kernels.cu
+struct LevelDims {
+  // translation from level t+1 (input) to level t (output)
+  int t;
+  const int32_t* cbK;  // T_K level t child_begin
+  const uint32_t* mK;  // T_K level t child_mask
+  const int32_t* cbX;  // T_X level L-t-1 child_begin
+  const uint32_t* mX;  // T_X level L-t-1 child_mask
+  int64_t b_lo, b_hi;   // B range at level t (groups)
+  int64_t ap_lo, ap_hi; // A' range at level L-t-1 (groups)
+  int64_t in_b0, in_nA, in_a0;   // input layout: [(iBc - in_b0) * in_nA + (iA' - in_a0)]
+  int64_t out_b0, out_nA, out_a0; // output layout: [(iB - out_b0) * out_nA + (iA - out_a0)]
+  const int64_t* seg;  // exchange mapping (nullptr = plain layout), see api.cu
+  int nseg;
+};
+
+cudaError_t launch_leaf(const sft_plan_s* P, const double2* f, double2* out, int64_t b_lo, int64_t b_hi);
+cudaError_t launch_translate(const sft_plan_s* P, const LevelDims& L, const double2* in, double2* out);
+cudaError_t launch_final(const sft_plan_s* P, const double2* g0, double2* u, int64_t a_lo, int64_t a_hi);
+cudaError_t launch_zero(double2* p, int64_t n, cudaStream_t s);
+
+}  // namespace sft

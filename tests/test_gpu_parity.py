@@ -1,0 +1,180 @@
+"""GPU parity: the CUDA path (through the C ABI, libsft.so) against the
+long-double oracle (oracle/), element by element on the same seeded inputs.
+
+Bars (BASELINE.json:5): GPU butterfly vs oracle butterfly rel. L2 <= 1e-10
+(FP64); both vs direct summation <= 5e-2 / 1e-3 / 1e-5 for p = 5 / 7 / 9.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+PARITY = 1e-10
+DIRECT_TOL = {5: 5e-2, 7: 1e-3, 9: 1e-5}
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def gpu_transform(x, k, f, N, p, host=False):
+    torch = _torch()
+    import paper_0801_1524_b200 as sft
+    d = x.shape[1]
+    if host:
+        xt, kt, ft = x, k, f
+    else:
+        xt = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+        kt = torch.from_numpy(np.ascontiguousarray(k)).cuda()
+        ft = torch.from_numpy(np.ascontiguousarray(f)).cuda()
+    with sft.Plan(d, N, p, xt, kt) as plan:
+        u = plan.apply(ft)
+        torch.cuda.synchronize()
+        st = plan.stats()
+    u = u.cpu().numpy() if hasattr(u, "cpu") else np.asarray(u)
+    return u, st
+
+
+@pytest.mark.parametrize("name,p", [("C0", 5), ("C0", 7), ("C0", 9), ("C1", 7), ("C1", 5), ("C1", 9)])
+def test_parity_2d_small(name, p):
+    w = synth.make_workload(name, p=p)
+    u, st = gpu_transform(w.x, w.k, w.f, w.N, p)
+    ub = oracle.butterfly(w.x, w.k, w.f, w.N, p)
+    assert oracle.rel_l2(u, ub) <= PARITY
+    # trees: per-level counts equal the oracle's
+    assert list(st["counts_x"]) == list(oracle.tree_counts(w.x, w.N))
+    assert list(st["counts_k"]) == list(oracle.tree_counts(w.k, w.N))
+    if name == "C0":
+        ud = oracle.direct(w.x, w.k, w.f, w.N)
+        assert oracle.rel_l2(u, ud) <= DIRECT_TOL[p]
+
+
+@pytest.mark.parametrize("N,p", [(16, 5), (16, 7), (16, 9), (32, 7)])
+def test_parity_3d_small(N, p):
+    w = synth.make_workload("C3", N=N, p=p)
+    u, st = gpu_transform(w.x, w.k, w.f, w.N, p)
+    ub = oracle.butterfly(w.x, w.k, w.f, w.N, p)
+    assert oracle.rel_l2(u, ub) <= PARITY
+    ud = oracle.direct(w.x, w.k, w.f, w.N, targets=w.sample[:512] if len(w.x) > 512 else None)
+    uu = u[w.sample[:512]] if len(w.x) > 512 else u
+    assert oracle.rel_l2(uu, ud) <= DIRECT_TOL[p]
+
+
+def test_parity_C1_direct_all_targets():
+    w = synth.make_workload("C1")
+    u, _ = gpu_transform(w.x, w.k, w.f, w.N, w.p)
+    ud = oracle.direct(w.x, w.k, w.f, w.N)
+    assert oracle.rel_l2(u, ud) <= DIRECT_TOL[w.p]
+
+
+def test_parity_C2_full():
+    """C2 at full size: full oracle butterfly on every target, direct on the
+    1024 seeded targets (BASELINE.json:9)."""
+    w = synth.make_workload("C2")
+    u, _ = gpu_transform(w.x, w.k, w.f, w.N, w.p)
+    ub = oracle.butterfly(w.x, w.k, w.f, w.N, w.p)
+    assert oracle.rel_l2(u, ub) <= PARITY
+    ud = oracle.direct(w.x, w.k, w.f, w.N, targets=w.sample)
+    assert oracle.rel_l2(u[w.sample], ud) <= DIRECT_TOL[w.p]
+
+
+def test_parity_C3_full():
+    w = synth.make_workload("C3")
+    u, _ = gpu_transform(w.x, w.k, w.f, w.N, w.p)
+    ub = oracle.butterfly(w.x, w.k, w.f, w.N, w.p, targets=w.sample[:2048] if len(w.sample) > 2048 else w.sample)
+    tg = w.sample[:2048] if len(w.sample) > 2048 else w.sample
+    assert oracle.rel_l2(u[tg], ub) <= PARITY
+    ud = oracle.direct(w.x, w.k, w.f, w.N, targets=synth.error_sample(len(w.x), w.seed))
+    assert oracle.rel_l2(u[synth.error_sample(len(w.x), w.seed)], ud) <= DIRECT_TOL[w.p]
+
+
+def test_parity_C4_sampled():
+    """C4 at full size in the bench launch configuration: the oracle evaluates
+    256 seeded targets with the charges of one T_K subtree active (all other
+    f_j = 0 on both sides), which skips only zero or unused pairs."""
+    w = synth.make_workload("C4")
+    leaf = np.minimum(np.floor(w.k).astype(np.int64), w.N - 1)
+    sub = leaf >> 6  # level-3 subtree of T_K
+    key = sub[:, 0] * 64 + sub[:, 1] * 8 + sub[:, 2]
+    vals, cnt = np.unique(key, return_counts=True)
+    act = key == vals[np.argmax(cnt)]
+    f = np.where(act, w.f, 0)
+    u, _ = gpu_transform(w.x, w.k, f, w.N, w.p)
+    tg = w.sample[:256]
+    ub = oracle.butterfly(w.x, w.k, w.f, w.N, w.p, targets=tg, src_active=act.astype(np.uint8))
+    assert oracle.rel_l2(u[tg], ub) <= PARITY
+    ud = oracle.direct(w.x, w.k[act], f[act], w.N, targets=tg)
+    assert oracle.rel_l2(u[tg], ud) <= DIRECT_TOL[w.p]
+
+
+# ------------------------------------------------------------------ edge cases
+def test_single_source_single_target():
+    x = np.array([[3.25, 17.5]]); k = np.array([[60.75, 0.0]]); f = np.array([1.5 - 0.5j])
+    for p in (5, 7, 9):
+        u, _ = gpu_transform(x, k, f, 64, p)
+        ub = oracle.butterfly(x, k, f, 64, p)
+        assert abs(u[0] - ub[0]) <= PARITY * abs(ub[0])
+        assert abs(u[0] - oracle.direct(x, k, f, 64)[0]) <= DIRECT_TOL[p] * abs(f[0])
+
+
+def test_domain_boundaries_and_one_leaf():
+    """Points on x = 0 and x = N (closed upper face), all sources in one leaf."""
+    N = 32
+    rng = np.random.default_rng(7)
+    x = np.concatenate([rng.uniform(0, N, (50, 2)), [[0, 0], [N, N], [N, 0], [0, N], [N / 2, N]]])
+    k = 5.0 + rng.uniform(0, 1, (9, 2))
+    f = rng.normal(size=9) + 1j * rng.normal(size=9)
+    u, _ = gpu_transform(x, k, f, N, 7)
+    ub = oracle.butterfly(x, k, f, N, 7)
+    assert oracle.rel_l2(u, ub) <= PARITY
+
+
+def test_zero_linear_deterministic_host_device():
+    torch = _torch()
+    import paper_0801_1524_b200 as sft
+    w = synth.make_workload("C1", N=256, p=9)
+    g = synth.random_charges(len(w.k), 5)
+    xt = torch.from_numpy(w.x).cuda(); kt = torch.from_numpy(w.k).cuda()
+    with sft.Plan(2, w.N, w.p, xt, kt) as plan:
+        z = plan.apply(torch.zeros(len(w.k), dtype=torch.complex128, device="cuda"))
+        assert torch.count_nonzero(z).item() == 0
+        a = 0.25 - 2j
+        u1 = plan.apply(torch.from_numpy(w.f).cuda()).cpu().numpy()
+        u1b = plan.apply(torch.from_numpy(w.f).cuda()).cpu().numpy()
+        assert np.array_equal(u1, u1b)  # bitwise run to run
+        u2 = plan.apply(torch.from_numpy(g).cuda()).cpu().numpy()
+        u3 = plan.apply(torch.from_numpy(w.f + a * g).cuda()).cpu().numpy()
+        assert oracle.rel_l2(u3, u1 + a * u2) < 1e-13
+        uh = plan.apply(w.f)  # host numpy in, host numpy out
+        assert np.array_equal(uh, u1)
+        fp = torch.from_numpy(w.f).pin_memory()
+        up = plan.apply(fp)
+        assert np.array_equal(up.numpy(), u1)
+    # host coordinates give the same plan
+    u_host, _ = gpu_transform(w.x, w.k, w.f, w.N, w.p, host=True)
+    assert np.array_equal(u_host, u1)
+
+
+def test_errors():
+    import paper_0801_1524_b200 as sft
+    torch = _torch()
+    x = torch.rand(10, 2, dtype=torch.float64, device="cuda") * 16
+    with pytest.raises(sft.SftError):
+        sft.Plan(2, 48, 5, x, x)  # N not a power of two
+    with pytest.raises(sft.SftError):
+        sft.Plan(2, 16, 6, x, x)  # unsupported p
+    with pytest.raises(sft.SftError):
+        sft.Plan(4, 16, 5, x, x)  # bad dim
+    bad = x.clone(); bad[3, 1] = float("nan")
+    with pytest.raises(sft.SftError, match="outside"):
+        sft.Plan(2, 16, 5, bad, x)
+    bad = x.clone(); bad[0, 0] = 16.5
+    with pytest.raises(sft.SftError, match="outside"):
+        sft.Plan(2, 16, 5, x, bad)
+    with sft.Plan(2, 16, 5, x, x) as plan:
+        with pytest.raises(sft.SftError):
+            plan.exchange_counts()  # world == 1
