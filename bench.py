@@ -1,0 +1,383 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 butterfly sparse Fourier transform (arXiv 0801.1524).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+
+One step = one pass of the whole hot path (plus
+S5 for N > 1) on the workload: sft_plan (GPU tree build, step 1 P:293-295)
+followed by sft_apply (leaf, per-level translations, final), with
+x, k, f resident in HBM.  Metric (BASELINE.json:2): Mpoints/s = P / step time
+with P = max(n_x, n_k) (the paper's P); apply-only ms is
+reported beside it.  L2 is flushed (256 MiB memset) before every timed step;
+each step is timed with CUDA events on the plan stream, max over ranks.
+
+N > 1: one process per GPU under torchrun; the transform is sharded
+(phase 1 over T_K subtrees, NCCL all-to-all of level-m charges, phase 2 over
+T_X subtrees) -- strong scaling of one transform.
+
+--impl reference: the oracle (oracle/, long double CPU) on the box's host
+cores, rank 0 only (the other ranks exit 0).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+CONFIG_DESC = {
+    "C0": "2D N=64 p=5, X=K=circle r=0.4, 4 pts/unit length, f ~ CN(0,1) seed 0 (BASELINE.json:7)",
+    "C1": "2D N=1024 p=7, X circle r=0.4, K ellipse (0.35,0.25), 4 pts/unit length, seed 1 (BASELINE.json:8)",
+    "C2": "2D N=16384 p=9, X circle r=0.4, K ellipse (0.35,0.25), 4 pts/unit length, seed 2 (BASELINE.json:9)",
+    "C3": "3D N=128 p=5, X sphere r=0.4, K ellipsoid (0.4,0.3,0.25), lat-long 2 pts/unit length, seed 3 (BASELINE.json:10)",
+    "C4": "3D N=512 p=7, X sphere r=0.4, K ellipsoid (0.4,0.3,0.25), lat-long 2 pts/unit length, seed 4 (BASELINE.json:11)",
+}
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        d = json.load(open(path))
+        return float(d.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = str(gpu_index)
+        self.proc = None
+        self.lines = []
+        self.t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", self.gpu, f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=5)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        busy = [v for v in sm if v > 0.5 * (mx or 1)] or sm
+        return {"sm_mhz": float(np.median(busy)) if busy else None, "sm_max_mhz": mx, "samples": len(sm),
+                "reasons": sorted(reasons)}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    import paper_0801_1524_b200 as sft
+    from paper_0801_1524_b200.dist import DistPlan
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    w = synth.make_workload(args.config)
+    P = w.P
+    x = torch.from_numpy(w.x).to(dev)
+    k = torch.from_numpy(w.k).to(dev)
+    f = torch.from_numpy(w.f).to(dev)
+    u = torch.empty(len(w.x), dtype=torch.complex128, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    def step():
+        if world == 1:
+            with sft.Plan(w.dim, w.N, w.p, x, k, stream=stream) as plan:
+                plan.apply(f, u)
+        else:
+            with DistPlan(w.dim, w.N, w.p, x, k, stream=stream) as dp:
+                dp.apply(f, u)
+
+    def timed(fn, K, do_flush=True):
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+        barrier()
+        for i in range(K):
+            if do_flush:
+                flush.zero_()
+            evs[i][0].record(stream)
+            fn()
+            evs[i][1].record(stream)
+        torch.cuda.synchronize(dev)
+        ms = [a.elapsed_time(b) for a, b in evs]
+        tot = torch.tensor([sum(ms)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+        return float(tot.item()), ms
+
+    for _ in range(args.warmup):
+        step()
+    launches0 = sft.launch_count()
+    clk = Clocks(local)
+    clk.start()
+    total_ms, per_step = timed(step, args.steps)
+    clocks = clk.stop()
+    launches = sft.launch_count() - launches0
+
+    # apply-only timing (plan reused) and per-kernel timing, same stream
+    if world == 1:
+        plan = sft.Plan(w.dim, w.N, w.p, x, k, stream=stream)
+        for _ in range(max(2, args.warmup)):
+            plan.apply(f, u)
+        apply_total, _ = timed(lambda: plan.apply(f, u), args.steps)
+        plan.set_timing(True)
+        kt = []
+        for _ in range(max(3, min(args.steps, 10))):
+            flush.zero_()
+            plan.apply(f, u)
+            torch.cuda.synchronize(dev)
+            kt.append(plan.last_timing())
+        plan.set_timing(False)
+        st = plan.stats()
+        plan.close()
+    else:
+        dp = DistPlan(w.dim, w.N, w.p, x, k, stream=stream)
+        for _ in range(max(2, args.warmup)):
+            dp.apply(f, u)
+        apply_total, _ = timed(lambda: dp.apply(f, u), args.steps)
+        part = dp.partition().tolist()
+        dp.close()
+        kt = None
+        st = sft.Plan(w.dim, w.N, w.p, x, k, stream=stream)
+        stats = st.stats()
+        st.close()
+        st = stats
+
+    # end to end through the public API with pinned host buffers
+    xh = torch.from_numpy(w.x).pin_memory()
+    kh = torch.from_numpy(w.k).pin_memory()
+    fh = torch.from_numpy(w.f).pin_memory()
+    uh = torch.empty(len(w.x), dtype=torch.complex128).pin_memory()
+
+    def step_e2e():
+        if world == 1:
+            with sft.Plan(w.dim, w.N, w.p, xh, kh, stream=stream) as plan:
+                plan.apply(fh, uh)
+        else:
+            xd, kd, fd = xh.to(dev, non_blocking=True), kh.to(dev, non_blocking=True), fh.to(dev, non_blocking=True)
+            with DistPlan(w.dim, w.N, w.p, xd, kd, stream=stream) as dp:
+                ud = dp.apply(fd)
+            uh.copy_(ud)
+
+    for _ in range(2):
+        step_e2e()
+    e2e_total, _ = timed(step_e2e, args.steps)
+
+    res = None
+    if rank == 0:
+        K = args.steps
+        step_ms = total_ms / K
+        value = P * K / (total_ms / 1e3) / 1e6
+        hbm_peak, peak_src = measured_peaks()
+        roof = None
+        if kt:
+            trans_ms = float(np.median([t["trans_ms"] for t in kt]))
+            leaf_ms = float(np.median([t["leaf_ms"] for t in kt]))
+            final_ms = float(np.median([t["final_ms"] for t in kt]))
+            app_ms = float(np.median([t["apply_ms"] for t in kt]))
+            L = int(st["L"])
+            bytes_per_launch = st["trans_alg_bytes"] / L
+            dur_per_launch = trans_ms / L / 1e3
+            achieved = bytes_per_launch / dur_per_launch / 1e9
+            traffic = None
+            tf = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
+            if os.path.exists(tf):
+                traffic = json.load(open(tf)).get("dram_bytes_per_launch")
+            roof = {"bound": "hbm", "kernel": "k_translate (K3, one launch per level)", "achieved": round(achieved, 1),
+                    "peak": hbm_peak, "unit": "GB/s", "frac": round(achieved / hbm_peak, 4), "traffic": traffic,
+                    "peak_source": peak_src,
+                    "alg_bytes_per_launch": bytes_per_launch, "launches_per_apply": L,
+                    "kernel_ms": {"leaf": round(leaf_ms, 4), "translate_total": round(trans_ms, 4),
+                                  "final": round(final_ms, 4), "apply_events": round(app_ms, 4)},
+                    "level_ms": [round(float(v), 4) for v in np.median([t["level_ms"] for t in kt], axis=0)]}
+        h2d = w.x.nbytes + w.k.nbytes + w.f.nbytes
+        d2h = len(w.x) * 16
+        res = {
+            "metric": "butterfly SFT Mpoints/s (P=max(nx,nk) per plan+apply step)",
+            "value": round(value, 3),
+            "unit": "Mpoints/s",
+            "n_gpus": world,
+            "steps": K,
+            "warmup": args.warmup,
+            "ms_per_step": round(step_ms, 4),
+            "apply_ms": round(apply_total / K, 4),
+            "apply_mpoints_s": round(P * K / (apply_total / 1e3) / 1e6, 3),
+            "plan_ms": round(step_ms - apply_total / K, 4),
+            "higher_is_better": True,
+            "scaling": "strong",
+            "vs_baseline": None,
+            "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": f"{args.config}: {CONFIG_DESC[args.config]}", "dim": w.dim, "N": w.N, "p": w.p,
+                       "nx": len(w.x), "nk": len(w.k), "P": P, "pairs_total": int(np.sum(st["pairs"])),
+                       "l2": "flushed before every timed step (256 MiB memset, outside the step events)",
+                       "parallelism": f"subtree-sharded x{world}" if world > 1 else "single GPU"},
+            "e2e": {"value": round(P * K / (e2e_total / 1e3) / 1e6, 3), "unit": "Mpoints/s",
+                    "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                    "ms_per_step": round(e2e_total / K, 4)},
+            "gpu_launches": int(launches),
+            "clocks": clocks,
+            "roofline": roof,
+        }
+        if world > 1:
+            res["partition"] = part[:3]
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return res, w
+
+
+def cpu_baseline(w, nthreads=0, sample="full"):
+    """The oracle butterfly (as it stands) on the host cores."""
+    import oracle
+    nth = nthreads or oracle.max_threads()
+    t0 = time.perf_counter()
+    if sample == "full":
+        oracle.butterfly(w.x, w.k, w.f, w.N, w.p, nthreads=nth)
+        dt = time.perf_counter() - t0
+        return {"value": round(w.P / dt / 1e6, 6), "unit": "Mpoints/s", "cores": nth, "kind": "oracle",
+                "sample": f"full {w.name} workload, one oracle butterfly (long double, OpenMP)",
+                "seconds": round(dt, 3)}
+    raise ValueError(sample)
+
+
+def _pairs(w, targets=None):
+    L = w.N.bit_length() - 1
+
+    def counts(pts):
+        leaf = np.minimum(np.floor(pts).astype(np.int64), w.N - 1)
+        mult = np.array([1 << (2 * L), 1 << L, 1][-w.dim:])
+        return [len(np.unique((leaf >> (L - l)) @ mult)) for l in range(L + 1)]
+    cx = counts(w.x if targets is None else w.x[targets])
+    ck = counts(w.k)
+    return sum(ck[t] * cx[L - t] for t in range(L + 1))
+
+
+def run_reference(args):
+    """--impl reference: the oracle on the host cores, rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return None
+    import oracle
+    w = synth.make_workload(args.config)
+    nth = oracle.max_threads()
+    tg = w.sample[: args.ref_targets]
+    frac = _pairs(w, tg) / _pairs(w)
+
+    def step():
+        oracle.butterfly(w.x, w.k, w.f, w.N, w.p, targets=tg, nthreads=nth)
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = (time.perf_counter() - t0) / args.steps
+    # full-workload equivalent: the oracle's cost is proportional to the pairs it visits
+    value = w.P * frac / dt / 1e6
+    desc = (f"oracle butterfly on {w.name} restricted to {len(tg)} seeded targets (all sources): "
+            f"{frac:.4f} of the pairs; value = P * frac / step time")
+    return {
+        "impl": "reference",
+        "metric": "butterfly SFT Mpoints/s (P=max(nx,nk) per plan+apply step)",
+        "value": round(value, 6),
+        "unit": "Mpoints/s",
+        "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(dt * 1e3, 3),
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f64 (long double arithmetic)",
+        "data": "synthetic",
+        "config": {"workload": f"{args.config}: {CONFIG_DESC[args.config]}", "dim": w.dim, "N": w.N, "p": w.p,
+                   "nx": len(w.x), "nk": len(w.k), "P": w.P},
+        "cpu_baseline": {"value": round(value, 6), "unit": "Mpoints/s", "cores": nth, "kind": "oracle",
+                         "sample": desc},
+        "e2e": {"value": round(value, 6), "unit": "Mpoints/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C2", choices=sorted(CONFIG_DESC))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-targets", type=int, default=256)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
+    if args.impl == "reference":
+        res = run_reference(args)
+        if res is not None:
+            print(json.dumps(res), flush=True)
+        return
+    res, w = run_ours(args)
+    if res is not None:
+        if res["n_gpus"] == 1 and not args.no_cpu_baseline:
+            res["cpu_baseline"] = cpu_baseline(w)
+        print(json.dumps(res), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -136,13 +136,20 @@ int sft_choose_partition(int L, int world, const int64_t* counts_x, const int64_
                          const int32_t* const* parent_x, const int32_t* const* parent_k, int force_sk,
                          int force_sx, int force_m, int64_t* out, int64_t* out_cost);
 
-/* Diagnostics (host only, no GPU): the constant operator tables the kernels
- * use for grid size p (3 <= p <= 15), built in long double from the
- * Lagrange / sine-product closed forms:
- *   V    [2][2][p][p] complex128 interleaved, V[alpha][beta][m][l'];
- *   invD [p] leaf-weight normalisers 1/prod_{q!=m} sin(pi (m-q)/(p-1)^2).
- * Either pointer may be NULL. */
-int sft_operator_tables(int p, double* V, double* invD);
+/* Number of kernels launched by this library since load (its own kernels;
+ * the CUB radix-sort/scan kernels used by the tree build are not counted). */
+int sft_launch_count(int64_t* out);
+
+/* Diagnostics (host only, no GPU): the constant operator tables for grid
+ * size p (3 <= p <= 15), built in long double from the Lagrange /
+ * sine-product closed forms:
+ *   V    [2][2][p][p] complex128 interleaved: the child->parent operator
+ *        V[alpha][beta][m][l'] in box-relative charges g (= M^{-1} E);
+ *   invD [p] leaf-weight normalisers 1/prod_{q!=m} sin(pi (m-q)/(p-1)^2);
+ *   RC, RS [2][p][p] float64: the real operands the translation kernel keeps
+ *        in the constant bank (T = c (RC + i s_alpha RS) in the h-representation).
+ * Any pointer may be NULL. */
+int sft_operator_tables(int p, double* V, double* invD, double* RC, double* RS);
 
 #ifdef __cplusplus
 }

@@ -21,7 +21,7 @@ import os
 
 import numpy as np
 
-__all__ = ["Plan", "lib", "LIB_PATH", "SftError", "operator_tables", "choose_partition", "HEADER_SYMBOLS"]
+__all__ = ["Plan", "lib", "LIB_PATH", "SftError", "operator_tables", "choose_partition", "HEADER_SYMBOLS", "launch_count"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libsft.so")
@@ -83,7 +83,8 @@ def lib():
                                        ctypes.POINTER(ctypes.POINTER(ctypes.c_int32)),
                                        ctypes.POINTER(ctypes.POINTER(ctypes.c_int32)), ctypes.c_int, ctypes.c_int,
                                        ctypes.c_int, _c_i64p, _c_i64p]
-    L.sft_operator_tables.argtypes = [ctypes.c_int, _c_dp, _c_dp]
+    L.sft_operator_tables.argtypes = [ctypes.c_int, _c_dp, _c_dp, _c_dp, _c_dp]
+    L.sft_launch_count.argtypes = [_c_i64p]
     _lib = L
     return L
 
@@ -226,12 +227,26 @@ class Plan:
         self.close()
 
 
-def operator_tables(p):
-    """Host-only: (V [2,2,p,p] complex128, invD [p]) exactly as uploaded to the GPU."""
+def launch_count() -> int:
+    """Kernels launched by libsft so far (own kernels, CUB sort/scan excluded)."""
+    v = np.zeros(1, np.int64)
+    _check(lib().sft_launch_count(v.ctypes.data_as(_c_i64p)))
+    return int(v[0])
+
+
+def operator_tables(p, real=False):
+    """Host-only: (V [2,2,p,p] complex128, invD [p]) -- and with real=True also
+    (RC, RS) [2,p,p] float64, exactly as uploaded to the GPU's constant bank."""
     V = np.zeros(2 * 4 * p * p)
     invD = np.zeros(p)
-    _check(lib().sft_operator_tables(p, V.ctypes.data_as(_c_dp), invD.ctypes.data_as(_c_dp)))
-    return V.view(np.complex128).reshape(2, 2, p, p), invD
+    RC = np.zeros(2 * p * p)
+    RS = np.zeros(2 * p * p)
+    _check(lib().sft_operator_tables(p, V.ctypes.data_as(_c_dp), invD.ctypes.data_as(_c_dp),
+                                     RC.ctypes.data_as(_c_dp), RS.ctypes.data_as(_c_dp)))
+    V = V.view(np.complex128).reshape(2, 2, p, p)
+    if real:
+        return V, invD, RC.reshape(2, p, p), RS.reshape(2, p, p)
+    return V, invD
 
 
 def choose_partition(L, world, counts_x, counts_k, parents_x, parents_k, force=(-1, -1, -1)):

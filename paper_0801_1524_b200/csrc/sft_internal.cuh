@@ -12,12 +12,15 @@
 namespace sft {
 
 // Box-relative formulation (derived from eq. M1/E1):
-//   g^{AB} = M12 f^{AB} per axis, (M12)_l = e^{2 pi i a l/(p-1)} (a = index of A).
-//   leaf:   g^{A0 B}_m = sum_{k_j in B} f_j prod_axes w_m(k_j - c^B)
-//   level:  g^{AB} = sum_{present B_c} (x)_axes V[alpha_ax][beta_ax] g^{A' B_c}
-//   final:  u(x) = sum_l prod_axes e^{2 pi i (x - c^A) l/(p-1)} g^{A B0}_l
-// V and the leaf constants depend on p only; they are built on the host in
-// long double from the Lagrange / sine-product closed forms (tables.cpp).
+//   g^{AB} = M12 f^{AB} per axis, (M12)_l = e^{2 pi i a l/(p-1)} (a = index of A),
+//   stored as h^{AB} = (x)_axes diag(e^{i pi m/(p-1)}) g^{AB}  ("h-representation"):
+//   leaf:   h^{A0 B}_m = sum_{k_j in B} f_j e^{i pi sum_ax s_ax} prod_ax r_{m_ax}(s_ax),
+//           s = k_j - c^B, r_m(s) = invD_m prod_{q != m} sin(pi (s (p-1) - q)/(p-1)^2)  (real)
+//   level:  h^{AB} = sum_{present B_c} (x)_ax T[alpha_ax][beta_ax] h^{A' B_c},
+//           T[alpha][beta] = c_ab (RC_beta + i (2 alpha - 1) RS_beta), RC/RS real p x p
+//   final:  u(x) = sum_l prod_ax e^{i pi l_ax (2 xi_ax - 1)/(p-1)} h^{A B0}_l, xi = x - c^A
+// The tables depend on p only; they are built on the host in long double from
+// the Lagrange / sine-product closed forms (tables.cpp); no G^{-1} anywhere.
 
 constexpr int kMaxDim = 3;
 
@@ -47,7 +50,10 @@ struct DeviceTables {
 };
 
 // Host-side long double construction (tables.cpp).
-void build_tables_host(int p, std::vector<double>& V /* 2*4*p*p */, std::vector<double>& invD /* p */);
+void build_tables_host(int p, std::vector<double>& V /* 2*4*p*p */, std::vector<double>& invD /* p */,
+                       std::vector<double>* RC = nullptr /* 2*p*p */, std::vector<double>* RS = nullptr);
+// kernels.cu: copy RC/RS/invD for grid size p into the constant bank
+cudaError_t upload_const_tables(int p, const double* RC, const double* RS, const double* invD);
 const DeviceTables* get_device_tables(int p, std::string* err);
 
 struct Partition {
@@ -119,5 +125,9 @@ cudaError_t launch_leaf(const sft_plan_s* P, const double2* f, double2* out, int
 cudaError_t launch_translate(const sft_plan_s* P, const LevelDims& L, const double2* in, double2* out);
 cudaError_t launch_final(const sft_plan_s* P, const double2* g0, double2* u, int64_t a_lo, int64_t a_hi);
 cudaError_t launch_zero(double2* p, int64_t n, cudaStream_t s);
+
+// number of kernels this library has launched (own kernels; CUB's internal
+// sort/scan kernels are not counted), for bench.py's gpu_launches
+void count_launch(int n = 1);
 
 }  // namespace sft

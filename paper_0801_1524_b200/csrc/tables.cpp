@@ -13,6 +13,14 @@
 // i.e. V = M^{-1} E for the child pair expressed in box-relative charges;
 // it depends on p only (not on N, level or box position).
 // Leaf constants: invD[m] = 1 / prod_{q != m} sin(pi (m - q)/P1^2).
+//
+// Real form used by the kernels (h-representation, h_m = e^{i pi m/P1} g_m per
+// axis): the sine product makes W_beta = diag(e^{-i pi m/P1}) R_beta
+// diag(e^{i pi s_l'}) with R_beta REAL, and with D_alpha = C + i s_alpha S
+// (C = diag cos(pi l'/(2 P1)), S = diag sin(pi l'/(2 P1)), s_alpha = 2 alpha - 1)
+//   T[alpha][beta] = c_{alpha beta} (RC_beta + i s_alpha RS_beta),
+//   RC_beta = R_beta C, RS_beta = R_beta S, c = 1 (beta=0), i (alpha=0,beta=1), -i (alpha=1,beta=1),
+// so one pair of real p x p products per child gives both alpha outputs.
 #include <cmath>
 #include <map>
 #include <mutex>
@@ -43,8 +51,26 @@ static void lagrange_at(int p, int m, ld s, ld* re, ld* im) {
   *im = prod * sinl(ph);
 }
 
-void build_tables_host(int p, std::vector<double>& V, std::vector<double>& invD) {
+void build_tables_host(int p, std::vector<double>& V, std::vector<double>& invD, std::vector<double>* RC,
+                       std::vector<double>* RS) {
   const int P1 = p - 1;
+  if (RC && RS) {
+    RC->assign((size_t)2 * p * p, 0.0);
+    RS->assign((size_t)2 * p * p, 0.0);
+    for (int be = 0; be < 2; ++be)
+      for (int m = 0; m < p; ++m)
+        for (int lp = 0; lp < p; ++lp) {
+          ld s = ((ld)be + (ld)lp / P1) / 2.0L;
+          ld r = 1.0L;
+          for (int q = 0; q < p; ++q) {
+            if (q == m) continue;
+            r *= sinl(PI_L * (s * P1 - (ld)q) / ((ld)P1 * P1)) / sinl(PI_L * (ld)(m - q) / ((ld)P1 * P1));
+          }
+          ld c = cosl(PI_L * (ld)lp / (2.0L * P1)), sn = sinl(PI_L * (ld)lp / (2.0L * P1));
+          (*RC)[((size_t)be * p + m) * p + lp] = (double)(r * c);
+          (*RS)[((size_t)be * p + m) * p + lp] = (double)(r * sn);
+        }
+  }
   V.assign((size_t)2 * 4 * p * p, 0.0);
   for (int al = 0; al < 2; ++al)
     for (int be = 0; be < 2; ++be)
@@ -82,8 +108,12 @@ const DeviceTables* get_device_tables(int p, std::string* err) {
   auto key = std::make_pair(dev, p);
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
-  std::vector<double> V, invD;
-  build_tables_host(p, V, invD);
+  std::vector<double> V, invD, RC, RS;
+  build_tables_host(p, V, invD, &RC, &RS);
+  if (upload_const_tables(p, RC.data(), RS.data(), invD.data()) != cudaSuccess) {
+    if (err) *err = "constant table upload failed";
+    return nullptr;
+  }
   DeviceTables* t = new DeviceTables();
   t->p = p;
   if (cudaMalloc(&t->V, V.size() * sizeof(double)) != cudaSuccess ||
@@ -100,14 +130,19 @@ const DeviceTables* get_device_tables(int p, std::string* err) {
 
 }  // namespace sft
 
-// Exposed for CPU tests (host only): V [2][2][p][p] complex interleaved, invD [p].
-extern "C" int sft_operator_tables(int p, double* V, double* invD) {
+// Exposed for CPU tests (host only): V [2][2][p][p] complex interleaved, invD [p],
+// RC, RS [2][p][p] real (the constant-bank operands of the translation kernel).
+extern "C" int sft_operator_tables(int p, double* V, double* invD, double* RC, double* RS) {
   if (p < 3 || p > 15) return SFT_E_ARG;
-  std::vector<double> v, d;
-  sft::build_tables_host(p, v, d);
+  std::vector<double> v, d, rc, rs;
+  sft::build_tables_host(p, v, d, &rc, &rs);
   if (V)
     for (size_t i = 0; i < v.size(); ++i) V[i] = v[i];
   if (invD)
     for (size_t i = 0; i < d.size(); ++i) invD[i] = d[i];
+  if (RC)
+    for (size_t i = 0; i < rc.size(); ++i) RC[i] = rc[i];
+  if (RS)
+    for (size_t i = 0; i < rs.size(); ++i) RS[i] = rs[i];
   return SFT_OK;
 }

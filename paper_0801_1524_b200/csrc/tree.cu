@@ -137,6 +137,7 @@ static int tree_phase1(sft_plan_s* P, Tree& T, const double* pts, int64_t n, Scr
   CK(dalloc(&S.hist, L + 1, s));
   CK(cudaMemsetAsync(S.hist, 0, (L + 1) * sizeof(unsigned long long), s));
   k_leaf_keys<<<nblk(n, 256), 256, 0, s>>>(pts, n, d, L, (double)P->N, P->N, S.keys_in, S.idx_in, P->d_err);
+  count_launch();
   CK(cudaGetLastError());
   size_t need = 0;
   CK(cub::DeviceRadixSort::SortPairs(nullptr, need, S.keys_in, T.keys_sorted, S.idx_in, T.perm, (int)n, 0, d * L, s));
@@ -147,6 +148,7 @@ static int tree_phase1(sft_plan_s* P, Tree& T, const double* pts, int64_t n, Scr
   CK(cub::DeviceRadixSort::SortPairs(S.cub_tmp, need, S.keys_in, T.keys_sorted, S.idx_in, T.perm, (int)n, 0, d * L,
                                      s));
   k_min_level<<<nblk(n, 256), 256, 0, s>>>(T.keys_sorted, n, d, L, S.ml, S.hist);
+  count_launch();
   CK(cudaGetLastError());
   return SFT_OK;
 }
@@ -183,6 +185,7 @@ static int tree_phase2(sft_plan_s* P, Tree& T, const double* pts, const std::vec
   for (int l = L; l >= 0; --l) {
     int32_t* bid = bufs[l & 1];
     k_flags<<<nblk(n, 256), 256, 0, s>>>(S.ml, n, l, bid);
+    count_launch();
     CK(cudaGetLastError());
     size_t nb = S.cub_bytes;
     CK(cub::DeviceScan::InclusiveSum(S.cub_tmp, nb, bid, bid, (int)n, s));
@@ -190,11 +193,13 @@ static int tree_phase2(sft_plan_s* P, Tree& T, const double* pts, const std::vec
     k_fill_level<<<nblk(n, 256), 256, 0, s>>>(T.keys_sorted, S.ml, n, d, L, l, bid, bid_up, lv.key, lv.child_begin,
                                               lv.child_mask, l < L ? T.lev[l + 1].parent : nullptr,
                                               l == L ? T.first_pt : nullptr);
+    count_launch();
     CK(cudaGetLastError());
     bid_up = bid;
   }
   k_set_i32<<<1, 1, 0, s>>>(T.first_pt + T.lev[L].n, (int32_t)n);
   k_gather_pts<<<nblk(n, 256), 256, 0, s>>>(pts, T.perm, n, d, T.pts_sorted);
+  count_launch(2);
   CK(cudaGetLastError());
   CK(cudaFreeAsync(S.keys_in, s));
   CK(cudaFreeAsync(S.idx_in, s));

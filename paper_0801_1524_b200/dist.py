@@ -1,0 +1,90 @@
+"""Multi-GPU butterfly: one process per GPU.
+
+Phase 1 runs levels t = L..m over this rank's T_K subtrees (level s_K),
+one ``all_to_all_single`` over NCCL/NVLink redistributes the level-m
+equivalent charges to the owners of the T_X subtrees (level s_X), phase 2
+runs levels t = m-1..0 and the final evaluation for this rank's targets, and
+a sum all-reduce assembles u (each entry has exactly one non-zero
+contributor, so the sum is exact and u is bitwise equal to the 1-GPU result).
+
+torch.distributed is plumbing only (process group, the collective calls);
+every arithmetic step runs in libsft's kernels.  ``exchange`` may be
+replaced (tests use a gloo group on CPU with host-side buffers).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import Plan
+
+
+class DistPlan:
+    def __init__(self, dim, N, p, x, k, group=None, stream=None, exchange_level=-1, split_k=-1, split_x=-1):
+        import torch
+        import torch.distributed as dist
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.plan = Plan(dim, N, p, x, k, stream=stream, rank=self.rank, world=self.world,
+                         exchange_level=exchange_level, split_k=split_k, split_x=split_x)
+        self.nx = self.plan.nx
+        s, r = self.plan.exchange_counts()
+        self.send_counts = [int(v) for v in s]
+        self.recv_counts = [int(v) for v in r]
+        dev = x.device if isinstance(x, torch.Tensor) and x.is_cuda else torch.device("cuda", torch.cuda.current_device())
+        self.sendbuf = torch.empty(max(1, sum(self.send_counts)), dtype=torch.complex128, device=dev)
+        self.recvbuf = torch.empty(max(1, sum(self.recv_counts)), dtype=torch.complex128, device=dev)
+        self.device = dev
+
+    def partition(self):
+        return self.plan.partition()
+
+    def apply(self, f, u=None):
+        import torch
+        import torch.distributed as dist
+        if u is None:
+            u = torch.empty(self.nx, dtype=torch.complex128, device=self.device)
+        self.plan.apply_phase1(f, self.sendbuf)
+        # the level-m charge exchange (NCCL all-to-allv over NVLink)
+        dist.all_to_all_single(self.recvbuf[: sum(self.recv_counts)], self.sendbuf[: sum(self.send_counts)],
+                               output_split_sizes=self.recv_counts, input_split_sizes=self.send_counts,
+                               group=self.group)
+        self.plan.apply_phase2(self.recvbuf, u)
+        dist.all_reduce(u, op=dist.ReduceOp.SUM, group=self.group)
+        return u
+
+    def close(self):
+        self.plan.close()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+
+def exchange_layout(counts_x, counts_k, parents_x, parents_k, world, pd, force=(-1, -1, -1)):
+    """Host-side description of the level-m exchange that DistPlan performs,
+    computed from the same partitioner the library uses (sft_choose_partition):
+    returns dict with s_K, s_X, m, per-rank B ranges at level m, A ranges at
+    level L-m, and send/recv element counts per (src, dst)."""
+    from . import choose_partition
+    L = len(counts_x) - 1
+    sk, sx, m, rng, cost = choose_partition(L, world, counts_x, counts_k, parents_x, parents_k, force)
+
+    def desc_range(parents, s, lo, hi, lev):
+        """boxes at level `lev` whose ancestor at level s lies in [lo, hi)"""
+        if lev == s:
+            return int(lo), int(hi)
+        a = np.asarray(parents[lev])          # ancestors at lev-1
+        for l in range(lev - 1, s, -1):
+            a = np.asarray(parents[l])[a]     # ... up to level s
+        return int(np.searchsorted(a, lo)), int(np.searchsorted(a, hi))
+
+    b_rng = [desc_range(parents_k, sk, rng[r, 0], rng[r, 1], m) for r in range(world)]
+    a_rng = [desc_range(parents_x, sx, rng[r, 2], rng[r, 3], L - m) for r in range(world)]
+    counts = np.zeros((world, world), np.int64)
+    for src in range(world):
+        for dst in range(world):
+            counts[src, dst] = (b_rng[src][1] - b_rng[src][0]) * (a_rng[dst][1] - a_rng[dst][0]) * pd
+    return dict(sk=sk, sx=sx, m=m, b_rng=b_rng, a_rng=a_rng, counts=counts, cost=cost)
