@@ -19,22 +19,31 @@ from . import Plan
 
 
 class DistPlan:
-    def __init__(self, dim, N, p, x, k, group=None, stream=None, exchange_level=-1, split_k=-1, split_x=-1):
+    """One rank of the sharded transform.  ``plan`` may be injected (tests use
+    a host-side stand-in with a gloo group); by default it is a libsft plan
+    with rank/world taken from the process group."""
+
+    def __init__(self, dim, N, p, x, k, group=None, stream=None, exchange_level=-1, split_k=-1, split_x=-1,
+                 plan=None, device=None):
         import torch
         import torch.distributed as dist
         self.group = group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
-        self.plan = Plan(dim, N, p, x, k, stream=stream, rank=self.rank, world=self.world,
-                         exchange_level=exchange_level, split_k=split_k, split_x=split_x)
-        self.nx = self.plan.nx
-        s, r = self.plan.exchange_counts()
+        if plan is None:
+            plan = Plan(dim, N, p, x, k, stream=stream, rank=self.rank, world=self.world,
+                        exchange_level=exchange_level, split_k=split_k, split_x=split_x)
+        self.plan = plan
+        self.nx = plan.nx
+        s, r = plan.exchange_counts()
         self.send_counts = [int(v) for v in s]
         self.recv_counts = [int(v) for v in r]
-        dev = x.device if isinstance(x, torch.Tensor) and x.is_cuda else torch.device("cuda", torch.cuda.current_device())
-        self.sendbuf = torch.empty(max(1, sum(self.send_counts)), dtype=torch.complex128, device=dev)
-        self.recvbuf = torch.empty(max(1, sum(self.recv_counts)), dtype=torch.complex128, device=dev)
-        self.device = dev
+        if device is None:
+            device = x.device if isinstance(x, torch.Tensor) and x.is_cuda else torch.device(
+                "cuda", torch.cuda.current_device())
+        self.device = torch.device(device)
+        self.sendbuf = torch.empty(max(1, sum(self.send_counts)), dtype=torch.complex128, device=self.device)
+        self.recvbuf = torch.empty(max(1, sum(self.recv_counts)), dtype=torch.complex128, device=self.device)
 
     def partition(self):
         return self.plan.partition()
@@ -45,12 +54,16 @@ class DistPlan:
         if u is None:
             u = torch.empty(self.nx, dtype=torch.complex128, device=self.device)
         self.plan.apply_phase1(f, self.sendbuf)
-        # the level-m charge exchange (NCCL all-to-allv over NVLink)
-        dist.all_to_all_single(self.recvbuf[: sum(self.recv_counts)], self.sendbuf[: sum(self.send_counts)],
-                               output_split_sizes=self.recv_counts, input_split_sizes=self.send_counts,
-                               group=self.group)
+        # the level-m charge exchange (NCCL all-to-allv over NVLink); complex128
+        # moved as (re, im) float64 pairs
+        ns, nr = sum(self.send_counts), sum(self.recv_counts)
+        dist.all_to_all_single(torch.view_as_real(self.recvbuf[:nr]).reshape(-1),
+                               torch.view_as_real(self.sendbuf[:ns]).reshape(-1),
+                               output_split_sizes=[2 * c for c in self.recv_counts],
+                               input_split_sizes=[2 * c for c in self.send_counts], group=self.group)
         self.plan.apply_phase2(self.recvbuf, u)
-        dist.all_reduce(u, op=dist.ReduceOp.SUM, group=self.group)
+        # every target has exactly one non-zero contributor: the sum is exact
+        dist.all_reduce(torch.view_as_real(u), op=dist.ReduceOp.SUM, group=self.group)
         return u
 
     def close(self):
