@@ -24,7 +24,7 @@ import numpy as np
 __all__ = ["Plan", "lib", "LIB_PATH", "SftError", "operator_tables", "choose_partition", "HEADER_SYMBOLS", "launch_count"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsft.so")
+LIB_PATH = os.environ.get("SFT_LIB", os.path.join(_HERE, "libsft.so"))
 HEADER = os.path.join(os.path.dirname(_HERE), "include", "sft.h")
 
 _c_i64p = ctypes.POINTER(ctypes.c_int64)

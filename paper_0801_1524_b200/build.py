@@ -27,9 +27,10 @@ def _stale() -> bool:
     return any(os.path.getmtime(p) > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False, extra=()) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, extra=(), out=None) -> str:
+    if out is None and not force and not _stale():
         return LIB
+    target = out or LIB
     srcs = []
     for f in SOURCES:
         path = os.path.join(CSRC, f)
@@ -37,12 +38,12 @@ def build(force: bool = False, verbose: bool = False, extra=()) -> str:
             srcs += ["-x", "cu", path]
         else:
             srcs.append(path)
-    cmd = [NVCC, *FLAGS, *extra, "-shared", "-o", LIB + ".tmp", *srcs]
+    cmd = [NVCC, *FLAGS, *extra, "-shared", "-o", target + ".tmp", *srcs]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(target + ".tmp", target)
+    return target
 
 
 if __name__ == "__main__":

@@ -14,6 +14,7 @@
 //
 // No floating-point atomics: every output is produced by one thread in a fixed
 // order, so results are bitwise reproducible.
+#include <algorithm>
 #include <atomic>
 
 #include "sft_internal.cuh"
@@ -197,100 +198,143 @@ __device__ __forceinline__ int nth_set(uint32_t m, int n) {
   return __ffs(m) - 1;
 }
 
-// y_alpha += T[alpha][B] x  for both alpha (CS form, constant-bank operands)
-template <int P, int B>
-__device__ __forceinline__ void contract(const double2 (&x)[P], double2 (&z0)[P], double2 (&z1)[P]) {
+// One fiber, both outputs, children present per CLS (bit 0: beta=0, bit 1:
+// beta=1); straight-line code over all rows so the compiler can interleave
+// the independent DFMA chains.  CS form with constant-bank operands:
+//   z_alpha[m] = sum_beta c_{alpha beta} (RC_beta[m] . x_beta + i (2 alpha - 1) RS_beta[m] . x_beta)
+// c_{alpha,0} = 1, c_{0,1} = i, c_{1,1} = -i.
+template <int P, int CLS, class Store>
+__device__ __forceinline__ void contract_fiber(const double2 (&x0)[P], const double2 (&x1)[P], Store store) {
 #pragma unroll
   for (int m = 0; m < P; ++m) {
-    double ur = 0.0, ui = 0.0, vr = 0.0, vi = 0.0;
+    double2 z0 = make_double2(0.0, 0.0), z1 = make_double2(0.0, 0.0);
+    if (CLS & 1) {
+      double ur = 0.0, ui = 0.0, vr = 0.0, vi = 0.0;
 #pragma unroll
-    for (int l = 0; l < P; ++l) {
-      const double c = CT<P>::rc(B, m, l), s = CT<P>::rs(B, m, l);
-      ur = fma(c, x[l].x, ur);
-      ui = fma(c, x[l].y, ui);
-      vr = fma(s, x[l].x, vr);
-      vi = fma(s, x[l].y, vi);
+      for (int l = 0; l < P; ++l) {
+        const double c = CT<P>::rc(0, m, l), s = CT<P>::rs(0, m, l);
+        ur = fma(c, x0[l].x, ur);
+        ui = fma(c, x0[l].y, ui);
+        vr = fma(s, x0[l].x, vr);
+        vi = fma(s, x0[l].y, vi);
+      }
+      z0 = make_double2(ur + vi, ui - vr);
+      z1 = make_double2(ur - vi, ui + vr);
     }
-    // alpha=0: u - i v = (ur + vi) + i (ui - vr);  alpha=1: u + i v = (ur - vi) + i (ui + vr)
-    if (B == 0) {
-      z0[m].x += ur + vi;
-      z0[m].y += ui - vr;
-      z1[m].x += ur - vi;
-      z1[m].y += ui + vr;
-    } else {  // c_{0,1} = i, c_{1,1} = -i
-      z0[m].x -= ui - vr;
-      z0[m].y += ur + vi;
-      z1[m].x += ui + vr;
-      z1[m].y -= ur - vi;
+    if (CLS & 2) {
+      double ur = 0.0, ui = 0.0, vr = 0.0, vi = 0.0;
+#pragma unroll
+      for (int l = 0; l < P; ++l) {
+        const double c = CT<P>::rc(1, m, l), s = CT<P>::rs(1, m, l);
+        ur = fma(c, x1[l].x, ur);
+        ui = fma(c, x1[l].y, ui);
+        vr = fma(s, x1[l].x, vr);
+        vi = fma(s, x1[l].y, vi);
+      }
+      z0.x -= ui - vr;
+      z0.y += ur + vi;
+      z1.x += ui + vr;
+      z1.y -= ur - vi;
     }
+    store(m, z0, z1);
   }
 }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
-template <int D, int P, int G, int NT, int AX, bool LAST>
+// named barrier over the NT consumer threads (the producer warp never joins)
+template <int NT>
+__device__ __forceinline__ void cons_sync() {
+  asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
+}
+
+struct TaskEntry {
+  uint8_t j, bp, as, cls;
+};
+
+// One axis pass over a tile of ng groups held in shared memory (slots
+// [j][NS][PD]).  Tasks = (group, beta-prefix bp, alpha-suffix as) x fiber;
+// each reads the fibers of slots (bp,0,as) and (bp,1,as) and writes both
+// alpha outputs in place (or to HBM in the last pass).  Task entries are
+// sorted by child class (both / beta=0 only / beta=1 only) so that warps run
+// one straight-line code path.
+template <int D, int P, int G, int NT, int AX, bool LAST, class Sync>
 __device__ __forceinline__ void trans_pass(const TransArgs& a, double2* __restrict__ sb, const GroupMeta* gm, int ng,
-                                           int* pre) {
+                                           TaskEntry* ent, int* cnt, int tid, Sync sync) {
   constexpr int PD = Pow<P, D>::v;
   constexpr int NS = 1 << D;
   constexpr int PF = PD / P;
   constexpr int STR = Pow<P, D - 1 - AX>::v;  // stride of axis AX
   constexpr int SH = D - 1 - AX;              // bit of axis AX in a slot index
-  // per-group task counts -> prefix (G is small)
-  if (threadIdx.x == 0) {
-    int acc = 0;
-    for (int j = 0; j < ng; ++j) {
-      pre[j] = acc;
-      const uint32_t PBp = AX > 0 ? proj_hi<D>(gm[j].mB, AX) : 1u;
-      const uint32_t PAs = proj_lo<D>(gm[j].mA, D - 1 - AX);
-      acc += __popc(PBp) * __popc(PAs) * PF;
+  constexpr int MAXE = 1 << (D - 1);          // combos per group
+  // entries of group tid (tid < ng), per class
+  TaskEntry mine[MAXE];
+  int nmine = 0, c3 = 0, c1 = 0, c2 = 0;
+  if (tid < ng) {
+    const uint32_t mB = gm[tid].mB, mA = gm[tid].mA;
+    const uint32_t PBp = AX > 0 ? proj_hi<D>(mB, AX) : 1u;
+    const uint32_t PAs = proj_lo<D>(mA, D - 1 - AX);
+    const uint32_t PBa = proj_hi<D>(mB, AX + 1);
+#pragma unroll
+    for (int bp = 0; bp < (1 << AX); ++bp) {
+      if (!(PBp >> bp & 1)) continue;
+      const int cls = (int)((PBa >> (bp << 1)) & 3u);
+#pragma unroll
+      for (int as = 0; as < (1 << (D - 1 - AX)); ++as) {
+        if (!(PAs >> as & 1)) continue;
+        mine[nmine++] = TaskEntry{(uint8_t)tid, (uint8_t)bp, (uint8_t)as, (uint8_t)cls};
+        c3 += cls == 3;
+        c1 += cls == 1;
+        c2 += cls == 2;
+      }
     }
-    pre[ng] = acc;
+    cnt[tid] = c3;
+    cnt[G + tid] = c1;
+    cnt[2 * G + tid] = c2;
   }
-  __syncthreads();
-  const int ntot = pre[ng];
-  for (int tau = threadIdx.x; tau < ntot; tau += NT) {
-    int j = 0;
-    while (j + 1 < ng && tau >= pre[j + 1]) ++j;
-    const GroupMeta g = gm[j];
-    const int local = tau - pre[j];
-    const int combo = local / PF, f = local % PF;
-    const uint32_t PBp = AX > 0 ? proj_hi<D>(g.mB, AX) : 1u;
-    const uint32_t PAs = proj_lo<D>(g.mA, D - 1 - AX);
-    const uint32_t PBa = proj_hi<D>(g.mB, AX + 1);
-    const uint32_t PAa = proj_lo<D>(g.mA, D - AX);
-    const int nas = __popc(PAs);
-    const int bp = nth_set(PBp, combo / nas), as = nth_set(PAs, combo % nas);
-    const bool vb0 = PBa >> (bp << 1) & 1, vb1 = PBa >> ((bp << 1) | 1) & 1;
+  sync();
+  if (tid < ng) {
+    // offsets: all class-3 entries first, then class 1, then class 2
+    int o3 = 0, o1 = 0, o2 = 0, t3 = 0, t1 = 0;
+    for (int j = 0; j < ng; ++j) {
+      if (j < tid) {
+        o3 += cnt[j];
+        o1 += cnt[G + j];
+        o2 += cnt[2 * G + j];
+      }
+      t3 += cnt[j];
+      t1 += cnt[G + j];
+    }
+    o1 += t3;
+    o2 += t3 + t1;
+    for (int e = 0; e < nmine; ++e) {
+      const int cls = mine[e].cls;
+      const int pos = cls == 3 ? o3++ : (cls == 1 ? o1++ : o2++);
+      ent[pos] = mine[e];
+    }
+    if (tid == ng - 1) cnt[3 * G] = o2;  // total entries
+  }
+  sync();
+  const int ntot = cnt[3 * G] * PF;
+  for (int tau = tid; tau < ntot; tau += NT) {
+    const TaskEntry te = ent[tau / PF];
+    const int f = tau % PF;
+    const GroupMeta& g = gm[te.j];
     const int lo = f % STR, hi = f / STR;
     const int ebase = hi * STR * P + lo;
-    const int slot0 = (bp << (D - AX)) | as;  // slot with bit SH = 0
-    double2* s0 = sb + ((int64_t)j * NS + slot0) * PD + ebase;
-    double2* s1 = sb + ((int64_t)j * NS + (slot0 | (1 << SH))) * PD + ebase;
-    double2 z0[P], z1[P], x[P];
-#pragma unroll
-    for (int m = 0; m < P; ++m) z0[m] = z1[m] = make_double2(0.0, 0.0);
-    if (vb0) {
-#pragma unroll
-      for (int l = 0; l < P; ++l) x[l] = s0[l * STR];
-      contract<P, 0>(x, z0, z1);
-    }
-    if (vb1) {
-#pragma unroll
-      for (int l = 0; l < P; ++l) x[l] = s1[l * STR];
-      contract<P, 1>(x, z0, z1);
-    }
+    const int slot0 = (te.bp << (D - AX)) | te.as;  // slot with bit SH = 0
+    double2* s0 = sb + ((int64_t)te.j * NS + slot0) * PD + ebase;
+    double2* s1 = sb + ((int64_t)te.j * NS + (slot0 | (1 << SH))) * PD + ebase;
+    double2 x0[P], x1[P];
+    double2* o0 = nullptr;
+    double2* o1 = nullptr;
     if (!LAST) {
-      // in place: slot (bp, t, as) now holds alpha_AX = t
-#pragma unroll
-      for (int m = 0; m < P; ++m) {
-        s0[m * STR] = z0[m];
-        s1[m * STR] = z1[m];
-      }
+      o0 = s0;
+      o1 = s1;
     } else {
 #pragma unroll
       for (int t = 0; t < 2; ++t) {
-        const int alpha = (t << SH) | as;  // child index of A within A'
+        const int alpha = (t << SH) | te.as;  // child index of A within A'
         if (!(g.mA >> alpha & 1)) continue;
         const int64_t iA = (int64_t)g.cbX + __popc(g.mA & ((1u << alpha) - 1));
         int64_t pidx;
@@ -302,26 +346,160 @@ __device__ __forceinline__ void trans_pass(const TransArgs& a, double2* __restri
           const int64_t wq = a.seg[q + 1] - a.seg[q];
           pidx = a.seg[a.nseg + 1 + q] + (g.iB - a.out_b0) * wq + (iA - a.seg[q]);
         }
-        double2* o = a.out + pidx * PD + ebase;
-        const double2* z = t ? z1 : z0;
-#pragma unroll
-        for (int m = 0; m < P; ++m) o[m * STR] = z[m];
+        (t ? o1 : o0) = a.out + pidx * PD + ebase;
       }
     }
+    auto store = [&](int m, double2 z0, double2 z1) {
+      if (o0) o0[m * STR] = z0;
+      if (o1) o1[m * STR] = z1;
+    };
+    if (te.cls == 3) {
+#pragma unroll
+      for (int l = 0; l < P; ++l) {
+        x0[l] = s0[l * STR];
+        x1[l] = s1[l * STR];
+      }
+      contract_fiber<P, 3>(x0, x1, store);
+    } else if (te.cls == 1) {
+#pragma unroll
+      for (int l = 0; l < P; ++l) x0[l] = s0[l * STR];
+      contract_fiber<P, 1>(x0, x1, store);
+    } else {
+#pragma unroll
+      for (int l = 0; l < P; ++l) x1[l] = s1[l * STR];
+      contract_fiber<P, 2>(x0, x1, store);
+    }
   }
-  __syncthreads();
+  sync();
 }
 
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  }
+}
+
+// Persistent, warp-specialised translation kernel.  Warp 0 is the producer:
+// for each tile of G groups it reads the group metadata (child masks and
+// first-child indices of B and A') and issues one 1-D TMA bulk copy per
+// present child array into a 2-stage shared-memory ring (mbarrier
+// complete_tx).  Warps 1..NT/32 consume: the axis passes run in place in the
+// stage, the last pass stores the parent arrays to HBM, then the stage is
+// released to the producer.  Loads of tile i+1 overlap the math of tile i.
 template <int D, int P, int G, int NT>
-__global__ __launch_bounds__(NT) void k_translate(TransArgs a) {
+__global__ __launch_bounds__(NT + 32) void k_translate(TransArgs a, int64_t ntiles) {
+  constexpr int PD = Pow<P, D>::v;
+  constexpr int NS = 1 << D;
+  constexpr int STAGE = G * NS * PD;  // double2 per stage
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double2* ring = reinterpret_cast<double2*>(smem_raw);  // [2][G][NS][PD]
+  __shared__ GroupMeta gm[2][G];
+  __shared__ int ngs[2];
+  __shared__ TaskEntry ent[G << (D - 1)];
+  __shared__ int cnt[3 * G + 1];
+  __shared__ __align__(8) uint64_t full[2], empty[2];
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < 2; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full[s])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&empty[s])));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == 0) {
+    // ---------------- producer ----------------
+    for (int64_t i = 0;; ++i) {
+      const int64_t tile = blockIdx.x + i * (int64_t)gridDim.x;
+      if (tile >= ntiles) break;
+      const int s = (int)(i & 1);
+      if (i >= 2) mbar_wait(smem_u32(&empty[s]), (uint32_t)(((i >> 1) + 1) & 1));
+      const int64_t g0 = tile * G;
+      const int ng = (int)min((int64_t)G, a.ngroups - g0);
+      uint32_t nbytes = 0;
+      if (lane < ng) {
+        const int64_t g = g0 + lane;
+        GroupMeta m;
+        m.iB = a.b_lo + g / a.nAp_grp;
+        m.iAp = a.ap_lo + g % a.nAp_grp;
+        m.cbK = a.cbK[m.iB];
+        m.mB = a.mK[m.iB];
+        m.cbX = a.cbX[m.iAp];
+        m.mA = a.mX[m.iAp];
+        gm[s][lane] = m;
+        nbytes = __popc(m.mB) * PD * (uint32_t)sizeof(double2);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) nbytes += __shfl_xor_sync(0xffffffffu, nbytes, o);
+      if (lane == 0) {
+        ngs[s] = ng;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&full[s])),
+                     "r"(nbytes)
+                     : "memory");
+      }
+      __syncwarp();
+      if (lane < ng) {
+        const GroupMeta& m = gm[s][lane];
+        uint32_t mm = m.mB;
+        int r = 0;
+        while (mm) {
+          const int c = __ffs(mm) - 1;
+          mm &= mm - 1;
+          const int64_t iBc = (int64_t)m.cbK + r++;
+          const int64_t pin = (iBc - a.in_b0) * a.in_nA + (m.iAp - a.in_a0);
+          const double2* src = a.in + pin * PD;
+          double2* dst = ring + (int64_t)s * STAGE + ((int64_t)lane * NS + c) * PD;
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                  smem_u32(dst)),
+              "l"(src), "r"((uint32_t)(PD * sizeof(double2))), "r"(smem_u32(&full[s]))
+              : "memory");
+        }
+      }
+    }
+    return;
+  }
+  // ---------------- consumers ----------------
+  const int tid = threadIdx.x - 32;
+  for (int64_t i = 0;; ++i) {
+    const int64_t tile = blockIdx.x + i * (int64_t)gridDim.x;
+    if (tile >= ntiles) break;
+    const int s = (int)(i & 1);
+    mbar_wait(smem_u32(&full[s]), (uint32_t)((i >> 1) & 1));
+    double2* sb = ring + (int64_t)s * STAGE;
+    const int ng = ngs[s];
+    auto sync = [] { cons_sync<NT>(); };
+    if constexpr (D == 2) {
+      trans_pass<D, P, G, NT, 1, false>(a, sb, gm[s], ng, ent, cnt, tid, sync);
+      trans_pass<D, P, G, NT, 0, true>(a, sb, gm[s], ng, ent, cnt, tid, sync);
+    } else {
+      trans_pass<D, P, G, NT, 2, false>(a, sb, gm[s], ng, ent, cnt, tid, sync);
+      trans_pass<D, P, G, NT, 1, false>(a, sb, gm[s], ng, ent, cnt, tid, sync);
+      trans_pass<D, P, G, NT, 0, true>(a, sb, gm[s], ng, ent, cnt, tid, sync);
+    }
+    if (tid == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[s])) : "memory");
+  }
+}
+
+// Non-persistent variant: one CTA per tile, single stage; several CTAs per SM
+// overlap loads and math.  Selected per (d, p) by TransCfg::PERSIST.
+template <int D, int P, int G, int NT>
+__global__ __launch_bounds__(NT) void k_translate_np(TransArgs a) {
   constexpr int PD = Pow<P, D>::v;
   constexpr int NS = 1 << D;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double2* sb = reinterpret_cast<double2*>(smem_raw);  // [G][NS][PD]
   __shared__ GroupMeta gm[G];
-  __shared__ int pre[G + 1];
+  __shared__ TaskEntry ent[G << (D - 1)];
+  __shared__ int cnt[3 * G + 1];
   __shared__ __align__(8) uint64_t bar;
-
   const int64_t g0 = (int64_t)blockIdx.x * G;
   const int ng = (int)min((int64_t)G, a.ngroups - g0);
   if (threadIdx.x < ng) {
@@ -340,47 +518,42 @@ __global__ __launch_bounds__(NT) void k_translate(TransArgs a) {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  // stage the child arrays h^{A' B_c} of every group into slot c with 1-D TMA
-  if (threadIdx.x == 0) {
-    uint32_t bytes = 0;
-    for (int j = 0; j < ng; ++j) bytes += __popc(gm[j].mB) * PD * (uint32_t)sizeof(double2);
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar)), "r"(bytes)
-                 : "memory");
-    for (int j = 0; j < ng; ++j) {
-      uint32_t mm = gm[j].mB;
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    uint32_t nbytes = lane < ng ? __popc(gm[lane].mB) * PD * (uint32_t)sizeof(double2) : 0u;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) nbytes += __shfl_xor_sync(0xffffffffu, nbytes, o);
+    if (lane == 0)
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar)), "r"(nbytes)
+                   : "memory");
+    __syncwarp();
+    if (lane < ng) {
+      const GroupMeta& m = gm[lane];
+      uint32_t mm = m.mB;
       int r = 0;
       while (mm) {
         const int c = __ffs(mm) - 1;
         mm &= mm - 1;
-        const int64_t iBc = (int64_t)gm[j].cbK + r++;
-        const int64_t pin = (iBc - a.in_b0) * a.in_nA + (gm[j].iAp - a.in_a0);
-        const double2* src = a.in + pin * PD;
-        double2* dst = sb + ((int64_t)j * NS + c) * PD;
+        const int64_t iBc = (int64_t)m.cbK + r++;
+        const int64_t pin = (iBc - a.in_b0) * a.in_nA + (m.iAp - a.in_a0);
         asm volatile(
             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                smem_u32(dst)),
-            "l"(src), "r"((uint32_t)(PD * sizeof(double2))), "r"(smem_u32(&bar))
+                smem_u32(sb + ((int64_t)lane * NS + c) * PD)),
+            "l"(a.in + pin * PD), "r"((uint32_t)(PD * sizeof(double2))), "r"(smem_u32(&bar))
             : "memory");
       }
     }
   }
-  {
-    uint32_t done = 0;
-    while (!done) {
-      asm volatile(
-          "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n selp.u32 %0, 1, 0, p;\n}\n"
-          : "=r"(done)
-          : "r"(smem_u32(&bar))
-          : "memory");
-    }
-  }
+  mbar_wait(smem_u32(&bar), 0);
+  auto sync = [] { __syncthreads(); };
+  const int tid = threadIdx.x;
   if constexpr (D == 2) {
-    trans_pass<D, P, G, NT, 1, false>(a, sb, gm, ng, pre);
-    trans_pass<D, P, G, NT, 0, true>(a, sb, gm, ng, pre);
+    trans_pass<D, P, G, NT, 1, false>(a, sb, gm, ng, ent, cnt, tid, sync);
+    trans_pass<D, P, G, NT, 0, true>(a, sb, gm, ng, ent, cnt, tid, sync);
   } else {
-    trans_pass<D, P, G, NT, 2, false>(a, sb, gm, ng, pre);
-    trans_pass<D, P, G, NT, 1, false>(a, sb, gm, ng, pre);
-    trans_pass<D, P, G, NT, 0, true>(a, sb, gm, ng, pre);
+    trans_pass<D, P, G, NT, 2, false>(a, sb, gm, ng, ent, cnt, tid, sync);
+    trans_pass<D, P, G, NT, 1, false>(a, sb, gm, ng, ent, cnt, tid, sync);
+    trans_pass<D, P, G, NT, 0, true>(a, sb, gm, ng, ent, cnt, tid, sync);
   }
 }
 
@@ -451,32 +624,69 @@ __global__ void k_zero(double2* p, int64_t n) {
 // ------------------------------------------------------------------------
 // launchers
 // ------------------------------------------------------------------------
+// tile configuration: G groups per CTA, NT threads (tuned on B200)
+#ifndef SFT_PERSIST
+#define SFT_PERSIST 0
+#endif
+#ifndef SFT_G25
+#define SFT_G25 16
+#define SFT_NT25 128
+#endif
+#ifndef SFT_G27
+#define SFT_G27 12
+#define SFT_NT27 128
+#endif
+#ifndef SFT_G29
+#define SFT_G29 16
+#define SFT_NT29 256
+#endif
+#ifndef SFT_G35
+#define SFT_G35 4
+#define SFT_NT35 256
+#endif
+#ifndef SFT_G37
+#define SFT_G37 2
+#define SFT_NT37 256
+#endif
+#ifndef SFT_G39
+#define SFT_G39 1
+#define SFT_NT39 256
+#endif
 template <int D, int P>
 struct TransCfg;
 template <>
-struct TransCfg<2, 5> { static constexpr int G = 16, NT = 128; };
+struct TransCfg<2, 5> { static constexpr int G = SFT_G25, NT = SFT_NT25, PERSIST = SFT_PERSIST; };
 template <>
-struct TransCfg<2, 7> { static constexpr int G = 12, NT = 128; };
+struct TransCfg<2, 7> { static constexpr int G = SFT_G27, NT = SFT_NT27, PERSIST = SFT_PERSIST; };
 template <>
-struct TransCfg<2, 9> { static constexpr int G = 8, NT = 128; };
+struct TransCfg<2, 9> { static constexpr int G = SFT_G29, NT = SFT_NT29, PERSIST = SFT_PERSIST; };
 template <>
-struct TransCfg<3, 5> { static constexpr int G = 4, NT = 256; };
+struct TransCfg<3, 5> { static constexpr int G = SFT_G35, NT = SFT_NT35, PERSIST = SFT_PERSIST; };
 template <>
-struct TransCfg<3, 7> { static constexpr int G = 2, NT = 256; };
+struct TransCfg<3, 7> { static constexpr int G = SFT_G37, NT = SFT_NT37, PERSIST = SFT_PERSIST; };
 template <>
-struct TransCfg<3, 9> { static constexpr int G = 1, NT = 256; };
+struct TransCfg<3, 9> { static constexpr int G = SFT_G39, NT = SFT_NT39, PERSIST = SFT_PERSIST; };
 
 template <int D, int P>
 static cudaError_t launch_translate_t(const sft_plan_s* Pl, const LevelDims& L, const double2* in, double2* out) {
   constexpr int PD = Pow<P, D>::v;
   constexpr int G = TransCfg<D, P>::G, NT = TransCfg<D, P>::NT;
-  const size_t smem = (size_t)G * (1 << D) * PD * sizeof(double2);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(k_translate<D, P, G, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+  constexpr bool PERSIST = TransCfg<D, P>::PERSIST != 0;
+  const size_t smem = (size_t)(PERSIST ? 2 : 1) * G * (1 << D) * PD * sizeof(double2);
+  static int blocks_per_sm = -1, nsm = 0;
+  if (blocks_per_sm < 0) {
+    cudaError_t e = PERSIST ? cudaFuncSetAttribute(k_translate<D, P, G, NT>,
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
+                            : cudaFuncSetAttribute(k_translate_np<D, P, G, NT>,
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    attr_set = true;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    e = PERSIST ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_translate<D, P, G, NT>, NT + 32, smem)
+                : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_translate_np<D, P, G, NT>, NT, smem);
+    if (e != cudaSuccess) return e;
+    if (blocks_per_sm < 1) return cudaErrorInvalidConfiguration;
   }
   TransArgs a;
   a.in = in;
@@ -498,8 +708,13 @@ static cudaError_t launch_translate_t(const sft_plan_s* Pl, const LevelDims& L, 
   a.seg = L.seg;
   a.nseg = L.nseg;
   if (a.ngroups <= 0) return cudaSuccess;
-  const int64_t nblocks = (a.ngroups + G - 1) / G;
-  k_translate<D, P, G, NT><<<(unsigned)nblocks, NT, smem, Pl->stream>>>(a);
+  const int64_t ntiles = (a.ngroups + G - 1) / G;
+  if (PERSIST) {
+    const int64_t grid = std::min<int64_t>(ntiles, (int64_t)nsm * blocks_per_sm);
+    k_translate<D, P, G, NT><<<(unsigned)grid, NT + 32, smem, Pl->stream>>>(a, ntiles);
+  } else {
+    k_translate_np<D, P, G, NT><<<(unsigned)ntiles, NT, smem, Pl->stream>>>(a);
+  }
   count_launch();
   return cudaGetLastError();
 }
