@@ -266,10 +266,11 @@ __device__ __forceinline__ void trans_pass(const TransArgs& a, double2* __restri
   constexpr int PF = PD / P;
   constexpr int STR = Pow<P, D - 1 - AX>::v;  // stride of axis AX
   constexpr int SH = D - 1 - AX;              // bit of axis AX in a slot index
-  constexpr int MAXE = 1 << (D - 1);          // combos per group
-  // entries of group tid (tid < ng), per class
-  TaskEntry mine[MAXE];
-  int nmine = 0, c3 = 0, c1 = 0, c2 = 0;
+  constexpr int MAXE = G << (D - 1);  // combos per tile (upper bound)
+  // cnt[0..2]: per-class counts (class 3, 1, 2); entries appended per class
+  // (the order of independent tasks does not affect any result)
+  if (tid < 3) cnt[tid] = 0;
+  sync();
   if (tid < ng) {
     const uint32_t mB = gm[tid].mB, mA = gm[tid].mA;
     const uint32_t PBp = AX > 0 ? proj_hi<D>(mB, AX) : 1u;
@@ -279,45 +280,21 @@ __device__ __forceinline__ void trans_pass(const TransArgs& a, double2* __restri
     for (int bp = 0; bp < (1 << AX); ++bp) {
       if (!(PBp >> bp & 1)) continue;
       const int cls = (int)((PBa >> (bp << 1)) & 3u);
+      const int ci = cls == 3 ? 0 : (cls == 1 ? 1 : 2);
 #pragma unroll
       for (int as = 0; as < (1 << (D - 1 - AX)); ++as) {
         if (!(PAs >> as & 1)) continue;
-        mine[nmine++] = TaskEntry{(uint8_t)tid, (uint8_t)bp, (uint8_t)as, (uint8_t)cls};
-        c3 += cls == 3;
-        c1 += cls == 1;
-        c2 += cls == 2;
+        const int pos = atomicAdd(&cnt[ci], 1);
+        ent[ci * MAXE + pos] = TaskEntry{(uint8_t)tid, (uint8_t)bp, (uint8_t)as, (uint8_t)cls};
       }
     }
-    cnt[tid] = c3;
-    cnt[G + tid] = c1;
-    cnt[2 * G + tid] = c2;
   }
   sync();
-  if (tid < ng) {
-    // offsets: all class-3 entries first, then class 1, then class 2
-    int o3 = 0, o1 = 0, o2 = 0, t3 = 0, t1 = 0;
-    for (int j = 0; j < ng; ++j) {
-      if (j < tid) {
-        o3 += cnt[j];
-        o1 += cnt[G + j];
-        o2 += cnt[2 * G + j];
-      }
-      t3 += cnt[j];
-      t1 += cnt[G + j];
-    }
-    o1 += t3;
-    o2 += t3 + t1;
-    for (int e = 0; e < nmine; ++e) {
-      const int cls = mine[e].cls;
-      const int pos = cls == 3 ? o3++ : (cls == 1 ? o1++ : o2++);
-      ent[pos] = mine[e];
-    }
-    if (tid == ng - 1) cnt[3 * G] = o2;  // total entries
-  }
-  sync();
-  const int ntot = cnt[3 * G] * PF;
+  const int n3 = cnt[0], n1 = cnt[1], n2 = cnt[2];
+  const int ntot = (n3 + n1 + n2) * PF;
   for (int tau = tid; tau < ntot; tau += NT) {
-    const TaskEntry te = ent[tau / PF];
+    const int ei = tau / PF;
+    const TaskEntry te = ei < n3 ? ent[ei] : (ei < n3 + n1 ? ent[MAXE + ei - n3] : ent[2 * MAXE + ei - n3 - n1]);
     const int f = tau % PF;
     const GroupMeta& g = gm[te.j];
     const int lo = f % STR, hi = f / STR;
@@ -353,6 +330,12 @@ __device__ __forceinline__ void trans_pass(const TransArgs& a, double2* __restri
       if (o0) o0[m * STR] = z0;
       if (o1) o1[m * STR] = z1;
     };
+#ifdef SFT_ABL_NOCOMPUTE
+    if (true) {
+#pragma unroll
+      for (int m = 0; m < P; ++m) store(m, s0[m * STR], s1[m * STR]);
+    } else
+#endif
     if (te.cls == 3) {
 #pragma unroll
       for (int l = 0; l < P; ++l) {
@@ -391,22 +374,22 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
 // complete_tx).  Warps 1..NT/32 consume: the axis passes run in place in the
 // stage, the last pass stores the parent arrays to HBM, then the stage is
 // released to the producer.  Loads of tile i+1 overlap the math of tile i.
-template <int D, int P, int G, int NT>
-__global__ __launch_bounds__(NT + 32) void k_translate(TransArgs a, int64_t ntiles) {
+template <int D, int P, int G, int NT, int NSTAGE>
+__global__ __launch_bounds__(NT + 32, 1) void k_translate(TransArgs a, int64_t ntiles) {
   constexpr int PD = Pow<P, D>::v;
   constexpr int NS = 1 << D;
   constexpr int STAGE = G * NS * PD;  // double2 per stage
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  double2* ring = reinterpret_cast<double2*>(smem_raw);  // [2][G][NS][PD]
-  __shared__ GroupMeta gm[2][G];
-  __shared__ int ngs[2];
-  __shared__ TaskEntry ent[G << (D - 1)];
-  __shared__ int cnt[3 * G + 1];
-  __shared__ __align__(8) uint64_t full[2], empty[2];
+  double2* ring = reinterpret_cast<double2*>(smem_raw);  // [NSTAGE][G][NS][PD]
+  __shared__ GroupMeta gm[NSTAGE][G];
+  __shared__ int ngs[NSTAGE];
+  __shared__ TaskEntry ent[3 * (G << (D - 1))];
+  __shared__ int cnt[4];
+  __shared__ __align__(8) uint64_t full[NSTAGE], empty[NSTAGE];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < NSTAGE; ++s) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full[s])));
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&empty[s])));
     }
@@ -419,8 +402,8 @@ __global__ __launch_bounds__(NT + 32) void k_translate(TransArgs a, int64_t ntil
     for (int64_t i = 0;; ++i) {
       const int64_t tile = blockIdx.x + i * (int64_t)gridDim.x;
       if (tile >= ntiles) break;
-      const int s = (int)(i & 1);
-      if (i >= 2) mbar_wait(smem_u32(&empty[s]), (uint32_t)(((i >> 1) + 1) & 1));
+      const int s = (int)(i % NSTAGE);
+      if (i >= NSTAGE) mbar_wait(smem_u32(&empty[s]), (uint32_t)(((i / NSTAGE) + 1) & 1));
       const int64_t g0 = tile * G;
       const int ng = (int)min((int64_t)G, a.ngroups - g0);
       uint32_t nbytes = 0;
@@ -471,8 +454,8 @@ __global__ __launch_bounds__(NT + 32) void k_translate(TransArgs a, int64_t ntil
   for (int64_t i = 0;; ++i) {
     const int64_t tile = blockIdx.x + i * (int64_t)gridDim.x;
     if (tile >= ntiles) break;
-    const int s = (int)(i & 1);
-    mbar_wait(smem_u32(&full[s]), (uint32_t)((i >> 1) & 1));
+    const int s = (int)(i % NSTAGE);
+    mbar_wait(smem_u32(&full[s]), (uint32_t)((i / NSTAGE) & 1));
     double2* sb = ring + (int64_t)s * STAGE;
     const int ng = ngs[s];
     auto sync = [] { cons_sync<NT>(); };
@@ -490,16 +473,36 @@ __global__ __launch_bounds__(NT + 32) void k_translate(TransArgs a, int64_t ntil
 
 // Non-persistent variant: one CTA per tile, single stage; several CTAs per SM
 // overlap loads and math.  Selected per (d, p) by TransCfg::PERSIST.
+#ifdef SFT_INSTR
+__device__ unsigned long long* g_instr = nullptr;  // [blocks][8]
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define INSTR(k)                                                        \
+  if (threadIdx.x == 0 && g_instr) g_instr[(size_t)blockIdx.x * 8 + (k)] = gtime();
+#else
+#define INSTR(k)
+#endif
+
+// minBlocksPerSM: target 16 resident warps (an explicit 1 lets ptxas take
+// ~200 registers and halves occupancy; forcing fewer than ~120 spills)
+#ifndef SFT_WARPS_PER_SM
+#define SFT_WARPS_PER_SM 16
+#endif
+#define SFT_MINB(NT) ((SFT_WARPS_PER_SM * 32 / (NT)) > 0 ? (SFT_WARPS_PER_SM * 32 / (NT)) : 1)
 template <int D, int P, int G, int NT>
-__global__ __launch_bounds__(NT) void k_translate_np(TransArgs a) {
+__global__ __launch_bounds__(NT, SFT_MINB(NT)) void k_translate_np(TransArgs a) {
   constexpr int PD = Pow<P, D>::v;
   constexpr int NS = 1 << D;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double2* sb = reinterpret_cast<double2*>(smem_raw);  // [G][NS][PD]
   __shared__ GroupMeta gm[G];
-  __shared__ TaskEntry ent[G << (D - 1)];
-  __shared__ int cnt[3 * G + 1];
+  __shared__ TaskEntry ent[3 * (G << (D - 1))];
+  __shared__ int cnt[4];
   __shared__ __align__(8) uint64_t bar;
+  INSTR(0);
   const int64_t g0 = (int64_t)blockIdx.x * G;
   const int ng = (int)min((int64_t)G, a.ngroups - g0);
   if (threadIdx.x < ng) {
@@ -536,20 +539,37 @@ __global__ __launch_bounds__(NT) void k_translate_np(TransArgs a) {
         mm &= mm - 1;
         const int64_t iBc = (int64_t)m.cbK + r++;
         const int64_t pin = (iBc - a.in_b0) * a.in_nA + (m.iAp - a.in_a0);
+#ifndef SFT_ABL_NOLOAD
         asm volatile(
             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                 smem_u32(sb + ((int64_t)lane * NS + c) * PD)),
             "l"(a.in + pin * PD), "r"((uint32_t)(PD * sizeof(double2))), "r"(smem_u32(&bar))
             : "memory");
+#else
+        (void)pin;
+        asm volatile("mbarrier.complete_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&bar)),
+                     "r"((uint32_t)(PD * sizeof(double2))) : "memory");
+#endif
       }
     }
   }
+  INSTR(1);
   mbar_wait(smem_u32(&bar), 0);
+  INSTR(2);
   auto sync = [] { __syncthreads(); };
   const int tid = threadIdx.x;
   if constexpr (D == 2) {
     trans_pass<D, P, G, NT, 1, false>(a, sb, gm, ng, ent, cnt, tid, sync);
+    INSTR(3);
     trans_pass<D, P, G, NT, 0, true>(a, sb, gm, ng, ent, cnt, tid, sync);
+    INSTR(4);
+#ifdef SFT_INSTR
+    if (threadIdx.x == 0 && g_instr) {
+      unsigned smid;
+      asm("mov.u32 %0, %smid;" : "=r"(smid));
+      g_instr[(size_t)blockIdx.x * 8 + 7] = smid;
+    }
+#endif
   } else {
     trans_pass<D, P, G, NT, 2, false>(a, sb, gm, ng, ent, cnt, tid, sync);
     trans_pass<D, P, G, NT, 1, false>(a, sb, gm, ng, ent, cnt, tid, sync);
@@ -628,6 +648,9 @@ __global__ void k_zero(double2* p, int64_t n) {
 #ifndef SFT_PERSIST
 #define SFT_PERSIST 0
 #endif
+#ifndef SFT_NSTAGE
+#define SFT_NSTAGE 2
+#endif
 #ifndef SFT_G25
 #define SFT_G25 16
 #define SFT_NT25 128
@@ -672,10 +695,11 @@ static cudaError_t launch_translate_t(const sft_plan_s* Pl, const LevelDims& L, 
   constexpr int PD = Pow<P, D>::v;
   constexpr int G = TransCfg<D, P>::G, NT = TransCfg<D, P>::NT;
   constexpr bool PERSIST = TransCfg<D, P>::PERSIST != 0;
-  const size_t smem = (size_t)(PERSIST ? 2 : 1) * G * (1 << D) * PD * sizeof(double2);
+  constexpr int NSTAGE = SFT_NSTAGE;
+  const size_t smem = (size_t)(PERSIST ? NSTAGE : 1) * G * (1 << D) * PD * sizeof(double2);
   static int blocks_per_sm = -1, nsm = 0;
   if (blocks_per_sm < 0) {
-    cudaError_t e = PERSIST ? cudaFuncSetAttribute(k_translate<D, P, G, NT>,
+    cudaError_t e = PERSIST ? cudaFuncSetAttribute(k_translate<D, P, G, NT, NSTAGE>,
                                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
                             : cudaFuncSetAttribute(k_translate_np<D, P, G, NT>,
                                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -683,7 +707,7 @@ static cudaError_t launch_translate_t(const sft_plan_s* Pl, const LevelDims& L, 
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    e = PERSIST ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_translate<D, P, G, NT>, NT + 32, smem)
+    e = PERSIST ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_translate<D, P, G, NT, NSTAGE>, NT + 32, smem)
                 : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_translate_np<D, P, G, NT>, NT, smem);
     if (e != cudaSuccess) return e;
     if (blocks_per_sm < 1) return cudaErrorInvalidConfiguration;
@@ -711,7 +735,7 @@ static cudaError_t launch_translate_t(const sft_plan_s* Pl, const LevelDims& L, 
   const int64_t ntiles = (a.ngroups + G - 1) / G;
   if (PERSIST) {
     const int64_t grid = std::min<int64_t>(ntiles, (int64_t)nsm * blocks_per_sm);
-    k_translate<D, P, G, NT><<<(unsigned)grid, NT + 32, smem, Pl->stream>>>(a, ntiles);
+    k_translate<D, P, G, NT, NSTAGE><<<(unsigned)grid, NT + 32, smem, Pl->stream>>>(a, ntiles);
   } else {
     k_translate_np<D, P, G, NT><<<(unsigned)ntiles, NT, smem, Pl->stream>>>(a);
   }
@@ -763,6 +787,12 @@ cudaError_t launch_zero(double2* p, int64_t n, cudaStream_t s) {
 }
 
 }  // namespace sft
+
+#ifdef SFT_INSTR
+extern "C" int sft_instr_set(void* dev_buf) {
+  return cudaMemcpyToSymbol(sft::g_instr, &dev_buf, sizeof(void*)) == cudaSuccess ? 0 : 4;
+}
+#endif
 
 extern "C" int sft_launch_count(int64_t* out) {
   if (!out) return SFT_E_ARG;
