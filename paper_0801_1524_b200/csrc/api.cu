@@ -271,7 +271,7 @@ static void plan_free(sft_plan_s* P) {
   if (P->d_err) cudaFreeAsync(P->d_err, s);
   if (P->d_seg) cudaFreeAsync(P->d_seg, s);
   for (int i = 0; i < P->ev_created; ++i) cudaEventDestroy(P->ev[i]);
-  cudaStreamSynchronize(s);
+  // no sync: the frees above are stream-ordered behind any pending work
   delete P;
 }
 

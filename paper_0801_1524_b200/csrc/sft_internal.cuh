@@ -23,6 +23,7 @@ namespace sft {
 // the Lagrange / sine-product closed forms (tables.cpp); no G^{-1} anywhere.
 
 constexpr int kMaxDim = 3;
+constexpr int kMaxLevels = 21;  // N <= 2^20
 
 struct TreeLevel {
   int64_t n = 0;                  // non-empty boxes at this level
@@ -40,7 +41,7 @@ struct Tree {
   int32_t* first_pt = nullptr;     // [n_leaf+1] CSR of sorted points per leaf
   int32_t* perm = nullptr;         // [npts] sorted position -> user index
   double* pts_sorted = nullptr;    // [npts][d]
-  uint64_t* keys_sorted = nullptr; // [npts] leaf Morton keys in sorted order
+  void* arena = nullptr;           // one allocation holding every array above (X owns both trees')
 };
 
 struct DeviceTables {

@@ -1,28 +1,43 @@
 // tree.cu -- step 1 of the butterfly: adaptive quadtrees /
 // octrees T_X and T_K with unit-width leaves, keeping only non-empty boxes.
 //
-// GPU build, one pass per tree:
-//   1. leaf Morton key per point (c = min(floor(y), N-1) per axis; axis 0 is
-//      the most significant bit of each d-bit digit), domain check;
-//   2. radix sort of (key, index) -- CUB, compiled into this library;
-//   3. for every point the coarsest level at which it opens a new box
-//      (from the highest differing bit with its predecessor), one histogram
-//      -> exact box counts per level with a single host sync for both trees;
-//   4. per level: flag -> inclusive scan -> box ids; box keys, parent, child
-//      begin and child mask (children of a box are contiguous in Morton order).
+// Both trees are built together, in four launches and one host sync:
+//   1. k_leaf_keys: leaf Morton key of every point of x and k (c = min(floor(y),
+//      N-1) per axis; axis 0 is the most significant bit of each d-bit digit),
+//      tagged with a tree bit above the d*L key bits (X first), domain check;
+//   2. one radix sort of (key, index) over d*L+1 bits -- CUB, compiled into
+//      this library;
+//   3. k_count: per sorted point the coarsest level at which it opens a new
+//      box (highest differing key bit with its predecessor; the first point of
+//      each tree opens the root), and per 1024-point block the number of
+//      box-opening points at every level (warp ballots, no global atomics);
+//   4. k_fill: per block, the exclusive prefix of those counts over the
+//      earlier blocks of the same tree, then for every point its box id at
+//      every level (inclusive count of openers - 1); box-opening points write
+//      the box's key, parent, first child and their bit in the parent's child
+//      mask; every point writes its sorted coordinates and permutation entry;
+//      the last block of each tree writes the per-level box counts.
+// Level arrays live in one arena sized by the upper bound min(n, 2^(d*l)) per
+// level, so nothing on the device waits for the host; the single sync at the
+// end reads the exact counts (the apply needs them to size grids and buffers).
 #include <cub/cub.cuh>
 
 #include "sft_internal.cuh"
 
 namespace sft {
 
-__global__ void k_leaf_keys(const double* __restrict__ pts, int64_t n, int d, int L, double Nf, int64_t N,
-                            uint64_t* __restrict__ key, int32_t* __restrict__ idx, int* err) {
+constexpr int kBlk = 1024;  // points per block in k_count / k_fill
+
+__global__ void k_leaf_keys(const double* __restrict__ x, int64_t nx, const double* __restrict__ k, int64_t nk,
+                            int d, int L, double Nf, int64_t N, uint64_t* __restrict__ key,
+                            int32_t* __restrict__ idx, int* err) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
+  if (i >= nx + nk) return;
+  const bool tk = i >= nx;
+  const double* pts = tk ? k + (i - nx) * d : x + i * d;
   uint64_t c[kMaxDim] = {0, 0, 0};
   for (int a = 0; a < d; ++a) {
-    double y = pts[i * d + a];
+    double y = pts[a];
     if (!(y >= 0.0 && y <= Nf)) {  // also catches NaN
       atomicOr(err, 1);
       y = 0.0;
@@ -31,236 +46,319 @@ __global__ void k_leaf_keys(const double* __restrict__ pts, int64_t n, int d, in
     if (ci > N - 1) ci = N - 1;
     c[a] = (uint64_t)ci;
   }
-  uint64_t k = 0;
+  uint64_t kk = tk ? 1ull : 0ull;
   for (int b = L - 1; b >= 0; --b)
-    for (int a = 0; a < d; ++a) k = (k << 1) | ((c[a] >> b) & 1ull);
-  key[i] = k;
+    for (int a = 0; a < d; ++a) kk = (kk << 1) | ((c[a] >> b) & 1ull);
+  key[i] = kk;
   idx[i] = (int32_t)i;
 }
 
-// coarsest level at which sorted point i starts a new box
-__global__ void k_min_level(const uint64_t* __restrict__ key, int64_t n, int d, int L, uint8_t* __restrict__ ml,
-                            unsigned long long* __restrict__ hist) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  int lev = 0;
-  if (i > 0) {
-    uint64_t x = key[i] ^ key[i - 1];
-    if (x == 0) {
-      lev = L + 1;  // same leaf: never opens a box
-    } else {
-      int hb = 63 - __clzll((long long)x);
-      lev = L - hb / d;
+struct BlockMap {
+  int64_t nx, n;
+  int nbx;  // blocks covering [0, nx); blocks >= nbx cover [nx, n)
+  __device__ __forceinline__ void get(int b, int& tree, int64_t& ts, int64_t& lo, int64_t& hi) const {
+    tree = b >= nbx;
+    ts = tree ? nx : 0;
+    lo = ts + (int64_t)(tree ? b - nbx : b) * kBlk;
+    hi = min(lo + kBlk, tree ? n : nx);
+  }
+};
+
+// level at which sorted point i (of the tree starting at ts) opens a box;
+// L+1 = never (same leaf as its predecessor)
+__device__ __forceinline__ int open_level(const uint64_t* key, int64_t i, int64_t ts, int d, int L) {
+  if (i == ts) return 0;
+  const uint64_t x = key[i] ^ key[i - 1];
+  if (x == 0) return L + 1;
+  const int hb = 63 - __clzll((long long)x);
+  return L - hb / d;
+}
+
+__global__ __launch_bounds__(kBlk) void k_count(const uint64_t* __restrict__ key, BlockMap bm, int d, int L,
+                                                uint8_t* __restrict__ ml, int32_t* __restrict__ counts) {
+  __shared__ int cnt[kMaxLevels];
+  int tree;
+  int64_t ts, lo, hi;
+  bm.get(blockIdx.x, tree, ts, lo, hi);
+  if (threadIdx.x <= L) cnt[threadIdx.x] = 0;
+  __syncthreads();
+  const int64_t i = lo + threadIdx.x;
+  int m = L + 1;
+  if (i < hi) {
+    m = open_level(key, i, ts, d, L);
+    ml[i] = (uint8_t)m;
+  }
+  const int lane = threadIdx.x & 31;
+  for (int l = 0; l <= L; ++l) {
+    const unsigned b = __ballot_sync(0xffffffffu, m <= l);
+    if (lane == 0 && b) atomicAdd(&cnt[l], __popc(b));
+  }
+  __syncthreads();
+  if (threadIdx.x <= L) counts[(int64_t)blockIdx.x * (L + 1) + threadIdx.x] = cnt[threadIdx.x];
+}
+
+struct TreeOut {
+  uint64_t* key[kMaxLevels];
+  int32_t* child_begin[kMaxLevels];
+  uint32_t* child_mask[kMaxLevels];
+  int32_t* parent[kMaxLevels];
+  int32_t* first_pt;
+  int32_t* perm;
+  double* pts_sorted;
+  const double* pts;
+  int64_t* totals;  // [L+1] box counts per level
+};
+
+struct FillArgs {
+  TreeOut t[2];
+  BlockMap bm;
+  int nbk;
+};
+
+__global__ __launch_bounds__(kBlk) void k_fill(const uint64_t* __restrict__ key, const int32_t* __restrict__ idx,
+                                               const uint8_t* __restrict__ ml, const int32_t* __restrict__ counts,
+                                               FillArgs A, int d, int L) {
+  __shared__ int base[kMaxLevels];
+  __shared__ int woff[32][kMaxLevels];
+  int tree;
+  int64_t ts, lo, hi;
+  A.bm.get(blockIdx.x, tree, ts, lo, hi);
+  const TreeOut& T = A.t[tree];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int b_first = tree ? A.bm.nbx : 0;
+  const int b_last = tree ? A.bm.nbx + A.nbk - 1 : A.bm.nbx - 1;
+  // exclusive prefix of the level counts over the earlier blocks of this tree
+  if (warp <= L) {
+    int s = 0;
+    for (int b = b_first + lane; b < (int)blockIdx.x; b += 32) s += counts[(int64_t)b * (L + 1) + warp];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) base[warp] = s;
+  }
+  const int64_t i = lo + threadIdx.x;
+  const int m = i < hi ? (int)ml[i] : L + 1;
+  const unsigned le = (lane == 31) ? 0xffffffffu : ((2u << lane) - 1u);
+  for (int l = 0; l <= L; ++l) {
+    const unsigned b = __ballot_sync(0xffffffffu, m <= l);
+    if (lane == 0) woff[warp][l] = __popc(b);
+  }
+  __syncthreads();
+  if (threadIdx.x <= L) {  // exclusive scan over warps, per level; block total
+    int s = 0;
+    for (int w = 0; w < 32; ++w) {
+      const int v = woff[w][threadIdx.x];
+      woff[w][threadIdx.x] = s;
+      s += v;
     }
+    if ((int)blockIdx.x == b_last) T.totals[threadIdx.x] = base[threadIdx.x] + s;
   }
-  ml[i] = (uint8_t)lev;
-  if (lev <= L) atomicAdd(&hist[lev], 1ull);
-}
-
-__global__ void k_flags(const uint8_t* __restrict__ ml, int64_t n, int lev, int32_t* __restrict__ flag) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < n) flag[i] = ml[i] <= lev ? 1 : 0;
-}
-
-// bid: inclusive scan of flags at this level (box id + 1 of every point)
-// bid_up: same for level lev+1 (nullptr at the leaf level)
-__global__ void k_fill_level(const uint64_t* __restrict__ key, const uint8_t* __restrict__ ml, int64_t n, int d,
-                             int L, int lev, const int32_t* __restrict__ bid, const int32_t* __restrict__ bid_up,
-                             uint64_t* __restrict__ bkey, int32_t* __restrict__ child_begin,
-                             uint32_t* __restrict__ child_mask, int32_t* __restrict__ parent_up,
-                             int32_t* __restrict__ first_pt) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  int m = ml[i];
-  int32_t b = bid[i] - 1;
-  if (m <= lev) {
-    bkey[b] = key[i] >> (d * (L - lev));
-    if (first_pt) first_pt[b] = (int32_t)i;
-    if (bid_up) child_begin[b] = bid_up[i] - 1;
+  __syncthreads();
+  const bool valid = i < hi;
+  const uint64_t kk = valid ? key[i] : 0ull;
+  const int64_t li = i - ts;  // index within this tree's sorted points
+  int bid_prev = -1;
+  for (int l = 0; l <= L; ++l) {
+    const unsigned b = __ballot_sync(0xffffffffu, m <= l);
+    const int bid = base[l] + woff[warp][l] + __popc(b & le) - 1;  // box of point i at level l
+    if (m <= l) {  // point i opens box bid at level l (m <= L implies valid)
+      const uint64_t kl = (kk >> (d * (L - l))) & ((1ull << (d * l)) - 1ull);
+      T.key[l][bid] = kl;
+      if (l > 0) {
+        T.parent[l][bid] = bid_prev;
+        atomicOr(&T.child_mask[l - 1][bid_prev], 1u << (uint32_t)(kl & ((1u << d) - 1u)));
+        // the opener of the parent box also opens its first child
+        if (m <= l - 1) T.child_begin[l - 1][bid_prev] = bid;
+      }
+      if (l == L) T.first_pt[bid] = (int32_t)li;
+    }
+    bid_prev = bid;
   }
-  if (bid_up && m <= lev + 1) {
-    int32_t c = bid_up[i] - 1;
-    parent_up[c] = b;
-    uint32_t bits = (uint32_t)((key[i] >> (d * (L - lev - 1))) & ((1u << d) - 1));
-    atomicOr(&child_mask[b], 1u << bits);
-  }
+  if (!valid) return;
+  if (i == hi - 1 && (int)blockIdx.x == b_last) T.first_pt[bid_prev + 1] = (int32_t)(li + 1);
+  const int32_t j = idx[i] - (int32_t)ts;
+  T.perm[li] = j;
+  for (int a = 0; a < d; ++a) T.pts_sorted[li * d + a] = T.pts[(int64_t)j * d + a];
 }
-
-__global__ void k_gather_pts(const double* __restrict__ pts, const int32_t* __restrict__ perm, int64_t n, int d,
-                             double* __restrict__ out) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  int64_t j = perm[i];
-  for (int a = 0; a < d; ++a) out[i * d + a] = pts[j * d + a];
-}
-
-__global__ void k_set_i32(int32_t* p, int32_t v) { *p = v; }
 
 static inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
-#define CK(x)                                                   \
-  do {                                                          \
-    cudaError_t e_ = (x);                                       \
-    if (e_ != cudaSuccess) {                                    \
-      if (err) *err = std::string(#x) + ": " + cudaGetErrorString(e_); \
-      return SFT_E_CUDA;                                        \
-    }                                                           \
+#define CK(x)                                                            \
+  do {                                                                   \
+    cudaError_t e_ = (x);                                                \
+    if (e_ != cudaSuccess) {                                             \
+      if (err) *err = std::string(#x) + ": " + cudaGetErrorString(e_);   \
+      return SFT_E_CUDA;                                                 \
+    }                                                                    \
   } while (0)
 
-template <class T>
-static cudaError_t dalloc(T** p, size_t n, cudaStream_t s) {
-  return cudaMallocAsync((void**)p, (n > 0 ? n : 1) * sizeof(T), s);
-}
+static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
-struct Scratch {
-  uint64_t* keys_in = nullptr;
-  int32_t* idx_in = nullptr;
-  uint8_t* ml = nullptr;
-  int32_t* bidA = nullptr;
-  int32_t* bidB = nullptr;
-  unsigned long long* hist = nullptr;
-  void* cub_tmp = nullptr;
-  size_t cub_bytes = 0;
-};
-
-static int tree_phase1(sft_plan_s* P, Tree& T, const double* pts, int64_t n, Scratch& S, std::string* err) {
-  cudaStream_t s = P->stream;
-  const int d = P->d, L = P->L;
-  T.d = d;
-  T.L = L;
-  T.npts = n;
-  CK(dalloc(&S.keys_in, n, s));
-  CK(dalloc(&S.idx_in, n, s));
-  CK(dalloc(&T.keys_sorted, n, s));
-  CK(dalloc(&T.perm, n, s));
-  CK(dalloc(&S.ml, n, s));
-  CK(dalloc(&S.hist, L + 1, s));
-  CK(cudaMemsetAsync(S.hist, 0, (L + 1) * sizeof(unsigned long long), s));
-  k_leaf_keys<<<nblk(n, 256), 256, 0, s>>>(pts, n, d, L, (double)P->N, P->N, S.keys_in, S.idx_in, P->d_err);
-  count_launch();
-  CK(cudaGetLastError());
-  size_t need = 0;
-  CK(cub::DeviceRadixSort::SortPairs(nullptr, need, S.keys_in, T.keys_sorted, S.idx_in, T.perm, (int)n, 0, d * L, s));
-  size_t need2 = 0;
-  CK(cub::DeviceScan::InclusiveSum(nullptr, need2, (int32_t*)nullptr, (int32_t*)nullptr, (int)n, s));
-  S.cub_bytes = need > need2 ? need : need2;
-  CK(cudaMallocAsync(&S.cub_tmp, S.cub_bytes > 0 ? S.cub_bytes : 1, s));
-  CK(cub::DeviceRadixSort::SortPairs(S.cub_tmp, need, S.keys_in, T.keys_sorted, S.idx_in, T.perm, (int)n, 0, d * L,
-                                     s));
-  k_min_level<<<nblk(n, 256), 256, 0, s>>>(T.keys_sorted, n, d, L, S.ml, S.hist);
-  count_launch();
-  CK(cudaGetLastError());
-  return SFT_OK;
-}
-
-static int tree_phase2(sft_plan_s* P, Tree& T, const double* pts, const std::vector<int64_t>& hist, Scratch& S,
-                       std::string* err) {
-  cudaStream_t s = P->stream;
-  const int d = P->d, L = P->L;
-  const int64_t n = T.npts;
-  T.lev.assign(L + 1, TreeLevel());
-  T.counts.assign(L + 1, 0);
-  int64_t acc = 0;
-  for (int l = 0; l <= L; ++l) {
-    acc += hist[l];
-    T.counts[l] = acc;
-    T.lev[l].n = acc;
-  }
-  for (int l = 0; l <= L; ++l) {
-    TreeLevel& lv = T.lev[l];
-    CK(dalloc(&lv.key, lv.n, s));
-    if (l < L) {
-      CK(dalloc(&lv.child_begin, lv.n, s));
-      CK(dalloc(&lv.child_mask, lv.n, s));
-      CK(cudaMemsetAsync(lv.child_mask, 0, lv.n * sizeof(uint32_t), s));
-    }
-    if (l > 0) CK(dalloc(&lv.parent, lv.n, s));
-  }
-  CK(dalloc(&T.first_pt, T.lev[L].n + 1, s));
-  CK(dalloc(&T.pts_sorted, n * d, s));
-  CK(dalloc(&S.bidA, n, s));
-  CK(dalloc(&S.bidB, n, s));
-  int32_t* bid_up = nullptr;
-  int32_t* bufs[2] = {S.bidA, S.bidB};
-  for (int l = L; l >= 0; --l) {
-    int32_t* bid = bufs[l & 1];
-    k_flags<<<nblk(n, 256), 256, 0, s>>>(S.ml, n, l, bid);
-    count_launch();
-    CK(cudaGetLastError());
-    size_t nb = S.cub_bytes;
-    CK(cub::DeviceScan::InclusiveSum(S.cub_tmp, nb, bid, bid, (int)n, s));
-    TreeLevel& lv = T.lev[l];
-    k_fill_level<<<nblk(n, 256), 256, 0, s>>>(T.keys_sorted, S.ml, n, d, L, l, bid, bid_up, lv.key, lv.child_begin,
-                                              lv.child_mask, l < L ? T.lev[l + 1].parent : nullptr,
-                                              l == L ? T.first_pt : nullptr);
-    count_launch();
-    CK(cudaGetLastError());
-    bid_up = bid;
-  }
-  k_set_i32<<<1, 1, 0, s>>>(T.first_pt + T.lev[L].n, (int32_t)n);
-  k_gather_pts<<<nblk(n, 256), 256, 0, s>>>(pts, T.perm, n, d, T.pts_sorted);
-  count_launch(2);
-  CK(cudaGetLastError());
-  CK(cudaFreeAsync(S.keys_in, s));
-  CK(cudaFreeAsync(S.idx_in, s));
-  CK(cudaFreeAsync(S.ml, s));
-  CK(cudaFreeAsync(S.hist, s));
-  CK(cudaFreeAsync(S.bidA, s));
-  CK(cudaFreeAsync(S.bidB, s));
-  CK(cudaFreeAsync(S.cub_tmp, s));
-  return SFT_OK;
+// upper bound on the non-empty boxes of a tree with n points at level l
+static int64_t level_cap(int64_t n, int d, int l) {
+  if (d * l >= 40) return n;
+  return std::min<int64_t>(n, int64_t(1) << (d * l));
 }
 
 int build_trees(sft_plan_s* P, const double* x_dev, const double* k_dev, std::string* err) {
-  Scratch SX, SK;
-  int rc = tree_phase1(P, P->X, x_dev, P->nx, SX, err);
-  if (rc) return rc;
-  rc = tree_phase1(P, P->K, k_dev, P->nk, SK, err);
-  if (rc) return rc;
-  // one host sync for both trees: level histograms + domain error flag
-  const int L = P->L;
-  std::vector<unsigned long long> h(2 * (L + 1) + 1);
-  CK(cudaMemcpyAsync(h.data(), SX.hist, (L + 1) * sizeof(unsigned long long), cudaMemcpyDeviceToHost, P->stream));
-  CK(cudaMemcpyAsync(h.data() + L + 1, SK.hist, (L + 1) * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
-                     P->stream));
+  cudaStream_t s = P->stream;
+  const int d = P->d, L = P->L;
+  const int64_t nx = P->nx, nk = P->nk, n = nx + nk;
+  if (L + 1 > kMaxLevels) {
+    if (err) *err = "tree depth exceeds kMaxLevels";
+    return SFT_E_ARG;
+  }
+  Tree* trees[2] = {&P->X, &P->K};
+  const int64_t npt[2] = {nx, nk};
+  const double* src[2] = {x_dev, k_dev};
+
+  // ---- persistent arena: level arrays (upper bounds) + sorted points ----
+  size_t off = 0;
+  std::vector<size_t> o_key[2], o_cb[2], o_cm[2], o_par[2];
+  size_t o_first[2], o_perm[2], o_pts[2], o_tot[2];
+  size_t cm_lo = 0, cm_hi = 0;
+  for (int t = 0; t < 2; ++t) {
+    o_key[t].resize(L + 1);
+    o_par[t].resize(L + 1);
+    for (int l = 0; l <= L; ++l) {
+      o_key[t][l] = off;
+      off = align_up(off + 8 * level_cap(npt[t], d, l), 256);
+      o_par[t][l] = off;
+      off = align_up(off + 4 * level_cap(npt[t], d, l), 256);
+    }
+  }
+  // child masks of both trees contiguous (one memset)
+  cm_lo = off;
+  for (int t = 0; t < 2; ++t) {
+    o_cm[t].resize(L + 1);
+    for (int l = 0; l <= L; ++l) {
+      o_cm[t][l] = off;
+      off = align_up(off + 4 * level_cap(npt[t], d, l), 256);
+    }
+  }
+  cm_hi = off;
+  for (int t = 0; t < 2; ++t) {
+    o_cb[t].resize(L + 1);
+    for (int l = 0; l <= L; ++l) {
+      o_cb[t][l] = off;
+      off = align_up(off + 4 * level_cap(npt[t], d, l), 256);
+    }
+    o_first[t] = off;
+    off = align_up(off + 4 * (level_cap(npt[t], d, L) + 1), 256);
+    o_perm[t] = off;
+    off = align_up(off + 4 * npt[t], 256);
+    o_pts[t] = off;
+    off = align_up(off + 8 * d * npt[t], 256);
+    o_tot[t] = off;
+    off = align_up(off + 8 * (L + 1), 256);
+  }
+  char* arena = nullptr;
+  CK(cudaMallocAsync((void**)&arena, off, s));
+  P->X.arena = arena;
+  P->K.arena = nullptr;
+  CK(cudaMemsetAsync(arena + cm_lo, 0, cm_hi - cm_lo, s));
+
+  // ---- scratch ----
+  const int nbx = (int)nblk(nx, kBlk), nbk = (int)nblk(nk, kBlk);
+  size_t cub_bytes = 0;
+  CK(cub::DeviceRadixSort::SortPairs(nullptr, cub_bytes, (uint64_t*)nullptr, (uint64_t*)nullptr, (int32_t*)nullptr,
+                                     (int32_t*)nullptr, (int)n, 0, d * L + 1, s));
+  size_t so = 0;
+  const size_t s_kin = so;
+  so = align_up(so + 8 * n, 256);
+  const size_t s_kout = so;
+  so = align_up(so + 8 * n, 256);
+  const size_t s_iin = so;
+  so = align_up(so + 4 * n, 256);
+  const size_t s_iout = so;
+  so = align_up(so + 4 * n, 256);
+  const size_t s_ml = so;
+  so = align_up(so + n, 256);
+  const size_t s_cnt = so;
+  so = align_up(so + 4 * (size_t)(nbx + nbk) * (L + 1), 256);
+  const size_t s_cub = so;
+  so = align_up(so + cub_bytes, 256);
+  char* scr = nullptr;
+  CK(cudaMallocAsync((void**)&scr, so, s));
+  uint64_t* keys_in = (uint64_t*)(scr + s_kin);
+  uint64_t* keys_out = (uint64_t*)(scr + s_kout);
+  int32_t* idx_in = (int32_t*)(scr + s_iin);
+  int32_t* idx_out = (int32_t*)(scr + s_iout);
+  uint8_t* ml = (uint8_t*)(scr + s_ml);
+  int32_t* counts = (int32_t*)(scr + s_cnt);
+
+  k_leaf_keys<<<nblk(n, 256), 256, 0, s>>>(x_dev, nx, k_dev, nk, d, L, (double)P->N, P->N, keys_in, idx_in, P->d_err);
+  count_launch();
+  CK(cudaGetLastError());
+  CK(cub::DeviceRadixSort::SortPairs(scr + s_cub, cub_bytes, keys_in, keys_out, idx_in, idx_out, (int)n, 0, d * L + 1,
+                                     s));
+  BlockMap bm{nx, n, nbx};
+  k_count<<<nbx + nbk, kBlk, 0, s>>>(keys_out, bm, d, L, ml, counts);
+  count_launch();
+  CK(cudaGetLastError());
+
+  FillArgs fa;
+  fa.bm = bm;
+  fa.nbk = nbk;
+  for (int t = 0; t < 2; ++t) {
+    TreeOut& o = fa.t[t];
+    for (int l = 0; l < kMaxLevels; ++l) {
+      const bool ok = l <= L;
+      o.key[l] = ok ? (uint64_t*)(arena + o_key[t][l]) : nullptr;
+      o.parent[l] = ok ? (int32_t*)(arena + o_par[t][l]) : nullptr;
+      o.child_mask[l] = ok ? (uint32_t*)(arena + o_cm[t][l]) : nullptr;
+      o.child_begin[l] = ok ? (int32_t*)(arena + o_cb[t][l]) : nullptr;
+    }
+    o.first_pt = (int32_t*)(arena + o_first[t]);
+    o.perm = (int32_t*)(arena + o_perm[t]);
+    o.pts_sorted = (double*)(arena + o_pts[t]);
+    o.pts = src[t];
+    o.totals = (int64_t*)(arena + o_tot[t]);
+  }
+  k_fill<<<nbx + nbk, kBlk, 0, s>>>(keys_out, idx_out, ml, counts, fa, d, L);
+  count_launch();
+  CK(cudaGetLastError());
+
+  // ---- the one host sync: exact box counts + domain error flag ----
+  std::vector<int64_t> h(2 * (L + 1));
+  CK(cudaMemcpyAsync(h.data(), arena + o_tot[0], (L + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(h.data() + L + 1, arena + o_tot[1], (L + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   int herr = 0;
-  CK(cudaMemcpyAsync(&herr, P->d_err, sizeof(int), cudaMemcpyDeviceToHost, P->stream));
-  CK(cudaStreamSynchronize(P->stream));
+  CK(cudaMemcpyAsync(&herr, P->d_err, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaFreeAsync(scr, s));
+  CK(cudaStreamSynchronize(s));
   if (herr) {
     if (err) *err = "a coordinate is non-finite or outside [0,N]";
-    // release scratch before failing
-    cudaFreeAsync(SX.keys_in, P->stream); cudaFreeAsync(SX.idx_in, P->stream); cudaFreeAsync(SX.ml, P->stream);
-    cudaFreeAsync(SX.hist, P->stream); cudaFreeAsync(SX.cub_tmp, P->stream);
-    cudaFreeAsync(SK.keys_in, P->stream); cudaFreeAsync(SK.idx_in, P->stream); cudaFreeAsync(SK.ml, P->stream);
-    cudaFreeAsync(SK.hist, P->stream); cudaFreeAsync(SK.cub_tmp, P->stream);
     return SFT_E_DOMAIN;
   }
-  std::vector<int64_t> hx(L + 1), hk(L + 1);
-  for (int l = 0; l <= L; ++l) {
-    hx[l] = (int64_t)h[l];
-    hk[l] = (int64_t)h[L + 1 + l];
+  for (int t = 0; t < 2; ++t) {
+    Tree& T = *trees[t];
+    T.d = d;
+    T.L = L;
+    T.npts = npt[t];
+    T.lev.assign(L + 1, TreeLevel());
+    T.counts.assign(L + 1, 0);
+    for (int l = 0; l <= L; ++l) {
+      TreeLevel& lv = T.lev[l];
+      lv.n = T.counts[l] = h[t * (L + 1) + l];
+      lv.key = fa.t[t].key[l];
+      lv.parent = l > 0 ? fa.t[t].parent[l] : nullptr;
+      lv.child_mask = l < L ? fa.t[t].child_mask[l] : nullptr;
+      lv.child_begin = l < L ? fa.t[t].child_begin[l] : nullptr;
+    }
+    T.first_pt = fa.t[t].first_pt;
+    T.perm = fa.t[t].perm;
+    T.pts_sorted = fa.t[t].pts_sorted;
   }
-  rc = tree_phase2(P, P->X, x_dev, hx, SX, err);
-  if (rc) return rc;
-  return tree_phase2(P, P->K, k_dev, hk, SK, err);
+  return SFT_OK;
 }
 
 void free_tree(Tree& T, cudaStream_t s) {
-  for (auto& lv : T.lev) {
-    if (lv.key) cudaFreeAsync(lv.key, s);
-    if (lv.child_begin) cudaFreeAsync(lv.child_begin, s);
-    if (lv.child_mask) cudaFreeAsync(lv.child_mask, s);
-    if (lv.parent) cudaFreeAsync(lv.parent, s);
-  }
+  if (T.arena) cudaFreeAsync(T.arena, s);
+  T.arena = nullptr;
   T.lev.clear();
-  if (T.first_pt) cudaFreeAsync(T.first_pt, s);
-  if (T.perm) cudaFreeAsync(T.perm, s);
-  if (T.pts_sorted) cudaFreeAsync(T.pts_sorted, s);
-  if (T.keys_sorted) cudaFreeAsync(T.keys_sorted, s);
   T.first_pt = nullptr;
   T.perm = nullptr;
   T.pts_sorted = nullptr;
-  T.keys_sorted = nullptr;
 }
 
 }  // namespace sft
