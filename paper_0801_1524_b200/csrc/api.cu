@@ -256,6 +256,74 @@ extern "C" int sft_choose_partition(int L, int world, const int64_t* counts_x, c
   return SFT_OK;
 }
 
+static LevelDims level_dims(const sft_plan_s* P, int t) {
+  const int L = P->L;
+  LevelDims ld;
+  ld.t = t;
+  ld.cbK = P->K.lev[t].child_begin;
+  ld.mK = P->K.lev[t].child_mask;
+  ld.cbX = P->X.lev[L - t - 1].child_begin;
+  ld.mX = P->X.lev[L - t - 1].child_mask;
+  ld.seg = nullptr;
+  ld.nseg = 0;
+  return ld;
+}
+
+// Phase-1 style level (B restricted to this rank's T_K range, all A).
+static LevelDims level_dims_k(const sft_plan_s* P, int t) {
+  const int L = P->L;
+  LevelDims ld = level_dims(P, t);
+  ld.b_lo = P->k_rng[t].lo;
+  ld.b_hi = P->k_rng[t].hi;
+  ld.ap_lo = 0;
+  ld.ap_hi = P->X.counts[L - t - 1];
+  ld.in_b0 = P->k_rng[t + 1].lo;
+  ld.in_nA = P->X.counts[L - t - 1];
+  ld.in_a0 = 0;
+  ld.out_b0 = P->k_rng[t].lo;
+  ld.out_nA = P->X.counts[L - t];
+  ld.out_a0 = 0;
+  return ld;
+}
+
+// Phase-2 style level (all B, A restricted to this rank's T_X range).
+static LevelDims level_dims_x(const sft_plan_s* P, int t) {
+  const int L = P->L;
+  LevelDims ld = level_dims(P, t);
+  ld.b_lo = 0;
+  ld.b_hi = P->K.counts[t];
+  ld.ap_lo = P->x_rng[L - t - 1].lo;
+  ld.ap_hi = P->x_rng[L - t - 1].hi;
+  ld.in_b0 = 0;
+  ld.in_nA = P->x_rng[L - t - 1].hi - P->x_rng[L - t - 1].lo;
+  ld.in_a0 = P->x_rng[L - t - 1].lo;
+  ld.out_b0 = 0;
+  ld.out_nA = P->x_rng[L - t].hi - P->x_rng[L - t].lo;
+  ld.out_a0 = P->x_rng[L - t].lo;
+  return ld;
+}
+
+// The dims of level t exactly as the apply calls use them (sft_apply, or the
+// two phases of a multi-rank plan, with the exchange layout at level m).
+static LevelDims apply_dims(const sft_plan_s* P, int t) {
+  if (P->world == 1) return level_dims_k(P, t);
+  if (t >= P->part.m) {
+    LevelDims ld = level_dims_k(P, t);
+    if (t == P->part.m) {
+      ld.seg = P->d_seg;
+      ld.nseg = P->world;
+    }
+    return ld;
+  }
+  return level_dims_x(P, t);
+}
+
+static LevelDims apply_dims_sched(const sft_plan_s* P, int t) {
+  LevelDims ld = apply_dims(P, t);
+  ld.sched = P->sched ? P->sched + P->sched_off[t] : nullptr;
+  return ld;
+}
+
 // ---------------------------------------------------------------------------
 // plan
 // ---------------------------------------------------------------------------
@@ -270,6 +338,7 @@ static void plan_free(sft_plan_s* P) {
   if (P->u_stage) cudaFreeAsync(P->u_stage, s);
   if (P->d_err) cudaFreeAsync(P->d_err, s);
   if (P->d_seg) cudaFreeAsync(P->d_seg, s);
+  if (P->sched) cudaFreeAsync(P->sched, s);
   for (int i = 0; i < P->ev_created; ++i) cudaEventDestroy(P->ev[i]);
   // no sync: the frees above are stream-ordered behind any pending work
   delete P;
@@ -420,6 +489,22 @@ extern "C" int sft_plan(int dim, int64_t N, int p, const double* x, int64_t nx, 
   for (int i = 0; i < 2; ++i)
     if (cudaMallocAsync(&P->buf[i], P->buf_elems * sizeof(double2), s) != cudaSuccess)
       return bail(SFT_E_NOMEM, "level buffer allocation failed");
+  // tile schedules of every translation level (kernel-side task lists)
+  {
+    P->sched_off.assign(L + 1, 0);
+    size_t tot = 0;
+    for (int t = 0; t < L; ++t) {
+      P->sched_off[t] = tot;
+      tot += (schedule_bytes(P, apply_dims(P, t)) + 255) / 256 * 256;
+    }
+    if (tot > 0) {
+      if (cudaMallocAsync(&P->sched, tot, s) != cudaSuccess) return bail(SFT_E_NOMEM, "schedule allocation failed");
+      for (int t = 0; t < L; ++t) {
+        cudaError_t ce = launch_schedule(P, apply_dims(P, t), P->sched + P->sched_off[t]);
+        if (ce != cudaSuccess) return bail(SFT_E_CUDA, std::string("schedule: ") + cudaGetErrorString(ce));
+      }
+    }
+  }
   cudaEventRecord(e1, s);
   if (cudaEventSynchronize(e1) != cudaSuccess) return bail(SFT_E_CUDA, "plan sync failed");
   float ms = 0;
@@ -447,53 +532,6 @@ extern "C" int sft_destroy(sft_plan_t plan) {
 static void tmark(sft_plan_s* P) {
   if (!P->timing) return;
   if (P->n_ev < 64) cudaEventRecord(P->ev[P->n_ev++], P->stream);
-}
-
-static LevelDims level_dims(const sft_plan_s* P, int t) {
-  const int L = P->L;
-  LevelDims ld;
-  ld.t = t;
-  ld.cbK = P->K.lev[t].child_begin;
-  ld.mK = P->K.lev[t].child_mask;
-  ld.cbX = P->X.lev[L - t - 1].child_begin;
-  ld.mX = P->X.lev[L - t - 1].child_mask;
-  ld.seg = nullptr;
-  ld.nseg = 0;
-  return ld;
-}
-
-// Phase-1 style level (B restricted to this rank's T_K range, all A).
-static LevelDims level_dims_k(const sft_plan_s* P, int t) {
-  const int L = P->L;
-  LevelDims ld = level_dims(P, t);
-  ld.b_lo = P->k_rng[t].lo;
-  ld.b_hi = P->k_rng[t].hi;
-  ld.ap_lo = 0;
-  ld.ap_hi = P->X.counts[L - t - 1];
-  ld.in_b0 = P->k_rng[t + 1].lo;
-  ld.in_nA = P->X.counts[L - t - 1];
-  ld.in_a0 = 0;
-  ld.out_b0 = P->k_rng[t].lo;
-  ld.out_nA = P->X.counts[L - t];
-  ld.out_a0 = 0;
-  return ld;
-}
-
-// Phase-2 style level (all B, A restricted to this rank's T_X range).
-static LevelDims level_dims_x(const sft_plan_s* P, int t) {
-  const int L = P->L;
-  LevelDims ld = level_dims(P, t);
-  ld.b_lo = 0;
-  ld.b_hi = P->K.counts[t];
-  ld.ap_lo = P->x_rng[L - t - 1].lo;
-  ld.ap_hi = P->x_rng[L - t - 1].hi;
-  ld.in_b0 = 0;
-  ld.in_nA = P->x_rng[L - t - 1].hi - P->x_rng[L - t - 1].lo;
-  ld.in_a0 = P->x_rng[L - t - 1].lo;
-  ld.out_b0 = 0;
-  ld.out_nA = P->x_rng[L - t].hi - P->x_rng[L - t].lo;
-  ld.out_a0 = P->x_rng[L - t].lo;
-  return ld;
 }
 
 static int finish_timing(sft_plan_s* P, int n_levels_first) {
@@ -548,7 +586,7 @@ extern "C" int sft_apply(sft_plan_t P, const void* f, void* u) {
   tmark(P);
   // step 3: t = L-1 .. 0
   for (int t = L - 1; t >= 0; --t) {
-    LevelDims ld = level_dims_k(P, t);
+    LevelDims ld = apply_dims_sched(P, t);
     CKR(launch_translate(P, ld, P->buf[(t + 1) & 1], P->buf[t & 1]));
     tmark(P);
   }
@@ -613,13 +651,8 @@ extern "C" int sft_apply_phase1(sft_plan_t P, const void* f, void* sendbuf) {
   }
   CKR(launch_leaf(P, fd, P->buf[L & 1], kl.lo, kl.hi));
   for (int t = L - 1; t >= m; --t) {
-    LevelDims ld = level_dims_k(P, t);
-    double2* out = P->buf[t & 1];
-    if (t == m) {
-      ld.seg = P->d_seg;
-      ld.nseg = P->world;
-      out = sb;
-    }
+    LevelDims ld = apply_dims_sched(P, t);
+    double2* out = t == m ? sb : P->buf[t & 1];
     CKR(launch_translate(P, ld, P->buf[(t + 1) & 1], out));
   }
   return SFT_OK;
@@ -640,7 +673,7 @@ extern "C" int sft_apply_phase2(sft_plan_t P, const void* recvbuf, void* u) {
   CKR(launch_zero(ud, P->nx, s));
   const double2* in = (const double2*)recvbuf;
   for (int t = m - 1; t >= 0; --t) {
-    LevelDims ld = level_dims_x(P, t);
+    LevelDims ld = apply_dims_sched(P, t);
     double2* out = P->buf[t & 1];
     CKR(launch_translate(P, ld, in, out));
     in = out;

@@ -90,6 +90,9 @@ struct sft_plan_s {
   std::vector<sft::LevelRange> x_rng;  // [L+1] this rank's T_X range per level (phase 2)
   std::vector<int64_t> send_counts, recv_counts;  // [world] complex elements
   int64_t* d_seg = nullptr;  // device [2*world+1]: a-boundaries at level L-m, send segment bases
+  // tile schedules of the translation levels (one allocation; offsets per level t)
+  unsigned char* sched = nullptr;
+  std::vector<size_t> sched_off;
   // timing
   bool timing = false;
   cudaEvent_t ev[64];
@@ -120,12 +123,36 @@ struct LevelDims {
   int64_t out_b0, out_nA, out_a0; // output layout: [(iB - out_b0) * out_nA + (iA - out_a0)]
   const int64_t* seg;  // exchange mapping (nullptr = plain layout), see api.cu
   int nseg;
+  const unsigned char* sched = nullptr;  // tile schedule of this level (translate.cu, built by sft_plan)
 };
 
 cudaError_t launch_leaf(const sft_plan_s* P, const double2* f, double2* out, int64_t b_lo, int64_t b_hi);
 cudaError_t launch_translate(const sft_plan_s* P, const LevelDims& L, const double2* in, double2* out);
+// tile schedule of one level (sizes and builder; 0 bytes when the kernel needs none)
+size_t schedule_bytes(const sft_plan_s* P, const LevelDims& L);
+cudaError_t launch_schedule(const sft_plan_s* P, const LevelDims& L, unsigned char* dst);
 cudaError_t launch_final(const sft_plan_s* P, const double2* g0, double2* u, int64_t a_lo, int64_t a_hi);
 cudaError_t launch_zero(double2* p, int64_t n, cudaStream_t s);
+
+template <int B, int E>
+struct Pow {
+  static constexpr int v = B * Pow<B, E - 1>::v;
+};
+template <int B>
+struct Pow<B, 0> {
+  static constexpr int v = 1;
+};
+
+#define SFT_DISPATCH(D_, P_, CALL)                                       \
+  do {                                                                   \
+    if (D_ == 2 && P_ == 5) { constexpr int D = 2, P = 5; CALL; }        \
+    else if (D_ == 2 && P_ == 7) { constexpr int D = 2, P = 7; CALL; }   \
+    else if (D_ == 2 && P_ == 9) { constexpr int D = 2, P = 9; CALL; }   \
+    else if (D_ == 3 && P_ == 5) { constexpr int D = 3, P = 5; CALL; }   \
+    else if (D_ == 3 && P_ == 7) { constexpr int D = 3, P = 7; CALL; }   \
+    else if (D_ == 3 && P_ == 9) { constexpr int D = 3, P = 9; CALL; }   \
+    else return cudaErrorInvalidValue;                                   \
+  } while (0)
 
 // number of kernels this library has launched (own kernels; CUB's internal
 // sort/scan kernels are not counted), for bench.py's gpu_launches

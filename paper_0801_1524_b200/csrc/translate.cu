@@ -1,0 +1,1120 @@
+// translate.cu -- step 3 of the butterfly (fig. 1 and eq. E1,
+// P:231-286): for every level t = L-1 .. 0 and every group (A', B) with B at
+// level t of T_K and A' at level L-t-1 of T_X, the charges of the pairs
+// (A, B), A a child of A', from the charges of the pairs (A', B_c):
+//
+//   h^{AB} = sum_{present B_c} (x)_ax T[alpha_ax][beta_ax] h^{A' B_c},
+//   T[a][b] = c_ab (RC_b + i (2a-1) RS_b)   (h-representation)
+//
+// sum-factorised axis by axis: pass AX combines the two children that differ
+// in the bit of axis AX and produces both alpha outputs of that axis at once.
+// Per fiber (p complex values along axis AX) and child pair (x_0, x_1):
+//
+//   z_0 = P - iQ,  z_1 = P + iQ,   P = RC_0 x_0 + RS_1 x_1,  Q = RS_0 x_0 - RC_1 x_1.
+//
+// Default kernel, k_translate_ws (SFT_TRANSLATE unset or "ws"): a persistent,
+// warp-specialised CTA.  The producer warp runs up to NST tiles ahead: for a
+// tile of G groups it loads the group metadata, builds per-pass row
+// descriptors (one per fiber task: shared-memory position, live children,
+// HBM output offsets) and issues 1-D TMA bulk copies of the child arrays into
+// a shared-memory stage (mbarrier complete_tx).  NC consumer warps run the
+// passes in place in the stage on the FP64 tensor cores: the contraction is a
+// real GEMM [fiber rows] x [K = 2p stacked child elements] x [N = (P_m, Q_m)
+// interleaved] with mma.sync.m8n8k4.f64 (DMMA -- tcgen05 has no f64 kind);
+// the real and imaginary parts of 8 fibers form two A tiles sharing the
+// register-resident B fragments, so each lane ends with re and im of (P_m,
+// Q_m) and forms z_0, z_1 locally.  K is padded to a multiple of 4 (p=9: 18
+// -> 20); the last m of p = 5, 9 runs on DFMA with a 4-lane transpose-reduce
+// (N padding avoided: p=9 waste 1.11x instead of 1.78x).  One named barrier
+// between passes; the last pass stores straight to HBM.
+//
+// k_translate_fma (SFT_TRANSLATE=fma): one thread per fiber on DFMA with
+// constant-bank operands (round-1 design, kept for ablation).
+//
+// No floating-point atomics: bitwise reproducible, identical for any world
+// size.
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <vector>
+
+#include "sft_internal.cuh"
+
+namespace sft {
+
+// ------------------------------------------------------------------------
+// constant-bank operators for the FMA kernel (uploaded once per device and p)
+// ------------------------------------------------------------------------
+__constant__ double c_RC5[2][5][5], c_RS5[2][5][5];
+__constant__ double c_RC7[2][7][7], c_RS7[2][7][7];
+__constant__ double c_RC9[2][9][9], c_RS9[2][9][9];
+
+template <int P>
+struct CT;
+template <>
+struct CT<5> {
+  __device__ __forceinline__ static double rc(int b, int m, int l) { return c_RC5[b][m][l]; }
+  __device__ __forceinline__ static double rs(int b, int m, int l) { return c_RS5[b][m][l]; }
+};
+template <>
+struct CT<7> {
+  __device__ __forceinline__ static double rc(int b, int m, int l) { return c_RC7[b][m][l]; }
+  __device__ __forceinline__ static double rs(int b, int m, int l) { return c_RS7[b][m][l]; }
+};
+template <>
+struct CT<9> {
+  __device__ __forceinline__ static double rc(int b, int m, int l) { return c_RC9[b][m][l]; }
+  __device__ __forceinline__ static double rs(int b, int m, int l) { return c_RS9[b][m][l]; }
+};
+
+cudaError_t upload_const_tables(int p, const double* RC, const double* RS, const double* /*invD*/) {
+  const size_t n2 = sizeof(double) * 2 * p * p;
+  cudaError_t e = cudaErrorInvalidValue;
+  if (p == 5) {
+    if ((e = cudaMemcpyToSymbol(c_RC5, RC, n2)) != cudaSuccess) return e;
+    e = cudaMemcpyToSymbol(c_RS5, RS, n2);
+  } else if (p == 7) {
+    if ((e = cudaMemcpyToSymbol(c_RC7, RC, n2)) != cudaSuccess) return e;
+    e = cudaMemcpyToSymbol(c_RS7, RS, n2);
+  } else if (p == 9) {
+    if ((e = cudaMemcpyToSymbol(c_RC9, RC, n2)) != cudaSuccess) return e;
+    e = cudaMemcpyToSymbol(c_RS9, RS, n2);
+  }
+  return e;
+}
+
+// ------------------------------------------------------------------------
+// shared pieces: arguments, group metadata, TMA tile prologue, task lists
+// ------------------------------------------------------------------------
+struct TransArgs {
+  const double2* in;
+  double2* out;
+  const int32_t* cbK;
+  const uint32_t* mK;
+  const int32_t* cbX;
+  const uint32_t* mX;
+  int64_t b_lo, nAp_grp, ap_lo, ngroups;
+  int64_t in_b0, in_nA, in_a0;
+  int64_t out_b0, out_nA, out_a0;
+  const int64_t* seg;  // [nseg+1] A boundaries at the output level, then [nseg] segment bases
+  int nseg;
+};
+
+struct GroupMeta {
+  int64_t iB, iAp;
+  int32_t cbK, cbX;
+  uint32_t mB, mA;
+};
+
+struct TaskEntry {
+  uint8_t j, bp, as, cls;
+};
+
+// projections of a child mask: set of top-k-bit prefixes / low-k-bit suffixes
+template <int D>
+__device__ __forceinline__ uint32_t proj_hi(uint32_t m, int k) {
+  uint32_t r = 0;
+#pragma unroll
+  for (int c = 0; c < (1 << D); ++c)
+    if (m >> c & 1) r |= 1u << (c >> (D - k));
+  return r;
+}
+template <int D>
+__device__ __forceinline__ uint32_t proj_lo(uint32_t m, int k) {
+  uint32_t r = 0;
+#pragma unroll
+  for (int c = 0; c < (1 << D); ++c)
+    if (m >> c & 1) r |= 1u << (c & ((1 << k) - 1));
+  return r;
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  }
+}
+
+// Tile of G consecutive groups (B-major, A' fastest): group metadata into
+// shared memory, then one elected warp issues a 1-D TMA bulk copy of every
+// present child array (iB_c, iA') into slot c of its group, all completing on
+// one mbarrier.  Returns the number of groups in the tile.
+template <int D, int P, int G>
+__device__ __forceinline__ int tile_prologue(const TransArgs& a, double2* sb, GroupMeta* gm, uint64_t* bar) {
+  constexpr int PD = Pow<P, D>::v;
+  constexpr int NS = 1 << D;
+  static_assert(G <= 32, "one lane per group");
+  const int64_t g0 = (int64_t)blockIdx.x * G;
+  const int ng = (int)min((int64_t)G, a.ngroups - g0);
+  if (threadIdx.x < ng) {
+    const int64_t g = g0 + threadIdx.x;
+    GroupMeta m;
+    m.iB = a.b_lo + g / a.nAp_grp;
+    m.iAp = a.ap_lo + g % a.nAp_grp;
+    m.cbK = a.cbK[m.iB];
+    m.mB = a.mK[m.iB];
+    m.cbX = a.cbX[m.iAp];
+    m.mA = a.mX[m.iAp];
+    gm[threadIdx.x] = m;
+  }
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    uint32_t nbytes = lane < ng ? __popc(gm[lane].mB) * PD * (uint32_t)sizeof(double2) : 0u;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) nbytes += __shfl_xor_sync(0xffffffffu, nbytes, o);
+    if (lane == 0)
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(nbytes)
+                   : "memory");
+    __syncwarp();
+    if (lane < ng) {
+      const GroupMeta& m = gm[lane];
+      uint32_t mm = m.mB;
+      int r = 0;
+      while (mm) {
+        const int c = __ffs(mm) - 1;
+        mm &= mm - 1;
+        const int64_t iBc = (int64_t)m.cbK + r++;
+        const int64_t pin = (iBc - a.in_b0) * a.in_nA + (m.iAp - a.in_a0);
+#ifndef SFT_ABL_NOLOAD
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                smem_u32(sb + ((int64_t)lane * NS + c) * PD)),
+            "l"(a.in + pin * PD), "r"((uint32_t)(PD * sizeof(double2))), "r"(smem_u32(bar))
+            : "memory");
+#else  // ablation: no HBM reads, the transaction count is completed by hand
+        (void)pin;
+        asm volatile("mbarrier.complete_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)),
+                     "r"((uint32_t)(PD * sizeof(double2)))
+                     : "memory");
+#endif
+      }
+    }
+  }
+  return ng;
+}
+
+// Task list of pass AX: one entry per (group, beta-prefix bp, alpha-suffix as)
+// whose two input slots (bp,0,as), (bp,1,as) are live; cls bit 0/1 = the
+// slot with axis bit 0/1 holds data.  Entries are appended per class (both /
+// bit 0 only / bit 1 only) so that consecutive tasks share a class.
+template <int D, int G, int AX>
+__device__ __forceinline__ void build_tasks(const GroupMeta* gm, int ng, TaskEntry* ent, int* cnt) {
+  constexpr int MAXE = G << (D - 1);
+  if (threadIdx.x < 3) cnt[threadIdx.x] = 0;
+  __syncthreads();
+  if ((int)threadIdx.x < ng) {
+    const int j = threadIdx.x;
+    const uint32_t mB = gm[j].mB, mA = gm[j].mA;
+    const uint32_t PBp = AX > 0 ? proj_hi<D>(mB, AX) : 1u;
+    const uint32_t PAs = proj_lo<D>(mA, D - 1 - AX);
+    const uint32_t PBa = proj_hi<D>(mB, AX + 1);
+#pragma unroll
+    for (int bp = 0; bp < (1 << AX); ++bp) {
+      if (!(PBp >> bp & 1)) continue;
+      const int cls = (int)((PBa >> (bp << 1)) & 3u);
+      const int ci = cls == 3 ? 0 : (cls == 1 ? 1 : 2);
+#pragma unroll
+      for (int as = 0; as < (1 << (D - 1 - AX)); ++as) {
+        if (!(PAs >> as & 1)) continue;
+        const int pos = atomicAdd(&cnt[ci], 1);
+        ent[ci * MAXE + pos] = TaskEntry{(uint8_t)j, (uint8_t)bp, (uint8_t)as, (uint8_t)cls};
+      }
+    }
+  }
+  __syncthreads();
+}
+
+template <int MAXE>
+__device__ __forceinline__ TaskEntry task_at(const TaskEntry* ent, int ei, int n3, int n1) {
+  return ei < n3 ? ent[ei] : (ei < n3 + n1 ? ent[MAXE + ei - n3] : ent[2 * MAXE + ei - n3 - n1]);
+}
+
+// Index of the output pair (child alpha of A', B) in the level output for
+// the last pass, -1 if A' has no such child.
+__device__ __forceinline__ int64_t out_pair(const TransArgs& a, const GroupMeta& g, int alpha) {
+  if (!(g.mA >> alpha & 1)) return -1;
+  const int64_t iA = (int64_t)g.cbX + __popc(g.mA & ((1u << alpha) - 1));
+  if (a.nseg == 0) return (g.iB - a.out_b0) * a.out_nA + (iA - a.out_a0);
+  int q = 0;
+  while (q + 1 < a.nseg && iA >= a.seg[q + 1]) ++q;
+  const int64_t wq = a.seg[q + 1] - a.seg[q];
+  return a.seg[a.nseg + 1 + q] + (g.iB - a.out_b0) * wq + (iA - a.seg[q]);
+}
+
+// HBM address of the output pair (child alpha of A', B) for the last pass
+template <int PD>
+__device__ __forceinline__ double2* out_array(const TransArgs& a, const GroupMeta& g, int alpha) {
+  if (!(g.mA >> alpha & 1)) return nullptr;
+  const int64_t iA = (int64_t)g.cbX + __popc(g.mA & ((1u << alpha) - 1));
+  int64_t pidx;
+  if (a.nseg == 0) {
+    pidx = (g.iB - a.out_b0) * a.out_nA + (iA - a.out_a0);
+  } else {
+    int q = 0;
+    while (q + 1 < a.nseg && iA >= a.seg[q + 1]) ++q;
+    const int64_t wq = a.seg[q + 1] - a.seg[q];
+    pidx = a.seg[a.nseg + 1 + q] + (g.iB - a.out_b0) * wq + (iA - a.seg[q]);
+  }
+  return a.out + pidx * PD;
+}
+
+// ------------------------------------------------------------------------
+// DMMA kernel
+// ------------------------------------------------------------------------
+template <int P>
+struct MmaShape {
+  static constexpr int K = 2 * P;                 // stacked child elements
+  static constexpr int NK = (K + 3) / 4;          // k-steps of 4
+  static constexpr bool TAIL = (P % 4) == 1;      // m = P-1 by DFMA
+  static constexpr int NM = TAIL ? P - 1 : P;     // m's on the tensor cores
+  static constexpr int NT = (2 * NM + 7) / 8;     // N tiles of 8 (P_m, Q_m interleaved)
+  static constexpr int K0_HI = (P + 3) / 4;       // k-steps [0, K0_HI) hold child-0 elements
+  static constexpr int K1_LO = P / 4;             // k-steps [K1_LO, NK) hold child-1 elements
+  static constexpr int NFRAG = NK * NT * 32 + (TAIL ? NK * 2 * 32 : 0);  // doubles in the table
+};
+
+__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(d[0]), "+d"(d[1])
+      : "d"(a), "d"(b));
+}
+
+template <int P>
+struct LaneOps {
+  using S = MmaShape<P>;
+  double fb[S::NK][S::NT];           // B fragments of the operator
+  double ft[S::NK][2];               // tail column (m = P-1): P and Q weights of this lane's k
+  int lk[S::NK], bk[S::NK];          // element index l and child (2 = padding) of this lane's k
+};
+
+// k-steps [K_LO, K_HI) of one MMA super-tile: A fragments (re and im of one
+// complex element per lane, one 16-byte shared-memory load) times the B
+// fragments held in registers; tail column m = P-1 on DFMA.
+template <int P, int K_LO, int K_HI>
+__device__ __forceinline__ void mma_steps(const LaneOps<P>& op, const double2* __restrict__ x, const int (&off)[MmaShape<P>::NK],
+                                          bool p0, bool p1, double (&are)[MmaShape<P>::NT][2],
+                                          double (&aim)[MmaShape<P>::NT][2], double (&tl)[4]) {
+  using S = MmaShape<P>;
+#pragma unroll
+  for (int kk = K_LO; kk < K_HI; ++kk) {
+    const int b = op.bk[kk];
+    const bool live = b == 0 ? p0 : (b == 1 ? p1 : false);
+    const double2 av = live ? x[off[kk]] : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int n = 0; n < S::NT; ++n) {
+      dmma(are[n], av.x, op.fb[kk][n]);
+      dmma(aim[n], av.y, op.fb[kk][n]);
+    }
+    if (S::TAIL) {
+      tl[0] = fma(av.x, op.ft[kk][0], tl[0]);
+      tl[1] = fma(av.x, op.ft[kk][1], tl[1]);
+      tl[2] = fma(av.y, op.ft[kk][0], tl[2]);
+      tl[3] = fma(av.y, op.ft[kk][1], tl[3]);
+    }
+  }
+}
+
+// One axis pass of the DMMA kernel.  A warp takes super-tiles of 8 fiber
+// tasks: MMA row r (= lane/4) is one fiber, the real parts form one m8n8k4 A
+// tile and the imaginary parts a second one with the same B fragments, so a
+// lane ends up holding re and im of (P_m, Q_m) for its fiber and m = 4n +
+// lane%4 and forms z_0 = P - iQ, z_1 = P + iQ locally.  Rows 2q, 2q+1 take
+// fibers q, q+4 of the super-tile (conflict-free 16-byte shared loads for
+// the unit and p-strided fibers of p = 9).  Outputs go back in place, or to
+// HBM in the last pass.
+
+// ------------------------------------------------------------------------
+// Tile schedule (built once per plan by k_schedule, read by the producer)
+// ------------------------------------------------------------------------
+// Per tile of G consecutive groups (B-major, A' fastest) one block of BLK
+// bytes in HBM:
+//   cnt[3][3]  int32: per pass AX, task counts of class both / bit-0 only / bit-1 only
+//   grp[G]     {pin0, mB}: pair index of the first child array (iB_c, iA') in the
+//              level input, and the child mask of B (children r at pin0 + r*in_nA)
+//   task[D][MAXT] TaskRec, per pass packed in class order
+// A task = (group j, beta-prefix, alpha-suffix) of pass AX: the fibers of the
+// stage slots (bp,0,as) / (bp,1,as).
+struct __align__(16) TaskRec {
+  uint32_t x;    // stage offset (complex) of the slot with axis bit 0: (j*2^d + slot0)*p^d
+  uint32_t cls;  // bit 0 / bit 1: the slot with axis bit 0 / 1 holds data
+  uint32_t o0;   // last pass: output offset (complex) from a.out of child alpha-bit 0 of A'; ~0u = absent
+  uint32_t o1;   //            ... alpha-bit 1
+};
+
+template <int D, int P, int G>
+struct Sched {
+  static constexpr int MAXT = G << (D - 1);  // tasks per pass (max)
+  static constexpr int HDR = 48;
+  static constexpr int GRP = (8 * G + 15) / 16 * 16;
+  static constexpr int BLK = HDR + GRP + D * MAXT * (int)sizeof(TaskRec);
+  __device__ __forceinline__ static const int* cnt(const unsigned char* b) { return reinterpret_cast<const int*>(b); }
+  __device__ __forceinline__ static const uint2* grp(const unsigned char* b) {
+    return reinterpret_cast<const uint2*>(b + HDR);
+  }
+  __device__ __forceinline__ static const TaskRec* task(const unsigned char* b, int ax) {
+    return reinterpret_cast<const TaskRec*>(b + HDR + GRP) + ax * MAXT;
+  }
+};
+
+// One warp per tile: task lists of pass AX for the tile's groups (lanes),
+// packed in class order with warp scans.
+template <int D, int P, int G, int AX, bool LAST>
+__device__ __forceinline__ void schedule_pass(const TransArgs& a, const GroupMeta& m, bool valid, int* cnt,
+                                              TaskRec* out) {
+  constexpr int PD = Pow<P, D>::v;
+  constexpr int NS = 1 << D;
+  constexpr int SH = D - 1 - AX;
+  constexpr int NE = 1 << (D - 1);
+  const int lane = threadIdx.x & 31;
+  TaskRec mine[NE];
+  int n = 0, c3 = 0, c1 = 0, c2 = 0;
+  if (valid) {
+    const uint32_t PBp = AX > 0 ? proj_hi<D>(m.mB, AX) : 1u;
+    const uint32_t PAs = proj_lo<D>(m.mA, D - 1 - AX);
+    const uint32_t PBa = proj_hi<D>(m.mB, AX + 1);
+#pragma unroll
+    for (int bp = 0; bp < (1 << AX); ++bp) {
+      if (!(PBp >> bp & 1)) continue;
+      const uint32_t cls = (PBa >> (bp << 1)) & 3u;
+#pragma unroll
+      for (int as = 0; as < (1 << (D - 1 - AX)); ++as) {
+        if (!(PAs >> as & 1)) continue;
+        TaskRec t;
+        t.x = (uint32_t)((lane * NS + ((bp << (D - AX)) | as)) * PD);
+        t.cls = cls;
+        t.o0 = t.o1 = ~0u;
+        if (LAST) {
+          const int64_t q0 = out_pair(a, m, as), q1 = out_pair(a, m, (1 << SH) | as);
+          if (q0 >= 0) t.o0 = (uint32_t)(q0 * PD);
+          if (q1 >= 0) t.o1 = (uint32_t)(q1 * PD);
+        }
+        mine[n++ & (NE - 1)] = t;
+        c3 += cls == 3;
+        c1 += cls == 1;
+        c2 += cls == 2;
+      }
+    }
+  }
+  int o3 = c3, o1 = c1, o2 = c2;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int t3 = __shfl_up_sync(0xffffffffu, o3, d), t1 = __shfl_up_sync(0xffffffffu, o1, d),
+              t2 = __shfl_up_sync(0xffffffffu, o2, d);
+    if (lane >= d) {
+      o3 += t3;
+      o1 += t1;
+      o2 += t2;
+    }
+  }
+  const int n3 = __shfl_sync(0xffffffffu, o3, 31), n1 = __shfl_sync(0xffffffffu, o1, 31);
+  const int n2 = __shfl_sync(0xffffffffu, o2, 31);
+  o3 -= c3;
+  o1 += n3 - c1;
+  o2 += n3 + n1 - c2;
+#pragma unroll
+  for (int q = 0; q < NE; ++q) {
+    if (q < n) {
+      const TaskRec t = mine[q];
+      out[t.cls == 3 ? o3++ : (t.cls == 1 ? o1++ : o2++)] = t;
+    }
+  }
+  if (lane == 0) {
+    cnt[0] = n3;
+    cnt[1] = n1;
+    cnt[2] = n2;
+  }
+}
+
+template <int D, int P, int G>
+__global__ __launch_bounds__(128) void k_schedule(TransArgs a, unsigned char* __restrict__ sched, int64_t ntiles) {
+  using SC = Sched<D, P, G>;
+  const int lane = threadIdx.x & 31;
+  const int64_t tile = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (tile >= ntiles) return;
+  unsigned char* b = sched + tile * SC::BLK;
+  const int64_t g = tile * G + lane;
+  const bool valid = lane < G && g < a.ngroups;
+  GroupMeta m;
+  m.iB = m.iAp = 0;
+  m.cbK = m.cbX = 0;
+  m.mB = m.mA = 0;
+  if (valid) {
+    const uint32_t gg = (uint32_t)g, nap = (uint32_t)a.nAp_grp;
+    const uint32_t q = gg / nap;
+    m.iB = a.b_lo + q;
+    m.iAp = a.ap_lo + (gg - q * nap);
+    m.cbK = a.cbK[m.iB];
+    m.mB = a.mK[m.iB];
+    m.cbX = a.cbX[m.iAp];
+    m.mA = a.mX[m.iAp];
+  }
+  if (lane < G) {
+    const int64_t pin0 = ((int64_t)m.cbK - a.in_b0) * a.in_nA + (m.iAp - a.in_a0);
+    reinterpret_cast<uint2*>(b + SC::HDR)[lane] = valid ? make_uint2((uint32_t)pin0, m.mB) : make_uint2(0u, 0u);
+  }
+  int* cnt = reinterpret_cast<int*>(b);
+  TaskRec* tk = reinterpret_cast<TaskRec*>(b + SC::HDR + SC::GRP);
+  if constexpr (D == 2) {
+    schedule_pass<D, P, G, 1, false>(a, m, valid, cnt + 3, tk + SC::MAXT);
+    schedule_pass<D, P, G, 0, true>(a, m, valid, cnt, tk);
+  } else {
+    schedule_pass<D, P, G, 2, false>(a, m, valid, cnt + 6, tk + 2 * SC::MAXT);
+    schedule_pass<D, P, G, 1, false>(a, m, valid, cnt + 3, tk + SC::MAXT);
+    schedule_pass<D, P, G, 0, true>(a, m, valid, cnt, tk);
+  }
+}
+
+// One pass of the consumers (NC warps): super-tiles of 8 fiber rows.
+template <int D, int P, int G, int NC, int AX, bool LAST>
+__device__ __forceinline__ void consumer_pass(const TransArgs& a, double2* __restrict__ sb,
+                                              const unsigned char* __restrict__ blk, const LaneOps<P>& op) {
+  using S = MmaShape<P>;
+  using SC = Sched<D, P, G>;
+  constexpr int PD = Pow<P, D>::v;
+  constexpr int PF = PD / P;
+  constexpr int STR = Pow<P, D - 1 - AX>::v;
+  constexpr int SH = D - 1 - AX;
+  const int* cnt = SC::cnt(blk) + 3 * AX;
+  const TaskRec* tasks = SC::task(blk, AX);
+  const int ntot = (cnt[0] + cnt[1] + cnt[2]) * PF;
+  const int nst = __shfl_sync(0xffffffffu, (ntot + 7) >> 3, 0);
+  const int lane = threadIdx.x & 31, warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
+  const int r = lane >> 2, c = lane & 3;
+  const int rfib = (r >> 1) + 4 * (r & 1);  // rows 2q, 2q+1 <- fibers q, q+4 (bank-conflict-free)
+  int off[S::NK];
+#pragma unroll
+  for (int kk = 0; kk < S::NK; ++kk) off[kk] = (op.bk[kk] == 1 ? (1 << SH) * PD : 0) + op.lk[kk] * STR;
+  for (int st = warp; st < nst; st += NC) {
+    const int tau = st * 8 + rfib;
+    const bool vrow = tau < ntot;
+    TaskRec d;
+    int ebase = 0;
+    if (vrow) {
+      d = tasks[tau / PF];
+      const int f = tau % PF;
+      ebase = (f / STR) * STR * P + f % STR;
+    } else {
+      d.x = 0;
+      d.cls = 0;
+      d.o0 = d.o1 = ~0u;
+    }
+    const bool p0 = d.cls & 1, p1 = (d.cls >> 1) & 1;
+    const uint32_t xo = d.x + (uint32_t)ebase;
+    const double2* x = sb + xo;
+    const int cls = __shfl_sync(0xffffffffu,
+                                (__any_sync(0xffffffffu, p0) ? 1 : 0) | (__any_sync(0xffffffffu, p1) ? 2 : 0), 0);
+    double are[S::NT][2], aim[S::NT][2], tl[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int n = 0; n < S::NT; ++n) are[n][0] = are[n][1] = aim[n][0] = aim[n][1] = 0.0;
+#ifdef SFT_ABL_NOCOMPUTE  // ablation: no tensor-core work, everything else unchanged
+    if (false)
+#else
+    if (cls == 3)
+#endif
+      mma_steps<P, 0, S::NK>(op, x, off, p0, p1, are, aim, tl);
+    else if (cls == 1)
+      mma_steps<P, 0, S::K0_HI>(op, x, off, p0, p1, are, aim, tl);
+    else if (cls == 2)
+      mma_steps<P, S::K1_LO, S::NK>(op, x, off, p0, p1, are, aim, tl);
+    double2* o0;
+    double2* o1;
+#ifdef SFT_ABL_NOSTORE  // ablation: no output stores (shared or global)
+    if (true) {
+      o0 = o1 = nullptr;
+    } else
+#endif
+    if (LAST) {
+      o0 = d.o0 != ~0u ? a.out + d.o0 + ebase : nullptr;
+      o1 = d.o1 != ~0u ? a.out + d.o1 + ebase : nullptr;
+    } else {
+      o0 = vrow ? sb + xo : nullptr;
+      o1 = vrow ? sb + xo + (1 << SH) * PD : nullptr;
+    }
+#pragma unroll
+    for (int n = 0; n < S::NT; ++n) {
+      const int m = 4 * n + c;
+      if (m < S::NM) {
+        if (o0) o0[m * STR] = make_double2(are[n][0] + aim[n][1], aim[n][0] - are[n][1]);
+        if (o1) o1[m * STR] = make_double2(are[n][0] - aim[n][1], aim[n][0] + are[n][1]);
+      }
+    }
+    if (S::TAIL) {
+      // z_0 = (P.re + Q.im, P.im - Q.re), z_1 = (P.re - Q.im, P.im + Q.re) of m = P-1,
+      // partial over this lane's k; transpose-reduce over the 4 lanes of the row
+      const double u0 = tl[0] + tl[3], u1 = tl[2] - tl[1], u2 = tl[0] - tl[3], u3 = tl[2] + tl[1];
+      const bool odd = c & 1, hi = c & 2;
+      double va = odd ? u1 : u0, vb = odd ? u3 : u2;
+      va += __shfl_xor_sync(0xffffffffu, odd ? u0 : u1, 1);
+      vb += __shfl_xor_sync(0xffffffffu, odd ? u2 : u3, 1);
+      double w = hi ? vb : va;
+      w += __shfl_xor_sync(0xffffffffu, hi ? va : vb, 2);
+      double2* o = hi ? o1 : o0;  // lane c holds component c&1 of z_{c>>1}
+      if (o) reinterpret_cast<double*>(o + (P - 1) * STR)[c & 1] = w;
+    }
+  }
+}
+
+// Optional cycle accounting (-DSFT_INSTR): per-CTA sums of clock64 intervals
+// into g_instr[blockIdx][8]: 0 producer total, 1 producer wait(empty),
+// 2 producer issue, 3 consumer total, 4 consumer wait(full),
+// 5 consumer first pass(es), 6 consumer wait before the last pass, 7 consumer last pass.
+#ifdef SFT_INSTR
+__device__ unsigned long long* g_instr = nullptr;
+#define INSTR_T0(v) const long long v = clock64()
+#define INSTR_ADD(k, t0)                                                                      \
+  do {                                                                                        \
+    if ((threadIdx.x & 31) == 0 && g_instr)                                                   \
+      atomicAdd(&g_instr[(size_t)blockIdx.x * 8 + (k)], (unsigned long long)(clock64() - (t0))); \
+  } while (0)
+#else
+#define INSTR_T0(v)
+#define INSTR_ADD(k, t0)
+#endif
+
+// named barrier over the NT consumer threads (the producer warp never joins)
+template <int NT>
+__device__ __forceinline__ void consumer_sync() {
+  asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (true) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    if (done) break;
+    __nanosleep(32);
+  }
+}
+
+template <int P>
+__device__ __forceinline__ void load_lane_ops(LaneOps<P>& op, const double* __restrict__ frag, int lane) {
+  using S = MmaShape<P>;
+#pragma unroll
+  for (int kk = 0; kk < S::NK; ++kk) {
+#pragma unroll
+    for (int n = 0; n < S::NT; ++n) op.fb[kk][n] = frag[(kk * S::NT + n) * 32 + lane];
+    if (S::TAIL) {
+      op.ft[kk][0] = frag[S::NK * S::NT * 32 + (kk * 2 + 0) * 32 + lane];
+      op.ft[kk][1] = frag[S::NK * S::NT * 32 + (kk * 2 + 1) * 32 + lane];
+    } else {
+      op.ft[kk][0] = op.ft[kk][1] = 0.0;
+    }
+    const int k = 4 * kk + (lane & 3);
+    op.bk[kk] = k < 2 * P ? k / P : 2;
+    op.lk[kk] = k < 2 * P ? k % P : 0;
+  }
+}
+
+// Warp-specialised translation kernel (default).  Warp NC is the producer: it
+// runs up to NST tiles ahead, and per tile arms full[s] with the byte count,
+// bulk-copies the tile's schedule block into the stage bookkeeping and every
+// present child array into the stage (reading the group records of its next
+// tile from HBM while it waits for a free stage).  Warps 0..NC-1 consume.
+// 2D with NST >= 3: skewed pipeline, pass 1 of tile i+1 runs before pass 0 of
+// tile i, and pass 0 waits on an mbarrier (p1done) every consumer thread
+// arrives on after its pass-1 rows, so warps do not idle at a pass barrier.
+#ifndef SFT_WS_MINB
+#define SFT_WS_MINB 1
+#endif
+template <int D, int P, int G, int NC, int NST>
+__global__ __launch_bounds__((NC + 1) * 32, SFT_WS_MINB) void k_translate_ws(TransArgs a, const double* __restrict__ frag,
+                                                                             const unsigned char* __restrict__ sched,
+                                                                             int64_t ntiles) {
+  using SC = Sched<D, P, G>;
+  constexpr int PD = Pow<P, D>::v;
+  constexpr int NS = 1 << D;
+  constexpr int STAGE = G * NS * PD;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double2* ring = reinterpret_cast<double2*>(smem_raw);  // [NST][G][NS][PD]
+  __shared__ __align__(128) unsigned char blk[NST][SC::BLK];
+  __shared__ __align__(8) uint64_t full[NST], empty[NST], p1done[NST];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x < NST) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full[threadIdx.x])));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&empty[threadIdx.x])), "r"(NC));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&p1done[threadIdx.x])), "r"(NC * 32));
+  }
+  if (threadIdx.x == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+  if (warp == NC) {
+    // ---------------- producer ----------------
+    INSTR_T0(tp0);
+    int s = 0;
+    uint32_t ph = 0;
+    int64_t tile = blockIdx.x;
+    uint2 gr = (tile < ntiles && lane < G) ? __ldg(reinterpret_cast<const uint2*>(sched + tile * SC::BLK + SC::HDR) + lane)
+                                           : make_uint2(0u, 0u);
+    for (int i = 0; tile < ntiles; ++i) {
+      const int64_t next = tile + gridDim.x;
+      const uint2 gn = (next < ntiles && lane < G)
+                           ? __ldg(reinterpret_cast<const uint2*>(sched + next * SC::BLK + SC::HDR) + lane)
+                           : make_uint2(0u, 0u);
+      INSTR_T0(tw0);
+      if (i >= NST) mbar_wait_sleep(smem_u32(&empty[s]), ph ^ 1u);
+      INSTR_ADD(1, tw0);
+      INSTR_T0(tb0);
+      uint32_t nbytes = __popc(gr.y) * PD * (uint32_t)sizeof(double2);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) nbytes += __shfl_xor_sync(0xffffffffu, nbytes, o);
+      double2* sb = ring + s * STAGE;
+      if (lane == 0) {
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&full[s])),
+                     "r"(nbytes + (uint32_t)SC::BLK)
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                smem_u32(&blk[s][0])),
+            "l"(sched + tile * SC::BLK), "r"((uint32_t)SC::BLK), "r"(smem_u32(&full[s]))
+            : "memory");
+      }
+      __syncwarp();
+      uint32_t mm = gr.y;
+      int r = 0;
+      while (mm) {
+        const int c = __ffs(mm) - 1;
+        mm &= mm - 1;
+        const int64_t pin = (int64_t)gr.x + (int64_t)(r++) * a.in_nA;
+#ifndef SFT_ABL_NOLOAD
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                smem_u32(sb + ((int64_t)lane * NS + c) * PD)),
+            "l"(a.in + pin * PD), "r"((uint32_t)(PD * sizeof(double2))), "r"(smem_u32(&full[s]))
+            : "memory");
+#else
+        (void)pin;
+        asm volatile("mbarrier.complete_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&full[s])),
+                     "r"((uint32_t)(PD * sizeof(double2)))
+                     : "memory");
+#endif
+      }
+      INSTR_ADD(2, tb0);
+      gr = gn;
+      tile = next;
+      if (++s == NST) {
+        s = 0;
+        ph ^= 1u;
+      }
+    }
+    INSTR_ADD(0, tp0);
+    return;
+  }
+  // ---------------- consumers ----------------
+  LaneOps<P> op;
+  load_lane_ops<P>(op, frag, lane);
+  int s = 0;
+  uint32_t ph = 0;
+  INSTR_T0(tc0);
+  if constexpr (D == 2 && NST >= 3) {
+    int64_t tile = blockIdx.x;
+    if (tile < ntiles) {
+      mbar_wait(smem_u32(&full[0]), 0);
+      consumer_pass<D, P, G, NC, 1, false>(a, ring, blk[0], op);
+      asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&p1done[0])) : "memory");
+    }
+    for (; tile < ntiles; tile += gridDim.x) {
+      const int64_t nt = tile + gridDim.x;
+      const int sn = s + 1 == NST ? 0 : s + 1;
+      const uint32_t phn = sn == 0 ? ph ^ 1u : ph;
+      if (nt < ntiles) {
+        INSTR_T0(tf0);
+        mbar_wait(smem_u32(&full[sn]), phn);
+        INSTR_ADD(4, tf0);
+        INSTR_T0(t1);
+        consumer_pass<D, P, G, NC, 1, false>(a, ring + sn * STAGE, blk[sn], op);
+        asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&p1done[sn])) : "memory");
+        INSTR_ADD(5, t1);
+      }
+      INSTR_T0(t2);
+      mbar_wait(smem_u32(&p1done[s]), ph);
+      INSTR_ADD(6, t2);
+      INSTR_T0(t3);
+      consumer_pass<D, P, G, NC, 0, true>(a, ring + s * STAGE, blk[s], op);
+      INSTR_ADD(7, t3);
+      __syncwarp();
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[s])) : "memory");
+      s = sn;
+      ph = phn;
+    }
+  } else {
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      INSTR_T0(tf0);
+      mbar_wait(smem_u32(&full[s]), ph);
+      INSTR_ADD(4, tf0);
+      double2* sb = ring + s * STAGE;
+      if constexpr (D == 2) {
+        consumer_pass<D, P, G, NC, 1, false>(a, sb, blk[s], op);
+        consumer_sync<NC * 32>();
+        consumer_pass<D, P, G, NC, 0, true>(a, sb, blk[s], op);
+      } else {
+        consumer_pass<D, P, G, NC, 2, false>(a, sb, blk[s], op);
+        consumer_sync<NC * 32>();
+        consumer_pass<D, P, G, NC, 1, false>(a, sb, blk[s], op);
+        consumer_sync<NC * 32>();
+        consumer_pass<D, P, G, NC, 0, true>(a, sb, blk[s], op);
+      }
+      __syncwarp();
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[s])) : "memory");
+      if (++s == NST) {
+        s = 0;
+        ph ^= 1u;
+      }
+    }
+  }
+  INSTR_ADD(3, tc0);
+}
+
+template <int P>
+static std::vector<double> mma_fragments() {
+  using S = MmaShape<P>;
+  std::vector<double> V, invD, RC, RS;
+  build_tables_host(P, V, invD, &RC, &RS);
+  auto rc = [&](int b, int m, int l) { return RC[((size_t)b * P + m) * P + l]; };
+  auto rs = [&](int b, int m, int l) { return RS[((size_t)b * P + m) * P + l]; };
+  auto bop = [&](int k, int m, int pq) -> double {
+    if (k >= 2 * P || m >= P) return 0.0;
+    const int b = k / P, l = k % P;
+    if (pq == 0) return b == 0 ? rc(0, m, l) : rs(1, m, l);
+    return b == 0 ? rs(0, m, l) : -rc(1, m, l);
+  };
+  std::vector<double> fr(S::NFRAG, 0.0);
+  for (int kk = 0; kk < S::NK; ++kk)
+    for (int n = 0; n < S::NT; ++n)
+      for (int lane = 0; lane < 32; ++lane) {
+        const int k = 4 * kk + (lane & 3), col = 8 * n + (lane >> 2);
+        const int m = col / 2, pq = col & 1;
+        fr[(kk * S::NT + n) * 32 + lane] = m < S::NM ? bop(k, m, pq) : 0.0;
+      }
+  if (S::TAIL)
+    for (int kk = 0; kk < S::NK; ++kk)
+      for (int pq = 0; pq < 2; ++pq)
+        for (int lane = 0; lane < 32; ++lane)
+          fr[S::NK * S::NT * 32 + (kk * 2 + pq) * 32 + lane] = bop(4 * kk + (lane & 3), P - 1, pq);
+  return fr;
+}
+
+template <int P>
+static const double* device_fragments(cudaError_t* err) {
+  static std::mutex mu;
+  static std::map<int, double*> cache;
+  int dev = 0;
+  if ((*err = cudaGetDevice(&dev)) != cudaSuccess) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(dev);
+  if (it != cache.end()) return it->second;
+  std::vector<double> fr = mma_fragments<P>();
+  double* d = nullptr;
+  if ((*err = cudaMalloc(&d, fr.size() * sizeof(double))) != cudaSuccess) return nullptr;
+  if ((*err = cudaMemcpy(d, fr.data(), fr.size() * sizeof(double), cudaMemcpyHostToDevice)) != cudaSuccess)
+    return nullptr;
+  cache[dev] = d;
+  return d;
+}
+
+// ------------------------------------------------------------------------
+// FMA kernel (round-1 design, kept for ablation: SFT_TRANSLATE=fma)
+// ------------------------------------------------------------------------
+// One fiber, both outputs, children present per CLS (bit 0: beta=0, bit 1:
+// beta=1); straight-line code over all rows.  CS form with constant-bank
+// operands: z_alpha[m] = sum_beta c_{alpha beta} (RC_beta[m] . x_beta + i (2 alpha - 1) RS_beta[m] . x_beta),
+// c_{alpha,0} = 1, c_{0,1} = i, c_{1,1} = -i.
+template <int P, int CLS, class Store>
+__device__ __forceinline__ void contract_fiber(const double2 (&x0)[P], const double2 (&x1)[P], Store store) {
+#pragma unroll
+  for (int m = 0; m < P; ++m) {
+    double2 z0 = make_double2(0.0, 0.0), z1 = make_double2(0.0, 0.0);
+    if (CLS & 1) {
+      double ur = 0.0, ui = 0.0, vr = 0.0, vi = 0.0;
+#pragma unroll
+      for (int l = 0; l < P; ++l) {
+        const double cc = CT<P>::rc(0, m, l), s = CT<P>::rs(0, m, l);
+        ur = fma(cc, x0[l].x, ur);
+        ui = fma(cc, x0[l].y, ui);
+        vr = fma(s, x0[l].x, vr);
+        vi = fma(s, x0[l].y, vi);
+      }
+      z0 = make_double2(ur + vi, ui - vr);
+      z1 = make_double2(ur - vi, ui + vr);
+    }
+    if (CLS & 2) {
+      double ur = 0.0, ui = 0.0, vr = 0.0, vi = 0.0;
+#pragma unroll
+      for (int l = 0; l < P; ++l) {
+        const double cc = CT<P>::rc(1, m, l), s = CT<P>::rs(1, m, l);
+        ur = fma(cc, x1[l].x, ur);
+        ui = fma(cc, x1[l].y, ui);
+        vr = fma(s, x1[l].x, vr);
+        vi = fma(s, x1[l].y, vi);
+      }
+      z0.x -= ui - vr;
+      z0.y += ur + vi;
+      z1.x += ui + vr;
+      z1.y -= ur - vi;
+    }
+    store(m, z0, z1);
+  }
+}
+
+template <int D, int P, int G, int NT, int AX, bool LAST>
+__device__ __forceinline__ void fma_pass(const TransArgs& a, double2* __restrict__ sb, const GroupMeta* gm, int ng,
+                                         TaskEntry* ent, int* cnt) {
+  constexpr int PD = Pow<P, D>::v;
+  constexpr int NS = 1 << D;
+  constexpr int PF = PD / P;
+  constexpr int STR = Pow<P, D - 1 - AX>::v;
+  constexpr int SH = D - 1 - AX;
+  constexpr int MAXE = G << (D - 1);
+  build_tasks<D, G, AX>(gm, ng, ent, cnt);
+  const int n3 = cnt[0], n1 = cnt[1], n2 = cnt[2];
+  const int ntot = (n3 + n1 + n2) * PF;
+  for (int tau = threadIdx.x; tau < ntot; tau += NT) {
+    const TaskEntry te = task_at<MAXE>(ent, tau / PF, n3, n1);
+    const int f = tau % PF;
+    const GroupMeta& g = gm[te.j];
+    const int lo = f % STR, hi = f / STR;
+    const int ebase = hi * STR * P + lo;
+    const int slot0 = (te.bp << (D - AX)) | te.as;
+    double2* s0 = sb + ((int)te.j * NS + slot0) * PD + ebase;
+    double2* s1 = s0 + (1 << SH) * PD;
+    double2 x0[P], x1[P];
+    double2* o0;
+    double2* o1;
+    if (!LAST) {
+      o0 = s0;
+      o1 = s1;
+    } else {
+      o0 = out_array<PD>(a, g, te.as);
+      o1 = out_array<PD>(a, g, (1 << SH) | te.as);
+      if (o0) o0 += ebase;
+      if (o1) o1 += ebase;
+    }
+    auto store = [&](int m, double2 z0, double2 z1) {
+      if (o0) o0[m * STR] = z0;
+      if (o1) o1[m * STR] = z1;
+    };
+    if (te.cls == 3) {
+#pragma unroll
+      for (int l = 0; l < P; ++l) {
+        x0[l] = s0[l * STR];
+        x1[l] = s1[l * STR];
+      }
+      contract_fiber<P, 3>(x0, x1, store);
+    } else if (te.cls == 1) {
+#pragma unroll
+      for (int l = 0; l < P; ++l) x0[l] = s0[l * STR];
+      contract_fiber<P, 1>(x0, x1, store);
+    } else {
+#pragma unroll
+      for (int l = 0; l < P; ++l) x1[l] = s1[l * STR];
+      contract_fiber<P, 2>(x0, x1, store);
+    }
+  }
+  __syncthreads();
+}
+
+// minBlocksPerSM: target 16 resident warps (an explicit 1 lets ptxas take
+// ~200 registers and halves occupancy; forcing fewer than ~120 spills)
+#define SFT_FMA_MINB(NT) ((16 * 32 / (NT)) > 0 ? (16 * 32 / (NT)) : 1)
+template <int D, int P, int G, int NT>
+__global__ __launch_bounds__(NT, SFT_FMA_MINB(NT)) void k_translate_fma(TransArgs a) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double2* sb = reinterpret_cast<double2*>(smem_raw);  // [G][NS][PD]
+  __shared__ GroupMeta gm[G];
+  __shared__ TaskEntry ent[3 * (G << (D - 1))];
+  __shared__ int cnt[4];
+  __shared__ __align__(8) uint64_t bar;
+  const int ng = tile_prologue<D, P, G>(a, sb, gm, &bar);
+  mbar_wait(smem_u32(&bar), 0);
+  if constexpr (D == 2) {
+    fma_pass<D, P, G, NT, 1, false>(a, sb, gm, ng, ent, cnt);
+    fma_pass<D, P, G, NT, 0, true>(a, sb, gm, ng, ent, cnt);
+  } else {
+    fma_pass<D, P, G, NT, 2, false>(a, sb, gm, ng, ent, cnt);
+    fma_pass<D, P, G, NT, 1, false>(a, sb, gm, ng, ent, cnt);
+    fma_pass<D, P, G, NT, 0, true>(a, sb, gm, ng, ent, cnt);
+  }
+}
+
+
+// ------------------------------------------------------------------------
+// launch configuration (tile of G groups per stage; tuned on B200)
+// ------------------------------------------------------------------------
+#ifndef SFT_WS_G29
+#define SFT_WS_G29 4
+#endif
+#ifndef SFT_WS_NC29
+#define SFT_WS_NC29 4
+#endif
+#ifndef SFT_WS_NST29
+#define SFT_WS_NST29 3
+#endif
+template <int D, int P>
+struct WsCfg;
+template <> struct WsCfg<2, 5> { static constexpr int G = 16, NC = 4, NST = 3; };
+template <> struct WsCfg<2, 7> { static constexpr int G = 8, NC = 4, NST = 3; };
+template <> struct WsCfg<2, 9> { static constexpr int G = SFT_WS_G29, NC = SFT_WS_NC29, NST = SFT_WS_NST29; };
+template <> struct WsCfg<3, 5> { static constexpr int G = 2, NC = 4, NST = 3; };
+template <> struct WsCfg<3, 7> { static constexpr int G = 1, NC = 4, NST = 2; };
+template <> struct WsCfg<3, 9> { static constexpr int G = 1, NC = 8, NST = 2; };
+
+template <int D, int P>
+struct FmaCfg;
+template <> struct FmaCfg<2, 5> { static constexpr int G = 16, NT = 128; };
+template <> struct FmaCfg<2, 7> { static constexpr int G = 12, NT = 128; };
+template <> struct FmaCfg<2, 9> { static constexpr int G = 16, NT = 256; };
+template <> struct FmaCfg<3, 5> { static constexpr int G = 4, NT = 256; };
+template <> struct FmaCfg<3, 7> { static constexpr int G = 2, NT = 256; };
+template <> struct FmaCfg<3, 9> { static constexpr int G = 1, NT = 256; };
+
+static TransArgs make_args(const LevelDims& L, const double2* in, double2* out) {
+  TransArgs a;
+  a.in = in;
+  a.out = out;
+  a.cbK = L.cbK;
+  a.mK = L.mK;
+  a.cbX = L.cbX;
+  a.mX = L.mX;
+  a.b_lo = L.b_lo;
+  a.nAp_grp = L.ap_hi - L.ap_lo;
+  a.ap_lo = L.ap_lo;
+  a.ngroups = (L.b_hi - L.b_lo) * a.nAp_grp;
+  a.in_b0 = L.in_b0;
+  a.in_nA = L.in_nA;
+  a.in_a0 = L.in_a0;
+  a.out_b0 = L.out_b0;
+  a.out_nA = L.out_nA;
+  a.out_a0 = L.out_a0;
+  a.seg = L.seg;
+  a.nseg = L.nseg;
+  return a;
+}
+
+// SFT_TRANSLATE = ws (default) | fma
+int translate_kernel_choice() {
+  static int mode = -1;
+  if (mode < 0) {
+    const char* e = getenv("SFT_TRANSLATE");
+    mode = (e && strcmp(e, "fma") == 0) ? 1 : 0;
+  }
+  return mode;
+}
+
+// resident-CTA grid size for a persistent kernel
+template <class K>
+static cudaError_t persistent_grid(K kernel, int threads, size_t smem, int* grid) {
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int dev = 0, nsm = 0, bps = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kernel, threads, smem);
+  if (e != cudaSuccess) return e;
+  if (bps < 1) return cudaErrorInvalidConfiguration;
+  *grid = nsm * bps;
+  return cudaSuccess;
+}
+
+template <int D, int P>
+static cudaError_t launch_translate_t(const sft_plan_s* Pl, const LevelDims& L, const double2* in, double2* out) {
+  constexpr int PD = Pow<P, D>::v;
+  TransArgs a = make_args(L, in, out);
+  if (a.ngroups <= 0) return cudaSuccess;
+  if (translate_kernel_choice() == 0) {
+    constexpr int G = WsCfg<D, P>::G, NC = WsCfg<D, P>::NC, NST = WsCfg<D, P>::NST;
+    const size_t smem = (size_t)NST * G * (1 << D) * PD * sizeof(double2);
+    static int grid_max = 0;
+    static const double* frag = nullptr;
+    if (!grid_max) {
+      cudaError_t e = persistent_grid(k_translate_ws<D, P, G, NC, NST>, (NC + 1) * 32, smem, &grid_max);
+      if (e != cudaSuccess) return e;
+      frag = device_fragments<P>(&e);
+      if (!frag) return e;
+    }
+    if (!L.sched) return cudaErrorInvalidValue;
+    const int64_t ntiles = (a.ngroups + G - 1) / G;
+    const int64_t grid = std::min<int64_t>(ntiles, grid_max);
+    k_translate_ws<D, P, G, NC, NST><<<(unsigned)grid, (NC + 1) * 32, smem, Pl->stream>>>(a, frag, L.sched, ntiles);
+  } else {
+    constexpr int G = FmaCfg<D, P>::G, NT = FmaCfg<D, P>::NT;
+    const size_t smem = (size_t)G * (1 << D) * PD * sizeof(double2);
+    static bool attr = false;
+    if (!attr) {
+      cudaError_t e = cudaFuncSetAttribute(k_translate_fma<D, P, G, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem);
+      if (e != cudaSuccess) return e;
+      attr = true;
+    }
+    const int64_t ntiles = (a.ngroups + G - 1) / G;
+    k_translate_fma<D, P, G, NT><<<(unsigned)ntiles, NT, smem, Pl->stream>>>(a);
+  }
+  count_launch();
+  return cudaGetLastError();
+}
+
+template <int D, int P>
+static size_t schedule_bytes_t(const LevelDims& L) {
+  if (translate_kernel_choice() != 0) return 0;
+  constexpr int G = WsCfg<D, P>::G;
+  const int64_t ng = (L.b_hi - L.b_lo) * (L.ap_hi - L.ap_lo);
+  if (ng <= 0) return 0;
+  return (size_t)((ng + G - 1) / G) * Sched<D, P, G>::BLK;
+}
+
+template <int D, int P>
+static cudaError_t launch_schedule_t(const sft_plan_s* Pl, const LevelDims& L, unsigned char* dst) {
+  if (translate_kernel_choice() != 0) return cudaSuccess;
+  constexpr int G = WsCfg<D, P>::G;
+  TransArgs a = make_args(L, nullptr, nullptr);
+  if (a.ngroups <= 0) return cudaSuccess;
+  const int64_t ntiles = (a.ngroups + G - 1) / G;
+  k_schedule<D, P, G><<<(unsigned)((ntiles + 3) / 4), 128, 0, Pl->stream>>>(a, dst, ntiles);
+  count_launch();
+  return cudaGetLastError();
+}
+
+static cudaError_t schedule_bytes_d(const sft_plan_s* Pl, const LevelDims& L, size_t* r) {
+  SFT_DISPATCH(Pl->d, Pl->p, (*r = schedule_bytes_t<D, P>(L)));
+  return cudaSuccess;
+}
+
+size_t schedule_bytes(const sft_plan_s* Pl, const LevelDims& L) {
+  size_t r = 0;
+  schedule_bytes_d(Pl, L, &r);
+  return r;
+}
+
+cudaError_t launch_schedule(const sft_plan_s* Pl, const LevelDims& L, unsigned char* dst) {
+  SFT_DISPATCH(Pl->d, Pl->p, return (launch_schedule_t<D, P>(Pl, L, dst)));
+  return cudaSuccess;
+}
+
+cudaError_t launch_translate(const sft_plan_s* Pl, const LevelDims& L, const double2* in, double2* out) {
+  SFT_DISPATCH(Pl->d, Pl->p, return (launch_translate_t<D, P>(Pl, L, in, out)));
+  return cudaSuccess;
+}
+
+}  // namespace sft
+
+#ifdef SFT_INSTR
+extern "C" int sft_instr_set(void* dev_buf) {
+  return cudaMemcpyToSymbol(sft::g_instr, &dev_buf, sizeof(void*)) == cudaSuccess ? 0 : 4;
+}
+#endif

@@ -80,6 +80,65 @@ __global__ void dmma(double* out, int iters) {
   if (s == 12345.678) out[0] = s;
 }
 
+
+// latency of one dependent DMMA (single warp, one accumulator chain)
+__global__ void dmma_lat(double* out, long long* cyc, int iters) {
+  double a = threadIdx.x * 1e-3, b = 1.0 + threadIdx.x * 1e-4;
+  double c0[2] = {0, 0};
+  long long t0 = clock64();
+  for (int i = 0; i < iters; ++i)
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(c0[0]), "+d"(c0[1]) : "d"(a), "d"(b));
+  long long t1 = clock64();
+  if (threadIdx.x == 0) cyc[0] = t1 - t0;
+  if (c0[0] + c0[1] == 12345.678) out[0] = c0[0];
+}
+
+// DMMA with CH independent chains per warp
+template <int CH>
+__global__ void dmma_ch(double* out, int iters) {
+  double a = threadIdx.x * 1e-3, b = 1.0 + threadIdx.x * 1e-4;
+  double c[CH][2];
+#pragma unroll
+  for (int j = 0; j < CH; ++j) c[j][0] = c[j][1] = 0;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int j = 0; j < CH; ++j)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                   : "+d"(c[j][0]), "+d"(c[j][1]) : "d"(a), "d"(b));
+  }
+  double s = 0;
+#pragma unroll
+  for (int j = 0; j < CH; ++j) s += c[j][0] + c[j][1];
+  if (s == 12345.678) out[0] = s;
+}
+
+// DMMA (4 chains) and DFMA (8 chains) interleaved in the same warp: do the
+// two pipes add up?
+__global__ void mixed(double* out, int iters, double fa, double fb) {
+  double a = threadIdx.x * 1e-3, b = 1.0 + threadIdx.x * 1e-4;
+  double c[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
+  double acc[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) acc[j] = threadIdx.x * 1e-3 + j;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                   : "+d"(c[j][0]), "+d"(c[j][1]) : "d"(a), "d"(b));
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] = fma(acc[j], fa, fb);
+  }
+  double s = 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) s += c[j][0] + c[j][1];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) s += acc[j];
+  if (s == 12345.678) out[0] = s;
+}
+
 __global__ void clk(long long* o) {
   long long t0 = clock64();
   long long g0;
@@ -149,6 +208,31 @@ int main() {
     float ms = timeit([&] { dmma<<<blocks, threads>>>(out, iters / 4); });
     double fl = 2.0 * 8 * 8 * 4 * 4 * (iters / 4) * (double)(threads / 32) * blocks;
     printf("{\"test\": \"dmma_m8n8k4\", \"ms\": %.3f, \"tflops\": %.2f}\n", ms, fl / ms / 1e9);
+  }
+  {
+    dmma_lat<<<1, 32>>>(out, ck, 10000);
+    cudaDeviceSynchronize();
+    long long cyc;
+    cudaMemcpy(&cyc, ck, 8, cudaMemcpyDeviceToHost);
+    printf("{\"test\": \"dmma_dependent_latency\", \"cycles\": %.1f}\n", cyc / 10000.0);
+  }
+  for (int wps : {4, 8, 16, 32}) {
+    float ms = timeit([&] { dmma_ch<4><<<nsm, 32 * wps>>>(out, iters / 4); });
+    double fl = 2.0 * 256 * 4 * (iters / 4) * (double)wps * nsm;
+    printf("{\"test\": \"dmma_4chains\", \"warps_per_sm\": %d, \"tflops\": %.2f}\n", wps, fl / ms / 1e9);
+  }
+  for (int wps : {4, 8, 16}) {
+    float ms = timeit([&] { dmma_ch<8><<<nsm, 32 * wps>>>(out, iters / 8); });
+    double fl = 2.0 * 256 * 8 * (iters / 8) * (double)wps * nsm;
+    printf("{\"test\": \"dmma_8chains\", \"warps_per_sm\": %d, \"tflops\": %.2f}\n", wps, fl / ms / 1e9);
+  }
+  {
+    const int it2 = iters / 4;
+    float ms = timeit([&] { mixed<<<blocks, threads>>>(out, it2, 0.999, 1e-6); });
+    double fl_mma = 2.0 * 256 * 4 * it2 * (double)(threads / 32) * blocks;
+    double fl_fma = 2.0 * 32 * 32 * it2 * (double)(threads / 32) * blocks;
+    printf("{\"test\": \"mixed_dmma_dfma\", \"ms\": %.3f, \"tflops_total\": %.2f, \"tflops_dmma\": %.2f, \"tflops_dfma\": %.2f}\n",
+           ms, (fl_mma + fl_fma) / ms / 1e9, fl_mma / ms / 1e9, fl_fma / ms / 1e9);
   }
   {
     clk<<<1, 1>>>(ck);
