@@ -303,26 +303,36 @@ struct LaneOps {
 // k-steps [K_LO, K_HI) of one MMA super-tile: A fragments (re and im of one
 // complex element per lane, one 16-byte shared-memory load) times the B
 // fragments held in registers; tail column m = P-1 on DFMA.
-template <int P, int K_LO, int K_HI>
-__device__ __forceinline__ void mma_steps(const LaneOps<P>& op, const double2* __restrict__ x, const int (&off)[MmaShape<P>::NK],
-                                          bool p0, bool p1, double (&are)[MmaShape<P>::NT][2],
-                                          double (&aim)[MmaShape<P>::NT][2], double (&tl)[4]) {
+template <int P, int K_LO, int K_HI, int NSUB>
+__device__ __forceinline__ void mma_steps(const LaneOps<P>& op, const double2* const (&x)[NSUB],
+                                          const int (&off)[MmaShape<P>::NK], const bool (&p0)[NSUB],
+                                          const bool (&p1)[NSUB], double (&are)[NSUB][MmaShape<P>::NT][2],
+                                          double (&aim)[NSUB][MmaShape<P>::NT][2], double (&tl)[NSUB][4]) {
   using S = MmaShape<P>;
 #pragma unroll
   for (int kk = K_LO; kk < K_HI; ++kk) {
     const int b = op.bk[kk];
-    const bool live = b == 0 ? p0 : (b == 1 ? p1 : false);
-    const double2 av = live ? x[off[kk]] : make_double2(0.0, 0.0);
+    double2 av[NSUB];
 #pragma unroll
-    for (int n = 0; n < S::NT; ++n) {
-      dmma(are[n], av.x, op.fb[kk][n]);
-      dmma(aim[n], av.y, op.fb[kk][n]);
+    for (int u = 0; u < NSUB; ++u) {
+      const bool live = b == 0 ? p0[u] : (b == 1 ? p1[u] : false);
+      av[u] = live ? x[u][off[kk]] : make_double2(0.0, 0.0);
     }
+#pragma unroll
+    for (int n = 0; n < S::NT; ++n)
+#pragma unroll
+      for (int u = 0; u < NSUB; ++u) {
+        dmma(are[u][n], av[u].x, op.fb[kk][n]);
+        dmma(aim[u][n], av[u].y, op.fb[kk][n]);
+      }
     if (S::TAIL) {
-      tl[0] = fma(av.x, op.ft[kk][0], tl[0]);
-      tl[1] = fma(av.x, op.ft[kk][1], tl[1]);
-      tl[2] = fma(av.y, op.ft[kk][0], tl[2]);
-      tl[3] = fma(av.y, op.ft[kk][1], tl[3]);
+#pragma unroll
+      for (int u = 0; u < NSUB; ++u) {
+        tl[u][0] = fma(av[u].x, op.ft[kk][0], tl[u][0]);
+        tl[u][1] = fma(av[u].x, op.ft[kk][1], tl[u][1]);
+        tl[u][2] = fma(av[u].y, op.ft[kk][0], tl[u][2]);
+        tl[u][3] = fma(av[u].y, op.ft[kk][1], tl[u][3]);
+      }
     }
   }
 }
@@ -335,6 +345,47 @@ __device__ __forceinline__ void mma_steps(const LaneOps<P>& op, const double2* _
 // fibers q, q+4 of the super-tile (conflict-free 16-byte shared loads for
 // the unit and p-strided fibers of p = 9).  Outputs go back in place, or to
 // HBM in the last pass.
+
+// One fiber, both outputs, children present per CLS (bit 0: beta=0, bit 1:
+// beta=1); straight-line code over all rows.  CS form with constant-bank
+// operands: z_alpha[m] = sum_beta c_{alpha beta} (RC_beta[m] . x_beta + i (2 alpha - 1) RS_beta[m] . x_beta),
+// c_{alpha,0} = 1, c_{0,1} = i, c_{1,1} = -i.
+template <int P, int CLS, class Store>
+__device__ __forceinline__ void contract_fiber(const double2 (&x0)[P], const double2 (&x1)[P], Store store) {
+#pragma unroll
+  for (int m = 0; m < P; ++m) {
+    double2 z0 = make_double2(0.0, 0.0), z1 = make_double2(0.0, 0.0);
+    if (CLS & 1) {
+      double ur = 0.0, ui = 0.0, vr = 0.0, vi = 0.0;
+#pragma unroll
+      for (int l = 0; l < P; ++l) {
+        const double cc = CT<P>::rc(0, m, l), s = CT<P>::rs(0, m, l);
+        ur = fma(cc, x0[l].x, ur);
+        ui = fma(cc, x0[l].y, ui);
+        vr = fma(s, x0[l].x, vr);
+        vi = fma(s, x0[l].y, vi);
+      }
+      z0 = make_double2(ur + vi, ui - vr);
+      z1 = make_double2(ur - vi, ui + vr);
+    }
+    if (CLS & 2) {
+      double ur = 0.0, ui = 0.0, vr = 0.0, vi = 0.0;
+#pragma unroll
+      for (int l = 0; l < P; ++l) {
+        const double cc = CT<P>::rc(1, m, l), s = CT<P>::rs(1, m, l);
+        ur = fma(cc, x1[l].x, ur);
+        ui = fma(cc, x1[l].y, ui);
+        vr = fma(s, x1[l].x, vr);
+        vi = fma(s, x1[l].y, vi);
+      }
+      z0.x -= ui - vr;
+      z0.y += ur + vi;
+      z1.x += ui + vr;
+      z1.y -= ur - vi;
+    }
+    store(m, z0, z1);
+  }
+}
 
 // ------------------------------------------------------------------------
 // Tile schedule (built once per plan by k_schedule, read by the producer)
@@ -477,12 +528,17 @@ __global__ __launch_bounds__(128) void k_schedule(TransArgs a, unsigned char* __
   }
 }
 
-// One pass of the consumers (NC warps): super-tiles of 8 fiber rows.
+// One pass of the consumers (NC warps): super-tiles of 8 fiber rows, NSUB
+// super-tiles per warp iteration (independent MMA chains interleaved).
+#ifndef SFT_NSUB
+#define SFT_NSUB 1
+#endif
 template <int D, int P, int G, int NC, int AX, bool LAST>
 __device__ __forceinline__ void consumer_pass(const TransArgs& a, double2* __restrict__ sb,
                                               const unsigned char* __restrict__ blk, const LaneOps<P>& op) {
   using S = MmaShape<P>;
   using SC = Sched<D, P, G>;
+  constexpr int NSUB = SFT_NSUB;
   constexpr int PD = Pow<P, D>::v;
   constexpr int PF = PD / P;
   constexpr int STR = Pow<P, D - 1 - AX>::v;
@@ -497,72 +553,90 @@ __device__ __forceinline__ void consumer_pass(const TransArgs& a, double2* __res
   int off[S::NK];
 #pragma unroll
   for (int kk = 0; kk < S::NK; ++kk) off[kk] = (op.bk[kk] == 1 ? (1 << SH) * PD : 0) + op.lk[kk] * STR;
-  for (int st = warp; st < nst; st += NC) {
-    const int tau = st * 8 + rfib;
-    const bool vrow = tau < ntot;
-    TaskRec d;
-    int ebase = 0;
-    if (vrow) {
-      d = tasks[tau / PF];
-      const int f = tau % PF;
-      ebase = (f / STR) * STR * P + f % STR;
-    } else {
-      d.x = 0;
-      d.cls = 0;
-      d.o0 = d.o1 = ~0u;
-    }
-    const bool p0 = d.cls & 1, p1 = (d.cls >> 1) & 1;
-    const uint32_t xo = d.x + (uint32_t)ebase;
-    const double2* x = sb + xo;
-    const int cls = __shfl_sync(0xffffffffu,
-                                (__any_sync(0xffffffffu, p0) ? 1 : 0) | (__any_sync(0xffffffffu, p1) ? 2 : 0), 0);
-    double are[S::NT][2], aim[S::NT][2], tl[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int st0 = warp * NSUB; st0 < nst; st0 += NC * NSUB) {
+    const double2* x[NSUB];
+    double2* o0[NSUB];
+    double2* o1[NSUB];
+    bool p0[NSUB], p1[NSUB];
+    int any = 0;
 #pragma unroll
-    for (int n = 0; n < S::NT; ++n) are[n][0] = are[n][1] = aim[n][0] = aim[n][1] = 0.0;
+    for (int u = 0; u < NSUB; ++u) {
+      const int tau = (st0 + u) * 8 + rfib;
+      const bool vrow = tau < ntot;
+      TaskRec d;
+      int ebase = 0;
+      if (vrow) {
+        d = tasks[tau / PF];
+        const int f = tau % PF;
+        ebase = (f / STR) * STR * P + f % STR;
+      } else {
+        d.x = 0;
+        d.cls = 0;
+        d.o0 = d.o1 = ~0u;
+      }
+      p0[u] = d.cls & 1;
+      p1[u] = (d.cls >> 1) & 1;
+      any |= (int)d.cls;
+      const uint32_t xo = d.x + (uint32_t)ebase;
+      x[u] = sb + xo;
+#ifdef SFT_ABL_NOSTORE  // ablation: no output stores (shared or global)
+      o0[u] = o1[u] = nullptr;
+#else
+      if (LAST) {
+        o0[u] = d.o0 != ~0u ? a.out + d.o0 + ebase : nullptr;
+        o1[u] = d.o1 != ~0u ? a.out + d.o1 + ebase : nullptr;
+      } else {
+        o0[u] = vrow ? sb + xo : nullptr;
+        o1[u] = vrow ? sb + xo + (1 << SH) * PD : nullptr;
+      }
+#endif
+    }
+    // warp-uniform union of the live child classes: k-step range
+    const int cls = __shfl_sync(0xffffffffu, __reduce_or_sync(0xffffffffu, (unsigned)any), 0);
+    double are[NSUB][S::NT][2], aim[NSUB][S::NT][2], tl[NSUB][4];
+#pragma unroll
+    for (int u = 0; u < NSUB; ++u) {
+#pragma unroll
+      for (int n = 0; n < S::NT; ++n) are[u][n][0] = are[u][n][1] = aim[u][n][0] = aim[u][n][1] = 0.0;
+      tl[u][0] = tl[u][1] = tl[u][2] = tl[u][3] = 0.0;
+    }
 #ifdef SFT_ABL_NOCOMPUTE  // ablation: no tensor-core work, everything else unchanged
     if (false)
 #else
     if (cls == 3)
 #endif
-      mma_steps<P, 0, S::NK>(op, x, off, p0, p1, are, aim, tl);
+      mma_steps<P, 0, S::NK, NSUB>(op, x, off, p0, p1, are, aim, tl);
     else if (cls == 1)
-      mma_steps<P, 0, S::K0_HI>(op, x, off, p0, p1, are, aim, tl);
+      mma_steps<P, 0, S::K0_HI, NSUB>(op, x, off, p0, p1, are, aim, tl);
     else if (cls == 2)
-      mma_steps<P, S::K1_LO, S::NK>(op, x, off, p0, p1, are, aim, tl);
-    double2* o0;
-    double2* o1;
-#ifdef SFT_ABL_NOSTORE  // ablation: no output stores (shared or global)
-    if (true) {
-      o0 = o1 = nullptr;
-    } else
-#endif
-    if (LAST) {
-      o0 = d.o0 != ~0u ? a.out + d.o0 + ebase : nullptr;
-      o1 = d.o1 != ~0u ? a.out + d.o1 + ebase : nullptr;
-    } else {
-      o0 = vrow ? sb + xo : nullptr;
-      o1 = vrow ? sb + xo + (1 << SH) * PD : nullptr;
-    }
+      mma_steps<P, S::K1_LO, S::NK, NSUB>(op, x, off, p0, p1, are, aim, tl);
 #pragma unroll
-    for (int n = 0; n < S::NT; ++n) {
-      const int m = 4 * n + c;
-      if (m < S::NM) {
-        if (o0) o0[m * STR] = make_double2(are[n][0] + aim[n][1], aim[n][0] - are[n][1]);
-        if (o1) o1[m * STR] = make_double2(are[n][0] - aim[n][1], aim[n][0] + are[n][1]);
+    for (int u = 0; u < NSUB; ++u) {
+#pragma unroll
+      for (int n = 0; n < S::NT; ++n) {
+        const int m = 4 * n + c;
+        if (m < S::NM) {
+          if (o0[u]) o0[u][m * STR] = make_double2(are[u][n][0] + aim[u][n][1], aim[u][n][0] - are[u][n][1]);
+          if (o1[u]) o1[u][m * STR] = make_double2(are[u][n][0] - aim[u][n][1], aim[u][n][0] + are[u][n][1]);
+        }
       }
     }
     if (S::TAIL) {
       // z_0 = (P.re + Q.im, P.im - Q.re), z_1 = (P.re - Q.im, P.im + Q.re) of m = P-1,
       // partial over this lane's k; transpose-reduce over the 4 lanes of the row
-      const double u0 = tl[0] + tl[3], u1 = tl[2] - tl[1], u2 = tl[0] - tl[3], u3 = tl[2] + tl[1];
       const bool odd = c & 1, hi = c & 2;
-      double va = odd ? u1 : u0, vb = odd ? u3 : u2;
-      va += __shfl_xor_sync(0xffffffffu, odd ? u0 : u1, 1);
-      vb += __shfl_xor_sync(0xffffffffu, odd ? u2 : u3, 1);
-      double w = hi ? vb : va;
-      w += __shfl_xor_sync(0xffffffffu, hi ? va : vb, 2);
-      double2* o = hi ? o1 : o0;  // lane c holds component c&1 of z_{c>>1}
-      if (o) reinterpret_cast<double*>(o + (P - 1) * STR)[c & 1] = w;
+#pragma unroll
+      for (int u = 0; u < NSUB; ++u) {
+        const double u0 = tl[u][0] + tl[u][3], u1 = tl[u][2] - tl[u][1];
+        const double u2 = tl[u][0] - tl[u][3], u3 = tl[u][2] + tl[u][1];
+        double va = odd ? u1 : u0, vb = odd ? u3 : u2;
+        va += __shfl_xor_sync(0xffffffffu, odd ? u0 : u1, 1);
+        vb += __shfl_xor_sync(0xffffffffu, odd ? u2 : u3, 1);
+        double w = hi ? vb : va;
+        w += __shfl_xor_sync(0xffffffffu, hi ? va : vb, 2);
+        double2* o = hi ? o1[u] : o0[u];  // lane c holds component c&1 of z_{c>>1}
+        if (o) reinterpret_cast<double*>(o + (P - 1) * STR)[c & 1] = w;
+      }
     }
   }
 }
@@ -622,39 +696,19 @@ __device__ __forceinline__ void load_lane_ops(LaneOps<P>& op, const double* __re
   }
 }
 
-// Warp-specialised translation kernel (default).  Warp NC is the producer: it
-// runs up to NST tiles ahead, and per tile arms full[s] with the byte count,
-// bulk-copies the tile's schedule block into the stage bookkeeping and every
-// present child array into the stage (reading the group records of its next
-// tile from HBM while it waits for a free stage).  Warps 0..NC-1 consume.
-// 2D with NST >= 3: skewed pipeline, pass 1 of tile i+1 runs before pass 0 of
-// tile i, and pass 0 waits on an mbarrier (p1done) every consumer thread
-// arrives on after its pass-1 rows, so warps do not idle at a pass barrier.
-#ifndef SFT_WS_MINB
-#define SFT_WS_MINB 1
-#endif
-template <int D, int P, int G, int NC, int NST>
-__global__ __launch_bounds__((NC + 1) * 32, SFT_WS_MINB) void k_translate_ws(TransArgs a, const double* __restrict__ frag,
-                                                                             const unsigned char* __restrict__ sched,
-                                                                             int64_t ntiles) {
+// Producer warp of the warp-specialised kernels: runs up to NST tiles ahead;
+// per tile arms full[s] with the byte count, bulk-copies the tile's schedule
+// block into blk[s] and every present child array into stage s (reading the
+// group records of its next tile from HBM while it waits for a free stage).
+template <int D, int P, int G, int NST>
+__device__ __forceinline__ void ws_producer(const TransArgs& a, const unsigned char* __restrict__ sched, int64_t ntiles,
+                                            double2* ring, unsigned char (*blk)[Sched<D, P, G>::BLK], uint64_t* full,
+                                            uint64_t* empty) {
   using SC = Sched<D, P, G>;
   constexpr int PD = Pow<P, D>::v;
   constexpr int NS = 1 << D;
   constexpr int STAGE = G * NS * PD;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  double2* ring = reinterpret_cast<double2*>(smem_raw);  // [NST][G][NS][PD]
-  __shared__ __align__(128) unsigned char blk[NST][SC::BLK];
-  __shared__ __align__(8) uint64_t full[NST], empty[NST], p1done[NST];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x < NST) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full[threadIdx.x])));
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&empty[threadIdx.x])), "r"(NC));
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&p1done[threadIdx.x])), "r"(NC * 32));
-  }
-  if (threadIdx.x == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  __syncthreads();
-  if (warp == NC) {
-    // ---------------- producer ----------------
+  const int lane = threadIdx.x & 31;
     INSTR_T0(tp0);
     int s = 0;
     uint32_t ph = 0;
@@ -713,6 +767,38 @@ __global__ __launch_bounds__((NC + 1) * 32, SFT_WS_MINB) void k_translate_ws(Tra
       }
     }
     INSTR_ADD(0, tp0);
+}
+
+// Warp-specialised translation kernel (default).  Warp NC is the producer: it
+// runs up to NST tiles ahead, and per tile arms full[s] with the byte count,
+// bulk-copies the tile's schedule block into the stage bookkeeping and every
+// present child array into the stage (reading the group records of its next
+// tile from HBM while it waits for a free stage).  Warps 0..NC-1 consume.
+// 2D with NST >= 3: skewed pipeline, pass 1 of tile i+1 runs before pass 0 of
+// tile i, and pass 0 waits on an mbarrier (p1done) every consumer thread
+// arrives on after its pass-1 rows, so warps do not idle at a pass barrier.
+template <int D, int P, int G, int NC, int NST, int MINB>
+__global__ __launch_bounds__((NC + 1) * 32, MINB) void k_translate_ws(TransArgs a, const double* __restrict__ frag,
+                                                                             const unsigned char* __restrict__ sched,
+                                                                             int64_t ntiles) {
+  using SC = Sched<D, P, G>;
+  constexpr int PD = Pow<P, D>::v;
+  constexpr int NS = 1 << D;
+  constexpr int STAGE = G * NS * PD;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double2* ring = reinterpret_cast<double2*>(smem_raw);  // [NST][G][NS][PD]
+  __shared__ __align__(128) unsigned char blk[NST][SC::BLK];
+  __shared__ __align__(8) uint64_t full[NST], empty[NST], p1done[NST];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x < NST) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full[threadIdx.x])));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&empty[threadIdx.x])), "r"(NC));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&p1done[threadIdx.x])), "r"(NC * 32));
+  }
+  if (threadIdx.x == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+  if (warp == NC) {
+    ws_producer<D, P, G, NST>(a, sched, ntiles, ring, blk, full, empty);
     return;
   }
   // ---------------- consumers ----------------
@@ -832,47 +918,6 @@ static const double* device_fragments(cudaError_t* err) {
 // ------------------------------------------------------------------------
 // FMA kernel (round-1 design, kept for ablation: SFT_TRANSLATE=fma)
 // ------------------------------------------------------------------------
-// One fiber, both outputs, children present per CLS (bit 0: beta=0, bit 1:
-// beta=1); straight-line code over all rows.  CS form with constant-bank
-// operands: z_alpha[m] = sum_beta c_{alpha beta} (RC_beta[m] . x_beta + i (2 alpha - 1) RS_beta[m] . x_beta),
-// c_{alpha,0} = 1, c_{0,1} = i, c_{1,1} = -i.
-template <int P, int CLS, class Store>
-__device__ __forceinline__ void contract_fiber(const double2 (&x0)[P], const double2 (&x1)[P], Store store) {
-#pragma unroll
-  for (int m = 0; m < P; ++m) {
-    double2 z0 = make_double2(0.0, 0.0), z1 = make_double2(0.0, 0.0);
-    if (CLS & 1) {
-      double ur = 0.0, ui = 0.0, vr = 0.0, vi = 0.0;
-#pragma unroll
-      for (int l = 0; l < P; ++l) {
-        const double cc = CT<P>::rc(0, m, l), s = CT<P>::rs(0, m, l);
-        ur = fma(cc, x0[l].x, ur);
-        ui = fma(cc, x0[l].y, ui);
-        vr = fma(s, x0[l].x, vr);
-        vi = fma(s, x0[l].y, vi);
-      }
-      z0 = make_double2(ur + vi, ui - vr);
-      z1 = make_double2(ur - vi, ui + vr);
-    }
-    if (CLS & 2) {
-      double ur = 0.0, ui = 0.0, vr = 0.0, vi = 0.0;
-#pragma unroll
-      for (int l = 0; l < P; ++l) {
-        const double cc = CT<P>::rc(1, m, l), s = CT<P>::rs(1, m, l);
-        ur = fma(cc, x1[l].x, ur);
-        ui = fma(cc, x1[l].y, ui);
-        vr = fma(s, x1[l].x, vr);
-        vi = fma(s, x1[l].y, vi);
-      }
-      z0.x -= ui - vr;
-      z0.y += ur + vi;
-      z1.x += ui + vr;
-      z1.y -= ur - vi;
-    }
-    store(m, z0, z1);
-  }
-}
-
 template <int D, int P, int G, int NT, int AX, bool LAST>
 __device__ __forceinline__ void fma_pass(const TransArgs& a, double2* __restrict__ sb, const GroupMeta* gm, int ng,
                                          TaskEntry* ent, int* cnt) {
@@ -964,16 +1009,23 @@ __global__ __launch_bounds__(NT, SFT_FMA_MINB(NT)) void k_translate_fma(TransArg
 #define SFT_WS_NC29 4
 #endif
 #ifndef SFT_WS_NST29
-#define SFT_WS_NST29 3
+#define SFT_WS_NST29 2
+#endif
+// G groups per tile, NC consumer warps, NST stages, MINB resident CTAs per SM
+// (the register cap: MINB * (NC+1) warps share the 64K registers)
+#ifndef SFT_WS_MINB29
+#define SFT_WS_MINB29 4
 #endif
 template <int D, int P>
 struct WsCfg;
-template <> struct WsCfg<2, 5> { static constexpr int G = 16, NC = 4, NST = 3; };
-template <> struct WsCfg<2, 7> { static constexpr int G = 8, NC = 4, NST = 3; };
-template <> struct WsCfg<2, 9> { static constexpr int G = SFT_WS_G29, NC = SFT_WS_NC29, NST = SFT_WS_NST29; };
-template <> struct WsCfg<3, 5> { static constexpr int G = 2, NC = 4, NST = 3; };
-template <> struct WsCfg<3, 7> { static constexpr int G = 1, NC = 4, NST = 2; };
-template <> struct WsCfg<3, 9> { static constexpr int G = 1, NC = 8, NST = 2; };
+template <> struct WsCfg<2, 5> { static constexpr int G = 16, NC = 4, NST = 3, MINB = 2; };
+template <> struct WsCfg<2, 7> { static constexpr int G = 8, NC = 4, NST = 3, MINB = 3; };
+template <> struct WsCfg<2, 9> {
+  static constexpr int G = SFT_WS_G29, NC = SFT_WS_NC29, NST = SFT_WS_NST29, MINB = SFT_WS_MINB29;
+};
+template <> struct WsCfg<3, 5> { static constexpr int G = 2, NC = 4, NST = 3, MINB = 2; };
+template <> struct WsCfg<3, 7> { static constexpr int G = 1, NC = 4, NST = 2, MINB = 2; };
+template <> struct WsCfg<3, 9> { static constexpr int G = 1, NC = 8, NST = 2, MINB = 1; };
 
 template <int D, int P>
 struct FmaCfg;
@@ -1007,16 +1059,18 @@ static TransArgs make_args(const LevelDims& L, const double2* in, double2* out) 
   return a;
 }
 
-// SFT_TRANSLATE = ws (default) | fma
+// SFT_TRANSLATE = mma (DMMA consumers, default) | fma (round-1 kernel)
 int translate_kernel_choice() {
   static int mode = -1;
   if (mode < 0) {
     const char* e = getenv("SFT_TRANSLATE");
-    mode = (e && strcmp(e, "fma") == 0) ? 1 : 0;
+    mode = 0;
+    if (e && strcmp(e, "fma") == 0) mode = 1;
   }
   return mode;
 }
 
+// groups per tile of the schedule for the selected kernel (0: no schedule)
 // resident-CTA grid size for a persistent kernel
 template <class K>
 static cudaError_t persistent_grid(K kernel, int threads, size_t smem, int* grid) {
@@ -1038,12 +1092,12 @@ static cudaError_t launch_translate_t(const sft_plan_s* Pl, const LevelDims& L, 
   TransArgs a = make_args(L, in, out);
   if (a.ngroups <= 0) return cudaSuccess;
   if (translate_kernel_choice() == 0) {
-    constexpr int G = WsCfg<D, P>::G, NC = WsCfg<D, P>::NC, NST = WsCfg<D, P>::NST;
+    constexpr int G = WsCfg<D, P>::G, NC = WsCfg<D, P>::NC, NST = WsCfg<D, P>::NST, MB = WsCfg<D, P>::MINB;
     const size_t smem = (size_t)NST * G * (1 << D) * PD * sizeof(double2);
     static int grid_max = 0;
     static const double* frag = nullptr;
     if (!grid_max) {
-      cudaError_t e = persistent_grid(k_translate_ws<D, P, G, NC, NST>, (NC + 1) * 32, smem, &grid_max);
+      cudaError_t e = persistent_grid(k_translate_ws<D, P, G, NC, NST, MB>, (NC + 1) * 32, smem, &grid_max);
       if (e != cudaSuccess) return e;
       frag = device_fragments<P>(&e);
       if (!frag) return e;
@@ -1051,7 +1105,7 @@ static cudaError_t launch_translate_t(const sft_plan_s* Pl, const LevelDims& L, 
     if (!L.sched) return cudaErrorInvalidValue;
     const int64_t ntiles = (a.ngroups + G - 1) / G;
     const int64_t grid = std::min<int64_t>(ntiles, grid_max);
-    k_translate_ws<D, P, G, NC, NST><<<(unsigned)grid, (NC + 1) * 32, smem, Pl->stream>>>(a, frag, L.sched, ntiles);
+    k_translate_ws<D, P, G, NC, NST, MB><<<(unsigned)grid, (NC + 1) * 32, smem, Pl->stream>>>(a, frag, L.sched, ntiles);
   } else {
     constexpr int G = FmaCfg<D, P>::G, NT = FmaCfg<D, P>::NT;
     const size_t smem = (size_t)G * (1 << D) * PD * sizeof(double2);
@@ -1069,25 +1123,35 @@ static cudaError_t launch_translate_t(const sft_plan_s* Pl, const LevelDims& L, 
   return cudaGetLastError();
 }
 
-template <int D, int P>
-static size_t schedule_bytes_t(const LevelDims& L) {
-  if (translate_kernel_choice() != 0) return 0;
-  constexpr int G = WsCfg<D, P>::G;
+template <int D, int P, int G>
+static size_t schedule_bytes_g(const LevelDims& L) {
   const int64_t ng = (L.b_hi - L.b_lo) * (L.ap_hi - L.ap_lo);
   if (ng <= 0) return 0;
   return (size_t)((ng + G - 1) / G) * Sched<D, P, G>::BLK;
 }
 
 template <int D, int P>
-static cudaError_t launch_schedule_t(const sft_plan_s* Pl, const LevelDims& L, unsigned char* dst) {
-  if (translate_kernel_choice() != 0) return cudaSuccess;
-  constexpr int G = WsCfg<D, P>::G;
+static size_t schedule_bytes_t(const LevelDims& L) {
+  const int mode = translate_kernel_choice();
+  if (mode == 0) return schedule_bytes_g<D, P, WsCfg<D, P>::G>(L);
+  return 0;
+}
+
+template <int D, int P, int G>
+static cudaError_t launch_schedule_g(const sft_plan_s* Pl, const LevelDims& L, unsigned char* dst) {
   TransArgs a = make_args(L, nullptr, nullptr);
   if (a.ngroups <= 0) return cudaSuccess;
   const int64_t ntiles = (a.ngroups + G - 1) / G;
   k_schedule<D, P, G><<<(unsigned)((ntiles + 3) / 4), 128, 0, Pl->stream>>>(a, dst, ntiles);
   count_launch();
   return cudaGetLastError();
+}
+
+template <int D, int P>
+static cudaError_t launch_schedule_t(const sft_plan_s* Pl, const LevelDims& L, unsigned char* dst) {
+  const int mode = translate_kernel_choice();
+  if (mode == 0) return launch_schedule_g<D, P, WsCfg<D, P>::G>(Pl, L, dst);
+  return cudaSuccess;
 }
 
 static cudaError_t schedule_bytes_d(const sft_plan_s* Pl, const LevelDims& L, size_t* r) {
