@@ -136,6 +136,13 @@ int sft_choose_partition(int L, int world, const int64_t* counts_x, const int64_
                          const int32_t* const* parent_x, const int32_t* const* parent_k, int force_sk,
                          int force_sx, int force_m, int64_t* out, int64_t* out_cost);
 
+/* Diagnostics: the tile schedule of translation level t (built by sft_plan
+ * for the translation kernel: per tile of groups, task counts, child-array
+ * sources and task records; layout in translate.cu).  *bytes = its size;
+ * if dst (host) is non-NULL the schedule is copied there (synchronises the
+ * plan stream). */
+int sft_schedule_bytes(sft_plan_t plan, int t, int64_t* bytes, void* dst);
+
 /* Number of kernels launched by this library since load (its own kernels;
  * the CUB radix-sort/scan kernels used by the tree build are not counted). */
 int sft_launch_count(int64_t* out);

@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -497,11 +498,26 @@ extern "C" int sft_plan(int dim, int64_t N, int p, const double* x, int64_t nx, 
       P->sched_off[t] = tot;
       tot += (schedule_bytes(P, apply_dims(P, t)) + 255) / 256 * 256;
     }
+    P->sched_off[L] = tot;
     if (tot > 0) {
       if (cudaMallocAsync(&P->sched, tot, s) != cudaSuccess) return bail(SFT_E_NOMEM, "schedule allocation failed");
       for (int t = 0; t < L; ++t) {
         cudaError_t ce = launch_schedule(P, apply_dims(P, t), P->sched + P->sched_off[t]);
         if (ce != cudaSuccess) return bail(SFT_E_CUDA, std::string("schedule: ") + cudaGetErrorString(ce));
+      }
+      const char* chk = getenv("SFT_CHECK_SCHED");
+      if (chk && chk[0] == '1') {
+        // debug: every level's schedule against its buffer sizes
+        for (int t = 0; t < L; ++t) {
+          const LevelDims ld = apply_dims(P, t);
+          const int64_t in_pairs = (int64_t)(P->buf_elems / PD), out_pairs = (int64_t)(P->buf_elems / PD);
+          cudaError_t ce = check_schedule(P, ld, P->sched + P->sched_off[t], in_pairs, out_pairs, P->d_err);
+          if (ce != cudaSuccess) return bail(SFT_E_CUDA, std::string("check: ") + cudaGetErrorString(ce));
+        }
+        int herr = 0;
+        cudaMemcpyAsync(&herr, P->d_err, sizeof(int), cudaMemcpyDeviceToHost, s);
+        cudaStreamSynchronize(s);
+        if (herr & 4) return bail(SFT_E_CUDA, "tile schedule failed its invariants");
       }
     }
   }
@@ -713,6 +729,17 @@ extern "C" int sft_plan_stats(sft_plan_t P, int64_t* counts_x, int64_t* counts_k
     info[5] = P->plan_ms;
     info[6] = groups;
     info[7] = bytes;
+  }
+  return SFT_OK;
+}
+
+extern "C" int sft_schedule_bytes(sft_plan_t P, int t, int64_t* bytes, void* dst) {
+  if (!P || !bytes || t < 0 || t >= P->L) return fail(SFT_E_ARG, "bad arguments");
+  const size_t n = P->sched ? P->sched_off[t + 1] - P->sched_off[t] : 0;
+  *bytes = (int64_t)n;
+  if (dst && n) {
+    CKR(cudaMemcpyAsync(dst, P->sched + P->sched_off[t], n, cudaMemcpyDeviceToHost, P->stream));
+    CKR(cudaStreamSynchronize(P->stream));
   }
   return SFT_OK;
 }

@@ -42,7 +42,7 @@ __global__ __launch_bounds__(128) void k_leaf(const double* __restrict__ k_sorte
   constexpr int PD = Pow<P, D>::v;
   constexpr int NACC = (PD + 31) / 32;
   constexpr int P1 = P - 1;
-  __shared__ double r_s[4][D][P];
+  __shared__ double r_s[4][D][P], sn_s[4][D][P];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t b = b_lo + blockIdx.x * 4 + warp;
   if (b >= b_hi) return;
@@ -58,15 +58,21 @@ __global__ __launch_bounds__(128) void k_leaf(const double* __restrict__ k_sorte
       const double kk = k_sorted[(int64_t)j * D + a];
       ssum += kk - fmin(floor(kk), (double)(N - 1));
     }
+    // r_m(s) = invD_m prod_{q != m} sin(pi (s P1 - q)/P1^2): lane (a, q) evaluates
+    // one sine, lane (a, m) then multiplies the p-1 others
     if (lane < D * P) {
-      const int a = lane / P, m = lane % P;
+      const int a = lane / P, q = lane % P;
       const double kk = k_sorted[(int64_t)j * D + a];
       const double s = kk - fmin(floor(kk), (double)(N - 1));
-      // r_m(s) = invD_m prod_{q != m} sin(pi (s P1 - q)/P1^2)
+      sn_s[warp][a][q] = sinpi((s * P1 - q) / (double)(P1 * P1));
+    }
+    __syncwarp();
+    if (lane < D * P) {
+      const int a = lane / P, m = lane % P;
       double prod = invD[m];
 #pragma unroll
       for (int q = 0; q < P; ++q)
-        if (q != m) prod *= sinpi((s * P1 - q) / (double)(P1 * P1));
+        if (q != m) prod *= sn_s[warp][a][q];
       r_s[warp][a][m] = prod;
     }
     __syncwarp();

@@ -131,6 +131,9 @@ cudaError_t launch_translate(const sft_plan_s* P, const LevelDims& L, const doub
 // tile schedule of one level (sizes and builder; 0 bytes when the kernel needs none)
 size_t schedule_bytes(const sft_plan_s* P, const LevelDims& L);
 cudaError_t launch_schedule(const sft_plan_s* P, const LevelDims& L, unsigned char* dst);
+// debug: validate a level's schedule against its input/output pair counts (sets *err bit 2)
+cudaError_t check_schedule(const sft_plan_s* P, const LevelDims& L, const unsigned char* sched, int64_t in_pairs,
+                           int64_t out_pairs, int* err);
 cudaError_t launch_final(const sft_plan_s* P, const double2* g0, double2* u, int64_t a_lo, int64_t a_hi);
 cudaError_t launch_zero(double2* p, int64_t n, cudaStream_t s);
 

@@ -420,11 +420,12 @@ struct Sched {
   }
 };
 
-// One warp per tile: task lists of pass AX for the tile's groups (lanes),
-// packed in class order with warp scans.
+// Task lists of pass AX for one tile: the tile's G groups sit in G adjacent
+// lanes (a warp holds 32/G tiles); entries packed in class order with scans
+// over the G-lane segment.
 template <int D, int P, int G, int AX, bool LAST>
-__device__ __forceinline__ void schedule_pass(const TransArgs& a, const GroupMeta& m, bool valid, int* cnt,
-                                              TaskRec* out) {
+__device__ __forceinline__ void schedule_pass(const TransArgs& a, const GroupMeta& m, bool valid, bool write_cnt,
+                                              int* cnt, TaskRec* out) {
   constexpr int PD = Pow<P, D>::v;
   constexpr int NS = 1 << D;
   constexpr int SH = D - 1 - AX;
@@ -444,7 +445,7 @@ __device__ __forceinline__ void schedule_pass(const TransArgs& a, const GroupMet
       for (int as = 0; as < (1 << (D - 1 - AX)); ++as) {
         if (!(PAs >> as & 1)) continue;
         TaskRec t;
-        t.x = (uint32_t)((lane * NS + ((bp << (D - AX)) | as)) * PD);
+        t.x = (uint32_t)(((lane % G) * NS + ((bp << (D - AX)) | as)) * PD);
         t.cls = cls;
         t.o0 = t.o1 = ~0u;
         if (LAST) {
@@ -459,19 +460,20 @@ __device__ __forceinline__ void schedule_pass(const TransArgs& a, const GroupMet
       }
     }
   }
+  const int j = lane % G;
   int o3 = c3, o1 = c1, o2 = c2;
 #pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const int t3 = __shfl_up_sync(0xffffffffu, o3, d), t1 = __shfl_up_sync(0xffffffffu, o1, d),
-              t2 = __shfl_up_sync(0xffffffffu, o2, d);
-    if (lane >= d) {
+  for (int d = 1; d < G; d <<= 1) {
+    const int t3 = __shfl_up_sync(0xffffffffu, o3, d, G), t1 = __shfl_up_sync(0xffffffffu, o1, d, G),
+              t2 = __shfl_up_sync(0xffffffffu, o2, d, G);
+    if (j >= d) {
       o3 += t3;
       o1 += t1;
       o2 += t2;
     }
   }
-  const int n3 = __shfl_sync(0xffffffffu, o3, 31), n1 = __shfl_sync(0xffffffffu, o1, 31);
-  const int n2 = __shfl_sync(0xffffffffu, o2, 31);
+  const int n3 = __shfl_sync(0xffffffffu, o3, G - 1, G), n1 = __shfl_sync(0xffffffffu, o1, G - 1, G);
+  const int n2 = __shfl_sync(0xffffffffu, o2, G - 1, G);
   o3 -= c3;
   o1 += n3 - c1;
   o2 += n3 + n1 - c2;
@@ -482,7 +484,7 @@ __device__ __forceinline__ void schedule_pass(const TransArgs& a, const GroupMet
       out[t.cls == 3 ? o3++ : (t.cls == 1 ? o1++ : o2++)] = t;
     }
   }
-  if (lane == 0) {
+  if (j == 0 && write_cnt) {
     cnt[0] = n3;
     cnt[1] = n1;
     cnt[2] = n2;
@@ -492,12 +494,16 @@ __device__ __forceinline__ void schedule_pass(const TransArgs& a, const GroupMet
 template <int D, int P, int G>
 __global__ __launch_bounds__(128) void k_schedule(TransArgs a, unsigned char* __restrict__ sched, int64_t ntiles) {
   using SC = Sched<D, P, G>;
+  static_assert(G >= 1 && G <= 32 && (G & (G - 1)) == 0, "G must be a power of two");
+  constexpr int TPW = 32 / G;  // tiles per warp
   const int lane = threadIdx.x & 31;
-  const int64_t tile = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
-  if (tile >= ntiles) return;
-  unsigned char* b = sched + tile * SC::BLK;
-  const int64_t g = tile * G + lane;
-  const bool valid = lane < G && g < a.ngroups;
+  const int64_t tile = ((int64_t)blockIdx.x * 4 + (threadIdx.x >> 5)) * TPW + lane / G;
+  const int j = lane % G;
+  if (tile - lane / G >= ntiles) return;  // whole warp out of range
+  const bool tv = tile < ntiles;
+  unsigned char* b = sched + (tv ? tile : 0) * SC::BLK;
+  const int64_t g = tile * G + j;
+  const bool valid = tv && g < a.ngroups;
   GroupMeta m;
   m.iB = m.iAp = 0;
   m.cbK = m.cbX = 0;
@@ -512,20 +518,54 @@ __global__ __launch_bounds__(128) void k_schedule(TransArgs a, unsigned char* __
     m.cbX = a.cbX[m.iAp];
     m.mA = a.mX[m.iAp];
   }
-  if (lane < G) {
+  if (tv) {
     const int64_t pin0 = ((int64_t)m.cbK - a.in_b0) * a.in_nA + (m.iAp - a.in_a0);
-    reinterpret_cast<uint2*>(b + SC::HDR)[lane] = valid ? make_uint2((uint32_t)pin0, m.mB) : make_uint2(0u, 0u);
+    reinterpret_cast<uint2*>(b + SC::HDR)[j] = valid ? make_uint2((uint32_t)pin0, m.mB) : make_uint2(0u, 0u);
   }
-  int* cnt = reinterpret_cast<int*>(b);
+  int* cnt = reinterpret_cast<int*>(b);  // written by the first lane of each valid tile only
   TaskRec* tk = reinterpret_cast<TaskRec*>(b + SC::HDR + SC::GRP);
   if constexpr (D == 2) {
-    schedule_pass<D, P, G, 1, false>(a, m, valid, cnt + 3, tk + SC::MAXT);
-    schedule_pass<D, P, G, 0, true>(a, m, valid, cnt, tk);
+    schedule_pass<D, P, G, 1, false>(a, m, valid, tv, cnt + 3, tk + SC::MAXT);
+    schedule_pass<D, P, G, 0, true>(a, m, valid, tv, cnt, tk);
   } else {
-    schedule_pass<D, P, G, 2, false>(a, m, valid, cnt + 6, tk + 2 * SC::MAXT);
-    schedule_pass<D, P, G, 1, false>(a, m, valid, cnt + 3, tk + SC::MAXT);
-    schedule_pass<D, P, G, 0, true>(a, m, valid, cnt, tk);
+    schedule_pass<D, P, G, 2, false>(a, m, valid, tv, cnt + 6, tk + 2 * SC::MAXT);
+    schedule_pass<D, P, G, 1, false>(a, m, valid, tv, cnt + 3, tk + SC::MAXT);
+    schedule_pass<D, P, G, 0, true>(a, m, valid, tv, cnt, tk);
   }
+}
+
+// Schedule invariants (debug: SFT_CHECK_SCHED=1 at plan time): one thread
+// per tile checks counts, stage offsets, classes and HBM offsets against the
+// level sizes; any violation sets *err (bit 2).
+template <int D, int P, int G>
+__global__ void k_check_schedule(TransArgs a, const unsigned char* __restrict__ sched, int64_t ntiles,
+                                 int64_t in_pairs, int64_t out_pairs, int* err) {
+  using SC = Sched<D, P, G>;
+  constexpr int PD = Pow<P, D>::v;
+  constexpr int STAGE = G * (1 << D) * PD;
+  const int64_t tile = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (tile >= ntiles) return;
+  const unsigned char* b = sched + tile * SC::BLK;
+  bool bad = false;
+  for (int j = 0; j < G; ++j) {
+    const uint2 gr = SC::grp(b)[j];
+    const int np = __popc(gr.y);
+    if (np > 0 && (int64_t)gr.x + (int64_t)(np - 1) * a.in_nA >= in_pairs) bad = true;
+  }
+  for (int ax = 0; ax < D; ++ax) {
+    const int* c = SC::cnt(b) + 3 * ax;
+    const int nt = c[0] + c[1] + c[2];
+    if (c[0] < 0 || c[1] < 0 || c[2] < 0 || nt > SC::MAXT) bad = true;
+    for (int t = 0; t < nt && t < SC::MAXT; ++t) {
+      const TaskRec r = SC::task(b, ax)[t];
+      if (r.x >= STAGE || r.cls < 1 || r.cls > 3) bad = true;
+      if (ax == 0) {
+        if (r.o0 != ~0u && (int64_t)r.o0 / PD >= out_pairs) bad = true;
+        if (r.o1 != ~0u && (int64_t)r.o1 / PD >= out_pairs) bad = true;
+      }
+    }
+  }
+  if (bad) atomicOr(err, 4);
 }
 
 // One pass of the consumers (NC warps): super-tiles of 8 fiber rows, NSUB
@@ -1142,7 +1182,8 @@ static cudaError_t launch_schedule_g(const sft_plan_s* Pl, const LevelDims& L, u
   TransArgs a = make_args(L, nullptr, nullptr);
   if (a.ngroups <= 0) return cudaSuccess;
   const int64_t ntiles = (a.ngroups + G - 1) / G;
-  k_schedule<D, P, G><<<(unsigned)((ntiles + 3) / 4), 128, 0, Pl->stream>>>(a, dst, ntiles);
+  const int64_t nwarps = (ntiles + 32 / G - 1) / (32 / G);
+  k_schedule<D, P, G><<<(unsigned)((nwarps + 3) / 4), 128, 0, Pl->stream>>>(a, dst, ntiles);
   count_launch();
   return cudaGetLastError();
 }
@@ -1156,6 +1197,25 @@ static cudaError_t launch_schedule_t(const sft_plan_s* Pl, const LevelDims& L, u
 
 static cudaError_t schedule_bytes_d(const sft_plan_s* Pl, const LevelDims& L, size_t* r) {
   SFT_DISPATCH(Pl->d, Pl->p, (*r = schedule_bytes_t<D, P>(L)));
+  return cudaSuccess;
+}
+
+template <int D, int P>
+static cudaError_t check_schedule_t(const sft_plan_s* Pl, const LevelDims& L, const unsigned char* sched,
+                                   int64_t in_pairs, int64_t out_pairs, int* err) {
+  if (translate_kernel_choice() != 0) return cudaSuccess;
+  constexpr int G = WsCfg<D, P>::G;
+  TransArgs a = make_args(L, nullptr, nullptr);
+  if (a.ngroups <= 0) return cudaSuccess;
+  const int64_t ntiles = (a.ngroups + G - 1) / G;
+  k_check_schedule<D, P, G><<<(unsigned)((ntiles + 127) / 128), 128, 0, Pl->stream>>>(a, sched, ntiles, in_pairs,
+                                                                                       out_pairs, err);
+  return cudaGetLastError();
+}
+
+cudaError_t check_schedule(const sft_plan_s* Pl, const LevelDims& L, const unsigned char* sched, int64_t in_pairs,
+                           int64_t out_pairs, int* err) {
+  SFT_DISPATCH(Pl->d, Pl->p, return (check_schedule_t<D, P>(Pl, L, sched, in_pairs, out_pairs, err)));
   return cudaSuccess;
 }
 
