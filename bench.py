@@ -125,6 +125,7 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     w = synth.make_workload(args.config)
     P = w.P
+    prec = 1 if args.precision == "f32" else 0
     x = torch.from_numpy(w.x).to(dev)
     k = torch.from_numpy(w.k).to(dev)
     f = torch.from_numpy(w.f).to(dev)
@@ -139,7 +140,7 @@ def run_ours(args):
 
     def step():
         if world == 1:
-            with sft.Plan(w.dim, w.N, w.p, x, k, stream=stream) as plan:
+            with sft.Plan(w.dim, w.N, w.p, x, k, stream=stream, precision=prec) as plan:
                 plan.apply(f, u)
         else:
             with DistPlan(w.dim, w.N, w.p, x, k, stream=stream) as dp:
@@ -172,7 +173,7 @@ def run_ours(args):
 
     # apply-only timing (plan reused) and per-kernel timing, same stream
     if world == 1:
-        plan = sft.Plan(w.dim, w.N, w.p, x, k, stream=stream)
+        plan = sft.Plan(w.dim, w.N, w.p, x, k, stream=stream, precision=prec)
         for _ in range(max(2, args.warmup)):
             plan.apply(f, u)
         apply_total, _ = timed(lambda: plan.apply(f, u), args.steps)
@@ -207,7 +208,7 @@ def run_ours(args):
 
     def step_e2e():
         if world == 1:
-            with sft.Plan(w.dim, w.N, w.p, xh, kh, stream=stream) as plan:
+            with sft.Plan(w.dim, w.N, w.p, xh, kh, stream=stream, precision=prec) as plan:
                 plan.apply(fh, uh)
         else:
             xd, kd, fd = xh.to(dev, non_blocking=True), kh.to(dev, non_blocking=True), fh.to(dev, non_blocking=True)
@@ -262,7 +263,7 @@ def run_ours(args):
             "higher_is_better": True,
             "scaling": "strong",
             "vs_baseline": None,
-            "dtype": "f64",
+            "dtype": args.precision,
             "data": "synthetic",
             "config": {"workload": f"{args.config}: {CONFIG_DESC[args.config]}", "dim": w.dim, "N": w.N, "p": w.p,
                        "nx": len(w.x), "nk": len(w.k), "P": P, "pairs_total": int(np.sum(st["pairs"])),
@@ -364,6 +365,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-targets", type=int, default=256)
+    ap.add_argument("--precision", default="f64", choices=["f64", "f32"],
+                    help="arithmetic of the level charges (f32: the optional FP32 variant, single GPU)")
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)

@@ -127,10 +127,14 @@ def _stream_handle(stream):
 class Plan:
     """sft_plan / sft_apply / sft_destroy (include/sft.h)."""
 
-    def __init__(self, dim, N, p, x, k, stream=None, rank=0, world=1, exchange_level=-1, split_k=-1, split_x=-1):
+    def __init__(self, dim, N, p, x, k, stream=None, rank=0, world=1, exchange_level=-1, split_k=-1, split_x=-1,
+                 precision=0):
+        """precision 0: FP64 charges (default); 1: the FP32 variant (single GPU;
+        f and u stay complex128 at the boundary, the level charges are complex64)."""
         L = lib()
         o = _Opts()
         L.sft_default_opts(ctypes.byref(o))
+        o.precision = int(precision)
         o.stream = _stream_handle(stream)
         o.rank, o.world = int(rank), int(world)
         o.exchange_level, o.split_k, o.split_x = int(exchange_level), int(split_k), int(split_x)

@@ -358,7 +358,8 @@ extern "C" int sft_plan(int dim, int64_t N, int p, const double* x, int64_t nx, 
   sft_opts o;
   sft_default_opts(&o);
   if (opts) o = *opts;
-  if (o.precision != 0) return fail(SFT_E_ARG, "only precision 0 (FP64) is built");
+  if (o.precision != 0 && o.precision != 1) return fail(SFT_E_ARG, "precision must be 0 (FP64) or 1 (FP32)");
+  if (o.precision == 1 && o.world != 1) return fail(SFT_E_ARG, "the FP32 variant is single-GPU (world == 1)");
   if (o.world < 1 || o.rank < 0 || o.rank >= o.world) return fail(SFT_E_ARG, "bad rank/world");
 
   sft_plan_s* P = new (std::nothrow) sft_plan_s();
@@ -373,6 +374,11 @@ extern "C" int sft_plan(int dim, int64_t N, int p, const double* x, int64_t nx, 
   P->nk = nk;
   P->rank = o.rank;
   P->world = o.world;
+  P->prec = o.precision;
+  {
+    const int64_t pd = ipow64(p, dim);
+    P->pds = (int)(P->prec == 1 ? pd + (pd & 1) : pd);  // FP32: 16-byte multiple per array
+  }
   P->stream = (cudaStream_t)o.stream;
   cudaStream_t s = P->stream;
 
@@ -475,11 +481,11 @@ extern "C" int sft_plan(int dim, int64_t N, int p, const double* x, int64_t nx, 
     int64_t mx = 0;
     for (int t = m; t <= L; ++t) mx = std::max(mx, (P->k_rng[t].hi - P->k_rng[t].lo) * P->X.counts[L - t]);
     for (int t = 0; t <= m; ++t) mx = std::max(mx, P->K.counts[t] * (P->x_rng[L - t].hi - P->x_rng[L - t].lo));
-    P->buf_elems = (size_t)mx * PD;
+    P->buf_elems = (size_t)mx * P->pds;
   } else {
     int64_t mx = 0;
     for (int t = 0; t <= L; ++t) mx = std::max(mx, P->K.counts[t] * P->X.counts[L - t]);
-    P->buf_elems = (size_t)mx * PD;
+    P->buf_elems = (size_t)mx * P->pds;
     P->k_rng.assign(L + 1, LevelRange());
     P->x_rng.assign(L + 1, LevelRange());
     for (int l = 0; l <= L; ++l) {
@@ -488,7 +494,8 @@ extern "C" int sft_plan(int dim, int64_t N, int p, const double* x, int64_t nx, 
     }
   }
   for (int i = 0; i < 2; ++i)
-    if (cudaMallocAsync(&P->buf[i], P->buf_elems * sizeof(double2), s) != cudaSuccess)
+    if (cudaMallocAsync(&P->buf[i], P->buf_elems * (P->prec == 1 ? sizeof(float2) : sizeof(double2)), s) !=
+        cudaSuccess)
       return bail(SFT_E_NOMEM, "level buffer allocation failed");
   // tile schedules of every translation level (kernel-side task lists)
   {
@@ -510,7 +517,7 @@ extern "C" int sft_plan(int dim, int64_t N, int p, const double* x, int64_t nx, 
         // debug: every level's schedule against its buffer sizes
         for (int t = 0; t < L; ++t) {
           const LevelDims ld = apply_dims(P, t);
-          const int64_t in_pairs = (int64_t)(P->buf_elems / PD), out_pairs = (int64_t)(P->buf_elems / PD);
+          const int64_t in_pairs = (int64_t)(P->buf_elems / P->pds), out_pairs = in_pairs;
           cudaError_t ce = check_schedule(P, ld, P->sched + P->sched_off[t], in_pairs, out_pairs, P->d_err);
           if (ce != cudaSuccess) return bail(SFT_E_CUDA, std::string("check: ") + cudaGetErrorString(ce));
         }
@@ -718,14 +725,15 @@ extern "C" int sft_plan_stats(sft_plan_t P, int64_t* counts_x, int64_t* counts_k
   }
   for (int t = 0; t < L; ++t) {
     groups += (double)P->K.counts[t] * P->X.counts[L - t - 1];
-    bytes += 16.0 * PD * ((double)P->K.counts[t] * P->X.counts[L - t] + (double)P->K.counts[t + 1] * P->X.counts[L - t - 1]);
+    bytes += (P->prec == 1 ? 8.0 : 16.0) * PD *
+             ((double)P->K.counts[t] * P->X.counts[L - t] + (double)P->K.counts[t + 1] * P->X.counts[L - t - 1]);
   }
   if (info) {
     info[0] = L;
     info[1] = (double)PD;
     info[2] = (double)P->nx;
     info[3] = (double)P->nk;
-    info[4] = 2.0 * P->buf_elems * sizeof(double2);
+    info[4] = 2.0 * P->buf_elems * (P->prec == 1 ? sizeof(float2) : sizeof(double2));
     info[5] = P->plan_ms;
     info[6] = groups;
     info[7] = bytes;

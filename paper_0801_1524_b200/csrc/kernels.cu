@@ -34,11 +34,11 @@ __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
 // ------------------------------------------------------------------------
 // K2: leaf kernel, one warp per leaf B of T_K (h-representation)
 // ------------------------------------------------------------------------
-template <int D, int P>
+template <int D, int P, typename T2, int PS>
 __global__ __launch_bounds__(128) void k_leaf(const double* __restrict__ k_sorted, const int32_t* __restrict__ perm,
                                               const int32_t* __restrict__ first_pt,
                                               const double2* __restrict__ f, const double* __restrict__ invD,
-                                              double2* __restrict__ out, int64_t b_lo, int64_t b_hi, int64_t N) {
+                                              T2* __restrict__ out, int64_t b_lo, int64_t b_hi, int64_t N) {
   constexpr int PD = Pow<P, D>::v;
   constexpr int NACC = (PD + 31) / 32;
   constexpr int P1 = P - 1;
@@ -96,21 +96,26 @@ __global__ __launch_bounds__(128) void k_leaf(const double* __restrict__ k_sorte
     }
     __syncwarp();
   }
-  double2* o = out + (b - b_lo) * (int64_t)PD;
+  T2* o = out + (b - b_lo) * (int64_t)PS;
 #pragma unroll
   for (int i = 0; i < NACC; ++i) {
     const int e = lane + 32 * i;
-    if (e < PD) o[e] = acc[i];
+    if (e < PD) {
+      T2 v;
+      v.x = acc[i].x;
+      v.y = acc[i].y;
+      o[e] = v;
+    }
   }
 }
 
 // ------------------------------------------------------------------------
 // K4: final kernel, one warp per leaf A of T_X (h-representation)
 // ------------------------------------------------------------------------
-template <int D, int P>
+template <int D, int P, typename T2, int PS>
 __global__ __launch_bounds__(128) void k_final(const double* __restrict__ x_sorted, const int32_t* __restrict__ perm,
                                                const int32_t* __restrict__ first_pt,
-                                               const double2* __restrict__ h0, double2* __restrict__ u,
+                                               const T2* __restrict__ h0, double2* __restrict__ u,
                                                int64_t a_lo, int64_t a_hi, int64_t N) {
   constexpr int PD = Pow<P, D>::v;
   constexpr int NACC = (PD + 31) / 32;
@@ -119,12 +124,16 @@ __global__ __launch_bounds__(128) void k_final(const double* __restrict__ x_sort
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t A = a_lo + blockIdx.x * 4 + warp;
   if (A >= a_hi) return;
-  const double2* h = h0 + (A - a_lo) * (int64_t)PD;
+  const T2* h = h0 + (A - a_lo) * (int64_t)PS;
   double2 hr[NACC];
 #pragma unroll
   for (int i = 0; i < NACC; ++i) {
     const int e = lane + 32 * i;
-    hr[i] = e < PD ? h[e] : make_double2(0.0, 0.0);
+    hr[i] = make_double2(0.0, 0.0);
+    if (e < PD) {
+      const T2 v = h[e];
+      hr[i] = make_double2(v.x, v.y);
+    }
   }
   const int j0 = first_pt[A], j1 = first_pt[A + 1];
   for (int j = j0; j < j1; ++j) {
@@ -172,22 +181,36 @@ __global__ void k_zero(double2* p, int64_t n) {
 // launchers
 // ------------------------------------------------------------------------
 
-cudaError_t launch_leaf(const sft_plan_s* Pl, const double2* f, double2* out, int64_t b_lo, int64_t b_hi) {
+cudaError_t launch_leaf(const sft_plan_s* Pl, const double2* f, void* out, int64_t b_lo, int64_t b_hi) {
   if (b_hi <= b_lo) return cudaSuccess;
   const unsigned nb = (unsigned)((b_hi - b_lo + 3) / 4);
-  SFT_DISPATCH(Pl->d, Pl->p,
-               (k_leaf<D, P><<<nb, 128, 0, Pl->stream>>>(Pl->K.pts_sorted, Pl->K.perm, Pl->K.first_pt, f, Pl->tab->leaf_invD, out, b_lo,
-                                                         b_hi, Pl->N)));
+  if (Pl->prec == 1) {
+    SFT_DISPATCH(Pl->d, Pl->p,
+                 (k_leaf<D, P, float2, Pow<P, D>::v + (Pow<P, D>::v & 1)><<<nb, 128, 0, Pl->stream>>>(
+                     Pl->K.pts_sorted, Pl->K.perm, Pl->K.first_pt, f, Pl->tab->leaf_invD, (float2*)out, b_lo, b_hi,
+                     Pl->N)));
+  } else {
+    SFT_DISPATCH(Pl->d, Pl->p,
+                 (k_leaf<D, P, double2, Pow<P, D>::v><<<nb, 128, 0, Pl->stream>>>(
+                     Pl->K.pts_sorted, Pl->K.perm, Pl->K.first_pt, f, Pl->tab->leaf_invD, (double2*)out, b_lo, b_hi,
+                     Pl->N)));
+  }
   count_launch();
   return cudaGetLastError();
 }
 
-cudaError_t launch_final(const sft_plan_s* Pl, const double2* h0, double2* u, int64_t a_lo, int64_t a_hi) {
+cudaError_t launch_final(const sft_plan_s* Pl, const void* h0, double2* u, int64_t a_lo, int64_t a_hi) {
   if (a_hi <= a_lo) return cudaSuccess;
   const unsigned nb = (unsigned)((a_hi - a_lo + 3) / 4);
-  SFT_DISPATCH(Pl->d, Pl->p,
-               (k_final<D, P><<<nb, 128, 0, Pl->stream>>>(Pl->X.pts_sorted, Pl->X.perm, Pl->X.first_pt, h0, u, a_lo,
-                                                          a_hi, Pl->N)));
+  if (Pl->prec == 1) {
+    SFT_DISPATCH(Pl->d, Pl->p,
+                 (k_final<D, P, float2, Pow<P, D>::v + (Pow<P, D>::v & 1)><<<nb, 128, 0, Pl->stream>>>(
+                     Pl->X.pts_sorted, Pl->X.perm, Pl->X.first_pt, (const float2*)h0, u, a_lo, a_hi, Pl->N)));
+  } else {
+    SFT_DISPATCH(Pl->d, Pl->p,
+                 (k_final<D, P, double2, Pow<P, D>::v><<<nb, 128, 0, Pl->stream>>>(
+                     Pl->X.pts_sorted, Pl->X.perm, Pl->X.first_pt, (const double2*)h0, u, a_lo, a_hi, Pl->N)));
+  }
   count_launch();
   return cudaGetLastError();
 }

@@ -74,10 +74,12 @@ struct sft_plan_s {
   int d = 0, p = 0, L = 0;
   int64_t N = 0, nx = 0, nk = 0;
   int rank = 0, world = 1;
+  int prec = 0;  // 0 = FP64 charges (complex128), 1 = FP32 charges (complex64)
+  int pds = 0;   // stride (complex elements) of one pair array in the level buffers
   cudaStream_t stream = nullptr;
   sft::Tree X, K;
   const sft::DeviceTables* tab = nullptr;
-  // two live level buffers, complex128
+  // two live level buffers, complex128 (or complex64 if prec == 1)
   double2* buf[2] = {nullptr, nullptr};
   size_t buf_elems = 0;
   // staging for host pointers
@@ -126,15 +128,16 @@ struct LevelDims {
   const unsigned char* sched = nullptr;  // tile schedule of this level (translate.cu, built by sft_plan)
 };
 
-cudaError_t launch_leaf(const sft_plan_s* P, const double2* f, double2* out, int64_t b_lo, int64_t b_hi);
-cudaError_t launch_translate(const sft_plan_s* P, const LevelDims& L, const double2* in, double2* out);
+// level buffers are void*: complex128 (prec 0) or complex64 (prec 1) pair arrays of stride P->pds
+cudaError_t launch_leaf(const sft_plan_s* P, const double2* f, void* out, int64_t b_lo, int64_t b_hi);
+cudaError_t launch_translate(const sft_plan_s* P, const LevelDims& L, const void* in, void* out);
 // tile schedule of one level (sizes and builder; 0 bytes when the kernel needs none)
 size_t schedule_bytes(const sft_plan_s* P, const LevelDims& L);
 cudaError_t launch_schedule(const sft_plan_s* P, const LevelDims& L, unsigned char* dst);
 // debug: validate a level's schedule against its input/output pair counts (sets *err bit 2)
 cudaError_t check_schedule(const sft_plan_s* P, const LevelDims& L, const unsigned char* sched, int64_t in_pairs,
                            int64_t out_pairs, int* err);
-cudaError_t launch_final(const sft_plan_s* P, const double2* g0, double2* u, int64_t a_lo, int64_t a_hi);
+cudaError_t launch_final(const sft_plan_s* P, const void* g0, double2* u, int64_t a_lo, int64_t a_hi);
 cudaError_t launch_zero(double2* p, int64_t n, cudaStream_t s);
 
 template <int B, int E>

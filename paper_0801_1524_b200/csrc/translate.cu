@@ -69,9 +69,54 @@ struct CT<9> {
   __device__ __forceinline__ static double rs(int b, int m, int l) { return c_RS9[b][m][l]; }
 };
 
+// FP32 variant: the same operators rounded to float
+__constant__ float c_RC5f[2][5][5], c_RS5f[2][5][5];
+__constant__ float c_RC7f[2][7][7], c_RS7f[2][7][7];
+__constant__ float c_RC9f[2][9][9], c_RS9f[2][9][9];
+
+template <int P>
+struct CTf;
+template <>
+struct CTf<5> {
+  __device__ __forceinline__ static float rc(int b, int m, int l) { return c_RC5f[b][m][l]; }
+  __device__ __forceinline__ static float rs(int b, int m, int l) { return c_RS5f[b][m][l]; }
+};
+template <>
+struct CTf<7> {
+  __device__ __forceinline__ static float rc(int b, int m, int l) { return c_RC7f[b][m][l]; }
+  __device__ __forceinline__ static float rs(int b, int m, int l) { return c_RS7f[b][m][l]; }
+};
+template <>
+struct CTf<9> {
+  __device__ __forceinline__ static float rc(int b, int m, int l) { return c_RC9f[b][m][l]; }
+  __device__ __forceinline__ static float rs(int b, int m, int l) { return c_RS9f[b][m][l]; }
+};
+
+static cudaError_t upload_const_tables_f(int p, const double* RC, const double* RS) {
+  float rc[2 * 9 * 9], rs[2 * 9 * 9];
+  for (int i = 0; i < 2 * p * p; ++i) {
+    rc[i] = (float)RC[i];
+    rs[i] = (float)RS[i];
+  }
+  const size_t n2 = sizeof(float) * 2 * p * p;
+  cudaError_t e = cudaErrorInvalidValue;
+  if (p == 5) {
+    if ((e = cudaMemcpyToSymbol(c_RC5f, rc, n2)) != cudaSuccess) return e;
+    e = cudaMemcpyToSymbol(c_RS5f, rs, n2);
+  } else if (p == 7) {
+    if ((e = cudaMemcpyToSymbol(c_RC7f, rc, n2)) != cudaSuccess) return e;
+    e = cudaMemcpyToSymbol(c_RS7f, rs, n2);
+  } else if (p == 9) {
+    if ((e = cudaMemcpyToSymbol(c_RC9f, rc, n2)) != cudaSuccess) return e;
+    e = cudaMemcpyToSymbol(c_RS9f, rs, n2);
+  }
+  return e;
+}
+
 cudaError_t upload_const_tables(int p, const double* RC, const double* RS, const double* /*invD*/) {
   const size_t n2 = sizeof(double) * 2 * p * p;
-  cudaError_t e = cudaErrorInvalidValue;
+  cudaError_t e = upload_const_tables_f(p, RC, RS);
+  if (e != cudaSuccess) return e;
   if (p == 5) {
     if ((e = cudaMemcpyToSymbol(c_RC5, RC, n2)) != cudaSuccess) return e;
     e = cudaMemcpyToSymbol(c_RS5, RS, n2);
@@ -348,35 +393,40 @@ __device__ __forceinline__ void mma_steps(const LaneOps<P>& op, const double2* c
 
 // One fiber, both outputs, children present per CLS (bit 0: beta=0, bit 1:
 // beta=1); straight-line code over all rows.  CS form with constant-bank
-// operands: z_alpha[m] = sum_beta c_{alpha beta} (RC_beta[m] . x_beta + i (2 alpha - 1) RS_beta[m] . x_beta),
+// operands (OP = CT<P> for FP64, CTf<P> for FP32):
+//   z_alpha[m] = sum_beta c_{alpha beta} (RC_beta[m] . x_beta + i (2 alpha - 1) RS_beta[m] . x_beta),
 // c_{alpha,0} = 1, c_{0,1} = i, c_{1,1} = -i.
-template <int P, int CLS, class Store>
-__device__ __forceinline__ void contract_fiber(const double2 (&x0)[P], const double2 (&x1)[P], Store store) {
+template <typename T2, class OP, int P, int CLS, class Store>
+__device__ __forceinline__ void contract_fiber_t(const T2 (&x0)[P], const T2 (&x1)[P], Store store) {
+  using T = decltype(x0[0].x);
 #pragma unroll
   for (int m = 0; m < P; ++m) {
-    double2 z0 = make_double2(0.0, 0.0), z1 = make_double2(0.0, 0.0);
+    T2 z0, z1;
+    z0.x = z0.y = z1.x = z1.y = T(0);
     if (CLS & 1) {
-      double ur = 0.0, ui = 0.0, vr = 0.0, vi = 0.0;
+      T ur = 0, ui = 0, vr = 0, vi = 0;
 #pragma unroll
       for (int l = 0; l < P; ++l) {
-        const double cc = CT<P>::rc(0, m, l), s = CT<P>::rs(0, m, l);
+        const T cc = OP::rc(0, m, l), sn = OP::rs(0, m, l);
         ur = fma(cc, x0[l].x, ur);
         ui = fma(cc, x0[l].y, ui);
-        vr = fma(s, x0[l].x, vr);
-        vi = fma(s, x0[l].y, vi);
+        vr = fma(sn, x0[l].x, vr);
+        vi = fma(sn, x0[l].y, vi);
       }
-      z0 = make_double2(ur + vi, ui - vr);
-      z1 = make_double2(ur - vi, ui + vr);
+      z0.x = ur + vi;
+      z0.y = ui - vr;
+      z1.x = ur - vi;
+      z1.y = ui + vr;
     }
     if (CLS & 2) {
-      double ur = 0.0, ui = 0.0, vr = 0.0, vi = 0.0;
+      T ur = 0, ui = 0, vr = 0, vi = 0;
 #pragma unroll
       for (int l = 0; l < P; ++l) {
-        const double cc = CT<P>::rc(1, m, l), s = CT<P>::rs(1, m, l);
+        const T cc = OP::rc(1, m, l), sn = OP::rs(1, m, l);
         ur = fma(cc, x1[l].x, ur);
         ui = fma(cc, x1[l].y, ui);
-        vr = fma(s, x1[l].x, vr);
-        vi = fma(s, x1[l].y, vi);
+        vr = fma(sn, x1[l].x, vr);
+        vi = fma(sn, x1[l].y, vi);
       }
       z0.x -= ui - vr;
       z0.y += ur + vi;
@@ -385,6 +435,11 @@ __device__ __forceinline__ void contract_fiber(const double2 (&x0)[P], const dou
     }
     store(m, z0, z1);
   }
+}
+
+template <int P, int CLS, class Store>
+__device__ __forceinline__ void contract_fiber(const double2 (&x0)[P], const double2 (&x1)[P], Store store) {
+  contract_fiber_t<double2, CT<P>, P, CLS>(x0, x1, store);
 }
 
 // ------------------------------------------------------------------------
@@ -423,10 +478,10 @@ struct Sched {
 // Task lists of pass AX for one tile: the tile's G groups sit in G adjacent
 // lanes (a warp holds 32/G tiles); entries packed in class order with scans
 // over the G-lane segment.
-template <int D, int P, int G, int AX, bool LAST>
+template <int D, int P, int G, int PS, int AX, bool LAST>
 __device__ __forceinline__ void schedule_pass(const TransArgs& a, const GroupMeta& m, bool valid, bool write_cnt,
                                               int* cnt, TaskRec* out) {
-  constexpr int PD = Pow<P, D>::v;
+  constexpr int PD = PS;  // offsets in units of the array stride
   constexpr int NS = 1 << D;
   constexpr int SH = D - 1 - AX;
   constexpr int NE = 1 << (D - 1);
@@ -491,7 +546,7 @@ __device__ __forceinline__ void schedule_pass(const TransArgs& a, const GroupMet
   }
 }
 
-template <int D, int P, int G>
+template <int D, int P, int G, int PS>
 __global__ __launch_bounds__(128) void k_schedule(TransArgs a, unsigned char* __restrict__ sched, int64_t ntiles) {
   using SC = Sched<D, P, G>;
   static_assert(G >= 1 && G <= 32 && (G & (G - 1)) == 0, "G must be a power of two");
@@ -525,12 +580,12 @@ __global__ __launch_bounds__(128) void k_schedule(TransArgs a, unsigned char* __
   int* cnt = reinterpret_cast<int*>(b);  // written by the first lane of each valid tile only
   TaskRec* tk = reinterpret_cast<TaskRec*>(b + SC::HDR + SC::GRP);
   if constexpr (D == 2) {
-    schedule_pass<D, P, G, 1, false>(a, m, valid, tv, cnt + 3, tk + SC::MAXT);
-    schedule_pass<D, P, G, 0, true>(a, m, valid, tv, cnt, tk);
+    schedule_pass<D, P, G, PS, 1, false>(a, m, valid, tv, cnt + 3, tk + SC::MAXT);
+    schedule_pass<D, P, G, PS, 0, true>(a, m, valid, tv, cnt, tk);
   } else {
-    schedule_pass<D, P, G, 2, false>(a, m, valid, tv, cnt + 6, tk + 2 * SC::MAXT);
-    schedule_pass<D, P, G, 1, false>(a, m, valid, tv, cnt + 3, tk + SC::MAXT);
-    schedule_pass<D, P, G, 0, true>(a, m, valid, tv, cnt, tk);
+    schedule_pass<D, P, G, PS, 2, false>(a, m, valid, tv, cnt + 6, tk + 2 * SC::MAXT);
+    schedule_pass<D, P, G, PS, 1, false>(a, m, valid, tv, cnt + 3, tk + SC::MAXT);
+    schedule_pass<D, P, G, PS, 0, true>(a, m, valid, tv, cnt, tk);
   }
 }
 
@@ -740,12 +795,12 @@ __device__ __forceinline__ void load_lane_ops(LaneOps<P>& op, const double* __re
 // per tile arms full[s] with the byte count, bulk-copies the tile's schedule
 // block into blk[s] and every present child array into stage s (reading the
 // group records of its next tile from HBM while it waits for a free stage).
-template <int D, int P, int G, int NST>
+template <int D, int P, int G, int NST, typename E = double2, int PS = Pow<P, D>::v>
 __device__ __forceinline__ void ws_producer(const TransArgs& a, const unsigned char* __restrict__ sched, int64_t ntiles,
-                                            double2* ring, unsigned char (*blk)[Sched<D, P, G>::BLK], uint64_t* full,
+                                            E* ring, unsigned char (*blk)[Sched<D, P, G>::BLK], uint64_t* full,
                                             uint64_t* empty) {
   using SC = Sched<D, P, G>;
-  constexpr int PD = Pow<P, D>::v;
+  constexpr int PD = PS;  // stage and HBM arrays have stride PS elements of type E
   constexpr int NS = 1 << D;
   constexpr int STAGE = G * NS * PD;
   const int lane = threadIdx.x & 31;
@@ -764,10 +819,10 @@ __device__ __forceinline__ void ws_producer(const TransArgs& a, const unsigned c
       if (i >= NST) mbar_wait_sleep(smem_u32(&empty[s]), ph ^ 1u);
       INSTR_ADD(1, tw0);
       INSTR_T0(tb0);
-      uint32_t nbytes = __popc(gr.y) * PD * (uint32_t)sizeof(double2);
+      uint32_t nbytes = __popc(gr.y) * PD * (uint32_t)sizeof(E);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) nbytes += __shfl_xor_sync(0xffffffffu, nbytes, o);
-      double2* sb = ring + s * STAGE;
+      E* sb = ring + s * STAGE;
       if (lane == 0) {
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&full[s])),
                      "r"(nbytes + (uint32_t)SC::BLK)
@@ -789,12 +844,12 @@ __device__ __forceinline__ void ws_producer(const TransArgs& a, const unsigned c
         asm volatile(
             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                 smem_u32(sb + ((int64_t)lane * NS + c) * PD)),
-            "l"(a.in + pin * PD), "r"((uint32_t)(PD * sizeof(double2))), "r"(smem_u32(&full[s]))
+            "l"(reinterpret_cast<const E*>(a.in) + pin * PD), "r"((uint32_t)(PD * sizeof(E))), "r"(smem_u32(&full[s]))
             : "memory");
 #else
         (void)pin;
         asm volatile("mbarrier.complete_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&full[s])),
-                     "r"((uint32_t)(PD * sizeof(double2)))
+                     "r"((uint32_t)(PD * sizeof(E)))
                      : "memory");
 #endif
       }
@@ -886,9 +941,15 @@ __global__ __launch_bounds__((NC + 1) * 32, MINB) void k_translate_ws(TransArgs 
       INSTR_ADD(4, tf0);
       double2* sb = ring + s * STAGE;
       if constexpr (D == 2) {
+        INSTR_T0(t1);
         consumer_pass<D, P, G, NC, 1, false>(a, sb, blk[s], op);
+        INSTR_ADD(5, t1);
+        INSTR_T0(t2);
         consumer_sync<NC * 32>();
+        INSTR_ADD(6, t2);
+        INSTR_T0(t3);
         consumer_pass<D, P, G, NC, 0, true>(a, sb, blk[s], op);
+        INSTR_ADD(7, t3);
       } else {
         consumer_pass<D, P, G, NC, 2, false>(a, sb, blk[s], op);
         consumer_sync<NC * 32>();
@@ -906,6 +967,155 @@ __global__ __launch_bounds__((NC + 1) * 32, MINB) void k_translate_ws(TransArgs 
     }
   }
   INSTR_ADD(3, tc0);
+}
+
+// ------------------------------------------------------------------------
+// FP32 variant (opts.precision = 1): same producer / stage ring / schedule,
+// FFMA consumers, one thread per fiber task, constant-bank float operators.
+// Pair arrays have stride PS = p^d rounded up to even (16-byte bulk copies).
+// ------------------------------------------------------------------------
+template <int D, int P>
+struct F32 {
+  static constexpr int PD = Pow<P, D>::v;
+  static constexpr int PS = PD + (PD & 1);
+};
+
+// One pass: chunk j (32 fibers) of this pass goes to consumer warp (base + j)
+// mod NC, `base` running over the whole sequence of passes so that warps
+// stay balanced however few fibers a pass has.  Returns the next base.
+template <int D, int P, int G, int NC, int AX, bool LAST>
+__device__ __noinline__ int f32_consumer_pass(float2* __restrict__ out, float2* __restrict__ sb,
+                                             const unsigned char* __restrict__ blk, int base, int warp) {
+  using SC = Sched<D, P, G>;
+  constexpr int PS = F32<D, P>::PS;
+  constexpr int PF = Pow<P, D>::v / P;
+  constexpr int STR = Pow<P, D - 1 - AX>::v;
+  constexpr int SH = D - 1 - AX;
+  const int* cnt = SC::cnt(blk) + 3 * AX;
+  const TaskRec* tasks = SC::task(blk, AX);
+  const int ntot = (cnt[0] + cnt[1] + cnt[2]) * PF;
+  const int nch = (ntot + 31) >> 5;
+  const int lane = threadIdx.x & 31;
+  for (int j = (warp - base % NC + NC) % NC; j < nch; j += NC) {
+    const int tau = j * 32 + lane;
+    if (tau < ntot) {
+      const TaskRec te = tasks[tau / PF];
+      const int f = tau % PF;
+      const int ebase = (f / STR) * STR * P + f % STR;
+      float2* s0 = sb + te.x + ebase;
+      float2* s1 = s0 + (1 << SH) * PS;
+      float2* o0;
+      float2* o1;
+      if (!LAST) {
+        o0 = s0;
+        o1 = s1;
+      } else {
+        o0 = te.o0 != ~0u ? out + te.o0 + ebase : nullptr;
+        o1 = te.o1 != ~0u ? out + te.o1 + ebase : nullptr;
+      }
+      auto store = [&](int m, float2 z0, float2 z1) {
+        if (o0) o0[m * STR] = z0;
+        if (o1) o1[m * STR] = z1;
+      };
+      float2 x0[P], x1[P];
+      if (te.cls == 3) {
+#pragma unroll
+        for (int l = 0; l < P; ++l) {
+          x0[l] = s0[l * STR];
+          x1[l] = s1[l * STR];
+        }
+        contract_fiber_t<float2, CTf<P>, P, 3>(x0, x1, store);
+      } else if (te.cls == 1) {
+#pragma unroll
+        for (int l = 0; l < P; ++l) x0[l] = s0[l * STR];
+        contract_fiber_t<float2, CTf<P>, P, 1>(x0, x1, store);
+      } else {
+#pragma unroll
+        for (int l = 0; l < P; ++l) x1[l] = s1[l * STR];
+        contract_fiber_t<float2, CTf<P>, P, 2>(x0, x1, store);
+      }
+    }
+  }
+  return base + nch;
+}
+
+template <int D, int P, int G, int NC, int NST, int MINB>
+__global__ __launch_bounds__((NC + 1) * 32, MINB) void k_translate_f32(TransArgs a, const unsigned char* __restrict__ sched,
+                                                                      int64_t ntiles) {
+  using SC = Sched<D, P, G>;
+  constexpr int PS = F32<D, P>::PS;
+  constexpr int NS = 1 << D;
+  constexpr int STAGE = G * NS * PS;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float2* ring = reinterpret_cast<float2*>(smem_raw);  // [NST][G][NS][PS]
+  __shared__ __align__(128) unsigned char blk[NST][SC::BLK];
+  __shared__ __align__(8) uint64_t full[NST], empty[NST], p1done[NST];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x < NST) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full[threadIdx.x])));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&empty[threadIdx.x])), "r"(NC));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&p1done[threadIdx.x])), "r"(NC * 32));
+  }
+  if (threadIdx.x == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+  if (warp == NC) {
+    ws_producer<D, P, G, NST, float2, PS>(a, sched, ntiles, ring, blk, full, empty);
+    return;
+  }
+  float2* out = reinterpret_cast<float2*>(a.out);
+  int s = 0, base = 0;
+  uint32_t ph = 0;
+  auto release = [&](int st) {
+    __syncwarp();
+    if (lane == 0)
+      asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[st])) : "memory");
+  };
+  if constexpr (D == 2 && NST >= 3) {
+    // step k: pass 1 of this CTA's tile k (if any), then pass 0 of tile k-1
+    int sp = 0;
+    uint32_t php = 0;
+    for (int64_t k = 0;; ++k) {
+      const int64_t t1 = blockIdx.x + k * (int64_t)gridDim.x;
+      if (k > 0 && t1 - gridDim.x >= ntiles) break;
+      if (t1 < ntiles) {
+        mbar_wait(smem_u32(&full[s]), ph);
+        base = f32_consumer_pass<D, P, G, NC, 1, false>(out, ring + s * STAGE, blk[s], base, warp);
+        asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&p1done[s])) : "memory");
+      }
+      if (k > 0) {
+        mbar_wait(smem_u32(&p1done[sp]), php);
+        base = f32_consumer_pass<D, P, G, NC, 0, true>(out, ring + sp * STAGE, blk[sp], base, warp);
+        release(sp);
+      }
+      sp = s;
+      php = ph;
+      if (++s == NST) {
+        s = 0;
+        ph ^= 1u;
+      }
+    }
+  } else {
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      mbar_wait(smem_u32(&full[s]), ph);
+      float2* sb = ring + s * STAGE;
+      if constexpr (D == 2) {
+        base = f32_consumer_pass<D, P, G, NC, 1, false>(out, sb, blk[s], base, warp);
+        consumer_sync<NC * 32>();
+        base = f32_consumer_pass<D, P, G, NC, 0, true>(out, sb, blk[s], base, warp);
+      } else {
+        base = f32_consumer_pass<D, P, G, NC, 2, false>(out, sb, blk[s], base, warp);
+        consumer_sync<NC * 32>();
+        base = f32_consumer_pass<D, P, G, NC, 1, false>(out, sb, blk[s], base, warp);
+        consumer_sync<NC * 32>();
+        base = f32_consumer_pass<D, P, G, NC, 0, true>(out, sb, blk[s], base, warp);
+      }
+      release(s);
+      if (++s == NST) {
+        s = 0;
+        ph ^= 1u;
+      }
+    }
+  }
 }
 
 template <int P>
@@ -1067,6 +1277,16 @@ template <> struct WsCfg<3, 5> { static constexpr int G = 2, NC = 4, NST = 3, MI
 template <> struct WsCfg<3, 7> { static constexpr int G = 1, NC = 4, NST = 2, MINB = 2; };
 template <> struct WsCfg<3, 9> { static constexpr int G = 1, NC = 8, NST = 2, MINB = 1; };
 
+// FP32 kernel: G groups per tile, NC FFMA consumer warps, NST stages, MINB CTAs/SM
+template <int D, int P>
+struct F32Cfg;
+template <> struct F32Cfg<2, 5> { static constexpr int G = 32, NC = 8, NST = 3, MINB = 2; };
+template <> struct F32Cfg<2, 7> { static constexpr int G = 16, NC = 8, NST = 3, MINB = 2; };
+template <> struct F32Cfg<2, 9> { static constexpr int G = 8, NC = 8, NST = 3, MINB = 2; };
+template <> struct F32Cfg<3, 5> { static constexpr int G = 4, NC = 8, NST = 3, MINB = 2; };
+template <> struct F32Cfg<3, 7> { static constexpr int G = 1, NC = 8, NST = 3, MINB = 2; };
+template <> struct F32Cfg<3, 9> { static constexpr int G = 1, NC = 8, NST = 2, MINB = 1; };
+
 template <int D, int P>
 struct FmaCfg;
 template <> struct FmaCfg<2, 5> { static constexpr int G = 16, NT = 128; };
@@ -1127,11 +1347,23 @@ static cudaError_t persistent_grid(K kernel, int threads, size_t smem, int* grid
 }
 
 template <int D, int P>
-static cudaError_t launch_translate_t(const sft_plan_s* Pl, const LevelDims& L, const double2* in, double2* out) {
+static cudaError_t launch_translate_t(const sft_plan_s* Pl, const LevelDims& L, const void* in, void* out) {
   constexpr int PD = Pow<P, D>::v;
-  TransArgs a = make_args(L, in, out);
+  TransArgs a = make_args(L, (const double2*)in, (double2*)out);
   if (a.ngroups <= 0) return cudaSuccess;
-  if (translate_kernel_choice() == 0) {
+  if (Pl->prec == 1) {
+    constexpr int G = F32Cfg<D, P>::G, NC = F32Cfg<D, P>::NC, NST = F32Cfg<D, P>::NST, MB = F32Cfg<D, P>::MINB;
+    const size_t smem = (size_t)NST * G * (1 << D) * F32<D, P>::PS * sizeof(float2);
+    static int grid_max = 0;
+    if (!grid_max) {
+      cudaError_t e = persistent_grid(k_translate_f32<D, P, G, NC, NST, MB>, (NC + 1) * 32, smem, &grid_max);
+      if (e != cudaSuccess) return e;
+    }
+    if (!L.sched) return cudaErrorInvalidValue;
+    const int64_t ntiles = (a.ngroups + G - 1) / G;
+    const int64_t grid = std::min<int64_t>(ntiles, grid_max);
+    k_translate_f32<D, P, G, NC, NST, MB><<<(unsigned)grid, (NC + 1) * 32, smem, Pl->stream>>>(a, L.sched, ntiles);
+  } else if (translate_kernel_choice() == 0) {
     constexpr int G = WsCfg<D, P>::G, NC = WsCfg<D, P>::NC, NST = WsCfg<D, P>::NST, MB = WsCfg<D, P>::MINB;
     const size_t smem = (size_t)NST * G * (1 << D) * PD * sizeof(double2);
     static int grid_max = 0;
@@ -1171,39 +1403,36 @@ static size_t schedule_bytes_g(const LevelDims& L) {
 }
 
 template <int D, int P>
-static size_t schedule_bytes_t(const LevelDims& L) {
+static size_t schedule_bytes_t(const sft_plan_s* Pl, const LevelDims& L) {
+  if (Pl->prec == 1) return schedule_bytes_g<D, P, F32Cfg<D, P>::G>(L);
   const int mode = translate_kernel_choice();
   if (mode == 0) return schedule_bytes_g<D, P, WsCfg<D, P>::G>(L);
   return 0;
 }
 
-template <int D, int P, int G>
+template <int D, int P, int G, int PS>
 static cudaError_t launch_schedule_g(const sft_plan_s* Pl, const LevelDims& L, unsigned char* dst) {
   TransArgs a = make_args(L, nullptr, nullptr);
   if (a.ngroups <= 0) return cudaSuccess;
   const int64_t ntiles = (a.ngroups + G - 1) / G;
   const int64_t nwarps = (ntiles + 32 / G - 1) / (32 / G);
-  k_schedule<D, P, G><<<(unsigned)((nwarps + 3) / 4), 128, 0, Pl->stream>>>(a, dst, ntiles);
+  k_schedule<D, P, G, PS><<<(unsigned)((nwarps + 3) / 4), 128, 0, Pl->stream>>>(a, dst, ntiles);
   count_launch();
   return cudaGetLastError();
 }
 
 template <int D, int P>
 static cudaError_t launch_schedule_t(const sft_plan_s* Pl, const LevelDims& L, unsigned char* dst) {
+  if (Pl->prec == 1) return launch_schedule_g<D, P, F32Cfg<D, P>::G, F32<D, P>::PS>(Pl, L, dst);
   const int mode = translate_kernel_choice();
-  if (mode == 0) return launch_schedule_g<D, P, WsCfg<D, P>::G>(Pl, L, dst);
-  return cudaSuccess;
-}
-
-static cudaError_t schedule_bytes_d(const sft_plan_s* Pl, const LevelDims& L, size_t* r) {
-  SFT_DISPATCH(Pl->d, Pl->p, (*r = schedule_bytes_t<D, P>(L)));
+  if (mode == 0) return launch_schedule_g<D, P, WsCfg<D, P>::G, Pow<P, D>::v>(Pl, L, dst);
   return cudaSuccess;
 }
 
 template <int D, int P>
 static cudaError_t check_schedule_t(const sft_plan_s* Pl, const LevelDims& L, const unsigned char* sched,
                                    int64_t in_pairs, int64_t out_pairs, int* err) {
-  if (translate_kernel_choice() != 0) return cudaSuccess;
+  if (translate_kernel_choice() != 0 || Pl->prec != 0) return cudaSuccess;
   constexpr int G = WsCfg<D, P>::G;
   TransArgs a = make_args(L, nullptr, nullptr);
   if (a.ngroups <= 0) return cudaSuccess;
@@ -1219,6 +1448,11 @@ cudaError_t check_schedule(const sft_plan_s* Pl, const LevelDims& L, const unsig
   return cudaSuccess;
 }
 
+static cudaError_t schedule_bytes_d(const sft_plan_s* Pl, const LevelDims& L, size_t* r) {
+  SFT_DISPATCH(Pl->d, Pl->p, (*r = schedule_bytes_t<D, P>(Pl, L)));
+  return cudaSuccess;
+}
+
 size_t schedule_bytes(const sft_plan_s* Pl, const LevelDims& L) {
   size_t r = 0;
   schedule_bytes_d(Pl, L, &r);
@@ -1230,7 +1464,7 @@ cudaError_t launch_schedule(const sft_plan_s* Pl, const LevelDims& L, unsigned c
   return cudaSuccess;
 }
 
-cudaError_t launch_translate(const sft_plan_s* Pl, const LevelDims& L, const double2* in, double2* out) {
+cudaError_t launch_translate(const sft_plan_s* Pl, const LevelDims& L, const void* in, void* out) {
   SFT_DISPATCH(Pl->d, Pl->p, return (launch_translate_t<D, P>(Pl, L, in, out)));
   return cudaSuccess;
 }
