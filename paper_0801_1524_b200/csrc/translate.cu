@@ -331,6 +331,13 @@ struct MmaShape {
   static constexpr int NFRAG = NK * NT * 32 + (TAIL ? NK * 2 * 32 : 0);  // doubles in the table
 };
 
+// first k-step: D = A*B (C = 0)
+__device__ __forceinline__ void dmma0(double (&d)[2], double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%4,%4};"
+      : "=d"(d[0]), "=d"(d[1])
+      : "d"(a), "d"(b), "d"(0.0));
+}
+
 __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
       : "+d"(d[0]), "+d"(d[1])
@@ -356,27 +363,45 @@ __device__ __forceinline__ void mma_steps(const LaneOps<P>& op, const double2* c
   using S = MmaShape<P>;
 #pragma unroll
   for (int kk = K_LO; kk < K_HI; ++kk) {
-    const int b = op.bk[kk];
     double2 av[NSUB];
 #pragma unroll
     for (int u = 0; u < NSUB; ++u) {
+#ifdef SFT_NO_ZEROFILL
+      const int b = op.bk[kk];
       const bool live = b == 0 ? p0[u] : (b == 1 ? p1[u] : false);
       av[u] = live ? x[u][off[kk]] : make_double2(0.0, 0.0);
+#else
+      // absent children's slots are zero-filled by the producer and the B
+      // rows of padding k are zero: no masking needed
+      av[u] = x[u][off[kk]];
+#endif
     }
 #pragma unroll
     for (int n = 0; n < S::NT; ++n)
 #pragma unroll
       for (int u = 0; u < NSUB; ++u) {
-        dmma(are[u][n], av[u].x, op.fb[kk][n]);
-        dmma(aim[u][n], av[u].y, op.fb[kk][n]);
+        if (kk == K_LO) {
+          dmma0(are[u][n], av[u].x, op.fb[kk][n]);
+          dmma0(aim[u][n], av[u].y, op.fb[kk][n]);
+        } else {
+          dmma(are[u][n], av[u].x, op.fb[kk][n]);
+          dmma(aim[u][n], av[u].y, op.fb[kk][n]);
+        }
       }
     if (S::TAIL) {
 #pragma unroll
       for (int u = 0; u < NSUB; ++u) {
-        tl[u][0] = fma(av[u].x, op.ft[kk][0], tl[u][0]);
-        tl[u][1] = fma(av[u].x, op.ft[kk][1], tl[u][1]);
-        tl[u][2] = fma(av[u].y, op.ft[kk][0], tl[u][2]);
-        tl[u][3] = fma(av[u].y, op.ft[kk][1], tl[u][3]);
+        if (kk == K_LO) {
+          tl[u][0] = av[u].x * op.ft[kk][0];
+          tl[u][1] = av[u].x * op.ft[kk][1];
+          tl[u][2] = av[u].y * op.ft[kk][0];
+          tl[u][3] = av[u].y * op.ft[kk][1];
+        } else {
+          tl[u][0] = fma(av[u].x, op.ft[kk][0], tl[u][0]);
+          tl[u][1] = fma(av[u].x, op.ft[kk][1], tl[u][1]);
+          tl[u][2] = fma(av[u].y, op.ft[kk][0], tl[u][2]);
+          tl[u][3] = fma(av[u].y, op.ft[kk][1], tl[u][3]);
+        }
       }
     }
   }
@@ -768,7 +793,7 @@ __device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
         : "r"(bar), "r"(parity)
         : "memory");
     if (done) break;
-    __nanosleep(32);
+    __nanosleep(200);
   }
 }
 
@@ -823,6 +848,22 @@ __device__ __forceinline__ void ws_producer(const TransArgs& a, const unsigned c
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) nbytes += __shfl_xor_sync(0xffffffffu, nbytes, o);
       E* sb = ring + s * STAGE;
+#ifndef SFT_NO_ZEROFILL
+      // zero the slots of absent children of the tile's groups: the consumers
+      // then read every slot unmasked (absent children and padding contribute 0)
+      {
+        const int ng = (int)min((int64_t)G, a.ngroups - tile * G);
+        constexpr int CH = PD * (int)sizeof(E) / 16;  // 16-byte chunks per slot
+        for (int js = 0; js < ng * NS; ++js) {
+          const uint32_t mB = __shfl_sync(0xffffffffu, gr.y, js / NS);
+          if (mB >> (js % NS) & 1) continue;
+          float4* z = reinterpret_cast<float4*>(sb + (int64_t)js * PD);
+          for (int q = lane; q < CH; q += 32) z[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+      }
+#endif
       if (lane == 0) {
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&full[s])),
                      "r"(nbytes + (uint32_t)SC::BLK)
@@ -1273,8 +1314,37 @@ template <> struct WsCfg<2, 7> { static constexpr int G = 8, NC = 4, NST = 3, MI
 template <> struct WsCfg<2, 9> {
   static constexpr int G = SFT_WS_G29, NC = SFT_WS_NC29, NST = SFT_WS_NST29, MINB = SFT_WS_MINB29;
 };
-template <> struct WsCfg<3, 5> { static constexpr int G = 2, NC = 4, NST = 3, MINB = 2; };
-template <> struct WsCfg<3, 7> { static constexpr int G = 1, NC = 4, NST = 2, MINB = 2; };
+// 3D configurations, overridable per field for sweeps (nvcc splits -D values at commas)
+#ifndef SFT_WS_G35
+#define SFT_WS_G35 2
+#endif
+#ifndef SFT_WS_NC35
+#define SFT_WS_NC35 4
+#endif
+#ifndef SFT_WS_NST35
+#define SFT_WS_NST35 2
+#endif
+#ifndef SFT_WS_MINB35
+#define SFT_WS_MINB35 3
+#endif
+#ifndef SFT_WS_G37
+#define SFT_WS_G37 1
+#endif
+#ifndef SFT_WS_NC37
+#define SFT_WS_NC37 8
+#endif
+#ifndef SFT_WS_NST37
+#define SFT_WS_NST37 2
+#endif
+#ifndef SFT_WS_MINB37
+#define SFT_WS_MINB37 1
+#endif
+template <> struct WsCfg<3, 5> {
+  static constexpr int G = SFT_WS_G35, NC = SFT_WS_NC35, NST = SFT_WS_NST35, MINB = SFT_WS_MINB35;
+};
+template <> struct WsCfg<3, 7> {
+  static constexpr int G = SFT_WS_G37, NC = SFT_WS_NC37, NST = SFT_WS_NST37, MINB = SFT_WS_MINB37;
+};
 template <> struct WsCfg<3, 9> { static constexpr int G = 1, NC = 8, NST = 2, MINB = 1; };
 
 // FP32 kernel: G groups per tile, NC FFMA consumer warps, NST stages, MINB CTAs/SM
