@@ -451,6 +451,13 @@ extern "C" int sft_plan(int dim, int64_t N, int p, const double* x, int64_t nx, 
     const Partition& pt = P->part;
     descend_ranges(pk, pt.sk, pt.k_lo[P->rank], pt.k_hi[P->rank], L, P->k_rng);
     descend_ranges(px, pt.sx, pt.x_lo[P->rank], pt.x_hi[P->rank], L, P->x_rng);
+    {
+      int32_t fp[2] = {0, 0};
+      cudaMemcpy(&fp[0], P->X.first_pt + P->x_rng[L].lo, sizeof(int32_t), cudaMemcpyDeviceToHost);
+      cudaMemcpy(&fp[1], P->X.first_pt + P->x_rng[L].hi, sizeof(int32_t), cudaMemcpyDeviceToHost);
+      P->x_pt_lo = fp[0];
+      P->x_pt_hi = fp[1];
+    }
     // exchange layout at level m: A boundaries at level L-m for every rank
     const int m = pt.m, W = P->world;
     std::vector<int64_t> abound(W + 1), nb_of(W);
@@ -488,6 +495,8 @@ extern "C" int sft_plan(int dim, int64_t N, int p, const double* x, int64_t nx, 
     P->buf_elems = (size_t)mx * P->pds;
     P->k_rng.assign(L + 1, LevelRange());
     P->x_rng.assign(L + 1, LevelRange());
+    P->x_pt_lo = 0;
+    P->x_pt_hi = nx;
     for (int l = 0; l <= L; ++l) {
       P->k_rng[l].hi = P->K.counts[l];
       P->x_rng[l].hi = P->X.counts[l];
@@ -614,7 +623,7 @@ extern "C" int sft_apply(sft_plan_t P, const void* f, void* u) {
     tmark(P);
   }
   // step 4: final evaluation, level 0 buffer [A leaves]
-  CKR(launch_final(P, P->buf[0], ud, 0, P->X.counts[L]));
+  CKR(launch_final(P, P->buf[0], ud, 0, 0, P->nx));
   tmark(P);
   if (u_host) {
     CKR(cudaMemcpyAsync(u, ud, P->nx * sizeof(double2), cudaMemcpyDeviceToHost, s));
@@ -702,7 +711,7 @@ extern "C" int sft_apply_phase2(sft_plan_t P, const void* recvbuf, void* u) {
     in = out;
   }
   const LevelRange xl = P->x_rng[L];
-  CKR(launch_final(P, in, ud, xl.lo, xl.hi));
+  CKR(launch_final(P, in, ud, xl.lo, P->x_pt_lo, P->x_pt_hi));
   if (u_host) {
     CKR(cudaMemcpyAsync(u, ud, P->nx * sizeof(double2), cudaMemcpyDeviceToHost, s));
     CKR(cudaStreamSynchronize(s));

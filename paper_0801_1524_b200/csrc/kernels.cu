@@ -32,17 +32,33 @@ __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
 }
 
 // ------------------------------------------------------------------------
-// K2: leaf kernel, one warp per leaf B of T_K (h-representation)
+// K2: leaf kernel, one warp per leaf B of T_K, one lane per source
 // ------------------------------------------------------------------------
+// Lane j (source k_j of B, s = k_j - c^B in [0,1]^d) evaluates its weights
+//   r_m(s_a) = invD_m prod_{q != m} sin(pi (s_a (p-1) - q)/(p-1)^2)
+// with one sincospi per axis (sin(theta - q delta) by angle addition, theta =
+// pi s_a/(p-1), delta = pi/(p-1)^2) and prefix/suffix products, and its
+// rotated charge f_j e^{i pi sum_a s_a}; then lane e (output element) sums
+// over the leaf's sources.  Sources beyond 32 are processed in chunks.
 template <int D, int P, typename T2, int PS>
-__global__ __launch_bounds__(128) void k_leaf(const double* __restrict__ k_sorted, const int32_t* __restrict__ perm,
+__global__ __launch_bounds__(128, D == 2 ? 4 : 2) void k_leaf(const double* __restrict__ k_sorted, const int32_t* __restrict__ perm,
                                               const int32_t* __restrict__ first_pt,
                                               const double2* __restrict__ f, const double* __restrict__ invD,
                                               T2* __restrict__ out, int64_t b_lo, int64_t b_hi, int64_t N) {
   constexpr int PD = Pow<P, D>::v;
   constexpr int NACC = (PD + 31) / 32;
   constexpr int P1 = P - 1;
-  __shared__ double r_s[4][D][P], sn_s[4][D][P];
+  __shared__ double w_s[4][32][D][P];
+  __shared__ double2 f_s[4][32];
+  __shared__ double cdq[P], sdq[P], inv_s[P];
+  if (threadIdx.x < P) {
+    double sn, cs;
+    sincospi((double)threadIdx.x / (double)(P1 * P1), &sn, &cs);
+    cdq[threadIdx.x] = cs;
+    sdq[threadIdx.x] = sn;
+    inv_s[threadIdx.x] = invD[threadIdx.x];
+  }
+  __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t b = b_lo + blockIdx.x * 4 + warp;
   if (b >= b_hi) return;
@@ -50,48 +66,55 @@ __global__ __launch_bounds__(128) void k_leaf(const double* __restrict__ k_sorte
 #pragma unroll
   for (int i = 0; i < NACC; ++i) acc[i] = make_double2(0.0, 0.0);
   const int j0 = first_pt[b], j1 = first_pt[b + 1];
-  for (int j = j0; j < j1; ++j) {
-    // s = k - c^B in [0,1] (exact); c^B = min(floor(k), N-1) per axis
-    double ssum = 0.0;
+  for (int c0 = j0; c0 < j1; c0 += 32) {
+    const int n = min(32, j1 - c0);
+    if (lane < n) {
+      const int j = c0 + lane;
+      double ssum = 0.0;
 #pragma unroll
-    for (int a = 0; a < D; ++a) {
-      const double kk = k_sorted[(int64_t)j * D + a];
-      ssum += kk - fmin(floor(kk), (double)(N - 1));
-    }
-    // r_m(s) = invD_m prod_{q != m} sin(pi (s P1 - q)/P1^2): lane (a, q) evaluates
-    // one sine, lane (a, m) then multiplies the p-1 others
-    if (lane < D * P) {
-      const int a = lane / P, q = lane % P;
-      const double kk = k_sorted[(int64_t)j * D + a];
-      const double s = kk - fmin(floor(kk), (double)(N - 1));
-      sn_s[warp][a][q] = sinpi((s * P1 - q) / (double)(P1 * P1));
-    }
-    __syncwarp();
-    if (lane < D * P) {
-      const int a = lane / P, m = lane % P;
-      double prod = invD[m];
+      for (int a = 0; a < D; ++a) {
+        const double kk = k_sorted[(int64_t)j * D + a];
+        const double sa = kk - fmin(floor(kk), (double)(N - 1));  // exact
+        ssum += sa;
+        double sn, cs;
+        sincospi(sa / (double)P1, &sn, &cs);
+        double sq[P], pre[P];
 #pragma unroll
-      for (int q = 0; q < P; ++q)
-        if (q != m) prod *= sn_s[warp][a][q];
-      r_s[warp][a][m] = prod;
-    }
-    __syncwarp();
-    double sn, cs;
-    sincospi(ssum, &sn, &cs);
-    const double2 fj = cmul(f[perm[j]], make_double2(cs, sn));
+        for (int q = 0; q < P; ++q) sq[q] = fma(sn, cdq[q], -cs * sdq[q]);  // sin(theta - q delta)
+        double acc_p = 1.0;
 #pragma unroll
-    for (int i = 0; i < NACC; ++i) {
-      const int e = lane + 32 * i;
-      if (e < PD) {
-        double w = 1.0;
-        int r = e;
-#pragma unroll
-        for (int a = D - 1; a >= 0; --a) {
-          w *= r_s[warp][a][r % P];
-          r /= P;
+        for (int m = 0; m < P; ++m) {
+          pre[m] = acc_p;
+          acc_p *= sq[m];
         }
-        acc[i].x = fma(w, fj.x, acc[i].x);
-        acc[i].y = fma(w, fj.y, acc[i].y);
+        double suf = 1.0;
+#pragma unroll
+        for (int m = P - 1; m >= 0; --m) {
+          w_s[warp][lane][a][m] = inv_s[m] * pre[m] * suf;
+          suf *= sq[m];
+        }
+      }
+      double sn, cs;
+      sincospi(ssum, &sn, &cs);
+      f_s[warp][lane] = cmul(f[perm[j]], make_double2(cs, sn));
+    }
+    __syncwarp();
+    for (int t = 0; t < n; ++t) {
+      const double2 fj = f_s[warp][t];
+#pragma unroll
+      for (int i = 0; i < NACC; ++i) {
+        const int e = lane + 32 * i;
+        if (e < PD) {
+          double w = 1.0;
+          int r = e;
+#pragma unroll
+          for (int a = D - 1; a >= 0; --a) {
+            w *= w_s[warp][t][a][r % P];
+            r /= P;
+          }
+          acc[i].x = fma(w, fj.x, acc[i].x);
+          acc[i].y = fma(w, fj.y, acc[i].y);
+        }
       }
     }
     __syncwarp();
@@ -110,66 +133,74 @@ __global__ __launch_bounds__(128) void k_leaf(const double* __restrict__ k_sorte
 }
 
 // ------------------------------------------------------------------------
-// K4: final kernel, one warp per leaf A of T_X (h-representation)
+// K4: final kernel, one thread per target (32 consecutive sorted targets per
+// warp, across leaf boundaries)
 // ------------------------------------------------------------------------
+// Target x_i in leaf A (xi = x_i - c^A in [0,1]^d): z_a = e^{i pi (2 xi_a - 1)/(p-1)}
+// (one sincospi per axis), powers by recurrence, and
+//   u_i = sum_l prod_a z_a^{l_a} h^{A B0}_l
+// sum-factorised over the axes; h is read through L1 (the ~3 targets of a
+// leaf share it).
 template <int D, int P, typename T2, int PS>
 __global__ __launch_bounds__(128) void k_final(const double* __restrict__ x_sorted, const int32_t* __restrict__ perm,
-                                               const int32_t* __restrict__ first_pt,
+                                               const int32_t* __restrict__ leaf_of,
                                                const T2* __restrict__ h0, double2* __restrict__ u,
-                                               int64_t a_lo, int64_t a_hi, int64_t N) {
-  constexpr int PD = Pow<P, D>::v;
-  constexpr int NACC = (PD + 31) / 32;
+                                               int64_t i_lo, int64_t i_hi, int64_t a_lo, int64_t N) {
   constexpr int P1 = P - 1;
-  __shared__ double2 e_s[4][D][P];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t A = a_lo + blockIdx.x * 4 + warp;
-  if (A >= a_hi) return;
-  const T2* h = h0 + (A - a_lo) * (int64_t)PS;
-  double2 hr[NACC];
+  const int64_t j = i_lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= i_hi) return;
+  const T2* h = h0 + ((int64_t)leaf_of[j] - a_lo) * (int64_t)PS;
+  double2 z[D], el[P];
 #pragma unroll
-  for (int i = 0; i < NACC; ++i) {
-    const int e = lane + 32 * i;
-    hr[i] = make_double2(0.0, 0.0);
-    if (e < PD) {
-      const T2 v = h[e];
-      hr[i] = make_double2(v.x, v.y);
-    }
+  for (int a = 0; a < D; ++a) {
+    const double xx = x_sorted[j * D + a];
+    const double xi = xx - fmin(floor(xx), (double)(N - 1));  // in [0,1], exact
+    double sn, cs;
+    sincospi((2.0 * xi - 1.0) / (double)P1, &sn, &cs);
+    z[a] = make_double2(cs, sn);
   }
-  const int j0 = first_pt[A], j1 = first_pt[A + 1];
-  for (int j = j0; j < j1; ++j) {
-    if (lane < D * P) {
-      const int a = lane / P, l = lane % P;
-      const double xx = x_sorted[(int64_t)j * D + a];
-      const double xi = xx - fmin(floor(xx), (double)(N - 1));  // in [0,1], exact
-      double sn, cs;
-      sincospi((2.0 * xi - 1.0) * l / P1, &sn, &cs);
-      e_s[warp][a][l] = make_double2(cs, sn);
+  el[0] = make_double2(1.0, 0.0);
+#pragma unroll
+  for (int l = 1; l < P; ++l) el[l] = cmul(el[l - 1], z[D - 1]);
+  auto inner = [&](int base) {
+    double2 t = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int l = 0; l < P; ++l) {
+      const T2 hq = __ldg(h + base + l);
+      const double hx = hq.x, hy = hq.y;
+      t.x = fma(el[l].x, hx, fma(-el[l].y, hy, t.x));
+      t.y = fma(el[l].x, hy, fma(el[l].y, hx, t.y));
     }
-    __syncwarp();
-    double2 s = make_double2(0.0, 0.0);
+    return t;
+  };
+  double2 s = make_double2(0.0, 0.0);
+  double2 w0 = make_double2(1.0, 0.0);
+  if constexpr (D == 2) {
 #pragma unroll
-    for (int i = 0; i < NACC; ++i) {
-      const int e = lane + 32 * i;
-      if (e < PD) {
-        double2 w = hr[i];
-        int r = e;
+    for (int l0 = 0; l0 < P; ++l0) {
+      const double2 t = inner(l0 * P);
+      s.x = fma(w0.x, t.x, fma(-w0.y, t.y, s.x));
+      s.y = fma(w0.x, t.y, fma(w0.y, t.x, s.y));
+      w0 = cmul(w0, z[0]);
+    }
+  } else {
+#pragma unroll 1
+    for (int l0 = 0; l0 < P; ++l0) {
+      double2 t1 = make_double2(0.0, 0.0);
+      double2 w1 = make_double2(1.0, 0.0);
 #pragma unroll
-        for (int a = D - 1; a >= 0; --a) {
-          w = cmul(w, e_s[warp][a][r % P]);
-          r /= P;
-        }
-        s.x += w.x;
-        s.y += w.y;
+      for (int l1 = 0; l1 < P; ++l1) {
+        const double2 t = inner((l0 * P + l1) * P);
+        t1.x = fma(w1.x, t.x, fma(-w1.y, t.y, t1.x));
+        t1.y = fma(w1.x, t.y, fma(w1.y, t.x, t1.y));
+        w1 = cmul(w1, z[1]);
       }
+      s.x = fma(w0.x, t1.x, fma(-w0.y, t1.y, s.x));
+      s.y = fma(w0.x, t1.y, fma(w0.y, t1.x, s.y));
+      w0 = cmul(w0, z[0]);
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      s.x += __shfl_xor_sync(0xffffffffu, s.x, o);
-      s.y += __shfl_xor_sync(0xffffffffu, s.y, o);
-    }
-    if (lane == 0) u[perm[j]] = s;
-    __syncwarp();
   }
+  u[perm[j]] = s;
 }
 
 __global__ void k_zero(double2* p, int64_t n) {
@@ -199,17 +230,18 @@ cudaError_t launch_leaf(const sft_plan_s* Pl, const double2* f, void* out, int64
   return cudaGetLastError();
 }
 
-cudaError_t launch_final(const sft_plan_s* Pl, const void* h0, double2* u, int64_t a_lo, int64_t a_hi) {
-  if (a_hi <= a_lo) return cudaSuccess;
-  const unsigned nb = (unsigned)((a_hi - a_lo + 3) / 4);
+cudaError_t launch_final(const sft_plan_s* Pl, const void* h0, double2* u, int64_t a_lo, int64_t i_lo, int64_t i_hi) {
+  // targets = sorted points [i_lo, i_hi) of T_X; h0 holds the leaves from a_lo on
+  if (i_hi <= i_lo) return cudaSuccess;
+  const unsigned nb = (unsigned)((i_hi - i_lo + 127) / 128);
   if (Pl->prec == 1) {
     SFT_DISPATCH(Pl->d, Pl->p,
                  (k_final<D, P, float2, Pow<P, D>::v + (Pow<P, D>::v & 1)><<<nb, 128, 0, Pl->stream>>>(
-                     Pl->X.pts_sorted, Pl->X.perm, Pl->X.first_pt, (const float2*)h0, u, a_lo, a_hi, Pl->N)));
+                     Pl->X.pts_sorted, Pl->X.perm, Pl->X.leaf_of, (const float2*)h0, u, i_lo, i_hi, a_lo, Pl->N)));
   } else {
     SFT_DISPATCH(Pl->d, Pl->p,
                  (k_final<D, P, double2, Pow<P, D>::v><<<nb, 128, 0, Pl->stream>>>(
-                     Pl->X.pts_sorted, Pl->X.perm, Pl->X.first_pt, (const double2*)h0, u, a_lo, a_hi, Pl->N)));
+                     Pl->X.pts_sorted, Pl->X.perm, Pl->X.leaf_of, (const double2*)h0, u, i_lo, i_hi, a_lo, Pl->N)));
   }
   count_launch();
   return cudaGetLastError();

@@ -39,6 +39,7 @@ struct Tree {
   std::vector<TreeLevel> lev;      // [L+1]
   std::vector<int64_t> counts;     // host copy of lev[l].n
   int32_t* first_pt = nullptr;     // [n_leaf+1] CSR of sorted points per leaf
+  int32_t* leaf_of = nullptr;      // [npts] leaf index of each sorted point
   int32_t* perm = nullptr;         // [npts] sorted position -> user index
   double* pts_sorted = nullptr;    // [npts][d]
   void* arena = nullptr;           // one allocation holding every array above (X owns both trees')
@@ -90,6 +91,7 @@ struct sft_plan_s {
   sft::Partition part;
   std::vector<sft::LevelRange> k_rng;  // [L+1] this rank's T_K range per level (phase 1)
   std::vector<sft::LevelRange> x_rng;  // [L+1] this rank's T_X range per level (phase 2)
+  int64_t x_pt_lo = 0, x_pt_hi = 0;     // sorted target range of this rank's T_X leaves
   std::vector<int64_t> send_counts, recv_counts;  // [world] complex elements
   int64_t* d_seg = nullptr;  // device [2*world+1]: a-boundaries at level L-m, send segment bases
   // tile schedules of the translation levels (one allocation; offsets per level t)
@@ -137,7 +139,8 @@ cudaError_t launch_schedule(const sft_plan_s* P, const LevelDims& L, unsigned ch
 // debug: validate a level's schedule against its input/output pair counts (sets *err bit 2)
 cudaError_t check_schedule(const sft_plan_s* P, const LevelDims& L, const unsigned char* sched, int64_t in_pairs,
                            int64_t out_pairs, int* err);
-cudaError_t launch_final(const sft_plan_s* P, const void* g0, double2* u, int64_t a_lo, int64_t a_hi);
+// step 4 for the sorted targets [i_lo, i_hi) (the points of leaves a_lo...); g0 holds leaves from a_lo on
+cudaError_t launch_final(const sft_plan_s* P, const void* g0, double2* u, int64_t a_lo, int64_t i_lo, int64_t i_hi);
 cudaError_t launch_zero(double2* p, int64_t n, cudaStream_t s);
 
 template <int B, int E>

@@ -103,6 +103,7 @@ struct TreeOut {
   uint32_t* child_mask[kMaxLevels];
   int32_t* parent[kMaxLevels];
   int32_t* first_pt;
+  int32_t* leaf_of;  // [npts] leaf index of each sorted point
   int32_t* perm;
   double* pts_sorted;
   const double* pts;
@@ -177,6 +178,7 @@ __global__ __launch_bounds__(kBlk) void k_fill(const uint64_t* __restrict__ key,
   if (i == hi - 1 && (int)blockIdx.x == b_last) T.first_pt[bid_prev + 1] = (int32_t)(li + 1);
   const int32_t j = idx[i] - (int32_t)ts;
   T.perm[li] = j;
+  T.leaf_of[li] = bid_prev;  // box of the point at level L
   for (int a = 0; a < d; ++a) T.pts_sorted[li * d + a] = T.pts[(int64_t)j * d + a];
 }
 
@@ -214,7 +216,7 @@ int build_trees(sft_plan_s* P, const double* x_dev, const double* k_dev, std::st
   // ---- persistent arena: level arrays (upper bounds) + sorted points ----
   size_t off = 0;
   std::vector<size_t> o_key[2], o_cb[2], o_cm[2], o_par[2];
-  size_t o_first[2], o_perm[2], o_pts[2], o_tot[2];
+  size_t o_first[2], o_leafof[2], o_perm[2], o_pts[2], o_tot[2];
   size_t cm_lo = 0, cm_hi = 0;
   for (int t = 0; t < 2; ++t) {
     o_key[t].resize(L + 1);
@@ -244,6 +246,8 @@ int build_trees(sft_plan_s* P, const double* x_dev, const double* k_dev, std::st
     }
     o_first[t] = off;
     off = align_up(off + 4 * (level_cap(npt[t], d, L) + 1), 256);
+    o_leafof[t] = off;
+    off = align_up(off + 4 * npt[t], 256);
     o_perm[t] = off;
     off = align_up(off + 4 * npt[t], 256);
     o_pts[t] = off;
@@ -309,6 +313,7 @@ int build_trees(sft_plan_s* P, const double* x_dev, const double* k_dev, std::st
       o.child_begin[l] = ok ? (int32_t*)(arena + o_cb[t][l]) : nullptr;
     }
     o.first_pt = (int32_t*)(arena + o_first[t]);
+    o.leaf_of = (int32_t*)(arena + o_leafof[t]);
     o.perm = (int32_t*)(arena + o_perm[t]);
     o.pts_sorted = (double*)(arena + o_pts[t]);
     o.pts = src[t];
@@ -346,6 +351,7 @@ int build_trees(sft_plan_s* P, const double* x_dev, const double* k_dev, std::st
       lv.child_begin = l < L ? fa.t[t].child_begin[l] : nullptr;
     }
     T.first_pt = fa.t[t].first_pt;
+    T.leaf_of = fa.t[t].leaf_of;
     T.perm = fa.t[t].perm;
     T.pts_sorted = fa.t[t].pts_sorted;
   }
