@@ -341,6 +341,8 @@ static void plan_free(sft_plan_s* P) {
   if (P->d_seg) cudaFreeAsync(P->d_seg, s);
   if (P->sched) cudaFreeAsync(P->sched, s);
   for (int i = 0; i < P->ev_created; ++i) cudaEventDestroy(P->ev[i]);
+  for (int i = 0; i < 2; ++i)
+    if (P->plan_ev[i]) cudaEventDestroy(P->plan_ev[i]);
   // no sync: the frees above are stream-ordered behind any pending work
   delete P;
 }
@@ -404,8 +406,10 @@ extern "C" int sft_plan(int dim, int64_t N, int p, const double* x, int64_t nx, 
   cudaEventCreate(&e1);
   cudaEventRecord(e0, s);
   auto bail = [&](int code, const std::string& m) {
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
+    if (!P->plan_ev[0]) {
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+    }
     plan_free(P);
     return fail(code, m);
   };
@@ -517,10 +521,14 @@ extern "C" int sft_plan(int dim, int64_t N, int p, const double* x, int64_t nx, 
     P->sched_off[L] = tot;
     if (tot > 0) {
       if (cudaMallocAsync(&P->sched, tot, s) != cudaSuccess) return bail(SFT_E_NOMEM, "schedule allocation failed");
+      std::vector<LevelDims> dims(L);
+      std::vector<unsigned char*> dst(L);
       for (int t = 0; t < L; ++t) {
-        cudaError_t ce = launch_schedule(P, apply_dims(P, t), P->sched + P->sched_off[t]);
-        if (ce != cudaSuccess) return bail(SFT_E_CUDA, std::string("schedule: ") + cudaGetErrorString(ce));
+        dims[t] = apply_dims(P, t);
+        dst[t] = P->sched + P->sched_off[t];
       }
+      cudaError_t ce = launch_schedule(P, dims.data(), L, dst.data());
+      if (ce != cudaSuccess) return bail(SFT_E_CUDA, std::string("schedule: ") + cudaGetErrorString(ce));
       const char* chk = getenv("SFT_CHECK_SCHED");
       if (chk && chk[0] == '1') {
         // debug: every level's schedule against its buffer sizes
@@ -537,13 +545,12 @@ extern "C" int sft_plan(int dim, int64_t N, int p, const double* x, int64_t nx, 
       }
     }
   }
+  // no sync here: the schedule kernel runs behind the caller's next launches;
+  // the plan's device time is read lazily (sft_plan_stats)
   cudaEventRecord(e1, s);
-  if (cudaEventSynchronize(e1) != cudaSuccess) return bail(SFT_E_CUDA, "plan sync failed");
-  float ms = 0;
-  cudaEventElapsedTime(&ms, e0, e1);
-  P->plan_ms = ms;
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
+  P->plan_ev[0] = e0;
+  P->plan_ev[1] = e1;
+  P->plan_ms = -1.0;
   cudaError_t ce = cudaGetLastError();
   if (ce != cudaSuccess) {
     plan_free(P);
@@ -743,6 +750,12 @@ extern "C" int sft_plan_stats(sft_plan_t P, int64_t* counts_x, int64_t* counts_k
     info[2] = (double)P->nx;
     info[3] = (double)P->nk;
     info[4] = 2.0 * P->buf_elems * (P->prec == 1 ? sizeof(float2) : sizeof(double2));
+    if (P->plan_ms < 0 && P->plan_ev[1]) {
+      float ms = 0;
+      cudaEventSynchronize(P->plan_ev[1]);
+      cudaEventElapsedTime(&ms, P->plan_ev[0], P->plan_ev[1]);
+      P->plan_ms = ms;
+    }
     info[5] = P->plan_ms;
     info[6] = groups;
     info[7] = bytes;

@@ -104,7 +104,8 @@ struct sft_plan_s {
   int ev_created = 0;
   double last_ms[4] = {0, 0, 0, 0};
   std::vector<double> level_ms;
-  double plan_ms = 0;
+  double plan_ms = 0;               // device time of sft_plan (events below), read lazily
+  cudaEvent_t plan_ev[2] = {nullptr, nullptr};
 };
 
 namespace sft {
@@ -135,7 +136,8 @@ cudaError_t launch_leaf(const sft_plan_s* P, const double2* f, void* out, int64_
 cudaError_t launch_translate(const sft_plan_s* P, const LevelDims& L, const void* in, void* out);
 // tile schedule of one level (sizes and builder; 0 bytes when the kernel needs none)
 size_t schedule_bytes(const sft_plan_s* P, const LevelDims& L);
-cudaError_t launch_schedule(const sft_plan_s* P, const LevelDims& L, unsigned char* dst);
+// builds the schedules of nlev levels (dims L[i], destination dst[i]) in one launch
+cudaError_t launch_schedule(const sft_plan_s* P, const LevelDims* L, int nlev, unsigned char* const* dst);
 // debug: validate a level's schedule against its input/output pair counts (sets *err bit 2)
 cudaError_t check_schedule(const sft_plan_s* P, const LevelDims& L, const unsigned char* sched, int64_t in_pairs,
                            int64_t out_pairs, int* err);

@@ -571,17 +571,30 @@ __device__ __forceinline__ void schedule_pass(const TransArgs& a, const GroupMet
   }
 }
 
+// All levels of a plan in one launch: level lv owns the global tiles
+// [tile0[lv], tile0[lv+1]) and writes its blocks at dst[lv].
+struct SchedLevels {
+  TransArgs a[kMaxLevels];
+  unsigned char* dst[kMaxLevels];
+  int64_t tile0[kMaxLevels + 1];
+  int nlev;
+};
+
 template <int D, int P, int G, int PS>
-__global__ __launch_bounds__(128) void k_schedule(TransArgs a, unsigned char* __restrict__ sched, int64_t ntiles) {
+__global__ __launch_bounds__(128) void k_schedule(const __grid_constant__ SchedLevels S) {
   using SC = Sched<D, P, G>;
   static_assert(G >= 1 && G <= 32 && (G & (G - 1)) == 0, "G must be a power of two");
-  constexpr int TPW = 32 / G;  // tiles per warp
+  constexpr int TPW = 32 / G;  // tiles per warp (G-lane segments)
   const int lane = threadIdx.x & 31;
-  const int64_t tile = ((int64_t)blockIdx.x * 4 + (threadIdx.x >> 5)) * TPW + lane / G;
+  const int64_t T = ((int64_t)blockIdx.x * 4 + (threadIdx.x >> 5)) * TPW + lane / G;  // global tile
   const int j = lane % G;
-  if (tile - lane / G >= ntiles) return;  // whole warp out of range
-  const bool tv = tile < ntiles;
-  unsigned char* b = sched + (tv ? tile : 0) * SC::BLK;
+  if (T - lane / G >= S.tile0[S.nlev]) return;  // whole warp out of range
+  int lv = 0;
+  while (lv + 1 < S.nlev && T >= S.tile0[lv + 1]) ++lv;
+  const TransArgs& a = S.a[lv];
+  const int64_t tile = T - S.tile0[lv];
+  const bool tv = T < S.tile0[S.nlev];
+  unsigned char* b = S.dst[lv] + (tv ? tile : 0) * SC::BLK;
   const int64_t g = tile * G + j;
   const bool valid = tv && g < a.ngroups;
   GroupMeta m;
@@ -1481,21 +1494,32 @@ static size_t schedule_bytes_t(const sft_plan_s* Pl, const LevelDims& L) {
 }
 
 template <int D, int P, int G, int PS>
-static cudaError_t launch_schedule_g(const sft_plan_s* Pl, const LevelDims& L, unsigned char* dst) {
-  TransArgs a = make_args(L, nullptr, nullptr);
-  if (a.ngroups <= 0) return cudaSuccess;
-  const int64_t ntiles = (a.ngroups + G - 1) / G;
-  const int64_t nwarps = (ntiles + 32 / G - 1) / (32 / G);
-  k_schedule<D, P, G, PS><<<(unsigned)((nwarps + 3) / 4), 128, 0, Pl->stream>>>(a, dst, ntiles);
+static cudaError_t launch_schedule_g(const sft_plan_s* Pl, const LevelDims* L, int nlev, unsigned char* const* dst) {
+  SchedLevels S;
+  int64_t t0 = 0;
+  S.nlev = 0;
+  for (int i = 0; i < nlev && S.nlev < kMaxLevels; ++i) {
+    TransArgs a = make_args(L[i], nullptr, nullptr);
+    if (a.ngroups <= 0) continue;
+    S.a[S.nlev] = a;
+    S.dst[S.nlev] = dst[i];
+    S.tile0[S.nlev] = t0;
+    t0 += (a.ngroups + G - 1) / G;
+    ++S.nlev;
+  }
+  S.tile0[S.nlev] = t0;
+  if (S.nlev == 0) return cudaSuccess;
+  const int64_t nwarps = (t0 + 32 / G - 1) / (32 / G);
+  k_schedule<D, P, G, PS><<<(unsigned)((nwarps + 3) / 4), 128, 0, Pl->stream>>>(S);
   count_launch();
   return cudaGetLastError();
 }
 
 template <int D, int P>
-static cudaError_t launch_schedule_t(const sft_plan_s* Pl, const LevelDims& L, unsigned char* dst) {
-  if (Pl->prec == 1) return launch_schedule_g<D, P, F32Cfg<D, P>::G, F32<D, P>::PS>(Pl, L, dst);
+static cudaError_t launch_schedule_t(const sft_plan_s* Pl, const LevelDims* L, int nlev, unsigned char* const* dst) {
+  if (Pl->prec == 1) return launch_schedule_g<D, P, F32Cfg<D, P>::G, F32<D, P>::PS>(Pl, L, nlev, dst);
   const int mode = translate_kernel_choice();
-  if (mode == 0) return launch_schedule_g<D, P, WsCfg<D, P>::G, Pow<P, D>::v>(Pl, L, dst);
+  if (mode == 0) return launch_schedule_g<D, P, WsCfg<D, P>::G, Pow<P, D>::v>(Pl, L, nlev, dst);
   return cudaSuccess;
 }
 
@@ -1529,8 +1553,8 @@ size_t schedule_bytes(const sft_plan_s* Pl, const LevelDims& L) {
   return r;
 }
 
-cudaError_t launch_schedule(const sft_plan_s* Pl, const LevelDims& L, unsigned char* dst) {
-  SFT_DISPATCH(Pl->d, Pl->p, return (launch_schedule_t<D, P>(Pl, L, dst)));
+cudaError_t launch_schedule(const sft_plan_s* Pl, const LevelDims* L, int nlev, unsigned char* const* dst) {
+  SFT_DISPATCH(Pl->d, Pl->p, return (launch_schedule_t<D, P>(Pl, L, nlev, dst)));
   return cudaSuccess;
 }
 

@@ -28,8 +28,9 @@ namespace sft {
 
 constexpr int kBlk = 1024;  // points per block in k_count / k_fill
 
+template <typename KT>
 __global__ void k_leaf_keys(const double* __restrict__ x, int64_t nx, const double* __restrict__ k, int64_t nk,
-                            int d, int L, double Nf, int64_t N, uint64_t* __restrict__ key,
+                            int d, int L, double Nf, int64_t N, KT* __restrict__ key,
                             int32_t* __restrict__ idx, int* err) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= nx + nk) return;
@@ -49,7 +50,7 @@ __global__ void k_leaf_keys(const double* __restrict__ x, int64_t nx, const doub
   uint64_t kk = tk ? 1ull : 0ull;
   for (int b = L - 1; b >= 0; --b)
     for (int a = 0; a < d; ++a) kk = (kk << 1) | ((c[a] >> b) & 1ull);
-  key[i] = kk;
+  key[i] = (KT)kk;
   idx[i] = (int32_t)i;
 }
 
@@ -66,15 +67,17 @@ struct BlockMap {
 
 // level at which sorted point i (of the tree starting at ts) opens a box;
 // L+1 = never (same leaf as its predecessor)
-__device__ __forceinline__ int open_level(const uint64_t* key, int64_t i, int64_t ts, int d, int L) {
+template <typename KT>
+__device__ __forceinline__ int open_level(const KT* key, int64_t i, int64_t ts, int d, int L) {
   if (i == ts) return 0;
-  const uint64_t x = key[i] ^ key[i - 1];
+  const uint64_t x = (uint64_t)key[i] ^ (uint64_t)key[i - 1];
   if (x == 0) return L + 1;
   const int hb = 63 - __clzll((long long)x);
   return L - hb / d;
 }
 
-__global__ __launch_bounds__(kBlk) void k_count(const uint64_t* __restrict__ key, BlockMap bm, int d, int L,
+template <typename KT>
+__global__ __launch_bounds__(kBlk) void k_count(const KT* __restrict__ key, BlockMap bm, int d, int L,
                                                 uint8_t* __restrict__ ml, int32_t* __restrict__ counts) {
   __shared__ int cnt[kMaxLevels];
   int tree;
@@ -116,7 +119,8 @@ struct FillArgs {
   int nbk;
 };
 
-__global__ __launch_bounds__(kBlk) void k_fill(const uint64_t* __restrict__ key, const int32_t* __restrict__ idx,
+template <typename KT>
+__global__ __launch_bounds__(kBlk) void k_fill(const KT* __restrict__ key, const int32_t* __restrict__ idx,
                                                const uint8_t* __restrict__ ml, const int32_t* __restrict__ counts,
                                                FillArgs A, int d, int L) {
   __shared__ int base[kMaxLevels];
@@ -155,7 +159,7 @@ __global__ __launch_bounds__(kBlk) void k_fill(const uint64_t* __restrict__ key,
   }
   __syncthreads();
   const bool valid = i < hi;
-  const uint64_t kk = valid ? key[i] : 0ull;
+  const uint64_t kk = valid ? (uint64_t)key[i] : 0ull;
   const int64_t li = i - ts;  // index within this tree's sorted points
   int bid_prev = -1;
   for (int l = 0; l <= L; ++l) {
@@ -199,6 +203,80 @@ static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 static int64_t level_cap(int64_t n, int d, int l) {
   if (d * l >= 40) return n;
   return std::min<int64_t>(n, int64_t(1) << (d * l));
+}
+
+template <typename KT>
+static int sort_and_fill(sft_plan_s* P, const double* x_dev, const double* k_dev, char* arena,
+                         const std::vector<size_t>* o_key, const std::vector<size_t>* o_par,
+                         const std::vector<size_t>* o_cm, const std::vector<size_t>* o_cb, const size_t* o_first,
+                         const size_t* o_leafof, const size_t* o_perm, const size_t* o_pts, const size_t* o_tot,
+                         const double* const* src, char** scr_out, FillArgs& fa, std::string* err) {
+  cudaStream_t s = P->stream;
+  const int d = P->d, L = P->L;
+  const int64_t nx = P->nx, nk = P->nk, n = nx + nk;
+  // ---- scratch ----
+  const int nbx = (int)nblk(nx, kBlk), nbk = (int)nblk(nk, kBlk);
+  size_t cub_bytes = 0;
+  CK(cub::DeviceRadixSort::SortPairs(nullptr, cub_bytes, (KT*)nullptr, (KT*)nullptr, (int32_t*)nullptr,
+                                     (int32_t*)nullptr, (int)n, 0, d * L + 1, s));
+  size_t so = 0;
+  const size_t s_kin = so;
+  so = align_up(so + sizeof(KT) * n, 256);
+  const size_t s_kout = so;
+  so = align_up(so + sizeof(KT) * n, 256);
+  const size_t s_iin = so;
+  so = align_up(so + 4 * n, 256);
+  const size_t s_iout = so;
+  so = align_up(so + 4 * n, 256);
+  const size_t s_ml = so;
+  so = align_up(so + n, 256);
+  const size_t s_cnt = so;
+  so = align_up(so + 4 * (size_t)(nbx + nbk) * (L + 1), 256);
+  const size_t s_cub = so;
+  so = align_up(so + cub_bytes, 256);
+  char* scr = nullptr;
+  CK(cudaMallocAsync((void**)&scr, so, s));
+  KT* keys_in = (KT*)(scr + s_kin);
+  KT* keys_out = (KT*)(scr + s_kout);
+  int32_t* idx_in = (int32_t*)(scr + s_iin);
+  int32_t* idx_out = (int32_t*)(scr + s_iout);
+  uint8_t* ml = (uint8_t*)(scr + s_ml);
+  int32_t* counts = (int32_t*)(scr + s_cnt);
+
+  k_leaf_keys<KT><<<nblk(n, 256), 256, 0, s>>>(x_dev, nx, k_dev, nk, d, L, (double)P->N, P->N, keys_in, idx_in, P->d_err);
+  count_launch();
+  CK(cudaGetLastError());
+  CK(cub::DeviceRadixSort::SortPairs(scr + s_cub, cub_bytes, keys_in, keys_out, idx_in, idx_out, (int)n, 0, d * L + 1,
+                                     s));
+  BlockMap bm{nx, n, nbx};
+  k_count<KT><<<nbx + nbk, kBlk, 0, s>>>(keys_out, bm, d, L, ml, counts);
+  count_launch();
+  CK(cudaGetLastError());
+
+  fa.bm = bm;
+  fa.nbk = nbk;
+  for (int t = 0; t < 2; ++t) {
+    TreeOut& o = fa.t[t];
+    for (int l = 0; l < kMaxLevels; ++l) {
+      const bool ok = l <= L;
+      o.key[l] = ok ? (uint64_t*)(arena + o_key[t][l]) : nullptr;
+      o.parent[l] = ok ? (int32_t*)(arena + o_par[t][l]) : nullptr;
+      o.child_mask[l] = ok ? (uint32_t*)(arena + o_cm[t][l]) : nullptr;
+      o.child_begin[l] = ok ? (int32_t*)(arena + o_cb[t][l]) : nullptr;
+    }
+    o.first_pt = (int32_t*)(arena + o_first[t]);
+    o.leaf_of = (int32_t*)(arena + o_leafof[t]);
+    o.perm = (int32_t*)(arena + o_perm[t]);
+    o.pts_sorted = (double*)(arena + o_pts[t]);
+    o.pts = src[t];
+    o.totals = (int64_t*)(arena + o_tot[t]);
+  }
+  k_fill<KT><<<nbx + nbk, kBlk, 0, s>>>(keys_out, idx_out, ml, counts, fa, d, L);
+  count_launch();
+  CK(cudaGetLastError());
+
+  *scr_out = scr;
+  return SFT_OK;
 }
 
 int build_trees(sft_plan_s* P, const double* x_dev, const double* k_dev, std::string* err) {
@@ -261,67 +339,15 @@ int build_trees(sft_plan_s* P, const double* x_dev, const double* k_dev, std::st
   P->K.arena = nullptr;
   CK(cudaMemsetAsync(arena + cm_lo, 0, cm_hi - cm_lo, s));
 
-  // ---- scratch ----
-  const int nbx = (int)nblk(nx, kBlk), nbk = (int)nblk(nk, kBlk);
-  size_t cub_bytes = 0;
-  CK(cub::DeviceRadixSort::SortPairs(nullptr, cub_bytes, (uint64_t*)nullptr, (uint64_t*)nullptr, (int32_t*)nullptr,
-                                     (int32_t*)nullptr, (int)n, 0, d * L + 1, s));
-  size_t so = 0;
-  const size_t s_kin = so;
-  so = align_up(so + 8 * n, 256);
-  const size_t s_kout = so;
-  so = align_up(so + 8 * n, 256);
-  const size_t s_iin = so;
-  so = align_up(so + 4 * n, 256);
-  const size_t s_iout = so;
-  so = align_up(so + 4 * n, 256);
-  const size_t s_ml = so;
-  so = align_up(so + n, 256);
-  const size_t s_cnt = so;
-  so = align_up(so + 4 * (size_t)(nbx + nbk) * (L + 1), 256);
-  const size_t s_cub = so;
-  so = align_up(so + cub_bytes, 256);
+  // ---- sort + fill (32-bit point keys when d*L+1 <= 32) ----
   char* scr = nullptr;
-  CK(cudaMallocAsync((void**)&scr, so, s));
-  uint64_t* keys_in = (uint64_t*)(scr + s_kin);
-  uint64_t* keys_out = (uint64_t*)(scr + s_kout);
-  int32_t* idx_in = (int32_t*)(scr + s_iin);
-  int32_t* idx_out = (int32_t*)(scr + s_iout);
-  uint8_t* ml = (uint8_t*)(scr + s_ml);
-  int32_t* counts = (int32_t*)(scr + s_cnt);
-
-  k_leaf_keys<<<nblk(n, 256), 256, 0, s>>>(x_dev, nx, k_dev, nk, d, L, (double)P->N, P->N, keys_in, idx_in, P->d_err);
-  count_launch();
-  CK(cudaGetLastError());
-  CK(cub::DeviceRadixSort::SortPairs(scr + s_cub, cub_bytes, keys_in, keys_out, idx_in, idx_out, (int)n, 0, d * L + 1,
-                                     s));
-  BlockMap bm{nx, n, nbx};
-  k_count<<<nbx + nbk, kBlk, 0, s>>>(keys_out, bm, d, L, ml, counts);
-  count_launch();
-  CK(cudaGetLastError());
-
   FillArgs fa;
-  fa.bm = bm;
-  fa.nbk = nbk;
-  for (int t = 0; t < 2; ++t) {
-    TreeOut& o = fa.t[t];
-    for (int l = 0; l < kMaxLevels; ++l) {
-      const bool ok = l <= L;
-      o.key[l] = ok ? (uint64_t*)(arena + o_key[t][l]) : nullptr;
-      o.parent[l] = ok ? (int32_t*)(arena + o_par[t][l]) : nullptr;
-      o.child_mask[l] = ok ? (uint32_t*)(arena + o_cm[t][l]) : nullptr;
-      o.child_begin[l] = ok ? (int32_t*)(arena + o_cb[t][l]) : nullptr;
-    }
-    o.first_pt = (int32_t*)(arena + o_first[t]);
-    o.leaf_of = (int32_t*)(arena + o_leafof[t]);
-    o.perm = (int32_t*)(arena + o_perm[t]);
-    o.pts_sorted = (double*)(arena + o_pts[t]);
-    o.pts = src[t];
-    o.totals = (int64_t*)(arena + o_tot[t]);
-  }
-  k_fill<<<nbx + nbk, kBlk, 0, s>>>(keys_out, idx_out, ml, counts, fa, d, L);
-  count_launch();
-  CK(cudaGetLastError());
+  int rc = (d * L + 1 <= 32)
+               ? sort_and_fill<uint32_t>(P, x_dev, k_dev, arena, o_key, o_par, o_cm, o_cb, o_first, o_leafof, o_perm,
+                                         o_pts, o_tot, src, &scr, fa, err)
+               : sort_and_fill<uint64_t>(P, x_dev, k_dev, arena, o_key, o_par, o_cm, o_cb, o_first, o_leafof, o_perm,
+                                         o_pts, o_tot, src, &scr, fa, err);
+  if (rc) return rc;
 
   // ---- the one host sync: exact box counts + domain error flag ----
   std::vector<int64_t> h(2 * (L + 1));
