@@ -488,9 +488,14 @@ struct __align__(16) TaskRec {
 template <int D, int P, int G>
 struct Sched {
   static constexpr int MAXT = G << (D - 1);  // tasks per pass (max)
-  static constexpr int HDR = 48;
+  // task lists: 3D: list = axis of the pass (2, 1, 0 in order).  2D: list 1 =
+  // first pass on axis 1 and list 0 = last pass on axis 0 (default order);
+  // list 2 = first pass on axis 0 and list 3 = last pass on axis 1 (groups
+  // whose reversed axis order needs fewer MMA k-steps)
+  static constexpr int NL = D == 2 ? 4 : D;
+  static constexpr int HDR = 48;  // int cnt[NL][3]
   static constexpr int GRP = (8 * G + 15) / 16 * 16;
-  static constexpr int BLK = HDR + GRP + D * MAXT * (int)sizeof(TaskRec);
+  static constexpr int BLK = HDR + GRP + NL * MAXT * (int)sizeof(TaskRec);
   __device__ __forceinline__ static const int* cnt(const unsigned char* b) { return reinterpret_cast<const int*>(b); }
   __device__ __forceinline__ static const uint2* grp(const unsigned char* b) {
     return reinterpret_cast<const uint2*>(b + HDR);
@@ -503,17 +508,52 @@ struct Sched {
 // Task lists of pass AX for one tile: the tile's G groups sit in G adjacent
 // lanes (a warp holds 32/G tiles); entries packed in class order with scans
 // over the G-lane segment.
-template <int D, int P, int G, int PS, int AX, bool LAST>
+// REV (2D only): the axes are processed in the order 0, 1 instead of 1, 0.
+// Pass over axis 0 first: tasks by beta_1 (slots (0,b1), (1,b1)); then axis 1
+// (last): tasks by alpha_0 (slots (a0,0), (a0,1)), outputs (a0,0), (a0,1).
+template <int D, int P, int G, int PS, int AX, bool LAST, bool REV = false>
 __device__ __forceinline__ void schedule_pass(const TransArgs& a, const GroupMeta& m, bool valid, bool write_cnt,
                                               int* cnt, TaskRec* out) {
   constexpr int PD = PS;  // offsets in units of the array stride
   constexpr int NS = 1 << D;
   constexpr int SH = D - 1 - AX;
   constexpr int NE = 1 << (D - 1);
+  static_assert(!REV || D == 2, "reversed axis order is 2D only");
   const int lane = threadIdx.x & 31;
   TaskRec mine[NE];
   int n = 0, c3 = 0, c1 = 0, c2 = 0;
-  if (valid) {
+  if (REV && valid) {
+    // AX == 0 first: task b1 in {b1 : some (b0,b1) present}, slots (0,b1)/(1,b1)
+    // AX == 1 last:  task a0 in proj_hi(mA,1), slots (a0,0)/(a0,1), class = beta_1 presence
+    const uint32_t b1set = proj_lo<D>(m.mB, 1), a0set = proj_hi<D>(m.mA, 1);
+#pragma unroll
+    for (int v = 0; v < 2; ++v) {
+      if (!((AX == 0 ? b1set : a0set) >> v & 1)) continue;
+      TaskRec t;
+      uint32_t cls;
+      int slot0;
+      if (AX == 0) {
+        cls = (m.mB >> v & 1u) | ((m.mB >> (2 + v) & 1u) << 1);  // (0,b1), (1,b1)
+        slot0 = v;
+      } else {
+        cls = b1set;
+        slot0 = v << 1;
+      }
+      t.x = (uint32_t)(((lane % G) * NS + slot0) * PD);
+      t.cls = cls;
+      t.o0 = t.o1 = ~0u;
+      if (LAST) {
+        const int64_t q0 = out_pair(a, m, v << 1), q1 = out_pair(a, m, (v << 1) | 1);
+        if (q0 >= 0) t.o0 = (uint32_t)(q0 * PD);
+        if (q1 >= 0) t.o1 = (uint32_t)(q1 * PD);
+      }
+      mine[n++ & (NE - 1)] = t;
+      c3 += cls == 3;
+      c1 += cls == 1;
+      c2 += cls == 2;
+    }
+  }
+  if (!REV && valid) {
     const uint32_t PBp = AX > 0 ? proj_hi<D>(m.mB, AX) : 1u;
     const uint32_t PAs = proj_lo<D>(m.mA, D - 1 - AX);
     const uint32_t PBa = proj_hi<D>(m.mB, AX + 1);
@@ -618,8 +658,33 @@ __global__ __launch_bounds__(128) void k_schedule(const __grid_constant__ SchedL
   int* cnt = reinterpret_cast<int*>(b);  // written by the first lane of each valid tile only
   TaskRec* tk = reinterpret_cast<TaskRec*>(b + SC::HDR + SC::GRP);
   if constexpr (D == 2) {
-    schedule_pass<D, P, G, PS, 1, false>(a, m, valid, tv, cnt + 3, tk + SC::MAXT);
-    schedule_pass<D, P, G, PS, 0, true>(a, m, valid, tv, cnt, tk);
+    // axis order per group (from its own masks only, so identical for any
+    // partition of the work): the one with fewer MMA k-steps over its fiber
+    // rows (rows of a task with one live child skip that child's k-steps)
+    using S = MmaShape<P>;
+    constexpr int KB = S::NK, K0 = S::K0_HI, K1 = S::NK - S::K1_LO;
+    auto kc = [](uint32_t cls) { return cls == 3 ? KB : (cls == 1 ? K0 : (cls == 2 ? K1 : 0)); };
+    int cf = 0, cr = 0;  // default (axis 1 first) / reversed
+    if (valid) {
+      const uint32_t mB = m.mB, mA = m.mA;
+      const uint32_t b0set = proj_hi<D>(mB, 1), b1set = proj_lo<D>(mB, 1);
+      const int na1 = __popc(proj_lo<D>(mA, 1)), na0 = __popc(proj_hi<D>(mA, 1));
+      for (int v = 0; v < 2; ++v) {
+        if (b0set >> v & 1) cf += kc((mB >> (2 * v)) & 3u);
+        if (b1set >> v & 1) cr += kc((mB >> v & 1u) | ((mB >> (2 + v) & 1u) << 1));
+      }
+      cf += na1 * kc(b0set);
+      cr += na0 * kc(b1set);
+    }
+#ifdef SFT_FIXED_ORDER
+    const bool rev = false;
+#else
+    const bool rev = cr < cf;
+#endif
+    schedule_pass<D, P, G, PS, 1, false>(a, m, valid && !rev, tv, cnt + 3, tk + SC::MAXT);
+    schedule_pass<D, P, G, PS, 0, true>(a, m, valid && !rev, tv, cnt, tk);
+    schedule_pass<D, P, G, PS, 0, false, true>(a, m, valid && rev, tv, cnt + 6, tk + 2 * SC::MAXT);
+    schedule_pass<D, P, G, PS, 1, true, true>(a, m, valid && rev, tv, cnt + 9, tk + 3 * SC::MAXT);
   } else {
     schedule_pass<D, P, G, PS, 2, false>(a, m, valid, tv, cnt + 6, tk + 2 * SC::MAXT);
     schedule_pass<D, P, G, PS, 1, false>(a, m, valid, tv, cnt + 3, tk + SC::MAXT);
@@ -645,14 +710,14 @@ __global__ void k_check_schedule(TransArgs a, const unsigned char* __restrict__ 
     const int np = __popc(gr.y);
     if (np > 0 && (int64_t)gr.x + (int64_t)(np - 1) * a.in_nA >= in_pairs) bad = true;
   }
-  for (int ax = 0; ax < D; ++ax) {
+  for (int ax = 0; ax < SC::NL; ++ax) {
     const int* c = SC::cnt(b) + 3 * ax;
     const int nt = c[0] + c[1] + c[2];
     if (c[0] < 0 || c[1] < 0 || c[2] < 0 || nt > SC::MAXT) bad = true;
     for (int t = 0; t < nt && t < SC::MAXT; ++t) {
       const TaskRec r = SC::task(b, ax)[t];
       if (r.x >= STAGE || r.cls < 1 || r.cls > 3) bad = true;
-      if (ax == 0) {
+      if (ax == 0 || ax == 3) {
         if (r.o0 != ~0u && (int64_t)r.o0 / PD >= out_pairs) bad = true;
         if (r.o1 != ~0u && (int64_t)r.o1 / PD >= out_pairs) bad = true;
       }
@@ -666,7 +731,7 @@ __global__ void k_check_schedule(TransArgs a, const unsigned char* __restrict__ 
 #ifndef SFT_NSUB
 #define SFT_NSUB 1
 #endif
-template <int D, int P, int G, int NC, int AX, bool LAST>
+template <int D, int P, int G, int NC, int AX, bool LAST, int LIST = AX>
 __device__ __forceinline__ void consumer_pass(const TransArgs& a, double2* __restrict__ sb,
                                               const unsigned char* __restrict__ blk, const LaneOps<P>& op) {
   using S = MmaShape<P>;
@@ -676,8 +741,8 @@ __device__ __forceinline__ void consumer_pass(const TransArgs& a, double2* __res
   constexpr int PF = PD / P;
   constexpr int STR = Pow<P, D - 1 - AX>::v;
   constexpr int SH = D - 1 - AX;
-  const int* cnt = SC::cnt(blk) + 3 * AX;
-  const TaskRec* tasks = SC::task(blk, AX);
+  const int* cnt = SC::cnt(blk) + 3 * LIST;
+  const TaskRec* tasks = SC::task(blk, LIST);
   const int ntot = (cnt[0] + cnt[1] + cnt[2]) * PF;
   const int nst = __shfl_sync(0xffffffffu, (ntot + 7) >> 3, 0);
   const int lane = threadIdx.x & 31, warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
@@ -956,11 +1021,21 @@ __global__ __launch_bounds__((NC + 1) * 32, MINB) void k_translate_ws(TransArgs 
   int s = 0;
   uint32_t ph = 0;
   INSTR_T0(tc0);
+  // 2D: first passes (list 1: axis 1, list 2: axis 0 for groups in reversed
+  // order), then last passes (list 0: axis 0, list 3: axis 1)
+  auto first2d = [&](double2* sb_, const unsigned char* bk) {
+    consumer_pass<D, P, G, NC, D - 1, false, 1>(a, sb_, bk, op);
+    if constexpr (D == 2) consumer_pass<D, P, G, NC, 0, false, 2>(a, sb_, bk, op);
+  };
+  auto last2d = [&](double2* sb_, const unsigned char* bk) {
+    consumer_pass<D, P, G, NC, 0, true, 0>(a, sb_, bk, op);
+    if constexpr (D == 2) consumer_pass<D, P, G, NC, D - 1, true, 3>(a, sb_, bk, op);
+  };
   if constexpr (D == 2 && NST >= 3) {
     int64_t tile = blockIdx.x;
     if (tile < ntiles) {
       mbar_wait(smem_u32(&full[0]), 0);
-      consumer_pass<D, P, G, NC, 1, false>(a, ring, blk[0], op);
+      first2d(ring, blk[0]);
       asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&p1done[0])) : "memory");
     }
     for (; tile < ntiles; tile += gridDim.x) {
@@ -972,7 +1047,7 @@ __global__ __launch_bounds__((NC + 1) * 32, MINB) void k_translate_ws(TransArgs 
         mbar_wait(smem_u32(&full[sn]), phn);
         INSTR_ADD(4, tf0);
         INSTR_T0(t1);
-        consumer_pass<D, P, G, NC, 1, false>(a, ring + sn * STAGE, blk[sn], op);
+        first2d(ring + sn * STAGE, blk[sn]);
         asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&p1done[sn])) : "memory");
         INSTR_ADD(5, t1);
       }
@@ -980,7 +1055,7 @@ __global__ __launch_bounds__((NC + 1) * 32, MINB) void k_translate_ws(TransArgs 
       mbar_wait(smem_u32(&p1done[s]), ph);
       INSTR_ADD(6, t2);
       INSTR_T0(t3);
-      consumer_pass<D, P, G, NC, 0, true>(a, ring + s * STAGE, blk[s], op);
+      last2d(ring + s * STAGE, blk[s]);
       INSTR_ADD(7, t3);
       __syncwarp();
       if (lane == 0)
@@ -996,13 +1071,13 @@ __global__ __launch_bounds__((NC + 1) * 32, MINB) void k_translate_ws(TransArgs 
       double2* sb = ring + s * STAGE;
       if constexpr (D == 2) {
         INSTR_T0(t1);
-        consumer_pass<D, P, G, NC, 1, false>(a, sb, blk[s], op);
+        first2d(sb, blk[s]);
         INSTR_ADD(5, t1);
         INSTR_T0(t2);
         consumer_sync<NC * 32>();
         INSTR_ADD(6, t2);
         INSTR_T0(t3);
-        consumer_pass<D, P, G, NC, 0, true>(a, sb, blk[s], op);
+        last2d(sb, blk[s]);
         INSTR_ADD(7, t3);
       } else {
         consumer_pass<D, P, G, NC, 2, false>(a, sb, blk[s], op);
@@ -1037,7 +1112,7 @@ struct F32 {
 // One pass: chunk j (32 fibers) of this pass goes to consumer warp (base + j)
 // mod NC, `base` running over the whole sequence of passes so that warps
 // stay balanced however few fibers a pass has.  Returns the next base.
-template <int D, int P, int G, int NC, int AX, bool LAST>
+template <int D, int P, int G, int NC, int AX, bool LAST, int LIST = AX>
 __device__ __noinline__ int f32_consumer_pass(float2* __restrict__ out, float2* __restrict__ sb,
                                              const unsigned char* __restrict__ blk, int base, int warp) {
   using SC = Sched<D, P, G>;
@@ -1045,8 +1120,8 @@ __device__ __noinline__ int f32_consumer_pass(float2* __restrict__ out, float2* 
   constexpr int PF = Pow<P, D>::v / P;
   constexpr int STR = Pow<P, D - 1 - AX>::v;
   constexpr int SH = D - 1 - AX;
-  const int* cnt = SC::cnt(blk) + 3 * AX;
-  const TaskRec* tasks = SC::task(blk, AX);
+  const int* cnt = SC::cnt(blk) + 3 * LIST;
+  const TaskRec* tasks = SC::task(blk, LIST);
   const int ntot = (cnt[0] + cnt[1] + cnt[2]) * PF;
   const int nch = (ntot + 31) >> 5;
   const int lane = threadIdx.x & 31;
@@ -1117,6 +1192,16 @@ __global__ __launch_bounds__((NC + 1) * 32, MINB) void k_translate_f32(TransArgs
     return;
   }
   float2* out = reinterpret_cast<float2*>(a.out);
+  auto first2d = [&](float2* sb_, const unsigned char* bk, int b_) {
+    b_ = f32_consumer_pass<D, P, G, NC, D - 1, false, 1>(out, sb_, bk, b_, warp);
+    if constexpr (D == 2) b_ = f32_consumer_pass<D, P, G, NC, 0, false, 2>(out, sb_, bk, b_, warp);
+    return b_;
+  };
+  auto last2d = [&](float2* sb_, const unsigned char* bk, int b_) {
+    b_ = f32_consumer_pass<D, P, G, NC, 0, true, 0>(out, sb_, bk, b_, warp);
+    if constexpr (D == 2) b_ = f32_consumer_pass<D, P, G, NC, D - 1, true, 3>(out, sb_, bk, b_, warp);
+    return b_;
+  };
   int s = 0, base = 0;
   uint32_t ph = 0;
   auto release = [&](int st) {
@@ -1133,12 +1218,12 @@ __global__ __launch_bounds__((NC + 1) * 32, MINB) void k_translate_f32(TransArgs
       if (k > 0 && t1 - gridDim.x >= ntiles) break;
       if (t1 < ntiles) {
         mbar_wait(smem_u32(&full[s]), ph);
-        base = f32_consumer_pass<D, P, G, NC, 1, false>(out, ring + s * STAGE, blk[s], base, warp);
+        base = first2d(ring + s * STAGE, blk[s], base);
         asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&p1done[s])) : "memory");
       }
       if (k > 0) {
         mbar_wait(smem_u32(&p1done[sp]), php);
-        base = f32_consumer_pass<D, P, G, NC, 0, true>(out, ring + sp * STAGE, blk[sp], base, warp);
+        base = last2d(ring + sp * STAGE, blk[sp], base);
         release(sp);
       }
       sp = s;
@@ -1153,9 +1238,9 @@ __global__ __launch_bounds__((NC + 1) * 32, MINB) void k_translate_f32(TransArgs
       mbar_wait(smem_u32(&full[s]), ph);
       float2* sb = ring + s * STAGE;
       if constexpr (D == 2) {
-        base = f32_consumer_pass<D, P, G, NC, 1, false>(out, sb, blk[s], base, warp);
+        base = first2d(sb, blk[s], base);
         consumer_sync<NC * 32>();
-        base = f32_consumer_pass<D, P, G, NC, 0, true>(out, sb, blk[s], base, warp);
+        base = last2d(sb, blk[s], base);
       } else {
         base = f32_consumer_pass<D, P, G, NC, 2, false>(out, sb, blk[s], base, warp);
         consumer_sync<NC * 32>();
