@@ -461,6 +461,10 @@ extern "C" int sft_plan(int dim, int64_t N, int p, const double* x, int64_t nx, 
       cudaMemcpy(&fp[1], P->X.first_pt + P->x_rng[L].hi, sizeof(int32_t), cudaMemcpyDeviceToHost);
       P->x_pt_lo = fp[0];
       P->x_pt_hi = fp[1];
+      cudaMemcpy(&fp[0], P->K.first_pt + P->k_rng[L].lo, sizeof(int32_t), cudaMemcpyDeviceToHost);
+      cudaMemcpy(&fp[1], P->K.first_pt + P->k_rng[L].hi, sizeof(int32_t), cudaMemcpyDeviceToHost);
+      P->k_src_lo = fp[0];
+      P->k_src_hi = fp[1];
     }
     // exchange layout at level m: A boundaries at level L-m for every rank
     const int m = pt.m, W = P->world;
@@ -501,6 +505,8 @@ extern "C" int sft_plan(int dim, int64_t N, int p, const double* x, int64_t nx, 
     P->x_rng.assign(L + 1, LevelRange());
     P->x_pt_lo = 0;
     P->x_pt_hi = nx;
+    P->k_src_lo = 0;
+    P->k_src_hi = nk;
     for (int l = 0; l <= L; ++l) {
       P->k_rng[l].hi = P->K.counts[l];
       P->x_rng[l].hi = P->X.counts[l];

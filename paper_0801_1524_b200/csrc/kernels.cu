@@ -32,19 +32,60 @@ __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
 }
 
 // ------------------------------------------------------------------------
-// K2: leaf kernel, one warp per leaf B of T_K, one lane per source
-// ------------------------------------------------------------------------
-// Lane j (source k_j of B, s = k_j - c^B in [0,1]^d) evaluates its weights
+// K2: leaf kernel.  Warp k takes the leaves of T_K whose first source lies in
+// the window [W k, W (k+1)) of the sorted sources (W = 24: with <= 8 sources
+// per leaf a batch has <= 31 sources; larger leaves are handled in chunks).
+// Lane = source: s = k_j - c^B in [0,1]^d, the weights
 //   r_m(s_a) = invD_m prod_{q != m} sin(pi (s_a (p-1) - q)/(p-1)^2)
-// with one sincospi per axis (sin(theta - q delta) by angle addition, theta =
-// pi s_a/(p-1), delta = pi/(p-1)^2) and prefix/suffix products, and its
-// rotated charge f_j e^{i pi sum_a s_a}; then lane e (output element) sums
-// over the leaf's sources.  Sources beyond 32 are processed in chunks.
+// (one sincospi per axis, sines by angle addition theta - q delta with
+// theta = pi s_a/(p-1), delta = pi/(p-1)^2, prefix/suffix products) and the
+// rotated charge f_j e^{i pi sum_a s_a}, into shared memory; then, leaf by
+// leaf, lane = output element: h^{A0 B}_m = sum_j f'_j prod_a r_{m_a}(s_{j,a}).
+// ------------------------------------------------------------------------
+constexpr int kLeafWin = 24;
+
+template <int D, int P>
+__device__ __forceinline__ void leaf_weights(const double* __restrict__ k_sorted, const int32_t* __restrict__ perm,
+                                             const double2* __restrict__ f, int64_t N, int j, const double* cdq,
+                                             const double* sdq, const double* inv_s, double (*w)[P], double2* fo) {
+  constexpr int P1 = P - 1;
+  double ssum = 0.0;
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    const double kk = k_sorted[(int64_t)j * D + a];
+    const double sa = kk - fmin(floor(kk), (double)(N - 1));  // exact
+    ssum += sa;
+    double sn, cs;
+    sincospi(sa / (double)P1, &sn, &cs);
+    double sq[P], pre[P];
+#pragma unroll
+    for (int q = 0; q < P; ++q) sq[q] = fma(sn, cdq[q], -cs * sdq[q]);  // sin(theta - q delta)
+    double acc_p = 1.0;
+#pragma unroll
+    for (int m = 0; m < P; ++m) {
+      pre[m] = acc_p;
+      acc_p *= sq[m];
+    }
+    double suf = 1.0;
+#pragma unroll
+    for (int m = P - 1; m >= 0; --m) {
+      w[a][m] = inv_s[m] * pre[m] * suf;
+      suf *= sq[m];
+    }
+  }
+  double sn, cs;
+  sincospi(ssum, &sn, &cs);
+  *fo = cmul(f[perm[j]], make_double2(cs, sn));
+}
+
 template <int D, int P, typename T2, int PS>
-__global__ __launch_bounds__(128, D == 2 ? 4 : 2) void k_leaf(const double* __restrict__ k_sorted, const int32_t* __restrict__ perm,
-                                              const int32_t* __restrict__ first_pt,
-                                              const double2* __restrict__ f, const double* __restrict__ invD,
-                                              T2* __restrict__ out, int64_t b_lo, int64_t b_hi, int64_t N) {
+__global__ __launch_bounds__(128, D == 2 ? 4 : 2) void k_leaf(const double* __restrict__ k_sorted,
+                                                              const int32_t* __restrict__ perm,
+                                                              const int32_t* __restrict__ first_pt,
+                                                              const int32_t* __restrict__ leaf_of,
+                                                              const double2* __restrict__ f,
+                                                              const double* __restrict__ invD, T2* __restrict__ out,
+                                                              int64_t b_lo, int64_t b_hi, int64_t N) {
   constexpr int PD = Pow<P, D>::v;
   constexpr int NACC = (PD + 31) / 32;
   constexpr int P1 = P - 1;
@@ -60,75 +101,59 @@ __global__ __launch_bounds__(128, D == 2 ? 4 : 2) void k_leaf(const double* __re
   }
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t b = b_lo + blockIdx.x * 4 + warp;
-  if (b >= b_hi) return;
-  double2 acc[NACC];
-#pragma unroll
-  for (int i = 0; i < NACC; ++i) acc[i] = make_double2(0.0, 0.0);
-  const int j0 = first_pt[b], j1 = first_pt[b + 1];
-  for (int c0 = j0; c0 < j1; c0 += 32) {
-    const int n = min(32, j1 - c0);
-    if (lane < n) {
-      const int j = c0 + lane;
-      double ssum = 0.0;
-#pragma unroll
-      for (int a = 0; a < D; ++a) {
-        const double kk = k_sorted[(int64_t)j * D + a];
-        const double sa = kk - fmin(floor(kk), (double)(N - 1));  // exact
-        ssum += sa;
-        double sn, cs;
-        sincospi(sa / (double)P1, &sn, &cs);
-        double sq[P], pre[P];
-#pragma unroll
-        for (int q = 0; q < P; ++q) sq[q] = fma(sn, cdq[q], -cs * sdq[q]);  // sin(theta - q delta)
-        double acc_p = 1.0;
-#pragma unroll
-        for (int m = 0; m < P; ++m) {
-          pre[m] = acc_p;
-          acc_p *= sq[m];
-        }
-        double suf = 1.0;
-#pragma unroll
-        for (int m = P - 1; m >= 0; --m) {
-          w_s[warp][lane][a][m] = inv_s[m] * pre[m] * suf;
-          suf *= sq[m];
-        }
-      }
-      double sn, cs;
-      sincospi(ssum, &sn, &cs);
-      f_s[warp][lane] = cmul(f[perm[j]], make_double2(cs, sn));
-    }
+  const int64_t kw = (int64_t)blockIdx.x * 4 + warp;
+  // leaves [lb, le) of this warp: first source in [s0 + W kw, s0 + W (kw+1))
+  const int32_t s0 = first_pt[b_lo], s1 = first_pt[b_hi];
+  const int64_t w0 = s0 + (int64_t)kLeafWin * kw, w1 = s0 + (int64_t)kLeafWin * (kw + 1);
+  if (w0 >= s1) return;
+  auto lower = [&](int64_t v) {  // first leaf in [b_lo, b_hi] with first_pt >= v (leaf_of: two loads)
+    if (v >= s1) return b_hi;
+    const int64_t l = leaf_of[v];
+    return first_pt[l] >= v ? l : l + 1;
+  };
+  const int64_t lb = lower(w0), le = lower(w1);
+  if (lb >= le) return;
+  const int js = first_pt[lb], je = first_pt[le];
+  for (int c0 = js; c0 < je; c0 += 32) {
+    // weights of the sources [c0, c0 + 32) of this batch
+    const int n = min(32, je - c0);
+    if (lane < n) leaf_weights<D, P>(k_sorted, perm, f, N, c0 + lane, cdq, sdq, inv_s, w_s[warp][lane], &f_s[warp][lane]);
     __syncwarp();
-    for (int t = 0; t < n; ++t) {
-      const double2 fj = f_s[warp][t];
+    // leaves whose sources intersect [c0, c0 + n)
+    for (int64_t b = lb; b < le; ++b) {
+      const int jb0 = first_pt[b], jb1 = first_pt[b + 1];
+      if (jb1 <= c0 || jb0 >= c0 + n) continue;
+      const int t0 = max(jb0, c0) - c0, t1 = min(jb1, c0 + n) - c0;
+      T2* o = out + (b - b_lo) * (int64_t)PS;
 #pragma unroll
       for (int i = 0; i < NACC; ++i) {
         const int e = lane + 32 * i;
         if (e < PD) {
-          double w = 1.0;
-          int r = e;
-#pragma unroll
-          for (int a = D - 1; a >= 0; --a) {
-            w *= w_s[warp][t][a][r % P];
-            r /= P;
+          double2 acc = make_double2(0.0, 0.0);
+          if (jb0 < c0) {  // continuing a leaf from the previous chunk
+            const T2 v = o[e];
+            acc = make_double2(v.x, v.y);
           }
-          acc[i].x = fma(w, fj.x, acc[i].x);
-          acc[i].y = fma(w, fj.y, acc[i].y);
+          for (int t = t0; t < t1; ++t) {
+            const double2 fj = f_s[warp][t];
+            double w = 1.0;
+            int r = e;
+#pragma unroll
+            for (int a = D - 1; a >= 0; --a) {
+              w *= w_s[warp][t][a][r % P];
+              r /= P;
+            }
+            acc.x = fma(w, fj.x, acc.x);
+            acc.y = fma(w, fj.y, acc.y);
+          }
+          T2 v;
+          v.x = acc.x;
+          v.y = acc.y;
+          o[e] = v;
         }
       }
     }
     __syncwarp();
-  }
-  T2* o = out + (b - b_lo) * (int64_t)PS;
-#pragma unroll
-  for (int i = 0; i < NACC; ++i) {
-    const int e = lane + 32 * i;
-    if (e < PD) {
-      T2 v;
-      v.x = acc[i].x;
-      v.y = acc[i].y;
-      o[e] = v;
-    }
   }
 }
 
@@ -214,16 +239,19 @@ __global__ void k_zero(double2* p, int64_t n) {
 
 cudaError_t launch_leaf(const sft_plan_s* Pl, const double2* f, void* out, int64_t b_lo, int64_t b_hi) {
   if (b_hi <= b_lo) return cudaSuccess;
-  const unsigned nb = (unsigned)((b_hi - b_lo + 3) / 4);
+  // sources of leaves [b_lo, b_hi): one warp per window of kLeafWin sources
+  const int64_t ns = b_lo == 0 && b_hi == Pl->K.counts[Pl->L] ? Pl->nk : Pl->k_src_hi - Pl->k_src_lo;
+  const int64_t nw = (ns + kLeafWin - 1) / kLeafWin;
+  const unsigned nb = (unsigned)((nw + 3) / 4);
   if (Pl->prec == 1) {
     SFT_DISPATCH(Pl->d, Pl->p,
                  (k_leaf<D, P, float2, Pow<P, D>::v + (Pow<P, D>::v & 1)><<<nb, 128, 0, Pl->stream>>>(
-                     Pl->K.pts_sorted, Pl->K.perm, Pl->K.first_pt, f, Pl->tab->leaf_invD, (float2*)out, b_lo, b_hi,
+                     Pl->K.pts_sorted, Pl->K.perm, Pl->K.first_pt, Pl->K.leaf_of, f, Pl->tab->leaf_invD, (float2*)out, b_lo, b_hi,
                      Pl->N)));
   } else {
     SFT_DISPATCH(Pl->d, Pl->p,
                  (k_leaf<D, P, double2, Pow<P, D>::v><<<nb, 128, 0, Pl->stream>>>(
-                     Pl->K.pts_sorted, Pl->K.perm, Pl->K.first_pt, f, Pl->tab->leaf_invD, (double2*)out, b_lo, b_hi,
+                     Pl->K.pts_sorted, Pl->K.perm, Pl->K.first_pt, Pl->K.leaf_of, f, Pl->tab->leaf_invD, (double2*)out, b_lo, b_hi,
                      Pl->N)));
   }
   count_launch();

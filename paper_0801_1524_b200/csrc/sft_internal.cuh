@@ -92,6 +92,7 @@ struct sft_plan_s {
   std::vector<sft::LevelRange> k_rng;  // [L+1] this rank's T_K range per level (phase 1)
   std::vector<sft::LevelRange> x_rng;  // [L+1] this rank's T_X range per level (phase 2)
   int64_t x_pt_lo = 0, x_pt_hi = 0;     // sorted target range of this rank's T_X leaves
+  int64_t k_src_lo = 0, k_src_hi = 0;   // sorted source range of this rank's T_K leaves
   std::vector<int64_t> send_counts, recv_counts;  // [world] complex elements
   int64_t* d_seg = nullptr;  // device [2*world+1]: a-boundaries at level L-m, send segment bases
   // tile schedules of the translation levels (one allocation; offsets per level t)
