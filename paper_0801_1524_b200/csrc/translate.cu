@@ -323,7 +323,11 @@ template <int P>
 struct MmaShape {
   static constexpr int K = 2 * P;                 // stacked child elements
   static constexpr int NK = (K + 3) / 4;          // k-steps of 4
+#ifdef SFT_TAIL_DMMA
+  static constexpr bool TAIL = false;             // m = P-1 in a third N tile on the tensor cores
+#else
   static constexpr bool TAIL = (P % 4) == 1;      // m = P-1 by DFMA
+#endif
   static constexpr int NM = TAIL ? P - 1 : P;     // m's on the tensor cores
   static constexpr int NT = (2 * NM + 7) / 8;     // N tiles of 8 (P_m, Q_m interleaved)
   static constexpr int K0_HI = (P + 3) / 4;       // k-steps [0, K0_HI) hold child-0 elements

@@ -227,3 +227,55 @@ def test_fp32_c2_sampled_vs_direct():
     tg = w.sample[:1024]
     ud = oracle.direct(w.x[tg], w.k, w.f, w.N)
     assert oracle.rel_l2(u[tg], ud) <= DIRECT_TOL[9]
+
+
+def test_dense_leaves_chunked_paths():
+    """Leaves with many more points than a warp has lanes: 200 sources and 150
+    targets inside single unit boxes (k_leaf processes a leaf's sources in
+    chunks of 32 and its window/leaf_of ranges; k_final reads one leaf's
+    charges for many targets), mixed with a curve of ordinary points."""
+    N = 64
+    rng = np.random.default_rng(11)
+    w = synth.make_workload("C0")
+    k = np.concatenate([w.k, 17.0 + rng.uniform(0, 1, (200, 2)), 40.0 + rng.uniform(0, 1, (45, 2))])
+    x = np.concatenate([w.x, 33.0 + rng.uniform(0, 1, (150, 2))])
+    f = rng.normal(size=len(k)) + 1j * rng.normal(size=len(k))
+    for p in (5, 9):
+        u, _ = gpu_transform(x, k, f, N, p)
+        ub = oracle.butterfly(x, k, f, N, p)
+        assert oracle.rel_l2(u, ub) <= PARITY
+
+
+def test_dense_leaves_3d():
+    N = 16
+    rng = np.random.default_rng(12)
+    k = np.concatenate([rng.uniform(0, N, (300, 3)), 5.0 + rng.uniform(0, 1, (120, 3))])
+    x = np.concatenate([rng.uniform(0, N, (300, 3)), 9.0 + rng.uniform(0, 1, (80, 3))])
+    f = rng.normal(size=len(k)) + 1j * rng.normal(size=len(k))
+    u, _ = gpu_transform(x, k, f, N, 7)
+    ub = oracle.butterfly(x, k, f, N, 7)
+    assert oracle.rel_l2(u, ub) <= PARITY
+
+
+def test_schedule_invariants_checker():
+    """SFT_CHECK_SCHED=1: sft_plan validates every level's tile schedule
+    (counts, stage offsets, classes, HBM offsets) on the device."""
+    import os
+    import subprocess
+    import sys
+    code = ("import sys; sys.path.insert(0, %r); import torch, synth, paper_0801_1524_b200 as sft;"
+            "w = synth.make_workload('C1');"
+            "pl = sft.Plan(2, w.N, w.p, torch.from_numpy(w.x).cuda(), torch.from_numpy(w.k).cuda());"
+            "u = pl.apply(torch.from_numpy(w.f).cuda()); torch.cuda.synchronize(); print('ok')") % (
+        os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    env = dict(os.environ, SFT_CHECK_SCHED="1")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+def test_fp32_rejects_multirank():
+    torch = _torch()
+    import paper_0801_1524_b200 as sft
+    w = synth.make_workload("C0")
+    with pytest.raises(sft.SftError):
+        sft.Plan(2, w.N, 5, torch.from_numpy(w.x).cuda(), torch.from_numpy(w.k).cuda(), rank=0, world=2, precision=1)
