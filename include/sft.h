@@ -62,9 +62,15 @@ typedef struct {
   int exchange_level; /* world > 1: level m of the charge exchange; -1 = choose */
   int split_k;        /* world > 1: T_K subtree level s_K; -1 = choose */
   int split_x;        /* world > 1: T_X subtree level s_X; -1 = choose */
+  int adjoint;        /* 1: the plan applies the adjoint transform
+                       *    v_j = sum_i exp(-2*pi*i x_i . k_j / N) g_i   (g on the x points,
+                       *    v on the k points; eq. sfft conjugate-transposed) -- the same
+                       *    butterfly with the roles of the point sets swapped and the
+                       *    charges / potentials conjugated; sft_apply then takes g [nx]
+                       *    and writes v [nk].  0 = forward (default).  world == 1 only. */
 } sft_opts;
 
-/* Fill *o with defaults: FP64, NULL stream, rank 0, world 1, automatic levels. */
+/* Fill *o with defaults: FP64, NULL stream, rank 0, world 1, automatic levels, forward. */
 void sft_default_opts(sft_opts* o);
 
 /* Step 1: build T_X from targets x and T_K from sources k.

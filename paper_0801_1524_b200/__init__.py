@@ -38,7 +38,7 @@ class SftError(RuntimeError):
 class _Opts(ctypes.Structure):
     _fields_ = [("precision", ctypes.c_int), ("stream", ctypes.c_void_p), ("rank", ctypes.c_int),
                 ("world", ctypes.c_int), ("exchange_level", ctypes.c_int), ("split_k", ctypes.c_int),
-                ("split_x", ctypes.c_int)]
+                ("split_x", ctypes.c_int), ("adjoint", ctypes.c_int)]
 
 
 _lib = None
@@ -128,13 +128,16 @@ class Plan:
     """sft_plan / sft_apply / sft_destroy (include/sft.h)."""
 
     def __init__(self, dim, N, p, x, k, stream=None, rank=0, world=1, exchange_level=-1, split_k=-1, split_x=-1,
-                 precision=0):
+                 precision=0, adjoint=False):
         """precision 0: FP64 charges (default); 1: the FP32 variant (single GPU;
-        f and u stay complex128 at the boundary, the level charges are complex64)."""
+        f and u stay complex128 at the boundary, the level charges are complex64).
+        adjoint=True: apply() computes v_j = sum_i exp(-2 pi i x_i.k_j/N) g_i
+        (g on the x points, v on the k points)."""
         L = lib()
         o = _Opts()
         L.sft_default_opts(ctypes.byref(o))
         o.precision = int(precision)
+        o.adjoint = 1 if adjoint else 0
         o.stream = _stream_handle(stream)
         o.rank, o.world = int(rank), int(world)
         o.exchange_level, o.split_k, o.split_x = int(exchange_level), int(split_k), int(split_x)
@@ -143,6 +146,7 @@ class Plan:
         self.dim, self.N, self.p = int(dim), int(N), int(p)
         self.nx = int(self._x.shape[0]) if len(self._x.shape) else 0
         self.nk = int(self._k.shape[0]) if len(self._k.shape) else 0
+        self.adjoint = bool(adjoint)
         self.world, self.rank = int(world), int(rank)
         self.L = int(N).bit_length() - 1
         h = ctypes.c_void_p()
@@ -155,7 +159,7 @@ class Plan:
         """u = butterfly(f).  If ``u`` is None a buffer like ``f`` (device or host) is allocated."""
         fp, fk = _ptr(f, np.complex128)
         if u is None:
-            u = self._like(fk, self.nx)
+            u = self._like(fk, self.nk if self.adjoint else self.nx)
         up, uk = _ptr(u, np.complex128)
         _check(lib().sft_apply(self._h, fp, up))
         return uk

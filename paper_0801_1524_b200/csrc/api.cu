@@ -52,6 +52,7 @@ extern "C" void sft_default_opts(sft_opts* o) {
   o->exchange_level = -1;
   o->split_k = -1;
   o->split_x = -1;
+  o->adjoint = 0;
 }
 
 extern "C" const char* sft_strerror(int status) {
@@ -364,8 +365,15 @@ extern "C" int sft_plan(int dim, int64_t N, int p, const double* x, int64_t nx, 
   if (o.precision == 1 && o.world != 1) return fail(SFT_E_ARG, "the FP32 variant is single-GPU (world == 1)");
   if (o.world < 1 || o.rank < 0 || o.rank >= o.world) return fail(SFT_E_ARG, "bad rank/world");
 
+  if (o.adjoint && o.world != 1) return fail(SFT_E_ARG, "the adjoint plan is single-GPU (world == 1)");
+  if (o.adjoint) {
+    // adjoint = conj o forward(targets k, sources x) o conj: swap the point sets
+    std::swap(x, k);
+    std::swap(nx, nk);
+  }
   sft_plan_s* P = new (std::nothrow) sft_plan_s();
   if (!P) return fail(SFT_E_NOMEM, "host allocation failed");
+  P->conj = o.adjoint ? 1 : 0;
   P->d = dim;
   P->p = p;
   P->N = N;

@@ -46,7 +46,7 @@ constexpr int kLeafWin = 24;
 
 template <int D, int P>
 __device__ __forceinline__ void leaf_weights(const double* __restrict__ k_sorted, const int32_t* __restrict__ perm,
-                                             const double2* __restrict__ f, int64_t N, int j, const double* cdq,
+                                             const double2* __restrict__ f, int conj, int64_t N, int j, const double* cdq,
                                              const double* sdq, const double* inv_s, double (*w)[P], double2* fo) {
   constexpr int P1 = P - 1;
   double ssum = 0.0;
@@ -75,7 +75,9 @@ __device__ __forceinline__ void leaf_weights(const double* __restrict__ k_sorted
   }
   double sn, cs;
   sincospi(ssum, &sn, &cs);
-  *fo = cmul(f[perm[j]], make_double2(cs, sn));
+  double2 fj = f[perm[j]];
+  if (conj) fj.y = -fj.y;
+  *fo = cmul(fj, make_double2(cs, sn));
 }
 
 template <int D, int P, typename T2, int PS>
@@ -85,7 +87,7 @@ __global__ __launch_bounds__(128, D == 2 ? 4 : 2) void k_leaf(const double* __re
                                                               const int32_t* __restrict__ leaf_of,
                                                               const double2* __restrict__ f,
                                                               const double* __restrict__ invD, T2* __restrict__ out,
-                                                              int64_t b_lo, int64_t b_hi, int64_t N) {
+                                                              int64_t b_lo, int64_t b_hi, int64_t N, int conj) {
   constexpr int PD = Pow<P, D>::v;
   constexpr int NACC = (PD + 31) / 32;
   constexpr int P1 = P - 1;
@@ -117,7 +119,7 @@ __global__ __launch_bounds__(128, D == 2 ? 4 : 2) void k_leaf(const double* __re
   for (int c0 = js; c0 < je; c0 += 32) {
     // weights of the sources [c0, c0 + 32) of this batch
     const int n = min(32, je - c0);
-    if (lane < n) leaf_weights<D, P>(k_sorted, perm, f, N, c0 + lane, cdq, sdq, inv_s, w_s[warp][lane], &f_s[warp][lane]);
+    if (lane < n) leaf_weights<D, P>(k_sorted, perm, f, conj, N, c0 + lane, cdq, sdq, inv_s, w_s[warp][lane], &f_s[warp][lane]);
     __syncwarp();
     // leaves whose sources intersect [c0, c0 + n)
     for (int64_t b = lb; b < le; ++b) {
@@ -170,7 +172,7 @@ template <int D, int P, typename T2, int PS>
 __global__ __launch_bounds__(128) void k_final(const double* __restrict__ x_sorted, const int32_t* __restrict__ perm,
                                                const int32_t* __restrict__ leaf_of,
                                                const T2* __restrict__ h0, double2* __restrict__ u,
-                                               int64_t i_lo, int64_t i_hi, int64_t a_lo, int64_t N) {
+                                               int64_t i_lo, int64_t i_hi, int64_t a_lo, int64_t N, int conj) {
   constexpr int P1 = P - 1;
   const int64_t j = i_lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (j >= i_hi) return;
@@ -225,6 +227,7 @@ __global__ __launch_bounds__(128) void k_final(const double* __restrict__ x_sort
       w0 = cmul(w0, z[0]);
     }
   }
+  if (conj) s.y = -s.y;
   u[perm[j]] = s;
 }
 
@@ -247,12 +250,12 @@ cudaError_t launch_leaf(const sft_plan_s* Pl, const double2* f, void* out, int64
     SFT_DISPATCH(Pl->d, Pl->p,
                  (k_leaf<D, P, float2, Pow<P, D>::v + (Pow<P, D>::v & 1)><<<nb, 128, 0, Pl->stream>>>(
                      Pl->K.pts_sorted, Pl->K.perm, Pl->K.first_pt, Pl->K.leaf_of, f, Pl->tab->leaf_invD, (float2*)out, b_lo, b_hi,
-                     Pl->N)));
+                     Pl->N, Pl->conj)));
   } else {
     SFT_DISPATCH(Pl->d, Pl->p,
                  (k_leaf<D, P, double2, Pow<P, D>::v><<<nb, 128, 0, Pl->stream>>>(
                      Pl->K.pts_sorted, Pl->K.perm, Pl->K.first_pt, Pl->K.leaf_of, f, Pl->tab->leaf_invD, (double2*)out, b_lo, b_hi,
-                     Pl->N)));
+                     Pl->N, Pl->conj)));
   }
   count_launch();
   return cudaGetLastError();
@@ -265,11 +268,11 @@ cudaError_t launch_final(const sft_plan_s* Pl, const void* h0, double2* u, int64
   if (Pl->prec == 1) {
     SFT_DISPATCH(Pl->d, Pl->p,
                  (k_final<D, P, float2, Pow<P, D>::v + (Pow<P, D>::v & 1)><<<nb, 128, 0, Pl->stream>>>(
-                     Pl->X.pts_sorted, Pl->X.perm, Pl->X.leaf_of, (const float2*)h0, u, i_lo, i_hi, a_lo, Pl->N)));
+                     Pl->X.pts_sorted, Pl->X.perm, Pl->X.leaf_of, (const float2*)h0, u, i_lo, i_hi, a_lo, Pl->N, Pl->conj)));
   } else {
     SFT_DISPATCH(Pl->d, Pl->p,
                  (k_final<D, P, double2, Pow<P, D>::v><<<nb, 128, 0, Pl->stream>>>(
-                     Pl->X.pts_sorted, Pl->X.perm, Pl->X.leaf_of, (const double2*)h0, u, i_lo, i_hi, a_lo, Pl->N)));
+                     Pl->X.pts_sorted, Pl->X.perm, Pl->X.leaf_of, (const double2*)h0, u, i_lo, i_hi, a_lo, Pl->N, Pl->conj)));
   }
   count_launch();
   return cudaGetLastError();

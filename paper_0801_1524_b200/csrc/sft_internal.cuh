@@ -76,6 +76,7 @@ struct sft_plan_s {
   int64_t N = 0, nx = 0, nk = 0;
   int rank = 0, world = 1;
   int prec = 0;  // 0 = FP64 charges (complex128), 1 = FP32 charges (complex64)
+  int conj = 0;  // adjoint plan: conjugate the charges on input and the potentials on output
   int pds = 0;   // stride (complex elements) of one pair array in the level buffers
   cudaStream_t stream = nullptr;
   sft::Tree X, K;

@@ -279,3 +279,27 @@ def test_fp32_rejects_multirank():
     w = synth.make_workload("C0")
     with pytest.raises(sft.SftError):
         sft.Plan(2, w.N, 5, torch.from_numpy(w.x).cuda(), torch.from_numpy(w.k).cuda(), rank=0, world=2, precision=1)
+
+
+@pytest.mark.parametrize("p", [5, 9])
+def test_adjoint(p):
+    """opts.adjoint: v_j = sum_i exp(-2 pi i x_i.k_j / N) g_i (the conjugate
+    transpose of eq. sfft): the oracle's direct sum of the conjugate
+    and the oracle butterfly with the point sets swapped."""
+    torch = _torch()
+    import paper_0801_1524_b200 as sft
+    w = synth.make_workload("C0", p=p)
+    g = synth.random_charges(len(w.x), 9)
+    with sft.Plan(2, w.N, p, torch.from_numpy(w.x).cuda(), torch.from_numpy(w.k).cuda(), adjoint=True) as plan:
+        v = plan.apply(torch.from_numpy(g).cuda()).cpu().numpy()
+    assert v.shape == (len(w.k),)
+    vb = np.conj(oracle.butterfly(w.k, w.x, np.conj(g), w.N, p))
+    assert oracle.rel_l2(v, vb) <= PARITY
+    vd = np.conj(oracle.direct(w.k, w.x, np.conj(g), w.N))
+    assert oracle.rel_l2(v, vd) <= DIRECT_TOL[p]
+    # <A f, g> = <f, A^H g>
+    f = w.f
+    with sft.Plan(2, w.N, p, torch.from_numpy(w.x).cuda(), torch.from_numpy(w.k).cuda()) as plan:
+        u = plan.apply(torch.from_numpy(f).cuda()).cpu().numpy()
+    lhs, rhs = np.vdot(g, u), np.vdot(v, f)
+    assert abs(lhs - rhs) <= 5 * DIRECT_TOL[p] * np.linalg.norm(g) * np.linalg.norm(u)
