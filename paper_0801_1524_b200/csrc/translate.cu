@@ -917,6 +917,11 @@ __device__ __forceinline__ void ws_producer(const TransArgs& a, const unsigned c
     int64_t tile = blockIdx.x;
     uint2 gr = (tile < ntiles && lane < G) ? __ldg(reinterpret_cast<const uint2*>(sched + tile * SC::BLK + SC::HDR) + lane)
                                            : make_uint2(0u, 0u);
+    // programmatic dependent launch: everything above (schedule reads, barrier
+    // init, the consumers' operand loads) overlaps the previous level's tail;
+    // the previous level's output (our input) and input (our output buffer)
+    // are touched only after it has completed
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     for (int i = 0; tile < ntiles; ++i) {
       const int64_t next = tile + gridDim.x;
       const uint2 gn = (next < ntiles && lane < G)
@@ -1491,6 +1496,16 @@ static TransArgs make_args(const LevelDims& L, const double2* in, double2* out) 
   return a;
 }
 
+// SFT_PDL=0 disables programmatic dependent launch (ablation)
+static bool pdl_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SFT_PDL");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 // SFT_TRANSLATE = mma (DMMA consumers, default) | fma (round-1 kernel)
 int translate_kernel_choice() {
   static int mode = -1;
@@ -1503,6 +1518,25 @@ int translate_kernel_choice() {
 }
 
 // groups per tile of the schedule for the selected kernel (0: no schedule)
+// Launch with programmatic stream serialization (PDL): the kernel may start
+// while the previous kernel on the stream drains; it must execute
+// griddepcontrol.wait before touching that kernel's data.
+template <typename... KArgs, typename... Args>
+static void launch_pdl(void (*kernel)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t st,
+                       Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 // resident-CTA grid size for a persistent kernel
 template <class K>
 static cudaError_t persistent_grid(K kernel, int threads, size_t smem, int* grid) {
@@ -1534,7 +1568,8 @@ static cudaError_t launch_translate_t(const sft_plan_s* Pl, const LevelDims& L, 
     if (!L.sched) return cudaErrorInvalidValue;
     const int64_t ntiles = (a.ngroups + G - 1) / G;
     const int64_t grid = std::min<int64_t>(ntiles, grid_max);
-    k_translate_f32<D, P, G, NC, NST, MB><<<(unsigned)grid, (NC + 1) * 32, smem, Pl->stream>>>(a, L.sched, ntiles);
+    launch_pdl(k_translate_f32<D, P, G, NC, NST, MB>, (unsigned)grid, (NC + 1) * 32, smem, Pl->stream, a, L.sched,
+               ntiles);
   } else if (translate_kernel_choice() == 0) {
     constexpr int G = WsCfg<D, P>::G, NC = WsCfg<D, P>::NC, NST = WsCfg<D, P>::NST, MB = WsCfg<D, P>::MINB;
     const size_t smem = (size_t)NST * G * (1 << D) * PD * sizeof(double2);
@@ -1549,7 +1584,8 @@ static cudaError_t launch_translate_t(const sft_plan_s* Pl, const LevelDims& L, 
     if (!L.sched) return cudaErrorInvalidValue;
     const int64_t ntiles = (a.ngroups + G - 1) / G;
     const int64_t grid = std::min<int64_t>(ntiles, grid_max);
-    k_translate_ws<D, P, G, NC, NST, MB><<<(unsigned)grid, (NC + 1) * 32, smem, Pl->stream>>>(a, frag, L.sched, ntiles);
+    launch_pdl(k_translate_ws<D, P, G, NC, NST, MB>, (unsigned)grid, (NC + 1) * 32, smem, Pl->stream, a, frag,
+               L.sched, ntiles);
   } else {
     constexpr int G = FmaCfg<D, P>::G, NT = FmaCfg<D, P>::NT;
     const size_t smem = (size_t)G * (1 << D) * PD * sizeof(double2);
