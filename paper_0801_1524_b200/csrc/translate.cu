@@ -335,6 +335,29 @@ struct MmaShape {
   static constexpr int NFRAG = NK * NT * 32 + (TAIL ? NK * 2 * 32 : 0);  // doubles in the table
 };
 
+// complex element of the level buffers / stages: double2 (FP64) or float2
+// (FP32 storage variant; the arithmetic stays FP64 on the tensor cores)
+template <typename E>
+struct ElemT;
+template <>
+struct ElemT<double2> {
+  using scalar = double;
+  __device__ __forceinline__ static double2 ld(const double2& v) { return v; }
+  __device__ __forceinline__ static double2 mk(double re, double im) { return make_double2(re, im); }
+};
+template <>
+struct ElemT<float2> {
+  using scalar = float;
+  __device__ __forceinline__ static double2 ld(const float2& v) { return make_double2(v.x, v.y); }
+  __device__ __forceinline__ static float2 mk(double re, double im) { return make_float2((float)re, (float)im); }
+};
+// pair-array stride (elements) in buffers and stages: FP32 arrays padded to an
+// even count so every array is a multiple of 16 bytes (bulk copies)
+template <typename E, int PD>
+struct StrideT {
+  static constexpr int v = sizeof(E) == 8 ? PD + (PD & 1) : PD;
+};
+
 // first k-step: D = A*B (C = 0)
 __device__ __forceinline__ void dmma0(double (&d)[2], double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%4,%4};"
@@ -359,8 +382,8 @@ struct LaneOps {
 // k-steps [K_LO, K_HI) of one MMA super-tile: A fragments (re and im of one
 // complex element per lane, one 16-byte shared-memory load) times the B
 // fragments held in registers; tail column m = P-1 on DFMA.
-template <int P, int K_LO, int K_HI, int NSUB>
-__device__ __forceinline__ void mma_steps(const LaneOps<P>& op, const double2* const (&x)[NSUB],
+template <int P, int K_LO, int K_HI, int NSUB, typename E = double2>
+__device__ __forceinline__ void mma_steps(const LaneOps<P>& op, const E* const (&x)[NSUB],
                                           const int (&off)[MmaShape<P>::NK], const bool (&p0)[NSUB],
                                           const bool (&p1)[NSUB], double (&are)[NSUB][MmaShape<P>::NT][2],
                                           double (&aim)[NSUB][MmaShape<P>::NT][2], double (&tl)[NSUB][4]) {
@@ -373,11 +396,11 @@ __device__ __forceinline__ void mma_steps(const LaneOps<P>& op, const double2* c
 #ifdef SFT_NO_ZEROFILL
       const int b = op.bk[kk];
       const bool live = b == 0 ? p0[u] : (b == 1 ? p1[u] : false);
-      av[u] = live ? x[u][off[kk]] : make_double2(0.0, 0.0);
+      av[u] = live ? ElemT<E>::ld(x[u][off[kk]]) : make_double2(0.0, 0.0);
 #else
       // absent children's slots are zero-filled by the producer and the B
       // rows of padding k are zero: no masking needed
-      av[u] = x[u][off[kk]];
+      av[u] = ElemT<E>::ld(x[u][off[kk]]);
 #endif
     }
 #pragma unroll
@@ -735,14 +758,15 @@ __global__ void k_check_schedule(TransArgs a, const unsigned char* __restrict__ 
 #ifndef SFT_NSUB
 #define SFT_NSUB 1
 #endif
-template <int D, int P, int G, int NC, int AX, bool LAST, int LIST = AX>
-__device__ __forceinline__ void consumer_pass(const TransArgs& a, double2* __restrict__ sb,
+template <int D, int P, int G, int NC, int AX, bool LAST, int LIST = AX, typename E = double2>
+__device__ __forceinline__ void consumer_pass(const TransArgs& a, E* __restrict__ sb,
                                               const unsigned char* __restrict__ blk, const LaneOps<P>& op) {
   using S = MmaShape<P>;
   using SC = Sched<D, P, G>;
   constexpr int NSUB = SFT_NSUB;
-  constexpr int PD = Pow<P, D>::v;
-  constexpr int PF = PD / P;
+  constexpr int PF = Pow<P, D>::v / P;
+  constexpr int PD = StrideT<E, Pow<P, D>::v>::v;  // slot stride (elements)
+  E* const gout = reinterpret_cast<E*>(a.out);
   constexpr int STR = Pow<P, D - 1 - AX>::v;
   constexpr int SH = D - 1 - AX;
   const int* cnt = SC::cnt(blk) + 3 * LIST;
@@ -756,9 +780,9 @@ __device__ __forceinline__ void consumer_pass(const TransArgs& a, double2* __res
 #pragma unroll
   for (int kk = 0; kk < S::NK; ++kk) off[kk] = (op.bk[kk] == 1 ? (1 << SH) * PD : 0) + op.lk[kk] * STR;
   for (int st0 = warp * NSUB; st0 < nst; st0 += NC * NSUB) {
-    const double2* x[NSUB];
-    double2* o0[NSUB];
-    double2* o1[NSUB];
+    const E* x[NSUB];
+    E* o0[NSUB];
+    E* o1[NSUB];
     bool p0[NSUB], p1[NSUB];
     int any = 0;
 #pragma unroll
@@ -785,8 +809,8 @@ __device__ __forceinline__ void consumer_pass(const TransArgs& a, double2* __res
       o0[u] = o1[u] = nullptr;
 #else
       if (LAST) {
-        o0[u] = d.o0 != ~0u ? a.out + d.o0 + ebase : nullptr;
-        o1[u] = d.o1 != ~0u ? a.out + d.o1 + ebase : nullptr;
+        o0[u] = d.o0 != ~0u ? gout + d.o0 + ebase : nullptr;
+        o1[u] = d.o1 != ~0u ? gout + d.o1 + ebase : nullptr;
       } else {
         o0[u] = vrow ? sb + xo : nullptr;
         o1[u] = vrow ? sb + xo + (1 << SH) * PD : nullptr;
@@ -807,19 +831,19 @@ __device__ __forceinline__ void consumer_pass(const TransArgs& a, double2* __res
 #else
     if (cls == 3)
 #endif
-      mma_steps<P, 0, S::NK, NSUB>(op, x, off, p0, p1, are, aim, tl);
+      mma_steps<P, 0, S::NK, NSUB, E>(op, x, off, p0, p1, are, aim, tl);
     else if (cls == 1)
-      mma_steps<P, 0, S::K0_HI, NSUB>(op, x, off, p0, p1, are, aim, tl);
+      mma_steps<P, 0, S::K0_HI, NSUB, E>(op, x, off, p0, p1, are, aim, tl);
     else if (cls == 2)
-      mma_steps<P, S::K1_LO, S::NK, NSUB>(op, x, off, p0, p1, are, aim, tl);
+      mma_steps<P, S::K1_LO, S::NK, NSUB, E>(op, x, off, p0, p1, are, aim, tl);
 #pragma unroll
     for (int u = 0; u < NSUB; ++u) {
 #pragma unroll
       for (int n = 0; n < S::NT; ++n) {
         const int m = 4 * n + c;
         if (m < S::NM) {
-          if (o0[u]) o0[u][m * STR] = make_double2(are[u][n][0] + aim[u][n][1], aim[u][n][0] - are[u][n][1]);
-          if (o1[u]) o1[u][m * STR] = make_double2(are[u][n][0] - aim[u][n][1], aim[u][n][0] + are[u][n][1]);
+          if (o0[u]) o0[u][m * STR] = ElemT<E>::mk(are[u][n][0] + aim[u][n][1], aim[u][n][0] - are[u][n][1]);
+          if (o1[u]) o1[u][m * STR] = ElemT<E>::mk(are[u][n][0] - aim[u][n][1], aim[u][n][0] + are[u][n][1]);
         }
       }
     }
@@ -836,8 +860,8 @@ __device__ __forceinline__ void consumer_pass(const TransArgs& a, double2* __res
         vb += __shfl_xor_sync(0xffffffffu, odd ? u2 : u3, 1);
         double w = hi ? vb : va;
         w += __shfl_xor_sync(0xffffffffu, hi ? va : vb, 2);
-        double2* o = hi ? o1[u] : o0[u];  // lane c holds component c&1 of z_{c>>1}
-        if (o) reinterpret_cast<double*>(o + (P - 1) * STR)[c & 1] = w;
+        E* o = hi ? o1[u] : o0[u];  // lane c holds component c&1 of z_{c>>1}
+        if (o) reinterpret_cast<typename ElemT<E>::scalar*>(o + (P - 1) * STR)[c & 1] = (typename ElemT<E>::scalar)w;
       }
     }
   }
@@ -1000,16 +1024,16 @@ __device__ __forceinline__ void ws_producer(const TransArgs& a, const unsigned c
 // 2D with NST >= 3: skewed pipeline, pass 1 of tile i+1 runs before pass 0 of
 // tile i, and pass 0 waits on an mbarrier (p1done) every consumer thread
 // arrives on after its pass-1 rows, so warps do not idle at a pass barrier.
-template <int D, int P, int G, int NC, int NST, int MINB>
+template <int D, int P, int G, int NC, int NST, int MINB, typename E = double2>
 __global__ __launch_bounds__((NC + 1) * 32, MINB) void k_translate_ws(TransArgs a, const double* __restrict__ frag,
                                                                              const unsigned char* __restrict__ sched,
                                                                              int64_t ntiles) {
   using SC = Sched<D, P, G>;
-  constexpr int PD = Pow<P, D>::v;
+  constexpr int PD = StrideT<E, Pow<P, D>::v>::v;  // array stride (elements)
   constexpr int NS = 1 << D;
   constexpr int STAGE = G * NS * PD;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  double2* ring = reinterpret_cast<double2*>(smem_raw);  // [NST][G][NS][PD]
+  E* ring = reinterpret_cast<E*>(smem_raw);  // [NST][G][NS][PD]
   __shared__ __align__(128) unsigned char blk[NST][SC::BLK];
   __shared__ __align__(8) uint64_t full[NST], empty[NST], p1done[NST];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1021,7 +1045,7 @@ __global__ __launch_bounds__((NC + 1) * 32, MINB) void k_translate_ws(TransArgs 
   if (threadIdx.x == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncthreads();
   if (warp == NC) {
-    ws_producer<D, P, G, NST>(a, sched, ntiles, ring, blk, full, empty);
+    ws_producer<D, P, G, NST, E, PD>(a, sched, ntiles, ring, blk, full, empty);
     return;
   }
   // ---------------- consumers ----------------
@@ -1032,13 +1056,13 @@ __global__ __launch_bounds__((NC + 1) * 32, MINB) void k_translate_ws(TransArgs 
   INSTR_T0(tc0);
   // 2D: first passes (list 1: axis 1, list 2: axis 0 for groups in reversed
   // order), then last passes (list 0: axis 0, list 3: axis 1)
-  auto first2d = [&](double2* sb_, const unsigned char* bk) {
-    consumer_pass<D, P, G, NC, D - 1, false, 1>(a, sb_, bk, op);
-    if constexpr (D == 2) consumer_pass<D, P, G, NC, 0, false, 2>(a, sb_, bk, op);
+  auto first2d = [&](E* sb_, const unsigned char* bk) {
+    consumer_pass<D, P, G, NC, D - 1, false, 1, E>(a, sb_, bk, op);
+    if constexpr (D == 2) consumer_pass<D, P, G, NC, 0, false, 2, E>(a, sb_, bk, op);
   };
-  auto last2d = [&](double2* sb_, const unsigned char* bk) {
-    consumer_pass<D, P, G, NC, 0, true, 0>(a, sb_, bk, op);
-    if constexpr (D == 2) consumer_pass<D, P, G, NC, D - 1, true, 3>(a, sb_, bk, op);
+  auto last2d = [&](E* sb_, const unsigned char* bk) {
+    consumer_pass<D, P, G, NC, 0, true, 0, E>(a, sb_, bk, op);
+    if constexpr (D == 2) consumer_pass<D, P, G, NC, D - 1, true, 3, E>(a, sb_, bk, op);
   };
   if constexpr (D == 2 && NST >= 3) {
     int64_t tile = blockIdx.x;
@@ -1077,7 +1101,7 @@ __global__ __launch_bounds__((NC + 1) * 32, MINB) void k_translate_ws(TransArgs 
       INSTR_T0(tf0);
       mbar_wait(smem_u32(&full[s]), ph);
       INSTR_ADD(4, tf0);
-      double2* sb = ring + s * STAGE;
+      E* sb = ring + s * STAGE;
       if constexpr (D == 2) {
         INSTR_T0(t1);
         first2d(sb, blk[s]);
@@ -1089,11 +1113,11 @@ __global__ __launch_bounds__((NC + 1) * 32, MINB) void k_translate_ws(TransArgs 
         last2d(sb, blk[s]);
         INSTR_ADD(7, t3);
       } else {
-        consumer_pass<D, P, G, NC, 2, false>(a, sb, blk[s], op);
+        consumer_pass<D, P, G, NC, 2, false, 2, E>(a, sb, blk[s], op);
         consumer_sync<NC * 32>();
-        consumer_pass<D, P, G, NC, 1, false>(a, sb, blk[s], op);
+        consumer_pass<D, P, G, NC, 1, false, 1, E>(a, sb, blk[s], op);
         consumer_sync<NC * 32>();
-        consumer_pass<D, P, G, NC, 0, true>(a, sb, blk[s], op);
+        consumer_pass<D, P, G, NC, 0, true, 0, E>(a, sb, blk[s], op);
       }
       __syncwarp();
       if (lane == 0)
@@ -1400,6 +1424,15 @@ __global__ __launch_bounds__(NT, SFT_FMA_MINB(NT)) void k_translate_fma(TransArg
 // ------------------------------------------------------------------------
 // launch configuration (tile of G groups per stage; tuned on B200)
 // ------------------------------------------------------------------------
+#ifndef SFT_F32_G29
+#define SFT_F32_G29 8
+#endif
+#ifndef SFT_F32_NC29
+#define SFT_F32_NC29 4
+#endif
+#ifndef SFT_F32_MINB29
+#define SFT_F32_MINB29 4
+#endif
 #ifndef SFT_WS_G29
 #define SFT_WS_G29 4
 #endif
@@ -1453,6 +1486,27 @@ template <> struct WsCfg<3, 7> {
   static constexpr int G = SFT_WS_G37, NC = SFT_WS_NC37, NST = SFT_WS_NST37, MINB = SFT_WS_MINB37;
 };
 template <> struct WsCfg<3, 9> { static constexpr int G = 1, NC = 8, NST = 2, MINB = 1; };
+
+// FP32 storage on the DMMA kernel (default FP32 variant): arrays are half the
+// size, so twice the groups per stage at the same shared memory
+template <int D, int P>
+struct F32WsCfg;
+template <> struct F32WsCfg<2, 5> { static constexpr int G = 16, NC = 4, NST = 3, MINB = 3; };
+template <> struct F32WsCfg<2, 7> { static constexpr int G = 16, NC = 4, NST = 2, MINB = 3; };
+template <> struct F32WsCfg<2, 9> { static constexpr int G = SFT_F32_G29, NC = SFT_F32_NC29, NST = 2, MINB = SFT_F32_MINB29; };
+template <> struct F32WsCfg<3, 5> { static constexpr int G = 4, NC = 4, NST = 2, MINB = 3; };
+template <> struct F32WsCfg<3, 7> { static constexpr int G = 2, NC = 8, NST = 2, MINB = 1; };
+template <> struct F32WsCfg<3, 9> { static constexpr int G = 1, NC = 8, NST = 2, MINB = 1; };
+
+// SFT_F32_FFMA=1: the FP32 variant on the FFMA thread-per-fiber kernel (ablation)
+static bool f32_ffma() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SFT_F32_FFMA");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
 
 // FP32 kernel: G groups per tile, NC FFMA consumer warps, NST stages, MINB CTAs/SM
 template <int D, int P>
@@ -1557,7 +1611,25 @@ static cudaError_t launch_translate_t(const sft_plan_s* Pl, const LevelDims& L, 
   constexpr int PD = Pow<P, D>::v;
   TransArgs a = make_args(L, (const double2*)in, (double2*)out);
   if (a.ngroups <= 0) return cudaSuccess;
-  if (Pl->prec == 1) {
+  if (Pl->prec == 1 && !f32_ffma()) {
+    // FP32 storage, FP64 arithmetic on the tensor cores (same kernel as FP64)
+    constexpr int G = F32WsCfg<D, P>::G, NC = F32WsCfg<D, P>::NC, NST = F32WsCfg<D, P>::NST,
+                  MB = F32WsCfg<D, P>::MINB;
+    const size_t smem = (size_t)NST * G * (1 << D) * F32<D, P>::PS * sizeof(float2);
+    static int grid_max = 0;
+    static const double* frag = nullptr;
+    if (!grid_max) {
+      cudaError_t e = persistent_grid(k_translate_ws<D, P, G, NC, NST, MB, float2>, (NC + 1) * 32, smem, &grid_max);
+      if (e != cudaSuccess) return e;
+      frag = device_fragments<P>(&e);
+      if (!frag) return e;
+    }
+    if (!L.sched) return cudaErrorInvalidValue;
+    const int64_t ntiles = (a.ngroups + G - 1) / G;
+    const int64_t grid = std::min<int64_t>(ntiles, grid_max);
+    launch_pdl(k_translate_ws<D, P, G, NC, NST, MB, float2>, (unsigned)grid, (NC + 1) * 32, smem, Pl->stream, a, frag,
+               L.sched, ntiles);
+  } else if (Pl->prec == 1) {
     constexpr int G = F32Cfg<D, P>::G, NC = F32Cfg<D, P>::NC, NST = F32Cfg<D, P>::NST, MB = F32Cfg<D, P>::MINB;
     const size_t smem = (size_t)NST * G * (1 << D) * F32<D, P>::PS * sizeof(float2);
     static int grid_max = 0;
@@ -1612,7 +1684,8 @@ static size_t schedule_bytes_g(const LevelDims& L) {
 
 template <int D, int P>
 static size_t schedule_bytes_t(const sft_plan_s* Pl, const LevelDims& L) {
-  if (Pl->prec == 1) return schedule_bytes_g<D, P, F32Cfg<D, P>::G>(L);
+  if (Pl->prec == 1)
+    return f32_ffma() ? schedule_bytes_g<D, P, F32Cfg<D, P>::G>(L) : schedule_bytes_g<D, P, F32WsCfg<D, P>::G>(L);
   const int mode = translate_kernel_choice();
   if (mode == 0) return schedule_bytes_g<D, P, WsCfg<D, P>::G>(L);
   return 0;
@@ -1642,7 +1715,9 @@ static cudaError_t launch_schedule_g(const sft_plan_s* Pl, const LevelDims* L, i
 
 template <int D, int P>
 static cudaError_t launch_schedule_t(const sft_plan_s* Pl, const LevelDims* L, int nlev, unsigned char* const* dst) {
-  if (Pl->prec == 1) return launch_schedule_g<D, P, F32Cfg<D, P>::G, F32<D, P>::PS>(Pl, L, nlev, dst);
+  if (Pl->prec == 1)
+    return f32_ffma() ? launch_schedule_g<D, P, F32Cfg<D, P>::G, F32<D, P>::PS>(Pl, L, nlev, dst)
+                      : launch_schedule_g<D, P, F32WsCfg<D, P>::G, F32<D, P>::PS>(Pl, L, nlev, dst);
   const int mode = translate_kernel_choice();
   if (mode == 0) return launch_schedule_g<D, P, WsCfg<D, P>::G, Pow<P, D>::v>(Pl, L, nlev, dst);
   return cudaSuccess;
