@@ -28,6 +28,16 @@ static int fail(int code, const std::string& msg) {
       return fail(SFT_E_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_));  \
   } while (0)
 
+// one non-blocking side stream per device for the plan's schedule kernel
+static cudaStream_t side_stream() {
+  static cudaStream_t st[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return nullptr;
+  if (!st[dev]) cudaStreamCreateWithFlags(&st[dev], cudaStreamNonBlocking);
+  return st[dev];
+}
+
 static bool is_device_ptr(const void* p) {
   cudaPointerAttributes at;
   if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
@@ -332,6 +342,7 @@ static LevelDims apply_dims_sched(const sft_plan_s* P, int t) {
 static void plan_free(sft_plan_s* P) {
   if (!P) return;
   cudaStream_t s = P->stream;
+  if (P->sched_ready) cudaStreamWaitEvent(s, P->sched_ready, 0);
   free_tree(P->X, s);
   free_tree(P->K, s);
   for (int i = 0; i < 2; ++i)
@@ -344,6 +355,8 @@ static void plan_free(sft_plan_s* P) {
   for (int i = 0; i < P->ev_created; ++i) cudaEventDestroy(P->ev[i]);
   for (int i = 0; i < 2; ++i)
     if (P->plan_ev[i]) cudaEventDestroy(P->plan_ev[i]);
+  if (P->sched_fork) cudaEventDestroy(P->sched_fork);
+  if (P->sched_ready) cudaEventDestroy(P->sched_ready);
   // no sync: the frees above are stream-ordered behind any pending work
   delete P;
 }
@@ -541,10 +554,20 @@ extern "C" int sft_plan(int dim, int64_t N, int p, const double* x, int64_t nx, 
         dims[t] = apply_dims(P, t);
         dst[t] = P->sched + P->sched_off[t];
       }
-      cudaError_t ce = launch_schedule(P, dims.data(), L, dst.data());
+      // the schedules are built on a side stream so that they overlap the
+      // first kernels of the apply (the leaf kernel needs only the trees);
+      // the first translation waits on sched_ready
+      cudaStream_t side = side_stream();
+      cudaEventCreateWithFlags(&P->sched_fork, cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&P->sched_ready, cudaEventDisableTiming);
+      cudaEventRecord(P->sched_fork, s);
+      cudaStreamWaitEvent(side, P->sched_fork, 0);
+      cudaError_t ce = launch_schedule(P, dims.data(), L, dst.data(), side);
       if (ce != cudaSuccess) return bail(SFT_E_CUDA, std::string("schedule: ") + cudaGetErrorString(ce));
+      cudaEventRecord(P->sched_ready, side);
       const char* chk = getenv("SFT_CHECK_SCHED");
       if (chk && chk[0] == '1') {
+        cudaStreamWaitEvent(s, P->sched_ready, 0);
         // debug: every level's schedule against its buffer sizes
         for (int t = 0; t < L; ++t) {
           const LevelDims ld = apply_dims(P, t);
@@ -553,6 +576,7 @@ extern "C" int sft_plan(int dim, int64_t N, int p, const double* x, int64_t nx, 
           if (ce != cudaSuccess) return bail(SFT_E_CUDA, std::string("check: ") + cudaGetErrorString(ce));
         }
         int herr = 0;
+        cudaStreamWaitEvent(s, P->sched_ready, 0);
         cudaMemcpyAsync(&herr, P->d_err, sizeof(int), cudaMemcpyDeviceToHost, s);
         cudaStreamSynchronize(s);
         if (herr & 4) return bail(SFT_E_CUDA, "tile schedule failed its invariants");
@@ -637,7 +661,8 @@ extern "C" int sft_apply(sft_plan_t P, const void* f, void* u) {
   // step 2: leaf charges, level L buffer
   CKR(launch_leaf(P, fd, P->buf[L & 1], 0, P->K.counts[L]));
   tmark(P);
-  // step 3: t = L-1 .. 0
+  // step 3: t = L-1 .. 0 (after the plan's schedule kernel on the side stream)
+  if (P->sched_ready) CKR(cudaStreamWaitEvent(s, P->sched_ready, 0));
   for (int t = L - 1; t >= 0; --t) {
     LevelDims ld = apply_dims_sched(P, t);
     CKR(launch_translate(P, ld, P->buf[(t + 1) & 1], P->buf[t & 1]));
@@ -703,6 +728,7 @@ extern "C" int sft_apply_phase1(sft_plan_t P, const void* f, void* sendbuf) {
     return SFT_OK;
   }
   CKR(launch_leaf(P, fd, P->buf[L & 1], kl.lo, kl.hi));
+  if (P->sched_ready) CKR(cudaStreamWaitEvent(s, P->sched_ready, 0));
   for (int t = L - 1; t >= m; --t) {
     LevelDims ld = apply_dims_sched(P, t);
     double2* out = t == m ? sb : P->buf[t & 1];
@@ -724,6 +750,7 @@ extern "C" int sft_apply_phase2(sft_plan_t P, const void* recvbuf, void* u) {
     ud = P->u_stage;
   }
   CKR(launch_zero(ud, P->nx, s));
+  if (P->sched_ready) CKR(cudaStreamWaitEvent(s, P->sched_ready, 0));
   const double2* in = (const double2*)recvbuf;
   for (int t = m - 1; t >= 0; --t) {
     LevelDims ld = apply_dims_sched(P, t);

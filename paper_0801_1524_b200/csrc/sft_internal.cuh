@@ -99,6 +99,7 @@ struct sft_plan_s {
   // tile schedules of the translation levels (one allocation; offsets per level t)
   unsigned char* sched = nullptr;
   std::vector<size_t> sched_off;
+  cudaEvent_t sched_fork = nullptr, sched_ready = nullptr;  // schedule kernel on the side stream
   // timing
   bool timing = false;
   cudaEvent_t ev[64];
@@ -139,7 +140,8 @@ cudaError_t launch_translate(const sft_plan_s* P, const LevelDims& L, const void
 // tile schedule of one level (sizes and builder; 0 bytes when the kernel needs none)
 size_t schedule_bytes(const sft_plan_s* P, const LevelDims& L);
 // builds the schedules of nlev levels (dims L[i], destination dst[i]) in one launch
-cudaError_t launch_schedule(const sft_plan_s* P, const LevelDims* L, int nlev, unsigned char* const* dst);
+cudaError_t launch_schedule(const sft_plan_s* P, const LevelDims* L, int nlev, unsigned char* const* dst,
+                            cudaStream_t st);
 // debug: validate a level's schedule against its input/output pair counts (sets *err bit 2)
 cudaError_t check_schedule(const sft_plan_s* P, const LevelDims& L, const unsigned char* sched, int64_t in_pairs,
                            int64_t out_pairs, int* err);

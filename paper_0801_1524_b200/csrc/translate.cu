@@ -1692,7 +1692,8 @@ static size_t schedule_bytes_t(const sft_plan_s* Pl, const LevelDims& L) {
 }
 
 template <int D, int P, int G, int PS>
-static cudaError_t launch_schedule_g(const sft_plan_s* Pl, const LevelDims* L, int nlev, unsigned char* const* dst) {
+static cudaError_t launch_schedule_g(const sft_plan_s* Pl, const LevelDims* L, int nlev, unsigned char* const* dst,
+                                     cudaStream_t st) {
   SchedLevels S;
   int64_t t0 = 0;
   S.nlev = 0;
@@ -1708,18 +1709,19 @@ static cudaError_t launch_schedule_g(const sft_plan_s* Pl, const LevelDims* L, i
   S.tile0[S.nlev] = t0;
   if (S.nlev == 0) return cudaSuccess;
   const int64_t nwarps = (t0 + 32 / G - 1) / (32 / G);
-  k_schedule<D, P, G, PS><<<(unsigned)((nwarps + 3) / 4), 128, 0, Pl->stream>>>(S);
+  k_schedule<D, P, G, PS><<<(unsigned)((nwarps + 3) / 4), 128, 0, st>>>(S);
   count_launch();
   return cudaGetLastError();
 }
 
 template <int D, int P>
-static cudaError_t launch_schedule_t(const sft_plan_s* Pl, const LevelDims* L, int nlev, unsigned char* const* dst) {
+static cudaError_t launch_schedule_t(const sft_plan_s* Pl, const LevelDims* L, int nlev, unsigned char* const* dst,
+                                     cudaStream_t st) {
   if (Pl->prec == 1)
-    return f32_ffma() ? launch_schedule_g<D, P, F32Cfg<D, P>::G, F32<D, P>::PS>(Pl, L, nlev, dst)
-                      : launch_schedule_g<D, P, F32WsCfg<D, P>::G, F32<D, P>::PS>(Pl, L, nlev, dst);
+    return f32_ffma() ? launch_schedule_g<D, P, F32Cfg<D, P>::G, F32<D, P>::PS>(Pl, L, nlev, dst, st)
+                      : launch_schedule_g<D, P, F32WsCfg<D, P>::G, F32<D, P>::PS>(Pl, L, nlev, dst, st);
   const int mode = translate_kernel_choice();
-  if (mode == 0) return launch_schedule_g<D, P, WsCfg<D, P>::G, Pow<P, D>::v>(Pl, L, nlev, dst);
+  if (mode == 0) return launch_schedule_g<D, P, WsCfg<D, P>::G, Pow<P, D>::v>(Pl, L, nlev, dst, st);
   return cudaSuccess;
 }
 
@@ -1753,8 +1755,9 @@ size_t schedule_bytes(const sft_plan_s* Pl, const LevelDims& L) {
   return r;
 }
 
-cudaError_t launch_schedule(const sft_plan_s* Pl, const LevelDims* L, int nlev, unsigned char* const* dst) {
-  SFT_DISPATCH(Pl->d, Pl->p, return (launch_schedule_t<D, P>(Pl, L, nlev, dst)));
+cudaError_t launch_schedule(const sft_plan_s* Pl, const LevelDims* L, int nlev, unsigned char* const* dst,
+                            cudaStream_t st) {
+  SFT_DISPATCH(Pl->d, Pl->p, return (launch_schedule_t<D, P>(Pl, L, nlev, dst, st)));
   return cudaSuccess;
 }
 
