@@ -126,6 +126,7 @@ def run_ours(args):
     w = synth.make_workload(args.config)
     P = w.P
     prec = 1 if args.precision == "f32" else 0
+    fused = args.exchange == "fused"
     x = torch.from_numpy(w.x).to(dev)
     k = torch.from_numpy(w.k).to(dev)
     f = torch.from_numpy(w.f).to(dev)
@@ -143,7 +144,7 @@ def run_ours(args):
             with sft.Plan(w.dim, w.N, w.p, x, k, stream=stream, precision=prec) as plan:
                 plan.apply(f, u)
         else:
-            with DistPlan(w.dim, w.N, w.p, x, k, stream=stream) as dp:
+            with DistPlan(w.dim, w.N, w.p, x, k, stream=stream, fused=fused) as dp:
                 dp.apply(f, u)
 
     def timed(fn, K, do_flush=True):
@@ -188,7 +189,7 @@ def run_ours(args):
         st = plan.stats()
         plan.close()
     else:
-        dp = DistPlan(w.dim, w.N, w.p, x, k, stream=stream)
+        dp = DistPlan(w.dim, w.N, w.p, x, k, stream=stream, fused=fused)
         for _ in range(max(2, args.warmup)):
             dp.apply(f, u)
         apply_total, _ = timed(lambda: dp.apply(f, u), args.steps)
@@ -212,7 +213,7 @@ def run_ours(args):
                 plan.apply(fh, uh)
         else:
             xd, kd, fd = xh.to(dev, non_blocking=True), kh.to(dev, non_blocking=True), fh.to(dev, non_blocking=True)
-            with DistPlan(w.dim, w.N, w.p, xd, kd, stream=stream) as dp:
+            with DistPlan(w.dim, w.N, w.p, xd, kd, stream=stream, fused=fused) as dp:
                 ud = dp.apply(fd)
             uh.copy_(ud)
 
@@ -268,7 +269,7 @@ def run_ours(args):
             "config": {"workload": f"{args.config}: {CONFIG_DESC[args.config]}", "dim": w.dim, "N": w.N, "p": w.p,
                        "nx": len(w.x), "nk": len(w.k), "P": P, "pairs_total": int(np.sum(st["pairs"])),
                        "l2": "flushed before every timed step (256 MiB memset, outside the step events)",
-                       "parallelism": f"subtree-sharded x{world}" if world > 1 else "single GPU"},
+                       "parallelism": (f"subtree-sharded x{world}, exchange {args.exchange}" if world > 1 else "single GPU")},
             "e2e": {"value": round(P * K / (e2e_total / 1e3) / 1e6, 3), "unit": "Mpoints/s",
                     "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                     "ms_per_step": round(e2e_total / K, 4)},
@@ -365,6 +366,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-targets", type=int, default=256)
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "fused"],
+                    help="N > 1: level-m exchange by NCCL all-to-all, or fused into the exchange level's kernel "
+                         "(peer stores into IPC-mapped receive buffers over NVLink)")
     ap.add_argument("--precision", default="f64", choices=["f64", "f32"],
                     help="arithmetic of the level charges (f32: the optional FP32 variant, single GPU)")
     args = ap.parse_args()

@@ -123,6 +123,28 @@ int sft_exchange_counts(sft_plan_t plan, int64_t* send_counts, int64_t* recv_cou
 int sft_apply_phase1(sft_plan_t plan, const void* f, void* sendbuf);
 int sft_apply_phase2(sft_plan_t plan, const void* recvbuf, void* u);
 
+/* Fused exchange (compute + collective in one kernel over NVLink peer memory):
+ * sft_set_peer_buffers(plan, recv): recv[world] = every rank's receive buffer
+ *   (device pointers valid in this process: own buffer for this rank, peers'
+ *   buffers opened with sft_ipc_open).  Afterwards sft_apply_phase1 writes the
+ *   level-m charges straight into the receivers' buffers from the epilogue of
+ *   the exchange level's translation kernel (sendbuf may be NULL) -- the
+ *   caller only needs a stream-ordered barrier across ranks before
+ *   sft_apply_phase2.  recv == NULL switches back to the send buffer.
+ * sft_peer_offsets(plan, off[world]): element offset of this rank's segment in
+ *   each receiver's buffer.
+ * Device memory that can be shared across processes (cudaMalloc, not the
+ * stream-ordered pool): sft_device_alloc / sft_device_free; CUDA IPC:
+ * sft_ipc_handle(ptr, handle[64 bytes]) / sft_ipc_open(handle, &ptr) /
+ * sft_ipc_close(ptr).  world <= 8. */
+int sft_set_peer_buffers(sft_plan_t plan, void* const* recv);
+int sft_peer_offsets(sft_plan_t plan, int64_t* off);
+int sft_device_alloc(int64_t bytes, void** out);
+int sft_device_free(void* p);
+int sft_ipc_handle(void* p, void* handle64);
+int sft_ipc_open(const void* handle64, void** out);
+int sft_ipc_close(void* p);
+
 /* Partition actually used by a world > 1 plan (host, caller-allocated):
  * part[0..2] = s_K, s_X, m; then for every rank r: part[3+4r .. 3+4r+3] =
  * [first, last) T_K box range at level s_K and [first, last) T_X box range at

@@ -79,6 +79,13 @@ def lib():
     L.sft_apply_phase1.argtypes = [vp, vp, vp]
     L.sft_apply_phase2.argtypes = [vp, vp, vp]
     L.sft_partition_info.argtypes = [vp, _c_i64p]
+    L.sft_set_peer_buffers.argtypes = [vp, ctypes.POINTER(vp)]
+    L.sft_peer_offsets.argtypes = [vp, _c_i64p]
+    L.sft_device_alloc.argtypes = [ctypes.c_int64, ctypes.POINTER(vp)]
+    L.sft_device_free.argtypes = [vp]
+    L.sft_ipc_handle.argtypes = [vp, ctypes.c_char_p]
+    L.sft_ipc_open.argtypes = [ctypes.c_char_p, ctypes.POINTER(vp)]
+    L.sft_ipc_close.argtypes = [vp]
     L.sft_choose_partition.argtypes = [ctypes.c_int, ctypes.c_int, _c_i64p, _c_i64p,
                                        ctypes.POINTER(ctypes.POINTER(ctypes.c_int32)),
                                        ctypes.POINTER(ctypes.POINTER(ctypes.c_int32)), ctypes.c_int, ctypes.c_int,
@@ -187,15 +194,36 @@ class Plan:
         _check(lib().sft_partition_info(self._h, out.ctypes.data_as(_c_i64p)))
         return out
 
-    def apply_phase1(self, f, sendbuf):
+    def apply_phase1(self, f, sendbuf=None):
+        """sendbuf None: fused exchange (set_peer_buffers first)."""
         fp, fk = _ptr(f, np.complex128)
-        sp, _ = _ptr(sendbuf, np.complex128)
+        if sendbuf is None or isinstance(sendbuf, int):
+            sp = ctypes.c_void_p(sendbuf or 0)
+        else:
+            sp, _ = _ptr(sendbuf, np.complex128)
         _check(lib().sft_apply_phase1(self._h, fp, sp))
 
     def apply_phase2(self, recvbuf, u):
-        rp, _ = _ptr(recvbuf, np.complex128)
+        if isinstance(recvbuf, int):
+            rp = ctypes.c_void_p(recvbuf)
+        else:
+            rp, _ = _ptr(recvbuf, np.complex128)
         up, _ = _ptr(u, np.complex128)
         _check(lib().sft_apply_phase2(self._h, rp, up))
+
+    def set_peer_buffers(self, ptrs):
+        """Fused exchange: ptrs[world] = device addresses (ints) of every rank's
+        receive buffer as mapped in this process; None switches it off."""
+        if ptrs is None:
+            _check(lib().sft_set_peer_buffers(self._h, None))
+            return
+        arr = (ctypes.c_void_p * self.world)(*[int(q) for q in ptrs])
+        _check(lib().sft_set_peer_buffers(self._h, arr))
+
+    def peer_offsets(self):
+        out = np.zeros(self.world, np.int64)
+        _check(lib().sft_peer_offsets(self._h, out.ctypes.data_as(_c_i64p)))
+        return out
 
     # -- stats / timing -------------------------------------------------------
     def stats(self):
@@ -233,6 +261,33 @@ class Plan:
 
     def __exit__(self, *a):
         self.close()
+
+
+def device_alloc(nbytes: int) -> int:
+    """cudaMalloc'd device memory (IPC-shareable, unlike the stream-ordered pool)."""
+    p = ctypes.c_void_p()
+    _check(lib().sft_device_alloc(int(nbytes), ctypes.byref(p)))
+    return int(p.value)
+
+
+def device_free(ptr: int) -> None:
+    _check(lib().sft_device_free(ctypes.c_void_p(ptr)))
+
+
+def ipc_handle(ptr: int) -> bytes:
+    buf = ctypes.create_string_buffer(64)
+    _check(lib().sft_ipc_handle(ctypes.c_void_p(ptr), buf))
+    return buf.raw
+
+
+def ipc_open(handle: bytes) -> int:
+    p = ctypes.c_void_p()
+    _check(lib().sft_ipc_open(ctypes.c_char_p(handle), ctypes.byref(p)))
+    return int(p.value)
+
+
+def ipc_close(ptr: int) -> None:
+    _check(lib().sft_ipc_close(ctypes.c_void_p(ptr)))
 
 
 def launch_count() -> int:

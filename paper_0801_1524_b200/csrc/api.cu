@@ -512,6 +512,16 @@ extern "C" int sft_plan(int dim, int64_t N, int p, const double* x, int64_t nx, 
       base += my_nb * (abound[q + 1] - abound[q]);
     }
     seg[W] = abound[W];
+    // fused exchange: offset (elements) of this rank's segment in every
+    // receiver's buffer (receivers concatenate the senders' segments in rank order)
+    P->seg_host = seg;
+    P->peer_off.assign(W, 0);
+    for (int q = 0; q < W; ++q) {
+      const int64_t na_q = abound[q + 1] - abound[q];
+      int64_t o = 0;
+      for (int r = 0; r < P->rank; ++r) o += nb_of[r] * na_q;
+      P->peer_off[q] = o * PD;
+    }
     if (cudaMallocAsync(&P->d_seg, seg.size() * sizeof(int64_t), s) != cudaSuccess) return bail(SFT_E_NOMEM, "seg");
     cudaMemcpyAsync(P->d_seg, seg.data(), seg.size() * sizeof(int64_t), cudaMemcpyHostToDevice, s);
     int64_t mx = 0;
@@ -707,9 +717,9 @@ extern "C" int sft_partition_info(sft_plan_t P, int64_t* part) {
 }
 
 extern "C" int sft_apply_phase1(sft_plan_t P, const void* f, void* sendbuf) {
-  if (!P || !f || !sendbuf) return fail(SFT_E_ARG, "NULL argument");
+  if (!P || !f || (!sendbuf && P->peer.empty())) return fail(SFT_E_ARG, "NULL argument");
   if (P->world < 2) return fail(SFT_E_STATE, "plan is not multi-rank");
-  if (!is_device_ptr(sendbuf)) return fail(SFT_E_ARG, "sendbuf must be device memory");
+  if (sendbuf && !is_device_ptr(sendbuf)) return fail(SFT_E_ARG, "sendbuf must be device memory");
   cudaStream_t s = P->stream;
   const int L = P->L, m = P->part.m;
   const double2* fd = (const double2*)f;
@@ -719,12 +729,20 @@ extern "C" int sft_apply_phase1(sft_plan_t P, const void* f, void* sendbuf) {
     fd = P->f_stage;
   }
   double2* sb = (double2*)sendbuf;
+  const bool fused = !P->peer.empty();
   // leaf level: the local leaf range; if m == L the leaf output is the send buffer
   const LevelRange kl = P->k_rng[L];
   if (m == L) {
     // exchange at the leaf level: pairs (A0, B) with the single root A0 of T_X
     // (s_X = 0), so only its owner's segment is non-empty and starts at 0
-    CKR(launch_leaf(P, fd, sb, kl.lo, kl.hi));
+    double2* out = sb;
+    if (fused) {
+      int q0 = 0;  // the owner of A0: the only non-empty segment
+      for (int q = 0; q < P->world; ++q)
+        if (P->seg_host[q + 1] > P->seg_host[q]) q0 = q;
+      out = P->peer[q0] + P->peer_off[q0];
+    }
+    CKR(launch_leaf(P, fd, out, kl.lo, kl.hi));
     return SFT_OK;
   }
   CKR(launch_leaf(P, fd, P->buf[L & 1], kl.lo, kl.hi));
@@ -732,6 +750,19 @@ extern "C" int sft_apply_phase1(sft_plan_t P, const void* f, void* sendbuf) {
   for (int t = L - 1; t >= m; --t) {
     LevelDims ld = apply_dims_sched(P, t);
     double2* out = t == m ? sb : P->buf[t & 1];
+    if (t == m && fused) {
+      // the exchange level's outputs go straight into the receivers' buffers
+      // (NVLink peer stores from the kernel's epilogue): no send buffer, no
+      // all-to-all
+      ld.npeer = P->world;
+      for (int q = 0; q < P->world; ++q) {
+        ld.peer[q] = P->peer[q];
+        ld.peer_off[q] = P->peer_off[q];
+        ld.peer_seg[q] = P->seg_host[P->world + 1 + q];
+      }
+      ld.peer_seg[P->world] = INT64_MAX;
+      out = nullptr;
+    }
     CKR(launch_translate(P, ld, P->buf[(t + 1) & 1], out));
   }
   return SFT_OK;
@@ -801,6 +832,61 @@ extern "C" int sft_plan_stats(sft_plan_t P, int64_t* counts_x, int64_t* counts_k
     info[6] = groups;
     info[7] = bytes;
   }
+  return SFT_OK;
+}
+
+extern "C" int sft_set_peer_buffers(sft_plan_t P, void* const* recv) {
+  if (!P) return fail(SFT_E_ARG, "NULL plan");
+  if (P->world < 2) return fail(SFT_E_STATE, "plan is not multi-rank");
+  if (P->world > kMaxPeers) return fail(SFT_E_ARG, "too many ranks for the fused exchange");
+  if (!recv) {
+    P->peer.clear();
+    return SFT_OK;
+  }
+  P->peer.assign(P->world, nullptr);
+  for (int q = 0; q < P->world; ++q) {
+    if (!recv[q]) return fail(SFT_E_ARG, "NULL peer buffer");
+    P->peer[q] = (double2*)recv[q];
+  }
+  return SFT_OK;
+}
+
+extern "C" int sft_peer_offsets(sft_plan_t P, int64_t* off) {
+  if (!P || !off) return fail(SFT_E_ARG, "NULL argument");
+  if (P->world < 2) return fail(SFT_E_STATE, "plan is not multi-rank");
+  for (int q = 0; q < P->world; ++q) off[q] = P->peer_off[q];
+  return SFT_OK;
+}
+
+extern "C" int sft_device_alloc(int64_t bytes, void** out) {
+  if (!out || bytes < 0) return fail(SFT_E_ARG, "bad arguments");
+  CKR(cudaMalloc(out, bytes > 0 ? (size_t)bytes : 1));
+  return SFT_OK;
+}
+
+extern "C" int sft_device_free(void* p) {
+  if (p) CKR(cudaFree(p));
+  return SFT_OK;
+}
+
+extern "C" int sft_ipc_handle(void* p, void* handle64) {
+  if (!p || !handle64) return fail(SFT_E_ARG, "NULL argument");
+  cudaIpcMemHandle_t h;
+  CKR(cudaIpcGetMemHandle(&h, p));
+  std::memcpy(handle64, &h, sizeof(h));
+  return SFT_OK;
+}
+
+extern "C" int sft_ipc_open(const void* handle64, void** out) {
+  if (!handle64 || !out) return fail(SFT_E_ARG, "NULL argument");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle64, sizeof(h));
+  CKR(cudaIpcOpenMemHandle(out, h, cudaIpcMemLazyEnablePeerAccess));
+  return SFT_OK;
+}
+
+extern "C" int sft_ipc_close(void* p) {
+  if (p) CKR(cudaIpcCloseMemHandle(p));
   return SFT_OK;
 }
 

@@ -24,6 +24,7 @@ namespace sft {
 
 constexpr int kMaxDim = 3;
 constexpr int kMaxLevels = 21;  // N <= 2^20
+constexpr int kMaxPeers = 8;    // ranks of the fused (peer-store) exchange
 
 struct TreeLevel {
   int64_t n = 0;                  // non-empty boxes at this level
@@ -96,6 +97,9 @@ struct sft_plan_s {
   int64_t k_src_lo = 0, k_src_hi = 0;   // sorted source range of this rank's T_K leaves
   std::vector<int64_t> send_counts, recv_counts;  // [world] complex elements
   int64_t* d_seg = nullptr;  // device [2*world+1]: a-boundaries at level L-m, send segment bases
+  std::vector<int64_t> seg_host;   // host copy of the same
+  std::vector<int64_t> peer_off;   // [world] element offset of this rank's segment in each receiver's buffer
+  std::vector<double2*> peer;      // [world] receive buffers (fused exchange), empty = use the send buffer
   // tile schedules of the translation levels (one allocation; offsets per level t)
   unsigned char* sched = nullptr;
   std::vector<size_t> sched_off;
@@ -132,6 +136,12 @@ struct LevelDims {
   const int64_t* seg;  // exchange mapping (nullptr = plain layout), see api.cu
   int nseg;
   const unsigned char* sched = nullptr;  // tile schedule of this level (translate.cu, built by sft_plan)
+  // fused exchange: outputs of send-layout pair index i in segment q go to
+  // peer[q] + peer_off[q] + (i - peer_seg[q]) * p^d
+  int npeer = 0;
+  double2* peer[kMaxPeers] = {};
+  int64_t peer_off[kMaxPeers] = {};
+  int64_t peer_seg[kMaxPeers + 1] = {};
 };
 
 // level buffers are void*: complex128 (prec 0) or complex64 (prec 1) pair arrays of stride P->pds

@@ -145,6 +145,14 @@ struct TransArgs {
   int64_t out_b0, out_nA, out_a0;
   const int64_t* seg;  // [nseg+1] A boundaries at the output level, then [nseg] segment bases
   int nseg;
+  // fused exchange (multi-GPU, exchange level): the output pair with send-layout
+  // index i in segment q is stored at peer[q] + peer_off[q] + (i - peer_seg[q]) * p^d
+  // (the receiving rank's buffer, mapped into this process), i.e. the
+  // all-to-all happens in the kernel's epilogue as NVLink peer stores
+  int npeer;
+  double2* peer[kMaxPeers];
+  int64_t peer_off[kMaxPeers];
+  int64_t peer_seg[kMaxPeers + 1];
 };
 
 struct GroupMeta {
@@ -808,7 +816,18 @@ __device__ __forceinline__ void consumer_pass(const TransArgs& a, E* __restrict_
 #ifdef SFT_ABL_NOSTORE  // ablation: no output stores (shared or global)
       o0[u] = o1[u] = nullptr;
 #else
-      if (LAST) {
+      if (LAST && a.npeer > 0) {
+        // fused exchange: straight into the receiving rank's buffer
+        auto dst = [&](uint32_t off) -> E* {
+          if (off == ~0u) return nullptr;
+          const int64_t i = (int64_t)(off / (uint32_t)PD);
+          int q = 0;
+          while (q + 1 < a.npeer && i >= a.peer_seg[q + 1]) ++q;
+          return reinterpret_cast<E*>(a.peer[q]) + a.peer_off[q] + (i - a.peer_seg[q]) * PD + ebase;
+        };
+        o0[u] = dst(d.o0);
+        o1[u] = dst(d.o1);
+      } else if (LAST) {
         o0[u] = d.o0 != ~0u ? gout + d.o0 + ebase : nullptr;
         o1[u] = d.o1 != ~0u ? gout + d.o1 + ebase : nullptr;
       } else {
@@ -1128,6 +1147,9 @@ __global__ __launch_bounds__((NC + 1) * 32, MINB) void k_translate_ws(TransArgs 
       }
     }
   }
+  // fused exchange: make this rank's peer stores visible system-wide before
+  // the kernel completes (the caller's cross-rank barrier follows on the stream)
+  if (a.npeer > 0) __threadfence_system();
   INSTR_ADD(3, tc0);
 }
 
@@ -1547,6 +1569,13 @@ static TransArgs make_args(const LevelDims& L, const double2* in, double2* out) 
   a.out_a0 = L.out_a0;
   a.seg = L.seg;
   a.nseg = L.nseg;
+  a.npeer = L.npeer;
+  for (int q = 0; q < kMaxPeers; ++q) {
+    a.peer[q] = L.peer[q];
+    a.peer_off[q] = L.peer_off[q];
+    a.peer_seg[q] = L.peer_seg[q];
+  }
+  a.peer_seg[kMaxPeers] = L.peer_seg[kMaxPeers];
   return a;
 }
 

@@ -24,7 +24,7 @@ class DistPlan:
     with rank/world taken from the process group."""
 
     def __init__(self, dim, N, p, x, k, group=None, stream=None, exchange_level=-1, split_k=-1, split_x=-1,
-                 plan=None, device=None):
+                 plan=None, device=None, fused=False):
         import torch
         import torch.distributed as dist
         self.group = group
@@ -42,8 +42,21 @@ class DistPlan:
             device = x.device if isinstance(x, torch.Tensor) and x.is_cuda else torch.device(
                 "cuda", torch.cuda.current_device())
         self.device = torch.device(device)
-        self.sendbuf = torch.empty(max(1, sum(self.send_counts)), dtype=torch.complex128, device=self.device)
-        self.recvbuf = torch.empty(max(1, sum(self.recv_counts)), dtype=torch.complex128, device=self.device)
+        self.fused = bool(fused)
+        if not self.fused:
+            self.sendbuf = torch.empty(max(1, sum(self.send_counts)), dtype=torch.complex128, device=self.device)
+            self.recvbuf = torch.empty(max(1, sum(self.recv_counts)), dtype=torch.complex128, device=self.device)
+        else:
+            # fused exchange: every rank's receive buffer is mapped into every
+            # process (CUDA IPC over NVLink); the exchange level's kernel stores
+            # its outputs straight into the receivers' buffers
+            from . import device_alloc, ipc_handle, ipc_open
+            self._own = device_alloc(16 * max(1, sum(self.recv_counts)))
+            handles = [None] * self.world
+            dist.all_gather_object(handles, ipc_handle(self._own), group=group)
+            self._peers = [self._own if q == self.rank else ipc_open(handles[q]) for q in range(self.world)]
+            self.plan.set_peer_buffers(self._peers)
+            self._flag = torch.zeros(1, dtype=torch.float32, device=self.device)
 
     def partition(self):
         return self.plan.partition()
@@ -53,21 +66,37 @@ class DistPlan:
         import torch.distributed as dist
         if u is None:
             u = torch.empty(self.nx, dtype=torch.complex128, device=self.device)
-        self.plan.apply_phase1(f, self.sendbuf)
-        # the level-m charge exchange (NCCL all-to-allv over NVLink); complex128
-        # moved as (re, im) float64 pairs
-        ns, nr = sum(self.send_counts), sum(self.recv_counts)
-        dist.all_to_all_single(torch.view_as_real(self.recvbuf[:nr]).reshape(-1),
-                               torch.view_as_real(self.sendbuf[:ns]).reshape(-1),
-                               output_split_sizes=[2 * c for c in self.recv_counts],
-                               input_split_sizes=[2 * c for c in self.send_counts], group=self.group)
-        self.plan.apply_phase2(self.recvbuf, u)
+        if self.fused:
+            self.plan.apply_phase1(f, None)
+            # stream-ordered barrier: every rank's exchange-level kernel (and so
+            # its peer stores into our buffer) precedes this collective
+            dist.all_reduce(self._flag, group=self.group)
+            self.plan.apply_phase2(self._own, u)
+        else:
+            self.plan.apply_phase1(f, self.sendbuf)
+            # the level-m charge exchange (NCCL all-to-allv over NVLink); complex128
+            # moved as (re, im) float64 pairs
+            ns, nr = sum(self.send_counts), sum(self.recv_counts)
+            dist.all_to_all_single(torch.view_as_real(self.recvbuf[:nr]).reshape(-1),
+                                   torch.view_as_real(self.sendbuf[:ns]).reshape(-1),
+                                   output_split_sizes=[2 * c for c in self.recv_counts],
+                                   input_split_sizes=[2 * c for c in self.send_counts], group=self.group)
+            self.plan.apply_phase2(self.recvbuf, u)
         # every target has exactly one non-zero contributor: the sum is exact
         dist.all_reduce(torch.view_as_real(u), op=dist.ReduceOp.SUM, group=self.group)
         return u
 
     def close(self):
         self.plan.close()
+        if getattr(self, "fused", False):
+            from . import device_free, ipc_close
+            import torch
+            torch.cuda.synchronize(self.device)
+            for q, ptr in enumerate(self._peers):
+                if q != self.rank:
+                    ipc_close(ptr)
+            device_free(self._own)
+            self.fused = False
 
     def __enter__(self):
         return self

@@ -92,3 +92,47 @@ def test_multirank_C2_vs_oracle():
     tg = w.sample[:256]
     ub = oracle.butterfly(w.x, w.k, w.f, w.N, w.p, targets=tg)
     assert oracle.rel_l2(uw[tg], ub) <= 1e-10
+
+
+def emulate_fused(w, world, force=(-1, -1, -1)):
+    """Fused exchange: each emulated rank's exchange-level kernel stores its
+    level-m charges straight into the other ranks' receive buffers (here all on
+    one device, standing in for the IPC-mapped peer buffers of a multi-GPU run);
+    no send buffer and no all-to-all."""
+    import torch
+    import paper_0801_1524_b200 as sft
+    x = torch.from_numpy(w.x).cuda(); k = torch.from_numpy(w.k).cuda(); f = torch.from_numpy(w.f).cuda()
+    plans = [sft.Plan(w.dim, w.N, w.p, x, k, rank=r, world=world, split_k=force[0], split_x=force[1],
+                      exchange_level=force[2]) for r in range(world)]
+    counts = [pl.exchange_counts() for pl in plans]
+    recv = [torch.full((max(1, int(c[1].sum())),), complex("nan"), dtype=torch.complex128, device="cuda")
+            for c in counts]
+    ptrs = [t.data_ptr() for t in recv]
+    for r, pl in enumerate(plans):
+        pl.set_peer_buffers(ptrs)
+        offs = pl.peer_offsets()
+        for q in range(world):  # this rank's segment in q's buffer starts after the lower ranks' segments
+            assert int(offs[q]) == int(sum(counts[q][1][:r]))
+    for pl in plans:
+        pl.apply_phase1(f, None)
+    torch.cuda.synchronize()
+    u = torch.zeros(len(w.x), dtype=torch.complex128, device="cuda")
+    for q, pl in enumerate(plans):
+        uq = torch.empty(len(w.x), dtype=torch.complex128, device="cuda")
+        pl.apply_phase2(recv[q], uq)
+        u += uq
+    torch.cuda.synchronize()
+    for pl in plans:
+        pl.close()
+    return u.cpu().numpy()
+
+
+@pytest.mark.parametrize("name,world,force", [("C1", 2, (-1, -1, -1)), ("C1", 4, (-1, -1, -1)),
+                                              ("C0", 8, (-1, -1, -1)), ("C1", 2, (1, 0, 10)), ("C1", 2, (0, 3, 0))])
+def test_fused_exchange_bitwise(name, world, force):
+    w = synth.make_workload(name)
+    L = w.N.bit_length() - 1
+    force = tuple(L if v == 10 else v for v in force)
+    u1 = single(w)
+    uw = emulate_fused(w, world, force)
+    assert np.array_equal(uw, u1)
