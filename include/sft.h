@@ -55,7 +55,9 @@ enum {
 typedef struct sft_plan_s* sft_plan_t;
 
 typedef struct {
-  int precision;      /* 0 = FP64 (the only value supported in this build) */
+  int precision;      /* 0 = FP64 (default); 1 = FP32 storage of the level charges
+                       *     (operators, leaf/final arithmetic and tensor-core
+                       *     accumulation stay FP64; ~1e-6 relative error; world == 1 only) */
   void* stream;       /* cudaStream_t for all device work; NULL = default stream */
   int rank;           /* this rank's index, 0 <= rank < world */
   int world;          /* number of ranks sharing the transform; 1 = single GPU */

@@ -766,7 +766,7 @@ __global__ void k_check_schedule(TransArgs a, const unsigned char* __restrict__ 
 #ifndef SFT_NSUB
 #define SFT_NSUB 1
 #endif
-template <int D, int P, int G, int NC, int AX, bool LAST, int LIST = AX, typename E = double2>
+template <int D, int P, int G, int NC, int AX, bool LAST, int LIST = AX, typename E = double2, bool FUSED = false>
 __device__ __forceinline__ void consumer_pass(const TransArgs& a, E* __restrict__ sb,
                                               const unsigned char* __restrict__ blk, const LaneOps<P>& op) {
   using S = MmaShape<P>;
@@ -816,7 +816,7 @@ __device__ __forceinline__ void consumer_pass(const TransArgs& a, E* __restrict_
 #ifdef SFT_ABL_NOSTORE  // ablation: no output stores (shared or global)
       o0[u] = o1[u] = nullptr;
 #else
-      if (LAST && a.npeer > 0) {
+      if (LAST && FUSED) {
         // fused exchange: straight into the receiving rank's buffer
         auto dst = [&](uint32_t off) -> E* {
           if (off == ~0u) return nullptr;
@@ -1043,7 +1043,7 @@ __device__ __forceinline__ void ws_producer(const TransArgs& a, const unsigned c
 // 2D with NST >= 3: skewed pipeline, pass 1 of tile i+1 runs before pass 0 of
 // tile i, and pass 0 waits on an mbarrier (p1done) every consumer thread
 // arrives on after its pass-1 rows, so warps do not idle at a pass barrier.
-template <int D, int P, int G, int NC, int NST, int MINB, typename E = double2>
+template <int D, int P, int G, int NC, int NST, int MINB, typename E = double2, bool FUSED = false>
 __global__ __launch_bounds__((NC + 1) * 32, MINB) void k_translate_ws(TransArgs a, const double* __restrict__ frag,
                                                                              const unsigned char* __restrict__ sched,
                                                                              int64_t ntiles) {
@@ -1080,8 +1080,8 @@ __global__ __launch_bounds__((NC + 1) * 32, MINB) void k_translate_ws(TransArgs 
     if constexpr (D == 2) consumer_pass<D, P, G, NC, 0, false, 2, E>(a, sb_, bk, op);
   };
   auto last2d = [&](E* sb_, const unsigned char* bk) {
-    consumer_pass<D, P, G, NC, 0, true, 0, E>(a, sb_, bk, op);
-    if constexpr (D == 2) consumer_pass<D, P, G, NC, D - 1, true, 3, E>(a, sb_, bk, op);
+    consumer_pass<D, P, G, NC, 0, true, 0, E, FUSED>(a, sb_, bk, op);
+    if constexpr (D == 2) consumer_pass<D, P, G, NC, D - 1, true, 3, E, FUSED>(a, sb_, bk, op);
   };
   if constexpr (D == 2 && NST >= 3) {
     int64_t tile = blockIdx.x;
@@ -1136,7 +1136,7 @@ __global__ __launch_bounds__((NC + 1) * 32, MINB) void k_translate_ws(TransArgs 
         consumer_sync<NC * 32>();
         consumer_pass<D, P, G, NC, 1, false, 1, E>(a, sb, blk[s], op);
         consumer_sync<NC * 32>();
-        consumer_pass<D, P, G, NC, 0, true, 0, E>(a, sb, blk[s], op);
+        consumer_pass<D, P, G, NC, 0, true, 0, E, FUSED>(a, sb, blk[s], op);
       }
       __syncwarp();
       if (lane == 0)
@@ -1149,7 +1149,7 @@ __global__ __launch_bounds__((NC + 1) * 32, MINB) void k_translate_ws(TransArgs 
   }
   // fused exchange: make this rank's peer stores visible system-wide before
   // the kernel completes (the caller's cross-rank barrier follows on the stream)
-  if (a.npeer > 0) __threadfence_system();
+  if (FUSED) __threadfence_system();
   INSTR_ADD(3, tc0);
 }
 
@@ -1685,8 +1685,20 @@ static cudaError_t launch_translate_t(const sft_plan_s* Pl, const LevelDims& L, 
     if (!L.sched) return cudaErrorInvalidValue;
     const int64_t ntiles = (a.ngroups + G - 1) / G;
     const int64_t grid = std::min<int64_t>(ntiles, grid_max);
-    launch_pdl(k_translate_ws<D, P, G, NC, NST, MB>, (unsigned)grid, (NC + 1) * 32, smem, Pl->stream, a, frag,
-               L.sched, ntiles);
+    if (a.npeer > 0) {
+      static bool fattr = false;
+      if (!fattr) {
+        cudaError_t e = cudaFuncSetAttribute(k_translate_ws<D, P, G, NC, NST, MB, double2, true>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        fattr = true;
+      }
+      launch_pdl(k_translate_ws<D, P, G, NC, NST, MB, double2, true>, (unsigned)grid, (NC + 1) * 32, smem,
+                 Pl->stream, a, frag, L.sched, ntiles);
+    } else {
+      launch_pdl(k_translate_ws<D, P, G, NC, NST, MB>, (unsigned)grid, (NC + 1) * 32, smem, Pl->stream, a, frag,
+                 L.sched, ntiles);
+    }
   } else {
     constexpr int G = FmaCfg<D, P>::G, NT = FmaCfg<D, P>::NT;
     const size_t smem = (size_t)G * (1 << D) * PD * sizeof(double2);
