@@ -761,17 +761,30 @@ __global__ void k_check_schedule(TransArgs a, const unsigned char* __restrict__ 
   if (bad) atomicOr(err, 4);
 }
 
+#ifdef SFT_NSUB
+#define SFT_NSUB35 SFT_NSUB
+#define SFT_NSUB_OTHER SFT_NSUB
+#endif
+#ifndef SFT_NSUB35
+#define SFT_NSUB35 2
+#endif
+#ifndef SFT_NSUB_OTHER
+#define SFT_NSUB_OTHER 1
+#endif
 // One pass of the consumers (NC warps): super-tiles of 8 fiber rows, NSUB
 // super-tiles per warp iteration (independent MMA chains interleaved).
-#ifndef SFT_NSUB
-#define SFT_NSUB 1
-#endif
+// Measured (C3 translate, B200): 3D p = 5 1.108 -> 1.023 ms with NSUB = 2; 2D p = 9
+// 1.50 -> 2.37 ms and 3D p = 7 53.2 -> 55.8 ms (register pressure).  SFT_NSUB overrides.
+template <int D, int P>
+struct NsubCfg {
+  static constexpr int v = (D == 3 && P == 5) ? SFT_NSUB35 : SFT_NSUB_OTHER;
+};
 template <int D, int P, int G, int NC, int AX, bool LAST, int LIST = AX, typename E = double2, bool FUSED = false>
 __device__ __forceinline__ void consumer_pass(const TransArgs& a, E* __restrict__ sb,
                                               const unsigned char* __restrict__ blk, const LaneOps<P>& op) {
   using S = MmaShape<P>;
   using SC = Sched<D, P, G>;
-  constexpr int NSUB = SFT_NSUB;
+  constexpr int NSUB = NsubCfg<D, P>::v;
   constexpr int PF = Pow<P, D>::v / P;
   constexpr int PD = StrideT<E, Pow<P, D>::v>::v;  // slot stride (elements)
   E* const gout = reinterpret_cast<E*>(a.out);
