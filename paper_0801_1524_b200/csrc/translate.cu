@@ -765,6 +765,9 @@ __global__ void k_check_schedule(TransArgs a, const unsigned char* __restrict__ 
 #define SFT_NSUB35 SFT_NSUB
 #define SFT_NSUB_OTHER SFT_NSUB
 #endif
+#ifndef SFT_ROTATE
+#define SFT_ROTATE 1
+#endif
 #ifndef SFT_NSUB35
 #define SFT_NSUB35 2
 #endif
@@ -781,7 +784,8 @@ struct NsubCfg {
 };
 template <int D, int P, int G, int NC, int AX, bool LAST, int LIST = AX, typename E = double2, bool FUSED = false>
 __device__ __forceinline__ void consumer_pass(const TransArgs& a, E* __restrict__ sb,
-                                              const unsigned char* __restrict__ blk, const LaneOps<P>& op) {
+                                              const unsigned char* __restrict__ blk, const LaneOps<P>& op,
+                                              int& rot) {
   using S = MmaShape<P>;
   using SC = Sched<D, P, G>;
   constexpr int NSUB = NsubCfg<D, P>::v;
@@ -800,7 +804,13 @@ __device__ __forceinline__ void consumer_pass(const TransArgs& a, E* __restrict_
   int off[S::NK];
 #pragma unroll
   for (int kk = 0; kk < S::NK; ++kk) off[kk] = (op.bk[kk] == 1 ? (1 << SH) * PD : 0) + op.lk[kk] * STR;
-  for (int st0 = warp * NSUB; st0 < nst; st0 += NC * NSUB) {
+  // units of NSUB super-tiles go round-robin over the warps, continuing from
+  // where the previous pass stopped (rot), so that the extra unit of a pass
+  // whose count is not a multiple of NC does not always land on warp 0
+  const int j0 = warp >= rot ? warp - rot : warp - rot + NC;
+  // (measured: C2 -0.8%, C1 -2%, C3 +2%: 2D only)
+  if (SFT_ROTATE && D == 2) rot = (rot + (nst + NSUB - 1) / NSUB) % NC;
+  for (int st0 = j0 * NSUB; st0 < nst; st0 += NC * NSUB) {
     const E* x[NSUB];
     E* o0[NSUB];
     E* o1[NSUB];
@@ -1083,18 +1093,18 @@ __global__ __launch_bounds__((NC + 1) * 32, MINB) void k_translate_ws(TransArgs 
   // ---------------- consumers ----------------
   LaneOps<P> op;
   load_lane_ops<P>(op, frag, lane);
-  int s = 0;
+  int s = 0, rot = 0;
   uint32_t ph = 0;
   INSTR_T0(tc0);
   // 2D: first passes (list 1: axis 1, list 2: axis 0 for groups in reversed
   // order), then last passes (list 0: axis 0, list 3: axis 1)
   auto first2d = [&](E* sb_, const unsigned char* bk) {
-    consumer_pass<D, P, G, NC, D - 1, false, 1, E>(a, sb_, bk, op);
-    if constexpr (D == 2) consumer_pass<D, P, G, NC, 0, false, 2, E>(a, sb_, bk, op);
+    consumer_pass<D, P, G, NC, D - 1, false, 1, E>(a, sb_, bk, op, rot);
+    if constexpr (D == 2) consumer_pass<D, P, G, NC, 0, false, 2, E>(a, sb_, bk, op, rot);
   };
   auto last2d = [&](E* sb_, const unsigned char* bk) {
-    consumer_pass<D, P, G, NC, 0, true, 0, E, FUSED>(a, sb_, bk, op);
-    if constexpr (D == 2) consumer_pass<D, P, G, NC, D - 1, true, 3, E, FUSED>(a, sb_, bk, op);
+    consumer_pass<D, P, G, NC, 0, true, 0, E, FUSED>(a, sb_, bk, op, rot);
+    if constexpr (D == 2) consumer_pass<D, P, G, NC, D - 1, true, 3, E, FUSED>(a, sb_, bk, op, rot);
   };
   if constexpr (D == 2 && NST >= 3) {
     int64_t tile = blockIdx.x;
@@ -1145,11 +1155,11 @@ __global__ __launch_bounds__((NC + 1) * 32, MINB) void k_translate_ws(TransArgs 
         last2d(sb, blk[s]);
         INSTR_ADD(7, t3);
       } else {
-        consumer_pass<D, P, G, NC, 2, false, 2, E>(a, sb, blk[s], op);
+        consumer_pass<D, P, G, NC, 2, false, 2, E>(a, sb, blk[s], op, rot);
         consumer_sync<NC * 32>();
-        consumer_pass<D, P, G, NC, 1, false, 1, E>(a, sb, blk[s], op);
+        consumer_pass<D, P, G, NC, 1, false, 1, E>(a, sb, blk[s], op, rot);
         consumer_sync<NC * 32>();
-        consumer_pass<D, P, G, NC, 0, true, 0, E, FUSED>(a, sb, blk[s], op);
+        consumer_pass<D, P, G, NC, 0, true, 0, E, FUSED>(a, sb, blk[s], op, rot);
       }
       __syncwarp();
       if (lane == 0)
