@@ -379,19 +379,45 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
       : "d"(a), "d"(b));
 }
 
-template <int P>
+// measured: C2 translate 1.546 -> 1.457 ms with the table in shared memory,
+// C3 1.026 -> 1.044 ms: 2D only (SFT_TAIL_SMEM overrides)
+#ifndef SFT_TAIL_SMEM
+#define SFT_TAIL_SMEM 2
+#endif
+template <int D>
+struct TailSmem {
+  static constexpr bool v = SFT_TAIL_SMEM == 2 ? D == 2 : SFT_TAIL_SMEM == 1;
+};
+// tail column weights (m = P-1) per (k-step, lane%4) -- (P weight, Q weight);
+// in shared memory (SFT_TAIL_SMEM) they cost one broadcast load per k-step
+// instead of 2*NK registers per thread
+__shared__ double2 s_tail[8][4];
+
+template <int P, bool TS>
 struct LaneOps {
   using S = MmaShape<P>;
   double fb[S::NK][S::NT];           // B fragments of the operator
-  double ft[S::NK][2];               // tail column (m = P-1): P and Q weights of this lane's k
-  int lk[S::NK], bk[S::NK];          // element index l and child (2 = padding) of this lane's k
+  double ft[TS ? 1 : S::NK][2];      // tail column (m = P-1): P and Q weights of this lane's k
+  // child (0, 1; 2 = padding) and element index of this lane's k in k-step kk
+  __device__ __forceinline__ static int bk(int kk, int lane) {
+    const int k = 4 * kk + (lane & 3);
+    return k < 2 * P ? k / P : 2;
+  }
+  __device__ __forceinline__ static int lk(int kk, int lane) {
+    const int k = 4 * kk + (lane & 3);
+    return k < 2 * P ? k % P : 0;
+  }
+  __device__ __forceinline__ double2 tail(int kk, int lane) const {
+    if constexpr (TS) return s_tail[kk][lane & 3];
+    else return make_double2(ft[kk][0], ft[kk][1]);
+  }
 };
 
 // k-steps [K_LO, K_HI) of one MMA super-tile: A fragments (re and im of one
 // complex element per lane, one 16-byte shared-memory load) times the B
 // fragments held in registers; tail column m = P-1 on DFMA.
-template <int P, int K_LO, int K_HI, int NSUB, typename E = double2>
-__device__ __forceinline__ void mma_steps(const LaneOps<P>& op, const E* const (&x)[NSUB],
+template <int P, int K_LO, int K_HI, int NSUB, typename E, class OPS>
+__device__ __forceinline__ void mma_steps(const OPS& op, const E* const (&x)[NSUB],
                                           const int (&off)[MmaShape<P>::NK], const bool (&p0)[NSUB],
                                           const bool (&p1)[NSUB], double (&are)[NSUB][MmaShape<P>::NT][2],
                                           double (&aim)[NSUB][MmaShape<P>::NT][2], double (&tl)[NSUB][4]) {
@@ -402,7 +428,7 @@ __device__ __forceinline__ void mma_steps(const LaneOps<P>& op, const E* const (
 #pragma unroll
     for (int u = 0; u < NSUB; ++u) {
 #ifdef SFT_NO_ZEROFILL
-      const int b = op.bk[kk];
+      const int b = OPS::bk(kk, threadIdx.x);
       const bool live = b == 0 ? p0[u] : (b == 1 ? p1[u] : false);
       av[u] = live ? ElemT<E>::ld(x[u][off[kk]]) : make_double2(0.0, 0.0);
 #else
@@ -424,18 +450,19 @@ __device__ __forceinline__ void mma_steps(const LaneOps<P>& op, const E* const (
         }
       }
     if (S::TAIL) {
+      const double2 ft = op.tail(kk, threadIdx.x);
 #pragma unroll
       for (int u = 0; u < NSUB; ++u) {
         if (kk == K_LO) {
-          tl[u][0] = av[u].x * op.ft[kk][0];
-          tl[u][1] = av[u].x * op.ft[kk][1];
-          tl[u][2] = av[u].y * op.ft[kk][0];
-          tl[u][3] = av[u].y * op.ft[kk][1];
+          tl[u][0] = av[u].x * ft.x;
+          tl[u][1] = av[u].x * ft.y;
+          tl[u][2] = av[u].y * ft.x;
+          tl[u][3] = av[u].y * ft.y;
         } else {
-          tl[u][0] = fma(av[u].x, op.ft[kk][0], tl[u][0]);
-          tl[u][1] = fma(av[u].x, op.ft[kk][1], tl[u][1]);
-          tl[u][2] = fma(av[u].y, op.ft[kk][0], tl[u][2]);
-          tl[u][3] = fma(av[u].y, op.ft[kk][1], tl[u][3]);
+          tl[u][0] = fma(av[u].x, ft.x, tl[u][0]);
+          tl[u][1] = fma(av[u].x, ft.y, tl[u][1]);
+          tl[u][2] = fma(av[u].y, ft.x, tl[u][2]);
+          tl[u][3] = fma(av[u].y, ft.y, tl[u][3]);
         }
       }
     }
@@ -784,7 +811,8 @@ struct NsubCfg {
 };
 template <int D, int P, int G, int NC, int AX, bool LAST, int LIST = AX, typename E = double2, bool FUSED = false>
 __device__ __forceinline__ void consumer_pass(const TransArgs& a, E* __restrict__ sb,
-                                              const unsigned char* __restrict__ blk, const LaneOps<P>& op,
+                                              const unsigned char* __restrict__ blk,
+                                              const LaneOps<P, TailSmem<D>::v>& op,
                                               int& rot) {
   using S = MmaShape<P>;
   using SC = Sched<D, P, G>;
@@ -803,7 +831,8 @@ __device__ __forceinline__ void consumer_pass(const TransArgs& a, E* __restrict_
   const int rfib = (r >> 1) + 4 * (r & 1);  // rows 2q, 2q+1 <- fibers q, q+4 (bank-conflict-free)
   int off[S::NK];
 #pragma unroll
-  for (int kk = 0; kk < S::NK; ++kk) off[kk] = (op.bk[kk] == 1 ? (1 << SH) * PD : 0) + op.lk[kk] * STR;
+  for (int kk = 0; kk < S::NK; ++kk)
+    off[kk] = (LaneOps<P, true>::bk(kk, lane) == 1 ? (1 << SH) * PD : 0) + LaneOps<P, true>::lk(kk, lane) * STR;
   // units of NSUB super-tiles go round-robin over the warps, continuing from
   // where the previous pass stopped (rot), so that the extra unit of a pass
   // whose count is not a multiple of NC does not always land on warp 0
@@ -945,22 +974,33 @@ __device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
   }
 }
 
-template <int P>
-__device__ __forceinline__ void load_lane_ops(LaneOps<P>& op, const double* __restrict__ frag, int lane) {
+// the shared tail table, filled by threads 0..3 before the kernel's first __syncthreads
+template <int D, int P>
+__device__ __forceinline__ void fill_tail_smem(const double* __restrict__ frag) {
+  using S = MmaShape<P>;
+  if (TailSmem<D>::v && S::TAIL && threadIdx.x < 4) {
+#pragma unroll
+    for (int kk = 0; kk < S::NK; ++kk)
+      s_tail[kk][threadIdx.x] = make_double2(frag[S::NK * S::NT * 32 + (kk * 2 + 0) * 32 + threadIdx.x],
+                                             frag[S::NK * S::NT * 32 + (kk * 2 + 1) * 32 + threadIdx.x]);
+  }
+}
+
+template <int P, bool TS>
+__device__ __forceinline__ void load_lane_ops(LaneOps<P, TS>& op, const double* __restrict__ frag, int lane) {
   using S = MmaShape<P>;
 #pragma unroll
   for (int kk = 0; kk < S::NK; ++kk) {
 #pragma unroll
     for (int n = 0; n < S::NT; ++n) op.fb[kk][n] = frag[(kk * S::NT + n) * 32 + lane];
-    if (S::TAIL) {
-      op.ft[kk][0] = frag[S::NK * S::NT * 32 + (kk * 2 + 0) * 32 + lane];
-      op.ft[kk][1] = frag[S::NK * S::NT * 32 + (kk * 2 + 1) * 32 + lane];
-    } else {
-      op.ft[kk][0] = op.ft[kk][1] = 0.0;
+    if constexpr (!TS) {
+      if (S::TAIL) {
+        op.ft[kk][0] = frag[S::NK * S::NT * 32 + (kk * 2 + 0) * 32 + lane];
+        op.ft[kk][1] = frag[S::NK * S::NT * 32 + (kk * 2 + 1) * 32 + lane];
+      } else {
+        op.ft[kk][0] = op.ft[kk][1] = 0.0;
+      }
     }
-    const int k = 4 * kk + (lane & 3);
-    op.bk[kk] = k < 2 * P ? k / P : 2;
-    op.lk[kk] = k < 2 * P ? k % P : 0;
   }
 }
 
@@ -1085,14 +1125,15 @@ __global__ __launch_bounds__((NC + 1) * 32, MINB) void k_translate_ws(TransArgs 
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&p1done[threadIdx.x])), "r"(NC * 32));
   }
   if (threadIdx.x == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  fill_tail_smem<D, P>(frag);
   __syncthreads();
   if (warp == NC) {
     ws_producer<D, P, G, NST, E, PD>(a, sched, ntiles, ring, blk, full, empty);
     return;
   }
   // ---------------- consumers ----------------
-  LaneOps<P> op;
-  load_lane_ops<P>(op, frag, lane);
+  LaneOps<P, TailSmem<D>::v> op;
+  load_lane_ops(op, frag, lane);
   int s = 0, rot = 0;
   uint32_t ph = 0;
   INSTR_T0(tc0);
