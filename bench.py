@@ -187,6 +187,26 @@ def run_ours(args):
             kt.append(plan.last_timing())
         plan.set_timing(False)
         st = plan.stats()
+        # multi-RHS apply (sft_apply_batch): args.nrhs
+        # charge vectors through the plan, one launch per step for all of them;
+        # skipped when the batch's level buffers would not fit comfortably
+        batch = None
+        R = args.nrhs
+        need = R * st["level_buffer_bytes"]
+        if R > 1 and need < 0.5 * torch.cuda.get_device_properties(dev).total_memory:
+            F = torch.stack([torch.from_numpy(synth.random_charges(len(w.k), 1000 + r)) for r in range(R)]).to(dev)
+            U = torch.empty(R, len(w.x), dtype=torch.complex128, device=dev)
+            for _ in range(max(2, args.warmup)):
+                plan.apply_batch(F, U)
+            b_total, _ = timed(lambda: plan.apply_batch(F, U), args.steps)
+            b_ms = b_total / args.steps
+            batch = {"nrhs": R, "apply_ms": round(b_ms, 4), "apply_ms_per_rhs": round(b_ms / R, 4),
+                     "mpoints_s": round(P * R / (b_ms / 1e3) / 1e6, 3),
+                     "speedup_vs_single": round((apply_total / args.steps) * R / b_ms, 3),
+                     "note": "f resident in HBM, L2 flushed before each batch; value = P * nrhs / batch apply time"}
+            del F, U
+        elif R > 1:
+            batch = {"nrhs": R, "skipped": f"level buffers {need / 1e9:.1f} GB"}
         plan.close()
     else:
         dp = DistPlan(w.dim, w.N, w.p, x, k, stream=stream, fused=fused)
@@ -196,6 +216,7 @@ def run_ours(args):
         part = dp.partition().tolist()
         dp.close()
         kt = None
+        batch = None
         st = sft.Plan(w.dim, w.N, w.p, x, k, stream=stream)
         stats = st.stats()
         st.close()
@@ -277,6 +298,8 @@ def run_ours(args):
             "clocks": clocks,
             "roofline": roof,
         }
+        if batch is not None:
+            res["batch"] = batch
         if world > 1:
             res["partition"] = part[:3]
     if world > 1:
@@ -369,6 +392,8 @@ def main():
     ap.add_argument("--exchange", default="nccl", choices=["nccl", "fused"],
                     help="N > 1: level-m exchange by NCCL all-to-all, or fused into the exchange level's kernel "
                          "(peer stores into IPC-mapped receive buffers over NVLink)")
+    ap.add_argument("--nrhs", type=int, default=4,
+                    help="N = 1: also time sft_apply_batch with this many charge vectors (1 = skip)")
     ap.add_argument("--precision", default="f64", choices=["f64", "f32"],
                     help="arithmetic of the level charges (f32: the optional FP32 variant, single GPU)")
     args = ap.parse_args()

@@ -86,6 +86,17 @@ int sft_plan(int dim, int64_t N, int p, const double* x, int64_t nx, const doubl
  * complex128, host or device.  Only valid for world == 1 plans. */
 int sft_apply(sft_plan_t plan, const void* f, void* u);
 
+/* Multi-RHS apply: u_r = butterfly(f_r) for nrhs
+ * charge vectors through one plan, r = 0..nrhs-1.  f_r at f + r*ldf and u_r at
+ * u + r*ldu (complex128 elements, ldf >= nk, ldu >= nx); f and u host or device.
+ * Same arithmetic per vector as sft_apply (bitwise identical results), but one
+ * launch per step for all vectors: the leaf weights and final-step powers are
+ * computed once per point and the tile schedules once per tile for the whole
+ * batch.  Needs nrhs x the plan's level-buffer bytes of extra device memory
+ * (allocated on the first call and kept; SFT_E_NOMEM if it does not fit).
+ * 1 <= nrhs <= 4096; world == 1 plans only (SFT_E_STATE otherwise). */
+int sft_apply_batch(sft_plan_t plan, int nrhs, const void* f, int64_t ldf, void* u, int64_t ldu);
+
 /* NULL is a no-op. */
 int sft_destroy(sft_plan_t plan);
 

@@ -67,6 +67,7 @@ def lib():
     L.sft_plan.argtypes = [ctypes.c_int, ctypes.c_int64, ctypes.c_int, vp, ctypes.c_int64, vp, ctypes.c_int64,
                            ctypes.POINTER(_Opts), ctypes.POINTER(vp)]
     L.sft_apply.argtypes = [vp, vp, vp]
+    L.sft_apply_batch.argtypes = [vp, ctypes.c_int, vp, ctypes.c_int64, vp, ctypes.c_int64]
     L.sft_destroy.argtypes = [vp]
     L.sft_strerror.argtypes = [ctypes.c_int]
     L.sft_strerror.restype = ctypes.c_char_p
@@ -169,6 +170,22 @@ class Plan:
             u = self._like(fk, self.nk if self.adjoint else self.nx)
         up, uk = _ptr(u, np.complex128)
         _check(lib().sft_apply(self._h, fp, up))
+        return uk
+
+    def apply_batch(self, f, u=None):
+        """sft_apply_batch: f [nrhs, n_in] complex128 (row r = one charge vector,
+        rows contiguous), u [nrhs, n_out]; one launch per step for all rows."""
+        fp, fk = _ptr(f, np.complex128)
+        if len(fk.shape) != 2:
+            raise ValueError("apply_batch: f must be 2-D [nrhs, n]")
+        nrhs, ldf = int(fk.shape[0]), int(fk.shape[1])
+        nout = self.nk if self.adjoint else self.nx
+        if u is None:
+            u = self._like(fk, nrhs * nout).reshape(nrhs, nout)
+        up, uk = _ptr(u, np.complex128)
+        if tuple(uk.shape) != (nrhs, nout):
+            raise ValueError("apply_batch: u must be [nrhs, n_out]")
+        _check(lib().sft_apply_batch(self._h, nrhs, fp, ldf, up, nout))
         return uk
 
     @staticmethod

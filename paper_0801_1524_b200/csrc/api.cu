@@ -345,8 +345,10 @@ static void plan_free(sft_plan_s* P) {
   if (P->sched_ready) cudaStreamWaitEvent(s, P->sched_ready, 0);
   free_tree(P->X, s);
   free_tree(P->K, s);
-  for (int i = 0; i < 2; ++i)
+  for (int i = 0; i < 2; ++i) {
     if (P->buf[i]) cudaFreeAsync(P->buf[i], s);
+    if (P->bufb[i]) cudaFreeAsync(P->bufb[i], s);
+  }
   if (P->f_stage) cudaFreeAsync(P->f_stage, s);
   if (P->u_stage) cudaFreeAsync(P->u_stage, s);
   if (P->d_err) cudaFreeAsync(P->d_err, s);
@@ -645,22 +647,62 @@ static int finish_timing(sft_plan_s* P, int n_levels_first) {
   return SFT_OK;
 }
 
-extern "C" int sft_apply(sft_plan_t P, const void* f, void* u) {
-  if (!P || !f || !u) return fail(SFT_E_ARG, "NULL argument");
-  if (P->world != 1) return fail(SFT_E_STATE, "sft_apply needs a world == 1 plan; use the phase calls");
+// Steps 2-4 for nrhs charge vectors (f + r*ldf -> u + r*ldu, complex128
+// elements).  nrhs == 1 uses the plan's two level buffers; a batch uses
+// [nrhs][buf_elems] buffers (grown on demand) and one launch per step for all
+// vectors: the leaf weights, final-step powers, tile schedules and operator
+// fragments are computed / read once for every RHS.
+static int apply_impl(sft_plan_s* P, int nrhs, const void* f, int64_t ldf, void* u, int64_t ldu) {
   cudaStream_t s = P->stream;
   const int L = P->L;
   const double2* fd = (const double2*)f;
   double2* ud = (double2*)u;
   const bool f_host = !is_device_ptr(f), u_host = !is_device_ptr(u);
-  if (f_host) {
-    if (!P->f_stage) CKR(cudaMallocAsync(&P->f_stage, P->nk * sizeof(double2), s));
-    CKR(cudaMemcpyAsync(P->f_stage, f, P->nk * sizeof(double2), cudaMemcpyHostToDevice, s));
-    fd = P->f_stage;
+  if ((f_host || u_host) && P->stage_rhs < nrhs) {
+    if (P->f_stage) cudaFreeAsync(P->f_stage, s);
+    if (P->u_stage) cudaFreeAsync(P->u_stage, s);
+    P->f_stage = P->u_stage = nullptr;
+    P->stage_rhs = 0;
+    CKR(cudaMallocAsync(&P->f_stage, (size_t)nrhs * P->nk * sizeof(double2), s));
+    CKR(cudaMallocAsync(&P->u_stage, (size_t)nrhs * P->nx * sizeof(double2), s));
+    P->stage_rhs = nrhs;
   }
+  if (f_host) {
+    CKR(cudaMemcpy2DAsync(P->f_stage, P->nk * sizeof(double2), f, ldf * sizeof(double2), P->nk * sizeof(double2),
+                          nrhs, cudaMemcpyHostToDevice, s));
+    fd = P->f_stage;
+    ldf = P->nk;
+  }
+  int64_t ldu_dev = ldu;
   if (u_host) {
-    if (!P->u_stage) CKR(cudaMallocAsync(&P->u_stage, P->nx * sizeof(double2), s));
     ud = P->u_stage;
+    ldu_dev = P->nx;
+  }
+  double2* buf[2] = {P->buf[0], P->buf[1]};
+  int64_t rs = 0;
+  if (nrhs > 1) {
+    if (P->bufb_rhs < nrhs) {
+      const size_t esz = P->prec == 1 ? sizeof(float2) : sizeof(double2);
+      for (int i = 0; i < 2; ++i) {
+        if (P->bufb[i]) cudaFreeAsync(P->bufb[i], s);
+        P->bufb[i] = nullptr;
+      }
+      P->bufb_rhs = 0;
+      for (int i = 0; i < 2; ++i)
+        if (cudaMallocAsync(&P->bufb[i], (size_t)nrhs * P->buf_elems * esz, s) != cudaSuccess) {
+          cudaGetLastError();
+          for (int j = 0; j < 2; ++j) {
+            if (P->bufb[j]) cudaFreeAsync(P->bufb[j], s);
+            P->bufb[j] = nullptr;
+          }
+          return fail(SFT_E_NOMEM, "batch level buffers: " + std::to_string(nrhs) + " x " +
+                                       std::to_string(2.0 * P->buf_elems * esz / 1e9) + " GB");
+        }
+      P->bufb_rhs = nrhs;
+    }
+    buf[0] = P->bufb[0];
+    buf[1] = P->bufb[1];
+    rs = (int64_t)P->buf_elems;
   }
   if (P->timing && P->ev_created < L + 3) {
     for (int i = P->ev_created; i < L + 3; ++i) cudaEventCreate(&P->ev[i]);
@@ -669,23 +711,40 @@ extern "C" int sft_apply(sft_plan_t P, const void* f, void* u) {
   P->n_ev = 0;
   tmark(P);
   // step 2: leaf charges, level L buffer
-  CKR(launch_leaf(P, fd, P->buf[L & 1], 0, P->K.counts[L]));
+  CKR(launch_leaf(P, fd, buf[L & 1], 0, P->K.counts[L], nrhs, ldf, rs));
   tmark(P);
   // step 3: t = L-1 .. 0 (after the plan's schedule kernel on the side stream)
   if (P->sched_ready) CKR(cudaStreamWaitEvent(s, P->sched_ready, 0));
   for (int t = L - 1; t >= 0; --t) {
     LevelDims ld = apply_dims_sched(P, t);
-    CKR(launch_translate(P, ld, P->buf[(t + 1) & 1], P->buf[t & 1]));
+    ld.nrhs = nrhs;
+    ld.rs = rs;
+    CKR(launch_translate(P, ld, buf[(t + 1) & 1], buf[t & 1]));
     tmark(P);
   }
   // step 4: final evaluation, level 0 buffer [A leaves]
-  CKR(launch_final(P, P->buf[0], ud, 0, 0, P->nx));
+  CKR(launch_final(P, buf[0], ud, 0, 0, P->nx, nrhs, rs, ldu_dev));
   tmark(P);
   if (u_host) {
-    CKR(cudaMemcpyAsync(u, ud, P->nx * sizeof(double2), cudaMemcpyDeviceToHost, s));
+    CKR(cudaMemcpy2DAsync(u, ldu * sizeof(double2), ud, ldu_dev * sizeof(double2), P->nx * sizeof(double2), nrhs,
+                          cudaMemcpyDeviceToHost, s));
     CKR(cudaStreamSynchronize(s));
   }
   return finish_timing(P, L - 1);
+}
+
+extern "C" int sft_apply(sft_plan_t P, const void* f, void* u) {
+  if (!P || !f || !u) return fail(SFT_E_ARG, "NULL argument");
+  if (P->world != 1) return fail(SFT_E_STATE, "sft_apply needs a world == 1 plan; use the phase calls");
+  return apply_impl(P, 1, f, P->nk, u, P->nx);
+}
+
+extern "C" int sft_apply_batch(sft_plan_t P, int nrhs, const void* f, int64_t ldf, void* u, int64_t ldu) {
+  if (!P || !f || !u) return fail(SFT_E_ARG, "NULL argument");
+  if (nrhs < 1 || nrhs > 4096) return fail(SFT_E_ARG, "nrhs must be in [1, 4096]");
+  if (ldf < P->nk || ldu < P->nx) return fail(SFT_E_ARG, "ldf >= nk and ldu >= nx required");
+  if (P->world != 1) return fail(SFT_E_STATE, "sft_apply_batch needs a world == 1 plan");
+  return apply_impl(P, nrhs, f, ldf, u, ldu);
 }
 
 // ---------------------------------------------------------------------------

@@ -45,9 +45,8 @@ __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
 constexpr int kLeafWin = 24;
 
 template <int D, int P>
-__device__ __forceinline__ void leaf_weights(const double* __restrict__ k_sorted, const int32_t* __restrict__ perm,
-                                             const double2* __restrict__ f, int conj, int64_t N, int j, const double* cdq,
-                                             const double* sdq, const double* inv_s, double (*w)[P], double2* fo) {
+__device__ __forceinline__ void leaf_weights(const double* __restrict__ k_sorted, int64_t N, int j, const double* cdq,
+                                             const double* sdq, const double* inv_s, double (*w)[P], double2* rot) {
   constexpr int P1 = P - 1;
   double ssum = 0.0;
 #pragma unroll
@@ -75,9 +74,7 @@ __device__ __forceinline__ void leaf_weights(const double* __restrict__ k_sorted
   }
   double sn, cs;
   sincospi(ssum, &sn, &cs);
-  double2 fj = f[perm[j]];
-  if (conj) fj.y = -fj.y;
-  *fo = cmul(fj, make_double2(cs, sn));
+  *rot = make_double2(cs, sn);  // e^{i pi sum_a s_a}, applied to each RHS's charge
 }
 
 template <int D, int P, typename T2, int PS>
@@ -87,12 +84,13 @@ __global__ __launch_bounds__(128, D == 2 ? 4 : 2) void k_leaf(const double* __re
                                                               const int32_t* __restrict__ leaf_of,
                                                               const double2* __restrict__ f,
                                                               const double* __restrict__ invD, T2* __restrict__ out,
-                                                              int64_t b_lo, int64_t b_hi, int64_t N, int conj) {
+                                                              int64_t b_lo, int64_t b_hi, int64_t N, int conj,
+                                                              int nrhs, int64_t ldf, int64_t ors) {
   constexpr int PD = Pow<P, D>::v;
   constexpr int NACC = (PD + 31) / 32;
   constexpr int P1 = P - 1;
   __shared__ double w_s[4][32][D][P];
-  __shared__ double2 f_s[4][32];
+  __shared__ double2 f_s[4][32], rot_s[4][32];
   __shared__ double cdq[P], sdq[P], inv_s[P];
   if (threadIdx.x < P) {
     double sn, cs;
@@ -119,14 +117,22 @@ __global__ __launch_bounds__(128, D == 2 ? 4 : 2) void k_leaf(const double* __re
   for (int c0 = js; c0 < je; c0 += 32) {
     // weights of the sources [c0, c0 + 32) of this batch
     const int n = min(32, je - c0);
-    if (lane < n) leaf_weights<D, P>(k_sorted, perm, f, conj, N, c0 + lane, cdq, sdq, inv_s, w_s[warp][lane], &f_s[warp][lane]);
+    if (lane < n) leaf_weights<D, P>(k_sorted, N, c0 + lane, cdq, sdq, inv_s, w_s[warp][lane], &rot_s[warp][lane]);
+    const int pj = lane < n ? perm[c0 + lane] : 0;
+    // the weights are shared by every RHS of a batch (sft_apply_batch)
+    for (int rh = 0; rh < nrhs; ++rh) {
+    if (lane < n) {
+      double2 fj = f[(int64_t)rh * ldf + pj];
+      if (conj) fj.y = -fj.y;
+      f_s[warp][lane] = cmul(fj, rot_s[warp][lane]);
+    }
     __syncwarp();
     // leaves whose sources intersect [c0, c0 + n)
     for (int64_t b = lb; b < le; ++b) {
       const int jb0 = first_pt[b], jb1 = first_pt[b + 1];
       if (jb1 <= c0 || jb0 >= c0 + n) continue;
       const int t0 = max(jb0, c0) - c0, t1 = min(jb1, c0 + n) - c0;
-      T2* o = out + (b - b_lo) * (int64_t)PS;
+      T2* o = out + (int64_t)rh * ors + (b - b_lo) * (int64_t)PS;
 #pragma unroll
       for (int i = 0; i < NACC; ++i) {
         const int e = lane + 32 * i;
@@ -156,6 +162,7 @@ __global__ __launch_bounds__(128, D == 2 ? 4 : 2) void k_leaf(const double* __re
       }
     }
     __syncwarp();
+    }
   }
 }
 
@@ -172,11 +179,13 @@ template <int D, int P, typename T2, int PS>
 __global__ __launch_bounds__(128) void k_final(const double* __restrict__ x_sorted, const int32_t* __restrict__ perm,
                                                const int32_t* __restrict__ leaf_of,
                                                const T2* __restrict__ h0, double2* __restrict__ u,
-                                               int64_t i_lo, int64_t i_hi, int64_t a_lo, int64_t N, int conj) {
+                                               int64_t i_lo, int64_t i_hi, int64_t a_lo, int64_t N, int conj,
+                                               int nrhs, int64_t hrs, int64_t ldu) {
   constexpr int P1 = P - 1;
   const int64_t j = i_lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (j >= i_hi) return;
-  const T2* h = h0 + ((int64_t)leaf_of[j] - a_lo) * (int64_t)PS;
+  const T2* const hl = h0 + ((int64_t)leaf_of[j] - a_lo) * (int64_t)PS;
+  const int32_t pj = perm[j];
   double2 z[D], el[P];
 #pragma unroll
   for (int a = 0; a < D; ++a) {
@@ -189,6 +198,9 @@ __global__ __launch_bounds__(128) void k_final(const double* __restrict__ x_sort
   el[0] = make_double2(1.0, 0.0);
 #pragma unroll
   for (int l = 1; l < P; ++l) el[l] = cmul(el[l - 1], z[D - 1]);
+  // the powers are shared by every RHS of a batch (sft_apply_batch)
+  for (int rh = 0; rh < nrhs; ++rh) {
+  const T2* h = hl + (int64_t)rh * hrs;
   auto inner = [&](int base) {
     double2 t = make_double2(0.0, 0.0);
 #pragma unroll
@@ -228,7 +240,8 @@ __global__ __launch_bounds__(128) void k_final(const double* __restrict__ x_sort
     }
   }
   if (conj) s.y = -s.y;
-  u[perm[j]] = s;
+  u[(int64_t)rh * ldu + pj] = s;
+  }
 }
 
 __global__ void k_zero(double2* p, int64_t n) {
@@ -240,7 +253,8 @@ __global__ void k_zero(double2* p, int64_t n) {
 // launchers
 // ------------------------------------------------------------------------
 
-cudaError_t launch_leaf(const sft_plan_s* Pl, const double2* f, void* out, int64_t b_lo, int64_t b_hi) {
+cudaError_t launch_leaf(const sft_plan_s* Pl, const double2* f, void* out, int64_t b_lo, int64_t b_hi, int nrhs,
+                        int64_t ldf, int64_t ors) {
   if (b_hi <= b_lo) return cudaSuccess;
   // sources of leaves [b_lo, b_hi): one warp per window of kLeafWin sources
   const int64_t ns = b_lo == 0 && b_hi == Pl->K.counts[Pl->L] ? Pl->nk : Pl->k_src_hi - Pl->k_src_lo;
@@ -250,29 +264,30 @@ cudaError_t launch_leaf(const sft_plan_s* Pl, const double2* f, void* out, int64
     SFT_DISPATCH(Pl->d, Pl->p,
                  (k_leaf<D, P, float2, Pow<P, D>::v + (Pow<P, D>::v & 1)><<<nb, 128, 0, Pl->stream>>>(
                      Pl->K.pts_sorted, Pl->K.perm, Pl->K.first_pt, Pl->K.leaf_of, f, Pl->tab->leaf_invD, (float2*)out, b_lo, b_hi,
-                     Pl->N, Pl->conj)));
+                     Pl->N, Pl->conj, nrhs, ldf, ors)));
   } else {
     SFT_DISPATCH(Pl->d, Pl->p,
                  (k_leaf<D, P, double2, Pow<P, D>::v><<<nb, 128, 0, Pl->stream>>>(
                      Pl->K.pts_sorted, Pl->K.perm, Pl->K.first_pt, Pl->K.leaf_of, f, Pl->tab->leaf_invD, (double2*)out, b_lo, b_hi,
-                     Pl->N, Pl->conj)));
+                     Pl->N, Pl->conj, nrhs, ldf, ors)));
   }
   count_launch();
   return cudaGetLastError();
 }
 
-cudaError_t launch_final(const sft_plan_s* Pl, const void* h0, double2* u, int64_t a_lo, int64_t i_lo, int64_t i_hi) {
+cudaError_t launch_final(const sft_plan_s* Pl, const void* h0, double2* u, int64_t a_lo, int64_t i_lo, int64_t i_hi,
+                         int nrhs, int64_t hrs, int64_t ldu) {
   // targets = sorted points [i_lo, i_hi) of T_X; h0 holds the leaves from a_lo on
   if (i_hi <= i_lo) return cudaSuccess;
   const unsigned nb = (unsigned)((i_hi - i_lo + 127) / 128);
   if (Pl->prec == 1) {
     SFT_DISPATCH(Pl->d, Pl->p,
                  (k_final<D, P, float2, Pow<P, D>::v + (Pow<P, D>::v & 1)><<<nb, 128, 0, Pl->stream>>>(
-                     Pl->X.pts_sorted, Pl->X.perm, Pl->X.leaf_of, (const float2*)h0, u, i_lo, i_hi, a_lo, Pl->N, Pl->conj)));
+                     Pl->X.pts_sorted, Pl->X.perm, Pl->X.leaf_of, (const float2*)h0, u, i_lo, i_hi, a_lo, Pl->N, Pl->conj, nrhs, hrs, ldu)));
   } else {
     SFT_DISPATCH(Pl->d, Pl->p,
                  (k_final<D, P, double2, Pow<P, D>::v><<<nb, 128, 0, Pl->stream>>>(
-                     Pl->X.pts_sorted, Pl->X.perm, Pl->X.leaf_of, (const double2*)h0, u, i_lo, i_hi, a_lo, Pl->N, Pl->conj)));
+                     Pl->X.pts_sorted, Pl->X.perm, Pl->X.leaf_of, (const double2*)h0, u, i_lo, i_hi, a_lo, Pl->N, Pl->conj, nrhs, hrs, ldu)));
   }
   count_launch();
   return cudaGetLastError();

@@ -85,6 +85,10 @@ struct sft_plan_s {
   // two live level buffers, complex128 (or complex64 if prec == 1)
   double2* buf[2] = {nullptr, nullptr};
   size_t buf_elems = 0;
+  // level buffers of the multi-RHS apply (sft_apply_batch): [bufb_rhs][buf_elems] each, grown on demand
+  double2* bufb[2] = {nullptr, nullptr};
+  int bufb_rhs = 0;
+  int64_t stage_rhs = 0;  // RHS capacity of f_stage / u_stage (host-pointer batches)
   // staging for host pointers
   double2* f_stage = nullptr;
   double2* u_stage = nullptr;
@@ -142,10 +146,17 @@ struct LevelDims {
   double2* peer[kMaxPeers] = {};
   int64_t peer_off[kMaxPeers] = {};
   int64_t peer_seg[kMaxPeers + 1] = {};
+  // multi-RHS batch (sft_apply_batch): nrhs independent charge vectors through
+  // the same schedule; RHS r of the input / output level lives at in/out + r * rs
+  // (elements of the stored type)
+  int nrhs = 1;
+  int64_t rs = 0;
 };
 
 // level buffers are void*: complex128 (prec 0) or complex64 (prec 1) pair arrays of stride P->pds
-cudaError_t launch_leaf(const sft_plan_s* P, const double2* f, void* out, int64_t b_lo, int64_t b_hi);
+// nrhs > 1: charge vector r at f + r * ldf (complex128), its leaf level at out + r * ors (stored elements)
+cudaError_t launch_leaf(const sft_plan_s* P, const double2* f, void* out, int64_t b_lo, int64_t b_hi, int nrhs = 1,
+                        int64_t ldf = 0, int64_t ors = 0);
 cudaError_t launch_translate(const sft_plan_s* P, const LevelDims& L, const void* in, void* out);
 // tile schedule of one level (sizes and builder; 0 bytes when the kernel needs none)
 size_t schedule_bytes(const sft_plan_s* P, const LevelDims& L);
@@ -156,7 +167,9 @@ cudaError_t launch_schedule(const sft_plan_s* P, const LevelDims* L, int nlev, u
 cudaError_t check_schedule(const sft_plan_s* P, const LevelDims& L, const unsigned char* sched, int64_t in_pairs,
                            int64_t out_pairs, int* err);
 // step 4 for the sorted targets [i_lo, i_hi) (the points of leaves a_lo...); g0 holds leaves from a_lo on
-cudaError_t launch_final(const sft_plan_s* P, const void* g0, double2* u, int64_t a_lo, int64_t i_lo, int64_t i_hi);
+// nrhs > 1: level-0 charges of RHS r at g0 + r * hrs (stored elements), potentials at u + r * ldu
+cudaError_t launch_final(const sft_plan_s* P, const void* g0, double2* u, int64_t a_lo, int64_t i_lo, int64_t i_hi,
+                         int nrhs = 1, int64_t hrs = 0, int64_t ldu = 0);
 cudaError_t launch_zero(double2* p, int64_t n, cudaStream_t s);
 
 template <int B, int E>

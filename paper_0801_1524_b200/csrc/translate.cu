@@ -153,6 +153,10 @@ struct TransArgs {
   double2* peer[kMaxPeers];
   int64_t peer_off[kMaxPeers];
   int64_t peer_seg[kMaxPeers + 1];
+  // multi-RHS batch: work item w = (tile w / nrhs, RHS w % nrhs); RHS r reads
+  // in + r * rs and writes out + r * rs (elements of the stored type)
+  int nrhs;
+  int64_t rs;
 };
 
 struct GroupMeta {
@@ -813,13 +817,13 @@ template <int D, int P, int G, int NC, int AX, bool LAST, int LIST = AX, typenam
 __device__ __forceinline__ void consumer_pass(const TransArgs& a, E* __restrict__ sb,
                                               const unsigned char* __restrict__ blk,
                                               const LaneOps<P, TailSmem<D>::v>& op,
-                                              int& rot) {
+                                              int& rot, int64_t ooff = 0) {
   using S = MmaShape<P>;
   using SC = Sched<D, P, G>;
   constexpr int NSUB = NsubCfg<D, P>::v;
   constexpr int PF = Pow<P, D>::v / P;
   constexpr int PD = StrideT<E, Pow<P, D>::v>::v;  // slot stride (elements)
-  E* const gout = reinterpret_cast<E*>(a.out);
+  E* const gout = reinterpret_cast<E*>(a.out) + ooff;  // ooff: RHS offset of a batch
   constexpr int STR = Pow<P, D - 1 - AX>::v;
   constexpr int SH = D - 1 - AX;
   const int* cnt = SC::cnt(blk) + 3 * LIST;
@@ -1020,19 +1024,24 @@ __device__ __forceinline__ void ws_producer(const TransArgs& a, const unsigned c
     INSTR_T0(tp0);
     int s = 0;
     uint32_t ph = 0;
-    int64_t tile = blockIdx.x;
-    uint2 gr = (tile < ntiles && lane < G) ? __ldg(reinterpret_cast<const uint2*>(sched + tile * SC::BLK + SC::HDR) + lane)
-                                           : make_uint2(0u, 0u);
+    // work items w = tile * nrhs + r (nrhs = 1: w = tile)
+    const int64_t nwork = ntiles * a.nrhs;
+    int64_t w = blockIdx.x;
+    int64_t tile = a.nrhs == 1 ? w : w / a.nrhs;
+    uint2 gr = (w < nwork && lane < G) ? __ldg(reinterpret_cast<const uint2*>(sched + tile * SC::BLK + SC::HDR) + lane)
+                                       : make_uint2(0u, 0u);
     // programmatic dependent launch: everything above (schedule reads, barrier
     // init, the consumers' operand loads) overlaps the previous level's tail;
     // the previous level's output (our input) and input (our output buffer)
     // are touched only after it has completed
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    for (int i = 0; tile < ntiles; ++i) {
-      const int64_t next = tile + gridDim.x;
-      const uint2 gn = (next < ntiles && lane < G)
+    for (int i = 0; w < nwork; ++i) {
+      const int64_t wn = w + gridDim.x;
+      const int64_t next = a.nrhs == 1 ? wn : wn / a.nrhs;
+      const uint2 gn = (wn < nwork && lane < G)
                            ? __ldg(reinterpret_cast<const uint2*>(sched + next * SC::BLK + SC::HDR) + lane)
                            : make_uint2(0u, 0u);
+      const E* const ain = reinterpret_cast<const E*>(a.in) + (w - tile * a.nrhs) * a.rs;
       INSTR_T0(tw0);
       if (i >= NST) mbar_wait_sleep(smem_u32(&empty[s]), ph ^ 1u);
       INSTR_ADD(1, tw0);
@@ -1078,7 +1087,7 @@ __device__ __forceinline__ void ws_producer(const TransArgs& a, const unsigned c
         asm volatile(
             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                 smem_u32(sb + ((int64_t)lane * NS + c) * PD)),
-            "l"(reinterpret_cast<const E*>(a.in) + pin * PD), "r"((uint32_t)(PD * sizeof(E))), "r"(smem_u32(&full[s]))
+            "l"(ain + pin * PD), "r"((uint32_t)(PD * sizeof(E))), "r"(smem_u32(&full[s]))
             : "memory");
 #else
         (void)pin;
@@ -1089,6 +1098,7 @@ __device__ __forceinline__ void ws_producer(const TransArgs& a, const unsigned c
       }
       INSTR_ADD(2, tb0);
       gr = gn;
+      w = wn;
       tile = next;
       if (++s == NST) {
         s = 0;
@@ -1143,22 +1153,25 @@ __global__ __launch_bounds__((NC + 1) * 32, MINB) void k_translate_ws(TransArgs 
     consumer_pass<D, P, G, NC, D - 1, false, 1, E>(a, sb_, bk, op, rot);
     if constexpr (D == 2) consumer_pass<D, P, G, NC, 0, false, 2, E>(a, sb_, bk, op, rot);
   };
-  auto last2d = [&](E* sb_, const unsigned char* bk) {
-    consumer_pass<D, P, G, NC, 0, true, 0, E, FUSED>(a, sb_, bk, op, rot);
-    if constexpr (D == 2) consumer_pass<D, P, G, NC, D - 1, true, 3, E, FUSED>(a, sb_, bk, op, rot);
+  auto last2d = [&](E* sb_, const unsigned char* bk, int64_t oo) {
+    consumer_pass<D, P, G, NC, 0, true, 0, E, FUSED>(a, sb_, bk, op, rot, oo);
+    if constexpr (D == 2) consumer_pass<D, P, G, NC, D - 1, true, 3, E, FUSED>(a, sb_, bk, op, rot, oo);
   };
+  // work items w = tile * nrhs + r; the output of RHS r goes to out + r * rs
+  const int64_t nwork = ntiles * a.nrhs;
+  auto ooff = [&](int64_t w_) { return a.nrhs == 1 ? (int64_t)0 : (w_ % a.nrhs) * a.rs; };
   if constexpr (D == 2 && NST >= 3) {
     int64_t tile = blockIdx.x;
-    if (tile < ntiles) {
+    if (tile < nwork) {
       mbar_wait(smem_u32(&full[0]), 0);
       first2d(ring, blk[0]);
       asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&p1done[0])) : "memory");
     }
-    for (; tile < ntiles; tile += gridDim.x) {
+    for (; tile < nwork; tile += gridDim.x) {
       const int64_t nt = tile + gridDim.x;
       const int sn = s + 1 == NST ? 0 : s + 1;
       const uint32_t phn = sn == 0 ? ph ^ 1u : ph;
-      if (nt < ntiles) {
+      if (nt < nwork) {
         INSTR_T0(tf0);
         mbar_wait(smem_u32(&full[sn]), phn);
         INSTR_ADD(4, tf0);
@@ -1171,7 +1184,7 @@ __global__ __launch_bounds__((NC + 1) * 32, MINB) void k_translate_ws(TransArgs 
       mbar_wait(smem_u32(&p1done[s]), ph);
       INSTR_ADD(6, t2);
       INSTR_T0(t3);
-      last2d(ring + s * STAGE, blk[s]);
+      last2d(ring + s * STAGE, blk[s], ooff(tile));
       INSTR_ADD(7, t3);
       __syncwarp();
       if (lane == 0)
@@ -1180,7 +1193,7 @@ __global__ __launch_bounds__((NC + 1) * 32, MINB) void k_translate_ws(TransArgs 
       ph = phn;
     }
   } else {
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    for (int64_t w = blockIdx.x; w < nwork; w += gridDim.x) {
       INSTR_T0(tf0);
       mbar_wait(smem_u32(&full[s]), ph);
       INSTR_ADD(4, tf0);
@@ -1193,14 +1206,14 @@ __global__ __launch_bounds__((NC + 1) * 32, MINB) void k_translate_ws(TransArgs 
         consumer_sync<NC * 32>();
         INSTR_ADD(6, t2);
         INSTR_T0(t3);
-        last2d(sb, blk[s]);
+        last2d(sb, blk[s], ooff(w));
         INSTR_ADD(7, t3);
       } else {
         consumer_pass<D, P, G, NC, 2, false, 2, E>(a, sb, blk[s], op, rot);
         consumer_sync<NC * 32>();
         consumer_pass<D, P, G, NC, 1, false, 1, E>(a, sb, blk[s], op, rot);
         consumer_sync<NC * 32>();
-        consumer_pass<D, P, G, NC, 0, true, 0, E, FUSED>(a, sb, blk[s], op, rot);
+        consumer_pass<D, P, G, NC, 0, true, 0, E, FUSED>(a, sb, blk[s], op, rot, ooff(w));
       }
       __syncwarp();
       if (lane == 0)
@@ -1640,6 +1653,8 @@ static TransArgs make_args(const LevelDims& L, const double2* in, double2* out) 
     a.peer_seg[q] = L.peer_seg[q];
   }
   a.peer_seg[kMaxPeers] = L.peer_seg[kMaxPeers];
+  a.nrhs = L.nrhs;
+  a.rs = L.rs;
   return a;
 }
 
@@ -1704,6 +1719,8 @@ static cudaError_t launch_translate_t(const sft_plan_s* Pl, const LevelDims& L, 
   constexpr int PD = Pow<P, D>::v;
   TransArgs a = make_args(L, (const double2*)in, (double2*)out);
   if (a.ngroups <= 0) return cudaSuccess;
+  if (a.nrhs < 1 || (a.nrhs > 1 && (a.npeer > 0 || (Pl->prec == 1 ? f32_ffma() : translate_kernel_choice() != 0))))
+    return cudaErrorInvalidValue;  // batches run on the warp-specialised DMMA kernel only
   if (Pl->prec == 1 && !f32_ffma()) {
     // FP32 storage, FP64 arithmetic on the tensor cores (same kernel as FP64)
     constexpr int G = F32WsCfg<D, P>::G, NC = F32WsCfg<D, P>::NC, NST = F32WsCfg<D, P>::NST,
@@ -1719,7 +1736,7 @@ static cudaError_t launch_translate_t(const sft_plan_s* Pl, const LevelDims& L, 
     }
     if (!L.sched) return cudaErrorInvalidValue;
     const int64_t ntiles = (a.ngroups + G - 1) / G;
-    const int64_t grid = std::min<int64_t>(ntiles, grid_max);
+    const int64_t grid = std::min<int64_t>(ntiles * a.nrhs, grid_max);
     launch_pdl(k_translate_ws<D, P, G, NC, NST, MB, float2>, (unsigned)grid, (NC + 1) * 32, smem, Pl->stream, a, frag,
                L.sched, ntiles);
   } else if (Pl->prec == 1) {
@@ -1748,7 +1765,7 @@ static cudaError_t launch_translate_t(const sft_plan_s* Pl, const LevelDims& L, 
     }
     if (!L.sched) return cudaErrorInvalidValue;
     const int64_t ntiles = (a.ngroups + G - 1) / G;
-    const int64_t grid = std::min<int64_t>(ntiles, grid_max);
+    const int64_t grid = std::min<int64_t>(ntiles * a.nrhs, grid_max);
     if (a.npeer > 0) {
       static bool fattr = false;
       if (!fattr) {
