@@ -97,6 +97,27 @@ int sft_apply(sft_plan_t plan, const void* f, void* u);
  * 1 <= nrhs <= 4096; world == 1 plans only (SFT_E_STATE otherwise). */
 int sft_apply_batch(sft_plan_t plan, int nrhs, const void* f, int64_t ldf, void* u, int64_t ldu);
 
+/* Far-field adapter (eq. far): a plan whose sft_apply computes
+ *   u_inf(xhat_i) = sum_j exp(-i kappa xhat_i . y_j) F_j
+ * (F_j = f(y_j) ds_j, the quadrature-weighted density on the scatterer
+ * boundary; kappa = the wave number, written N in eq. far).
+ *   xhat: [nx][dim] unit directions, y: [ny][dim] points in [0,1]^dim
+ *   (float64 row-major, host or device; the caller rescales the scatterer
+ *   into the unit box).  kappa in (0, pi 2^20].
+ * The SFT size is N = the smallest power of two >= max(2, kappa/pi); the
+ * points become x = N/2 - kappa xhat/(2 pi) and k = N y (a kernel), so that
+ * 2 pi x.k/N = pi sum_a k_a - kappa xhat.y: "after we rescale xhat and y by a
+ * factor of N, (far) takes the form of (sfft)".  The leftover
+ * phase e^{i pi sum_a k_a} is folded into the leaf kernel (a sign per leaf
+ * box).  opts->adjoint = 1 gives the adjoint v_j = sum_i exp(+i kappa
+ * xhat_i . y_j) g_i (g on the directions, v on the scatterer points; the
+ * phase then goes into the final kernel).  sft_apply / sft_apply_batch /
+ * sft_destroy as for any plan; world == 1 only.  Errors as sft_plan, plus
+ * SFT_E_ARG for a bad kappa; SFT_E_DOMAIN if a y is outside [0,1]^dim or a
+ * |xhat_a| > 1. */
+int sft_farfield_plan(int dim, double kappa, int p, const double* xhat, int64_t nx, const double* y, int64_t ny,
+                      const sft_opts* opts, sft_plan_t* out);
+
 /* NULL is a no-op. */
 int sft_destroy(sft_plan_t plan);
 

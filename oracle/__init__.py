@@ -46,6 +46,8 @@ def lib():
         L = ctypes.CDLL(_LIB)
         L.oracle_direct.argtypes = [ctypes.c_int, ctypes.c_double, _c_dp, ctypes.c_int64, _c_dp, ctypes.c_int64,
                                     _c_dp, _c_dp, _c_i64p, ctypes.c_int64, ctypes.c_int]
+        L.oracle_farfield_direct.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.c_int, _c_dp, ctypes.c_int64, _c_dp,
+                                             ctypes.c_int64, _c_dp, _c_dp, ctypes.c_int]
         L.oracle_G.argtypes = [ctypes.c_int, _c_dp]
         L.oracle_H.argtypes = [ctypes.c_int, _c_dp]
         for fn in (L.oracle_M1, L.oracle_E1):
@@ -99,6 +101,20 @@ def direct(x, k, f, N, targets=None, nthreads=0) -> np.ndarray:
                              tp, nt, int(nthreads))
     if rc:
         raise ValueError(f"oracle_direct rc={rc}")
+    return u
+
+
+def farfield_direct(xhat, y, F, kappa, sign=-1, nthreads=0) -> np.ndarray:
+    """u_i = sum_j exp(sign * i kappa xhat_i.y_j) F_j: the far-field pattern of
+    eq. (far), PAPER.md:82-96, with the quadrature F_j = f(y_j) ds_j (sign -1);
+    sign +1 is the adjoint sum.  Long double, plain definition."""
+    xhat = _f64(xhat); y = _f64(y)
+    Fv = _cplx_view(F)
+    u = np.zeros(len(xhat), dtype=np.complex128)
+    rc = lib().oracle_farfield_direct(xhat.shape[1], float(kappa), int(sign), _dp(xhat), len(xhat), _dp(y), len(y),
+                                      _dp(Fv), _dp(u.view(np.float64)), int(nthreads))
+    if rc:
+        raise ValueError(f"oracle_farfield_direct rc={rc}")
     return u
 
 

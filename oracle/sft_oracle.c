@@ -24,6 +24,9 @@
  *   oracle_pair_charges    §2.1 fig. 1 + §2.2 step 3
  *   oracle_eval_charges    field of equivalent charges, P:191-197 / step 4 P:306-311
  *   oracle_butterfly       §2.2 steps 1-4
+ *   oracle_farfield_direct eq. (far), discretised: u_inf(xhat_i) =
+ *                          sum_j e^{-i kappa xhat_i.y_j} F_j (sign s = -1;
+ *                          s = +1 gives the adjoint sum)
  *
  * Box conventions (DESIGN.md readings): N = 2^L; level l boxes have width
  * N >> l and integer coordinates c in [0, 2^l)^d, corner c*(N>>l); a point
@@ -80,6 +83,32 @@ int oracle_direct(int d, double N, const double* x, int64_t nx, const double* k,
     }
     u[2 * ii] = (double)creall(acc);
     u[2 * ii + 1] = (double)cimagl(acc);
+  }
+  return 0;
+}
+
+/* Far-field pattern, eq. (far) P:82-96 with the integral replaced by the
+ * given quadrature (F_j = f(y_j) ds_j):
+ *   u_i = sum_j e^{s i kappa xhat_i . y_j} F_j,  s = -1 (eq. far) or +1 (adjoint).
+ * Plain definition in long double, fixed j order; the phase is reduced in
+ * turns before the sine/cosine (as in oracle_direct). */
+int oracle_farfield_direct(int d, double kappa, int sign, const double* xhat, int64_t nx, const double* y, int64_t ny,
+                           const double* F, double* u, int nthreads) {
+  if (d < 1 || d > 3 || !(kappa > 0) || (sign != 1 && sign != -1)) return 1;
+#ifdef _OPENMP
+  if (nthreads > 0) omp_set_num_threads(nthreads);
+#pragma omp parallel for schedule(dynamic, 16)
+#endif
+  for (int64_t i = 0; i < nx; ++i) {
+    cld acc = 0;
+    for (int64_t j = 0; j < ny; ++j) {
+      ld dot = 0;
+      for (int a = 0; a < d; ++a) dot += (ld)xhat[i * d + a] * (ld)y[j * d + a];
+      cld e = turn((ld)sign * (ld)kappa * dot / TWO_PI_L);
+      acc += e * ((ld)F[2 * j] + I * (ld)F[2 * j + 1]);
+    }
+    u[2 * i] = (double)creall(acc);
+    u[2 * i + 1] = (double)cimagl(acc);
   }
   return 0;
 }

@@ -67,6 +67,8 @@ def lib():
     L.sft_plan.argtypes = [ctypes.c_int, ctypes.c_int64, ctypes.c_int, vp, ctypes.c_int64, vp, ctypes.c_int64,
                            ctypes.POINTER(_Opts), ctypes.POINTER(vp)]
     L.sft_apply.argtypes = [vp, vp, vp]
+    L.sft_farfield_plan.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.c_int, vp, ctypes.c_int64, vp,
+                                    ctypes.c_int64, ctypes.POINTER(_Opts), ctypes.POINTER(vp)]
     L.sft_apply_batch.argtypes = [vp, ctypes.c_int, vp, ctypes.c_int64, vp, ctypes.c_int64]
     L.sft_destroy.argtypes = [vp]
     L.sft_strerror.argtypes = [ctypes.c_int]
@@ -161,6 +163,36 @@ class Plan:
         _check(L.sft_plan(self.dim, self.N, self.p, xp, self.nx, kp, self.nk, ctypes.byref(o), ctypes.byref(h)))
         self._h = h
         self._x = self._k = None  # the plan copied what it needs
+
+    @classmethod
+    def farfield(cls, dim, kappa, p, xhat, y, stream=None, precision=0, adjoint=False):
+        """sft_farfield_plan: apply(F) = u_inf(xhat_i) = sum_j exp(-i kappa xhat_i.y_j) F_j
+        (PAPER.md:82-96), xhat [nx, dim] unit directions, y [ny, dim] in [0,1]^dim.
+        adjoint=True: apply(g) = sum_i exp(+i kappa xhat_i.y_j) g_i on the y points."""
+        L = lib()
+        o = _Opts()
+        L.sft_default_opts(ctypes.byref(o))
+        o.precision = int(precision)
+        o.adjoint = 1 if adjoint else 0
+        o.stream = _stream_handle(stream)
+        xp, xk = _ptr(xhat, np.float64)
+        yp, yk = _ptr(y, np.float64)
+        nx, ny = int(xk.shape[0]), int(yk.shape[0])
+        h = ctypes.c_void_p()
+        _check(L.sft_farfield_plan(int(dim), float(kappa), int(p), xp, nx, yp, ny, ctypes.byref(o), ctypes.byref(h)))
+        self = cls.__new__(cls)
+        self._h = h
+        self._x = self._k = None
+        self.dim, self.p = int(dim), int(p)
+        self.nx, self.nk = nx, ny
+        self.adjoint = bool(adjoint)
+        self.world, self.rank = 1, 0
+        info = np.zeros(8)
+        _check(L.sft_plan_stats(h, None, None, None, info.ctypes.data_as(_c_dp)))
+        self.L = int(info[0])
+        self.N = 1 << self.L
+        self.kappa = float(kappa)
+        return self
 
     # -- single GPU ---------------------------------------------------------
     def apply(self, f, u=None):

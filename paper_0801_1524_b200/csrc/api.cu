@@ -610,6 +610,61 @@ extern "C" int sft_plan(int dim, int64_t N, int p, const double* x, int64_t nx, 
   return SFT_OK;
 }
 
+// Far-field adapter (eq. far): u_inf(xhat_i) = sum_j e^{-i kappa xhat_i . y_j} F_j.
+// With N = the smallest power of two >= max(2, kappa/pi), x = N/2 - kappa xhat/(2 pi) and
+// k = N y lie in [0,N]^d and 2 pi x.k/N = pi sum_a k_a - kappa xhat.y ("after we rescale
+// xhat and y by a factor of N, (far) takes the form of (sfft)").  The leftover
+// phase e^{i pi sum_a k_a} is folded into the leaf kernel (forward: a sign per leaf) or the
+// final kernel (adjoint); the butterfly itself is unchanged.
+extern "C" int sft_farfield_plan(int dim, double kappa, int p, const double* xhat, int64_t nx, const double* y,
+                                 int64_t ny, const sft_opts* opts, sft_plan_t* out) {
+  if (!out) return fail(SFT_E_ARG, "out is NULL");
+  if (dim != 2 && dim != 3) return fail(SFT_E_ARG, "dim must be 2 or 3");
+  if (!(kappa > 0.0) || !std::isfinite(kappa) || kappa > 3.14159265358979323846 * (1 << 20))
+    return fail(SFT_E_ARG, "kappa must be in (0, pi * 2^20]");
+  if (!xhat || !y) return fail(SFT_E_ARG, "xhat or y is NULL");
+  if (nx < 1 || ny < 1 || nx > INT32_MAX || ny > INT32_MAX) return fail(SFT_E_ARG, "point counts must be >= 1");
+  if (opts && opts->world != 1) return fail(SFT_E_ARG, "the far-field plan is single-GPU (world == 1)");
+  int64_t N = 2;
+  while ((double)N < kappa / 3.14159265358979323846) N <<= 1;
+  cudaStream_t s = opts ? (cudaStream_t)opts->stream : nullptr;
+  double *dx = nullptr, *dk = nullptr, *dxh = nullptr, *dy = nullptr;
+  auto cleanup = [&]() {
+    for (double* q : {dx, dk, dxh, dy})
+      if (q) cudaFreeAsync(q, s);
+  };
+  const size_t bx = (size_t)nx * dim * sizeof(double), by = (size_t)ny * dim * sizeof(double);
+  if (cudaMallocAsync(&dx, bx, s) != cudaSuccess || cudaMallocAsync(&dk, by, s) != cudaSuccess) {
+    cudaGetLastError();
+    cleanup();
+    return fail(SFT_E_NOMEM, "far-field coordinate buffers");
+  }
+  const double* sx = xhat;
+  const double* sy = y;
+  if (!is_device_ptr(xhat)) {
+    if (cudaMallocAsync(&dxh, bx, s) != cudaSuccess) { cleanup(); return fail(SFT_E_NOMEM, "xhat staging"); }
+    cudaMemcpyAsync(dxh, xhat, bx, cudaMemcpyHostToDevice, s);
+    sx = dxh;
+  }
+  if (!is_device_ptr(y)) {
+    if (cudaMallocAsync(&dy, by, s) != cudaSuccess) { cleanup(); return fail(SFT_E_NOMEM, "y staging"); }
+    cudaMemcpyAsync(dy, y, by, cudaMemcpyHostToDevice, s);
+    sy = dy;
+  }
+  cudaError_t ce = launch_ff_coords(sx, nx, sy, ny, dim, kappa, N, dx, dk, s);
+  if (ce != cudaSuccess) {
+    cleanup();
+    return fail(SFT_E_CUDA, cudaGetErrorString(ce));
+  }
+  sft_plan_t P = nullptr;
+  const int rc = sft_plan(dim, N, p, dx, nx, dk, ny, opts, &P);
+  cleanup();  // stream-ordered: sft_plan has consumed (copied) the coordinates
+  if (rc != SFT_OK) return rc;
+  P->ffmod = 1;
+  *out = P;
+  return SFT_OK;
+}
+
 extern "C" int sft_destroy(sft_plan_t plan) {
   plan_free(plan);
   return SFT_OK;

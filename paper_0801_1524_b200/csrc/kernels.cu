@@ -46,14 +46,18 @@ constexpr int kLeafWin = 24;
 
 template <int D, int P>
 __device__ __forceinline__ void leaf_weights(const double* __restrict__ k_sorted, int64_t N, int j, const double* cdq,
-                                             const double* sdq, const double* inv_s, double (*w)[P], double2* rot) {
+                                             const double* sdq, const double* inv_s, double (*w)[P], double2* rot,
+                                             int ffmod) {
   constexpr int P1 = P - 1;
   double ssum = 0.0;
+  int64_t csum = 0;
 #pragma unroll
   for (int a = 0; a < D; ++a) {
     const double kk = k_sorted[(int64_t)j * D + a];
-    const double sa = kk - fmin(floor(kk), (double)(N - 1));  // exact
+    const double ca = fmin(floor(kk), (double)(N - 1));
+    const double sa = kk - ca;  // exact
     ssum += sa;
+    csum += (int64_t)ca;
     double sn, cs;
     sincospi(sa / (double)P1, &sn, &cs);
     double sq[P], pre[P];
@@ -74,6 +78,12 @@ __device__ __forceinline__ void leaf_weights(const double* __restrict__ k_sorted
   }
   double sn, cs;
   sincospi(ssum, &sn, &cs);
+  // far-field adapter (sft_farfield_plan): the charges carry e^{-i pi sum_a k_a}
+  // = e^{-i pi sum_a s_a} (-1)^{sum_a c_a}, so the rotation becomes the sign (-1)^{sum c}
+  if (ffmod) {
+    cs = (csum & 1) ? -1.0 : 1.0;
+    sn = 0.0;
+  }
   *rot = make_double2(cs, sn);  // e^{i pi sum_a s_a}, applied to each RHS's charge
 }
 
@@ -85,7 +95,7 @@ __global__ __launch_bounds__(128, D == 2 ? 4 : 2) void k_leaf(const double* __re
                                                               const double2* __restrict__ f,
                                                               const double* __restrict__ invD, T2* __restrict__ out,
                                                               int64_t b_lo, int64_t b_hi, int64_t N, int conj,
-                                                              int nrhs, int64_t ldf, int64_t ors) {
+                                                              int nrhs, int64_t ldf, int64_t ors, int ffmod) {
   constexpr int PD = Pow<P, D>::v;
   constexpr int NACC = (PD + 31) / 32;
   constexpr int P1 = P - 1;
@@ -117,7 +127,7 @@ __global__ __launch_bounds__(128, D == 2 ? 4 : 2) void k_leaf(const double* __re
   for (int c0 = js; c0 < je; c0 += 32) {
     // weights of the sources [c0, c0 + 32) of this batch
     const int n = min(32, je - c0);
-    if (lane < n) leaf_weights<D, P>(k_sorted, N, c0 + lane, cdq, sdq, inv_s, w_s[warp][lane], &rot_s[warp][lane]);
+    if (lane < n) leaf_weights<D, P>(k_sorted, N, c0 + lane, cdq, sdq, inv_s, w_s[warp][lane], &rot_s[warp][lane], ffmod);
     const int pj = lane < n ? perm[c0 + lane] : 0;
     // the weights are shared by every RHS of a batch (sft_apply_batch)
     for (int rh = 0; rh < nrhs; ++rh) {
@@ -180,20 +190,32 @@ __global__ __launch_bounds__(128) void k_final(const double* __restrict__ x_sort
                                                const int32_t* __restrict__ leaf_of,
                                                const T2* __restrict__ h0, double2* __restrict__ u,
                                                int64_t i_lo, int64_t i_hi, int64_t a_lo, int64_t N, int conj,
-                                               int nrhs, int64_t hrs, int64_t ldu) {
+                                               int nrhs, int64_t hrs, int64_t ldu, int ffmod) {
   constexpr int P1 = P - 1;
   const int64_t j = i_lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (j >= i_hi) return;
   const T2* const hl = h0 + ((int64_t)leaf_of[j] - a_lo) * (int64_t)PS;
   const int32_t pj = perm[j];
   double2 z[D], el[P];
+  double xisum = 0.0;
+  int64_t csum = 0;
 #pragma unroll
   for (int a = 0; a < D; ++a) {
     const double xx = x_sorted[j * D + a];
-    const double xi = xx - fmin(floor(xx), (double)(N - 1));  // in [0,1], exact
+    const double ca = fmin(floor(xx), (double)(N - 1));
+    const double xi = xx - ca;  // in [0,1], exact
+    xisum += xi;
+    csum += (int64_t)ca;
     double sn, cs;
     sincospi((2.0 * xi - 1.0) / (double)P1, &sn, &cs);
     z[a] = make_double2(cs, sn);
+  }
+  // far-field adapter, adjoint plan: potentials carry e^{i pi sum_a x_a}
+  // = (-1)^{sum c} e^{i pi sum xi} (applied after the conjugation)
+  double2 fmod_ = make_double2(1.0, 0.0);
+  if (ffmod) {
+    sincospi(xisum, &fmod_.y, &fmod_.x);
+    if (csum & 1) fmod_ = make_double2(-fmod_.x, -fmod_.y);
   }
   el[0] = make_double2(1.0, 0.0);
 #pragma unroll
@@ -240,8 +262,36 @@ __global__ __launch_bounds__(128) void k_final(const double* __restrict__ x_sort
     }
   }
   if (conj) s.y = -s.y;
+  if (ffmod) s = cmul(s, fmod_);
   u[(int64_t)rh * ldu + pj] = s;
   }
+}
+
+// Far-field adapter (eq. far): directions xhat (|xhat| = 1) and
+// scatterer points y in [0,1]^d become SFT points x = N/2 - kappa xhat/(2 pi),
+// k = N y in [0,N]^d, so that 2 pi x.k/N = pi sum_a k_a - kappa xhat.y.
+// Rounding can push |x_a - N/2| past N/2 by an ulp when |xhat_a| = 1: such
+// points are clamped; anything further out is left for sft_plan's domain check.
+__global__ void k_ff_coords(const double* __restrict__ xhat, int64_t nx, const double* __restrict__ y, int64_t ny,
+                            int d, double kappa, double N, double* __restrict__ x, double* __restrict__ k) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const double sc = kappa / (2.0 * 3.14159265358979323846);
+  if (i < nx * d) {
+    double v = 0.5 * N - sc * xhat[i];
+    const double tol = 1e-12 * N;
+    if (v < 0.0 && v > -tol) v = 0.0;
+    if (v > N && v < N + tol) v = N;
+    x[i] = v;
+  }
+  if (i < ny * d) k[i] = N * y[i];
+}
+
+cudaError_t launch_ff_coords(const double* xhat, int64_t nx, const double* y, int64_t ny, int d, double kappa,
+                             int64_t N, double* x, double* k, cudaStream_t s) {
+  const int64_t n = std::max(nx, ny) * d;
+  k_ff_coords<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(xhat, nx, y, ny, d, kappa, (double)N, x, k);
+  count_launch();
+  return cudaGetLastError();
 }
 
 __global__ void k_zero(double2* p, int64_t n) {
@@ -264,12 +314,12 @@ cudaError_t launch_leaf(const sft_plan_s* Pl, const double2* f, void* out, int64
     SFT_DISPATCH(Pl->d, Pl->p,
                  (k_leaf<D, P, float2, Pow<P, D>::v + (Pow<P, D>::v & 1)><<<nb, 128, 0, Pl->stream>>>(
                      Pl->K.pts_sorted, Pl->K.perm, Pl->K.first_pt, Pl->K.leaf_of, f, Pl->tab->leaf_invD, (float2*)out, b_lo, b_hi,
-                     Pl->N, Pl->conj, nrhs, ldf, ors)));
+                     Pl->N, Pl->conj, nrhs, ldf, ors, Pl->ffmod && !Pl->conj)));
   } else {
     SFT_DISPATCH(Pl->d, Pl->p,
                  (k_leaf<D, P, double2, Pow<P, D>::v><<<nb, 128, 0, Pl->stream>>>(
                      Pl->K.pts_sorted, Pl->K.perm, Pl->K.first_pt, Pl->K.leaf_of, f, Pl->tab->leaf_invD, (double2*)out, b_lo, b_hi,
-                     Pl->N, Pl->conj, nrhs, ldf, ors)));
+                     Pl->N, Pl->conj, nrhs, ldf, ors, Pl->ffmod && !Pl->conj)));
   }
   count_launch();
   return cudaGetLastError();
@@ -283,11 +333,11 @@ cudaError_t launch_final(const sft_plan_s* Pl, const void* h0, double2* u, int64
   if (Pl->prec == 1) {
     SFT_DISPATCH(Pl->d, Pl->p,
                  (k_final<D, P, float2, Pow<P, D>::v + (Pow<P, D>::v & 1)><<<nb, 128, 0, Pl->stream>>>(
-                     Pl->X.pts_sorted, Pl->X.perm, Pl->X.leaf_of, (const float2*)h0, u, i_lo, i_hi, a_lo, Pl->N, Pl->conj, nrhs, hrs, ldu)));
+                     Pl->X.pts_sorted, Pl->X.perm, Pl->X.leaf_of, (const float2*)h0, u, i_lo, i_hi, a_lo, Pl->N, Pl->conj, nrhs, hrs, ldu, Pl->ffmod && Pl->conj)));
   } else {
     SFT_DISPATCH(Pl->d, Pl->p,
                  (k_final<D, P, double2, Pow<P, D>::v><<<nb, 128, 0, Pl->stream>>>(
-                     Pl->X.pts_sorted, Pl->X.perm, Pl->X.leaf_of, (const double2*)h0, u, i_lo, i_hi, a_lo, Pl->N, Pl->conj, nrhs, hrs, ldu)));
+                     Pl->X.pts_sorted, Pl->X.perm, Pl->X.leaf_of, (const double2*)h0, u, i_lo, i_hi, a_lo, Pl->N, Pl->conj, nrhs, hrs, ldu, Pl->ffmod && Pl->conj)));
   }
   count_launch();
   return cudaGetLastError();

@@ -78,6 +78,7 @@ struct sft_plan_s {
   int rank = 0, world = 1;
   int prec = 0;  // 0 = FP64 charges (complex128), 1 = FP32 charges (complex64)
   int conj = 0;  // adjoint plan: conjugate the charges on input and the potentials on output
+  int ffmod = 0; // far-field plan (sft_farfield_plan): source (forward) / target (adjoint) modulation e^{-+i pi sum k}
   int pds = 0;   // stride (complex elements) of one pair array in the level buffers
   cudaStream_t stream = nullptr;
   sft::Tree X, K;
@@ -171,6 +172,9 @@ cudaError_t check_schedule(const sft_plan_s* P, const LevelDims& L, const unsign
 cudaError_t launch_final(const sft_plan_s* P, const void* g0, double2* u, int64_t a_lo, int64_t i_lo, int64_t i_hi,
                          int nrhs = 1, int64_t hrs = 0, int64_t ldu = 0);
 cudaError_t launch_zero(double2* p, int64_t n, cudaStream_t s);
+// far-field adapter: x = N/2 - kappa xhat/(2 pi), k = N y (device arrays [n][d])
+cudaError_t launch_ff_coords(const double* xhat, int64_t nx, const double* y, int64_t ny, int d, double kappa,
+                             int64_t N, double* x, double* k, cudaStream_t s);
 
 template <int B, int E>
 struct Pow {
