@@ -2,6 +2,7 @@
 // multi-GPU phase calls.  Host orchestration only; every arithmetic step of
 // the transform runs in the kernels of tree.cu and kernels.cu.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -363,10 +364,42 @@ static void plan_free(sft_plan_s* P) {
   delete P;
 }
 
+// SFT_PLAN_TRACE=1: host timestamps (us since entry) of sft_plan's milestones on stderr
+struct PlanTrace {
+  bool on = false;
+  std::chrono::steady_clock::time_point t0;
+  char buf[512];
+  int n = 0;
+  PlanTrace() {
+    const char* e = getenv("SFT_PLAN_TRACE");
+    on = e && e[0] == '1';
+    t0 = std::chrono::steady_clock::now();
+  }
+  void mark(const char* what) {
+    if (!on || n > 440) return;
+    const double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+    n += snprintf(buf + n, sizeof(buf) - n, " %s=%.1f", what, us);
+  }
+  ~PlanTrace() {
+    if (on) fprintf(stderr, "[sft_plan]%s\n", buf);
+  }
+};
+static PlanTrace* g_trace = nullptr;
+namespace sft {
+void trace_mark(const char* what) {
+  if (g_trace) g_trace->mark(what);
+}
+}  // namespace sft
+
 static int supported_p(int d, int p) { return (d == 2 || d == 3) && (p == 5 || p == 7 || p == 9); }
 
 extern "C" int sft_plan(int dim, int64_t N, int p, const double* x, int64_t nx, const double* k, int64_t nk,
                         const sft_opts* opts, sft_plan_t* out) {
+  PlanTrace trace;
+  g_trace = trace.on ? &trace : nullptr;
+  struct Untrace {
+    ~Untrace() { g_trace = nullptr; }
+  } untrace;
   if (!out) return fail(SFT_E_ARG, "out is NULL");
   if (dim != 2 && dim != 3) return fail(SFT_E_ARG, "dim must be 2 or 3");
   if (N < 2 || N > (1 << 20) || (N & (N - 1))) return fail(SFT_E_ARG, "N must be a power of two in [2, 2^20]");
@@ -454,7 +487,9 @@ extern "C" int sft_plan(int dim, int64_t N, int p, const double* x, int64_t nx, 
     cudaMemcpyAsync(ks, k, nk * dim * sizeof(double), cudaMemcpyHostToDevice, s);
     kd = ks;
   }
+  trace_mark("pre_tree");
   int rc = build_trees(P, xd, kd, &err);
+  trace_mark("trees");
   if (xs) cudaFreeAsync(xs, s);
   if (ks) cudaFreeAsync(ks, s);
   if (rc) return bail(rc, err);
@@ -549,6 +584,7 @@ extern "C" int sft_plan(int dim, int64_t N, int p, const double* x, int64_t nx, 
     if (cudaMallocAsync(&P->buf[i], P->buf_elems * (P->prec == 1 ? sizeof(float2) : sizeof(double2)), s) !=
         cudaSuccess)
       return bail(SFT_E_NOMEM, "level buffer allocation failed");
+  trace_mark("bufs");
   // tile schedules of every translation level (kernel-side task lists)
   {
     P->sched_off.assign(L + 1, 0);
@@ -595,6 +631,7 @@ extern "C" int sft_plan(int dim, int64_t N, int p, const double* x, int64_t nx, 
       }
     }
   }
+  trace_mark("sched");
   // no sync here: the schedule kernel runs behind the caller's next launches;
   // the plan's device time is read lazily (sft_plan_stats)
   cudaEventRecord(e1, s);

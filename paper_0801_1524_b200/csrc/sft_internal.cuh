@@ -196,6 +196,9 @@ struct Pow<B, 0> {
     else return cudaErrorInvalidValue;                                   \
   } while (0)
 
+// SFT_PLAN_TRACE=1: host-time milestones of sft_plan (api.cu)
+void trace_mark(const char* what);
+
 // number of kernels this library has launched (own kernels; CUB's internal
 // sort/scan kernels are not counted), for bench.py's gpu_launches
 void count_launch(int n = 1);

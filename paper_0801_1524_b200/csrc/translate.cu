@@ -1012,7 +1012,7 @@ __device__ __forceinline__ void load_lane_ops(LaneOps<P, TS>& op, const double* 
 // per tile arms full[s] with the byte count, bulk-copies the tile's schedule
 // block into blk[s] and every present child array into stage s (reading the
 // group records of its next tile from HBM while it waits for a free stage).
-template <int D, int P, int G, int NST, typename E = double2, int PS = Pow<P, D>::v>
+template <int D, int P, int G, int NST, typename E = double2, int PS = Pow<P, D>::v, bool BATCH = false>
 __device__ __forceinline__ void ws_producer(const TransArgs& a, const unsigned char* __restrict__ sched, int64_t ntiles,
                                             E* ring, unsigned char (*blk)[Sched<D, P, G>::BLK], uint64_t* full,
                                             uint64_t* empty) {
@@ -1024,10 +1024,11 @@ __device__ __forceinline__ void ws_producer(const TransArgs& a, const unsigned c
     INSTR_T0(tp0);
     int s = 0;
     uint32_t ph = 0;
-    // work items w = tile * nrhs + r (nrhs = 1: w = tile)
-    const int64_t nwork = ntiles * a.nrhs;
+    // work items w = tile * nrhs + r (BATCH = false: nrhs = 1, w = tile)
+    const int64_t nr = BATCH ? a.nrhs : 1;
+    const int64_t nwork = ntiles * nr;
     int64_t w = blockIdx.x;
-    int64_t tile = a.nrhs == 1 ? w : w / a.nrhs;
+    int64_t tile = BATCH ? w / nr : w;
     uint2 gr = (w < nwork && lane < G) ? __ldg(reinterpret_cast<const uint2*>(sched + tile * SC::BLK + SC::HDR) + lane)
                                        : make_uint2(0u, 0u);
     // programmatic dependent launch: everything above (schedule reads, barrier
@@ -1037,11 +1038,11 @@ __device__ __forceinline__ void ws_producer(const TransArgs& a, const unsigned c
     asm volatile("griddepcontrol.wait;" ::: "memory");
     for (int i = 0; w < nwork; ++i) {
       const int64_t wn = w + gridDim.x;
-      const int64_t next = a.nrhs == 1 ? wn : wn / a.nrhs;
+      const int64_t next = BATCH ? wn / nr : wn;
       const uint2 gn = (wn < nwork && lane < G)
                            ? __ldg(reinterpret_cast<const uint2*>(sched + next * SC::BLK + SC::HDR) + lane)
                            : make_uint2(0u, 0u);
-      const E* const ain = reinterpret_cast<const E*>(a.in) + (w - tile * a.nrhs) * a.rs;
+      const E* const ain = reinterpret_cast<const E*>(a.in) + (BATCH ? (w - tile * nr) * a.rs : (int64_t)0);
       INSTR_T0(tw0);
       if (i >= NST) mbar_wait_sleep(smem_u32(&empty[s]), ph ^ 1u);
       INSTR_ADD(1, tw0);
@@ -1116,7 +1117,8 @@ __device__ __forceinline__ void ws_producer(const TransArgs& a, const unsigned c
 // 2D with NST >= 3: skewed pipeline, pass 1 of tile i+1 runs before pass 0 of
 // tile i, and pass 0 waits on an mbarrier (p1done) every consumer thread
 // arrives on after its pass-1 rows, so warps do not idle at a pass barrier.
-template <int D, int P, int G, int NC, int NST, int MINB, typename E = double2, bool FUSED = false>
+template <int D, int P, int G, int NC, int NST, int MINB, typename E = double2, bool FUSED = false,
+          bool BATCH = false>
 __global__ __launch_bounds__((NC + 1) * 32, MINB) void k_translate_ws(TransArgs a, const double* __restrict__ frag,
                                                                              const unsigned char* __restrict__ sched,
                                                                              int64_t ntiles) {
@@ -1138,7 +1140,7 @@ __global__ __launch_bounds__((NC + 1) * 32, MINB) void k_translate_ws(TransArgs 
   fill_tail_smem<D, P>(frag);
   __syncthreads();
   if (warp == NC) {
-    ws_producer<D, P, G, NST, E, PD>(a, sched, ntiles, ring, blk, full, empty);
+    ws_producer<D, P, G, NST, E, PD, BATCH>(a, sched, ntiles, ring, blk, full, empty);
     return;
   }
   // ---------------- consumers ----------------
@@ -1158,8 +1160,8 @@ __global__ __launch_bounds__((NC + 1) * 32, MINB) void k_translate_ws(TransArgs 
     if constexpr (D == 2) consumer_pass<D, P, G, NC, D - 1, true, 3, E, FUSED>(a, sb_, bk, op, rot, oo);
   };
   // work items w = tile * nrhs + r; the output of RHS r goes to out + r * rs
-  const int64_t nwork = ntiles * a.nrhs;
-  auto ooff = [&](int64_t w_) { return a.nrhs == 1 ? (int64_t)0 : (w_ % a.nrhs) * a.rs; };
+  const int64_t nwork = BATCH ? ntiles * a.nrhs : ntiles;
+  auto ooff = [&](int64_t w_) { return BATCH ? (w_ % a.nrhs) * a.rs : (int64_t)0; };
   if constexpr (D == 2 && NST >= 3) {
     int64_t tile = blockIdx.x;
     if (tile < nwork) {
@@ -1737,8 +1739,20 @@ static cudaError_t launch_translate_t(const sft_plan_s* Pl, const LevelDims& L, 
     if (!L.sched) return cudaErrorInvalidValue;
     const int64_t ntiles = (a.ngroups + G - 1) / G;
     const int64_t grid = std::min<int64_t>(ntiles * a.nrhs, grid_max);
-    launch_pdl(k_translate_ws<D, P, G, NC, NST, MB, float2>, (unsigned)grid, (NC + 1) * 32, smem, Pl->stream, a, frag,
-               L.sched, ntiles);
+    if (a.nrhs > 1) {
+      static bool battr = false;
+      if (!battr) {
+        cudaError_t e = cudaFuncSetAttribute(k_translate_ws<D, P, G, NC, NST, MB, float2, false, true>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        battr = true;
+      }
+      launch_pdl(k_translate_ws<D, P, G, NC, NST, MB, float2, false, true>, (unsigned)grid, (NC + 1) * 32, smem,
+                 Pl->stream, a, frag, L.sched, ntiles);
+    } else {
+      launch_pdl(k_translate_ws<D, P, G, NC, NST, MB, float2>, (unsigned)grid, (NC + 1) * 32, smem, Pl->stream, a,
+                 frag, L.sched, ntiles);
+    }
   } else if (Pl->prec == 1) {
     constexpr int G = F32Cfg<D, P>::G, NC = F32Cfg<D, P>::NC, NST = F32Cfg<D, P>::NST, MB = F32Cfg<D, P>::MINB;
     const size_t smem = (size_t)NST * G * (1 << D) * F32<D, P>::PS * sizeof(float2);
@@ -1775,6 +1789,16 @@ static cudaError_t launch_translate_t(const sft_plan_s* Pl, const LevelDims& L, 
         fattr = true;
       }
       launch_pdl(k_translate_ws<D, P, G, NC, NST, MB, double2, true>, (unsigned)grid, (NC + 1) * 32, smem,
+                 Pl->stream, a, frag, L.sched, ntiles);
+    } else if (a.nrhs > 1) {
+      static bool battr = false;
+      if (!battr) {
+        cudaError_t e = cudaFuncSetAttribute(k_translate_ws<D, P, G, NC, NST, MB, double2, false, true>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        battr = true;
+      }
+      launch_pdl(k_translate_ws<D, P, G, NC, NST, MB, double2, false, true>, (unsigned)grid, (NC + 1) * 32, smem,
                  Pl->stream, a, frag, L.sched, ntiles);
     } else {
       launch_pdl(k_translate_ws<D, P, G, NC, NST, MB>, (unsigned)grid, (NC + 1) * 32, smem, Pl->stream, a, frag,

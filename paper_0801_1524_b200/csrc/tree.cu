@@ -338,6 +338,7 @@ int build_trees(sft_plan_s* P, const double* x_dev, const double* k_dev, std::st
   P->X.arena = arena;
   P->K.arena = nullptr;
   CK(cudaMemsetAsync(arena + cm_lo, 0, cm_hi - cm_lo, s));
+  trace_mark("arena");
 
   // ---- sort + fill (32-bit point keys when d*L+1 <= 32) ----
   char* scr = nullptr;
@@ -349,6 +350,7 @@ int build_trees(sft_plan_s* P, const double* x_dev, const double* k_dev, std::st
                                          o_pts, o_tot, src, &scr, fa, err);
   if (rc) return rc;
 
+  trace_mark("enq");
   // ---- the one host sync: exact box counts + domain error flag ----
   std::vector<int64_t> h(2 * (L + 1));
   CK(cudaMemcpyAsync(h.data(), arena + o_tot[0], (L + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
@@ -357,6 +359,7 @@ int build_trees(sft_plan_s* P, const double* x_dev, const double* k_dev, std::st
   CK(cudaMemcpyAsync(&herr, P->d_err, sizeof(int), cudaMemcpyDeviceToHost, s));
   CK(cudaFreeAsync(scr, s));
   CK(cudaStreamSynchronize(s));
+  trace_mark("sync");
   if (herr) {
     if (err) *err = "a coordinate is non-finite or outside [0,N]";
     return SFT_E_DOMAIN;
