@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <new>
 #include <string>
 #include <vector>
@@ -340,26 +341,50 @@ static LevelDims apply_dims_sched(const sft_plan_s* P, int t) {
 // ---------------------------------------------------------------------------
 // plan
 // ---------------------------------------------------------------------------
+// Event pool: plans are created and destroyed per step in the bench (and in
+// serving loops); cudaEventCreate/Destroy cost several microseconds of host
+// time each, on the plan's critical path.  Events are recycled instead (a
+// re-recorded event is safe: stream waits capture the event's state at the
+// time of the wait call).
+static std::mutex g_ev_mu;
+static std::vector<cudaEvent_t> g_ev_pool[2];  // [0] timing, [1] cudaEventDisableTiming
+static cudaEvent_t ev_get(bool timing) {
+  {
+    std::lock_guard<std::mutex> lk(g_ev_mu);
+    auto& v = g_ev_pool[timing ? 0 : 1];
+    if (!v.empty()) {
+      cudaEvent_t e = v.back();
+      v.pop_back();
+      return e;
+    }
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreateWithFlags(&e, timing ? cudaEventDefault : cudaEventDisableTiming);
+  return e;
+}
+static void ev_put(cudaEvent_t e, bool timing) {
+  if (!e) return;
+  std::lock_guard<std::mutex> lk(g_ev_mu);
+  g_ev_pool[timing ? 0 : 1].push_back(e);
+}
+
 static void plan_free(sft_plan_s* P) {
   if (!P) return;
   cudaStream_t s = P->stream;
   if (P->sched_ready) cudaStreamWaitEvent(s, P->sched_ready, 0);
   free_tree(P->X, s);
   free_tree(P->K, s);
-  for (int i = 0; i < 2; ++i) {
-    if (P->buf[i]) cudaFreeAsync(P->buf[i], s);
+  if (P->buf[0]) cudaFreeAsync(P->buf[0], s);  // one block: both level buffers (+ schedules)
+  for (int i = 0; i < 2; ++i)
     if (P->bufb[i]) cudaFreeAsync(P->bufb[i], s);
-  }
   if (P->f_stage) cudaFreeAsync(P->f_stage, s);
   if (P->u_stage) cudaFreeAsync(P->u_stage, s);
   if (P->d_err) cudaFreeAsync(P->d_err, s);
   if (P->d_seg) cudaFreeAsync(P->d_seg, s);
-  if (P->sched) cudaFreeAsync(P->sched, s);
   for (int i = 0; i < P->ev_created; ++i) cudaEventDestroy(P->ev[i]);
-  for (int i = 0; i < 2; ++i)
-    if (P->plan_ev[i]) cudaEventDestroy(P->plan_ev[i]);
-  if (P->sched_fork) cudaEventDestroy(P->sched_fork);
-  if (P->sched_ready) cudaEventDestroy(P->sched_ready);
+  for (int i = 0; i < 2; ++i) ev_put(P->plan_ev[i], true);
+  ev_put(P->sched_fork, false);
+  ev_put(P->sched_ready, false);
   // no sync: the frees above are stream-ordered behind any pending work
   delete P;
 }
@@ -457,14 +482,21 @@ extern "C" int sft_plan(int dim, int64_t N, int p, const double* x, int64_t nx, 
     delete P;
     return fail(SFT_E_CUDA, err);
   }
-  cudaEvent_t e0, e1;
-  cudaEventCreate(&e0);
-  cudaEventCreate(&e1);
+  cudaEvent_t e0 = ev_get(true), e1 = ev_get(true);
   cudaEventRecord(e0, s);
+  // taken now (host time overlaps the tree build), used after the counts sync
+  P->sched_fork = ev_get(false);
+  P->sched_ready = ev_get(false);
+  bool sched_recorded = false;
   auto bail = [&](int code, const std::string& m) {
     if (!P->plan_ev[0]) {
-      cudaEventDestroy(e0);
-      cudaEventDestroy(e1);
+      ev_put(e0, true);
+      ev_put(e1, true);
+    }
+    if (!sched_recorded) {  // plan_free waits on sched_ready: never on an unrecorded pooled event
+      ev_put(P->sched_fork, false);
+      ev_put(P->sched_ready, false);
+      P->sched_fork = P->sched_ready = nullptr;
     }
     plan_free(P);
     return fail(code, m);
@@ -580,12 +612,7 @@ extern "C" int sft_plan(int dim, int64_t N, int p, const double* x, int64_t nx, 
       P->x_rng[l].hi = P->X.counts[l];
     }
   }
-  for (int i = 0; i < 2; ++i)
-    if (cudaMallocAsync(&P->buf[i], P->buf_elems * (P->prec == 1 ? sizeof(float2) : sizeof(double2)), s) !=
-        cudaSuccess)
-      return bail(SFT_E_NOMEM, "level buffer allocation failed");
-  trace_mark("bufs");
-  // tile schedules of every translation level (kernel-side task lists)
+  // one allocation: level buffer 0 | level buffer 1 | tile schedules of every level
   {
     P->sched_off.assign(L + 1, 0);
     size_t tot = 0;
@@ -594,8 +621,15 @@ extern "C" int sft_plan(int dim, int64_t N, int p, const double* x, int64_t nx, 
       tot += (schedule_bytes(P, apply_dims(P, t)) + 255) / 256 * 256;
     }
     P->sched_off[L] = tot;
+    const size_t bb = (P->buf_elems * (P->prec == 1 ? sizeof(float2) : sizeof(double2)) + 255) / 256 * 256;
+    char* blk = nullptr;
+    if (cudaMallocAsync((void**)&blk, 2 * bb + tot, s) != cudaSuccess)
+      return bail(SFT_E_NOMEM, "level buffer allocation failed");
+    P->buf[0] = (double2*)blk;
+    P->buf[1] = (double2*)(blk + bb);
+    P->sched = tot > 0 ? (unsigned char*)(blk + 2 * bb) : nullptr;
+    trace_mark("bufs");
     if (tot > 0) {
-      if (cudaMallocAsync(&P->sched, tot, s) != cudaSuccess) return bail(SFT_E_NOMEM, "schedule allocation failed");
       std::vector<LevelDims> dims(L);
       std::vector<unsigned char*> dst(L);
       for (int t = 0; t < L; ++t) {
@@ -606,13 +640,12 @@ extern "C" int sft_plan(int dim, int64_t N, int p, const double* x, int64_t nx, 
       // first kernels of the apply (the leaf kernel needs only the trees);
       // the first translation waits on sched_ready
       cudaStream_t side = side_stream();
-      cudaEventCreateWithFlags(&P->sched_fork, cudaEventDisableTiming);
-      cudaEventCreateWithFlags(&P->sched_ready, cudaEventDisableTiming);
       cudaEventRecord(P->sched_fork, s);
       cudaStreamWaitEvent(side, P->sched_fork, 0);
       cudaError_t ce = launch_schedule(P, dims.data(), L, dst.data(), side);
-      if (ce != cudaSuccess) return bail(SFT_E_CUDA, std::string("schedule: ") + cudaGetErrorString(ce));
       cudaEventRecord(P->sched_ready, side);
+      sched_recorded = true;
+      if (ce != cudaSuccess) return bail(SFT_E_CUDA, std::string("schedule: ") + cudaGetErrorString(ce));
       const char* chk = getenv("SFT_CHECK_SCHED");
       if (chk && chk[0] == '1') {
         cudaStreamWaitEvent(s, P->sched_ready, 0);
@@ -630,6 +663,12 @@ extern "C" int sft_plan(int dim, int64_t N, int p, const double* x, int64_t nx, 
         if (herr & 4) return bail(SFT_E_CUDA, "tile schedule failed its invariants");
       }
     }
+  }
+  if (!sched_recorded) {  // no schedule kernel (no translation groups / non-ws kernel)
+    ev_put(P->sched_fork, false);
+    ev_put(P->sched_ready, false);
+    P->sched_fork = P->sched_ready = nullptr;
+    sched_recorded = true;
   }
   trace_mark("sched");
   // no sync here: the schedule kernel runs behind the caller's next launches;

@@ -133,7 +133,9 @@ cudaError_t upload_const_tables(int p, const double* RC, const double* RS, const
 // ------------------------------------------------------------------------
 // shared pieces: arguments, group metadata, TMA tile prologue, task lists
 // ------------------------------------------------------------------------
-struct TransArgs {
+// Per-level layout arguments (everything the schedule builder needs); the
+// translation kernels' TransArgs adds the exchange and batch fields.
+struct LevelArgs {
   const double2* in;
   double2* out;
   const int32_t* cbK;
@@ -145,6 +147,9 @@ struct TransArgs {
   int64_t out_b0, out_nA, out_a0;
   const int64_t* seg;  // [nseg+1] A boundaries at the output level, then [nseg] segment bases
   int nseg;
+};
+
+struct TransArgs : LevelArgs {
   // fused exchange (multi-GPU, exchange level): the output pair with send-layout
   // index i in segment q is stored at peer[q] + peer_off[q] + (i - peer_seg[q]) * p^d
   // (the receiving rank's buffer, mapped into this process), i.e. the
@@ -301,7 +306,7 @@ __device__ __forceinline__ TaskEntry task_at(const TaskEntry* ent, int ei, int n
 
 // Index of the output pair (child alpha of A', B) in the level output for
 // the last pass, -1 if A' has no such child.
-__device__ __forceinline__ int64_t out_pair(const TransArgs& a, const GroupMeta& g, int alpha) {
+__device__ __forceinline__ int64_t out_pair(const LevelArgs& a, const GroupMeta& g, int alpha) {
   if (!(g.mA >> alpha & 1)) return -1;
   const int64_t iA = (int64_t)g.cbX + __popc(g.mA & ((1u << alpha) - 1));
   if (a.nseg == 0) return (g.iB - a.out_b0) * a.out_nA + (iA - a.out_a0);
@@ -313,7 +318,7 @@ __device__ __forceinline__ int64_t out_pair(const TransArgs& a, const GroupMeta&
 
 // HBM address of the output pair (child alpha of A', B) for the last pass
 template <int PD>
-__device__ __forceinline__ double2* out_array(const TransArgs& a, const GroupMeta& g, int alpha) {
+__device__ __forceinline__ double2* out_array(const LevelArgs& a, const GroupMeta& g, int alpha) {
   if (!(g.mA >> alpha & 1)) return nullptr;
   const int64_t iA = (int64_t)g.cbX + __popc(g.mA & ((1u << alpha) - 1));
   int64_t pidx;
@@ -578,7 +583,7 @@ struct Sched {
 // Pass over axis 0 first: tasks by beta_1 (slots (0,b1), (1,b1)); then axis 1
 // (last): tasks by alpha_0 (slots (a0,0), (a0,1)), outputs (a0,0), (a0,1).
 template <int D, int P, int G, int PS, int AX, bool LAST, bool REV = false>
-__device__ __forceinline__ void schedule_pass(const TransArgs& a, const GroupMeta& m, bool valid, bool write_cnt,
+__device__ __forceinline__ void schedule_pass(const LevelArgs& a, const GroupMeta& m, bool valid, bool write_cnt,
                                               int* cnt, TaskRec* out) {
   constexpr int PD = PS;  // offsets in units of the array stride
   constexpr int NS = 1 << D;
@@ -680,11 +685,12 @@ __device__ __forceinline__ void schedule_pass(const TransArgs& a, const GroupMet
 // All levels of a plan in one launch: level lv owns the global tiles
 // [tile0[lv], tile0[lv+1]) and writes its blocks at dst[lv].
 struct SchedLevels {
-  TransArgs a[kMaxLevels];
+  LevelArgs a[kMaxLevels];  // (slim: the whole struct is one < 4 KB kernel parameter)
   unsigned char* dst[kMaxLevels];
   int64_t tile0[kMaxLevels + 1];
   int nlev;
 };
+static_assert(sizeof(SchedLevels) <= 4096, "k_schedule's parameter must stay within 4 KB");
 
 template <int D, int P, int G, int PS>
 __global__ __launch_bounds__(128) void k_schedule(const __grid_constant__ SchedLevels S) {
@@ -697,7 +703,7 @@ __global__ __launch_bounds__(128) void k_schedule(const __grid_constant__ SchedL
   if (T - lane / G >= S.tile0[S.nlev]) return;  // whole warp out of range
   int lv = 0;
   while (lv + 1 < S.nlev && T >= S.tile0[lv + 1]) ++lv;
-  const TransArgs& a = S.a[lv];
+  const LevelArgs& a = S.a[lv];
   const int64_t tile = T - S.tile0[lv];
   const bool tv = T < S.tile0[S.nlev];
   unsigned char* b = S.dst[lv] + (tv ? tile : 0) * SC::BLK;
