@@ -33,6 +33,14 @@ def test_library_rejects_bad_args_without_gpu():
     assert L.sft_plan(2, 64, 5, x.ctypes.data, 0, x.ctypes.data, 4, None, ctypes.byref(h)) == 1
     assert L.sft_destroy(None) == 0
     assert L.sft_apply(None, None, None) == 1
+    # multi-RHS and far-field entry points validate before any device work
+    assert L.sft_apply_batch(None, 2, None, 4, None, 4) == 1
+    xh = np.array([[1.0, 0.0], [0.0, 1.0]])
+    assert L.sft_farfield_plan(2, -1.0, 9, xh.ctypes.data, 2, x.ctypes.data, 4, None, ctypes.byref(h)) == 1
+    assert L.sft_farfield_plan(2, float("nan"), 9, xh.ctypes.data, 2, x.ctypes.data, 4, None, ctypes.byref(h)) == 1
+    assert L.sft_farfield_plan(4, 10.0, 9, xh.ctypes.data, 2, x.ctypes.data, 4, None, ctypes.byref(h)) == 1
+    assert L.sft_farfield_plan(2, 10.0, 9, None, 2, x.ctypes.data, 4, None, ctypes.byref(h)) == 1
+    assert L.sft_farfield_plan(2, 10.0, 9, xh.ctypes.data, 0, x.ctypes.data, 4, None, ctypes.byref(h)) == 1
 
 
 # ------------------------------------------------------------- operator tables
