@@ -34,6 +34,7 @@
 // No floating-point atomics: bitwise reproducible, identical for any world
 // size.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -336,21 +337,35 @@ __device__ __forceinline__ double2* out_array(const LevelArgs& a, const GroupMet
 // ------------------------------------------------------------------------
 // DMMA kernel
 // ------------------------------------------------------------------------
+// Child-grid structure: a child box has half the width and the
+// same p nodes, so its even nodes l' = 2i coincide with parent nodes
+// (s (p-1) = (beta (p-1) + l')/2 is an integer) and the Lagrange basis is a
+// delta there: column l' of RC_beta / RS_beta is zero except at row
+// m = (beta (p-1) + l')/2.  Only the H = (p-1)/2 odd columns per child are
+// dense.  The tensor cores take K = 2H stacked odd elements (k = beta H + i,
+// l' = 2i + 1); the even (delta) columns are added to the accumulators up
+// front with two scalar coefficients per output (DFMA).  p = 9: 2 k-steps
+// instead of 5 (K 20 -> 8).
 template <int P>
 struct MmaShape {
-  static constexpr int K = 2 * P;                 // stacked child elements
+  static constexpr int H = (P - 1) / 2;           // dense (odd) columns per child
+  static constexpr int K = 2 * H;                 // stacked odd child elements
   static constexpr int NK = (K + 3) / 4;          // k-steps of 4
-#ifdef SFT_TAIL_DMMA
-  static constexpr bool TAIL = false;             // m = P-1 in a third N tile on the tensor cores
-#else
   static constexpr bool TAIL = (P % 4) == 1;      // m = P-1 by DFMA
-#endif
   static constexpr int NM = TAIL ? P - 1 : P;     // m's on the tensor cores
   static constexpr int NT = (2 * NM + 7) / 8;     // N tiles of 8 (P_m, Q_m interleaved)
-  static constexpr int K0_HI = (P + 3) / 4;       // k-steps [0, K0_HI) hold child-0 elements
-  static constexpr int K1_LO = P / 4;             // k-steps [K1_LO, NK) hold child-1 elements
-  static constexpr int NFRAG = NK * NT * 32 + (TAIL ? NK * 2 * 32 : 0);  // doubles in the table
+  static constexpr int K0_HI = (H + 3) / 4;       // k-steps [0, K0_HI) hold child-0 elements
+  static constexpr int K1_LO = H / 4;             // k-steps [K1_LO, NK) hold child-1 elements
+  // fragment table: B fragments, tail weights, then the delta coefficients
+  // (a0, b0, a1, b1) of m = 4n + lane%4 per N tile and (a1, b1) of the tail
+  static constexpr int OFF_TAIL = NK * NT * 32;
+  static constexpr int OFF_DELTA = OFF_TAIL + (TAIL ? NK * 2 * 32 : 0);
+  static constexpr int OFF_DTAIL = OFF_DELTA + NT * 4 * 32;
+  static constexpr int NFRAG = OFF_DTAIL + (TAIL ? 2 * 32 : 0);
 };
+#ifdef SFT_NO_ZEROFILL
+#error "the delta columns read absent children's slots: SFT_NO_ZEROFILL is not supported"
+#endif
 
 // complex element of the level buffers / stages: double2 (FP64) or float2
 // (FP32 storage variant; the arithmetic stays FP64 on the tensor cores)
@@ -375,13 +390,6 @@ struct StrideT {
   static constexpr int v = sizeof(E) == 8 ? PD + (PD & 1) : PD;
 };
 
-// first k-step: D = A*B (C = 0)
-__device__ __forceinline__ void dmma0(double (&d)[2], double a, double b) {
-  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%4,%4};"
-      : "=d"(d[0]), "=d"(d[1])
-      : "d"(a), "d"(b), "d"(0.0));
-}
-
 __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
       : "+d"(d[0]), "+d"(d[1])
@@ -405,16 +413,18 @@ __shared__ double2 s_tail[8][4];
 template <int P, bool TS>
 struct LaneOps {
   using S = MmaShape<P>;
-  double fb[S::NK][S::NT];           // B fragments of the operator
+  double fb[S::NK][S::NT];           // B fragments of the operator (odd columns)
   double ft[TS ? 1 : S::NK][2];      // tail column (m = P-1): P and Q weights of this lane's k
+  double dl[S::NT][4];               // delta columns of m = 4n + lane%4: (a0, b0, a1, b1)
+  double dt[S::TAIL ? 2 : 1];        // delta column of the tail (lane%4 == 0 only, else 0)
   // child (0, 1; 2 = padding) and element index of this lane's k in k-step kk
   __device__ __forceinline__ static int bk(int kk, int lane) {
     const int k = 4 * kk + (lane & 3);
-    return k < 2 * P ? k / P : 2;
+    return k < S::K ? k / S::H : 2;
   }
   __device__ __forceinline__ static int lk(int kk, int lane) {
     const int k = 4 * kk + (lane & 3);
-    return k < 2 * P ? k % P : 0;
+    return k < S::K ? 2 * (k % S::H) + 1 : 0;
   }
   __device__ __forceinline__ double2 tail(int kk, int lane) const {
     if constexpr (TS) return s_tail[kk][lane & 3];
@@ -436,43 +446,26 @@ __device__ __forceinline__ void mma_steps(const OPS& op, const E* const (&x)[NSU
     double2 av[NSUB];
 #pragma unroll
     for (int u = 0; u < NSUB; ++u) {
-#ifdef SFT_NO_ZEROFILL
-      const int b = OPS::bk(kk, threadIdx.x);
-      const bool live = b == 0 ? p0[u] : (b == 1 ? p1[u] : false);
-      av[u] = live ? ElemT<E>::ld(x[u][off[kk]]) : make_double2(0.0, 0.0);
-#else
       // absent children's slots are zero-filled by the producer and the B
       // rows of padding k are zero: no masking needed
       av[u] = ElemT<E>::ld(x[u][off[kk]]);
-#endif
     }
+    // the accumulators start from the delta columns (consumer_pass)
 #pragma unroll
     for (int n = 0; n < S::NT; ++n)
 #pragma unroll
       for (int u = 0; u < NSUB; ++u) {
-        if (kk == K_LO) {
-          dmma0(are[u][n], av[u].x, op.fb[kk][n]);
-          dmma0(aim[u][n], av[u].y, op.fb[kk][n]);
-        } else {
-          dmma(are[u][n], av[u].x, op.fb[kk][n]);
-          dmma(aim[u][n], av[u].y, op.fb[kk][n]);
-        }
+        dmma(are[u][n], av[u].x, op.fb[kk][n]);
+        dmma(aim[u][n], av[u].y, op.fb[kk][n]);
       }
     if (S::TAIL) {
       const double2 ft = op.tail(kk, threadIdx.x);
 #pragma unroll
       for (int u = 0; u < NSUB; ++u) {
-        if (kk == K_LO) {
-          tl[u][0] = av[u].x * ft.x;
-          tl[u][1] = av[u].x * ft.y;
-          tl[u][2] = av[u].y * ft.x;
-          tl[u][3] = av[u].y * ft.y;
-        } else {
-          tl[u][0] = fma(av[u].x, ft.x, tl[u][0]);
-          tl[u][1] = fma(av[u].x, ft.y, tl[u][1]);
-          tl[u][2] = fma(av[u].y, ft.x, tl[u][2]);
-          tl[u][3] = fma(av[u].y, ft.y, tl[u][3]);
-        }
+        tl[u][0] = fma(av[u].x, ft.x, tl[u][0]);
+        tl[u][1] = fma(av[u].x, ft.y, tl[u][1]);
+        tl[u][2] = fma(av[u].y, ft.x, tl[u][2]);
+        tl[u][3] = fma(av[u].y, ft.y, tl[u][3]);
       }
     }
   }
@@ -843,6 +836,15 @@ __device__ __forceinline__ void consumer_pass(const TransArgs& a, E* __restrict_
 #pragma unroll
   for (int kk = 0; kk < S::NK; ++kk)
     off[kk] = (LaneOps<P, true>::bk(kk, lane) == 1 ? (1 << SH) * PD : 0) + LaneOps<P, true>::lk(kk, lane) * STR;
+  // delta columns of this lane's outputs m = 4n + c: child-0 element 2m and
+  // child-1 element 2m - (P-1), clamped into range (their coefficient is 0 there)
+  int doff[S::NT][2];
+#pragma unroll
+  for (int n = 0; n < S::NT; ++n) {
+    const int m = 4 * n + c;
+    doff[n][0] = min(2 * m, P - 1) * STR;
+    doff[n][1] = (1 << SH) * PD + min(max(2 * m - (P - 1), 0), P - 1) * STR;  // in range: 0 * finite = 0
+  }
   // units of NSUB super-tiles go round-robin over the warps, continuing from
   // where the previous pass stopped (rot), so that the extra unit of a pass
   // whose count is not a multiple of NC does not always land on warp 0
@@ -903,9 +905,24 @@ __device__ __forceinline__ void consumer_pass(const TransArgs& a, E* __restrict_
     double are[NSUB][S::NT][2], aim[NSUB][S::NT][2], tl[NSUB][4];
 #pragma unroll
     for (int u = 0; u < NSUB; ++u) {
+      // accumulators start from the delta (even) columns of the operator
 #pragma unroll
-      for (int n = 0; n < S::NT; ++n) are[u][n][0] = are[u][n][1] = aim[u][n][0] = aim[u][n][1] = 0.0;
-      tl[u][0] = tl[u][1] = tl[u][2] = tl[u][3] = 0.0;
+      for (int n = 0; n < S::NT; ++n) {
+        const double2 x0 = ElemT<E>::ld(x[u][doff[n][0]]), x1 = ElemT<E>::ld(x[u][doff[n][1]]);
+        are[u][n][0] = fma(op.dl[n][2], x1.x, op.dl[n][0] * x0.x);
+        are[u][n][1] = fma(op.dl[n][3], x1.x, op.dl[n][1] * x0.x);
+        aim[u][n][0] = fma(op.dl[n][2], x1.y, op.dl[n][0] * x0.y);
+        aim[u][n][1] = fma(op.dl[n][3], x1.y, op.dl[n][1] * x0.y);
+      }
+      if (S::TAIL) {  // m = P-1: child-1 element P-1 only (coefficients non-zero on lane%4 == 0)
+        const double2 x1 = ElemT<E>::ld(x[u][(1 << SH) * PD + (P - 1) * STR]);
+        tl[u][0] = op.dt[0] * x1.x;
+        tl[u][1] = op.dt[S::TAIL ? 1 : 0] * x1.x;
+        tl[u][2] = op.dt[0] * x1.y;
+        tl[u][3] = op.dt[S::TAIL ? 1 : 0] * x1.y;
+      } else {
+        tl[u][0] = tl[u][1] = tl[u][2] = tl[u][3] = 0.0;
+      }
     }
 #ifdef SFT_ABL_NOCOMPUTE  // ablation: no tensor-core work, everything else unchanged
     if (false)
@@ -991,8 +1008,8 @@ __device__ __forceinline__ void fill_tail_smem(const double* __restrict__ frag) 
   if (TailSmem<D>::v && S::TAIL && threadIdx.x < 4) {
 #pragma unroll
     for (int kk = 0; kk < S::NK; ++kk)
-      s_tail[kk][threadIdx.x] = make_double2(frag[S::NK * S::NT * 32 + (kk * 2 + 0) * 32 + threadIdx.x],
-                                             frag[S::NK * S::NT * 32 + (kk * 2 + 1) * 32 + threadIdx.x]);
+      s_tail[kk][threadIdx.x] = make_double2(frag[S::OFF_TAIL + (kk * 2 + 0) * 32 + threadIdx.x],
+                                             frag[S::OFF_TAIL + (kk * 2 + 1) * 32 + threadIdx.x]);
   }
 }
 
@@ -1000,13 +1017,19 @@ template <int P, bool TS>
 __device__ __forceinline__ void load_lane_ops(LaneOps<P, TS>& op, const double* __restrict__ frag, int lane) {
   using S = MmaShape<P>;
 #pragma unroll
+  for (int n = 0; n < S::NT; ++n)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) op.dl[n][j] = frag[S::OFF_DELTA + (n * 4 + j) * 32 + lane];
+  op.dt[0] = S::TAIL ? frag[S::OFF_DTAIL + lane] : 0.0;
+  if (S::TAIL) op.dt[S::TAIL ? 1 : 0] = frag[S::OFF_DTAIL + 32 + lane];
+#pragma unroll
   for (int kk = 0; kk < S::NK; ++kk) {
 #pragma unroll
     for (int n = 0; n < S::NT; ++n) op.fb[kk][n] = frag[(kk * S::NT + n) * 32 + lane];
     if constexpr (!TS) {
       if (S::TAIL) {
-        op.ft[kk][0] = frag[S::NK * S::NT * 32 + (kk * 2 + 0) * 32 + lane];
-        op.ft[kk][1] = frag[S::NK * S::NT * 32 + (kk * 2 + 1) * 32 + lane];
+        op.ft[kk][0] = frag[S::OFF_TAIL + (kk * 2 + 0) * 32 + lane];
+        op.ft[kk][1] = frag[S::OFF_TAIL + (kk * 2 + 1) * 32 + lane];
       } else {
         op.ft[kk][0] = op.ft[kk][1] = 0.0;
       }
@@ -1404,11 +1427,15 @@ static std::vector<double> mma_fragments() {
   build_tables_host(P, V, invD, &RC, &RS);
   auto rc = [&](int b, int m, int l) { return RC[((size_t)b * P + m) * P + l]; };
   auto rs = [&](int b, int m, int l) { return RS[((size_t)b * P + m) * P + l]; };
-  auto bop = [&](int k, int m, int pq) -> double {
-    if (k >= 2 * P || m >= P) return 0.0;
-    const int b = k / P, l = k % P;
+  // full operator entry of stacked element (child b, element l) for output (m, P/Q)
+  auto opv = [&](int b, int l, int m, int pq) -> double {
     if (pq == 0) return b == 0 ? rc(0, m, l) : rs(1, m, l);
     return b == 0 ? rs(0, m, l) : -rc(1, m, l);
+  };
+  // tensor-core K index k -> (child k / H, odd element 2 (k % H) + 1)
+  auto bop = [&](int k, int m, int pq) -> double {
+    if (k >= S::K || m >= P) return 0.0;
+    return opv(k / S::H, 2 * (k % S::H) + 1, m, pq);
   };
   std::vector<double> fr(S::NFRAG, 0.0);
   for (int kk = 0; kk < S::NK; ++kk)
@@ -1422,7 +1449,33 @@ static std::vector<double> mma_fragments() {
     for (int kk = 0; kk < S::NK; ++kk)
       for (int pq = 0; pq < 2; ++pq)
         for (int lane = 0; lane < 32; ++lane)
-          fr[S::NK * S::NT * 32 + (kk * 2 + pq) * 32 + lane] = bop(4 * kk + (lane & 3), P - 1, pq);
+          fr[S::OFF_TAIL + (kk * 2 + pq) * 32 + lane] = bop(4 * kk + (lane & 3), P - 1, pq);
+  // delta (even) columns: output m takes child-0 element 2m and child-1 element
+  // 2m - (P-1) (when in range); every other even-column entry is exactly 0
+  for (int n = 0; n < S::NT; ++n)
+    for (int lane = 0; lane < 32; ++lane) {
+      const int m = 4 * n + (lane & 3);
+      const bool ok = m < S::NM;
+      const int l0 = 2 * m, l1 = 2 * m - (P - 1);
+      const bool v0 = ok && l0 <= P - 1, v1 = ok && l1 >= 0;
+      fr[S::OFF_DELTA + (n * 4 + 0) * 32 + lane] = v0 ? opv(0, l0, m, 0) : 0.0;
+      fr[S::OFF_DELTA + (n * 4 + 1) * 32 + lane] = v0 ? opv(0, l0, m, 1) : 0.0;
+      fr[S::OFF_DELTA + (n * 4 + 2) * 32 + lane] = v1 ? opv(1, l1, m, 0) : 0.0;
+      fr[S::OFF_DELTA + (n * 4 + 3) * 32 + lane] = v1 ? opv(1, l1, m, 1) : 0.0;
+    }
+  if (S::TAIL)
+    for (int lane = 0; lane < 32; ++lane) {
+      fr[S::OFF_DTAIL + lane] = (lane & 3) == 0 ? opv(1, P - 1, P - 1, 0) : 0.0;
+      fr[S::OFF_DTAIL + 32 + lane] = (lane & 3) == 0 ? opv(1, P - 1, P - 1, 1) : 0.0;
+    }
+  // the split is exact only if every even-column entry outside the delta is 0
+  for (int b = 0; b < 2; ++b)
+    for (int l = 0; l < P; l += 2)
+      for (int m = 0; m < P; ++m)
+        if (2 * m != b * (P - 1) + l && (rc(b, m, l) != 0.0 || rs(b, m, l) != 0.0)) {
+          fprintf(stderr, "sft: operator table is not delta-structured at (%d,%d,%d)\n", b, m, l);
+          abort();
+        }
   return fr;
 }
 
