@@ -1,0 +1,33 @@
+"""Build libsft variants (-D overrides of the translation kernel configs) into sweep_libs/."""
+import os
+import sys
+from concurrent.futures import ThreadPoolExecutor
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_0801_1524_b200 import build as b  # noqa: E402
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+VARIANTS = {
+    # name: list of -D flags
+}
+
+
+def parse(spec):
+    """'G29=8,NC29=8,MINB29=2' -> ['-DSFT_WS_G29=8', ...]; keys starting with NSUB map to SFT_NSUB*"""
+    out = []
+    for kv in spec.split(","):
+        k, v = kv.split("=")
+        out.append(f"-DSFT_{k}={v}" if k.startswith(("NSUB", "TAIL", "ROTATE")) else f"-DSFT_WS_{k}={v}")
+    return out
+
+
+if __name__ == "__main__":
+    os.makedirs(os.path.join(ROOT, "sweep_libs"), exist_ok=True)
+    specs = sys.argv[1:]
+    def one(spec):
+        name = "lib_" + spec.replace(",", "_").replace("=", "") + ".so"
+        b.build(extra=parse(spec), out=os.path.join(ROOT, "sweep_libs", name))
+        return name
+    with ThreadPoolExecutor(4) as ex:
+        for n in ex.map(one, specs):
+            print(n)
