@@ -379,7 +379,6 @@ static void plan_free(sft_plan_s* P) {
     if (P->bufb[i]) cudaFreeAsync(P->bufb[i], s);
   if (P->f_stage) cudaFreeAsync(P->f_stage, s);
   if (P->u_stage) cudaFreeAsync(P->u_stage, s);
-  if (P->d_err) cudaFreeAsync(P->d_err, s);
   if (P->d_seg) cudaFreeAsync(P->d_seg, s);
   for (int i = 0; i < P->ev_created; ++i) cudaEventDestroy(P->ev[i]);
   for (int i = 0; i < 2; ++i) ev_put(P->plan_ev[i], true);
@@ -389,30 +388,54 @@ static void plan_free(sft_plan_s* P) {
   delete P;
 }
 
-// SFT_PLAN_TRACE=1: host timestamps (us since entry) of sft_plan's milestones on stderr
+// SFT_PLAN_TRACE=1: host timestamps (us since entry) of sft_plan's milestones on
+// stderr; marks with dev = true also write the GPU's %globaltimer from a
+// one-thread kernel on the plan stream (device times relative to the first)
+__global__ void k_stamp(unsigned long long* out) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  *out = t;
+}
 struct PlanTrace {
   bool on = false;
   std::chrono::steady_clock::time_point t0;
-  char buf[512];
+  char buf[1024];
   int n = 0;
+  unsigned long long* d_ts = nullptr;
+  const char* evn[16];
+  int nev = 0;
   PlanTrace() {
     const char* e = getenv("SFT_PLAN_TRACE");
     on = e && e[0] == '1';
     t0 = std::chrono::steady_clock::now();
+    if (on) cudaMallocManaged(&d_ts, 16 * sizeof(unsigned long long));
   }
-  void mark(const char* what) {
-    if (!on || n > 440) return;
+  void mark(const char* what, cudaStream_t s, bool dev) {
+    if (!on || n > 900) return;
     const double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
     n += snprintf(buf + n, sizeof(buf) - n, " %s=%.1f", what, us);
+    if (dev && nev < 16 && d_ts) {
+      k_stamp<<<1, 1, 0, s>>>(d_ts + nev);
+      evn[nev++] = what;
+    }
   }
   ~PlanTrace() {
-    if (on) fprintf(stderr, "[sft_plan]%s\n", buf);
+    if (!on) return;
+    fprintf(stderr, "[sft_plan] host us:%s\n", buf);
+    if (nev) {
+      cudaDeviceSynchronize();
+      fprintf(stderr, "[sft_plan] device us:");
+      for (int i = 0; i < nev; ++i) fprintf(stderr, " %s=%.1f", evn[i], (d_ts[i] - d_ts[0]) * 1e-3);
+      fprintf(stderr, "\n");
+    }
+    cudaFree(d_ts);
+    cudaGetLastError();
   }
 };
 static PlanTrace* g_trace = nullptr;
 namespace sft {
-void trace_mark(const char* what) {
-  if (g_trace) g_trace->mark(what);
+void trace_mark(const char* what, cudaStream_t s, bool dev) {
+  if (g_trace) g_trace->mark(what, s, dev);
 }
 }  // namespace sft
 
@@ -501,8 +524,6 @@ extern "C" int sft_plan(int dim, int64_t N, int p, const double* x, int64_t nx, 
     plan_free(P);
     return fail(code, m);
   };
-  if (cudaMallocAsync(&P->d_err, sizeof(int), s) != cudaSuccess) return bail(SFT_E_NOMEM, "alloc");
-  cudaMemsetAsync(P->d_err, 0, sizeof(int), s);
 
   // stage host coordinates
   const double* xd = x;
@@ -519,9 +540,9 @@ extern "C" int sft_plan(int dim, int64_t N, int p, const double* x, int64_t nx, 
     cudaMemcpyAsync(ks, k, nk * dim * sizeof(double), cudaMemcpyHostToDevice, s);
     kd = ks;
   }
-  trace_mark("pre_tree");
+  trace_mark("pre_tree", s, true);
   int rc = build_trees(P, xd, kd, &err);
-  trace_mark("trees");
+  trace_mark("trees", s, true);
   if (xs) cudaFreeAsync(xs, s);
   if (ks) cudaFreeAsync(ks, s);
   if (rc) return bail(rc, err);

@@ -197,7 +197,7 @@ struct Pow<B, 0> {
   } while (0)
 
 // SFT_PLAN_TRACE=1: host-time milestones of sft_plan (api.cu)
-void trace_mark(const char* what);
+void trace_mark(const char* what, cudaStream_t s = nullptr, bool dev = false);  // dev: also a device event on s
 
 // number of kernels this library has launched (own kernels; CUB's internal
 // sort/scan kernels are not counted), for bench.py's gpu_launches
