@@ -188,6 +188,28 @@ __global__ __launch_bounds__(kBlk) void k_fill(const KT* __restrict__ key, const
 
 static inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
+// Per-thread cache of the tree-build scratch and of an instantiated CUDA graph
+// of the CUB radix sort for one (point count, key bits, key type): plans built
+// back to back with the same sizes replay the graph (a few us of host time
+// instead of ~50 us of CUB dispatch, during which the GPU idles).  The scratch
+// is only used before sft_plan's counts sync, so consecutive plans of one
+// thread never overlap on it.  SFT_SORT_GRAPH=0 disables (plain CUB call).
+struct SortCache {
+  int64_t n = -1;
+  int bits = -1, ksz = 0, nb = -1, L = -1, dev = -1;
+  char* scr = nullptr;
+  cudaGraphExec_t exec = nullptr;
+};
+static thread_local SortCache g_sort;
+static bool sort_graph_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SFT_SORT_GRAPH");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 #define CK(x)                                                            \
   do {                                                                   \
     cudaError_t e_ = (x);                                                \
@@ -216,9 +238,27 @@ static int sort_and_fill(sft_plan_s* P, const double* x_dev, const double* k_dev
   const int64_t nx = P->nx, nk = P->nk, n = nx + nk;
   // ---- scratch ----
   const int nbx = (int)nblk(nx, kBlk), nbk = (int)nblk(nk, kBlk);
-  size_t cub_bytes = 0;
-  CK(cub::DeviceRadixSort::SortPairs(nullptr, cub_bytes, (KT*)nullptr, (KT*)nullptr, (int32_t*)nullptr,
-                                     (int32_t*)nullptr, (int)n, 0, d * L + 1, s));
+  const int bits = d * L + 1;
+  SortCache& C = g_sort;
+  const bool use_graph = sort_graph_enabled() && n >= 32768;  // small sorts: one CUB single-tile kernel
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  const bool hit = use_graph && C.exec && C.n == n && C.bits == bits && C.ksz == (int)sizeof(KT) &&
+                   C.nb == nbx + nbk && C.L == L && C.dev == dev;
+  // graph path: X and K sorted as two parallel branches (disjoint halves of the
+  // key array, the tree bit is constant in each; each sort is latency-bound, so
+  // two half-size sorts side by side take ~60% of one full-size sort)
+  size_t cub_bytes = 0, cub_x = 0, cub_k = 0;
+  if (!hit && !use_graph)
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, cub_bytes, (KT*)nullptr, (KT*)nullptr, (int32_t*)nullptr,
+                                       (int32_t*)nullptr, (int)n, 0, bits, s));
+  if (use_graph) {
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, cub_x, (KT*)nullptr, (KT*)nullptr, (int32_t*)nullptr,
+                                       (int32_t*)nullptr, (int)nx, 0, bits - 1, s));
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, cub_k, (KT*)nullptr, (KT*)nullptr, (int32_t*)nullptr,
+                                       (int32_t*)nullptr, (int)nk, 0, bits - 1, s));
+    cub_bytes = align_up(cub_x, 256) + cub_k;
+  }
   size_t so = 0;
   const size_t s_kin = so;
   so = align_up(so + sizeof(KT) * n, 256);
@@ -235,7 +275,18 @@ static int sort_and_fill(sft_plan_s* P, const double* x_dev, const double* k_dev
   const size_t s_cub = so;
   so = align_up(so + cub_bytes, 256);
   char* scr = nullptr;
-  CK(cudaMallocAsync((void**)&scr, so, s));
+  if (hit) {
+    scr = C.scr;  // same sizes and offsets as when the graph was captured
+  } else if (use_graph) {
+    // (re)build the cached scratch and capture the sort into a graph
+    if (C.exec) cudaGraphExecDestroy(C.exec);
+    if (C.scr) cudaFree(C.scr);  // synchronises: nothing of the old scratch is in flight
+    C = SortCache();
+    CK(cudaMalloc((void**)&C.scr, so));
+    scr = C.scr;
+  } else {
+    CK(cudaMallocAsync((void**)&scr, so, s));
+  }
   trace_mark("scr", s, true);
   KT* keys_in = (KT*)(scr + s_kin);
   KT* keys_out = (KT*)(scr + s_kout);
@@ -248,8 +299,47 @@ static int sort_and_fill(sft_plan_s* P, const double* x_dev, const double* k_dev
   count_launch();
   CK(cudaGetLastError());
   trace_mark("keys", s, true);
-  CK(cub::DeviceRadixSort::SortPairs(scr + s_cub, cub_bytes, keys_in, keys_out, idx_in, idx_out, (int)n, 0, d * L + 1,
-                                     s));
+  if (!use_graph) {
+    CK(cub::DeviceRadixSort::SortPairs(scr + s_cub, cub_bytes, keys_in, keys_out, idx_in, idx_out, (int)n, 0, bits, s));
+  } else {
+    if (!hit) {
+      cudaStream_t cs = nullptr, cs2 = nullptr;
+      cudaEvent_t fork = nullptr, join = nullptr;
+      CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+      CK(cudaStreamCreateWithFlags(&cs2, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
+      CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+      cudaEventRecord(fork, cs);
+      cudaStreamWaitEvent(cs2, fork, 0);
+      const size_t ox = align_up(cub_x, 256);
+      cudaError_t ce = cub::DeviceRadixSort::SortPairs(scr + s_cub, cub_x, keys_in, keys_out, idx_in, idx_out,
+                                                       (int)nx, 0, bits - 1, cs);
+      cudaError_t ce3 = cub::DeviceRadixSort::SortPairs(scr + s_cub + ox, cub_k, keys_in + nx, keys_out + nx,
+                                                        idx_in + nx, idx_out + nx, (int)nk, 0, bits - 1, cs2);
+      cudaEventRecord(join, cs2);
+      cudaStreamWaitEvent(cs, join, 0);
+      cudaGraph_t g = nullptr;
+      cudaError_t ce2 = cudaStreamEndCapture(cs, &g);
+      cudaStreamDestroy(cs);
+      cudaStreamDestroy(cs2);
+      cudaEventDestroy(fork);
+      cudaEventDestroy(join);
+      CK(ce);
+      CK(ce3);
+      CK(ce2);
+      ce = cudaGraphInstantiate(&C.exec, g, 0);
+      cudaGraphDestroy(g);
+      CK(ce);
+      C.n = n;
+      C.bits = bits;
+      C.ksz = (int)sizeof(KT);
+      C.nb = nbx + nbk;
+      C.L = L;
+      C.dev = dev;
+    }
+    CK(cudaGraphLaunch(C.exec, s));
+  }
   trace_mark("sort", s, true);
   BlockMap bm{nx, n, nbx};
   k_count<KT><<<nbx + nbk, kBlk, 0, s>>>(keys_out, bm, d, L, ml, counts);
@@ -280,7 +370,7 @@ static int sort_and_fill(sft_plan_s* P, const double* x_dev, const double* k_dev
   CK(cudaGetLastError());
   trace_mark("fill", s, true);
 
-  *scr_out = scr;
+  *scr_out = use_graph ? nullptr : scr;  // the cached scratch is not the plan's to free
   return SFT_OK;
 }
 
@@ -367,7 +457,7 @@ int build_trees(sft_plan_s* P, const double* x_dev, const double* k_dev, std::st
   static thread_local int64_t* h = nullptr;
   if (!h) CK(cudaMallocHost((void**)&h, (2 * kMaxLevels + 1) * sizeof(int64_t)));
   CK(cudaMemcpyAsync(h, arena + o_hdr, (16 * (L + 1) + 8), cudaMemcpyDeviceToHost, s));
-  CK(cudaFreeAsync(scr, s));
+  if (scr) CK(cudaFreeAsync(scr, s));
   CK(cudaStreamSynchronize(s));
   trace_mark("sync");
   const int herr = (int)(h[2 * (L + 1)] & 0xffffffff);
