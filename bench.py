@@ -56,30 +56,85 @@ def measured_peaks():
 # clocks sampler (nvidia-smi during the timed region)
 # ---------------------------------------------------------------------------
 class Clocks:
+    """SM clock and clock-event (throttle) reasons sampled during the timed
+    region: NVML polled every ~1 ms from a thread (the timed regions are tens
+    of ms, too short for `nvidia-smi -lms`), nvidia-smi as the fallback."""
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, gpu_index):
-        self.gpu = str(gpu_index)
+        self.gpu = int(gpu_index)
         self.proc = None
         self.lines = []
         self.t = None
+        self.nv = None
+        self.samples = []  # (sm_mhz, reasons bitmask)
+        self.stop_flag = threading.Event()
 
     def start(self):
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", self.gpu, f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                                          "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            import pynvml
+            pynvml.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            idx = self.gpu
+            if vis:
+                try:
+                    idx = int(vis.split(",")[self.gpu])
+                except ValueError:
+                    idx = self.gpu
+            self.nv = (pynvml, pynvml.nvmlDeviceGetHandleByIndex(idx))
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.nv[1], pynvml.NVML_CLOCK_SM)
+            self.sample_once()
+            self.t = threading.Thread(target=self._poll, daemon=True)
+            self.t.start()
+            return
+        except Exception:
+            self.nv = None
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
         except Exception:
             self.proc = None
+
+    def sample_once(self):
+        nv, h = self.nv
+        self.samples.append((nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM),
+                             nv.nvmlDeviceGetCurrentClocksEventReasons(h)))
+
+    def _poll(self):
+        while not self.stop_flag.is_set():
+            try:
+                self.sample_once()
+            except Exception:
+                break
+            time.sleep(0.001)
 
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
     def stop(self):
+        if self.nv is not None:
+            self.stop_flag.set()
+            self.t.join(timeout=5)
+            try:
+                self.sample_once()
+            except Exception:
+                pass
+            nv = self.nv[0]
+            names = {"hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
+                     "hw_thermal_slowdown": nv.nvmlClocksEventReasonHwThermalSlowdown,
+                     "sw_thermal_slowdown": nv.nvmlClocksEventReasonSwThermalSlowdown,
+                     "sw_power_cap": nv.nvmlClocksEventReasonSwPowerCap}
+            reasons = sorted({n for _, r in self.samples for n, bit in names.items() if r & bit})
+            sm = [float(c) for c, _ in self.samples]
+            busy = [v for v in sm if v > 0.5 * self.max_mhz] or sm
+            return {"sm_mhz": float(np.median(busy)) if busy else None, "sm_max_mhz": float(self.max_mhz),
+                    "samples": len(sm), "reasons": reasons, "source": "nvml"}
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()
@@ -104,7 +159,7 @@ class Clocks:
                     reasons.add(n)
         busy = [v for v in sm if v > 0.5 * (mx or 1)] or sm
         return {"sm_mhz": float(np.median(busy)) if busy else None, "sm_max_mhz": mx, "samples": len(sm),
-                "reasons": sorted(reasons)}
+                "reasons": sorted(reasons), "source": "nvidia-smi"}
 
 
 # ---------------------------------------------------------------------------
