@@ -1041,101 +1041,115 @@ __device__ __forceinline__ void load_lane_ops(LaneOps<P, TS>& op, const double* 
 // per tile arms full[s] with the byte count, bulk-copies the tile's schedule
 // block into blk[s] and every present child array into stage s (reading the
 // group records of its next tile from HBM while it waits for a free stage).
-template <int D, int P, int G, int NST, typename E = double2, int PS = Pow<P, D>::v, bool BATCH = false>
-__device__ __forceinline__ void ws_producer(const TransArgs& a, const unsigned char* __restrict__ sched, int64_t ntiles,
-                                            E* ring, unsigned char (*blk)[Sched<D, P, G>::BLK], uint64_t* full,
-                                            uint64_t* empty) {
+// Issue one tile (work item w = tile * nrhs + r) into stage s, by one whole
+// warp: zero the slots of absent children (the consumers read every slot
+// unmasked), arm full[s] with the byte count, bulk-copy (1-D TMA) the tile's
+// schedule block and every present child array.  gr = this lane's group
+// record (first child pair index, child mask) for lane < G.
+template <int D, int P, int G, int NST, typename E, int PS, bool BATCH>
+__device__ __forceinline__ void ws_issue(const TransArgs& a, const unsigned char* __restrict__ sched, int64_t w,
+                                         int64_t tile, uint2 gr, E* ring, unsigned char (*blk)[Sched<D, P, G>::BLK],
+                                         uint64_t* full, int s) {
   using SC = Sched<D, P, G>;
   constexpr int PD = PS;  // stage and HBM arrays have stride PS elements of type E
   constexpr int NS = 1 << D;
   constexpr int STAGE = G * NS * PD;
   const int lane = threadIdx.x & 31;
-    INSTR_T0(tp0);
-    int s = 0;
-    uint32_t ph = 0;
-    // work items w = tile * nrhs + r (BATCH = false: nrhs = 1, w = tile)
-    const int64_t nr = BATCH ? a.nrhs : 1;
-    const int64_t nwork = ntiles * nr;
-    int64_t w = blockIdx.x;
-    int64_t tile = BATCH ? w / nr : w;
-    uint2 gr = (w < nwork && lane < G) ? __ldg(reinterpret_cast<const uint2*>(sched + tile * SC::BLK + SC::HDR) + lane)
-                                       : make_uint2(0u, 0u);
-    // programmatic dependent launch: everything above (schedule reads, barrier
-    // init, the consumers' operand loads) overlaps the previous level's tail;
-    // the previous level's output (our input) and input (our output buffer)
-    // are touched only after it has completed
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    for (int i = 0; w < nwork; ++i) {
-      const int64_t wn = w + gridDim.x;
-      const int64_t next = BATCH ? wn / nr : wn;
-      const uint2 gn = (wn < nwork && lane < G)
-                           ? __ldg(reinterpret_cast<const uint2*>(sched + next * SC::BLK + SC::HDR) + lane)
-                           : make_uint2(0u, 0u);
-      const E* const ain = reinterpret_cast<const E*>(a.in) + (BATCH ? (w - tile * nr) * a.rs : (int64_t)0);
-      INSTR_T0(tw0);
-      if (i >= NST) mbar_wait_sleep(smem_u32(&empty[s]), ph ^ 1u);
-      INSTR_ADD(1, tw0);
-      INSTR_T0(tb0);
-      uint32_t nbytes = __popc(gr.y) * PD * (uint32_t)sizeof(E);
+  const int64_t nr = BATCH ? a.nrhs : 1;
+  const E* const ain = reinterpret_cast<const E*>(a.in) + (BATCH ? (w - tile * nr) * a.rs : (int64_t)0);
+  uint32_t nbytes = __popc(gr.y) * PD * (uint32_t)sizeof(E);
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) nbytes += __shfl_xor_sync(0xffffffffu, nbytes, o);
-      E* sb = ring + s * STAGE;
-#ifndef SFT_NO_ZEROFILL
-      // zero the slots of absent children of the tile's groups: the consumers
-      // then read every slot unmasked (absent children and padding contribute 0)
-      {
-        const int ng = (int)min((int64_t)G, a.ngroups - tile * G);
-        constexpr int CH = PD * (int)sizeof(E) / 16;  // 16-byte chunks per slot
-        for (int js = 0; js < ng * NS; ++js) {
-          const uint32_t mB = __shfl_sync(0xffffffffu, gr.y, js / NS);
-          if (mB >> (js % NS) & 1) continue;
-          float4* z = reinterpret_cast<float4*>(sb + (int64_t)js * PD);
-          for (int q = lane; q < CH; q += 32) z[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncwarp();
-      }
-#endif
-      if (lane == 0) {
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&full[s])),
-                     "r"(nbytes + (uint32_t)SC::BLK)
-                     : "memory");
-        asm volatile(
-            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                smem_u32(&blk[s][0])),
-            "l"(sched + tile * SC::BLK), "r"((uint32_t)SC::BLK), "r"(smem_u32(&full[s]))
-            : "memory");
-      }
-      __syncwarp();
-      uint32_t mm = gr.y;
-      int r = 0;
-      while (mm) {
-        const int c = __ffs(mm) - 1;
-        mm &= mm - 1;
-        const int64_t pin = (int64_t)gr.x + (int64_t)(r++) * a.in_nA;
-#ifndef SFT_ABL_NOLOAD
-        asm volatile(
-            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                smem_u32(sb + ((int64_t)lane * NS + c) * PD)),
-            "l"(ain + pin * PD), "r"((uint32_t)(PD * sizeof(E))), "r"(smem_u32(&full[s]))
-            : "memory");
-#else
-        (void)pin;
-        asm volatile("mbarrier.complete_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&full[s])),
-                     "r"((uint32_t)(PD * sizeof(E)))
-                     : "memory");
-#endif
-      }
-      INSTR_ADD(2, tb0);
-      gr = gn;
-      w = wn;
-      tile = next;
-      if (++s == NST) {
-        s = 0;
-        ph ^= 1u;
-      }
+  for (int o = 16; o > 0; o >>= 1) nbytes += __shfl_xor_sync(0xffffffffu, nbytes, o);
+  E* sb = ring + s * STAGE;
+  {
+    const int ng = (int)min((int64_t)G, a.ngroups - tile * G);
+    constexpr int CH = PD * (int)sizeof(E) / 16;  // 16-byte chunks per slot
+    for (int js = 0; js < ng * NS; ++js) {
+      const uint32_t mB = __shfl_sync(0xffffffffu, gr.y, js / NS);
+      if (mB >> (js % NS) & 1) continue;
+      float4* z = reinterpret_cast<float4*>(sb + (int64_t)js * PD);
+      for (int q = lane; q < CH; q += 32) z[q] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    INSTR_ADD(0, tp0);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+  }
+  if (lane == 0) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&full[s])),
+                 "r"(nbytes + (uint32_t)SC::BLK)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(&blk[s][0])),
+        "l"(sched + tile * SC::BLK), "r"((uint32_t)SC::BLK), "r"(smem_u32(&full[s]))
+        : "memory");
+  }
+  __syncwarp();
+  uint32_t mm = gr.y;
+  int r = 0;
+  while (mm) {
+    const int c = __ffs(mm) - 1;
+    mm &= mm - 1;
+    const int64_t pin = (int64_t)gr.x + (int64_t)(r++) * a.in_nA;
+#ifndef SFT_ABL_NOLOAD
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(sb + ((int64_t)lane * NS + c) * PD)),
+        "l"(ain + pin * PD), "r"((uint32_t)(PD * sizeof(E))), "r"(smem_u32(&full[s]))
+        : "memory");
+#else
+    (void)pin;
+    asm volatile("mbarrier.complete_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&full[s])),
+                 "r"((uint32_t)(PD * sizeof(E)))
+                 : "memory");
+#endif
+  }
+}
+
+template <int D, int P, int G>
+__device__ __forceinline__ uint2 ws_group_record(const unsigned char* __restrict__ sched, int64_t tile, bool ok) {
+  using SC = Sched<D, P, G>;
+  const int lane = threadIdx.x & 31;
+  return (ok && lane < G) ? __ldg(reinterpret_cast<const uint2*>(sched + tile * SC::BLK + SC::HDR) + lane)
+                          : make_uint2(0u, 0u);
+}
+
+template <int D, int P, int G, int NST, typename E = double2, int PS = Pow<P, D>::v, bool BATCH = false>
+__device__ __forceinline__ void ws_producer(const TransArgs& a, const unsigned char* __restrict__ sched, int64_t ntiles,
+                                            E* ring, unsigned char (*blk)[Sched<D, P, G>::BLK], uint64_t* full,
+                                            uint64_t* empty) {
+  INSTR_T0(tp0);
+  int s = 0;
+  uint32_t ph = 0;
+  // work items w = tile * nrhs + r (BATCH = false: nrhs = 1, w = tile)
+  const int64_t nr = BATCH ? a.nrhs : 1;
+  const int64_t nwork = ntiles * nr;
+  int64_t w = blockIdx.x;
+  int64_t tile = BATCH ? w / nr : w;
+  uint2 gr = ws_group_record<D, P, G>(sched, tile, w < nwork);
+  // programmatic dependent launch: everything above (schedule reads, barrier
+  // init, the consumers' operand loads) overlaps the previous level's tail;
+  // the previous level's output (our input) and input (our output buffer)
+  // are touched only after it has completed
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  for (int i = 0; w < nwork; ++i) {
+    const int64_t wn = w + gridDim.x;
+    const int64_t next = BATCH ? wn / nr : wn;
+    const uint2 gn = ws_group_record<D, P, G>(sched, next, wn < nwork);
+    INSTR_T0(tw0);
+    if (i >= NST) mbar_wait_sleep(smem_u32(&empty[s]), ph ^ 1u);
+    INSTR_ADD(1, tw0);
+    INSTR_T0(tb0);
+    ws_issue<D, P, G, NST, E, PS, BATCH>(a, sched, w, tile, gr, ring, blk, full, s);
+    INSTR_ADD(2, tb0);
+    gr = gn;
+    w = wn;
+    tile = next;
+    if (++s == NST) {
+      s = 0;
+      ph ^= 1u;
+    }
+  }
+  INSTR_ADD(0, tp0);
 }
 
 // Warp-specialised translation kernel (default).  Warp NC is the producer: it
@@ -1146,11 +1160,20 @@ __device__ __forceinline__ void ws_producer(const TransArgs& a, const unsigned c
 // 2D with NST >= 3: skewed pipeline, pass 1 of tile i+1 runs before pass 0 of
 // tile i, and pass 0 waits on an mbarrier (p1done) every consumer thread
 // arrives on after its pass-1 rows, so warps do not idle at a pass barrier.
+//
+// SELF = true: no producer warp.  Warp 0 issues the first NST tiles; after
+// that, the consumer warp that finishes a stage last (a shared-memory
+// counter) refills it with the CTA's tile NST ahead -- the warp that would
+// otherwise idle at a barrier does the issue, and the CTA needs NC instead of
+// NC + 1 warps' registers (one more CTA per SM at 2D p = 9).  Non-skewed
+// pipeline only.
 template <int D, int P, int G, int NC, int NST, int MINB, typename E = double2, bool FUSED = false,
-          bool BATCH = false>
-__global__ __launch_bounds__((NC + 1) * 32, MINB) void k_translate_ws(TransArgs a, const double* __restrict__ frag,
-                                                                             const unsigned char* __restrict__ sched,
-                                                                             int64_t ntiles) {
+          bool BATCH = false, bool SELF = false>
+__global__ __launch_bounds__((NC + (SELF ? 0 : 1)) * 32, MINB) void k_translate_ws(TransArgs a,
+                                                                                  const double* __restrict__ frag,
+                                                                                  const unsigned char* __restrict__ sched,
+                                                                                  int64_t ntiles) {
+  static_assert(!SELF || D != 2 || NST < 3, "the self-fed mode has no skewed pipeline");
   using SC = Sched<D, P, G>;
   constexpr int PD = StrideT<E, Pow<P, D>::v>::v;  // array stride (elements)
   constexpr int NS = 1 << D;
@@ -1159,8 +1182,10 @@ __global__ __launch_bounds__((NC + 1) * 32, MINB) void k_translate_ws(TransArgs 
   E* ring = reinterpret_cast<E*>(smem_raw);  // [NST][G][NS][PD]
   __shared__ __align__(128) unsigned char blk[NST][SC::BLK];
   __shared__ __align__(8) uint64_t full[NST], empty[NST], p1done[NST];
+  __shared__ int done_cnt[NST];  // SELF: consumer warps finished with the stage's tile
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (threadIdx.x < NST) {
+    done_cnt[threadIdx.x] = 0;
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full[threadIdx.x])));
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&empty[threadIdx.x])), "r"(NC));
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&p1done[threadIdx.x])), "r"(NC * 32));
@@ -1168,10 +1193,44 @@ __global__ __launch_bounds__((NC + 1) * 32, MINB) void k_translate_ws(TransArgs 
   if (threadIdx.x == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   fill_tail_smem<D, P>(frag);
   __syncthreads();
-  if (warp == NC) {
+  if (!SELF && warp == NC) {
     ws_producer<D, P, G, NST, E, PD, BATCH>(a, sched, ntiles, ring, blk, full, empty);
     return;
   }
+  const int64_t nr_ = BATCH ? a.nrhs : 1;
+  if (SELF && warp == 0) {
+    // prologue: the first NST work items of this CTA (after the previous
+    // level has completed: programmatic dependent launch)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    for (int j = 0; j < NST; ++j) {
+      const int64_t wj = blockIdx.x + (int64_t)j * gridDim.x;
+      if (wj >= ntiles * nr_) break;
+      const int64_t tj = BATCH ? wj / nr_ : wj;
+      ws_issue<D, P, G, NST, E, PD, BATCH>(a, sched, wj, tj, ws_group_record<D, P, G>(sched, tj, true), ring, blk,
+                                           full, j);
+    }
+  }
+  // SELF: this warp is done with stage st (work item w_); the last of the NC
+  // warps to finish refills it with work item w_ + NST * gridDim.x
+  auto self_release = [&](int st, int64_t w_) {
+    __syncwarp();
+    int old = 0;
+    if (lane == 0) {
+      __threadfence_block();
+      old = atomicAdd(&done_cnt[st], 1);
+    }
+    old = __shfl_sync(0xffffffffu, old, 0);
+    if (old == NC - 1) {
+      __threadfence_block();
+      if (lane == 0) done_cnt[st] = 0;
+      const int64_t wn = w_ + (int64_t)NST * gridDim.x;
+      if (wn < ntiles * nr_) {
+        const int64_t tn = BATCH ? wn / nr_ : wn;
+        ws_issue<D, P, G, NST, E, PD, BATCH>(a, sched, wn, tn, ws_group_record<D, P, G>(sched, tn, true), ring,
+                                             blk, full, st);
+      }
+    }
+  };
   // ---------------- consumers ----------------
   LaneOps<P, TailSmem<D>::v> op;
   load_lane_ops(op, frag, lane);
@@ -1191,7 +1250,7 @@ __global__ __launch_bounds__((NC + 1) * 32, MINB) void k_translate_ws(TransArgs 
   // work items w = tile * nrhs + r; the output of RHS r goes to out + r * rs
   const int64_t nwork = BATCH ? ntiles * a.nrhs : ntiles;
   auto ooff = [&](int64_t w_) { return BATCH ? (w_ % a.nrhs) * a.rs : (int64_t)0; };
-  if constexpr (D == 2 && NST >= 3) {
+  if constexpr (D == 2 && NST >= 3 && !SELF) {
     int64_t tile = blockIdx.x;
     if (tile < nwork) {
       mbar_wait(smem_u32(&full[0]), 0);
@@ -1246,9 +1305,13 @@ __global__ __launch_bounds__((NC + 1) * 32, MINB) void k_translate_ws(TransArgs 
         consumer_sync<NC * 32>();
         consumer_pass<D, P, G, NC, 0, true, 0, E, FUSED>(a, sb, blk[s], op, rot, ooff(w));
       }
-      __syncwarp();
-      if (lane == 0)
-        asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[s])) : "memory");
+      if constexpr (SELF) {
+        self_release(s, w);
+      } else {
+        __syncwarp();
+        if (lane == 0)
+          asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[s])) : "memory");
+      }
       if (++s == NST) {
         s = 0;
         ph ^= 1u;
@@ -1342,8 +1405,10 @@ __global__ __launch_bounds__((NC + 1) * 32, MINB) void k_translate_f32(TransArgs
   float2* ring = reinterpret_cast<float2*>(smem_raw);  // [NST][G][NS][PS]
   __shared__ __align__(128) unsigned char blk[NST][SC::BLK];
   __shared__ __align__(8) uint64_t full[NST], empty[NST], p1done[NST];
+  __shared__ int done_cnt[NST];  // SELF: consumer warps finished with the stage's tile
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (threadIdx.x < NST) {
+    done_cnt[threadIdx.x] = 0;
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full[threadIdx.x])));
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&empty[threadIdx.x])), "r"(NC));
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&p1done[threadIdx.x])), "r"(NC * 32));
@@ -1607,6 +1672,9 @@ __global__ __launch_bounds__(NT, SFT_FMA_MINB(NT)) void k_translate_fma(TransArg
 #ifndef SFT_WS_MINB29
 #define SFT_WS_MINB29 4
 #endif
+#ifndef SFT_SELF_DEFAULT
+#define SFT_SELF_DEFAULT 0
+#endif
 template <int D, int P>
 struct WsCfg;
 template <> struct WsCfg<2, 5> { static constexpr int G = 16, NC = 4, NST = 3, MINB = 2; };
@@ -1646,6 +1714,28 @@ template <> struct WsCfg<3, 7> {
   static constexpr int G = SFT_WS_G37, NC = SFT_WS_NC37, NST = SFT_WS_NST37, MINB = SFT_WS_MINB37;
 };
 template <> struct WsCfg<3, 9> { static constexpr int G = 1, NC = 8, NST = 2, MINB = 1; };
+
+// self-fed mode (k_translate_ws<..., SELF = true>): min CTAs per SM for the
+// register cap (NC warps per CTA instead of NC + 1)
+template <int D, int P>
+struct SelfCfg {
+  static constexpr int MINB = D == 2 && P == 9 ? 5 : WsCfg<D, P>::MINB;
+};
+// SFT_SELF=0/1 overrides; default: on where measured faster
+static int self_env() {
+  static int v = -2;
+  if (v == -2) {
+    const char* e = getenv("SFT_SELF");
+    v = e ? (e[0] == '1' ? 1 : 0) : -1;
+  }
+  return v;
+}
+template <int D>
+static bool use_self(int nst) {
+  if (D == 2 && nst >= 3) return false;  // skewed pipeline needs the producer
+  const int v = self_env();
+  return v < 0 ? SFT_SELF_DEFAULT : v == 1;
+}
 
 // FP32 storage on the DMMA kernel (default FP32 variant): arrays are half the
 // size, so twice the groups per stage at the same shared memory
@@ -1859,6 +1949,20 @@ static cudaError_t launch_translate_t(const sft_plan_s* Pl, const LevelDims& L, 
       }
       launch_pdl(k_translate_ws<D, P, G, NC, NST, MB, double2, false, true>, (unsigned)grid, (NC + 1) * 32, smem,
                  Pl->stream, a, frag, L.sched, ntiles);
+    } else if (use_self<D>(NST)) {
+      // self-fed consumers (no producer warp): one more CTA per SM where registers allowed NC + 1 warps
+      if constexpr (!(D == 2 && NST >= 3)) {
+        constexpr int MBS = SelfCfg<D, P>::MINB;
+        static int grid_self = 0;
+        if (!grid_self) {
+          cudaError_t e = persistent_grid(k_translate_ws<D, P, G, NC, NST, MBS, double2, false, false, true>,
+                                          NC * 32, smem, &grid_self);
+          if (e != cudaSuccess) return e;
+        }
+        launch_pdl(k_translate_ws<D, P, G, NC, NST, MBS, double2, false, false, true>,
+                   (unsigned)std::min<int64_t>(ntiles, grid_self), NC * 32, smem, Pl->stream, a, frag, L.sched,
+                   ntiles);
+      }
     } else {
       launch_pdl(k_translate_ws<D, P, G, NC, NST, MB>, (unsigned)grid, (NC + 1) * 32, smem, Pl->stream, a, frag,
                  L.sched, ntiles);

@@ -303,3 +303,30 @@ def test_adjoint(p):
         u = plan.apply(torch.from_numpy(f).cuda()).cpu().numpy()
     lhs, rhs = np.vdot(g, u), np.vdot(v, f)
     assert abs(lhs - rhs) <= 5 * DIRECT_TOL[p] * np.linalg.norm(g) * np.linalg.norm(u)
+
+
+def test_sort_graph_cache_reuse_and_sizes():
+    """sft_plan replays a cached graph of the point sort when consecutive plans
+    of one thread have the same sizes (n >= 32K): alternating sizes rebuild it,
+    identical sizes with different points reuse it -- results stay bitwise equal
+    to a fresh plan and within parity of the oracle."""
+    torch = _torch()
+    rng = np.random.default_rng(21)
+    N, p = 1024, 5
+
+    def pts(n, r, seed):
+        t = np.random.default_rng(seed).uniform(0, 2 * np.pi, n)
+        return np.stack([0.5 + r * np.cos(t), 0.5 + r * np.sin(t)], 1) * N
+
+    cases = [(pts(20000, 0.40, 1), pts(18000, 0.30, 2)), (pts(25000, 0.35, 3), pts(16000, 0.25, 4)),
+             (pts(20000, 0.20, 5), pts(18000, 0.45, 6))]  # case 2 has case 0's sizes
+    f = [rng.normal(size=len(k)) + 1j * rng.normal(size=len(k)) for _, k in cases]
+    first = []
+    for (x, k), fi in zip(cases, f):
+        u, _ = gpu_transform(x, k, fi, N, p)
+        first.append(u)
+    for (x, k), fi, u0 in zip(cases, f, first):  # again, cache state different
+        u, _ = gpu_transform(x, k, fi, N, p)
+        assert np.array_equal(u.view(np.uint64), u0.view(np.uint64))
+    x, k = cases[2]
+    assert oracle.rel_l2(first[2], oracle.butterfly(x, k, f[2], N, p)) <= PARITY
