@@ -310,17 +310,22 @@ def run_ours(args):
             final_ms = float(np.median([t["final_ms"] for t in kt]))
             app_ms = float(np.median([t["apply_ms"] for t in kt]))
             L = int(st["L"])
-            bytes_per_launch = st["trans_alg_bytes"] / L
-            dur_per_launch = trans_ms / L / 1e3
+            nlaunch = len(st.get("launches", [])) or L
+            # achieved = algorithmic (level-synchronous) bytes of all levels / the
+            # launches' total device time (= per-launch bytes / mean launch duration)
+            bytes_per_launch = st["trans_alg_bytes"] / nlaunch
+            dur_per_launch = trans_ms / nlaunch / 1e3
             achieved = bytes_per_launch / dur_per_launch / 1e9
             traffic = None
             tf = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
             if os.path.exists(tf):
                 traffic = json.load(open(tf)).get("dram_bytes_per_launch")
-            roof = {"bound": "hbm", "kernel": "k_translate (K3, one launch per level)", "achieved": round(achieved, 1),
+            n2 = sum(1 for _, f2 in st.get("launches", []) if f2)
+            kname = "k_translate_ws (one launch per level" + (f", {n2} two-level launch)" if n2 else ")")
+            roof = {"bound": "hbm", "kernel": kname, "achieved": round(achieved, 1),
                     "peak": hbm_peak, "unit": "GB/s", "frac": round(achieved / hbm_peak, 4), "traffic": traffic,
                     "peak_source": peak_src,
-                    "alg_bytes_per_launch": bytes_per_launch, "launches_per_apply": L,
+                    "alg_bytes_per_launch": bytes_per_launch, "launches_per_apply": nlaunch,
                     "kernel_ms": {"leaf": round(leaf_ms, 4), "translate_total": round(trans_ms, 4),
                                   "final": round(final_ms, 4), "apply_events": round(app_ms, 4)},
                     "level_ms": [round(float(v), 4) for v in np.median([t["level_ms"] for t in kt], axis=0)]}

@@ -131,11 +131,20 @@ const char* sft_last_error(void);
  *               groups total, translation algorithmic bytes per apply. */
 int sft_plan_stats(sft_plan_t plan, int64_t* counts_x, int64_t* counts_k, int64_t* pairs, double* info);
 
+/* Translation launches of sft_apply (host, caller-allocated [L] arrays or NULL):
+ * *n launches in order; out_level[i] = the level t the launch writes;
+ * two_level[i] = 1 if it is a two-level (radix-4) launch computing levels t+1
+ * and t from level t+2 in one pass over super-groups (A'', B) without storing
+ * level t+1 (SURVEY.md §8(f) item 2 "cross-level fusion"; 2D FP64 single-GPU
+ * plans; SFT_F2=0 disables), else a single-level launch. */
+int sft_translation_launches(sft_plan_t plan, int* n, int* out_level, int* two_level);
+
 /* Device time (ms, CUDA events on the plan stream) of the kernels of the last
  * sft_apply when timing was enabled with sft_set_timing(plan, 1):
  *   t_ms[0] leaf kernel, t_ms[1] sum of translation kernels, t_ms[2] final
  *   kernel, t_ms[3] whole apply; per_level_ms [L] translation level t=0..L-1
- *   (or NULL). */
+ *   (or NULL; a two-level launch is booked on its output level t, level t+1
+ *   then reads 0). */
 int sft_set_timing(sft_plan_t plan, int enable);
 int sft_last_timing(sft_plan_t plan, double* t_ms, double* per_level_ms);
 

@@ -77,6 +77,8 @@ def lib():
     L.sft_last_error.restype = ctypes.c_char_p
     L.sft_plan_stats.argtypes = [vp, _c_i64p, _c_i64p, _c_i64p, _c_dp]
     L.sft_set_timing.argtypes = [vp, ctypes.c_int]
+    L.sft_translation_launches.argtypes = [vp, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
+                                           ctypes.POINTER(ctypes.c_int)]
     L.sft_last_timing.argtypes = [vp, _c_dp, _c_dp]
     L.sft_exchange_counts.argtypes = [vp, _c_i64p, _c_i64p]
     L.sft_apply_phase1.argtypes = [vp, vp, vp]
@@ -284,6 +286,11 @@ class Plan:
         keys = ["L", "pd", "nx", "nk", "level_buffer_bytes", "plan_ms", "groups", "trans_alg_bytes"]
         d = dict(zip(keys, info.tolist()))
         d.update(counts_x=cx, counts_k=ck, pairs=pr)
+        nl = ctypes.c_int(0)
+        lv = (ctypes.c_int * max(1, self.L))()
+        f2 = (ctypes.c_int * max(1, self.L))()
+        _check(lib().sft_translation_launches(self._h, ctypes.byref(nl), lv, f2))
+        d.update(launches=[(int(lv[i]), bool(f2[i])) for i in range(nl.value)])
         return d
 
     def set_timing(self, on=True):

@@ -332,8 +332,32 @@ static LevelDims apply_dims(const sft_plan_s* P, int t) {
   return level_dims_x(P, t);
 }
 
+// Two-level launch with output level t (world 1, 2D): super-groups (A'', B),
+// B at level t, A'' at level L-t-2; input = level t+2 pairs, output = level t.
+static LevelDims two_level_dims(const sft_plan_s* P, int t) {
+  const int L = P->L;
+  LevelDims ld = level_dims_k(P, t);
+  ld.f2 = 1;
+  ld.ap_lo = 0;
+  ld.ap_hi = P->X.counts[L - t - 2];
+  ld.in_b0 = 0;
+  ld.in_nA = P->X.counts[L - t - 2];
+  ld.in_a0 = 0;
+  ld.cbK1 = P->K.lev[t + 1].child_begin;
+  ld.mK1 = P->K.lev[t + 1].child_mask;
+  ld.cbX2 = P->X.lev[L - t - 2].child_begin;
+  ld.mX2 = P->X.lev[L - t - 2].child_mask;
+  return ld;
+}
+
+// Dims of the translation launch whose output level is t (two-level or single)
+static LevelDims launch_dims(const sft_plan_s* P, int t) {
+  const bool f2 = t < (int)P->launch_f2_out.size() && P->launch_f2_out[t];
+  return f2 ? two_level_dims(P, t) : apply_dims(P, t);
+}
+
 static LevelDims apply_dims_sched(const sft_plan_s* P, int t) {
-  LevelDims ld = apply_dims(P, t);
+  LevelDims ld = launch_dims(P, t);
   ld.sched = P->sched ? P->sched + P->sched_off[t] : nullptr;
   return ld;
 }
@@ -633,13 +657,41 @@ extern "C" int sft_plan(int dim, int64_t N, int p, const double* x, int64_t nx, 
       P->x_rng[l].hi = P->X.counts[l];
     }
   }
-  // one allocation: level buffer 0 | level buffer 1 | tile schedules of every level
+  // translation launches of the single-GPU apply: two-level launches (levels
+  // t+1 and t from t+2) where supported, from the leaf level down; a single
+  // level 0 is left when L is odd.  Multi-rank plans run single levels.
+  P->launch_t.clear();
+  P->launch_f2_out.assign(L, 0);
+  {
+    // measured (C2, per level pair): the two-level launch wins at the leaf end
+    // (levels 13+12: 0.1125 -> 0.1023 ms) and loses in the middle (e.g. 11+10:
+    // 0.201 -> 0.231 ms: a super-group's 16 stage slots hold ~2 present first-
+    // level groups on these curves), so by default only the first pair is fused;
+    // SFT_F2=all fuses every pair
+    const bool f2 = two_level_supported(P);
+    const char* fe = getenv("SFT_F2");
+    const bool f2_all = fe && std::string(fe) == "all";
+    int t = L - 1;
+    while (t >= 0) {
+      if (f2 && t >= 1 && (f2_all || t == L - 1)) {
+        P->launch_t.push_back(t - 1);
+        P->launch_f2_out[t - 1] = 1;
+        t -= 2;
+      } else {
+        P->launch_t.push_back(t);
+        t -= 1;
+      }
+    }
+  }
+  // one allocation: level buffer 0 | level buffer 1 | tile schedules of every launch
+  // (indexed by the launch's output level; levels consumed inside a two-level launch have none)
   {
     P->sched_off.assign(L + 1, 0);
     size_t tot = 0;
     for (int t = 0; t < L; ++t) {
       P->sched_off[t] = tot;
-      tot += (schedule_bytes(P, apply_dims(P, t)) + 255) / 256 * 256;
+      const bool inner = t >= 1 && P->launch_f2_out[t - 1];  // level t produced inside a two-level launch
+      if (!inner) tot += (schedule_bytes(P, launch_dims(P, t)) + 255) / 256 * 256;
     }
     P->sched_off[L] = tot;
     const size_t bb = (P->buf_elems * (P->prec == 1 ? sizeof(float2) : sizeof(double2)) + 255) / 256 * 256;
@@ -651,11 +703,12 @@ extern "C" int sft_plan(int dim, int64_t N, int p, const double* x, int64_t nx, 
     P->sched = tot > 0 ? (unsigned char*)(blk + 2 * bb) : nullptr;
     trace_mark("bufs");
     if (tot > 0) {
-      std::vector<LevelDims> dims(L);
-      std::vector<unsigned char*> dst(L);
+      std::vector<LevelDims> dims;
+      std::vector<unsigned char*> dst;
       for (int t = 0; t < L; ++t) {
-        dims[t] = apply_dims(P, t);
-        dst[t] = P->sched + P->sched_off[t];
+        if (t >= 1 && P->launch_f2_out[t - 1]) continue;
+        dims.push_back(launch_dims(P, t));
+        dst.push_back(P->sched + P->sched_off[t]);
       }
       // the schedules are built on a side stream so that they overlap the
       // first kernels of the apply (the leaf kernel needs only the trees);
@@ -663,7 +716,7 @@ extern "C" int sft_plan(int dim, int64_t N, int p, const double* x, int64_t nx, 
       cudaStream_t side = side_stream();
       cudaEventRecord(P->sched_fork, s);
       cudaStreamWaitEvent(side, P->sched_fork, 0);
-      cudaError_t ce = launch_schedule(P, dims.data(), L, dst.data(), side);
+      cudaError_t ce = launch_schedule(P, dims.data(), (int)dims.size(), dst.data(), side);
       cudaEventRecord(P->sched_ready, side);
       sched_recorded = true;
       if (ce != cudaSuccess) return bail(SFT_E_CUDA, std::string("schedule: ") + cudaGetErrorString(ce));
@@ -672,7 +725,8 @@ extern "C" int sft_plan(int dim, int64_t N, int p, const double* x, int64_t nx, 
         cudaStreamWaitEvent(s, P->sched_ready, 0);
         // debug: every level's schedule against its buffer sizes
         for (int t = 0; t < L; ++t) {
-          const LevelDims ld = apply_dims(P, t);
+          if (t >= 1 && P->launch_f2_out[t - 1]) continue;
+          const LevelDims ld = launch_dims(P, t);
           const int64_t in_pairs = (int64_t)(P->buf_elems / P->pds), out_pairs = in_pairs;
           cudaError_t ce = check_schedule(P, ld, P->sched + P->sched_off[t], in_pairs, out_pairs, P->d_err);
           if (ce != cudaSuccess) return bail(SFT_E_CUDA, std::string("check: ") + cudaGetErrorString(ce));
@@ -775,7 +829,9 @@ static void tmark(sft_plan_s* P) {
   if (P->n_ev < 64) cudaEventRecord(P->ev[P->n_ev++], P->stream);
 }
 
-static int finish_timing(sft_plan_s* P, int n_levels_first) {
+// tl: output level of each timed translation launch (nullptr: n_levels_first - i);
+// a two-level launch's time is booked on its output level (the inner level shows 0)
+static int finish_timing(sft_plan_s* P, int n_levels_first, const std::vector<int>* tl = nullptr) {
   if (!P->timing) return SFT_OK;
   CKR(cudaEventSynchronize(P->ev[P->n_ev - 1]));
   // events: [0] start, [1] after leaf, [2..] after each level, [n-1] after final
@@ -787,7 +843,7 @@ static int finish_timing(sft_plan_s* P, int n_levels_first) {
   int nlev = P->n_ev - 3;
   for (int i = 0; i < nlev; ++i) {
     cudaEventElapsedTime(&ms, P->ev[1 + i], P->ev[2 + i]);
-    int t = n_levels_first - i;
+    const int t = tl ? (i < (int)tl->size() ? (*tl)[i] : -1) : n_levels_first - i;
     if (t >= 0 && t < P->L) P->level_ms[t] = ms;
     trans += ms;
   }
@@ -863,26 +919,30 @@ static int apply_impl(sft_plan_s* P, int nrhs, const void* f, int64_t ldf, void*
   P->n_ev = 0;
   tmark(P);
   // step 2: leaf charges, level L buffer
-  CKR(launch_leaf(P, fd, buf[L & 1], 0, P->K.counts[L], nrhs, ldf, rs));
+  // the level buffers alternate per launch: leaf -> buf[0], launch i reads
+  // buf[i & 1] and writes buf[(i + 1) & 1]
+  CKR(launch_leaf(P, fd, buf[0], 0, P->K.counts[L], nrhs, ldf, rs));
   tmark(P);
-  // step 3: t = L-1 .. 0 (after the plan's schedule kernel on the side stream)
+  // step 3: the translation launches, t = L-1 .. 0 (two-level launches cover
+  // levels t+1 and t), after the plan's schedule kernel on the side stream
   if (P->sched_ready) CKR(cudaStreamWaitEvent(s, P->sched_ready, 0));
-  for (int t = L - 1; t >= 0; --t) {
-    LevelDims ld = apply_dims_sched(P, t);
+  const int nl = (int)P->launch_t.size();
+  for (int i = 0; i < nl; ++i) {
+    LevelDims ld = apply_dims_sched(P, P->launch_t[i]);
     ld.nrhs = nrhs;
     ld.rs = rs;
-    CKR(launch_translate(P, ld, buf[(t + 1) & 1], buf[t & 1]));
+    CKR(launch_translate(P, ld, buf[i & 1], buf[(i + 1) & 1]));
     tmark(P);
   }
   // step 4: final evaluation, level 0 buffer [A leaves]
-  CKR(launch_final(P, buf[0], ud, 0, 0, P->nx, nrhs, rs, ldu_dev));
+  CKR(launch_final(P, buf[nl & 1], ud, 0, 0, P->nx, nrhs, rs, ldu_dev));
   tmark(P);
   if (u_host) {
     CKR(cudaMemcpy2DAsync(u, ldu * sizeof(double2), ud, ldu_dev * sizeof(double2), P->nx * sizeof(double2), nrhs,
                           cudaMemcpyDeviceToHost, s));
     CKR(cudaStreamSynchronize(s));
   }
-  return finish_timing(P, L - 1);
+  return finish_timing(P, L - 1, &P->launch_t);
 }
 
 extern "C" int sft_apply(sft_plan_t P, const void* f, void* u) {
@@ -1108,6 +1168,25 @@ extern "C" int sft_schedule_bytes(sft_plan_t P, int t, int64_t* bytes, void* dst
   if (dst && n) {
     CKR(cudaMemcpyAsync(dst, P->sched + P->sched_off[t], n, cudaMemcpyDeviceToHost, P->stream));
     CKR(cudaStreamSynchronize(P->stream));
+  }
+  return SFT_OK;
+}
+
+extern "C" int sft_translation_launches(sft_plan_t P, int* n, int* out_level, int* two_level) {
+  if (!P || !n) return fail(SFT_E_ARG, "NULL argument");
+  const int nl = (int)P->launch_t.size();
+  if (P->world != 1) {  // multi-rank: one launch per level, split over the two phases
+    *n = P->L;
+    for (int i = 0; i < P->L; ++i) {
+      if (out_level) out_level[i] = P->L - 1 - i;
+      if (two_level) two_level[i] = 0;
+    }
+    return SFT_OK;
+  }
+  *n = nl;
+  for (int i = 0; i < nl; ++i) {
+    if (out_level) out_level[i] = P->launch_t[i];
+    if (two_level) two_level[i] = P->launch_f2_out[P->launch_t[i]];
   }
   return SFT_OK;
 }

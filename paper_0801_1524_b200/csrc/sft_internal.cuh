@@ -105,7 +105,11 @@ struct sft_plan_s {
   std::vector<int64_t> seg_host;   // host copy of the same
   std::vector<int64_t> peer_off;   // [world] element offset of this rank's segment in each receiver's buffer
   std::vector<double2*> peer;      // [world] receive buffers (fused exchange), empty = use the send buffer
-  // tile schedules of the translation levels (one allocation; offsets per level t)
+  // translation launches of a world-1 apply: output level and whether it is a
+  // two-level launch (levels t+1, t from t+2); schedules per launch
+  std::vector<int> launch_t, launch_f2_out;  // launch order (output levels); f2 flag per output level
+  // tile schedules of the translation launches (one allocation; offsets per launch,
+  // for multi-rank plans per level t)
   unsigned char* sched = nullptr;
   std::vector<size_t> sched_off;
   cudaEvent_t sched_fork = nullptr, sched_ready = nullptr;  // schedule kernel on the side stream
@@ -147,6 +151,13 @@ struct LevelDims {
   double2* peer[kMaxPeers] = {};
   int64_t peer_off[kMaxPeers] = {};
   int64_t peer_seg[kMaxPeers + 1] = {};
+  // two-level (radix-4) launch, 2D: levels t+1 and t from level t+2 in one
+  // pass over super-groups (A'', B); see translate.cu schedule_f2
+  int f2 = 0;
+  const int32_t* cbK1 = nullptr;  // T_K level t+1
+  const uint32_t* mK1 = nullptr;
+  const int32_t* cbX2 = nullptr;  // T_X level L-t-2 (A'' range in ap_lo/ap_hi)
+  const uint32_t* mX2 = nullptr;
   // multi-RHS batch (sft_apply_batch): nrhs independent charge vectors through
   // the same schedule; RHS r of the input / output level lives at in/out + r * rs
   // (elements of the stored type)
@@ -159,6 +170,8 @@ struct LevelDims {
 cudaError_t launch_leaf(const sft_plan_s* P, const double2* f, void* out, int64_t b_lo, int64_t b_hi, int nrhs = 1,
                         int64_t ldf = 0, int64_t ors = 0);
 cudaError_t launch_translate(const sft_plan_s* P, const LevelDims& L, const void* in, void* out);
+// two-level launches available for this plan (2D FP64 single-GPU; SFT_F2=0 disables)
+bool two_level_supported(const sft_plan_s* P);
 // tile schedule of one level (sizes and builder; 0 bytes when the kernel needs none)
 size_t schedule_bytes(const sft_plan_s* P, const LevelDims& L);
 // builds the schedules of nlev levels (dims L[i], destination dst[i]) in one launch

@@ -148,6 +148,15 @@ struct LevelArgs {
   int64_t out_b0, out_nA, out_a0;
   const int64_t* seg;  // [nseg+1] A boundaries at the output level, then [nseg] segment bases
   int nseg;
+  // two-level (radix-4) launch, 2D (f2 = 1): levels t+1 and t in one pass over
+  // super-groups (A'', B), B at level t of T_K, A'' at level L-t-2 of T_X;
+  // cbK/mK: T_K level t, cbK1/mK1: T_K level t+1, cbX/mX: T_X level L-t-1,
+  // cbX2/mX2: T_X level L-t-2; input = level t+2 pairs, output = level t
+  int f2;
+  const int32_t* cbK1;
+  const uint32_t* mK1;
+  const int32_t* cbX2;
+  const uint32_t* mX2;
 };
 
 struct TransArgs : LevelArgs {
@@ -575,7 +584,10 @@ struct Sched {
 // REV (2D only): the axes are processed in the order 0, 1 instead of 1, 0.
 // Pass over axis 0 first: tasks by beta_1 (slots (0,b1), (1,b1)); then axis 1
 // (last): tasks by alpha_0 (slots (a0,0), (a0,1)), outputs (a0,0), (a0,1).
-template <int D, int P, int G, int PS, int AX, bool LAST, bool REV = false>
+// TR (two-level launch, second level): group j's child slot c lives at stage
+// slot c * NS + j (the first level left pair (A'_j, B_c) in slot j of virtual
+// group c), so slot pairs are NS slots further apart
+template <int D, int P, int G, int PS, int AX, bool LAST, bool REV = false, bool TR = false>
 __device__ __forceinline__ void schedule_pass(const LevelArgs& a, const GroupMeta& m, bool valid, bool write_cnt,
                                               int* cnt, TaskRec* out) {
   constexpr int PD = PS;  // offsets in units of the array stride
@@ -629,7 +641,9 @@ __device__ __forceinline__ void schedule_pass(const LevelArgs& a, const GroupMet
       for (int as = 0; as < (1 << (D - 1 - AX)); ++as) {
         if (!(PAs >> as & 1)) continue;
         TaskRec t;
-        t.x = (uint32_t)(((lane % G) * NS + ((bp << (D - AX)) | as)) * PD);
+        const int sl = (bp << (D - AX)) | as;
+        t.x = TR ? (uint32_t)((((lane % G) & ~(NS - 1)) * NS + sl * NS + (lane % NS)) * PD)
+                 : (uint32_t)(((lane % G) * NS + sl) * PD);
         t.cls = cls;
         t.o0 = t.o1 = ~0u;
         if (LAST) {
@@ -675,12 +689,76 @@ __device__ __forceinline__ void schedule_pass(const LevelArgs& a, const GroupMet
   }
 }
 
+// Two-level tile (2D, f2): lane j of the G-lane segment is virtual group
+// v = j (super-group sg = j / 4 of the tile, child c = j % 4).  First level
+// (levels t+2 -> t+1): group (A'', B_c) with its children B_cc at level t+2 in
+// slots v*4 + c'; passes axis 1 (list 1) and axis 0 (list 2), in place, so
+// slot v*4 + alpha ends up holding pair (A'_alpha, B_c).  Second level
+// (t+1 -> t): group (A'_alpha, B) for alpha = j % 4 reads slots sg*16 + c*4 +
+// alpha (TR); passes axis 1 (list 3, in place) and axis 0 (list 0, to HBM).
+// Absent B_c leave zero-filled slots (they contribute nothing); absent A'_alpha
+// have no second-level group.
+template <int D, int P, int G, int PS>
+__device__ __forceinline__ void schedule_f2(const LevelArgs& a, int64_t tile, bool tv, unsigned char* b) {
+  using SC = Sched<D, P, G>;
+  constexpr int NS = 1 << D;
+  const int lane = threadIdx.x & 31;
+  const int j = lane % G;
+  const int64_t sgi = tile * (G / NS) + j / NS;  // super-group index
+  const int cj = j % NS;
+  const bool sv = tv && sgi * NS < a.ngroups;
+  GroupMeta m1, m2;
+  m1.iB = m1.iAp = m2.iB = m2.iAp = 0;
+  m1.cbK = m1.cbX = m2.cbK = m2.cbX = 0;
+  m1.mB = m1.mA = m2.mB = m2.mA = 0;
+  bool v1 = false, v2 = false;
+  if (sv) {
+    const uint32_t nap = (uint32_t)a.nAp_grp;
+    const int64_t iB = a.b_lo + sgi / nap, iA2 = a.ap_lo + sgi % nap;
+    const uint32_t mBB = a.mK[iB], mA2 = a.mX2[iA2];
+    const int32_t cbB = a.cbK[iB], cbA2 = a.cbX2[iA2];
+    // first level: (A'', B_c), c = cj
+    v1 = (mBB >> cj) & 1u;
+    if (v1) {
+      const int64_t iBc = cbB + __popc(mBB & ((1u << cj) - 1u));
+      m1.iB = iBc;
+      m1.iAp = iA2;
+      m1.cbK = a.cbK1[iBc];
+      m1.mB = a.mK1[iBc];
+      m1.cbX = cbA2;
+      m1.mA = mA2;
+    }
+    // second level: (A'_alpha, B), alpha = cj
+    v2 = (mA2 >> cj) & 1u;
+    if (v2) {
+      const int64_t iAp = cbA2 + __popc(mA2 & ((1u << cj) - 1u));
+      m2.iB = iB;
+      m2.iAp = iAp;
+      m2.cbK = cbB;
+      m2.mB = mBB;
+      m2.cbX = a.cbX[iAp];
+      m2.mA = a.mX[iAp];
+    }
+  }
+  if (tv) {
+    const int64_t pin0 = ((int64_t)m1.cbK - a.in_b0) * a.in_nA + (m1.iAp - a.in_a0);
+    reinterpret_cast<uint2*>(b + SC::HDR)[j] = v1 ? make_uint2((uint32_t)pin0, m1.mB) : make_uint2(0u, 0u);
+  }
+  int* cnt = reinterpret_cast<int*>(b);
+  TaskRec* tk = reinterpret_cast<TaskRec*>(b + SC::HDR + SC::GRP);
+  schedule_pass<D, P, G, PS, 1, false>(a, m1, v1, tv, cnt + 3, tk + SC::MAXT);
+  schedule_pass<D, P, G, PS, 0, false>(a, m1, v1, tv, cnt + 6, tk + 2 * SC::MAXT);
+  schedule_pass<D, P, G, PS, 1, false, false, true>(a, m2, v2, tv, cnt + 9, tk + 3 * SC::MAXT);
+  schedule_pass<D, P, G, PS, 0, true, false, true>(a, m2, v2, tv, cnt, tk);
+}
+
 // All levels of a plan in one launch: level lv owns the global tiles
 // [tile0[lv], tile0[lv+1]) and writes its blocks at dst[lv].
+constexpr int kSchedChunk = 16;  // levels per schedule launch (the struct is one < 4 KB kernel parameter)
 struct SchedLevels {
-  LevelArgs a[kMaxLevels];  // (slim: the whole struct is one < 4 KB kernel parameter)
-  unsigned char* dst[kMaxLevels];
-  int64_t tile0[kMaxLevels + 1];
+  LevelArgs a[kSchedChunk];
+  unsigned char* dst[kSchedChunk];
+  int64_t tile0[kSchedChunk + 1];
   int nlev;
 };
 static_assert(sizeof(SchedLevels) <= 4096, "k_schedule's parameter must stay within 4 KB");
@@ -700,6 +778,12 @@ __global__ __launch_bounds__(128) void k_schedule(const __grid_constant__ SchedL
   const int64_t tile = T - S.tile0[lv];
   const bool tv = T < S.tile0[S.nlev];
   unsigned char* b = S.dst[lv] + (tv ? tile : 0) * SC::BLK;
+  if constexpr (D == 2 && G % 4 == 0) {
+    if (a.f2) {
+      schedule_f2<D, P, G, PS>(a, tile, tv, b);
+      return;
+    }
+  }
   const int64_t g = tile * G + j;
   const bool valid = tv && g < a.ngroups;
   GroupMeta m;
@@ -812,7 +896,10 @@ template <int D, int P>
 struct NsubCfg {
   static constexpr int v = (D == 3 && P == 5) ? SFT_NSUB35 : SFT_NSUB_OTHER;
 };
-template <int D, int P, int G, int NC, int AX, bool LAST, int LIST = AX, typename E = double2, bool FUSED = false>
+// MUL: slot-pair distance in units of (1 << SH) slots -- NS for the second
+// level of a two-level tile (transposed slots), 1 otherwise
+template <int D, int P, int G, int NC, int AX, bool LAST, int LIST = AX, typename E = double2, bool FUSED = false,
+          int MUL = 1>
 __device__ __forceinline__ void consumer_pass(const TransArgs& a, E* __restrict__ sb,
                                               const unsigned char* __restrict__ blk,
                                               const LaneOps<P, TailSmem<D>::v>& op,
@@ -835,7 +922,7 @@ __device__ __forceinline__ void consumer_pass(const TransArgs& a, E* __restrict_
   int off[S::NK];
 #pragma unroll
   for (int kk = 0; kk < S::NK; ++kk)
-    off[kk] = (LaneOps<P, true>::bk(kk, lane) == 1 ? (1 << SH) * PD : 0) + LaneOps<P, true>::lk(kk, lane) * STR;
+    off[kk] = (LaneOps<P, true>::bk(kk, lane) == 1 ? (1 << SH) * PD * MUL : 0) + LaneOps<P, true>::lk(kk, lane) * STR;
   // delta columns of this lane's outputs m = 4n + c: child-0 element 2m and
   // child-1 element 2m - (P-1), clamped into range (their coefficient is 0 there)
   int doff[S::NT][2];
@@ -843,7 +930,7 @@ __device__ __forceinline__ void consumer_pass(const TransArgs& a, E* __restrict_
   for (int n = 0; n < S::NT; ++n) {
     const int m = 4 * n + c;
     doff[n][0] = min(2 * m, P - 1) * STR;
-    doff[n][1] = (1 << SH) * PD + min(max(2 * m - (P - 1), 0), P - 1) * STR;  // in range: 0 * finite = 0
+    doff[n][1] = (1 << SH) * PD * MUL + min(max(2 * m - (P - 1), 0), P - 1) * STR;  // in range: 0 * finite = 0
   }
   // units of NSUB super-tiles go round-robin over the warps, continuing from
   // where the previous pass stopped (rot), so that the extra unit of a pass
@@ -896,7 +983,7 @@ __device__ __forceinline__ void consumer_pass(const TransArgs& a, E* __restrict_
         o1[u] = d.o1 != ~0u ? gout + d.o1 + ebase : nullptr;
       } else {
         o0[u] = vrow ? sb + xo : nullptr;
-        o1[u] = vrow ? sb + xo + (1 << SH) * PD : nullptr;
+        o1[u] = vrow ? sb + xo + (1 << SH) * PD * MUL : nullptr;
       }
 #endif
     }
@@ -915,7 +1002,7 @@ __device__ __forceinline__ void consumer_pass(const TransArgs& a, E* __restrict_
         aim[u][n][1] = fma(op.dl[n][3], x1.y, op.dl[n][1] * x0.y);
       }
       if (S::TAIL) {  // m = P-1: child-1 element P-1 only (coefficients non-zero on lane%4 == 0)
-        const double2 x1 = ElemT<E>::ld(x[u][(1 << SH) * PD + (P - 1) * STR]);
+        const double2 x1 = ElemT<E>::ld(x[u][(1 << SH) * PD * MUL + (P - 1) * STR]);
         tl[u][0] = op.dt[0] * x1.x;
         tl[u][1] = op.dt[S::TAIL ? 1 : 0] * x1.x;
         tl[u][2] = op.dt[0] * x1.y;
@@ -1168,12 +1255,13 @@ __device__ __forceinline__ void ws_producer(const TransArgs& a, const unsigned c
 // NC + 1 warps' registers (one more CTA per SM at 2D p = 9).  Non-skewed
 // pipeline only.
 template <int D, int P, int G, int NC, int NST, int MINB, typename E = double2, bool FUSED = false,
-          bool BATCH = false, bool SELF = false>
+          bool BATCH = false, bool SELF = false, bool F2 = false>
 __global__ __launch_bounds__((NC + (SELF ? 0 : 1)) * 32, MINB) void k_translate_ws(TransArgs a,
                                                                                   const double* __restrict__ frag,
                                                                                   const unsigned char* __restrict__ sched,
                                                                                   int64_t ntiles) {
   static_assert(!SELF || D != 2 || NST < 3, "the self-fed mode has no skewed pipeline");
+  static_assert(!F2 || (D == 2 && NST < 3 && G % 4 == 0 && !FUSED), "two-level tiles: 2D, unskewed, G = 4k");
   using SC = Sched<D, P, G>;
   constexpr int PD = StrideT<E, Pow<P, D>::v>::v;  // array stride (elements)
   constexpr int NS = 1 << D;
@@ -1250,7 +1338,7 @@ __global__ __launch_bounds__((NC + (SELF ? 0 : 1)) * 32, MINB) void k_translate_
   // work items w = tile * nrhs + r; the output of RHS r goes to out + r * rs
   const int64_t nwork = BATCH ? ntiles * a.nrhs : ntiles;
   auto ooff = [&](int64_t w_) { return BATCH ? (w_ % a.nrhs) * a.rs : (int64_t)0; };
-  if constexpr (D == 2 && NST >= 3 && !SELF) {
+  if constexpr (D == 2 && NST >= 3 && !SELF && !F2) {
     int64_t tile = blockIdx.x;
     if (tile < nwork) {
       mbar_wait(smem_u32(&full[0]), 0);
@@ -1288,7 +1376,17 @@ __global__ __launch_bounds__((NC + (SELF ? 0 : 1)) * 32, MINB) void k_translate_
       mbar_wait(smem_u32(&full[s]), ph);
       INSTR_ADD(4, tf0);
       E* sb = ring + s * STAGE;
-      if constexpr (D == 2) {
+      if constexpr (F2) {
+        // two-level tile: first level (lists 1, 2) in place, second level on
+        // the transposed slots (lists 3, 0), the last pass to HBM
+        consumer_pass<D, P, G, NC, 1, false, 1, E>(a, sb, blk[s], op, rot);
+        consumer_sync<NC * 32>();
+        consumer_pass<D, P, G, NC, 0, false, 2, E>(a, sb, blk[s], op, rot);
+        consumer_sync<NC * 32>();
+        consumer_pass<D, P, G, NC, 1, false, 3, E, false, 1 << D>(a, sb, blk[s], op, rot);
+        consumer_sync<NC * 32>();
+        consumer_pass<D, P, G, NC, 0, true, 0, E, false, 1 << D>(a, sb, blk[s], op, rot, ooff(w));
+      } else if constexpr (D == 2) {
         INSTR_T0(t1);
         first2d(sb, blk[s]);
         INSTR_ADD(5, t1);
@@ -1797,6 +1895,12 @@ static TransArgs make_args(const LevelDims& L, const double2* in, double2* out) 
   a.out_a0 = L.out_a0;
   a.seg = L.seg;
   a.nseg = L.nseg;
+  a.f2 = L.f2;
+  a.cbK1 = L.cbK1;
+  a.mK1 = L.mK1;
+  a.cbX2 = L.cbX2;
+  a.mX2 = L.mX2;
+  if (L.f2) a.ngroups *= 4;  // virtual groups: the 2^d = 4 first-level groups of each super-group
   a.npeer = L.npeer;
   for (int q = 0; q < kMaxPeers; ++q) {
     a.peer[q] = L.peer[q];
@@ -1872,6 +1976,8 @@ static cudaError_t launch_translate_t(const sft_plan_s* Pl, const LevelDims& L, 
   if (a.ngroups <= 0) return cudaSuccess;
   if (a.nrhs < 1 || (a.nrhs > 1 && (a.npeer > 0 || (Pl->prec == 1 ? f32_ffma() : translate_kernel_choice() != 0))))
     return cudaErrorInvalidValue;  // batches run on the warp-specialised DMMA kernel only
+  if (a.f2 && (Pl->prec != 0 || translate_kernel_choice() != 0 || a.npeer > 0))
+    return cudaErrorInvalidValue;  // two-level launches: FP64 warp-specialised kernel only
   if (Pl->prec == 1 && !f32_ffma()) {
     // FP32 storage, FP64 arithmetic on the tensor cores (same kernel as FP64)
     constexpr int G = F32WsCfg<D, P>::G, NC = F32WsCfg<D, P>::NC, NST = F32WsCfg<D, P>::NST,
@@ -1939,6 +2045,28 @@ static cudaError_t launch_translate_t(const sft_plan_s* Pl, const LevelDims& L, 
       }
       launch_pdl(k_translate_ws<D, P, G, NC, NST, MB, double2, true>, (unsigned)grid, (NC + 1) * 32, smem,
                  Pl->stream, a, frag, L.sched, ntiles);
+    } else if (a.f2) {
+      // two-level launch (2D, G = 4k, unskewed configurations)
+      if constexpr (D == 2 && G % 4 == 0 && NST < 3) {
+        static bool fattr2 = false;
+        if (!fattr2) {
+          cudaError_t e = cudaFuncSetAttribute(k_translate_ws<D, P, G, NC, NST, MB, double2, false, false, false, true>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+          if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(k_translate_ws<D, P, G, NC, NST, MB, double2, false, true, false, true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+          if (e != cudaSuccess) return e;
+          fattr2 = true;
+        }
+        if (a.nrhs > 1)
+          launch_pdl(k_translate_ws<D, P, G, NC, NST, MB, double2, false, true, false, true>, (unsigned)grid,
+                     (NC + 1) * 32, smem, Pl->stream, a, frag, L.sched, ntiles);
+        else
+          launch_pdl(k_translate_ws<D, P, G, NC, NST, MB, double2, false, false, false, true>, (unsigned)grid,
+                     (NC + 1) * 32, smem, Pl->stream, a, frag, L.sched, ntiles);
+      } else {
+        return cudaErrorInvalidValue;
+      }
     } else if (a.nrhs > 1) {
       static bool battr = false;
       if (!battr) {
@@ -1986,7 +2114,7 @@ static cudaError_t launch_translate_t(const sft_plan_s* Pl, const LevelDims& L, 
 
 template <int D, int P, int G>
 static size_t schedule_bytes_g(const LevelDims& L) {
-  const int64_t ng = (L.b_hi - L.b_lo) * (L.ap_hi - L.ap_lo);
+  const int64_t ng = (L.b_hi - L.b_lo) * (L.ap_hi - L.ap_lo) * (L.f2 ? 4 : 1);  // f2: virtual groups
   if (ng <= 0) return 0;
   return (size_t)((ng + G - 1) / G) * Sched<D, P, G>::BLK;
 }
@@ -2003,24 +2131,28 @@ static size_t schedule_bytes_t(const sft_plan_s* Pl, const LevelDims& L) {
 template <int D, int P, int G, int PS>
 static cudaError_t launch_schedule_g(const sft_plan_s* Pl, const LevelDims* L, int nlev, unsigned char* const* dst,
                                      cudaStream_t st) {
-  SchedLevels S;
-  int64_t t0 = 0;
-  S.nlev = 0;
-  for (int i = 0; i < nlev && S.nlev < kMaxLevels; ++i) {
-    TransArgs a = make_args(L[i], nullptr, nullptr);
-    if (a.ngroups <= 0) continue;
-    S.a[S.nlev] = a;
-    S.dst[S.nlev] = dst[i];
+  for (int c0 = 0; c0 < nlev; c0 += kSchedChunk) {
+    SchedLevels S;
+    int64_t t0 = 0;
+    S.nlev = 0;
+    for (int i = c0; i < nlev && i < c0 + kSchedChunk; ++i) {
+      TransArgs a = make_args(L[i], nullptr, nullptr);
+      if (a.ngroups <= 0) continue;
+      S.a[S.nlev] = a;
+      S.dst[S.nlev] = dst[i];
+      S.tile0[S.nlev] = t0;
+      t0 += (a.ngroups + G - 1) / G;
+      ++S.nlev;
+    }
     S.tile0[S.nlev] = t0;
-    t0 += (a.ngroups + G - 1) / G;
-    ++S.nlev;
+    if (S.nlev == 0) continue;
+    const int64_t nwarps = (t0 + 32 / G - 1) / (32 / G);
+    k_schedule<D, P, G, PS><<<(unsigned)((nwarps + 3) / 4), 128, 0, st>>>(S);
+    count_launch();
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
   }
-  S.tile0[S.nlev] = t0;
-  if (S.nlev == 0) return cudaSuccess;
-  const int64_t nwarps = (t0 + 32 / G - 1) / (32 / G);
-  k_schedule<D, P, G, PS><<<(unsigned)((nwarps + 3) / 4), 128, 0, st>>>(S);
-  count_launch();
-  return cudaGetLastError();
+  return cudaSuccess;
 }
 
 template <int D, int P>
@@ -2037,7 +2169,7 @@ static cudaError_t launch_schedule_t(const sft_plan_s* Pl, const LevelDims* L, i
 template <int D, int P>
 static cudaError_t check_schedule_t(const sft_plan_s* Pl, const LevelDims& L, const unsigned char* sched,
                                    int64_t in_pairs, int64_t out_pairs, int* err) {
-  if (translate_kernel_choice() != 0 || Pl->prec != 0) return cudaSuccess;
+  if (translate_kernel_choice() != 0 || Pl->prec != 0 || L.f2) return cudaSuccess;  // (single-level layout only)
   constexpr int G = WsCfg<D, P>::G;
   TransArgs a = make_args(L, nullptr, nullptr);
   if (a.ngroups <= 0) return cudaSuccess;
@@ -2068,6 +2200,19 @@ cudaError_t launch_schedule(const sft_plan_s* Pl, const LevelDims* L, int nlev, 
                             cudaStream_t st) {
   SFT_DISPATCH(Pl->d, Pl->p, return (launch_schedule_t<D, P>(Pl, L, nlev, dst, st)));
   return cudaSuccess;
+}
+
+bool two_level_supported(const sft_plan_s* Pl) {
+  if (Pl->prec != 0 || Pl->world != 1 || translate_kernel_choice() != 0) return false;
+  const char* e = getenv("SFT_F2");
+  if (e && e[0] == '0') return false;
+  if (Pl->d != 2) return false;
+  switch (Pl->p) {
+    case 5: return WsCfg<2, 5>::G % 4 == 0 && WsCfg<2, 5>::NST < 3;
+    case 7: return WsCfg<2, 7>::G % 4 == 0 && WsCfg<2, 7>::NST < 3;
+    case 9: return WsCfg<2, 9>::G % 4 == 0 && WsCfg<2, 9>::NST < 3;
+  }
+  return false;
 }
 
 cudaError_t launch_translate(const sft_plan_s* Pl, const LevelDims& L, const void* in, void* out) {
