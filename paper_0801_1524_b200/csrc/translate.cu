@@ -615,7 +615,8 @@ __device__ __forceinline__ void schedule_pass(const LevelArgs& a, const GroupMet
         cls = b1set;
         slot0 = v << 1;
       }
-      t.x = (uint32_t)(((lane % G) * NS + slot0) * PD);
+      t.x = TR ? (uint32_t)((((lane % G) & ~(NS - 1)) * NS + slot0 * NS + (lane % NS)) * PD)
+               : (uint32_t)(((lane % G) * NS + slot0) * PD);
       t.cls = cls;
       t.o0 = t.o1 = ~0u;
       if (LAST) {
@@ -689,13 +690,45 @@ __device__ __forceinline__ void schedule_pass(const LevelArgs& a, const GroupMet
   }
 }
 
+// 2D axis order per group (from its own masks only, so identical for any
+// partition of the work and for single- or two-level launches): the one with
+// fewer MMA k-steps over its fiber rows (rows of a task with one live child
+// skip that child's k-steps).  true = axis 0 first.
+template <int P>
+__device__ __forceinline__ bool reversed_order(const GroupMeta& m) {
+#ifdef SFT_FIXED_ORDER
+  return false;
+#else
+  constexpr int D = 2;
+  using S = MmaShape<P>;
+  constexpr int KB = S::NK, K0 = S::K0_HI, K1 = S::NK - S::K1_LO;
+  auto kc = [](uint32_t cls) { return cls == 3 ? KB : (cls == 1 ? K0 : (cls == 2 ? K1 : 0)); };
+  int cf = 0, cr = 0;  // default (axis 1 first) / reversed
+  const uint32_t mB = m.mB, mA = m.mA;
+  const uint32_t b0set = proj_hi<D>(mB, 1), b1set = proj_lo<D>(mB, 1);
+  const int na1 = __popc(proj_lo<D>(mA, 1)), na0 = __popc(proj_hi<D>(mA, 1));
+  for (int v = 0; v < 2; ++v) {
+    if (b0set >> v & 1) cf += kc((mB >> (2 * v)) & 3u);
+    if (b1set >> v & 1) cr += kc((mB >> v & 1u) | ((mB >> (2 + v) & 1u) << 1));
+  }
+  cf += na1 * kc(b0set);
+  cr += na0 * kc(b1set);
+  return cr < cf;
+#endif
+}
+
 // Two-level tile (2D, f2): lane j of the G-lane segment is virtual group
-// v = j (super-group sg = j / 4 of the tile, child c = j % 4).  First level
-// (levels t+2 -> t+1): group (A'', B_c) with its children B_cc at level t+2 in
-// slots v*4 + c'; passes axis 1 (list 1) and axis 0 (list 2), in place, so
-// slot v*4 + alpha ends up holding pair (A'_alpha, B_c).  Second level
-// (t+1 -> t): group (A'_alpha, B) for alpha = j % 4 reads slots sg*16 + c*4 +
-// alpha (TR); passes axis 1 (list 3, in place) and axis 0 (list 0, to HBM).
+// v = j (super-group sg = j / 4 of the tile, child c = j % 4).  Two schedule
+// blocks per tile, each in the single-level format (lists 1/2 first passes,
+// 0/3 second passes, per-group axis order as in single-level launches, so
+// the arithmetic and the bits are the same):
+//   block 0, first level (levels t+2 -> t+1): group (A'', B_c), its children
+//     B_cc at level t+2 in slots v*4 + c', both passes in place, leaving pair
+//     (A'_alpha, B_c) in slot v*4 + alpha; block 0 also holds the group
+//     records the producer loads from;
+//   block 1, second level (t+1 -> t): group (A'_alpha, B), alpha = j % 4,
+//     reading its children on the transposed slots sg*16 + c*4 + alpha (TR),
+//     the second pass to HBM.
 // Absent B_c leave zero-filled slots (they contribute nothing); absent A'_alpha
 // have no second-level group.
 template <int D, int P, int G, int PS>
@@ -740,16 +773,25 @@ __device__ __forceinline__ void schedule_f2(const LevelArgs& a, int64_t tile, bo
       m2.mA = a.mX[iAp];
     }
   }
+  unsigned char* b1 = b + SC::BLK;
   if (tv) {
     const int64_t pin0 = ((int64_t)m1.cbK - a.in_b0) * a.in_nA + (m1.iAp - a.in_a0);
     reinterpret_cast<uint2*>(b + SC::HDR)[j] = v1 ? make_uint2((uint32_t)pin0, m1.mB) : make_uint2(0u, 0u);
+    reinterpret_cast<uint2*>(b1 + SC::HDR)[j] = make_uint2(0u, 0u);
   }
-  int* cnt = reinterpret_cast<int*>(b);
-  TaskRec* tk = reinterpret_cast<TaskRec*>(b + SC::HDR + SC::GRP);
-  schedule_pass<D, P, G, PS, 1, false>(a, m1, v1, tv, cnt + 3, tk + SC::MAXT);
-  schedule_pass<D, P, G, PS, 0, false>(a, m1, v1, tv, cnt + 6, tk + 2 * SC::MAXT);
-  schedule_pass<D, P, G, PS, 1, false, false, true>(a, m2, v2, tv, cnt + 9, tk + 3 * SC::MAXT);
-  schedule_pass<D, P, G, PS, 0, true, false, true>(a, m2, v2, tv, cnt, tk);
+  const bool r1 = v1 && reversed_order<P>(m1), r2 = v2 && reversed_order<P>(m2);
+  int* c0 = reinterpret_cast<int*>(b);
+  TaskRec* k0 = reinterpret_cast<TaskRec*>(b + SC::HDR + SC::GRP);
+  schedule_pass<D, P, G, PS, 1, false>(a, m1, v1 && !r1, tv, c0 + 3, k0 + SC::MAXT);
+  schedule_pass<D, P, G, PS, 0, false>(a, m1, v1 && !r1, tv, c0, k0);
+  schedule_pass<D, P, G, PS, 0, false, true>(a, m1, v1 && r1, tv, c0 + 6, k0 + 2 * SC::MAXT);
+  schedule_pass<D, P, G, PS, 1, false, true>(a, m1, v1 && r1, tv, c0 + 9, k0 + 3 * SC::MAXT);
+  int* c1 = reinterpret_cast<int*>(b1);
+  TaskRec* k1 = reinterpret_cast<TaskRec*>(b1 + SC::HDR + SC::GRP);
+  schedule_pass<D, P, G, PS, 1, false, false, true>(a, m2, v2 && !r2, tv, c1 + 3, k1 + SC::MAXT);
+  schedule_pass<D, P, G, PS, 0, true, false, true>(a, m2, v2 && !r2, tv, c1, k1);
+  schedule_pass<D, P, G, PS, 0, false, true, true>(a, m2, v2 && r2, tv, c1 + 6, k1 + 2 * SC::MAXT);
+  schedule_pass<D, P, G, PS, 1, true, true, true>(a, m2, v2 && r2, tv, c1 + 9, k1 + 3 * SC::MAXT);
 }
 
 // All levels of a plan in one launch: level lv owns the global tiles
@@ -777,13 +819,13 @@ __global__ __launch_bounds__(128) void k_schedule(const __grid_constant__ SchedL
   const LevelArgs& a = S.a[lv];
   const int64_t tile = T - S.tile0[lv];
   const bool tv = T < S.tile0[S.nlev];
-  unsigned char* b = S.dst[lv] + (tv ? tile : 0) * SC::BLK;
   if constexpr (D == 2 && G % 4 == 0) {
     if (a.f2) {
-      schedule_f2<D, P, G, PS>(a, tile, tv, b);
+      schedule_f2<D, P, G, PS>(a, tile, tv, S.dst[lv] + (tv ? tile : 0) * (2 * SC::BLK));
       return;
     }
   }
+  unsigned char* b = S.dst[lv] + (tv ? tile : 0) * SC::BLK;
   const int64_t g = tile * G + j;
   const bool valid = tv && g < a.ngroups;
   GroupMeta m;
@@ -807,29 +849,7 @@ __global__ __launch_bounds__(128) void k_schedule(const __grid_constant__ SchedL
   int* cnt = reinterpret_cast<int*>(b);  // written by the first lane of each valid tile only
   TaskRec* tk = reinterpret_cast<TaskRec*>(b + SC::HDR + SC::GRP);
   if constexpr (D == 2) {
-    // axis order per group (from its own masks only, so identical for any
-    // partition of the work): the one with fewer MMA k-steps over its fiber
-    // rows (rows of a task with one live child skip that child's k-steps)
-    using S = MmaShape<P>;
-    constexpr int KB = S::NK, K0 = S::K0_HI, K1 = S::NK - S::K1_LO;
-    auto kc = [](uint32_t cls) { return cls == 3 ? KB : (cls == 1 ? K0 : (cls == 2 ? K1 : 0)); };
-    int cf = 0, cr = 0;  // default (axis 1 first) / reversed
-    if (valid) {
-      const uint32_t mB = m.mB, mA = m.mA;
-      const uint32_t b0set = proj_hi<D>(mB, 1), b1set = proj_lo<D>(mB, 1);
-      const int na1 = __popc(proj_lo<D>(mA, 1)), na0 = __popc(proj_hi<D>(mA, 1));
-      for (int v = 0; v < 2; ++v) {
-        if (b0set >> v & 1) cf += kc((mB >> (2 * v)) & 3u);
-        if (b1set >> v & 1) cr += kc((mB >> v & 1u) | ((mB >> (2 + v) & 1u) << 1));
-      }
-      cf += na1 * kc(b0set);
-      cr += na0 * kc(b1set);
-    }
-#ifdef SFT_FIXED_ORDER
-    const bool rev = false;
-#else
-    const bool rev = cr < cf;
-#endif
+    const bool rev = valid && reversed_order<P>(m);
     schedule_pass<D, P, G, PS, 1, false>(a, m, valid && !rev, tv, cnt + 3, tk + SC::MAXT);
     schedule_pass<D, P, G, PS, 0, true>(a, m, valid && !rev, tv, cnt, tk);
     schedule_pass<D, P, G, PS, 0, false, true>(a, m, valid && rev, tv, cnt + 6, tk + 2 * SC::MAXT);
@@ -1133,10 +1153,11 @@ __device__ __forceinline__ void load_lane_ops(LaneOps<P, TS>& op, const double* 
 // unmasked), arm full[s] with the byte count, bulk-copy (1-D TMA) the tile's
 // schedule block and every present child array.  gr = this lane's group
 // record (first child pair index, child mask) for lane < G.
-template <int D, int P, int G, int NST, typename E, int PS, bool BATCH>
+// NB: schedule blocks per tile (2 for a two-level tile: one per level)
+template <int D, int P, int G, int NST, typename E, int PS, bool BATCH, int NB = 1>
 __device__ __forceinline__ void ws_issue(const TransArgs& a, const unsigned char* __restrict__ sched, int64_t w,
-                                         int64_t tile, uint2 gr, E* ring, unsigned char (*blk)[Sched<D, P, G>::BLK],
-                                         uint64_t* full, int s) {
+                                         int64_t tile, uint2 gr, E* ring,
+                                         unsigned char (*blk)[Sched<D, P, G>::BLK * NB], uint64_t* full, int s) {
   using SC = Sched<D, P, G>;
   constexpr int PD = PS;  // stage and HBM arrays have stride PS elements of type E
   constexpr int NS = 1 << D;
@@ -1162,12 +1183,12 @@ __device__ __forceinline__ void ws_issue(const TransArgs& a, const unsigned char
   }
   if (lane == 0) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&full[s])),
-                 "r"(nbytes + (uint32_t)SC::BLK)
+                 "r"(nbytes + (uint32_t)(SC::BLK * NB))
                  : "memory");
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
             smem_u32(&blk[s][0])),
-        "l"(sched + tile * SC::BLK), "r"((uint32_t)SC::BLK), "r"(smem_u32(&full[s]))
+        "l"(sched + tile * (SC::BLK * NB)), "r"((uint32_t)(SC::BLK * NB)), "r"(smem_u32(&full[s]))
         : "memory");
   }
   __syncwarp();
@@ -1192,17 +1213,17 @@ __device__ __forceinline__ void ws_issue(const TransArgs& a, const unsigned char
   }
 }
 
-template <int D, int P, int G>
+template <int D, int P, int G, int NB = 1>
 __device__ __forceinline__ uint2 ws_group_record(const unsigned char* __restrict__ sched, int64_t tile, bool ok) {
   using SC = Sched<D, P, G>;
   const int lane = threadIdx.x & 31;
-  return (ok && lane < G) ? __ldg(reinterpret_cast<const uint2*>(sched + tile * SC::BLK + SC::HDR) + lane)
+  return (ok && lane < G) ? __ldg(reinterpret_cast<const uint2*>(sched + tile * (SC::BLK * NB) + SC::HDR) + lane)
                           : make_uint2(0u, 0u);
 }
 
-template <int D, int P, int G, int NST, typename E = double2, int PS = Pow<P, D>::v, bool BATCH = false>
+template <int D, int P, int G, int NST, typename E = double2, int PS = Pow<P, D>::v, bool BATCH = false, int NB = 1>
 __device__ __forceinline__ void ws_producer(const TransArgs& a, const unsigned char* __restrict__ sched, int64_t ntiles,
-                                            E* ring, unsigned char (*blk)[Sched<D, P, G>::BLK], uint64_t* full,
+                                            E* ring, unsigned char (*blk)[Sched<D, P, G>::BLK * NB], uint64_t* full,
                                             uint64_t* empty) {
   INSTR_T0(tp0);
   int s = 0;
@@ -1212,7 +1233,7 @@ __device__ __forceinline__ void ws_producer(const TransArgs& a, const unsigned c
   const int64_t nwork = ntiles * nr;
   int64_t w = blockIdx.x;
   int64_t tile = BATCH ? w / nr : w;
-  uint2 gr = ws_group_record<D, P, G>(sched, tile, w < nwork);
+  uint2 gr = ws_group_record<D, P, G, NB>(sched, tile, w < nwork);
   // programmatic dependent launch: everything above (schedule reads, barrier
   // init, the consumers' operand loads) overlaps the previous level's tail;
   // the previous level's output (our input) and input (our output buffer)
@@ -1221,12 +1242,12 @@ __device__ __forceinline__ void ws_producer(const TransArgs& a, const unsigned c
   for (int i = 0; w < nwork; ++i) {
     const int64_t wn = w + gridDim.x;
     const int64_t next = BATCH ? wn / nr : wn;
-    const uint2 gn = ws_group_record<D, P, G>(sched, next, wn < nwork);
+    const uint2 gn = ws_group_record<D, P, G, NB>(sched, next, wn < nwork);
     INSTR_T0(tw0);
     if (i >= NST) mbar_wait_sleep(smem_u32(&empty[s]), ph ^ 1u);
     INSTR_ADD(1, tw0);
     INSTR_T0(tb0);
-    ws_issue<D, P, G, NST, E, PS, BATCH>(a, sched, w, tile, gr, ring, blk, full, s);
+    ws_issue<D, P, G, NST, E, PS, BATCH, NB>(a, sched, w, tile, gr, ring, blk, full, s);
     INSTR_ADD(2, tb0);
     gr = gn;
     w = wn;
@@ -1261,14 +1282,15 @@ __global__ __launch_bounds__((NC + (SELF ? 0 : 1)) * 32, MINB) void k_translate_
                                                                                   const unsigned char* __restrict__ sched,
                                                                                   int64_t ntiles) {
   static_assert(!SELF || D != 2 || NST < 3, "the self-fed mode has no skewed pipeline");
-  static_assert(!F2 || (D == 2 && NST < 3 && G % 4 == 0 && !FUSED), "two-level tiles: 2D, unskewed, G = 4k");
+  static_assert(!F2 || (D == 2 && NST < 3 && G % 4 == 0 && !FUSED && !SELF), "two-level tiles: 2D, unskewed, G = 4k");
   using SC = Sched<D, P, G>;
   constexpr int PD = StrideT<E, Pow<P, D>::v>::v;  // array stride (elements)
   constexpr int NS = 1 << D;
   constexpr int STAGE = G * NS * PD;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   E* ring = reinterpret_cast<E*>(smem_raw);  // [NST][G][NS][PD]
-  __shared__ __align__(128) unsigned char blk[NST][SC::BLK];
+  constexpr int NB = F2 ? 2 : 1;  // schedule blocks per tile
+  __shared__ __align__(128) unsigned char blk[NST][SC::BLK * NB];
   __shared__ __align__(8) uint64_t full[NST], empty[NST], p1done[NST];
   __shared__ int done_cnt[NST];  // SELF: consumer warps finished with the stage's tile
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1282,7 +1304,7 @@ __global__ __launch_bounds__((NC + (SELF ? 0 : 1)) * 32, MINB) void k_translate_
   fill_tail_smem<D, P>(frag);
   __syncthreads();
   if (!SELF && warp == NC) {
-    ws_producer<D, P, G, NST, E, PD, BATCH>(a, sched, ntiles, ring, blk, full, empty);
+    ws_producer<D, P, G, NST, E, PD, BATCH, NB>(a, sched, ntiles, ring, blk, full, empty);
     return;
   }
   const int64_t nr_ = BATCH ? a.nrhs : 1;
@@ -1294,7 +1316,7 @@ __global__ __launch_bounds__((NC + (SELF ? 0 : 1)) * 32, MINB) void k_translate_
       const int64_t wj = blockIdx.x + (int64_t)j * gridDim.x;
       if (wj >= ntiles * nr_) break;
       const int64_t tj = BATCH ? wj / nr_ : wj;
-      ws_issue<D, P, G, NST, E, PD, BATCH>(a, sched, wj, tj, ws_group_record<D, P, G>(sched, tj, true), ring, blk,
+      ws_issue<D, P, G, NST, E, PD, BATCH, NB>(a, sched, wj, tj, ws_group_record<D, P, G, NB>(sched, tj, true), ring, blk,
                                            full, j);
     }
   }
@@ -1314,7 +1336,7 @@ __global__ __launch_bounds__((NC + (SELF ? 0 : 1)) * 32, MINB) void k_translate_
       const int64_t wn = w_ + (int64_t)NST * gridDim.x;
       if (wn < ntiles * nr_) {
         const int64_t tn = BATCH ? wn / nr_ : wn;
-        ws_issue<D, P, G, NST, E, PD, BATCH>(a, sched, wn, tn, ws_group_record<D, P, G>(sched, tn, true), ring,
+        ws_issue<D, P, G, NST, E, PD, BATCH, NB>(a, sched, wn, tn, ws_group_record<D, P, G, NB>(sched, tn, true), ring,
                                              blk, full, st);
       }
     }
@@ -1377,15 +1399,21 @@ __global__ __launch_bounds__((NC + (SELF ? 0 : 1)) * 32, MINB) void k_translate_
       INSTR_ADD(4, tf0);
       E* sb = ring + s * STAGE;
       if constexpr (F2) {
-        // two-level tile: first level (lists 1, 2) in place, second level on
-        // the transposed slots (lists 3, 0), the last pass to HBM
-        consumer_pass<D, P, G, NC, 1, false, 1, E>(a, sb, blk[s], op, rot);
+        // two-level tile: first level (block 0) in place, second level (block
+        // 1) on the transposed slots, its second pass to HBM
+        const unsigned char* bk0 = blk[s];
+        const unsigned char* bk1 = blk[s] + SC::BLK;
+        consumer_pass<D, P, G, NC, 1, false, 1, E>(a, sb, bk0, op, rot);
+        consumer_pass<D, P, G, NC, 0, false, 2, E>(a, sb, bk0, op, rot);
         consumer_sync<NC * 32>();
-        consumer_pass<D, P, G, NC, 0, false, 2, E>(a, sb, blk[s], op, rot);
+        consumer_pass<D, P, G, NC, 0, false, 0, E>(a, sb, bk0, op, rot);
+        consumer_pass<D, P, G, NC, 1, false, 3, E>(a, sb, bk0, op, rot);
         consumer_sync<NC * 32>();
-        consumer_pass<D, P, G, NC, 1, false, 3, E, false, 1 << D>(a, sb, blk[s], op, rot);
+        consumer_pass<D, P, G, NC, 1, false, 1, E, false, 1 << D>(a, sb, bk1, op, rot);
+        consumer_pass<D, P, G, NC, 0, false, 2, E, false, 1 << D>(a, sb, bk1, op, rot);
         consumer_sync<NC * 32>();
-        consumer_pass<D, P, G, NC, 0, true, 0, E, false, 1 << D>(a, sb, blk[s], op, rot, ooff(w));
+        consumer_pass<D, P, G, NC, 0, true, 0, E, false, 1 << D>(a, sb, bk1, op, rot, ooff(w));
+        consumer_pass<D, P, G, NC, 1, true, 3, E, false, 1 << D>(a, sb, bk1, op, rot, ooff(w));
       } else if constexpr (D == 2) {
         INSTR_T0(t1);
         first2d(sb, blk[s]);
@@ -2116,7 +2144,7 @@ template <int D, int P, int G>
 static size_t schedule_bytes_g(const LevelDims& L) {
   const int64_t ng = (L.b_hi - L.b_lo) * (L.ap_hi - L.ap_lo) * (L.f2 ? 4 : 1);  // f2: virtual groups
   if (ng <= 0) return 0;
-  return (size_t)((ng + G - 1) / G) * Sched<D, P, G>::BLK;
+  return (size_t)((ng + G - 1) / G) * Sched<D, P, G>::BLK * (L.f2 ? 2 : 1);  // f2: one block per level
 }
 
 template <int D, int P>

@@ -330,3 +330,37 @@ def test_sort_graph_cache_reuse_and_sizes():
         assert np.array_equal(u.view(np.uint64), u0.view(np.uint64))
     x, k = cases[2]
     assert oracle.rel_l2(first[2], oracle.butterfly(x, k, f[2], N, p)) <= PARITY
+
+
+def test_two_level_launches_all_pairs():
+    """Cross-level fusion (two-level launches, 2D FP64): with every level pair
+    fused (SFT_F2=all, in a subprocess: the launch list is fixed per plan at
+    creation) the result is bitwise equal to single-level launches (SFT_F2=0)
+    and within parity of the oracle; odd L leaves a single level 0."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import sys; sys.path.insert(0, %r); import numpy as np, torch, synth, paper_0801_1524_b200 as sft\n"
+            "out = []\n"
+            "for name, N in (('C0', None), ('C1', None), ('C1', 512)):\n"
+            "    w = synth.make_workload(name, N=N, p=9)\n"
+            "    with sft.Plan(2, w.N, 9, torch.from_numpy(w.x).cuda(), torch.from_numpy(w.k).cuda()) as pl:\n"
+            "        u = pl.apply(torch.from_numpy(w.f).cuda()).cpu().numpy(); out.append(u.view(np.uint64))\n"
+            "        print(pl.stats()['launches'])\n"
+            "np.save(sys.argv[1], np.concatenate(out))") % root
+    res = {}
+    for mode in ("0", "all"):
+        path = os.path.join(root, "gpurun_out", f"f2_{mode}.npy") if os.path.isdir(os.path.join(root, "gpurun_out")) \
+            else f"/tmp/f2_{mode}.npy"
+        r = subprocess.run([sys.executable, "-c", code, path], env=dict(os.environ, SFT_F2=mode),
+                           capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        res[mode] = (np.load(path), r.stdout)
+    assert np.array_equal(res["0"][0], res["all"][0])
+    assert "True" in res["all"][1] and "True" not in res["0"][1]
+    # odd L = 9 (N = 512): four two-level launches and a single level 0
+    assert "(0, False)" in res["all"][1].splitlines()[-1]
+    w = synth.make_workload("C1", N=512, p=9)
+    u = res["all"][0][-2 * len(w.x):].view(np.complex128)
+    assert oracle.rel_l2(u, oracle.butterfly(w.x, w.k, w.f, w.N, 9)) <= PARITY
