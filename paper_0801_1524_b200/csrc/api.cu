@@ -408,6 +408,7 @@ static void plan_free(sft_plan_s* P) {
   for (int i = 0; i < 2; ++i) ev_put(P->plan_ev[i], true);
   ev_put(P->sched_fork, false);
   ev_put(P->sched_ready, false);
+  ev_put(P->sched_first, false);
   // no sync: the frees above are stream-ordered behind any pending work
   delete P;
 }
@@ -534,6 +535,7 @@ extern "C" int sft_plan(int dim, int64_t N, int p, const double* x, int64_t nx, 
   // taken now (host time overlaps the tree build), used after the counts sync
   P->sched_fork = ev_get(false);
   P->sched_ready = ev_get(false);
+  P->sched_first = ev_get(false);
   bool sched_recorded = false;
   auto bail = [&](int code, const std::string& m) {
     if (!P->plan_ev[0]) {
@@ -543,7 +545,8 @@ extern "C" int sft_plan(int dim, int64_t N, int p, const double* x, int64_t nx, 
     if (!sched_recorded) {  // plan_free waits on sched_ready: never on an unrecorded pooled event
       ev_put(P->sched_fork, false);
       ev_put(P->sched_ready, false);
-      P->sched_fork = P->sched_ready = nullptr;
+      ev_put(P->sched_first, false);
+      P->sched_fork = P->sched_ready = P->sched_first = nullptr;
     }
     plan_free(P);
     return fail(code, m);
@@ -668,9 +671,13 @@ extern "C" int sft_plan(int dim, int64_t N, int p, const double* x, int64_t nx, 
     // 0.201 -> 0.231 ms: a super-group's 16 stage slots hold ~2 present first-
     // level groups on these curves), so by default only the first pair is fused;
     // SFT_F2=all fuses every pair
-    const bool f2 = two_level_supported(P);
+    // Default off: with the leaf-end pair fused the translation gains ~8 us on
+    // C2 and the plan loses as much (a second schedule kernel and event on its
+    // critical path), A/B on one box 1.3825 -> 1.3887 ms per step.
+    // SFT_F2=first fuses the leaf-end pair, SFT_F2=all every pair.
     const char* fe = getenv("SFT_F2");
     const bool f2_all = fe && std::string(fe) == "all";
+    const bool f2 = two_level_supported(P) && fe && (f2_all || std::string(fe) == "first");
     int t = L - 1;
     while (t >= 0) {
       if (f2 && t >= 1 && (f2_all || t == L - 1)) {
@@ -703,10 +710,17 @@ extern "C" int sft_plan(int dim, int64_t N, int p, const double* x, int64_t nx, 
     P->sched = tot > 0 ? (unsigned char*)(blk + 2 * bb) : nullptr;
     trace_mark("bufs");
     if (tot > 0) {
+      // the first translation launch's schedule first (its own event: the
+      // first translation waits only for it), then all the others
       std::vector<LevelDims> dims;
       std::vector<unsigned char*> dst;
+      // (only when the first launch is a two-level one: its schedule kernel is
+      // a separate launch anyway)
+      const int t_first =
+          P->world == 1 && !P->launch_t.empty() && P->launch_f2_out[P->launch_t[0]] ? P->launch_t[0] : -1;
       for (int t = 0; t < L; ++t) {
         if (t >= 1 && P->launch_f2_out[t - 1]) continue;
+        if (t == t_first) continue;
         dims.push_back(launch_dims(P, t));
         dst.push_back(P->sched + P->sched_off[t]);
       }
@@ -716,7 +730,14 @@ extern "C" int sft_plan(int dim, int64_t N, int p, const double* x, int64_t nx, 
       cudaStream_t side = side_stream();
       cudaEventRecord(P->sched_fork, s);
       cudaStreamWaitEvent(side, P->sched_fork, 0);
-      cudaError_t ce = launch_schedule(P, dims.data(), (int)dims.size(), dst.data(), side);
+      cudaError_t ce = cudaSuccess;
+      if (t_first >= 0) {
+        const LevelDims d0 = launch_dims(P, t_first);
+        unsigned char* d0dst = P->sched + P->sched_off[t_first];
+        ce = launch_schedule(P, &d0, 1, &d0dst, side);
+        cudaEventRecord(P->sched_first, side);
+      }
+      if (ce == cudaSuccess) ce = launch_schedule(P, dims.data(), (int)dims.size(), dst.data(), side);
       cudaEventRecord(P->sched_ready, side);
       sched_recorded = true;
       if (ce != cudaSuccess) return bail(SFT_E_CUDA, std::string("schedule: ") + cudaGetErrorString(ce));
@@ -742,8 +763,13 @@ extern "C" int sft_plan(int dim, int64_t N, int p, const double* x, int64_t nx, 
   if (!sched_recorded) {  // no schedule kernel (no translation groups / non-ws kernel)
     ev_put(P->sched_fork, false);
     ev_put(P->sched_ready, false);
-    P->sched_fork = P->sched_ready = nullptr;
+    ev_put(P->sched_first, false);
+    P->sched_fork = P->sched_ready = P->sched_first = nullptr;
     sched_recorded = true;
+  }
+  if (P->world != 1 || P->launch_t.empty() || !P->launch_f2_out[P->launch_t[0]]) {  // launch 0 waits on sched_ready
+    ev_put(P->sched_first, false);
+    P->sched_first = nullptr;
   }
   trace_mark("sched");
   // no sync here: the schedule kernel runs behind the caller's next launches;
@@ -925,9 +951,11 @@ static int apply_impl(sft_plan_s* P, int nrhs, const void* f, int64_t ldf, void*
   tmark(P);
   // step 3: the translation launches, t = L-1 .. 0 (two-level launches cover
   // levels t+1 and t), after the plan's schedule kernel on the side stream
-  if (P->sched_ready) CKR(cudaStreamWaitEvent(s, P->sched_ready, 0));
   const int nl = (int)P->launch_t.size();
   for (int i = 0; i < nl; ++i) {
+    // launch 0 needs only its own schedule; the rest were built behind it
+    if (i == 0 && P->sched_first) CKR(cudaStreamWaitEvent(s, P->sched_first, 0));
+    else if (i <= 1 && P->sched_ready) CKR(cudaStreamWaitEvent(s, P->sched_ready, 0));
     LevelDims ld = apply_dims_sched(P, P->launch_t[i]);
     ld.nrhs = nrhs;
     ld.rs = rs;

@@ -113,6 +113,7 @@ struct sft_plan_s {
   unsigned char* sched = nullptr;
   std::vector<size_t> sched_off;
   cudaEvent_t sched_fork = nullptr, sched_ready = nullptr;  // schedule kernel on the side stream
+  cudaEvent_t sched_first = nullptr;  // the first translation launch's schedule (world 1)
   // timing
   bool timing = false;
   cudaEvent_t ev[64];

@@ -805,7 +805,9 @@ struct SchedLevels {
 };
 static_assert(sizeof(SchedLevels) <= 4096, "k_schedule's parameter must stay within 4 KB");
 
-template <int D, int P, int G, int PS>
+// F2K: the two-level (f2) levels' schedules (a separate instantiation, so the
+// single-level builder keeps its registers and occupancy)
+template <int D, int P, int G, int PS, bool F2K = false>
 __global__ __launch_bounds__(128) void k_schedule(const __grid_constant__ SchedLevels S) {
   using SC = Sched<D, P, G>;
   static_assert(G >= 1 && G <= 32 && (G & (G - 1)) == 0, "G must be a power of two");
@@ -819,11 +821,9 @@ __global__ __launch_bounds__(128) void k_schedule(const __grid_constant__ SchedL
   const LevelArgs& a = S.a[lv];
   const int64_t tile = T - S.tile0[lv];
   const bool tv = T < S.tile0[S.nlev];
-  if constexpr (D == 2 && G % 4 == 0) {
-    if (a.f2) {
-      schedule_f2<D, P, G, PS>(a, tile, tv, S.dst[lv] + (tv ? tile : 0) * (2 * SC::BLK));
-      return;
-    }
+  if constexpr (F2K) {
+    if constexpr (D == 2 && G % 4 == 0) schedule_f2<D, P, G, PS>(a, tile, tv, S.dst[lv] + (tv ? tile : 0) * (2 * SC::BLK));
+    return;
   }
   unsigned char* b = S.dst[lv] + (tv ? tile : 0) * SC::BLK;
   const int64_t g = tile * G + j;
@@ -2159,26 +2159,36 @@ static size_t schedule_bytes_t(const sft_plan_s* Pl, const LevelDims& L) {
 template <int D, int P, int G, int PS>
 static cudaError_t launch_schedule_g(const sft_plan_s* Pl, const LevelDims* L, int nlev, unsigned char* const* dst,
                                      cudaStream_t st) {
-  for (int c0 = 0; c0 < nlev; c0 += kSchedChunk) {
-    SchedLevels S;
-    int64_t t0 = 0;
-    S.nlev = 0;
-    for (int i = c0; i < nlev && i < c0 + kSchedChunk; ++i) {
-      TransArgs a = make_args(L[i], nullptr, nullptr);
-      if (a.ngroups <= 0) continue;
-      S.a[S.nlev] = a;
-      S.dst[S.nlev] = dst[i];
+  // two passes over the levels: single-level schedules, then two-level ones
+  for (int f2 = 0; f2 < 2; ++f2) {
+    std::vector<int> idx;
+    for (int i = 0; i < nlev; ++i)
+      if ((L[i].f2 != 0) == (f2 != 0)) idx.push_back(i);
+    for (size_t c0 = 0; c0 < idx.size(); c0 += kSchedChunk) {
+      SchedLevels S;
+      int64_t t0 = 0;
+      S.nlev = 0;
+      for (size_t q = c0; q < idx.size() && q < c0 + kSchedChunk; ++q) {
+        const int i = idx[q];
+        TransArgs a = make_args(L[i], nullptr, nullptr);
+        if (a.ngroups <= 0) continue;
+        S.a[S.nlev] = a;
+        S.dst[S.nlev] = dst[i];
+        S.tile0[S.nlev] = t0;
+        t0 += (a.ngroups + G - 1) / G;
+        ++S.nlev;
+      }
       S.tile0[S.nlev] = t0;
-      t0 += (a.ngroups + G - 1) / G;
-      ++S.nlev;
+      if (S.nlev == 0) continue;
+      const int64_t nwarps = (t0 + 32 / G - 1) / (32 / G);
+      if (f2)
+        k_schedule<D, P, G, PS, true><<<(unsigned)((nwarps + 3) / 4), 128, 0, st>>>(S);
+      else
+        k_schedule<D, P, G, PS><<<(unsigned)((nwarps + 3) / 4), 128, 0, st>>>(S);
+      count_launch();
+      cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) return e;
     }
-    S.tile0[S.nlev] = t0;
-    if (S.nlev == 0) continue;
-    const int64_t nwarps = (t0 + 32 / G - 1) / (32 / G);
-    k_schedule<D, P, G, PS><<<(unsigned)((nwarps + 3) / 4), 128, 0, st>>>(S);
-    count_launch();
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
 }

@@ -358,7 +358,7 @@ def test_two_level_launches_all_pairs():
         assert r.returncode == 0, r.stderr[-2000:]
         res[mode] = (np.load(path), r.stdout)
     assert np.array_equal(res["0"][0], res["all"][0])
-    assert "True" in res["all"][1] and "True" not in res["0"][1]
+    assert "True" in res["all"][1] and "True" not in res["0"][1]  # (default: off, see api.cu)
     # odd L = 9 (N = 512): four two-level launches and a single level 0
     assert "(0, False)" in res["all"][1].splitlines()[-1]
     w = synth.make_workload("C1", N=512, p=9)
