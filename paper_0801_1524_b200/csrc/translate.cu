@@ -360,7 +360,15 @@ struct MmaShape {
   static constexpr int H = (P - 1) / 2;           // dense (odd) columns per child
   static constexpr int K = 2 * H;                 // stacked odd child elements
   static constexpr int NK = (K + 3) / 4;          // k-steps of 4
-  static constexpr bool TAIL = (P % 4) == 1;      // m = P-1 by DFMA
+  // m = P-1: p = 5 by DFMA with a 4-lane transpose-reduce; p = 9 in a third N
+  // tile on the tensor cores (+50% DMMA on an otherwise idle pipe, ~25 fewer
+  // instructions per super-tile: C2 translate 1.215 -> 1.173 ms; for 3D p = 5
+  // the DFMA tail is faster, 0.895 vs 0.916 ms).  SFT_TAIL_DMMA=0/1 forces.
+#if defined(SFT_TAIL_DMMA)
+  static constexpr bool TAIL = SFT_TAIL_DMMA ? false : (P % 4) == 1;
+#else
+  static constexpr bool TAIL = (P % 4) == 1 && P != 9;
+#endif
   static constexpr int NM = TAIL ? P - 1 : P;     // m's on the tensor cores
   static constexpr int NT = (2 * NM + 7) / 8;     // N tiles of 8 (P_m, Q_m interleaved)
   static constexpr int K0_HI = (H + 3) / 4;       // k-steps [0, K0_HI) hold child-0 elements
@@ -1796,7 +1804,7 @@ __global__ __launch_bounds__(NT, SFT_FMA_MINB(NT)) void k_translate_fma(TransArg
 // G groups per tile, NC consumer warps, NST stages, MINB resident CTAs per SM
 // (the register cap: MINB * (NC+1) warps share the 64K registers)
 #ifndef SFT_WS_MINB29
-#define SFT_WS_MINB29 4
+#define SFT_WS_MINB29 3  // register cap only: 95 registers still fit 4 CTAs per SM
 #endif
 #ifndef SFT_SELF_DEFAULT
 #define SFT_SELF_DEFAULT 0
