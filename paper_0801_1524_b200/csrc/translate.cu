@@ -426,13 +426,23 @@ struct TailSmem {
 // in shared memory (SFT_TAIL_SMEM) they cost one broadcast load per k-step
 // instead of 2*NK registers per thread
 __shared__ double2 s_tail[8][4];
+// SFT_DELTA_SMEM: the delta coefficients (a0, b0, a1, b1) per (N tile, lane%4)
+// in shared memory instead of 4*NT registers per thread
+#ifndef SFT_DELTA_SMEM
+#define SFT_DELTA_SMEM 0
+#endif
+__shared__ double4 s_delta[4][4];
 
 template <int P, bool TS>
 struct LaneOps {
   using S = MmaShape<P>;
   double fb[S::NK][S::NT];           // B fragments of the operator (odd columns)
   double ft[TS ? 1 : S::NK][2];      // tail column (m = P-1): P and Q weights of this lane's k
-  double dl[S::NT][4];               // delta columns of m = 4n + lane%4: (a0, b0, a1, b1)
+  double dl[SFT_DELTA_SMEM ? 1 : S::NT][4];  // delta columns of m = 4n + lane%4: (a0, b0, a1, b1)
+  __device__ __forceinline__ double4 delta(int n, int lane) const {
+    if constexpr (SFT_DELTA_SMEM) return s_delta[n][lane & 3];
+    else return make_double4(dl[n][0], dl[n][1], dl[n][2], dl[n][3]);
+  }
   double dt[S::TAIL ? 2 : 1];        // delta column of the tail (lane%4 == 0 only, else 0)
   // child (0, 1; 2 = padding) and element index of this lane's k in k-step kk
   __device__ __forceinline__ static int bk(int kk, int lane) {
@@ -1024,10 +1034,11 @@ __device__ __forceinline__ void consumer_pass(const TransArgs& a, E* __restrict_
 #pragma unroll
       for (int n = 0; n < S::NT; ++n) {
         const double2 x0 = ElemT<E>::ld(x[u][doff[n][0]]), x1 = ElemT<E>::ld(x[u][doff[n][1]]);
-        are[u][n][0] = fma(op.dl[n][2], x1.x, op.dl[n][0] * x0.x);
-        are[u][n][1] = fma(op.dl[n][3], x1.x, op.dl[n][1] * x0.x);
-        aim[u][n][0] = fma(op.dl[n][2], x1.y, op.dl[n][0] * x0.y);
-        aim[u][n][1] = fma(op.dl[n][3], x1.y, op.dl[n][1] * x0.y);
+        const double4 dc = op.delta(n, lane);
+        are[u][n][0] = fma(dc.z, x1.x, dc.x * x0.x);
+        are[u][n][1] = fma(dc.w, x1.x, dc.y * x0.x);
+        aim[u][n][0] = fma(dc.z, x1.y, dc.x * x0.y);
+        aim[u][n][1] = fma(dc.w, x1.y, dc.y * x0.y);
       }
       if (S::TAIL) {  // m = P-1: child-1 element P-1 only (coefficients non-zero on lane%4 == 0)
         const double2 x1 = ElemT<E>::ld(x[u][(1 << SH) * PD * MUL + (P - 1) * STR]);
@@ -1120,6 +1131,14 @@ __device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
 template <int D, int P>
 __device__ __forceinline__ void fill_tail_smem(const double* __restrict__ frag) {
   using S = MmaShape<P>;
+  if (SFT_DELTA_SMEM && threadIdx.x < 4) {
+#pragma unroll
+    for (int n = 0; n < S::NT; ++n)
+      s_delta[n][threadIdx.x] = make_double4(frag[S::OFF_DELTA + (n * 4 + 0) * 32 + threadIdx.x],
+                                             frag[S::OFF_DELTA + (n * 4 + 1) * 32 + threadIdx.x],
+                                             frag[S::OFF_DELTA + (n * 4 + 2) * 32 + threadIdx.x],
+                                             frag[S::OFF_DELTA + (n * 4 + 3) * 32 + threadIdx.x]);
+  }
   if (TailSmem<D>::v && S::TAIL && threadIdx.x < 4) {
 #pragma unroll
     for (int kk = 0; kk < S::NK; ++kk)
@@ -1134,7 +1153,7 @@ __device__ __forceinline__ void load_lane_ops(LaneOps<P, TS>& op, const double* 
 #pragma unroll
   for (int n = 0; n < S::NT; ++n)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) op.dl[n][j] = frag[S::OFF_DELTA + (n * 4 + j) * 32 + lane];
+    for (int j = 0; j < 4; ++j) op.dl[SFT_DELTA_SMEM ? 0 : n][j] = frag[S::OFF_DELTA + (n * 4 + j) * 32 + lane];
   op.dt[0] = S::TAIL ? frag[S::OFF_DTAIL + lane] : 0.0;
   if (S::TAIL) op.dt[S::TAIL ? 1 : 0] = frag[S::OFF_DTAIL + 32 + lane];
 #pragma unroll
