@@ -1823,7 +1823,7 @@ __global__ __launch_bounds__(NT, SFT_FMA_MINB(NT)) void k_translate_fma(TransArg
 // G groups per tile, NC consumer warps, NST stages, MINB resident CTAs per SM
 // (the register cap: MINB * (NC+1) warps share the 64K registers)
 #ifndef SFT_WS_MINB29
-#define SFT_WS_MINB29 3  // register cap only: 95 registers still fit 4 CTAs per SM
+#define SFT_WS_MINB29 4  // caps every variant (batch, two-level) at 96 registers: 4 CTAs per SM
 #endif
 #ifndef SFT_SELF_DEFAULT
 #define SFT_SELF_DEFAULT 0
@@ -2050,15 +2050,15 @@ static cudaError_t launch_translate_t(const sft_plan_s* Pl, const LevelDims& L, 
     const int64_t ntiles = (a.ngroups + G - 1) / G;
     const int64_t grid = std::min<int64_t>(ntiles * a.nrhs, grid_max);
     if (a.nrhs > 1) {
-      static bool battr = false;
-      if (!battr) {
-        cudaError_t e = cudaFuncSetAttribute(k_translate_ws<D, P, G, NC, NST, MB, float2, false, true>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      static int grid_b = 0;
+      if (!grid_b) {
+        cudaError_t e = persistent_grid(k_translate_ws<D, P, G, NC, NST, MB, float2, false, true>, (NC + 1) * 32,
+                                        smem, &grid_b);
         if (e != cudaSuccess) return e;
-        battr = true;
       }
-      launch_pdl(k_translate_ws<D, P, G, NC, NST, MB, float2, false, true>, (unsigned)grid, (NC + 1) * 32, smem,
-                 Pl->stream, a, frag, L.sched, ntiles);
+      launch_pdl(k_translate_ws<D, P, G, NC, NST, MB, float2, false, true>,
+                 (unsigned)std::min<int64_t>(ntiles * a.nrhs, grid_b), (NC + 1) * 32, smem, Pl->stream, a, frag,
+                 L.sched, ntiles);
     } else {
       launch_pdl(k_translate_ws<D, P, G, NC, NST, MB, float2>, (unsigned)grid, (NC + 1) * 32, smem, Pl->stream, a,
                  frag, L.sched, ntiles);
@@ -2123,15 +2123,15 @@ static cudaError_t launch_translate_t(const sft_plan_s* Pl, const LevelDims& L, 
         return cudaErrorInvalidValue;
       }
     } else if (a.nrhs > 1) {
-      static bool battr = false;
-      if (!battr) {
-        cudaError_t e = cudaFuncSetAttribute(k_translate_ws<D, P, G, NC, NST, MB, double2, false, true>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      static int grid_b = 0;  // the batch variant's own occupancy (it may hold more registers)
+      if (!grid_b) {
+        cudaError_t e = persistent_grid(k_translate_ws<D, P, G, NC, NST, MB, double2, false, true>, (NC + 1) * 32,
+                                        smem, &grid_b);
         if (e != cudaSuccess) return e;
-        battr = true;
       }
-      launch_pdl(k_translate_ws<D, P, G, NC, NST, MB, double2, false, true>, (unsigned)grid, (NC + 1) * 32, smem,
-                 Pl->stream, a, frag, L.sched, ntiles);
+      launch_pdl(k_translate_ws<D, P, G, NC, NST, MB, double2, false, true>,
+                 (unsigned)std::min<int64_t>(ntiles * a.nrhs, grid_b), (NC + 1) * 32, smem, Pl->stream, a, frag,
+                 L.sched, ntiles);
     } else if (use_self<D>(NST)) {
       // self-fed consumers (no producer warp): one more CTA per SM where registers allowed NC + 1 warps
       if constexpr (!(D == 2 && NST >= 3)) {
