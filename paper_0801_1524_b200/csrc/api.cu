@@ -457,7 +457,7 @@ struct PlanTrace {
     cudaGetLastError();
   }
 };
-static PlanTrace* g_trace = nullptr;
+static thread_local PlanTrace* g_trace = nullptr;
 namespace sft {
 void trace_mark(const char* what, cudaStream_t s, bool dev) {
   if (g_trace) g_trace->mark(what, s, dev);
