@@ -358,7 +358,11 @@ __device__ __forceinline__ double2* out_array(const LevelArgs& a, const GroupMet
 template <int P>
 struct MmaShape {
   static constexpr int H = (P - 1) / 2;           // dense (odd) columns per child
-  static constexpr int K = 2 * H;                 // stacked odd child elements
+  // each child's odd elements padded to HP k-slots (p = 7: 3 -> 4), so a child
+  // never straddles a k-step: rows with one live child skip whole k-steps, and
+  // the padding lanes re-read element 1 (a broadcast, no bank conflict)
+  static constexpr int HP = H <= 2 ? 2 : 4;
+  static constexpr int K = 2 * HP;                // stacked (padded) odd child elements
   static constexpr int NK = (K + 3) / 4;          // k-steps of 4
   // m = P-1: p = 5 by DFMA with a 4-lane transpose-reduce; p = 9 in a third N
   // tile on the tensor cores (+50% DMMA on an otherwise idle pipe, ~25 fewer
@@ -371,8 +375,8 @@ struct MmaShape {
 #endif
   static constexpr int NM = TAIL ? P - 1 : P;     // m's on the tensor cores
   static constexpr int NT = (2 * NM + 7) / 8;     // N tiles of 8 (P_m, Q_m interleaved)
-  static constexpr int K0_HI = (H + 3) / 4;       // k-steps [0, K0_HI) hold child-0 elements
-  static constexpr int K1_LO = H / 4;             // k-steps [K1_LO, NK) hold child-1 elements
+  static constexpr int K0_HI = (HP + 3) / 4;      // k-steps [0, K0_HI) hold child-0 elements
+  static constexpr int K1_LO = HP / 4;            // k-steps [K1_LO, NK) hold child-1 elements
   // fragment table: B fragments, tail weights, then the delta coefficients
   // (a0, b0, a1, b1) of m = 4n + lane%4 per N tile and (a1, b1) of the tail
   static constexpr int OFF_TAIL = NK * NT * 32;
@@ -447,11 +451,11 @@ struct LaneOps {
   // child (0, 1; 2 = padding) and element index of this lane's k in k-step kk
   __device__ __forceinline__ static int bk(int kk, int lane) {
     const int k = 4 * kk + (lane & 3);
-    return k < S::K ? k / S::H : 2;
+    return k < S::K ? k / S::HP : 2;
   }
   __device__ __forceinline__ static int lk(int kk, int lane) {
     const int k = 4 * kk + (lane & 3);
-    return k < S::K ? 2 * (k % S::H) + 1 : 0;
+    return k < S::K && k % S::HP < S::H ? 2 * (k % S::HP) + 1 : 1;  // padding: element 1 (zero B row)
   }
   __device__ __forceinline__ double2 tail(int kk, int lane) const {
     if constexpr (TS) return s_tail[kk][lane & 3];
@@ -934,6 +938,22 @@ template <int D, int P>
 struct NsubCfg {
   static constexpr int v = (D == 3 && P == 5) ? SFT_NSUB35 : SFT_NSUB_OTHER;
 };
+// Row -> fiber map of a super-tile: chosen per (d, p, axis) by
+// scripts/rfib_search.py, which minimises the modelled shared-memory
+// wavefronts (A fragments, delta columns, in-place stores) of the pass; the
+// default (rows 2q, 2q+1 <- fibers q, q+4) is optimal for 2D p = 9.
+template <int D, int P, int AX>
+struct RowMap {
+  __device__ __forceinline__ static int fiber(int r) {
+    if constexpr (D == 2 && P == 5) return (0x43726150u >> (4 * r)) & 7;   // 0 5 1 6 2 7 3 4
+    else if constexpr (D == 2 && P == 7) return (0x63524170u >> (4 * r)) & 7;  // 0 7 1 4 2 5 3 6
+    else if constexpr (D == 3 && P == 5 && AX == 1) return (0x76432150u >> (4 * r)) & 7;  // 0 5 1 2 3 4 6 7
+    else if constexpr (D == 3 && P == 7 && AX == 1) return (0x74635210u >> (4 * r)) & 7;  // 0 1 2 5 3 6 4 7
+    else if constexpr (D == 3 && P == 7) return (0x63724150u >> (4 * r)) & 7;  // 0 5 1 4 2 7 3 6
+    else return (r >> 1) + 4 * (r & 1);
+  }
+};
+
 // MUL: slot-pair distance in units of (1 << SH) slots -- NS for the second
 // level of a two-level tile (transposed slots), 1 otherwise
 template <int D, int P, int G, int NC, int AX, bool LAST, int LIST = AX, typename E = double2, bool FUSED = false,
@@ -956,7 +976,7 @@ __device__ __forceinline__ void consumer_pass(const TransArgs& a, E* __restrict_
   const int nst = __shfl_sync(0xffffffffu, (ntot + 7) >> 3, 0);
   const int lane = threadIdx.x & 31, warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
   const int r = lane >> 2, c = lane & 3;
-  const int rfib = (r >> 1) + 4 * (r & 1);  // rows 2q, 2q+1 <- fibers q, q+4 (bank-conflict-free)
+  const int rfib = RowMap<D, P, AX>::fiber(r);  // row -> fiber of the super-tile (bank conflicts)
   int off[S::NK];
 #pragma unroll
   for (int kk = 0; kk < S::NK; ++kk)
@@ -1650,10 +1670,10 @@ static std::vector<double> mma_fragments() {
     if (pq == 0) return b == 0 ? rc(0, m, l) : rs(1, m, l);
     return b == 0 ? rs(0, m, l) : -rc(1, m, l);
   };
-  // tensor-core K index k -> (child k / H, odd element 2 (k % H) + 1)
+  // tensor-core K index k -> (child k / HP, odd element 2 (k % HP) + 1); padding rows are 0
   auto bop = [&](int k, int m, int pq) -> double {
-    if (k >= S::K || m >= P) return 0.0;
-    return opv(k / S::H, 2 * (k % S::H) + 1, m, pq);
+    if (k >= S::K || m >= P || k % S::HP >= S::H) return 0.0;
+    return opv(k / S::HP, 2 * (k % S::HP) + 1, m, pq);
   };
   std::vector<double> fr(S::NFRAG, 0.0);
   for (int kk = 0; kk < S::NK; ++kk)
