@@ -902,8 +902,11 @@ static int apply_impl(sft_plan_s* P, int nrhs, const void* f, int64_t ldf, void*
     P->stage_rhs = nrhs;
   }
   if (f_host) {
-    CKR(cudaMemcpy2DAsync(P->f_stage, P->nk * sizeof(double2), f, ldf * sizeof(double2), P->nk * sizeof(double2),
-                          nrhs, cudaMemcpyHostToDevice, s));
+    if (ldf == P->nk)  // contiguous: one plain copy (the 2-D path is slower for pinned memory)
+      CKR(cudaMemcpyAsync(P->f_stage, f, (size_t)nrhs * P->nk * sizeof(double2), cudaMemcpyHostToDevice, s));
+    else
+      CKR(cudaMemcpy2DAsync(P->f_stage, P->nk * sizeof(double2), f, ldf * sizeof(double2), P->nk * sizeof(double2),
+                            nrhs, cudaMemcpyHostToDevice, s));
     fd = P->f_stage;
     ldf = P->nk;
   }
@@ -966,8 +969,11 @@ static int apply_impl(sft_plan_s* P, int nrhs, const void* f, int64_t ldf, void*
   CKR(launch_final(P, buf[nl & 1], ud, 0, 0, P->nx, nrhs, rs, ldu_dev));
   tmark(P);
   if (u_host) {
-    CKR(cudaMemcpy2DAsync(u, ldu * sizeof(double2), ud, ldu_dev * sizeof(double2), P->nx * sizeof(double2), nrhs,
-                          cudaMemcpyDeviceToHost, s));
+    if (ldu == ldu_dev)
+      CKR(cudaMemcpyAsync(u, ud, (size_t)nrhs * P->nx * sizeof(double2), cudaMemcpyDeviceToHost, s));
+    else
+      CKR(cudaMemcpy2DAsync(u, ldu * sizeof(double2), ud, ldu_dev * sizeof(double2), P->nx * sizeof(double2), nrhs,
+                            cudaMemcpyDeviceToHost, s));
     CKR(cudaStreamSynchronize(s));
   }
   return finish_timing(P, L - 1, &P->launch_t);
