@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <new>
 #include <string>
@@ -370,12 +371,19 @@ static LevelDims apply_dims_sched(const sft_plan_s* P, int t) {
 // time each, on the plan's critical path.  Events are recycled instead (a
 // re-recorded event is safe: stream waits capture the event's state at the
 // time of the wait call).
+// (events belong to a device: one pool per device and kind)
 static std::mutex g_ev_mu;
-static std::vector<cudaEvent_t> g_ev_pool[2];  // [0] timing, [1] cudaEventDisableTiming
+static std::map<int, std::vector<cudaEvent_t>> g_ev_pool[2];  // [0] timing, [1] cudaEventDisableTiming
+static int current_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d;
+}
 static cudaEvent_t ev_get(bool timing) {
+  const int dev = current_device();
   {
     std::lock_guard<std::mutex> lk(g_ev_mu);
-    auto& v = g_ev_pool[timing ? 0 : 1];
+    auto& v = g_ev_pool[timing ? 0 : 1][dev];
     if (!v.empty()) {
       cudaEvent_t e = v.back();
       v.pop_back();
@@ -386,10 +394,10 @@ static cudaEvent_t ev_get(bool timing) {
   cudaEventCreateWithFlags(&e, timing ? cudaEventDefault : cudaEventDisableTiming);
   return e;
 }
-static void ev_put(cudaEvent_t e, bool timing) {
+static void ev_put(cudaEvent_t e, bool timing, int dev) {
   if (!e) return;
   std::lock_guard<std::mutex> lk(g_ev_mu);
-  g_ev_pool[timing ? 0 : 1].push_back(e);
+  g_ev_pool[timing ? 0 : 1][dev].push_back(e);
 }
 
 static void plan_free(sft_plan_s* P) {
@@ -405,10 +413,10 @@ static void plan_free(sft_plan_s* P) {
   if (P->u_stage) cudaFreeAsync(P->u_stage, s);
   if (P->d_seg) cudaFreeAsync(P->d_seg, s);
   for (int i = 0; i < P->ev_created; ++i) cudaEventDestroy(P->ev[i]);
-  for (int i = 0; i < 2; ++i) ev_put(P->plan_ev[i], true);
-  ev_put(P->sched_fork, false);
-  ev_put(P->sched_ready, false);
-  ev_put(P->sched_first, false);
+  for (int i = 0; i < 2; ++i) ev_put(P->plan_ev[i], true, P->dev);
+  ev_put(P->sched_fork, false, P->dev);
+  ev_put(P->sched_ready, false, P->dev);
+  ev_put(P->sched_first, false, P->dev);
   // no sync: the frees above are stream-ordered behind any pending work
   delete P;
 }
@@ -511,6 +519,7 @@ extern "C" int sft_plan(int dim, int64_t N, int p, const double* x, int64_t nx, 
     P->pds = (int)(P->prec == 1 ? pd + (pd & 1) : pd);  // FP32: 16-byte multiple per array
   }
   P->stream = (cudaStream_t)o.stream;
+  P->dev = current_device();
   cudaStream_t s = P->stream;
 
   // stream-ordered allocations: keep freed memory in the pool so plan/destroy
@@ -539,13 +548,13 @@ extern "C" int sft_plan(int dim, int64_t N, int p, const double* x, int64_t nx, 
   bool sched_recorded = false;
   auto bail = [&](int code, const std::string& m) {
     if (!P->plan_ev[0]) {
-      ev_put(e0, true);
-      ev_put(e1, true);
+      ev_put(e0, true, P->dev);
+      ev_put(e1, true, P->dev);
     }
     if (!sched_recorded) {  // plan_free waits on sched_ready: never on an unrecorded pooled event
-      ev_put(P->sched_fork, false);
-      ev_put(P->sched_ready, false);
-      ev_put(P->sched_first, false);
+      ev_put(P->sched_fork, false, P->dev);
+      ev_put(P->sched_ready, false, P->dev);
+      ev_put(P->sched_first, false, P->dev);
       P->sched_fork = P->sched_ready = P->sched_first = nullptr;
     }
     plan_free(P);
@@ -761,14 +770,14 @@ extern "C" int sft_plan(int dim, int64_t N, int p, const double* x, int64_t nx, 
     }
   }
   if (!sched_recorded) {  // no schedule kernel (no translation groups / non-ws kernel)
-    ev_put(P->sched_fork, false);
-    ev_put(P->sched_ready, false);
-    ev_put(P->sched_first, false);
+    ev_put(P->sched_fork, false, P->dev);
+    ev_put(P->sched_ready, false, P->dev);
+    ev_put(P->sched_first, false, P->dev);
     P->sched_fork = P->sched_ready = P->sched_first = nullptr;
     sched_recorded = true;
   }
   if (P->world != 1 || P->launch_t.empty() || !P->launch_f2_out[P->launch_t[0]]) {  // launch 0 waits on sched_ready
-    ev_put(P->sched_first, false);
+    ev_put(P->sched_first, false, P->dev);
     P->sched_first = nullptr;
   }
   trace_mark("sched");

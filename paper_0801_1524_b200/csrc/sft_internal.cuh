@@ -76,6 +76,7 @@ struct sft_plan_s {
   int d = 0, p = 0, L = 0;
   int64_t N = 0, nx = 0, nk = 0;
   int rank = 0, world = 1;
+  int dev = 0;   // CUDA device the plan was created on (its pooled events belong to it)
   int prec = 0;  // 0 = FP64 charges (complex128), 1 = FP32 charges (complex64)
   int conj = 0;  // adjoint plan: conjugate the charges on input and the potentials on output
   int ffmod = 0; // far-field plan (sft_farfield_plan): source (forward) / target (adjoint) modulation e^{-+i pi sum k}
