@@ -14,7 +14,7 @@ name = sys.argv[1]
 w = synth.make_workload(name)
 x = torch.from_numpy(w.x).cuda(); k = torch.from_numpy(w.k).cuda(); f = torch.from_numpy(w.f).cuda()
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-with sft.Plan(w.dim, w.N, w.p, x, k) as pl:
+with sft.Plan(w.dim, w.N, w.p, x, k, precision=int(os.environ.get('SWEEP_PREC', '0'))) as pl:
     pl.set_timing(True)
     ts = []
     for i in range(8):

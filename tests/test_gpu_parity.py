@@ -364,3 +364,19 @@ def test_two_level_launches_all_pairs():
     w = synth.make_workload("C1", N=512, p=9)
     u = res["all"][0][-2 * len(w.x):].view(np.complex128)
     assert oracle.rel_l2(u, oracle.butterfly(w.x, w.k, w.f, w.N, 9)) <= PARITY
+
+
+@pytest.mark.parametrize("d,N,n,p", [(2, 64, 3000, 5), (2, 64, 3000, 7), (2, 64, 3000, 9), (2, 256, 20000, 9),
+                                     (3, 16, 3000, 5), (3, 16, 3000, 7), (3, 16, 2000, 9)])
+def test_uniform_random_full_groups(d, N, n, p):
+    """Uniform random points fill whole boxes: every group has all 2^d children
+    (never the case on curves, where a 2D box has <= 3), so the class-3
+    super-tiles, full stage slots and both axis orders are exercised."""
+    rng = np.random.default_rng(100 + d * 10 + p)
+    x = rng.uniform(0, N, (n, d))
+    k = rng.uniform(0, N, (n + 17, d))
+    f = rng.normal(size=len(k)) + 1j * rng.normal(size=len(k))
+    u, st = gpu_transform(x, k, f, N, p)
+    ub = oracle.butterfly(x, k, f, N, p)
+    assert oracle.rel_l2(u, ub) <= PARITY
+    assert list(st["counts_x"]) == list(oracle.tree_counts(x, N))
