@@ -954,6 +954,15 @@ struct RowMap {
   }
 };
 
+// SFT_BRANCHLESS=1: rows without an output (padding rows of a partial super-tile,
+// absent children of A') store into a dummy array (shared memory for in-place
+// passes, a device scratch array for the last pass) instead of branching around
+// the store
+#ifndef SFT_BRANCHLESS
+#define SFT_BRANCHLESS 0
+#endif
+__device__ double2 g_dummy_out[729 + 1];  // >= p^d of every supported (d, p)
+
 // MUL: slot-pair distance in units of (1 << SH) slots -- NS for the second
 // level of a two-level tile (transposed slots), 1 otherwise
 template <int D, int P, int G, int NC, int AX, bool LAST, int LIST = AX, typename E = double2, bool FUSED = false,
@@ -961,7 +970,7 @@ template <int D, int P, int G, int NC, int AX, bool LAST, int LIST = AX, typenam
 __device__ __forceinline__ void consumer_pass(const TransArgs& a, E* __restrict__ sb,
                                               const unsigned char* __restrict__ blk,
                                               const LaneOps<P, TailSmem<D>::v>& op,
-                                              int& rot, int64_t ooff = 0) {
+                                              int& rot, int64_t ooff = 0, E* sdummy = nullptr) {
   using S = MmaShape<P>;
   using SC = Sched<D, P, G>;
   constexpr int NSUB = NsubCfg<D, P>::v;
@@ -1037,11 +1046,13 @@ __device__ __forceinline__ void consumer_pass(const TransArgs& a, E* __restrict_
         o0[u] = dst(d.o0);
         o1[u] = dst(d.o1);
       } else if (LAST) {
-        o0[u] = d.o0 != ~0u ? gout + d.o0 + ebase : nullptr;
-        o1[u] = d.o1 != ~0u ? gout + d.o1 + ebase : nullptr;
+        E* const nil = SFT_BRANCHLESS ? reinterpret_cast<E*>(g_dummy_out) : nullptr;
+        o0[u] = d.o0 != ~0u ? gout + d.o0 + ebase : nil;
+        o1[u] = d.o1 != ~0u ? gout + d.o1 + ebase : nil;
       } else {
-        o0[u] = vrow ? sb + xo : nullptr;
-        o1[u] = vrow ? sb + xo + (1 << SH) * PD * MUL : nullptr;
+        E* const nil = SFT_BRANCHLESS ? sdummy : nullptr;
+        o0[u] = vrow ? sb + xo : nil;
+        o1[u] = vrow ? sb + xo + (1 << SH) * PD * MUL : nil;
       }
 #endif
     }
@@ -1086,8 +1097,13 @@ __device__ __forceinline__ void consumer_pass(const TransArgs& a, E* __restrict_
       for (int n = 0; n < S::NT; ++n) {
         const int m = 4 * n + c;
         if (m < S::NM) {
-          if (o0[u]) o0[u][m * STR] = ElemT<E>::mk(are[u][n][0] + aim[u][n][1], aim[u][n][0] - are[u][n][1]);
-          if (o1[u]) o1[u][m * STR] = ElemT<E>::mk(are[u][n][0] - aim[u][n][1], aim[u][n][0] + are[u][n][1]);
+          if (SFT_BRANCHLESS && !(LAST && FUSED)) {
+            o0[u][m * STR] = ElemT<E>::mk(are[u][n][0] + aim[u][n][1], aim[u][n][0] - are[u][n][1]);
+            o1[u][m * STR] = ElemT<E>::mk(are[u][n][0] - aim[u][n][1], aim[u][n][0] + are[u][n][1]);
+          } else {
+            if (o0[u]) o0[u][m * STR] = ElemT<E>::mk(are[u][n][0] + aim[u][n][1], aim[u][n][0] - are[u][n][1]);
+            if (o1[u]) o1[u][m * STR] = ElemT<E>::mk(are[u][n][0] - aim[u][n][1], aim[u][n][0] + are[u][n][1]);
+          }
         }
       }
     }
@@ -1105,7 +1121,8 @@ __device__ __forceinline__ void consumer_pass(const TransArgs& a, E* __restrict_
         double w = hi ? vb : va;
         w += __shfl_xor_sync(0xffffffffu, hi ? va : vb, 2);
         E* o = hi ? o1[u] : o0[u];  // lane c holds component c&1 of z_{c>>1}
-        if (o) reinterpret_cast<typename ElemT<E>::scalar*>(o + (P - 1) * STR)[c & 1] = (typename ElemT<E>::scalar)w;
+        if ((SFT_BRANCHLESS && !(LAST && FUSED)) || o)
+          reinterpret_cast<typename ElemT<E>::scalar*>(o + (P - 1) * STR)[c & 1] = (typename ElemT<E>::scalar)w;
       }
     }
   }
@@ -1340,6 +1357,7 @@ __global__ __launch_bounds__((NC + (SELF ? 0 : 1)) * 32, MINB) void k_translate_
   __shared__ __align__(128) unsigned char blk[NST][SC::BLK * NB];
   __shared__ __align__(8) uint64_t full[NST], empty[NST], p1done[NST];
   __shared__ int done_cnt[NST];  // SELF: consumer warps finished with the stage's tile
+  __shared__ __align__(16) E s_dummy[Pow<P, D>::v];  // SFT_BRANCHLESS: in-place stores of rows without output
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (threadIdx.x < NST) {
     done_cnt[threadIdx.x] = 0;
@@ -1397,12 +1415,12 @@ __global__ __launch_bounds__((NC + (SELF ? 0 : 1)) * 32, MINB) void k_translate_
   // 2D: first passes (list 1: axis 1, list 2: axis 0 for groups in reversed
   // order), then last passes (list 0: axis 0, list 3: axis 1)
   auto first2d = [&](E* sb_, const unsigned char* bk) {
-    consumer_pass<D, P, G, NC, D - 1, false, 1, E>(a, sb_, bk, op, rot);
-    if constexpr (D == 2) consumer_pass<D, P, G, NC, 0, false, 2, E>(a, sb_, bk, op, rot);
+    consumer_pass<D, P, G, NC, D - 1, false, 1, E>(a, sb_, bk, op, rot, 0, s_dummy);
+    if constexpr (D == 2) consumer_pass<D, P, G, NC, 0, false, 2, E>(a, sb_, bk, op, rot, 0, s_dummy);
   };
   auto last2d = [&](E* sb_, const unsigned char* bk, int64_t oo) {
-    consumer_pass<D, P, G, NC, 0, true, 0, E, FUSED>(a, sb_, bk, op, rot, oo);
-    if constexpr (D == 2) consumer_pass<D, P, G, NC, D - 1, true, 3, E, FUSED>(a, sb_, bk, op, rot, oo);
+    consumer_pass<D, P, G, NC, 0, true, 0, E, FUSED>(a, sb_, bk, op, rot, oo, s_dummy);
+    if constexpr (D == 2) consumer_pass<D, P, G, NC, D - 1, true, 3, E, FUSED>(a, sb_, bk, op, rot, oo, s_dummy);
   };
   // work items w = tile * nrhs + r; the output of RHS r goes to out + r * rs
   const int64_t nwork = BATCH ? ntiles * a.nrhs : ntiles;
@@ -1450,17 +1468,17 @@ __global__ __launch_bounds__((NC + (SELF ? 0 : 1)) * 32, MINB) void k_translate_
         // 1) on the transposed slots, its second pass to HBM
         const unsigned char* bk0 = blk[s];
         const unsigned char* bk1 = blk[s] + SC::BLK;
-        consumer_pass<D, P, G, NC, 1, false, 1, E>(a, sb, bk0, op, rot);
-        consumer_pass<D, P, G, NC, 0, false, 2, E>(a, sb, bk0, op, rot);
+        consumer_pass<D, P, G, NC, 1, false, 1, E>(a, sb, bk0, op, rot, 0, s_dummy);
+        consumer_pass<D, P, G, NC, 0, false, 2, E>(a, sb, bk0, op, rot, 0, s_dummy);
         consumer_sync<NC * 32>();
-        consumer_pass<D, P, G, NC, 0, false, 0, E>(a, sb, bk0, op, rot);
-        consumer_pass<D, P, G, NC, 1, false, 3, E>(a, sb, bk0, op, rot);
+        consumer_pass<D, P, G, NC, 0, false, 0, E>(a, sb, bk0, op, rot, 0, s_dummy);
+        consumer_pass<D, P, G, NC, 1, false, 3, E>(a, sb, bk0, op, rot, 0, s_dummy);
         consumer_sync<NC * 32>();
-        consumer_pass<D, P, G, NC, 1, false, 1, E, false, 1 << D>(a, sb, bk1, op, rot);
-        consumer_pass<D, P, G, NC, 0, false, 2, E, false, 1 << D>(a, sb, bk1, op, rot);
+        consumer_pass<D, P, G, NC, 1, false, 1, E, false, 1 << D>(a, sb, bk1, op, rot, 0, s_dummy);
+        consumer_pass<D, P, G, NC, 0, false, 2, E, false, 1 << D>(a, sb, bk1, op, rot, 0, s_dummy);
         consumer_sync<NC * 32>();
-        consumer_pass<D, P, G, NC, 0, true, 0, E, false, 1 << D>(a, sb, bk1, op, rot, ooff(w));
-        consumer_pass<D, P, G, NC, 1, true, 3, E, false, 1 << D>(a, sb, bk1, op, rot, ooff(w));
+        consumer_pass<D, P, G, NC, 0, true, 0, E, false, 1 << D>(a, sb, bk1, op, rot, ooff(w), s_dummy);
+        consumer_pass<D, P, G, NC, 1, true, 3, E, false, 1 << D>(a, sb, bk1, op, rot, ooff(w), s_dummy);
       } else if constexpr (D == 2) {
         INSTR_T0(t1);
         first2d(sb, blk[s]);
@@ -1472,11 +1490,11 @@ __global__ __launch_bounds__((NC + (SELF ? 0 : 1)) * 32, MINB) void k_translate_
         last2d(sb, blk[s], ooff(w));
         INSTR_ADD(7, t3);
       } else {
-        consumer_pass<D, P, G, NC, 2, false, 2, E>(a, sb, blk[s], op, rot);
+        consumer_pass<D, P, G, NC, 2, false, 2, E>(a, sb, blk[s], op, rot, 0, s_dummy);
         consumer_sync<NC * 32>();
-        consumer_pass<D, P, G, NC, 1, false, 1, E>(a, sb, blk[s], op, rot);
+        consumer_pass<D, P, G, NC, 1, false, 1, E>(a, sb, blk[s], op, rot, 0, s_dummy);
         consumer_sync<NC * 32>();
-        consumer_pass<D, P, G, NC, 0, true, 0, E, FUSED>(a, sb, blk[s], op, rot, ooff(w));
+        consumer_pass<D, P, G, NC, 0, true, 0, E, FUSED>(a, sb, blk[s], op, rot, ooff(w), s_dummy);
       }
       if constexpr (SELF) {
         self_release(s, w);
