@@ -144,7 +144,8 @@ int sft_translation_launches(sft_plan_t plan, int* n, int* out_level, int* two_l
  *   t_ms[0] leaf kernel, t_ms[1] sum of translation kernels, t_ms[2] final
  *   kernel, t_ms[3] whole apply; per_level_ms [L] translation level t=0..L-1
  *   (or NULL; a two-level launch is booked on its output level t, level t+1
- *   then reads 0). */
+ *   then reads 0).  Multi-rank plans: after sft_apply_phase2, t_ms[1] is this
+ *   rank's translation time of both phases (the other entries are not set). */
 int sft_set_timing(sft_plan_t plan, int enable);
 int sft_last_timing(sft_plan_t plan, double* t_ms, double* per_level_ms);
 

@@ -1030,6 +1030,27 @@ extern "C" int sft_partition_info(sft_plan_t P, int64_t* part) {
   return SFT_OK;
 }
 
+// Timing of the phase calls (sft_set_timing): the translation launches of a
+// phase are bracketed by two events; t_ms[1] of sft_last_timing is the sum of
+// phase 1 and phase 2 (each phase synchronises its events: diagnostics only)
+static void phase_timing_begin(sft_plan_s* P) {
+  if (!P->timing) return;
+  if (P->ev_created < 2) {
+    for (int i = P->ev_created; i < 2; ++i) cudaEventCreate(&P->ev[i]);
+    P->ev_created = 2;
+  }
+  cudaEventRecord(P->ev[0], P->stream);
+}
+static int phase_timing_end(sft_plan_s* P, bool first) {
+  if (!P->timing) return SFT_OK;
+  cudaEventRecord(P->ev[1], P->stream);
+  CKR(cudaEventSynchronize(P->ev[1]));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, P->ev[0], P->ev[1]);
+  P->last_ms[1] = (first ? 0.0 : P->last_ms[1]) + ms;
+  return SFT_OK;
+}
+
 extern "C" int sft_apply_phase1(sft_plan_t P, const void* f, void* sendbuf) {
   if (!P || !f || (!sendbuf && P->peer.empty())) return fail(SFT_E_ARG, "NULL argument");
   if (P->world < 2) return fail(SFT_E_STATE, "plan is not multi-rank");
@@ -1057,10 +1078,12 @@ extern "C" int sft_apply_phase1(sft_plan_t P, const void* f, void* sendbuf) {
       out = P->peer[q0] + P->peer_off[q0];
     }
     CKR(launch_leaf(P, fd, out, kl.lo, kl.hi));
+    if (P->timing) P->last_ms[1] = 0.0;  // no translation in phase 1
     return SFT_OK;
   }
   CKR(launch_leaf(P, fd, P->buf[L & 1], kl.lo, kl.hi));
   if (P->sched_ready) CKR(cudaStreamWaitEvent(s, P->sched_ready, 0));
+  phase_timing_begin(P);
   for (int t = L - 1; t >= m; --t) {
     LevelDims ld = apply_dims_sched(P, t);
     double2* out = t == m ? sb : P->buf[t & 1];
@@ -1079,7 +1102,7 @@ extern "C" int sft_apply_phase1(sft_plan_t P, const void* f, void* sendbuf) {
     }
     CKR(launch_translate(P, ld, P->buf[(t + 1) & 1], out));
   }
-  return SFT_OK;
+  return phase_timing_end(P, true);
 }
 
 extern "C" int sft_apply_phase2(sft_plan_t P, const void* recvbuf, void* u) {
@@ -1097,12 +1120,14 @@ extern "C" int sft_apply_phase2(sft_plan_t P, const void* recvbuf, void* u) {
   CKR(launch_zero(ud, P->nx, s));
   if (P->sched_ready) CKR(cudaStreamWaitEvent(s, P->sched_ready, 0));
   const double2* in = (const double2*)recvbuf;
+  phase_timing_begin(P);
   for (int t = m - 1; t >= 0; --t) {
     LevelDims ld = apply_dims_sched(P, t);
     double2* out = P->buf[t & 1];
     CKR(launch_translate(P, ld, in, out));
     in = out;
   }
+  if (int rc = phase_timing_end(P, false)) return rc;
   const LevelRange xl = P->x_rng[L];
   CKR(launch_final(P, in, ud, xl.lo, P->x_pt_lo, P->x_pt_hi));
   if (u_host) {

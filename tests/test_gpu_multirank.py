@@ -13,7 +13,7 @@ import synth
 pytestmark = pytest.mark.gpu
 
 
-def emulate(w, world, force=(-1, -1, -1)):
+def emulate(w, world, force=(-1, -1, -1), timing=False):
     import torch
     import paper_0801_1524_b200 as sft
     x = torch.from_numpy(w.x).cuda(); k = torch.from_numpy(w.k).cuda(); f = torch.from_numpy(w.f).cuda()
@@ -23,6 +23,9 @@ def emulate(w, world, force=(-1, -1, -1)):
     parts = [pl.partition() for pl in plans]
     for pp in parts[1:]:
         assert np.array_equal(pp, parts[0])  # every rank derives the same partition
+    if timing:
+        for pl in plans:
+            pl.set_timing(True)
     send = [torch.empty(max(1, int(c[0].sum())), dtype=torch.complex128, device="cuda") for c in counts]
     for r, pl in enumerate(plans):
         pl.apply_phase1(f, send[r])
@@ -42,6 +45,9 @@ def emulate(w, world, force=(-1, -1, -1)):
         pl.apply_phase2(recv[q] if recv[q].numel() else torch.empty(1, dtype=torch.complex128, device="cuda"), uq)
         u += uq
     torch.cuda.synchronize()
+    if timing:  # per-rank translation time of both phases (bench.py's multi-GPU roofline)
+        tms = [pl.last_timing()["trans_ms"] for pl in plans]
+        assert all(t > 0 for t in tms), tms
     for pl in plans:
         pl.close()
     return u.cpu().numpy(), parts[0]
@@ -58,6 +64,10 @@ def single(w):
 @pytest.mark.parametrize("name,world", [("C1", 2), ("C1", 4), ("C1", 8), ("C0", 2)])
 def test_multirank_bitwise_2d(name, world):
     w = synth.make_workload(name)
+    if world == 4:  # also exercise the phase timing (sft_set_timing on multi-rank plans)
+        u, _ = emulate(w, world, timing=True)
+        assert np.array_equal(u.view(np.uint64), single(w).view(np.uint64))
+        return
     u1 = single(w)
     uw, part = emulate(w, world)
     assert np.array_equal(uw, u1), f"partition {part[:3]}"
