@@ -380,3 +380,26 @@ def test_uniform_random_full_groups(d, N, n, p):
     ub = oracle.butterfly(x, k, f, N, p)
     assert oracle.rel_l2(u, ub) <= PARITY
     assert list(st["counts_x"]) == list(oracle.tree_counts(x, N))
+
+
+@pytest.mark.parametrize("d,N,n,p", [(2, 2, 40, 5), (3, 2, 40, 9), (2, 1 << 17, 300, 9), (2, 1 << 20, 300, 5),
+                                     (3, 1 << 11, 300, 7), (3, 1 << 13, 200, 5)])
+def test_extreme_sizes(d, N, n, p):
+    """Smallest N (one level) and large N up to the supported 2^20: d*L+1 > 32
+    selects the 64-bit Morton keys of the tree build (the BASELINE configs all
+    fit 32 bits), and long level chains with a handful of pairs each."""
+    rng = np.random.default_rng(7 + d + N % 97)
+    if N <= 2:
+        x = rng.uniform(0, N, (n, d))
+        k = rng.uniform(0, N, (n + 3, d))
+    else:  # points on a sphere / circle of radius 0.3 N (sparse at this N)
+        def sph(m):
+            v = rng.normal(size=(m, d))
+            return 0.5 * N + 0.3 * N * v / np.linalg.norm(v, axis=1, keepdims=True)
+        x, k = sph(n), sph(n + 7)
+    f = rng.normal(size=len(k)) + 1j * rng.normal(size=len(k))
+    u, st = gpu_transform(x, k, f, N, p)
+    ub = oracle.butterfly(x, k, f, N, p)
+    assert oracle.rel_l2(u, ub) <= PARITY
+    assert list(st["counts_x"]) == list(oracle.tree_counts(x, N))
+    assert list(st["counts_k"]) == list(oracle.tree_counts(k, N))
