@@ -1151,6 +1151,9 @@ __device__ __forceinline__ void consumer_sync() {
   asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
 }
 
+#ifndef SFT_PRODUCER_SLEEP
+#define SFT_PRODUCER_SLEEP 200  // ns between the producer's polls of a stage's empty barrier
+#endif
 __device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
   uint32_t done = 0;
   while (true) {
@@ -1160,7 +1163,7 @@ __device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
         : "r"(bar), "r"(parity)
         : "memory");
     if (done) break;
-    __nanosleep(200);
+    if (SFT_PRODUCER_SLEEP > 0) __nanosleep(SFT_PRODUCER_SLEEP);
   }
 }
 
