@@ -606,9 +606,13 @@ struct Sched {
 // REV (2D only): the axes are processed in the order 0, 1 instead of 1, 0.
 // Pass over axis 0 first: tasks by beta_1 (slots (0,b1), (1,b1)); then axis 1
 // (last): tasks by alpha_0 (slots (a0,0), (a0,1)), outputs (a0,0), (a0,1).
-// TR (two-level launch, second level): group j's child slot c lives at stage
-// slot c * NS + j (the first level left pair (A'_j, B_c) in slot j of virtual
-// group c), so slot pairs are NS slots further apart
+// Stage layout: slot-major, child slot c of group j at stage slot c * G + j
+// (the G groups' arrays of one child slot are contiguous: one bulk copy when
+// the tile's groups share B and have consecutive A').  TR (two-level launch,
+// second level, G = 4k virtual groups): group alpha of super-group sg reads
+// child c at stage slot alpha * G + 4 sg + c -- the first level left pair
+// (A'_alpha, B_c) in slot alpha of virtual group 4 sg + c -- so its slot pairs
+// are 1 slot apart instead of G
 template <int D, int P, int G, int PS, int AX, bool LAST, bool REV = false, bool TR = false>
 __device__ __forceinline__ void schedule_pass(const LevelArgs& a, const GroupMeta& m, bool valid, bool write_cnt,
                                               int* cnt, TaskRec* out) {
@@ -637,8 +641,8 @@ __device__ __forceinline__ void schedule_pass(const LevelArgs& a, const GroupMet
         cls = b1set;
         slot0 = v << 1;
       }
-      t.x = TR ? (uint32_t)((((lane % G) & ~(NS - 1)) * NS + slot0 * NS + (lane % NS)) * PD)
-               : (uint32_t)(((lane % G) * NS + slot0) * PD);
+      t.x = TR ? (uint32_t)(((lane % NS) * G + ((lane % G) & ~(NS - 1)) + slot0) * PD)
+               : (uint32_t)((slot0 * G + (lane % G)) * PD);
       t.cls = cls;
       t.o0 = t.o1 = ~0u;
       if (LAST) {
@@ -665,8 +669,8 @@ __device__ __forceinline__ void schedule_pass(const LevelArgs& a, const GroupMet
         if (!(PAs >> as & 1)) continue;
         TaskRec t;
         const int sl = (bp << (D - AX)) | as;
-        t.x = TR ? (uint32_t)((((lane % G) & ~(NS - 1)) * NS + sl * NS + (lane % NS)) * PD)
-                 : (uint32_t)(((lane % G) * NS + sl) * PD);
+        t.x = TR ? (uint32_t)(((lane % NS) * G + ((lane % G) & ~(NS - 1)) + sl) * PD)
+                 : (uint32_t)((sl * G + (lane % G)) * PD);
         t.cls = cls;
         t.o0 = t.o1 = ~0u;
         if (LAST) {
@@ -963,10 +967,10 @@ struct RowMap {
 #endif
 __device__ double2 g_dummy_out[729 + 1];  // >= p^d of every supported (d, p)
 
-// MUL: slot-pair distance in units of (1 << SH) slots -- NS for the second
-// level of a two-level tile (transposed slots), 1 otherwise
+// MUL: stage-slot stride of consecutive child slots: 0 = G (slot-major
+// stage), 1 for the second level of a two-level tile (transposed slots)
 template <int D, int P, int G, int NC, int AX, bool LAST, int LIST = AX, typename E = double2, bool FUSED = false,
-          int MUL = 1>
+          int MUL = 0>
 __device__ __forceinline__ void consumer_pass(const TransArgs& a, E* __restrict__ sb,
                                               const unsigned char* __restrict__ blk,
                                               const LaneOps<P, TailSmem<D>::v>& op,
@@ -989,7 +993,7 @@ __device__ __forceinline__ void consumer_pass(const TransArgs& a, E* __restrict_
   int off[S::NK];
 #pragma unroll
   for (int kk = 0; kk < S::NK; ++kk)
-    off[kk] = (LaneOps<P, true>::bk(kk, lane) == 1 ? (1 << SH) * PD * MUL : 0) + LaneOps<P, true>::lk(kk, lane) * STR;
+    off[kk] = (LaneOps<P, true>::bk(kk, lane) == 1 ? (1 << SH) * PD * (MUL == 0 ? G : MUL) : 0) + LaneOps<P, true>::lk(kk, lane) * STR;
   // delta columns of this lane's outputs m = 4n + c: child-0 element 2m and
   // child-1 element 2m - (P-1), clamped into range (their coefficient is 0 there)
   int doff[S::NT][2];
@@ -997,7 +1001,7 @@ __device__ __forceinline__ void consumer_pass(const TransArgs& a, E* __restrict_
   for (int n = 0; n < S::NT; ++n) {
     const int m = 4 * n + c;
     doff[n][0] = min(2 * m, P - 1) * STR;
-    doff[n][1] = (1 << SH) * PD * MUL + min(max(2 * m - (P - 1), 0), P - 1) * STR;  // in range: 0 * finite = 0
+    doff[n][1] = (1 << SH) * PD * (MUL == 0 ? G : MUL) + min(max(2 * m - (P - 1), 0), P - 1) * STR;  // in range: 0 * finite = 0
   }
   // units of NSUB super-tiles go round-robin over the warps, continuing from
   // where the previous pass stopped (rot), so that the extra unit of a pass
@@ -1052,7 +1056,7 @@ __device__ __forceinline__ void consumer_pass(const TransArgs& a, E* __restrict_
       } else {
         E* const nil = SFT_BRANCHLESS ? sdummy : nullptr;
         o0[u] = vrow ? sb + xo : nil;
-        o1[u] = vrow ? sb + xo + (1 << SH) * PD * MUL : nil;
+        o1[u] = vrow ? sb + xo + (1 << SH) * PD * (MUL == 0 ? G : MUL) : nil;
       }
 #endif
     }
@@ -1072,7 +1076,7 @@ __device__ __forceinline__ void consumer_pass(const TransArgs& a, E* __restrict_
         aim[u][n][1] = fma(dc.w, x1.y, dc.y * x0.y);
       }
       if (S::TAIL) {  // m = P-1: child-1 element P-1 only (coefficients non-zero on lane%4 == 0)
-        const double2 x1 = ElemT<E>::ld(x[u][(1 << SH) * PD * MUL + (P - 1) * STR]);
+        const double2 x1 = ElemT<E>::ld(x[u][(1 << SH) * PD * (MUL == 0 ? G : MUL) + (P - 1) * STR]);
         tl[u][0] = op.dt[0] * x1.x;
         tl[u][1] = op.dt[S::TAIL ? 1 : 0] * x1.x;
         tl[u][2] = op.dt[0] * x1.y;
@@ -1236,14 +1240,30 @@ __device__ __forceinline__ void ws_issue(const TransArgs& a, const unsigned char
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) nbytes += __shfl_xor_sync(0xffffffffu, nbytes, o);
   E* sb = ring + s * STAGE;
+  // uniform tile: G groups of one B with consecutive A' (the common case) --
+  // every child slot's G arrays are contiguous in HBM and in the slot-major
+  // stage, so one bulk copy (or one zero-fill) per child slot
+  const int ng = (int)min((int64_t)G, a.ngroups - tile * G);
+  const uint32_t m0 = __shfl_sync(0xffffffffu, gr.y, 0), p0 = __shfl_sync(0xffffffffu, gr.x, 0);
+  const bool mine_ok = lane >= G || (gr.y == m0 && gr.x == p0 + (uint32_t)lane);
+  const bool uniform = __all_sync(0xffffffffu, mine_ok) && ng == G && m0 != 0u;
   {
-    const int ng = (int)min((int64_t)G, a.ngroups - tile * G);
     constexpr int CH = PD * (int)sizeof(E) / 16;  // 16-byte chunks per slot
-    for (int js = 0; js < ng * NS; ++js) {
-      const uint32_t mB = __shfl_sync(0xffffffffu, gr.y, js / NS);
-      if (mB >> (js % NS) & 1) continue;
-      float4* z = reinterpret_cast<float4*>(sb + (int64_t)js * PD);
-      for (int q = lane; q < CH; q += 32) z[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (uniform) {
+      for (int c = 0; c < NS; ++c) {
+        if (m0 >> c & 1) continue;
+        float4* z = reinterpret_cast<float4*>(sb + (int64_t)c * G * PD);
+        for (int q = lane; q < G * CH; q += 32) z[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    } else {
+      // zero the slots of absent children: the consumers read every slot unmasked
+      for (int js = 0; js < ng * NS; ++js) {
+        const int j = js / NS, c = js % NS;
+        const uint32_t mB = __shfl_sync(0xffffffffu, gr.y, j);
+        if (mB >> c & 1) continue;
+        float4* z = reinterpret_cast<float4*>(sb + ((int64_t)c * G + j) * PD);
+        for (int q = lane; q < CH; q += 32) z[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncwarp();
@@ -1259,6 +1279,26 @@ __device__ __forceinline__ void ws_issue(const TransArgs& a, const unsigned char
         : "memory");
   }
   __syncwarp();
+  if (uniform) {
+    // lane c < NS: child slot c of all G groups, one copy of G arrays
+    if (lane < NS && (m0 >> lane & 1)) {
+      const int r = __popc(m0 & ((1u << lane) - 1u));
+      const int64_t pin = (int64_t)p0 + (int64_t)r * a.in_nA;
+#ifndef SFT_ABL_NOLOAD
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              smem_u32(sb + (int64_t)lane * G * PD)),
+          "l"(ain + pin * PD), "r"((uint32_t)(G * PD * sizeof(E))), "r"(smem_u32(&full[s]))
+          : "memory");
+#else
+      (void)pin;
+      asm volatile("mbarrier.complete_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&full[s])),
+                   "r"((uint32_t)(G * PD * sizeof(E)))
+                   : "memory");
+#endif
+    }
+    return;
+  }
   uint32_t mm = gr.y;
   int r = 0;
   while (mm) {
@@ -1268,7 +1308,7 @@ __device__ __forceinline__ void ws_issue(const TransArgs& a, const unsigned char
 #ifndef SFT_ABL_NOLOAD
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_u32(sb + ((int64_t)lane * NS + c) * PD)),
+            smem_u32(sb + ((int64_t)c * G + lane) * PD)),
         "l"(ain + pin * PD), "r"((uint32_t)(PD * sizeof(E))), "r"(smem_u32(&full[s]))
         : "memory");
 #else
@@ -1477,11 +1517,11 @@ __global__ __launch_bounds__((NC + (SELF ? 0 : 1)) * 32, MINB) void k_translate_
         consumer_pass<D, P, G, NC, 0, false, 0, E>(a, sb, bk0, op, rot, 0, s_dummy);
         consumer_pass<D, P, G, NC, 1, false, 3, E>(a, sb, bk0, op, rot, 0, s_dummy);
         consumer_sync<NC * 32>();
-        consumer_pass<D, P, G, NC, 1, false, 1, E, false, 1 << D>(a, sb, bk1, op, rot, 0, s_dummy);
-        consumer_pass<D, P, G, NC, 0, false, 2, E, false, 1 << D>(a, sb, bk1, op, rot, 0, s_dummy);
+        consumer_pass<D, P, G, NC, 1, false, 1, E, false, 1>(a, sb, bk1, op, rot, 0, s_dummy);
+        consumer_pass<D, P, G, NC, 0, false, 2, E, false, 1>(a, sb, bk1, op, rot, 0, s_dummy);
         consumer_sync<NC * 32>();
-        consumer_pass<D, P, G, NC, 0, true, 0, E, false, 1 << D>(a, sb, bk1, op, rot, ooff(w), s_dummy);
-        consumer_pass<D, P, G, NC, 1, true, 3, E, false, 1 << D>(a, sb, bk1, op, rot, ooff(w), s_dummy);
+        consumer_pass<D, P, G, NC, 0, true, 0, E, false, 1>(a, sb, bk1, op, rot, ooff(w), s_dummy);
+        consumer_pass<D, P, G, NC, 1, true, 3, E, false, 1>(a, sb, bk1, op, rot, ooff(w), s_dummy);
       } else if constexpr (D == 2) {
         INSTR_T0(t1);
         first2d(sb, blk[s]);
@@ -1552,7 +1592,7 @@ __device__ __noinline__ int f32_consumer_pass(float2* __restrict__ out, float2* 
       const int f = tau % PF;
       const int ebase = (f / STR) * STR * P + f % STR;
       float2* s0 = sb + te.x + ebase;
-      float2* s1 = s0 + (1 << SH) * PS;
+      float2* s1 = s0 + (1 << SH) * G * PS;  // slot-major stage
       float2* o0;
       float2* o1;
       if (!LAST) {
