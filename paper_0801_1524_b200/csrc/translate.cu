@@ -1911,8 +1911,39 @@ __global__ __launch_bounds__(NT, SFT_FMA_MINB(NT)) void k_translate_fma(TransArg
 #endif
 template <int D, int P>
 struct WsCfg;
-template <> struct WsCfg<2, 5> { static constexpr int G = 16, NC = 4, NST = 3, MINB = 2; };
-template <> struct WsCfg<2, 7> { static constexpr int G = 8, NC = 4, NST = 3, MINB = 3; };
+#ifndef SFT_WS_G25
+#define SFT_WS_G25 8
+#endif
+#ifndef SFT_WS_NC25
+#define SFT_WS_NC25 4
+#endif
+#ifndef SFT_WS_NST25
+#define SFT_WS_NST25 3
+#endif
+#ifndef SFT_WS_MINB25
+#define SFT_WS_MINB25 3
+#endif
+#ifndef SFT_WS_G27
+#define SFT_WS_G27 4
+#endif
+#ifndef SFT_WS_NC27
+#define SFT_WS_NC27 4
+#endif
+#ifndef SFT_WS_NST27
+#define SFT_WS_NST27 4
+#endif
+#ifndef SFT_WS_MINB27
+#define SFT_WS_MINB27 4
+#endif
+// 2D p = 5 / 7 after the slot-major stage (translate ms, C0 | C2 geometry at p = 5:
+// (16,4,3,2) 0.074 | 0.653, (8,4,3,3) 0.061 | 0.515, (4,4,3,4) 0.051 | 0.610; C1 | C2 geometry at
+// p = 7: (8,4,3,3) 0.135 | 0.899, (4,4,4,4) 0.109 | 0.713, (2,4,3,4) 0.111 | 0.938)
+template <> struct WsCfg<2, 5> {
+  static constexpr int G = SFT_WS_G25, NC = SFT_WS_NC25, NST = SFT_WS_NST25, MINB = SFT_WS_MINB25;
+};
+template <> struct WsCfg<2, 7> {
+  static constexpr int G = SFT_WS_G27, NC = SFT_WS_NC27, NST = SFT_WS_NST27, MINB = SFT_WS_MINB27;
+};
 template <> struct WsCfg<2, 9> {
   static constexpr int G = SFT_WS_G29, NC = SFT_WS_NC29, NST = SFT_WS_NST29, MINB = SFT_WS_MINB29;
 };

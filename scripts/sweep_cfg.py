@@ -11,7 +11,7 @@ import paper_0801_1524_b200 as sft  # noqa: E402
 import synth  # noqa: E402
 
 name = sys.argv[1]
-w = synth.make_workload(name)
+w = synth.make_workload(name, p=int(os.environ['SWEEP_P']) if os.environ.get('SWEEP_P') else None)
 x = torch.from_numpy(w.x).cuda(); k = torch.from_numpy(w.k).cuda(); f = torch.from_numpy(w.f).cuda()
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 with sft.Plan(w.dim, w.N, w.p, x, k, precision=int(os.environ.get('SWEEP_PREC', '0'))) as pl:
