@@ -54,6 +54,41 @@ __global__ void k_leaf_keys(const double* __restrict__ x, int64_t nx, const doub
   idx[i] = (int32_t)i;
 }
 
+// Small trees (<= kBlockSortMax points each): both trees sorted in one launch,
+// one 1024-thread block per tree with a block-wide radix sort in shared memory
+// (cub::BlockRadixSort: stable, so ties keep the input = index order exactly as
+// the device-wide sort).  Keys are compared on bits [0, bits); padding items
+// carry all-ones keys and sort behind every real item (stable).
+constexpr int kBlockSortItems = 16;
+constexpr int kBlockSortMax = 1024 * kBlockSortItems;
+template <typename KT>
+__global__ __launch_bounds__(1024) void k_block_sort(const KT* __restrict__ kin, const int32_t* __restrict__ iin,
+                                                     KT* __restrict__ kout, int32_t* __restrict__ iout, int64_t nx,
+                                                     int64_t nk, int bits) {
+  using BRS = cub::BlockRadixSort<KT, 1024, kBlockSortItems, int32_t>;
+  extern __shared__ __align__(16) unsigned char bs_smem[];
+  auto& tmp = *reinterpret_cast<typename BRS::TempStorage*>(bs_smem);
+  const int64_t lo = blockIdx.x == 0 ? 0 : nx;
+  const int64_t n = blockIdx.x == 0 ? nx : nk;
+  KT k[kBlockSortItems];
+  int32_t v[kBlockSortItems];
+#pragma unroll
+  for (int i = 0; i < kBlockSortItems; ++i) {
+    const int64_t idx = (int64_t)threadIdx.x * kBlockSortItems + i;
+    k[i] = idx < n ? kin[lo + idx] : ~(KT)0;
+    v[i] = idx < n ? iin[lo + idx] : INT32_MAX;
+  }
+  BRS(tmp).SortBlockedToStriped(k, v, 0, bits);
+#pragma unroll
+  for (int i = 0; i < kBlockSortItems; ++i) {
+    const int64_t pos = (int64_t)i * 1024 + threadIdx.x;
+    if (pos < n) {
+      kout[lo + pos] = k[i];
+      iout[lo + pos] = v[i];
+    }
+  }
+}
+
 struct BlockMap {
   int64_t nx, n;
   int nbx;  // blocks covering [0, nx); blocks >= nbx cover [nx, n)
@@ -240,7 +275,12 @@ static int sort_and_fill(sft_plan_s* P, const double* x_dev, const double* k_dev
   const int nbx = (int)nblk(nx, kBlk), nbk = (int)nblk(nk, kBlk);
   const int bits = d * L + 1;
   SortCache& C = g_sort;
-  const bool use_graph = sort_graph_enabled() && n >= 32768;  // small sorts: one CUB single-tile kernel
+  // trees of <= kBlockSortMax points: one block-sort launch; larger: the cached
+  // graph of the device-wide sort (or the plain call, SFT_SORT_GRAPH=0)
+  constexpr bool bs_fits =
+      sizeof(typename cub::BlockRadixSort<KT, 1024, kBlockSortItems, int32_t>::TempStorage) <= 200 * 1024;
+  const bool block_sort = bs_fits && nx <= kBlockSortMax && nk <= kBlockSortMax && n >= 4096 && sort_graph_enabled();
+  const bool use_graph = sort_graph_enabled() && n >= 4096 && !block_sort;
   int dev = 0;
   CK(cudaGetDevice(&dev));
   const bool hit = use_graph && C.exec && C.n == n && C.bits == bits && C.ksz == (int)sizeof(KT) &&
@@ -249,7 +289,7 @@ static int sort_and_fill(sft_plan_s* P, const double* x_dev, const double* k_dev
   // key array, the tree bit is constant in each; each sort is latency-bound, so
   // two half-size sorts side by side take ~60% of one full-size sort)
   size_t cub_bytes = 0, cub_x = 0, cub_k = 0;
-  if (!hit && !use_graph)
+  if (!hit && !use_graph && !block_sort)
     CK(cub::DeviceRadixSort::SortPairs(nullptr, cub_bytes, (KT*)nullptr, (KT*)nullptr, (int32_t*)nullptr,
                                        (int32_t*)nullptr, (int)n, 0, bits, s));
   if (use_graph) {
@@ -299,7 +339,21 @@ static int sort_and_fill(sft_plan_s* P, const double* x_dev, const double* k_dev
   count_launch();
   CK(cudaGetLastError());
   trace_mark("keys", s, true);
-  if (!use_graph) {
+  if (block_sort) {
+    if constexpr (bs_fits) {
+    using BRS = cub::BlockRadixSort<KT, 1024, kBlockSortItems, int32_t>;
+    const size_t bsm = sizeof(typename BRS::TempStorage);
+    static bool attr = false;
+    if (!attr) {
+      CK(cudaFuncSetAttribute(k_block_sort<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm));
+      attr = true;
+    }
+    // (the tree bit above bit d*L is constant within a tree)
+    k_block_sort<KT><<<2, 1024, bsm, s>>>(keys_in, idx_in, keys_out, idx_out, nx, nk, bits - 1);
+    count_launch();
+    CK(cudaGetLastError());
+    }
+  } else if (!use_graph) {
     CK(cub::DeviceRadixSort::SortPairs(scr + s_cub, cub_bytes, keys_in, keys_out, idx_in, idx_out, (int)n, 0, bits, s));
   } else {
     if (!hit) {
