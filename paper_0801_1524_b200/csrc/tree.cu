@@ -59,13 +59,16 @@ __global__ void k_leaf_keys(const double* __restrict__ x, int64_t nx, const doub
 // (cub::BlockRadixSort: stable, so ties keep the input = index order exactly as
 // the device-wide sort).  Keys are compared on bits [0, bits); padding items
 // carry all-ones keys and sort behind every real item (stable).
+#ifndef SFT_BS_BITS
+#define SFT_BS_BITS 4  // radix digit bits of the block sort
+#endif
 constexpr int kBlockSortItems = 16;
 constexpr int kBlockSortMax = 1024 * kBlockSortItems;
 template <typename KT>
 __global__ __launch_bounds__(1024) void k_block_sort(const KT* __restrict__ kin, const int32_t* __restrict__ iin,
                                                      KT* __restrict__ kout, int32_t* __restrict__ iout, int64_t nx,
                                                      int64_t nk, int bits) {
-  using BRS = cub::BlockRadixSort<KT, 1024, kBlockSortItems, int32_t>;
+  using BRS = cub::BlockRadixSort<KT, 1024, kBlockSortItems, int32_t, SFT_BS_BITS>;
   extern __shared__ __align__(16) unsigned char bs_smem[];
   auto& tmp = *reinterpret_cast<typename BRS::TempStorage*>(bs_smem);
   const int64_t lo = blockIdx.x == 0 ? 0 : nx;
@@ -278,7 +281,7 @@ static int sort_and_fill(sft_plan_s* P, const double* x_dev, const double* k_dev
   // trees of <= kBlockSortMax points: one block-sort launch; larger: the cached
   // graph of the device-wide sort (or the plain call, SFT_SORT_GRAPH=0)
   constexpr bool bs_fits =
-      sizeof(typename cub::BlockRadixSort<KT, 1024, kBlockSortItems, int32_t>::TempStorage) <= 200 * 1024;
+      sizeof(typename cub::BlockRadixSort<KT, 1024, kBlockSortItems, int32_t, SFT_BS_BITS>::TempStorage) <= 200 * 1024;
   const bool block_sort = bs_fits && nx <= kBlockSortMax && nk <= kBlockSortMax && n >= 4096 && sort_graph_enabled();
   const bool use_graph = sort_graph_enabled() && n >= 4096 && !block_sort;
   int dev = 0;
@@ -341,7 +344,7 @@ static int sort_and_fill(sft_plan_s* P, const double* x_dev, const double* k_dev
   trace_mark("keys", s, true);
   if (block_sort) {
     if constexpr (bs_fits) {
-    using BRS = cub::BlockRadixSort<KT, 1024, kBlockSortItems, int32_t>;
+    using BRS = cub::BlockRadixSort<KT, 1024, kBlockSortItems, int32_t, SFT_BS_BITS>;
     const size_t bsm = sizeof(typename BRS::TempStorage);
     static bool attr = false;
     if (!attr) {
