@@ -226,6 +226,62 @@ __global__ __launch_bounds__(kBlk) void k_fill(const KT* __restrict__ key, const
 
 static inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
+// CUB radix-sort tuning for the tree build: the onesweep digit width (the
+// keys have d*L (+1) <= 29 bits at the BASELINE configs, so 10-bit digits need
+// 3 passes where CUB's default 8-bit digits need 4) and items per thread.
+// Everything else as CUB's SM100 policy.
+#ifndef SFT_SORT_BITS
+#define SFT_SORT_BITS 8
+#endif
+#ifndef SFT_SORT_ITEMS
+#define SFT_SORT_ITEMS 12  // C2 plan -8 us vs CUB's 23 (more, shorter tiles for ~150K keys)
+#endif
+#ifndef SFT_SORT_THREADS
+#define SFT_SORT_THREADS 384
+#endif
+template <typename KeyT, typename ValueT, typename OffsetT>
+struct SortHub {
+  using DominantT = ::cuda::std::_If<(sizeof(ValueT) > sizeof(KeyT)), ValueT, KeyT>;
+  struct Policy1000 : cub::ChainedPolicy<1000, Policy1000, Policy1000> {
+    static constexpr bool ONESWEEP = true;
+    static constexpr int ONESWEEP_RADIX_BITS = SFT_SORT_BITS;
+    using HistogramPolicy = cub::AgentRadixSortHistogramPolicy<128, 16, 1, KeyT, ONESWEEP_RADIX_BITS>;
+    using ExclusiveSumPolicy = cub::AgentRadixSortExclusiveSumPolicy<256, ONESWEEP_RADIX_BITS>;
+    using OnesweepPolicy =
+        cub::AgentRadixSortOnesweepPolicy<SFT_SORT_THREADS, SFT_SORT_ITEMS, DominantT, 1, cub::RADIX_RANK_MATCH_EARLY_COUNTS_ANY,
+                                          cub::BLOCK_SCAN_RAKING_MEMOIZE, cub::RADIX_SORT_STORE_DIRECT,
+                                          ONESWEEP_RADIX_BITS>;
+    using ScanPolicy = cub::AgentScanPolicy<512, 23, OffsetT, cub::BLOCK_LOAD_WARP_TRANSPOSE, cub::LOAD_DEFAULT,
+                                            cub::BLOCK_STORE_WARP_TRANSPOSE, cub::BLOCK_SCAN_RAKING_MEMOIZE>;
+    using DownsweepPolicy =
+        cub::AgentRadixSortDownsweepPolicy<512, 23, DominantT, cub::BLOCK_LOAD_TRANSPOSE, cub::LOAD_DEFAULT,
+                                           cub::RADIX_RANK_MATCH, cub::BLOCK_SCAN_WARP_SCANS, 7>;
+    using AltDownsweepPolicy =
+        cub::AgentRadixSortDownsweepPolicy<256, 47, DominantT, cub::BLOCK_LOAD_TRANSPOSE, cub::LOAD_DEFAULT,
+                                           cub::RADIX_RANK_MEMOIZE, cub::BLOCK_SCAN_WARP_SCANS, 6>;
+    using UpsweepPolicy = cub::AgentRadixSortUpsweepPolicy<256, 23, DominantT, cub::LOAD_DEFAULT, 7>;
+    using AltUpsweepPolicy = cub::AgentRadixSortUpsweepPolicy<256, 47, DominantT, cub::LOAD_DEFAULT, 6>;
+    using SingleTilePolicy =
+        cub::AgentRadixSortDownsweepPolicy<256, 19, DominantT, cub::BLOCK_LOAD_DIRECT, cub::LOAD_LDG,
+                                           cub::RADIX_RANK_MEMOIZE, cub::BLOCK_SCAN_WARP_SCANS, 6>;
+    using SegmentedPolicy =
+        cub::AgentRadixSortDownsweepPolicy<192, 39, DominantT, cub::BLOCK_LOAD_TRANSPOSE, cub::LOAD_DEFAULT,
+                                           cub::RADIX_RANK_MEMOIZE, cub::BLOCK_SCAN_WARP_SCANS, 6>;
+    using AltSegmentedPolicy =
+        cub::AgentRadixSortDownsweepPolicy<384, 11, DominantT, cub::BLOCK_LOAD_TRANSPOSE, cub::LOAD_DEFAULT,
+                                           cub::RADIX_RANK_MEMOIZE, cub::BLOCK_SCAN_WARP_SCANS, 5>;
+  };
+  using MaxPolicy = Policy1000;
+};
+template <typename KT>
+static cudaError_t sort_pairs(void* temp, size_t& bytes, const KT* kin, KT* kout, const int32_t* iin, int32_t* iout,
+                              int n, int bits, cudaStream_t s) {
+  cub::DoubleBuffer<KT> dk(const_cast<KT*>(kin), kout);
+  cub::DoubleBuffer<int32_t> dv(const_cast<int32_t*>(iin), iout);
+  return cub::DispatchRadixSort<false, KT, int32_t, int, SortHub<KT, int32_t, int>>::Dispatch(
+      temp, bytes, dk, dv, n, 0, bits, false, s);
+}
+
 // Per-thread cache of the tree-build scratch and of an instantiated CUDA graph
 // of the CUB radix sort for one (point count, key bits, key type): plans built
 // back to back with the same sizes replay the graph (a few us of host time
@@ -296,10 +352,10 @@ static int sort_and_fill(sft_plan_s* P, const double* x_dev, const double* k_dev
     CK(cub::DeviceRadixSort::SortPairs(nullptr, cub_bytes, (KT*)nullptr, (KT*)nullptr, (int32_t*)nullptr,
                                        (int32_t*)nullptr, (int)n, 0, bits, s));
   if (use_graph) {
-    CK(cub::DeviceRadixSort::SortPairs(nullptr, cub_x, (KT*)nullptr, (KT*)nullptr, (int32_t*)nullptr,
-                                       (int32_t*)nullptr, (int)nx, 0, bits - 1, s));
-    CK(cub::DeviceRadixSort::SortPairs(nullptr, cub_k, (KT*)nullptr, (KT*)nullptr, (int32_t*)nullptr,
-                                       (int32_t*)nullptr, (int)nk, 0, bits - 1, s));
+    CK(sort_pairs<KT>(nullptr, cub_x, (KT*)nullptr, (KT*)nullptr, (int32_t*)nullptr, (int32_t*)nullptr, (int)nx,
+                      bits - 1, s));
+    CK(sort_pairs<KT>(nullptr, cub_k, (KT*)nullptr, (KT*)nullptr, (int32_t*)nullptr, (int32_t*)nullptr, (int)nk,
+                      bits - 1, s));
     cub_bytes = align_up(cub_x, 256) + cub_k;
   }
   size_t so = 0;
@@ -370,10 +426,9 @@ static int sort_and_fill(sft_plan_s* P, const double* x_dev, const double* k_dev
       cudaEventRecord(fork, cs);
       cudaStreamWaitEvent(cs2, fork, 0);
       const size_t ox = align_up(cub_x, 256);
-      cudaError_t ce = cub::DeviceRadixSort::SortPairs(scr + s_cub, cub_x, keys_in, keys_out, idx_in, idx_out,
-                                                       (int)nx, 0, bits - 1, cs);
-      cudaError_t ce3 = cub::DeviceRadixSort::SortPairs(scr + s_cub + ox, cub_k, keys_in + nx, keys_out + nx,
-                                                        idx_in + nx, idx_out + nx, (int)nk, 0, bits - 1, cs2);
+      cudaError_t ce = sort_pairs<KT>(scr + s_cub, cub_x, keys_in, keys_out, idx_in, idx_out, (int)nx, bits - 1, cs);
+      cudaError_t ce3 = sort_pairs<KT>(scr + s_cub + ox, cub_k, keys_in + nx, keys_out + nx, idx_in + nx, idx_out + nx,
+                                       (int)nk, bits - 1, cs2);
       cudaEventRecord(join, cs2);
       cudaStreamWaitEvent(cs, join, 0);
       cudaGraph_t g = nullptr;
