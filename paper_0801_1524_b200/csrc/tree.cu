@@ -28,6 +28,25 @@ namespace sft {
 
 constexpr int kBlk = 1024;  // points per block in k_count / k_fill
 
+__device__ __forceinline__ uint64_t spread2(uint64_t x) {  // bit b -> bit 2b
+  x &= 0xFFFFFFFFull;
+  x = (x | (x << 16)) & 0x0000FFFF0000FFFFull;
+  x = (x | (x << 8)) & 0x00FF00FF00FF00FFull;
+  x = (x | (x << 4)) & 0x0F0F0F0F0F0F0F0Full;
+  x = (x | (x << 2)) & 0x3333333333333333ull;
+  x = (x | (x << 1)) & 0x5555555555555555ull;
+  return x;
+}
+__device__ __forceinline__ uint64_t spread3(uint64_t x) {  // bit b -> bit 3b (b < 21)
+  x &= 0x1FFFFFull;
+  x = (x | (x << 32)) & 0x1F00000000FFFFull;
+  x = (x | (x << 16)) & 0x1F0000FF0000FFull;
+  x = (x | (x << 8)) & 0x100F00F00F00F00Full;
+  x = (x | (x << 4)) & 0x10C30C30C30C30C3ull;
+  x = (x | (x << 2)) & 0x1249249249249249ull;
+  return x;
+}
+
 template <typename KT>
 __global__ void k_leaf_keys(const double* __restrict__ x, int64_t nx, const double* __restrict__ k, int64_t nk,
                             int d, int L, double Nf, int64_t N, KT* __restrict__ key,
@@ -47,9 +66,15 @@ __global__ void k_leaf_keys(const double* __restrict__ x, int64_t nx, const doub
     if (ci > N - 1) ci = N - 1;
     c[a] = (uint64_t)ci;
   }
-  uint64_t kk = tk ? 1ull : 0ull;
-  for (int b = L - 1; b >= 0; --b)
-    for (int a = 0; a < d; ++a) kk = (kk << 1) | ((c[a] >> b) & 1ull);
+  // Morton interleave, axis 0 the most significant bit of each d-bit digit, tree
+  // bit above the d*L key bits (bit spreading by magic masks; c < 2^20)
+  uint64_t kk;
+  if (d == 2) {
+    kk = (spread2(c[0]) << 1) | spread2(c[1]);
+  } else {
+    kk = (spread3(c[0]) << 2) | (spread3(c[1]) << 1) | spread3(c[2]);
+  }
+  kk |= (tk ? 1ull : 0ull) << (d * L);
   key[i] = (KT)kk;
   idx[i] = (int32_t)i;
 }
