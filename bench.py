@@ -181,7 +181,6 @@ def run_ours(args):
     w = synth.make_workload(args.config)
     P = w.P
     prec = 1 if args.precision == "f32" else 0
-    fused = args.exchange == "fused"
     x = torch.from_numpy(w.x).to(dev)
     k = torch.from_numpy(w.k).to(dev)
     f = torch.from_numpy(w.f).to(dev)
@@ -199,7 +198,7 @@ def run_ours(args):
             with sft.Plan(w.dim, w.N, w.p, x, k, stream=stream, precision=prec) as plan:
                 plan.apply(f, u)
         else:
-            with DistPlan(w.dim, w.N, w.p, x, k, stream=stream, fused=fused) as dp:
+            with DistPlan(w.dim, w.N, w.p, x, k, stream=stream, exchange=args.exchange) as dp:
                 dp.apply(f, u)
 
     def timed(fn, K, do_flush=True):
@@ -264,7 +263,7 @@ def run_ours(args):
             batch = {"nrhs": R, "skipped": f"level buffers {need / 1e9:.1f} GB"}
         plan.close()
     else:
-        dp = DistPlan(w.dim, w.N, w.p, x, k, stream=stream, fused=fused)
+        dp = DistPlan(w.dim, w.N, w.p, x, k, stream=stream, exchange=args.exchange)
         for _ in range(max(2, args.warmup)):
             dp.apply(f, u)
         apply_total, _ = timed(lambda: dp.apply(f, u), args.steps)
@@ -301,7 +300,7 @@ def run_ours(args):
                 plan.apply(fh, uh)
         else:
             xd, kd, fd = xh.to(dev, non_blocking=True), kh.to(dev, non_blocking=True), fh.to(dev, non_blocking=True)
-            with DistPlan(w.dim, w.N, w.p, xd, kd, stream=stream, fused=fused) as dp:
+            with DistPlan(w.dim, w.N, w.p, xd, kd, stream=stream, exchange=args.exchange) as dp:
                 ud = dp.apply(fd)
             uh.copy_(ud)
 
@@ -488,14 +487,28 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-targets", type=int, default=256)
-    ap.add_argument("--exchange", default="nccl", choices=["nccl", "fused"],
-                    help="N > 1: level-m exchange by NCCL all-to-all, or fused into the exchange level's kernel "
-                         "(peer stores into IPC-mapped receive buffers over NVLink)")
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "fused", "torch"],
+                    help="N > 1: level-m exchange and u all-gather by libsft's own NCCL calls (default), fused into "
+                         "the exchange level's kernel (peer stores into IPC-mapped receive buffers over NVLink), or "
+                         "torch.distributed collectives around the phase calls")
     ap.add_argument("--nrhs", type=int, default=4,
                     help="N = 1: also time sft_apply_batch with this many charge vectors (1 = skip)")
     ap.add_argument("--precision", default="f64", choices=["f64", "f32"],
                     help="arithmetic of the level charges (f32: the optional FP32 variant, single GPU)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: relaunch under torchrun (the driver launches us that way itself)
+        import socket
+        sk = socket.socket()
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+        sk.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
+    world_env = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.impl == "ours" and world_env != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world_env}")
     if args.warmup < 3:
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
     if args.impl == "reference":

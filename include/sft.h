@@ -50,6 +50,7 @@ enum {
   SFT_E_NOMEM = 3,   /* device or host allocation failed */
   SFT_E_CUDA = 4,    /* CUDA runtime error (message in sft_last_error) */
   SFT_E_STATE = 5,   /* call not valid for this plan (e.g. phase order, world size) */
+  SFT_E_NCCL = 6,    /* NCCL unavailable or a collective failed (message in sft_last_error) */
 };
 
 typedef struct sft_plan_s* sft_plan_t;
@@ -70,9 +71,19 @@ typedef struct {
                        *    butterfly with the roles of the point sets swapped and the
                        *    charges / potentials conjugated; sft_apply then takes g [nx]
                        *    and writes v [nk].  0 = forward (default).  world == 1 only. */
+  const void* nccl_id;  /* world > 1: a 128-byte ncclUniqueId (from sft_nccl_unique_id on one
+                         * rank, broadcast to all ranks by the caller, e.g. torch.distributed).
+                         * With it, sft_plan joins / reuses the NCCL communicator of that id
+                         * (ncclCommInitRank on the first plan of a rank with this id: every
+                         * rank must plan concurrently) and sft_apply runs the whole sharded
+                         * transform, exchange and u all-gather included.  NULL (default):
+                         * the caller drives the phase calls and the collective itself.
+                         * world == 1 with nccl_id and exchange_level >= 0 runs the sharded
+                         * path on a single rank (self send/recv; a test of the machinery). */
 } sft_opts;
 
-/* Fill *o with defaults: FP64, NULL stream, rank 0, world 1, automatic levels, forward. */
+/* Fill *o with defaults: FP64, NULL stream, rank 0, world 1, automatic levels, forward,
+ * no NCCL id. */
 void sft_default_opts(sft_opts* o);
 
 /* Step 1: build T_X from targets x and T_K from sources k.
@@ -83,7 +94,15 @@ int sft_plan(int dim, int64_t N, int p, const double* x, int64_t nx, const doubl
              const sft_opts* opts, sft_plan_t* out);
 
 /* Steps 2-4: u = butterfly(f).  f: [nk] complex128, u: [nx]
- * complex128, host or device.  Only valid for world == 1 plans. */
+ * complex128, host or device.  A host f may be modified as soon as the call
+ * returns (the call waits for its staging copy); a host u is complete on return.
+ * Sharded plans (world > 1) need opts.nccl_id at plan time: every rank passes
+ * the full f and gets the full u -- phase 1 over its T_K subtrees, the level-m
+ * exchange as grouped ncclSend/ncclRecv, phase 2 over its T_X subtrees, an
+ * ncclAllGather of the potentials and a scatter to user order, all on the plan
+ * stream; bitwise equal to the world == 1 result.
+ * SFT_E_STATE for a sharded plan without an NCCL id (use the phase calls);
+ * SFT_E_NCCL if a collective fails. */
 int sft_apply(sft_plan_t plan, const void* f, void* u);
 
 /* Multi-RHS apply: u_r = butterfly(f_r) for nrhs
@@ -149,11 +168,20 @@ int sft_translation_launches(sft_plan_t plan, int* n, int* out_level, int* two_l
 int sft_set_timing(sft_plan_t plan, int enable);
 int sft_last_timing(sft_plan_t plan, double* t_ms, double* per_level_ms);
 
+/* NCCL id for opts.nccl_id (ncclGetUniqueId; libnccl.so.2 is dlopen'ed: the
+ * NCCL already loaded in the process, e.g. torch's, is used).  id128: 128
+ * bytes.  SFT_E_NCCL if NCCL cannot be loaded. */
+int sft_nccl_unique_id(void* id128);
+/* Destroy this process's communicators of that id (plans using it must be
+ * destroyed first).  Unknown ids are a no-op. */
+int sft_nccl_release(const void* id128);
+
 /* ---- multi-GPU (world > 1), SURVEY.md §8(e) ----------------------------
  * Phase 1 (levels t = L..m) over this rank's T_K subtrees at level s_K,
  * one all-to-all of the level-m charges, phase 2 (t = m-1..0 and step 4) over
- * this rank's T_X subtrees at level s_X.  The collective itself is issued by
- * the caller (torch.distributed over NCCL) between the two calls.
+ * this rank's T_X subtrees at level s_X.  With opts.nccl_id sft_apply does all
+ * of it; the phase calls below let the caller drive the steps and the
+ * collective itself (torch.distributed, the fused exchange, tests).
  *
  * sft_exchange_counts: send_counts/recv_counts [world] in complex128 elements
  *   (contiguous per-peer segments in rank order).

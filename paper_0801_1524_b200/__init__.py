@@ -21,7 +21,8 @@ import os
 
 import numpy as np
 
-__all__ = ["Plan", "lib", "LIB_PATH", "SftError", "operator_tables", "choose_partition", "HEADER_SYMBOLS", "launch_count"]
+__all__ = ["Plan", "lib", "LIB_PATH", "SftError", "operator_tables", "choose_partition", "HEADER_SYMBOLS", "launch_count",
+           "nccl_unique_id", "nccl_release"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("SFT_LIB", os.path.join(_HERE, "libsft.so"))
@@ -38,7 +39,7 @@ class SftError(RuntimeError):
 class _Opts(ctypes.Structure):
     _fields_ = [("precision", ctypes.c_int), ("stream", ctypes.c_void_p), ("rank", ctypes.c_int),
                 ("world", ctypes.c_int), ("exchange_level", ctypes.c_int), ("split_k", ctypes.c_int),
-                ("split_x", ctypes.c_int), ("adjoint", ctypes.c_int)]
+                ("split_x", ctypes.c_int), ("adjoint", ctypes.c_int), ("nccl_id", ctypes.c_void_p)]
 
 
 _lib = None
@@ -97,6 +98,8 @@ def lib():
                                        ctypes.c_int, _c_i64p, _c_i64p]
     L.sft_operator_tables.argtypes = [ctypes.c_int, _c_dp, _c_dp, _c_dp, _c_dp]
     L.sft_launch_count.argtypes = [_c_i64p]
+    L.sft_nccl_unique_id.argtypes = [ctypes.c_char_p]
+    L.sft_nccl_release.argtypes = [ctypes.c_char_p]
     _lib = L
     return L
 
@@ -107,17 +110,27 @@ def _check(rc):
         raise SftError(f"{L.sft_strerror(rc).decode()} ({rc}): {L.sft_last_error().decode()}")
 
 
-def _ptr(a, dtype_np, shape_last=None):
-    """Return (pointer, keepalive) for a torch tensor or numpy array, contiguous, right dtype."""
+def _ptr(a, dtype_np, out=False):
+    """Return (pointer, keepalive) for a torch tensor or numpy array, contiguous, right dtype.
+    Inputs are converted if needed; an output buffer (out=True) must already be
+    contiguous with the right dtype -- the library writes into it, so a converted
+    temporary would silently drop the result."""
     try:
         import torch
         if isinstance(a, torch.Tensor):
             want = {np.float64: torch.float64, np.complex128: torch.complex128}[dtype_np]
             if a.dtype != want or not a.is_contiguous():
+                if out:
+                    raise ValueError(f"output buffer must be a contiguous {want} tensor (got {a.dtype}, "
+                                     f"contiguous={a.is_contiguous()})")
                 a = a.to(want).contiguous()
             return ctypes.c_void_p(a.data_ptr()), a
     except ImportError:  # pragma: no cover
         pass
+    if out:
+        if not (isinstance(a, np.ndarray) and a.dtype == dtype_np and a.flags.c_contiguous and a.flags.writeable):
+            raise ValueError(f"output buffer must be a writeable C-contiguous {np.dtype(dtype_np)} array")
+        return ctypes.c_void_p(a.ctypes.data), a
     a = np.ascontiguousarray(a, dtype=dtype_np)
     return ctypes.c_void_p(a.ctypes.data), a
 
@@ -140,11 +153,13 @@ class Plan:
     """sft_plan / sft_apply / sft_destroy (include/sft.h)."""
 
     def __init__(self, dim, N, p, x, k, stream=None, rank=0, world=1, exchange_level=-1, split_k=-1, split_x=-1,
-                 precision=0, adjoint=False):
+                 precision=0, adjoint=False, nccl_id=None):
         """precision 0: FP64 charges (default); 1: the FP32 variant (single GPU;
         f and u stay complex128 at the boundary, the level charges are complex64).
         adjoint=True: apply() computes v_j = sum_i exp(-2 pi i x_i.k_j/N) g_i
-        (g on the x points, v on the k points)."""
+        (g on the x points, v on the k points).  nccl_id (128 bytes, from
+        nccl_unique_id() on one rank, shared by all): apply() runs the whole
+        sharded transform with the library's own NCCL collectives."""
         L = lib()
         o = _Opts()
         L.sft_default_opts(ctypes.byref(o))
@@ -153,6 +168,12 @@ class Plan:
         o.stream = _stream_handle(stream)
         o.rank, o.world = int(rank), int(world)
         o.exchange_level, o.split_k, o.split_x = int(exchange_level), int(split_k), int(split_x)
+        self._nid = None
+        if nccl_id is not None:
+            if len(nccl_id) != 128:
+                raise ValueError("nccl_id must be 128 bytes")
+            self._nid = ctypes.create_string_buffer(bytes(nccl_id), 128)
+            o.nccl_id = ctypes.cast(self._nid, ctypes.c_void_p)
         xp, self._x = _ptr(x, np.float64)
         kp, self._k = _ptr(k, np.float64)
         self.dim, self.N, self.p = int(dim), int(N), int(p)
@@ -202,7 +223,7 @@ class Plan:
         fp, fk = _ptr(f, np.complex128)
         if u is None:
             u = self._like(fk, self.nk if self.adjoint else self.nx)
-        up, uk = _ptr(u, np.complex128)
+        up, uk = _ptr(u, np.complex128, out=True)
         _check(lib().sft_apply(self._h, fp, up))
         return uk
 
@@ -216,7 +237,7 @@ class Plan:
         nout = self.nk if self.adjoint else self.nx
         if u is None:
             u = self._like(fk, nrhs * nout).reshape(nrhs, nout)
-        up, uk = _ptr(u, np.complex128)
+        up, uk = _ptr(u, np.complex128, out=True)
         if tuple(uk.shape) != (nrhs, nout):
             raise ValueError("apply_batch: u must be [nrhs, n_out]")
         _check(lib().sft_apply_batch(self._h, nrhs, fp, ldf, up, nout))
@@ -251,7 +272,7 @@ class Plan:
         if sendbuf is None or isinstance(sendbuf, int):
             sp = ctypes.c_void_p(sendbuf or 0)
         else:
-            sp, _ = _ptr(sendbuf, np.complex128)
+            sp, _ = _ptr(sendbuf, np.complex128, out=True)
         _check(lib().sft_apply_phase1(self._h, fp, sp))
 
     def apply_phase2(self, recvbuf, u):
@@ -259,7 +280,7 @@ class Plan:
             rp = ctypes.c_void_p(recvbuf)
         else:
             rp, _ = _ptr(recvbuf, np.complex128)
-        up, _ = _ptr(u, np.complex128)
+        up, _ = _ptr(u, np.complex128, out=True)
         _check(lib().sft_apply_phase2(self._h, rp, up))
 
     def set_peer_buffers(self, ptrs):
@@ -344,6 +365,18 @@ def ipc_open(handle: bytes) -> int:
 
 def ipc_close(ptr: int) -> None:
     _check(lib().sft_ipc_close(ctypes.c_void_p(ptr)))
+
+
+def nccl_unique_id() -> bytes:
+    """sft_nccl_unique_id: a fresh 128-byte ncclUniqueId (call on one rank, share with all)."""
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().sft_nccl_unique_id(buf))
+    return buf.raw
+
+
+def nccl_release(nccl_id: bytes) -> None:
+    """sft_nccl_release: destroy this process's communicators of that id."""
+    _check(lib().sft_nccl_release(ctypes.create_string_buffer(bytes(nccl_id), 128)))
 
 
 def launch_count() -> int:

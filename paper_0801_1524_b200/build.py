@@ -15,7 +15,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(HERE, "build")
 LIB = os.path.join(HERE, "libsft.so")
-SOURCES = ["api.cu", "tree.cu", "kernels.cu", "translate.cu", "tables.cpp"]
+SOURCES = ["api.cu", "tree.cu", "kernels.cu", "translate.cu", "tables.cpp", "comm.cu"]
 HEADERS = [os.path.join(CSRC, "sft_internal.cuh"), os.path.join(HERE, "..", "include", "sft.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
@@ -66,7 +66,7 @@ def build(force: bool = False, verbose: bool = False, extra=(), out=None) -> str
     objs = [os.path.join(OBJ, os.path.splitext(f)[0] + tag + ".o") for f in srcs]
     with ThreadPoolExecutor(max_workers=len(srcs)) as ex:
         list(ex.map(lambda so: _compile(so[0], so[1], list(extra), verbose, force or bool(extra)), zip(srcs, objs)))
-    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", target + ".tmp", *objs]
+    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", target + ".tmp", *objs, "-ldl"]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)

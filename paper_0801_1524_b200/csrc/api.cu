@@ -66,6 +66,7 @@ extern "C" void sft_default_opts(sft_opts* o) {
   o->split_k = -1;
   o->split_x = -1;
   o->adjoint = 0;
+  o->nccl_id = nullptr;
 }
 
 extern "C" const char* sft_strerror(int status) {
@@ -76,6 +77,7 @@ extern "C" const char* sft_strerror(int status) {
     case SFT_E_NOMEM: return "out of memory";
     case SFT_E_CUDA: return "CUDA error";
     case SFT_E_STATE: return "invalid call for this plan";
+    case SFT_E_NCCL: return "NCCL error";
     default: return "unknown status";
   }
 }
@@ -321,7 +323,7 @@ static LevelDims level_dims_x(const sft_plan_s* P, int t) {
 // The dims of level t exactly as the apply calls use them (sft_apply, or the
 // two phases of a multi-rank plan, with the exchange layout at level m).
 static LevelDims apply_dims(const sft_plan_s* P, int t) {
-  if (P->world == 1) return level_dims_k(P, t);
+  if (!P->sharded) return level_dims_k(P, t);
   if (t >= P->part.m) {
     LevelDims ld = level_dims_k(P, t);
     if (t == P->part.m) {
@@ -412,7 +414,10 @@ static void plan_free(sft_plan_s* P) {
   if (P->f_stage) cudaFreeAsync(P->f_stage, s);
   if (P->u_stage) cudaFreeAsync(P->u_stage, s);
   if (P->d_seg) cudaFreeAsync(P->d_seg, s);
+  for (void* q : {(void*)P->xsend, (void*)P->xrecv, (void*)P->u_all, (void*)P->d_ubounds})
+    if (q) cudaFreeAsync(q, s);
   for (int i = 0; i < P->ev_created; ++i) cudaEventDestroy(P->ev[i]);
+  if (P->f_copied) cudaEventDestroy(P->f_copied);
   for (int i = 0; i < 2; ++i) ev_put(P->plan_ev[i], true, P->dev);
   ev_put(P->sched_fork, false, P->dev);
   ev_put(P->sched_ready, false, P->dev);
@@ -491,10 +496,10 @@ extern "C" int sft_plan(int dim, int64_t N, int p, const double* x, int64_t nx, 
   sft_default_opts(&o);
   if (opts) o = *opts;
   if (o.precision != 0 && o.precision != 1) return fail(SFT_E_ARG, "precision must be 0 (FP64) or 1 (FP32)");
-  if (o.precision == 1 && o.world != 1) return fail(SFT_E_ARG, "the FP32 variant is single-GPU (world == 1)");
   if (o.world < 1 || o.rank < 0 || o.rank >= o.world) return fail(SFT_E_ARG, "bad rank/world");
-
-  if (o.adjoint && o.world != 1) return fail(SFT_E_ARG, "the adjoint plan is single-GPU (world == 1)");
+  const bool sharded = o.world > 1 || (o.nccl_id != nullptr && o.exchange_level >= 0);
+  if (o.precision == 1 && sharded) return fail(SFT_E_ARG, "the FP32 variant is single-GPU (world == 1)");
+  if (o.adjoint && sharded) return fail(SFT_E_ARG, "the adjoint plan is single-GPU (world == 1)");
   if (o.adjoint) {
     // adjoint = conj o forward(targets k, sources x) o conj: swap the point sets
     std::swap(x, k);
@@ -513,6 +518,9 @@ extern "C" int sft_plan(int dim, int64_t N, int p, const double* x, int64_t nx, 
   P->nk = nk;
   P->rank = o.rank;
   P->world = o.world;
+  // sharded path: world > 1, or one rank forced onto it (nccl_id and an
+  // explicit exchange level: the exchange machinery on a single GPU)
+  P->sharded = sharded;
   P->prec = o.precision;
   {
     const int64_t pd = ipow64(p, dim);
@@ -585,7 +593,7 @@ extern "C" int sft_plan(int dim, int64_t N, int p, const double* x, int64_t nx, 
 
   // level buffers: max over t of (local) pairs(t)
   const int64_t PD = ipow64(p, dim);
-  if (P->world > 1) {
+  if (P->sharded) {
     // partition + per-rank ranges; needs parent arrays on the host
     std::vector<std::vector<int32_t>> px(L + 1), pk(L + 1);
     for (int l = 1; l <= L; ++l) {
@@ -650,6 +658,38 @@ extern "C" int sft_plan(int dim, int64_t N, int p, const double* x, int64_t nx, 
     }
     if (cudaMallocAsync(&P->d_seg, seg.size() * sizeof(int64_t), s) != cudaSuccess) return bail(SFT_E_NOMEM, "seg");
     cudaMemcpyAsync(P->d_seg, seg.data(), seg.size() * sizeof(int64_t), cudaMemcpyHostToDevice, s);
+    if (o.nccl_id) {
+      // in-library collectives: the communicator (cached per id),
+      // the exchange buffers, and the all-gather layout of u -- rank q's targets
+      // are the sorted points [xb[q], xb[q+1]) of its T_X subtrees
+      std::string nerr;
+      if (int nrc = nccl_comm_get(o.nccl_id, o.rank, W, &P->comm, &nerr)) return bail(nrc, nerr);
+      int64_t ns = 0, nr = 0;
+      for (int q = 0; q < W; ++q) {
+        ns += P->send_counts[q];
+        nr += P->recv_counts[q];
+      }
+      std::vector<int64_t> xb(W + 1, 0);
+      std::vector<int32_t> fp(W + 1, 0);
+      for (int q = 0; q <= W; ++q) {
+        descend_ranges(px, pt.sx, q < W ? pt.x_lo[q] : pt.x_hi[W - 1], q < W ? pt.x_hi[q] : pt.x_hi[W - 1], L, tmp);
+        cudaMemcpyAsync(&fp[q], P->X.first_pt + tmp[L].lo, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+      }
+      if (cudaStreamSynchronize(s) != cudaSuccess) return bail(SFT_E_CUDA, "sync");
+      int64_t mxc = 1;
+      for (int q = 0; q <= W; ++q) xb[q] = q < W ? fp[q] : nx;
+      xb[0] = 0;
+      for (int q = 0; q < W; ++q) mxc = std::max(mxc, xb[q + 1] - xb[q]);
+      P->u_cnt = mxc;
+      P->u_bounds = xb;
+      if (cudaMallocAsync(&P->xsend, std::max<int64_t>(ns, 1) * sizeof(double2), s) != cudaSuccess ||
+          cudaMallocAsync(&P->xrecv, std::max<int64_t>(nr, 1) * sizeof(double2), s) != cudaSuccess ||
+          cudaMallocAsync(&P->u_all, (size_t)(W + 1) * mxc * sizeof(double2), s) != cudaSuccess ||
+          cudaMallocAsync(&P->d_ubounds, (W + 1) * sizeof(int64_t), s) != cudaSuccess)
+        return bail(SFT_E_NOMEM, "exchange buffers");
+      cudaMemcpyAsync(P->d_ubounds, xb.data(), (W + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s);
+      if (cudaStreamSynchronize(s) != cudaSuccess) return bail(SFT_E_CUDA, "sync");  // (xb is a host temporary)
+    }
     int64_t mx = 0;
     for (int t = m; t <= L; ++t) mx = std::max(mx, (P->k_rng[t].hi - P->k_rng[t].lo) * P->X.counts[L - t]);
     for (int t = 0; t <= m; ++t) mx = std::max(mx, P->K.counts[t] * (P->x_rng[L - t].hi - P->x_rng[L - t].lo));
@@ -669,6 +709,12 @@ extern "C" int sft_plan(int dim, int64_t N, int p, const double* x, int64_t nx, 
       P->x_rng[l].hi = P->X.counts[l];
     }
   }
+  // the tile schedules address a level buffer with 32-bit element offsets
+  // (TaskRec, group records): reject plans whose largest level does not fit
+  // (e.g. 3D N = 1024 p = 9 on dense surfaces) instead of wrapping silently
+  if (P->buf_elems >= (size_t(1) << 32))
+    return bail(SFT_E_ARG, "a level of this plan holds " + std::to_string(P->buf_elems) +
+                               " complex elements; the translation schedules address at most 2^32 - 1");
   // translation launches of the single-GPU apply: two-level launches (levels
   // t+1 and t from t+2) where supported, from the leaf level down; a single
   // level 0 is left when L is odd.  Multi-rank plans run single levels.
@@ -726,7 +772,7 @@ extern "C" int sft_plan(int dim, int64_t N, int p, const double* x, int64_t nx, 
       // (only when the first launch is a two-level one: its schedule kernel is
       // a separate launch anyway)
       const int t_first =
-          P->world == 1 && !P->launch_t.empty() && P->launch_f2_out[P->launch_t[0]] ? P->launch_t[0] : -1;
+          !P->sharded && !P->launch_t.empty() && P->launch_f2_out[P->launch_t[0]] ? P->launch_t[0] : -1;
       for (int t = 0; t < L; ++t) {
         if (t >= 1 && P->launch_f2_out[t - 1]) continue;
         if (t == t_first) continue;
@@ -776,7 +822,7 @@ extern "C" int sft_plan(int dim, int64_t N, int p, const double* x, int64_t nx, 
     P->sched_fork = P->sched_ready = P->sched_first = nullptr;
     sched_recorded = true;
   }
-  if (P->world != 1 || P->launch_t.empty() || !P->launch_f2_out[P->launch_t[0]]) {  // launch 0 waits on sched_ready
+  if (P->sharded || P->launch_t.empty() || !P->launch_f2_out[P->launch_t[0]]) {  // launch 0 waits on sched_ready
     ev_put(P->sched_first, false, P->dev);
     P->sched_first = nullptr;
   }
@@ -864,6 +910,18 @@ static void tmark(sft_plan_s* P) {
   if (P->n_ev < 64) cudaEventRecord(P->ev[P->n_ev++], P->stream);
 }
 
+// Host f: the staging copy is stream-ordered; sft.h promises that the caller
+// may modify or free f once sft_apply returns, so the call waits for the copy
+// (not for the kernels queued behind it) before returning.
+static cudaError_t f_copy_mark(sft_plan_s* P) {
+  if (!P->f_copied) {
+    cudaError_t e = cudaEventCreateWithFlags(&P->f_copied, cudaEventDisableTiming);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaEventRecord(P->f_copied, P->stream);
+}
+static cudaError_t f_copy_wait(sft_plan_s* P) { return cudaEventSynchronize(P->f_copied); }
+
 // tl: output level of each timed translation launch (nullptr: n_levels_first - i);
 // a two-level launch's time is booked on its output level (the inner level shows 0)
 static int finish_timing(sft_plan_s* P, int n_levels_first, const std::vector<int>* tl = nullptr) {
@@ -918,6 +976,7 @@ static int apply_impl(sft_plan_s* P, int nrhs, const void* f, int64_t ldf, void*
                             nrhs, cudaMemcpyHostToDevice, s));
     fd = P->f_stage;
     ldf = P->nk;
+    CKR(f_copy_mark(P));
   }
   int64_t ldu_dev = ldu;
   if (u_host) {
@@ -984,13 +1043,22 @@ static int apply_impl(sft_plan_s* P, int nrhs, const void* f, int64_t ldf, void*
       CKR(cudaMemcpy2DAsync(u, ldu * sizeof(double2), ud, ldu_dev * sizeof(double2), P->nx * sizeof(double2), nrhs,
                             cudaMemcpyDeviceToHost, s));
     CKR(cudaStreamSynchronize(s));
+  } else if (f_host) {
+    CKR(f_copy_wait(P));  // the caller may reuse f as soon as we return (sft.h)
   }
   return finish_timing(P, L - 1, &P->launch_t);
 }
 
+static int apply_sharded(sft_plan_s* P, const void* f, void* u);
+
 extern "C" int sft_apply(sft_plan_t P, const void* f, void* u) {
   if (!P || !f || !u) return fail(SFT_E_ARG, "NULL argument");
-  if (P->world != 1) return fail(SFT_E_STATE, "sft_apply needs a world == 1 plan; use the phase calls");
+  if (P->sharded) {
+    if (!P->comm)
+      return fail(SFT_E_STATE, "sharded plan without opts.nccl_id: use the phase calls and your own collective");
+    if (!P->peer.empty()) return fail(SFT_E_STATE, "fused-exchange plan: use the phase calls");
+    return apply_sharded(P, f, u);
+  }
   return apply_impl(P, 1, f, P->nk, u, P->nx);
 }
 
@@ -998,7 +1066,7 @@ extern "C" int sft_apply_batch(sft_plan_t P, int nrhs, const void* f, int64_t ld
   if (!P || !f || !u) return fail(SFT_E_ARG, "NULL argument");
   if (nrhs < 1 || nrhs > 4096) return fail(SFT_E_ARG, "nrhs must be in [1, 4096]");
   if (ldf < P->nk || ldu < P->nx) return fail(SFT_E_ARG, "ldf >= nk and ldu >= nx required");
-  if (P->world != 1) return fail(SFT_E_STATE, "sft_apply_batch needs a world == 1 plan");
+  if (P->sharded) return fail(SFT_E_STATE, "sft_apply_batch needs a world == 1 plan");
   return apply_impl(P, nrhs, f, ldf, u, ldu);
 }
 
@@ -1007,7 +1075,7 @@ extern "C" int sft_apply_batch(sft_plan_t P, int nrhs, const void* f, int64_t ld
 // ---------------------------------------------------------------------------
 extern "C" int sft_exchange_counts(sft_plan_t P, int64_t* send_counts, int64_t* recv_counts) {
   if (!P) return fail(SFT_E_ARG, "NULL plan");
-  if (P->world < 2) return fail(SFT_E_STATE, "plan is not multi-rank");
+  if (!P->sharded) return fail(SFT_E_STATE, "plan is not multi-rank");
   for (int q = 0; q < P->world; ++q) {
     if (send_counts) send_counts[q] = P->send_counts[q];
     if (recv_counts) recv_counts[q] = P->recv_counts[q];
@@ -1017,7 +1085,7 @@ extern "C" int sft_exchange_counts(sft_plan_t P, int64_t* send_counts, int64_t* 
 
 extern "C" int sft_partition_info(sft_plan_t P, int64_t* part) {
   if (!P || !part) return fail(SFT_E_ARG, "NULL argument");
-  if (P->world < 2) return fail(SFT_E_STATE, "plan is not multi-rank");
+  if (!P->sharded) return fail(SFT_E_STATE, "plan is not multi-rank");
   part[0] = P->part.sk;
   part[1] = P->part.sx;
   part[2] = P->part.m;
@@ -1051,19 +1119,12 @@ static int phase_timing_end(sft_plan_s* P, bool first) {
   return SFT_OK;
 }
 
-extern "C" int sft_apply_phase1(sft_plan_t P, const void* f, void* sendbuf) {
-  if (!P || !f || (!sendbuf && P->peer.empty())) return fail(SFT_E_ARG, "NULL argument");
-  if (P->world < 2) return fail(SFT_E_STATE, "plan is not multi-rank");
-  if (sendbuf && !is_device_ptr(sendbuf)) return fail(SFT_E_ARG, "sendbuf must be device memory");
+// Phase 1 of a sharded plan (levels t = L..m over this rank's T_K subtrees):
+// the level-m charges in the send layout at sb, or -- fused exchange -- stored
+// straight into the receivers' buffers.  fd: device charges [nk].
+static int phase1_run(sft_plan_s* P, const double2* fd, double2* sb) {
   cudaStream_t s = P->stream;
   const int L = P->L, m = P->part.m;
-  const double2* fd = (const double2*)f;
-  if (!is_device_ptr(f)) {
-    if (!P->f_stage) CKR(cudaMallocAsync(&P->f_stage, P->nk * sizeof(double2), s));
-    CKR(cudaMemcpyAsync(P->f_stage, f, P->nk * sizeof(double2), cudaMemcpyHostToDevice, s));
-    fd = P->f_stage;
-  }
-  double2* sb = (double2*)sendbuf;
   const bool fused = !P->peer.empty();
   // leaf level: the local leaf range; if m == L the leaf output is the send buffer
   const LevelRange kl = P->k_rng[L];
@@ -1105,21 +1166,15 @@ extern "C" int sft_apply_phase1(sft_plan_t P, const void* f, void* sendbuf) {
   return phase_timing_end(P, true);
 }
 
-extern "C" int sft_apply_phase2(sft_plan_t P, const void* recvbuf, void* u) {
-  if (!P || !recvbuf || !u) return fail(SFT_E_ARG, "NULL argument");
-  if (P->world < 2) return fail(SFT_E_STATE, "plan is not multi-rank");
-  if (!is_device_ptr(recvbuf)) return fail(SFT_E_ARG, "recvbuf must be device memory");
+// Phase 2 (levels t = m-1..0 and step 4 over this rank's T_X subtrees) from
+// the received level-m charges.  sorted_out: the potentials of this rank's
+// targets in sorted order at ud[0 .. x_pt_hi - x_pt_lo) (the all-gather
+// layout); else ud [nx] in user order with every other entry zero.
+static int phase2_run(sft_plan_s* P, const double2* in, double2* ud, bool sorted_out) {
   cudaStream_t s = P->stream;
   const int L = P->L, m = P->part.m;
-  const bool u_host = !is_device_ptr(u);
-  double2* ud = (double2*)u;
-  if (u_host) {
-    if (!P->u_stage) CKR(cudaMallocAsync(&P->u_stage, P->nx * sizeof(double2), s));
-    ud = P->u_stage;
-  }
-  CKR(launch_zero(ud, P->nx, s));
+  if (!sorted_out) CKR(launch_zero(ud, P->nx, s));
   if (P->sched_ready) CKR(cudaStreamWaitEvent(s, P->sched_ready, 0));
-  const double2* in = (const double2*)recvbuf;
   phase_timing_begin(P);
   for (int t = m - 1; t >= 0; --t) {
     LevelDims ld = apply_dims_sched(P, t);
@@ -1129,7 +1184,77 @@ extern "C" int sft_apply_phase2(sft_plan_t P, const void* recvbuf, void* u) {
   }
   if (int rc = phase_timing_end(P, false)) return rc;
   const LevelRange xl = P->x_rng[L];
-  CKR(launch_final(P, in, ud, xl.lo, P->x_pt_lo, P->x_pt_hi));
+  CKR(launch_final(P, in, ud, xl.lo, P->x_pt_lo, P->x_pt_hi, 1, 0, 0, sorted_out));
+  return SFT_OK;
+}
+
+// sft_apply of a sharded plan with an NCCL communicator: phase 1, the level-m
+// exchange (grouped ncclSend/ncclRecv), phase 2 into this rank's slot of the
+// u all-gather buffer, ncclAllGather, and the scatter to user order -- every
+// rank ends with the full u.  All stream-ordered on the
+// plan stream.
+static int apply_sharded(sft_plan_s* P, const void* f, void* u) {
+  cudaStream_t s = P->stream;
+  const double2* fd = (const double2*)f;
+  const bool f_host = !is_device_ptr(f), u_host = !is_device_ptr(u);
+  if (f_host) {
+    if (!P->f_stage) CKR(cudaMallocAsync(&P->f_stage, P->nk * sizeof(double2), s));
+    CKR(cudaMemcpyAsync(P->f_stage, f, P->nk * sizeof(double2), cudaMemcpyHostToDevice, s));
+    CKR(f_copy_mark(P));
+    fd = P->f_stage;
+  }
+  double2* ud = (double2*)u;
+  if (u_host) {
+    if (!P->u_stage) CKR(cudaMallocAsync(&P->u_stage, P->nx * sizeof(double2), s));
+    ud = P->u_stage;
+  }
+  std::string err;
+  if (int rc = phase1_run(P, fd, P->xsend)) return rc;
+  if (int rc = nccl_exchange(P->comm, P->xsend, P->send_counts.data(), P->xrecv, P->recv_counts.data(), P->world, s,
+                             &err))
+    return fail(rc, err);
+  double2* mine = P->u_all + (int64_t)P->rank * P->u_cnt;
+  if (int rc = phase2_run(P, P->xrecv, mine, true)) return rc;
+  if (int rc = nccl_allgather(P->comm, mine, P->u_all, P->u_cnt, s, &err)) return fail(rc, err);
+  CKR(launch_unsort(P->u_all, P->u_cnt, P->d_ubounds, P->world, P->X.perm, ud, P->nx, s));
+  if (u_host) {
+    CKR(cudaMemcpyAsync(u, ud, P->nx * sizeof(double2), cudaMemcpyDeviceToHost, s));
+    CKR(cudaStreamSynchronize(s));
+  } else if (f_host) {
+    CKR(f_copy_wait(P));
+  }
+  return SFT_OK;
+}
+
+extern "C" int sft_apply_phase1(sft_plan_t P, const void* f, void* sendbuf) {
+  if (!P || !f || (!sendbuf && P->peer.empty())) return fail(SFT_E_ARG, "NULL argument");
+  if (!P->sharded) return fail(SFT_E_STATE, "plan is not multi-rank");
+  if (sendbuf && !is_device_ptr(sendbuf)) return fail(SFT_E_ARG, "sendbuf must be device memory");
+  cudaStream_t s = P->stream;
+  const double2* fd = (const double2*)f;
+  if (!is_device_ptr(f)) {
+    if (!P->f_stage) CKR(cudaMallocAsync(&P->f_stage, P->nk * sizeof(double2), s));
+    CKR(cudaMemcpyAsync(P->f_stage, f, P->nk * sizeof(double2), cudaMemcpyHostToDevice, s));
+    CKR(f_copy_mark(P));
+    fd = P->f_stage;
+  }
+  const int rc = phase1_run(P, fd, (double2*)sendbuf);
+  if (fd == P->f_stage) f_copy_wait(P);  // the caller may reuse f once we return
+  return rc;
+}
+
+extern "C" int sft_apply_phase2(sft_plan_t P, const void* recvbuf, void* u) {
+  if (!P || !recvbuf || !u) return fail(SFT_E_ARG, "NULL argument");
+  if (!P->sharded) return fail(SFT_E_STATE, "plan is not multi-rank");
+  if (!is_device_ptr(recvbuf)) return fail(SFT_E_ARG, "recvbuf must be device memory");
+  cudaStream_t s = P->stream;
+  const bool u_host = !is_device_ptr(u);
+  double2* ud = (double2*)u;
+  if (u_host) {
+    if (!P->u_stage) CKR(cudaMallocAsync(&P->u_stage, P->nx * sizeof(double2), s));
+    ud = P->u_stage;
+  }
+  if (int rc = phase2_run(P, (const double2*)recvbuf, ud, false)) return rc;
   if (u_host) {
     CKR(cudaMemcpyAsync(u, ud, P->nx * sizeof(double2), cudaMemcpyDeviceToHost, s));
     CKR(cudaStreamSynchronize(s));
@@ -1176,7 +1301,7 @@ extern "C" int sft_plan_stats(sft_plan_t P, int64_t* counts_x, int64_t* counts_k
 
 extern "C" int sft_set_peer_buffers(sft_plan_t P, void* const* recv) {
   if (!P) return fail(SFT_E_ARG, "NULL plan");
-  if (P->world < 2) return fail(SFT_E_STATE, "plan is not multi-rank");
+  if (!P->sharded) return fail(SFT_E_STATE, "plan is not multi-rank");
   if (P->world > kMaxPeers) return fail(SFT_E_ARG, "too many ranks for the fused exchange");
   if (!recv) {
     P->peer.clear();
@@ -1192,7 +1317,7 @@ extern "C" int sft_set_peer_buffers(sft_plan_t P, void* const* recv) {
 
 extern "C" int sft_peer_offsets(sft_plan_t P, int64_t* off) {
   if (!P || !off) return fail(SFT_E_ARG, "NULL argument");
-  if (P->world < 2) return fail(SFT_E_STATE, "plan is not multi-rank");
+  if (!P->sharded) return fail(SFT_E_STATE, "plan is not multi-rank");
   for (int q = 0; q < P->world; ++q) off[q] = P->peer_off[q];
   return SFT_OK;
 }
@@ -1243,7 +1368,7 @@ extern "C" int sft_schedule_bytes(sft_plan_t P, int t, int64_t* bytes, void* dst
 extern "C" int sft_translation_launches(sft_plan_t P, int* n, int* out_level, int* two_level) {
   if (!P || !n) return fail(SFT_E_ARG, "NULL argument");
   const int nl = (int)P->launch_t.size();
-  if (P->world != 1) {  // multi-rank: one launch per level, split over the two phases
+  if (P->sharded) {  // multi-rank: one launch per level, split over the two phases
     *n = P->L;
     for (int i = 0; i < P->L; ++i) {
       if (out_level) out_level[i] = P->L - 1 - i;

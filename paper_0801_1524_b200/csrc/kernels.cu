@@ -185,13 +185,7 @@ __global__ __launch_bounds__(128, D == 2 ? 4 : 2) void k_leaf(const double* __re
 //   u_i = sum_l prod_a z_a^{l_a} h^{A B0}_l
 // sum-factorised over the axes; h is read through L1 (the ~3 targets of a
 // leaf share it).
-//
-// MAXL > 0 (2D): a warp first copies the charges of the (contiguous) range of
-// leaves its 32 sorted targets fall in -- up to MAXL leaves -- into shared
-// memory with coalesced loads, and the targets read them there (scattered L1
-// reads of ~10 leaves per warp instruction cost ~10 wavefronts each); the
-// arithmetic is unchanged.
-template <int D, int P, typename T2, int PS, int MAXL = 0>
+template <int D, int P, typename T2, int PS>
 __global__ __launch_bounds__(128) void k_final(const double* __restrict__ x_sorted, const int32_t* __restrict__ perm,
                                                const int32_t* __restrict__ leaf_of,
                                                const T2* __restrict__ h0, double2* __restrict__ u,
@@ -199,29 +193,16 @@ __global__ __launch_bounds__(128) void k_final(const double* __restrict__ x_sort
                                                int nrhs, int64_t hrs, int64_t ldu, int ffmod) {
   constexpr int P1 = P - 1;
   const int64_t j = i_lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  extern __shared__ __align__(16) unsigned char fin_smem[];
-  T2* const sm = reinterpret_cast<T2*>(fin_smem) + (threadIdx.x >> 5) * (MAXL * PS);
-  int64_t lf0 = 0;
-  int nstaged = 0;
-  if constexpr (MAXL > 0) {
-    const int64_t jw0 = j - (threadIdx.x & 31);
-    if (jw0 >= i_hi) return;  // the whole warp is past the end
-    lf0 = leaf_of[jw0];
-    nstaged = (int)min((int64_t)MAXL, (int64_t)leaf_of[min(jw0 + 31, i_hi - 1)] - lf0 + 1);
-  } else {
-    if (j >= i_hi) return;
-  }
-  const bool live = j < i_hi;
-  const int64_t lj = live ? (int64_t)leaf_of[j] : lf0;
-  const bool staged = MAXL > 0 && lj - lf0 < nstaged;
+  if (j >= i_hi) return;
+  const int64_t lj = (int64_t)leaf_of[j];
   const T2* const hl = h0 + (lj - a_lo) * (int64_t)PS;
-  const int32_t pj = live ? perm[j] : 0;
+  const int64_t pj = perm ? (int64_t)perm[j] : j - i_lo;  // perm == nullptr: sorted output
   double2 z[D], el[P];
   double xisum = 0.0;
   int64_t csum = 0;
 #pragma unroll
   for (int a = 0; a < D; ++a) {
-    const double xx = live ? x_sorted[j * D + a] : 0.0;
+    const double xx = x_sorted[j * D + a];
     const double ca = fmin(floor(xx), (double)(N - 1));
     const double xi = xx - ca;  // in [0,1], exact
     xisum += xi;
@@ -242,19 +223,12 @@ __global__ __launch_bounds__(128) void k_final(const double* __restrict__ x_sort
   for (int l = 1; l < P; ++l) el[l] = cmul(el[l - 1], z[D - 1]);
   // the powers are shared by every RHS of a batch (sft_apply_batch)
   for (int rh = 0; rh < nrhs; ++rh) {
-  if constexpr (MAXL > 0) {
-    __syncwarp();
-    const T2* src = h0 + (int64_t)rh * hrs + (lf0 - a_lo) * (int64_t)PS;
-    for (int q = threadIdx.x & 31; q < nstaged * PS; q += 32) sm[q] = src[q];
-    __syncwarp();
-    if (!live) continue;
-  }
-  const T2* h = staged ? sm + (lj - lf0) * PS : hl + (int64_t)rh * hrs;
+  const T2* h = hl + (int64_t)rh * hrs;
   auto inner = [&](int base) {
     double2 t = make_double2(0.0, 0.0);
 #pragma unroll
     for (int l = 0; l < P; ++l) {
-      const T2 hq = MAXL > 0 ? h[base + l] : __ldg(h + base + l);
+      const T2 hq = __ldg(h + base + l);
       const double hx = hq.x, hy = hq.y;
       t.x = fma(el[l].x, hx, fma(-el[l].y, hy, t.x));
       t.y = fma(el[l].x, hy, fma(el[l].y, hx, t.y));
@@ -352,60 +326,40 @@ cudaError_t launch_leaf(const sft_plan_s* Pl, const double2* f, void* out, int64
   return cudaGetLastError();
 }
 
-// SFT_FINAL_STAGE=0/1: shared-memory staging of the warp's leaves in the final
-// kernel (2D only; 3D leaves are too large); default below
-#ifndef SFT_FINAL_STAGE_DEFAULT
-#define SFT_FINAL_STAGE_DEFAULT 0  // measured: no gain (C2 final 30.7 us either way), bitwise equal
-#endif
-static int final_stage_mode() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("SFT_FINAL_STAGE");
-    v = e ? (e[0] == '1' ? 1 : 0) : SFT_FINAL_STAGE_DEFAULT;
-  }
-  return v;
-}
-constexpr int kFinalMaxLeaves = 12;
-template <int D, int P, typename T2, int PS>
-static cudaError_t launch_final_t(int mode, unsigned nb, cudaStream_t st, const double* xs, const int32_t* perm,
-                                  const int32_t* leaf_of, const T2* h0, double2* u, int64_t i_lo, int64_t i_hi,
-                                  int64_t a_lo, int64_t N, int conj, int nrhs, int64_t hrs, int64_t ldu, int ffmod) {
-  if constexpr (D == 2) {
-    if (mode == 1) {
-      const size_t smem = (size_t)4 * kFinalMaxLeaves * PS * sizeof(T2);
-      static bool attr = false;
-      if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_final<D, P, T2, PS, kFinalMaxLeaves>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        attr = true;
-      }
-      k_final<D, P, T2, PS, kFinalMaxLeaves><<<nb, 128, smem, st>>>(xs, perm, leaf_of, h0, u, i_lo, i_hi, a_lo, N,
-                                                                     conj, nrhs, hrs, ldu, ffmod);
-      return cudaSuccess;
-    }
-  }
-  k_final<D, P, T2, PS><<<nb, 128, 0, st>>>(xs, perm, leaf_of, h0, u, i_lo, i_hi, a_lo, N, conj, nrhs, hrs, ldu, ffmod);
-  return cudaSuccess;
-}
-
 cudaError_t launch_final(const sft_plan_s* Pl, const void* h0, double2* u, int64_t a_lo, int64_t i_lo, int64_t i_hi,
-                         int nrhs, int64_t hrs, int64_t ldu) {
+                         int nrhs, int64_t hrs, int64_t ldu, bool sorted_out) {
   // targets = sorted points [i_lo, i_hi) of T_X; h0 holds the leaves from a_lo on
   if (i_hi <= i_lo) return cudaSuccess;
   const unsigned nb = (unsigned)((i_hi - i_lo + 127) / 128);
-  const int mode = final_stage_mode();
   if (Pl->prec == 1) {
     SFT_DISPATCH(Pl->d, Pl->p,
-                 (launch_final_t<D, P, float2, Pow<P, D>::v + (Pow<P, D>::v & 1)>(
-                     mode, nb, Pl->stream, Pl->X.pts_sorted, Pl->X.perm, Pl->X.leaf_of, (const float2*)h0, u, i_lo, i_hi,
-                     a_lo, Pl->N, Pl->conj, nrhs, hrs, ldu, Pl->ffmod && Pl->conj)));
+                 (k_final<D, P, float2, Pow<P, D>::v + (Pow<P, D>::v & 1)><<<nb, 128, 0, Pl->stream>>>(
+                     Pl->X.pts_sorted, sorted_out ? nullptr : Pl->X.perm, Pl->X.leaf_of, (const float2*)h0, u, i_lo, i_hi, a_lo, Pl->N,
+                     Pl->conj, nrhs, hrs, ldu, Pl->ffmod && Pl->conj)));
   } else {
     SFT_DISPATCH(Pl->d, Pl->p,
-                 (launch_final_t<D, P, double2, Pow<P, D>::v>(
-                     mode, nb, Pl->stream, Pl->X.pts_sorted, Pl->X.perm, Pl->X.leaf_of, (const double2*)h0, u, i_lo, i_hi,
-                     a_lo, Pl->N, Pl->conj, nrhs, hrs, ldu, Pl->ffmod && Pl->conj)));
+                 (k_final<D, P, double2, Pow<P, D>::v><<<nb, 128, 0, Pl->stream>>>(
+                     Pl->X.pts_sorted, sorted_out ? nullptr : Pl->X.perm, Pl->X.leaf_of, (const double2*)h0, u, i_lo, i_hi, a_lo, Pl->N,
+                     Pl->conj, nrhs, hrs, ldu, Pl->ffmod && Pl->conj)));
   }
+  count_launch();
+  return cudaGetLastError();
+}
+
+// all-gathered potentials (sorted order, [world][cnt]) to user order
+__global__ void k_unsort(const double2* __restrict__ u_all, int64_t cnt, const int64_t* __restrict__ bounds, int world,
+                         const int32_t* __restrict__ perm, double2* __restrict__ u, int64_t n) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  int q = 0;
+  while (q + 1 < world && j >= bounds[q + 1]) ++q;
+  u[perm[j]] = u_all[q * cnt + (j - bounds[q])];
+}
+
+cudaError_t launch_unsort(const double2* u_all, int64_t cnt, const int64_t* bounds, int world, const int32_t* perm,
+                          double2* u, int64_t n, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  k_unsort<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(u_all, cnt, bounds, world, perm, u, n);
   count_launch();
   return cudaGetLastError();
 }

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -55,8 +56,6 @@ struct DeviceTables {
 // Host-side long double construction (tables.cpp).
 void build_tables_host(int p, std::vector<double>& V /* 2*4*p*p */, std::vector<double>& invD /* p */,
                        std::vector<double>* RC = nullptr /* 2*p*p */, std::vector<double>* RS = nullptr);
-// kernels.cu: copy RC/RS/invD for grid size p into the constant bank
-cudaError_t upload_const_tables(int p, const double* RC, const double* RS, const double* invD);
 const DeviceTables* get_device_tables(int p, std::string* err);
 
 struct Partition {
@@ -76,6 +75,7 @@ struct sft_plan_s {
   int d = 0, p = 0, L = 0;
   int64_t N = 0, nx = 0, nk = 0;
   int rank = 0, world = 1;
+  bool sharded = false;  // the two-phase multi-rank path (world > 1, or forced on one rank)
   int dev = 0;   // CUDA device the plan was created on (its pooled events belong to it)
   int prec = 0;  // 0 = FP64 charges (complex128), 1 = FP32 charges (complex64)
   int conj = 0;  // adjoint plan: conjugate the charges on input and the potentials on output
@@ -94,6 +94,7 @@ struct sft_plan_s {
   // staging for host pointers
   double2* f_stage = nullptr;
   double2* u_stage = nullptr;
+  cudaEvent_t f_copied = nullptr;  // recorded after a host f's staging copy (sft_apply waits on it)
   int* d_err = nullptr;
   // multi-GPU
   sft::Partition part;
@@ -106,6 +107,16 @@ struct sft_plan_s {
   std::vector<int64_t> seg_host;   // host copy of the same
   std::vector<int64_t> peer_off;   // [world] element offset of this rank's segment in each receiver's buffer
   std::vector<double2*> peer;      // [world] receive buffers (fused exchange), empty = use the send buffer
+  // in-library collectives (opts.nccl_id): communicator (cached per id, not owned),
+  // exchange buffers, and the u all-gather: rank q's targets are the sorted
+  // points [u_bounds[q], u_bounds[q+1]), gathered as [world][u_cnt]
+  void* comm = nullptr;
+  double2* xsend = nullptr;
+  double2* xrecv = nullptr;
+  double2* u_all = nullptr;
+  int64_t* d_ubounds = nullptr;
+  int64_t u_cnt = 0;
+  std::vector<int64_t> u_bounds;
   // translation launches of a world-1 apply: output level and whether it is a
   // two-level launch (levels t+1, t from t+2); schedules per launch
   std::vector<int> launch_t, launch_f2_out;  // launch order (output levels); f2 flag per output level
@@ -184,8 +195,18 @@ cudaError_t check_schedule(const sft_plan_s* P, const LevelDims& L, const unsign
                            int64_t out_pairs, int* err);
 // step 4 for the sorted targets [i_lo, i_hi) (the points of leaves a_lo...); g0 holds leaves from a_lo on
 // nrhs > 1: level-0 charges of RHS r at g0 + r * hrs (stored elements), potentials at u + r * ldu
+// sorted_out: u[j - i_lo] for sorted target j (the all-gather layout) instead of u[perm[j]]
 cudaError_t launch_final(const sft_plan_s* P, const void* g0, double2* u, int64_t a_lo, int64_t i_lo, int64_t i_hi,
-                         int nrhs = 1, int64_t hrs = 0, int64_t ldu = 0);
+                         int nrhs = 1, int64_t hrs = 0, int64_t ldu = 0, bool sorted_out = false);
+// u[perm[j]] = u_all[q * cnt + j - bounds[q]] for the rank q with bounds[q] <= j < bounds[q+1]
+cudaError_t launch_unsort(const double2* u_all, int64_t cnt, const int64_t* bounds, int world, const int32_t* perm,
+                          double2* u, int64_t n, cudaStream_t s);
+
+// comm.cu: NCCL (dlopen'ed; SFT_E_NCCL on failure, message in *err)
+int nccl_comm_get(const void* id128, int rank, int world, void** comm, std::string* err);
+int nccl_exchange(void* comm, const double2* send, const int64_t* send_counts, double2* recv,
+                  const int64_t* recv_counts, int world, cudaStream_t s, std::string* err);
+int nccl_allgather(void* comm, const double2* send, double2* recv, int64_t count, cudaStream_t s, std::string* err);
 cudaError_t launch_zero(double2* p, int64_t n, cudaStream_t s);
 // far-field adapter: x = N/2 - kappa xhat/(2 pi), k = N y (device arrays [n][d])
 cudaError_t launch_ff_coords(const double* xhat, int64_t nx, const double* y, int64_t ny, int d, double kappa,
@@ -210,6 +231,36 @@ struct Pow<B, 0> {
     else if (D_ == 3 && P_ == 9) { constexpr int D = 3, P = 9; CALL; }   \
     else return cudaErrorInvalidValue;                                   \
   } while (0)
+
+// Per-device cache of a value computed once per CUDA device (launch attributes,
+// occupancy grids, device tables): a process may plan on several GPUs, so
+// nothing derived from one device may be reused on another.
+template <typename T>
+struct PerDevice {
+  static constexpr int kMaxDev = 64;
+  std::mutex mu;
+  T val[kMaxDev] = {};
+  bool ok[kMaxDev] = {};
+  // *out = the cached value of the current device, computing it with
+  // init(dev, &value) (returns cudaError_t) on first use
+  template <class F>
+  cudaError_t get(T* out, F init) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= kMaxDev) return cudaErrorInvalidDevice;
+    std::lock_guard<std::mutex> lk(mu);
+    if (!ok[dev]) {
+      T v{};
+      e = init(dev, &v);
+      if (e != cudaSuccess) return e;
+      val[dev] = v;
+      ok[dev] = true;
+    }
+    *out = val[dev];
+    return cudaSuccess;
+  }
+};
 
 // SFT_PLAN_TRACE=1: host-time milestones of sft_plan (api.cu)
 void trace_mark(const char* what, cudaStream_t s = nullptr, bool dev = false);  // dev: also a device event on s

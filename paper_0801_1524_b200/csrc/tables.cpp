@@ -110,10 +110,6 @@ const DeviceTables* get_device_tables(int p, std::string* err) {
   if (it != cache.end()) return it->second;
   std::vector<double> V, invD, RC, RS;
   build_tables_host(p, V, invD, &RC, &RS);
-  if (upload_const_tables(p, RC.data(), RS.data(), invD.data()) != cudaSuccess) {
-    if (err) *err = "constant table upload failed";
-    return nullptr;
-  }
   DeviceTables* t = new DeviceTables();
   t->p = p;
   if (cudaMalloc(&t->V, V.size() * sizeof(double)) != cudaSuccess ||

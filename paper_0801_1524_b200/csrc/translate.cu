@@ -28,9 +28,6 @@
 // (N padding avoided: p=9 waste 1.11x instead of 1.78x).  One named barrier
 // between passes; the last pass stores straight to HBM.
 //
-// k_translate_fma (SFT_TRANSLATE=fma): one thread per fiber on DFMA with
-// constant-bank operands (round-1 design, kept for ablation).
-//
 // No floating-point atomics: bitwise reproducible, identical for any world
 // size.
 #include <algorithm>
@@ -44,92 +41,6 @@
 #include "sft_internal.cuh"
 
 namespace sft {
-
-// ------------------------------------------------------------------------
-// constant-bank operators for the FMA kernel (uploaded once per device and p)
-// ------------------------------------------------------------------------
-__constant__ double c_RC5[2][5][5], c_RS5[2][5][5];
-__constant__ double c_RC7[2][7][7], c_RS7[2][7][7];
-__constant__ double c_RC9[2][9][9], c_RS9[2][9][9];
-
-template <int P>
-struct CT;
-template <>
-struct CT<5> {
-  __device__ __forceinline__ static double rc(int b, int m, int l) { return c_RC5[b][m][l]; }
-  __device__ __forceinline__ static double rs(int b, int m, int l) { return c_RS5[b][m][l]; }
-};
-template <>
-struct CT<7> {
-  __device__ __forceinline__ static double rc(int b, int m, int l) { return c_RC7[b][m][l]; }
-  __device__ __forceinline__ static double rs(int b, int m, int l) { return c_RS7[b][m][l]; }
-};
-template <>
-struct CT<9> {
-  __device__ __forceinline__ static double rc(int b, int m, int l) { return c_RC9[b][m][l]; }
-  __device__ __forceinline__ static double rs(int b, int m, int l) { return c_RS9[b][m][l]; }
-};
-
-// FP32 variant: the same operators rounded to float
-__constant__ float c_RC5f[2][5][5], c_RS5f[2][5][5];
-__constant__ float c_RC7f[2][7][7], c_RS7f[2][7][7];
-__constant__ float c_RC9f[2][9][9], c_RS9f[2][9][9];
-
-template <int P>
-struct CTf;
-template <>
-struct CTf<5> {
-  __device__ __forceinline__ static float rc(int b, int m, int l) { return c_RC5f[b][m][l]; }
-  __device__ __forceinline__ static float rs(int b, int m, int l) { return c_RS5f[b][m][l]; }
-};
-template <>
-struct CTf<7> {
-  __device__ __forceinline__ static float rc(int b, int m, int l) { return c_RC7f[b][m][l]; }
-  __device__ __forceinline__ static float rs(int b, int m, int l) { return c_RS7f[b][m][l]; }
-};
-template <>
-struct CTf<9> {
-  __device__ __forceinline__ static float rc(int b, int m, int l) { return c_RC9f[b][m][l]; }
-  __device__ __forceinline__ static float rs(int b, int m, int l) { return c_RS9f[b][m][l]; }
-};
-
-static cudaError_t upload_const_tables_f(int p, const double* RC, const double* RS) {
-  float rc[2 * 9 * 9], rs[2 * 9 * 9];
-  for (int i = 0; i < 2 * p * p; ++i) {
-    rc[i] = (float)RC[i];
-    rs[i] = (float)RS[i];
-  }
-  const size_t n2 = sizeof(float) * 2 * p * p;
-  cudaError_t e = cudaErrorInvalidValue;
-  if (p == 5) {
-    if ((e = cudaMemcpyToSymbol(c_RC5f, rc, n2)) != cudaSuccess) return e;
-    e = cudaMemcpyToSymbol(c_RS5f, rs, n2);
-  } else if (p == 7) {
-    if ((e = cudaMemcpyToSymbol(c_RC7f, rc, n2)) != cudaSuccess) return e;
-    e = cudaMemcpyToSymbol(c_RS7f, rs, n2);
-  } else if (p == 9) {
-    if ((e = cudaMemcpyToSymbol(c_RC9f, rc, n2)) != cudaSuccess) return e;
-    e = cudaMemcpyToSymbol(c_RS9f, rs, n2);
-  }
-  return e;
-}
-
-cudaError_t upload_const_tables(int p, const double* RC, const double* RS, const double* /*invD*/) {
-  const size_t n2 = sizeof(double) * 2 * p * p;
-  cudaError_t e = upload_const_tables_f(p, RC, RS);
-  if (e != cudaSuccess) return e;
-  if (p == 5) {
-    if ((e = cudaMemcpyToSymbol(c_RC5, RC, n2)) != cudaSuccess) return e;
-    e = cudaMemcpyToSymbol(c_RS5, RS, n2);
-  } else if (p == 7) {
-    if ((e = cudaMemcpyToSymbol(c_RC7, RC, n2)) != cudaSuccess) return e;
-    e = cudaMemcpyToSymbol(c_RS7, RS, n2);
-  } else if (p == 9) {
-    if ((e = cudaMemcpyToSymbol(c_RC9, RC, n2)) != cudaSuccess) return e;
-    e = cudaMemcpyToSymbol(c_RS9, RS, n2);
-  }
-  return e;
-}
 
 // ------------------------------------------------------------------------
 // shared pieces: arguments, group metadata, TMA tile prologue, task lists
@@ -180,10 +91,6 @@ struct GroupMeta {
   uint32_t mB, mA;
 };
 
-struct TaskEntry {
-  uint8_t j, bp, as, cls;
-};
-
 // projections of a child mask: set of top-k-bit prefixes / low-k-bit suffixes
 template <int D>
 __device__ __forceinline__ uint32_t proj_hi(uint32_t m, int k) {
@@ -215,105 +122,6 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   }
 }
 
-// Tile of G consecutive groups (B-major, A' fastest): group metadata into
-// shared memory, then one elected warp issues a 1-D TMA bulk copy of every
-// present child array (iB_c, iA') into slot c of its group, all completing on
-// one mbarrier.  Returns the number of groups in the tile.
-template <int D, int P, int G>
-__device__ __forceinline__ int tile_prologue(const TransArgs& a, double2* sb, GroupMeta* gm, uint64_t* bar) {
-  constexpr int PD = Pow<P, D>::v;
-  constexpr int NS = 1 << D;
-  static_assert(G <= 32, "one lane per group");
-  const int64_t g0 = (int64_t)blockIdx.x * G;
-  const int ng = (int)min((int64_t)G, a.ngroups - g0);
-  if (threadIdx.x < ng) {
-    const int64_t g = g0 + threadIdx.x;
-    GroupMeta m;
-    m.iB = a.b_lo + g / a.nAp_grp;
-    m.iAp = a.ap_lo + g % a.nAp_grp;
-    m.cbK = a.cbK[m.iB];
-    m.mB = a.mK[m.iB];
-    m.cbX = a.cbX[m.iAp];
-    m.mA = a.mX[m.iAp];
-    gm[threadIdx.x] = m;
-  }
-  if (threadIdx.x == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)));
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    const int lane = threadIdx.x;
-    uint32_t nbytes = lane < ng ? __popc(gm[lane].mB) * PD * (uint32_t)sizeof(double2) : 0u;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) nbytes += __shfl_xor_sync(0xffffffffu, nbytes, o);
-    if (lane == 0)
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(nbytes)
-                   : "memory");
-    __syncwarp();
-    if (lane < ng) {
-      const GroupMeta& m = gm[lane];
-      uint32_t mm = m.mB;
-      int r = 0;
-      while (mm) {
-        const int c = __ffs(mm) - 1;
-        mm &= mm - 1;
-        const int64_t iBc = (int64_t)m.cbK + r++;
-        const int64_t pin = (iBc - a.in_b0) * a.in_nA + (m.iAp - a.in_a0);
-#ifndef SFT_ABL_NOLOAD
-        asm volatile(
-            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                smem_u32(sb + ((int64_t)lane * NS + c) * PD)),
-            "l"(a.in + pin * PD), "r"((uint32_t)(PD * sizeof(double2))), "r"(smem_u32(bar))
-            : "memory");
-#else  // ablation: no HBM reads, the transaction count is completed by hand
-        (void)pin;
-        asm volatile("mbarrier.complete_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)),
-                     "r"((uint32_t)(PD * sizeof(double2)))
-                     : "memory");
-#endif
-      }
-    }
-  }
-  return ng;
-}
-
-// Task list of pass AX: one entry per (group, beta-prefix bp, alpha-suffix as)
-// whose two input slots (bp,0,as), (bp,1,as) are live; cls bit 0/1 = the
-// slot with axis bit 0/1 holds data.  Entries are appended per class (both /
-// bit 0 only / bit 1 only) so that consecutive tasks share a class.
-template <int D, int G, int AX>
-__device__ __forceinline__ void build_tasks(const GroupMeta* gm, int ng, TaskEntry* ent, int* cnt) {
-  constexpr int MAXE = G << (D - 1);
-  if (threadIdx.x < 3) cnt[threadIdx.x] = 0;
-  __syncthreads();
-  if ((int)threadIdx.x < ng) {
-    const int j = threadIdx.x;
-    const uint32_t mB = gm[j].mB, mA = gm[j].mA;
-    const uint32_t PBp = AX > 0 ? proj_hi<D>(mB, AX) : 1u;
-    const uint32_t PAs = proj_lo<D>(mA, D - 1 - AX);
-    const uint32_t PBa = proj_hi<D>(mB, AX + 1);
-#pragma unroll
-    for (int bp = 0; bp < (1 << AX); ++bp) {
-      if (!(PBp >> bp & 1)) continue;
-      const int cls = (int)((PBa >> (bp << 1)) & 3u);
-      const int ci = cls == 3 ? 0 : (cls == 1 ? 1 : 2);
-#pragma unroll
-      for (int as = 0; as < (1 << (D - 1 - AX)); ++as) {
-        if (!(PAs >> as & 1)) continue;
-        const int pos = atomicAdd(&cnt[ci], 1);
-        ent[ci * MAXE + pos] = TaskEntry{(uint8_t)j, (uint8_t)bp, (uint8_t)as, (uint8_t)cls};
-      }
-    }
-  }
-  __syncthreads();
-}
-
-template <int MAXE>
-__device__ __forceinline__ TaskEntry task_at(const TaskEntry* ent, int ei, int n3, int n1) {
-  return ei < n3 ? ent[ei] : (ei < n3 + n1 ? ent[MAXE + ei - n3] : ent[2 * MAXE + ei - n3 - n1]);
-}
-
 // Index of the output pair (child alpha of A', B) in the level output for
 // the last pass, -1 if A' has no such child.
 __device__ __forceinline__ int64_t out_pair(const LevelArgs& a, const GroupMeta& g, int alpha) {
@@ -324,23 +132,6 @@ __device__ __forceinline__ int64_t out_pair(const LevelArgs& a, const GroupMeta&
   while (q + 1 < a.nseg && iA >= a.seg[q + 1]) ++q;
   const int64_t wq = a.seg[q + 1] - a.seg[q];
   return a.seg[a.nseg + 1 + q] + (g.iB - a.out_b0) * wq + (iA - a.seg[q]);
-}
-
-// HBM address of the output pair (child alpha of A', B) for the last pass
-template <int PD>
-__device__ __forceinline__ double2* out_array(const LevelArgs& a, const GroupMeta& g, int alpha) {
-  if (!(g.mA >> alpha & 1)) return nullptr;
-  const int64_t iA = (int64_t)g.cbX + __popc(g.mA & ((1u << alpha) - 1));
-  int64_t pidx;
-  if (a.nseg == 0) {
-    pidx = (g.iB - a.out_b0) * a.out_nA + (iA - a.out_a0);
-  } else {
-    int q = 0;
-    while (q + 1 < a.nseg && iA >= a.seg[q + 1]) ++q;
-    const int64_t wq = a.seg[q + 1] - a.seg[q];
-    pidx = a.seg[a.nseg + 1 + q] + (g.iB - a.out_b0) * wq + (iA - a.seg[q]);
-  }
-  return a.out + pidx * PD;
 }
 
 // ------------------------------------------------------------------------
@@ -430,22 +221,14 @@ struct TailSmem {
 // in shared memory (SFT_TAIL_SMEM) they cost one broadcast load per k-step
 // instead of 2*NK registers per thread
 __shared__ double2 s_tail[8][4];
-// SFT_DELTA_SMEM: the delta coefficients (a0, b0, a1, b1) per (N tile, lane%4)
-// in shared memory instead of 4*NT registers per thread
-#ifndef SFT_DELTA_SMEM
-#define SFT_DELTA_SMEM 0
-#endif
-__shared__ double4 s_delta[4][4];
-
 template <int P, bool TS>
 struct LaneOps {
   using S = MmaShape<P>;
   double fb[S::NK][S::NT];           // B fragments of the operator (odd columns)
   double ft[TS ? 1 : S::NK][2];      // tail column (m = P-1): P and Q weights of this lane's k
-  double dl[SFT_DELTA_SMEM ? 1 : S::NT][4];  // delta columns of m = 4n + lane%4: (a0, b0, a1, b1)
-  __device__ __forceinline__ double4 delta(int n, int lane) const {
-    if constexpr (SFT_DELTA_SMEM) return s_delta[n][lane & 3];
-    else return make_double4(dl[n][0], dl[n][1], dl[n][2], dl[n][3]);
+  double dl[S::NT][4];               // delta columns of m = 4n + lane%4: (a0, b0, a1, b1)
+  __device__ __forceinline__ double4 delta(int n, int) const {
+    return make_double4(dl[n][0], dl[n][1], dl[n][2], dl[n][3]);
   }
   double dt[S::TAIL ? 2 : 1];        // delta column of the tail (lane%4 == 0 only, else 0)
   // child (0, 1; 2 = padding) and element index of this lane's k in k-step kk
@@ -510,57 +293,6 @@ __device__ __forceinline__ void mma_steps(const OPS& op, const E* const (&x)[NSU
 // fibers q, q+4 of the super-tile (conflict-free 16-byte shared loads for
 // the unit and p-strided fibers of p = 9).  Outputs go back in place, or to
 // HBM in the last pass.
-
-// One fiber, both outputs, children present per CLS (bit 0: beta=0, bit 1:
-// beta=1); straight-line code over all rows.  CS form with constant-bank
-// operands (OP = CT<P> for FP64, CTf<P> for FP32):
-//   z_alpha[m] = sum_beta c_{alpha beta} (RC_beta[m] . x_beta + i (2 alpha - 1) RS_beta[m] . x_beta),
-// c_{alpha,0} = 1, c_{0,1} = i, c_{1,1} = -i.
-template <typename T2, class OP, int P, int CLS, class Store>
-__device__ __forceinline__ void contract_fiber_t(const T2 (&x0)[P], const T2 (&x1)[P], Store store) {
-  using T = decltype(x0[0].x);
-#pragma unroll
-  for (int m = 0; m < P; ++m) {
-    T2 z0, z1;
-    z0.x = z0.y = z1.x = z1.y = T(0);
-    if (CLS & 1) {
-      T ur = 0, ui = 0, vr = 0, vi = 0;
-#pragma unroll
-      for (int l = 0; l < P; ++l) {
-        const T cc = OP::rc(0, m, l), sn = OP::rs(0, m, l);
-        ur = fma(cc, x0[l].x, ur);
-        ui = fma(cc, x0[l].y, ui);
-        vr = fma(sn, x0[l].x, vr);
-        vi = fma(sn, x0[l].y, vi);
-      }
-      z0.x = ur + vi;
-      z0.y = ui - vr;
-      z1.x = ur - vi;
-      z1.y = ui + vr;
-    }
-    if (CLS & 2) {
-      T ur = 0, ui = 0, vr = 0, vi = 0;
-#pragma unroll
-      for (int l = 0; l < P; ++l) {
-        const T cc = OP::rc(1, m, l), sn = OP::rs(1, m, l);
-        ur = fma(cc, x1[l].x, ur);
-        ui = fma(cc, x1[l].y, ui);
-        vr = fma(sn, x1[l].x, vr);
-        vi = fma(sn, x1[l].y, vi);
-      }
-      z0.x -= ui - vr;
-      z0.y += ur + vi;
-      z1.x += ui + vr;
-      z1.y -= ur - vi;
-    }
-    store(m, z0, z1);
-  }
-}
-
-template <int P, int CLS, class Store>
-__device__ __forceinline__ void contract_fiber(const double2 (&x0)[P], const double2 (&x1)[P], Store store) {
-  contract_fiber_t<double2, CT<P>, P, CLS>(x0, x1, store);
-}
 
 // ------------------------------------------------------------------------
 // Tile schedule (built once per plan by k_schedule, read by the producer)
@@ -958,15 +690,6 @@ struct RowMap {
   }
 };
 
-// SFT_BRANCHLESS=1: rows without an output (padding rows of a partial super-tile,
-// absent children of A') store into a dummy array (shared memory for in-place
-// passes, a device scratch array for the last pass) instead of branching around
-// the store
-#ifndef SFT_BRANCHLESS
-#define SFT_BRANCHLESS 0
-#endif
-__device__ double2 g_dummy_out[729 + 1];  // >= p^d of every supported (d, p)
-
 // MUL: stage-slot stride of consecutive child slots: 0 = G (slot-major
 // stage), 1 for the second level of a two-level tile (transposed slots)
 template <int D, int P, int G, int NC, int AX, bool LAST, int LIST = AX, typename E = double2, bool FUSED = false,
@@ -974,7 +697,7 @@ template <int D, int P, int G, int NC, int AX, bool LAST, int LIST = AX, typenam
 __device__ __forceinline__ void consumer_pass(const TransArgs& a, E* __restrict__ sb,
                                               const unsigned char* __restrict__ blk,
                                               const LaneOps<P, TailSmem<D>::v>& op,
-                                              int& rot, int64_t ooff = 0, E* sdummy = nullptr) {
+                                              int& rot, int64_t ooff = 0) {
   using S = MmaShape<P>;
   using SC = Sched<D, P, G>;
   constexpr int NSUB = NsubCfg<D, P>::v;
@@ -1050,13 +773,11 @@ __device__ __forceinline__ void consumer_pass(const TransArgs& a, E* __restrict_
         o0[u] = dst(d.o0);
         o1[u] = dst(d.o1);
       } else if (LAST) {
-        E* const nil = SFT_BRANCHLESS ? reinterpret_cast<E*>(g_dummy_out) : nullptr;
-        o0[u] = d.o0 != ~0u ? gout + d.o0 + ebase : nil;
-        o1[u] = d.o1 != ~0u ? gout + d.o1 + ebase : nil;
+        o0[u] = d.o0 != ~0u ? gout + d.o0 + ebase : nullptr;
+        o1[u] = d.o1 != ~0u ? gout + d.o1 + ebase : nullptr;
       } else {
-        E* const nil = SFT_BRANCHLESS ? sdummy : nullptr;
-        o0[u] = vrow ? sb + xo : nil;
-        o1[u] = vrow ? sb + xo + (1 << SH) * PD * (MUL == 0 ? G : MUL) : nil;
+        o0[u] = vrow ? sb + xo : nullptr;
+        o1[u] = vrow ? sb + xo + (1 << SH) * PD * (MUL == 0 ? G : MUL) : nullptr;
       }
 #endif
     }
@@ -1101,13 +822,8 @@ __device__ __forceinline__ void consumer_pass(const TransArgs& a, E* __restrict_
       for (int n = 0; n < S::NT; ++n) {
         const int m = 4 * n + c;
         if (m < S::NM) {
-          if (SFT_BRANCHLESS && !(LAST && FUSED)) {
-            o0[u][m * STR] = ElemT<E>::mk(are[u][n][0] + aim[u][n][1], aim[u][n][0] - are[u][n][1]);
-            o1[u][m * STR] = ElemT<E>::mk(are[u][n][0] - aim[u][n][1], aim[u][n][0] + are[u][n][1]);
-          } else {
-            if (o0[u]) o0[u][m * STR] = ElemT<E>::mk(are[u][n][0] + aim[u][n][1], aim[u][n][0] - are[u][n][1]);
-            if (o1[u]) o1[u][m * STR] = ElemT<E>::mk(are[u][n][0] - aim[u][n][1], aim[u][n][0] + are[u][n][1]);
-          }
+          if (o0[u]) o0[u][m * STR] = ElemT<E>::mk(are[u][n][0] + aim[u][n][1], aim[u][n][0] - are[u][n][1]);
+          if (o1[u]) o1[u][m * STR] = ElemT<E>::mk(are[u][n][0] - aim[u][n][1], aim[u][n][0] + are[u][n][1]);
         }
       }
     }
@@ -1125,7 +841,7 @@ __device__ __forceinline__ void consumer_pass(const TransArgs& a, E* __restrict_
         double w = hi ? vb : va;
         w += __shfl_xor_sync(0xffffffffu, hi ? va : vb, 2);
         E* o = hi ? o1[u] : o0[u];  // lane c holds component c&1 of z_{c>>1}
-        if ((SFT_BRANCHLESS && !(LAST && FUSED)) || o)
+        if (o)
           reinterpret_cast<typename ElemT<E>::scalar*>(o + (P - 1) * STR)[c & 1] = (typename ElemT<E>::scalar)w;
       }
     }
@@ -1175,14 +891,6 @@ __device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
 template <int D, int P>
 __device__ __forceinline__ void fill_tail_smem(const double* __restrict__ frag) {
   using S = MmaShape<P>;
-  if (SFT_DELTA_SMEM && threadIdx.x < 4) {
-#pragma unroll
-    for (int n = 0; n < S::NT; ++n)
-      s_delta[n][threadIdx.x] = make_double4(frag[S::OFF_DELTA + (n * 4 + 0) * 32 + threadIdx.x],
-                                             frag[S::OFF_DELTA + (n * 4 + 1) * 32 + threadIdx.x],
-                                             frag[S::OFF_DELTA + (n * 4 + 2) * 32 + threadIdx.x],
-                                             frag[S::OFF_DELTA + (n * 4 + 3) * 32 + threadIdx.x]);
-  }
   if (TailSmem<D>::v && S::TAIL && threadIdx.x < 4) {
 #pragma unroll
     for (int kk = 0; kk < S::NK; ++kk)
@@ -1197,7 +905,7 @@ __device__ __forceinline__ void load_lane_ops(LaneOps<P, TS>& op, const double* 
 #pragma unroll
   for (int n = 0; n < S::NT; ++n)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) op.dl[SFT_DELTA_SMEM ? 0 : n][j] = frag[S::OFF_DELTA + (n * 4 + j) * 32 + lane];
+    for (int j = 0; j < 4; ++j) op.dl[n][j] = frag[S::OFF_DELTA + (n * 4 + j) * 32 + lane];
   op.dt[0] = S::TAIL ? frag[S::OFF_DTAIL + lane] : 0.0;
   if (S::TAIL) op.dt[S::TAIL ? 1 : 0] = frag[S::OFF_DTAIL + 32 + lane];
 #pragma unroll
@@ -1375,21 +1083,13 @@ __device__ __forceinline__ void ws_producer(const TransArgs& a, const unsigned c
 // 2D with NST >= 3: skewed pipeline, pass 1 of tile i+1 runs before pass 0 of
 // tile i, and pass 0 waits on an mbarrier (p1done) every consumer thread
 // arrives on after its pass-1 rows, so warps do not idle at a pass barrier.
-//
-// SELF = true: no producer warp.  Warp 0 issues the first NST tiles; after
-// that, the consumer warp that finishes a stage last (a shared-memory
-// counter) refills it with the CTA's tile NST ahead -- the warp that would
-// otherwise idle at a barrier does the issue, and the CTA needs NC instead of
-// NC + 1 warps' registers (one more CTA per SM at 2D p = 9).  Non-skewed
-// pipeline only.
 template <int D, int P, int G, int NC, int NST, int MINB, typename E = double2, bool FUSED = false,
-          bool BATCH = false, bool SELF = false, bool F2 = false>
-__global__ __launch_bounds__((NC + (SELF ? 0 : 1)) * 32, MINB) void k_translate_ws(TransArgs a,
+          bool BATCH = false, bool F2 = false>
+__global__ __launch_bounds__((NC + 1) * 32, MINB) void k_translate_ws(TransArgs a,
                                                                                   const double* __restrict__ frag,
                                                                                   const unsigned char* __restrict__ sched,
                                                                                   int64_t ntiles) {
-  static_assert(!SELF || D != 2 || NST < 3, "the self-fed mode has no skewed pipeline");
-  static_assert(!F2 || (D == 2 && NST < 3 && G % 4 == 0 && !FUSED && !SELF), "two-level tiles: 2D, unskewed, G = 4k");
+  static_assert(!F2 || (D == 2 && NST < 3 && G % 4 == 0 && !FUSED), "two-level tiles: 2D, unskewed, G = 4k");
   using SC = Sched<D, P, G>;
   constexpr int PD = StrideT<E, Pow<P, D>::v>::v;  // array stride (elements)
   constexpr int NS = 1 << D;
@@ -1399,11 +1099,8 @@ __global__ __launch_bounds__((NC + (SELF ? 0 : 1)) * 32, MINB) void k_translate_
   constexpr int NB = F2 ? 2 : 1;  // schedule blocks per tile
   __shared__ __align__(128) unsigned char blk[NST][SC::BLK * NB];
   __shared__ __align__(8) uint64_t full[NST], empty[NST], p1done[NST];
-  __shared__ int done_cnt[NST];  // SELF: consumer warps finished with the stage's tile
-  __shared__ __align__(16) E s_dummy[Pow<P, D>::v];  // SFT_BRANCHLESS: in-place stores of rows without output
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (threadIdx.x < NST) {
-    done_cnt[threadIdx.x] = 0;
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full[threadIdx.x])));
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&empty[threadIdx.x])), "r"(NC));
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&p1done[threadIdx.x])), "r"(NC * 32));
@@ -1411,44 +1108,10 @@ __global__ __launch_bounds__((NC + (SELF ? 0 : 1)) * 32, MINB) void k_translate_
   if (threadIdx.x == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   fill_tail_smem<D, P>(frag);
   __syncthreads();
-  if (!SELF && warp == NC) {
+  if (warp == NC) {
     ws_producer<D, P, G, NST, E, PD, BATCH, NB>(a, sched, ntiles, ring, blk, full, empty);
     return;
   }
-  const int64_t nr_ = BATCH ? a.nrhs : 1;
-  if (SELF && warp == 0) {
-    // prologue: the first NST work items of this CTA (after the previous
-    // level has completed: programmatic dependent launch)
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    for (int j = 0; j < NST; ++j) {
-      const int64_t wj = blockIdx.x + (int64_t)j * gridDim.x;
-      if (wj >= ntiles * nr_) break;
-      const int64_t tj = BATCH ? wj / nr_ : wj;
-      ws_issue<D, P, G, NST, E, PD, BATCH, NB>(a, sched, wj, tj, ws_group_record<D, P, G, NB>(sched, tj, true), ring, blk,
-                                           full, j);
-    }
-  }
-  // SELF: this warp is done with stage st (work item w_); the last of the NC
-  // warps to finish refills it with work item w_ + NST * gridDim.x
-  auto self_release = [&](int st, int64_t w_) {
-    __syncwarp();
-    int old = 0;
-    if (lane == 0) {
-      __threadfence_block();
-      old = atomicAdd(&done_cnt[st], 1);
-    }
-    old = __shfl_sync(0xffffffffu, old, 0);
-    if (old == NC - 1) {
-      __threadfence_block();
-      if (lane == 0) done_cnt[st] = 0;
-      const int64_t wn = w_ + (int64_t)NST * gridDim.x;
-      if (wn < ntiles * nr_) {
-        const int64_t tn = BATCH ? wn / nr_ : wn;
-        ws_issue<D, P, G, NST, E, PD, BATCH, NB>(a, sched, wn, tn, ws_group_record<D, P, G, NB>(sched, tn, true), ring,
-                                             blk, full, st);
-      }
-    }
-  };
   // ---------------- consumers ----------------
   LaneOps<P, TailSmem<D>::v> op;
   load_lane_ops(op, frag, lane);
@@ -1458,17 +1121,17 @@ __global__ __launch_bounds__((NC + (SELF ? 0 : 1)) * 32, MINB) void k_translate_
   // 2D: first passes (list 1: axis 1, list 2: axis 0 for groups in reversed
   // order), then last passes (list 0: axis 0, list 3: axis 1)
   auto first2d = [&](E* sb_, const unsigned char* bk) {
-    consumer_pass<D, P, G, NC, D - 1, false, 1, E>(a, sb_, bk, op, rot, 0, s_dummy);
-    if constexpr (D == 2) consumer_pass<D, P, G, NC, 0, false, 2, E>(a, sb_, bk, op, rot, 0, s_dummy);
+    consumer_pass<D, P, G, NC, D - 1, false, 1, E>(a, sb_, bk, op, rot, 0);
+    if constexpr (D == 2) consumer_pass<D, P, G, NC, 0, false, 2, E>(a, sb_, bk, op, rot, 0);
   };
   auto last2d = [&](E* sb_, const unsigned char* bk, int64_t oo) {
-    consumer_pass<D, P, G, NC, 0, true, 0, E, FUSED>(a, sb_, bk, op, rot, oo, s_dummy);
-    if constexpr (D == 2) consumer_pass<D, P, G, NC, D - 1, true, 3, E, FUSED>(a, sb_, bk, op, rot, oo, s_dummy);
+    consumer_pass<D, P, G, NC, 0, true, 0, E, FUSED>(a, sb_, bk, op, rot, oo);
+    if constexpr (D == 2) consumer_pass<D, P, G, NC, D - 1, true, 3, E, FUSED>(a, sb_, bk, op, rot, oo);
   };
   // work items w = tile * nrhs + r; the output of RHS r goes to out + r * rs
   const int64_t nwork = BATCH ? ntiles * a.nrhs : ntiles;
   auto ooff = [&](int64_t w_) { return BATCH ? (w_ % a.nrhs) * a.rs : (int64_t)0; };
-  if constexpr (D == 2 && NST >= 3 && !SELF && !F2) {
+  if constexpr (D == 2 && NST >= 3 && !F2) {
     int64_t tile = blockIdx.x;
     if (tile < nwork) {
       mbar_wait(smem_u32(&full[0]), 0);
@@ -1511,17 +1174,17 @@ __global__ __launch_bounds__((NC + (SELF ? 0 : 1)) * 32, MINB) void k_translate_
         // 1) on the transposed slots, its second pass to HBM
         const unsigned char* bk0 = blk[s];
         const unsigned char* bk1 = blk[s] + SC::BLK;
-        consumer_pass<D, P, G, NC, 1, false, 1, E>(a, sb, bk0, op, rot, 0, s_dummy);
-        consumer_pass<D, P, G, NC, 0, false, 2, E>(a, sb, bk0, op, rot, 0, s_dummy);
+        consumer_pass<D, P, G, NC, 1, false, 1, E>(a, sb, bk0, op, rot, 0);
+        consumer_pass<D, P, G, NC, 0, false, 2, E>(a, sb, bk0, op, rot, 0);
         consumer_sync<NC * 32>();
-        consumer_pass<D, P, G, NC, 0, false, 0, E>(a, sb, bk0, op, rot, 0, s_dummy);
-        consumer_pass<D, P, G, NC, 1, false, 3, E>(a, sb, bk0, op, rot, 0, s_dummy);
+        consumer_pass<D, P, G, NC, 0, false, 0, E>(a, sb, bk0, op, rot, 0);
+        consumer_pass<D, P, G, NC, 1, false, 3, E>(a, sb, bk0, op, rot, 0);
         consumer_sync<NC * 32>();
-        consumer_pass<D, P, G, NC, 1, false, 1, E, false, 1>(a, sb, bk1, op, rot, 0, s_dummy);
-        consumer_pass<D, P, G, NC, 0, false, 2, E, false, 1>(a, sb, bk1, op, rot, 0, s_dummy);
+        consumer_pass<D, P, G, NC, 1, false, 1, E, false, 1>(a, sb, bk1, op, rot, 0);
+        consumer_pass<D, P, G, NC, 0, false, 2, E, false, 1>(a, sb, bk1, op, rot, 0);
         consumer_sync<NC * 32>();
-        consumer_pass<D, P, G, NC, 0, true, 0, E, false, 1>(a, sb, bk1, op, rot, ooff(w), s_dummy);
-        consumer_pass<D, P, G, NC, 1, true, 3, E, false, 1>(a, sb, bk1, op, rot, ooff(w), s_dummy);
+        consumer_pass<D, P, G, NC, 0, true, 0, E, false, 1>(a, sb, bk1, op, rot, ooff(w));
+        consumer_pass<D, P, G, NC, 1, true, 3, E, false, 1>(a, sb, bk1, op, rot, ooff(w));
       } else if constexpr (D == 2) {
         INSTR_T0(t1);
         first2d(sb, blk[s]);
@@ -1533,19 +1196,15 @@ __global__ __launch_bounds__((NC + (SELF ? 0 : 1)) * 32, MINB) void k_translate_
         last2d(sb, blk[s], ooff(w));
         INSTR_ADD(7, t3);
       } else {
-        consumer_pass<D, P, G, NC, 2, false, 2, E>(a, sb, blk[s], op, rot, 0, s_dummy);
+        consumer_pass<D, P, G, NC, 2, false, 2, E>(a, sb, blk[s], op, rot, 0);
         consumer_sync<NC * 32>();
-        consumer_pass<D, P, G, NC, 1, false, 1, E>(a, sb, blk[s], op, rot, 0, s_dummy);
+        consumer_pass<D, P, G, NC, 1, false, 1, E>(a, sb, blk[s], op, rot, 0);
         consumer_sync<NC * 32>();
-        consumer_pass<D, P, G, NC, 0, true, 0, E, FUSED>(a, sb, blk[s], op, rot, ooff(w), s_dummy);
+        consumer_pass<D, P, G, NC, 0, true, 0, E, FUSED>(a, sb, blk[s], op, rot, ooff(w));
       }
-      if constexpr (SELF) {
-        self_release(s, w);
-      } else {
-        __syncwarp();
-        if (lane == 0)
-          asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[s])) : "memory");
-      }
+      __syncwarp();
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[s])) : "memory");
       if (++s == NST) {
         s = 0;
         ph ^= 1u;
@@ -1556,167 +1215,6 @@ __global__ __launch_bounds__((NC + (SELF ? 0 : 1)) * 32, MINB) void k_translate_
   // the kernel completes (the caller's cross-rank barrier follows on the stream)
   if (FUSED) __threadfence_system();
   INSTR_ADD(3, tc0);
-}
-
-// ------------------------------------------------------------------------
-// FP32 variant (opts.precision = 1): same producer / stage ring / schedule,
-// FFMA consumers, one thread per fiber task, constant-bank float operators.
-// Pair arrays have stride PS = p^d rounded up to even (16-byte bulk copies).
-// ------------------------------------------------------------------------
-template <int D, int P>
-struct F32 {
-  static constexpr int PD = Pow<P, D>::v;
-  static constexpr int PS = PD + (PD & 1);
-};
-
-// One pass: chunk j (32 fibers) of this pass goes to consumer warp (base + j)
-// mod NC, `base` running over the whole sequence of passes so that warps
-// stay balanced however few fibers a pass has.  Returns the next base.
-template <int D, int P, int G, int NC, int AX, bool LAST, int LIST = AX>
-__device__ __noinline__ int f32_consumer_pass(float2* __restrict__ out, float2* __restrict__ sb,
-                                             const unsigned char* __restrict__ blk, int base, int warp) {
-  using SC = Sched<D, P, G>;
-  constexpr int PS = F32<D, P>::PS;
-  constexpr int PF = Pow<P, D>::v / P;
-  constexpr int STR = Pow<P, D - 1 - AX>::v;
-  constexpr int SH = D - 1 - AX;
-  const int* cnt = SC::cnt(blk) + 3 * LIST;
-  const TaskRec* tasks = SC::task(blk, LIST);
-  const int ntot = (cnt[0] + cnt[1] + cnt[2]) * PF;
-  const int nch = (ntot + 31) >> 5;
-  const int lane = threadIdx.x & 31;
-  for (int j = (warp - base % NC + NC) % NC; j < nch; j += NC) {
-    const int tau = j * 32 + lane;
-    if (tau < ntot) {
-      const TaskRec te = tasks[tau / PF];
-      const int f = tau % PF;
-      const int ebase = (f / STR) * STR * P + f % STR;
-      float2* s0 = sb + te.x + ebase;
-      float2* s1 = s0 + (1 << SH) * G * PS;  // slot-major stage
-      float2* o0;
-      float2* o1;
-      if (!LAST) {
-        o0 = s0;
-        o1 = s1;
-      } else {
-        o0 = te.o0 != ~0u ? out + te.o0 + ebase : nullptr;
-        o1 = te.o1 != ~0u ? out + te.o1 + ebase : nullptr;
-      }
-      auto store = [&](int m, float2 z0, float2 z1) {
-        if (o0) o0[m * STR] = z0;
-        if (o1) o1[m * STR] = z1;
-      };
-      float2 x0[P], x1[P];
-      if (te.cls == 3) {
-#pragma unroll
-        for (int l = 0; l < P; ++l) {
-          x0[l] = s0[l * STR];
-          x1[l] = s1[l * STR];
-        }
-        contract_fiber_t<float2, CTf<P>, P, 3>(x0, x1, store);
-      } else if (te.cls == 1) {
-#pragma unroll
-        for (int l = 0; l < P; ++l) x0[l] = s0[l * STR];
-        contract_fiber_t<float2, CTf<P>, P, 1>(x0, x1, store);
-      } else {
-#pragma unroll
-        for (int l = 0; l < P; ++l) x1[l] = s1[l * STR];
-        contract_fiber_t<float2, CTf<P>, P, 2>(x0, x1, store);
-      }
-    }
-  }
-  return base + nch;
-}
-
-template <int D, int P, int G, int NC, int NST, int MINB>
-__global__ __launch_bounds__((NC + 1) * 32, MINB) void k_translate_f32(TransArgs a, const unsigned char* __restrict__ sched,
-                                                                      int64_t ntiles) {
-  using SC = Sched<D, P, G>;
-  constexpr int PS = F32<D, P>::PS;
-  constexpr int NS = 1 << D;
-  constexpr int STAGE = G * NS * PS;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  float2* ring = reinterpret_cast<float2*>(smem_raw);  // [NST][G][NS][PS]
-  __shared__ __align__(128) unsigned char blk[NST][SC::BLK];
-  __shared__ __align__(8) uint64_t full[NST], empty[NST], p1done[NST];
-  __shared__ int done_cnt[NST];  // SELF: consumer warps finished with the stage's tile
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x < NST) {
-    done_cnt[threadIdx.x] = 0;
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full[threadIdx.x])));
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&empty[threadIdx.x])), "r"(NC));
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&p1done[threadIdx.x])), "r"(NC * 32));
-  }
-  if (threadIdx.x == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  __syncthreads();
-  if (warp == NC) {
-    ws_producer<D, P, G, NST, float2, PS>(a, sched, ntiles, ring, blk, full, empty);
-    return;
-  }
-  float2* out = reinterpret_cast<float2*>(a.out);
-  auto first2d = [&](float2* sb_, const unsigned char* bk, int b_) {
-    b_ = f32_consumer_pass<D, P, G, NC, D - 1, false, 1>(out, sb_, bk, b_, warp);
-    if constexpr (D == 2) b_ = f32_consumer_pass<D, P, G, NC, 0, false, 2>(out, sb_, bk, b_, warp);
-    return b_;
-  };
-  auto last2d = [&](float2* sb_, const unsigned char* bk, int b_) {
-    b_ = f32_consumer_pass<D, P, G, NC, 0, true, 0>(out, sb_, bk, b_, warp);
-    if constexpr (D == 2) b_ = f32_consumer_pass<D, P, G, NC, D - 1, true, 3>(out, sb_, bk, b_, warp);
-    return b_;
-  };
-  int s = 0, base = 0;
-  uint32_t ph = 0;
-  auto release = [&](int st) {
-    __syncwarp();
-    if (lane == 0)
-      asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[st])) : "memory");
-  };
-  if constexpr (D == 2 && NST >= 3) {
-    // step k: pass 1 of this CTA's tile k (if any), then pass 0 of tile k-1
-    int sp = 0;
-    uint32_t php = 0;
-    for (int64_t k = 0;; ++k) {
-      const int64_t t1 = blockIdx.x + k * (int64_t)gridDim.x;
-      if (k > 0 && t1 - gridDim.x >= ntiles) break;
-      if (t1 < ntiles) {
-        mbar_wait(smem_u32(&full[s]), ph);
-        base = first2d(ring + s * STAGE, blk[s], base);
-        asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&p1done[s])) : "memory");
-      }
-      if (k > 0) {
-        mbar_wait(smem_u32(&p1done[sp]), php);
-        base = last2d(ring + sp * STAGE, blk[sp], base);
-        release(sp);
-      }
-      sp = s;
-      php = ph;
-      if (++s == NST) {
-        s = 0;
-        ph ^= 1u;
-      }
-    }
-  } else {
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-      mbar_wait(smem_u32(&full[s]), ph);
-      float2* sb = ring + s * STAGE;
-      if constexpr (D == 2) {
-        base = first2d(sb, blk[s], base);
-        consumer_sync<NC * 32>();
-        base = last2d(sb, blk[s], base);
-      } else {
-        base = f32_consumer_pass<D, P, G, NC, 2, false>(out, sb, blk[s], base, warp);
-        consumer_sync<NC * 32>();
-        base = f32_consumer_pass<D, P, G, NC, 1, false>(out, sb, blk[s], base, warp);
-        consumer_sync<NC * 32>();
-        base = f32_consumer_pass<D, P, G, NC, 0, true>(out, sb, blk[s], base, warp);
-      }
-      release(s);
-      if (++s == NST) {
-        s = 0;
-        ph ^= 1u;
-      }
-    }
-  }
 }
 
 template <int P>
@@ -1771,10 +1269,8 @@ static std::vector<double> mma_fragments() {
   for (int b = 0; b < 2; ++b)
     for (int l = 0; l < P; l += 2)
       for (int m = 0; m < P; ++m)
-        if (2 * m != b * (P - 1) + l && (rc(b, m, l) != 0.0 || rs(b, m, l) != 0.0)) {
-          fprintf(stderr, "sft: operator table is not delta-structured at (%d,%d,%d)\n", b, m, l);
-          abort();
-        }
+        if (2 * m != b * (P - 1) + l && (rc(b, m, l) != 0.0 || rs(b, m, l) != 0.0))
+          return {};  // (never for p = 5, 7, 9; reported as an error by device_fragments)
   return fr;
 }
 
@@ -1788,6 +1284,10 @@ static const double* device_fragments(cudaError_t* err) {
   auto it = cache.find(dev);
   if (it != cache.end()) return it->second;
   std::vector<double> fr = mma_fragments<P>();
+  if (fr.empty()) {  // the operator tables are not delta-structured: the DMMA split would be wrong
+    *err = cudaErrorInvalidValue;
+    return nullptr;
+  }
   double* d = nullptr;
   if ((*err = cudaMalloc(&d, fr.size() * sizeof(double))) != cudaSuccess) return nullptr;
   if ((*err = cudaMemcpy(d, fr.data(), fr.size() * sizeof(double), cudaMemcpyHostToDevice)) != cudaSuccess)
@@ -1795,90 +1295,6 @@ static const double* device_fragments(cudaError_t* err) {
   cache[dev] = d;
   return d;
 }
-
-// ------------------------------------------------------------------------
-// FMA kernel (round-1 design, kept for ablation: SFT_TRANSLATE=fma)
-// ------------------------------------------------------------------------
-template <int D, int P, int G, int NT, int AX, bool LAST>
-__device__ __forceinline__ void fma_pass(const TransArgs& a, double2* __restrict__ sb, const GroupMeta* gm, int ng,
-                                         TaskEntry* ent, int* cnt) {
-  constexpr int PD = Pow<P, D>::v;
-  constexpr int NS = 1 << D;
-  constexpr int PF = PD / P;
-  constexpr int STR = Pow<P, D - 1 - AX>::v;
-  constexpr int SH = D - 1 - AX;
-  constexpr int MAXE = G << (D - 1);
-  build_tasks<D, G, AX>(gm, ng, ent, cnt);
-  const int n3 = cnt[0], n1 = cnt[1], n2 = cnt[2];
-  const int ntot = (n3 + n1 + n2) * PF;
-  for (int tau = threadIdx.x; tau < ntot; tau += NT) {
-    const TaskEntry te = task_at<MAXE>(ent, tau / PF, n3, n1);
-    const int f = tau % PF;
-    const GroupMeta& g = gm[te.j];
-    const int lo = f % STR, hi = f / STR;
-    const int ebase = hi * STR * P + lo;
-    const int slot0 = (te.bp << (D - AX)) | te.as;
-    double2* s0 = sb + ((int)te.j * NS + slot0) * PD + ebase;
-    double2* s1 = s0 + (1 << SH) * PD;
-    double2 x0[P], x1[P];
-    double2* o0;
-    double2* o1;
-    if (!LAST) {
-      o0 = s0;
-      o1 = s1;
-    } else {
-      o0 = out_array<PD>(a, g, te.as);
-      o1 = out_array<PD>(a, g, (1 << SH) | te.as);
-      if (o0) o0 += ebase;
-      if (o1) o1 += ebase;
-    }
-    auto store = [&](int m, double2 z0, double2 z1) {
-      if (o0) o0[m * STR] = z0;
-      if (o1) o1[m * STR] = z1;
-    };
-    if (te.cls == 3) {
-#pragma unroll
-      for (int l = 0; l < P; ++l) {
-        x0[l] = s0[l * STR];
-        x1[l] = s1[l * STR];
-      }
-      contract_fiber<P, 3>(x0, x1, store);
-    } else if (te.cls == 1) {
-#pragma unroll
-      for (int l = 0; l < P; ++l) x0[l] = s0[l * STR];
-      contract_fiber<P, 1>(x0, x1, store);
-    } else {
-#pragma unroll
-      for (int l = 0; l < P; ++l) x1[l] = s1[l * STR];
-      contract_fiber<P, 2>(x0, x1, store);
-    }
-  }
-  __syncthreads();
-}
-
-// minBlocksPerSM: target 16 resident warps (an explicit 1 lets ptxas take
-// ~200 registers and halves occupancy; forcing fewer than ~120 spills)
-#define SFT_FMA_MINB(NT) ((16 * 32 / (NT)) > 0 ? (16 * 32 / (NT)) : 1)
-template <int D, int P, int G, int NT>
-__global__ __launch_bounds__(NT, SFT_FMA_MINB(NT)) void k_translate_fma(TransArgs a) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  double2* sb = reinterpret_cast<double2*>(smem_raw);  // [G][NS][PD]
-  __shared__ GroupMeta gm[G];
-  __shared__ TaskEntry ent[3 * (G << (D - 1))];
-  __shared__ int cnt[4];
-  __shared__ __align__(8) uint64_t bar;
-  const int ng = tile_prologue<D, P, G>(a, sb, gm, &bar);
-  mbar_wait(smem_u32(&bar), 0);
-  if constexpr (D == 2) {
-    fma_pass<D, P, G, NT, 1, false>(a, sb, gm, ng, ent, cnt);
-    fma_pass<D, P, G, NT, 0, true>(a, sb, gm, ng, ent, cnt);
-  } else {
-    fma_pass<D, P, G, NT, 2, false>(a, sb, gm, ng, ent, cnt);
-    fma_pass<D, P, G, NT, 1, false>(a, sb, gm, ng, ent, cnt);
-    fma_pass<D, P, G, NT, 0, true>(a, sb, gm, ng, ent, cnt);
-  }
-}
-
 
 // ------------------------------------------------------------------------
 // launch configuration (tile of G groups per stage; tuned on B200)
@@ -1905,9 +1321,6 @@ __global__ __launch_bounds__(NT, SFT_FMA_MINB(NT)) void k_translate_fma(TransArg
 // (the register cap: MINB * (NC+1) warps share the 64K registers)
 #ifndef SFT_WS_MINB29
 #define SFT_WS_MINB29 4  // caps every variant (batch, two-level) at 96 registers: 4 CTAs per SM
-#endif
-#ifndef SFT_SELF_DEFAULT
-#define SFT_SELF_DEFAULT 0
 #endif
 template <int D, int P>
 struct WsCfg;
@@ -1980,29 +1393,7 @@ template <> struct WsCfg<3, 7> {
 };
 template <> struct WsCfg<3, 9> { static constexpr int G = 1, NC = 8, NST = 2, MINB = 1; };
 
-// self-fed mode (k_translate_ws<..., SELF = true>): min CTAs per SM for the
-// register cap (NC warps per CTA instead of NC + 1)
-template <int D, int P>
-struct SelfCfg {
-  static constexpr int MINB = D == 2 && P == 9 ? 5 : WsCfg<D, P>::MINB;
-};
-// SFT_SELF=0/1 overrides; default: on where measured faster
-static int self_env() {
-  static int v = -2;
-  if (v == -2) {
-    const char* e = getenv("SFT_SELF");
-    v = e ? (e[0] == '1' ? 1 : 0) : -1;
-  }
-  return v;
-}
-template <int D>
-static bool use_self(int nst) {
-  if (D == 2 && nst >= 3) return false;  // skewed pipeline needs the producer
-  const int v = self_env();
-  return v < 0 ? SFT_SELF_DEFAULT : v == 1;
-}
-
-// FP32 storage on the DMMA kernel (default FP32 variant): arrays are half the
+// FP32 storage on the DMMA kernel (the FP32 variant): arrays are half the
 // size, so twice the groups per stage at the same shared memory
 template <int D, int P>
 struct F32WsCfg;
@@ -2012,35 +1403,6 @@ template <> struct F32WsCfg<2, 9> { static constexpr int G = SFT_F32_G29, NC = S
 template <> struct F32WsCfg<3, 5> { static constexpr int G = 4, NC = 4, NST = 2, MINB = 3; };
 template <> struct F32WsCfg<3, 7> { static constexpr int G = 2, NC = 8, NST = 2, MINB = 1; };
 template <> struct F32WsCfg<3, 9> { static constexpr int G = 1, NC = 8, NST = 2, MINB = 1; };
-
-// SFT_F32_FFMA=1: the FP32 variant on the FFMA thread-per-fiber kernel (ablation)
-static bool f32_ffma() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("SFT_F32_FFMA");
-    v = (e && e[0] == '1') ? 1 : 0;
-  }
-  return v == 1;
-}
-
-// FP32 kernel: G groups per tile, NC FFMA consumer warps, NST stages, MINB CTAs/SM
-template <int D, int P>
-struct F32Cfg;
-template <> struct F32Cfg<2, 5> { static constexpr int G = 32, NC = 8, NST = 3, MINB = 2; };
-template <> struct F32Cfg<2, 7> { static constexpr int G = 16, NC = 8, NST = 3, MINB = 2; };
-template <> struct F32Cfg<2, 9> { static constexpr int G = 8, NC = 8, NST = 3, MINB = 2; };
-template <> struct F32Cfg<3, 5> { static constexpr int G = 4, NC = 8, NST = 3, MINB = 2; };
-template <> struct F32Cfg<3, 7> { static constexpr int G = 1, NC = 8, NST = 3, MINB = 2; };
-template <> struct F32Cfg<3, 9> { static constexpr int G = 1, NC = 8, NST = 2, MINB = 1; };
-
-template <int D, int P>
-struct FmaCfg;
-template <> struct FmaCfg<2, 5> { static constexpr int G = 16, NT = 128; };
-template <> struct FmaCfg<2, 7> { static constexpr int G = 12, NT = 128; };
-template <> struct FmaCfg<2, 9> { static constexpr int G = 16, NT = 256; };
-template <> struct FmaCfg<3, 5> { static constexpr int G = 4, NT = 256; };
-template <> struct FmaCfg<3, 7> { static constexpr int G = 2, NT = 256; };
-template <> struct FmaCfg<3, 9> { static constexpr int G = 1, NT = 256; };
 
 static TransArgs make_args(const LevelDims& L, const double2* in, double2* out) {
   TransArgs a;
@@ -2090,18 +1452,6 @@ static bool pdl_enabled() {
   return v == 1;
 }
 
-// SFT_TRANSLATE = mma (DMMA consumers, default) | fma (round-1 kernel)
-int translate_kernel_choice() {
-  static int mode = -1;
-  if (mode < 0) {
-    const char* e = getenv("SFT_TRANSLATE");
-    mode = 0;
-    if (e && strcmp(e, "fma") == 0) mode = 1;
-  }
-  return mode;
-}
-
-// groups per tile of the schedule for the selected kernel (0: no schedule)
 // Launch with programmatic stream serialization (PDL): the kernel may start
 // while the previous kernel on the stream drains; it must execute
 // griddepcontrol.wait before touching that kernel's data.
@@ -2121,162 +1471,70 @@ static void launch_pdl(void (*kernel)(KArgs...), unsigned grid, unsigned block, 
   cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
 
-// resident-CTA grid size for a persistent kernel
+// Resident-CTA grid of a persistent kernel on the current device, with the
+// kernel's dynamic shared-memory opt-in done once per device (a process may
+// plan on several GPUs: nothing here is shared between devices).
 template <class K>
 static cudaError_t persistent_grid(K kernel, int threads, size_t smem, int* grid) {
-  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  static PerDevice<int> cache;
+  return cache.get(grid, [&](int dev, int* out) {
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int nsm = 0, bps = 0;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kernel, threads, smem);
+    if (e != cudaSuccess) return e;
+    if (bps < 1) return cudaErrorInvalidConfiguration;
+    *out = nsm * bps;
+    return cudaSuccess;
+  });
+}
+
+// One persistent launch of k_translate_ws<D, P, G, NC, NST, MB, E, FUSED, BATCH, F2>
+template <int D, int P, int G, int NC, int NST, int MB, typename E, bool FUSED, bool BATCH, bool F2>
+static cudaError_t launch_ws(const sft_plan_s* Pl, const TransArgs& a, const LevelDims& L, int64_t work) {
+  constexpr int PS = StrideT<E, Pow<P, D>::v>::v;
+  const size_t smem = (size_t)NST * G * (1 << D) * PS * sizeof(E);
+  auto kern = k_translate_ws<D, P, G, NC, NST, MB, E, FUSED, BATCH, F2>;
+  int grid_max = 0;
+  cudaError_t e = persistent_grid(kern, (NC + 1) * 32, smem, &grid_max);
   if (e != cudaSuccess) return e;
-  int dev = 0, nsm = 0, bps = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kernel, threads, smem);
-  if (e != cudaSuccess) return e;
-  if (bps < 1) return cudaErrorInvalidConfiguration;
-  *grid = nsm * bps;
-  return cudaSuccess;
+  const double* frag = device_fragments<P>(&e);
+  if (!frag) return e;
+  const int64_t ntiles = (a.ngroups + G - 1) / G;
+  launch_pdl(kern, (unsigned)std::min<int64_t>(work, grid_max), (NC + 1) * 32, smem, Pl->stream, a, frag, L.sched,
+             ntiles);
+  count_launch();
+  return cudaGetLastError();
 }
 
 template <int D, int P>
 static cudaError_t launch_translate_t(const sft_plan_s* Pl, const LevelDims& L, const void* in, void* out) {
-  constexpr int PD = Pow<P, D>::v;
   TransArgs a = make_args(L, (const double2*)in, (double2*)out);
   if (a.ngroups <= 0) return cudaSuccess;
-  if (a.nrhs < 1 || (a.nrhs > 1 && (a.npeer > 0 || (Pl->prec == 1 ? f32_ffma() : translate_kernel_choice() != 0))))
-    return cudaErrorInvalidValue;  // batches run on the warp-specialised DMMA kernel only
-  if (a.f2 && (Pl->prec != 0 || translate_kernel_choice() != 0 || a.npeer > 0))
-    return cudaErrorInvalidValue;  // two-level launches: FP64 warp-specialised kernel only
-  if (Pl->prec == 1 && !f32_ffma()) {
+  if (!L.sched) return cudaErrorInvalidValue;
+  if (a.nrhs < 1 || (a.nrhs > 1 && a.npeer > 0)) return cudaErrorInvalidValue;
+  if (a.f2 && (Pl->prec != 0 || a.npeer > 0)) return cudaErrorInvalidValue;  // two-level: FP64 only
+  if (Pl->prec == 1) {
     // FP32 storage, FP64 arithmetic on the tensor cores (same kernel as FP64)
-    constexpr int G = F32WsCfg<D, P>::G, NC = F32WsCfg<D, P>::NC, NST = F32WsCfg<D, P>::NST,
-                  MB = F32WsCfg<D, P>::MINB;
-    const size_t smem = (size_t)NST * G * (1 << D) * F32<D, P>::PS * sizeof(float2);
-    static int grid_max = 0;
-    static const double* frag = nullptr;
-    if (!grid_max) {
-      cudaError_t e = persistent_grid(k_translate_ws<D, P, G, NC, NST, MB, float2>, (NC + 1) * 32, smem, &grid_max);
-      if (e != cudaSuccess) return e;
-      frag = device_fragments<P>(&e);
-      if (!frag) return e;
-    }
-    if (!L.sched) return cudaErrorInvalidValue;
-    const int64_t ntiles = (a.ngroups + G - 1) / G;
-    const int64_t grid = std::min<int64_t>(ntiles * a.nrhs, grid_max);
-    if (a.nrhs > 1) {
-      static int grid_b = 0;
-      if (!grid_b) {
-        cudaError_t e = persistent_grid(k_translate_ws<D, P, G, NC, NST, MB, float2, false, true>, (NC + 1) * 32,
-                                        smem, &grid_b);
-        if (e != cudaSuccess) return e;
-      }
-      launch_pdl(k_translate_ws<D, P, G, NC, NST, MB, float2, false, true>,
-                 (unsigned)std::min<int64_t>(ntiles * a.nrhs, grid_b), (NC + 1) * 32, smem, Pl->stream, a, frag,
-                 L.sched, ntiles);
-    } else {
-      launch_pdl(k_translate_ws<D, P, G, NC, NST, MB, float2>, (unsigned)grid, (NC + 1) * 32, smem, Pl->stream, a,
-                 frag, L.sched, ntiles);
-    }
-  } else if (Pl->prec == 1) {
-    constexpr int G = F32Cfg<D, P>::G, NC = F32Cfg<D, P>::NC, NST = F32Cfg<D, P>::NST, MB = F32Cfg<D, P>::MINB;
-    const size_t smem = (size_t)NST * G * (1 << D) * F32<D, P>::PS * sizeof(float2);
-    static int grid_max = 0;
-    if (!grid_max) {
-      cudaError_t e = persistent_grid(k_translate_f32<D, P, G, NC, NST, MB>, (NC + 1) * 32, smem, &grid_max);
-      if (e != cudaSuccess) return e;
-    }
-    if (!L.sched) return cudaErrorInvalidValue;
-    const int64_t ntiles = (a.ngroups + G - 1) / G;
-    const int64_t grid = std::min<int64_t>(ntiles, grid_max);
-    launch_pdl(k_translate_f32<D, P, G, NC, NST, MB>, (unsigned)grid, (NC + 1) * 32, smem, Pl->stream, a, L.sched,
-               ntiles);
-  } else if (translate_kernel_choice() == 0) {
-    constexpr int G = WsCfg<D, P>::G, NC = WsCfg<D, P>::NC, NST = WsCfg<D, P>::NST, MB = WsCfg<D, P>::MINB;
-    const size_t smem = (size_t)NST * G * (1 << D) * PD * sizeof(double2);
-    static int grid_max = 0;
-    static const double* frag = nullptr;
-    if (!grid_max) {
-      cudaError_t e = persistent_grid(k_translate_ws<D, P, G, NC, NST, MB>, (NC + 1) * 32, smem, &grid_max);
-      if (e != cudaSuccess) return e;
-      frag = device_fragments<P>(&e);
-      if (!frag) return e;
-    }
-    if (!L.sched) return cudaErrorInvalidValue;
-    const int64_t ntiles = (a.ngroups + G - 1) / G;
-    const int64_t grid = std::min<int64_t>(ntiles * a.nrhs, grid_max);
-    if (a.npeer > 0) {
-      static bool fattr = false;
-      if (!fattr) {
-        cudaError_t e = cudaFuncSetAttribute(k_translate_ws<D, P, G, NC, NST, MB, double2, true>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        fattr = true;
-      }
-      launch_pdl(k_translate_ws<D, P, G, NC, NST, MB, double2, true>, (unsigned)grid, (NC + 1) * 32, smem,
-                 Pl->stream, a, frag, L.sched, ntiles);
-    } else if (a.f2) {
-      // two-level launch (2D, G = 4k, unskewed configurations)
-      if constexpr (D == 2 && G % 4 == 0 && NST < 3) {
-        static bool fattr2 = false;
-        if (!fattr2) {
-          cudaError_t e = cudaFuncSetAttribute(k_translate_ws<D, P, G, NC, NST, MB, double2, false, false, false, true>,
-                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-          if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(k_translate_ws<D, P, G, NC, NST, MB, double2, false, true, false, true>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-          if (e != cudaSuccess) return e;
-          fattr2 = true;
-        }
-        if (a.nrhs > 1)
-          launch_pdl(k_translate_ws<D, P, G, NC, NST, MB, double2, false, true, false, true>, (unsigned)grid,
-                     (NC + 1) * 32, smem, Pl->stream, a, frag, L.sched, ntiles);
-        else
-          launch_pdl(k_translate_ws<D, P, G, NC, NST, MB, double2, false, false, false, true>, (unsigned)grid,
-                     (NC + 1) * 32, smem, Pl->stream, a, frag, L.sched, ntiles);
-      } else {
-        return cudaErrorInvalidValue;
-      }
-    } else if (a.nrhs > 1) {
-      static int grid_b = 0;  // the batch variant's own occupancy (it may hold more registers)
-      if (!grid_b) {
-        cudaError_t e = persistent_grid(k_translate_ws<D, P, G, NC, NST, MB, double2, false, true>, (NC + 1) * 32,
-                                        smem, &grid_b);
-        if (e != cudaSuccess) return e;
-      }
-      launch_pdl(k_translate_ws<D, P, G, NC, NST, MB, double2, false, true>,
-                 (unsigned)std::min<int64_t>(ntiles * a.nrhs, grid_b), (NC + 1) * 32, smem, Pl->stream, a, frag,
-                 L.sched, ntiles);
-    } else if (use_self<D>(NST)) {
-      // self-fed consumers (no producer warp): one more CTA per SM where registers allowed NC + 1 warps
-      if constexpr (!(D == 2 && NST >= 3)) {
-        constexpr int MBS = SelfCfg<D, P>::MINB;
-        static int grid_self = 0;
-        if (!grid_self) {
-          cudaError_t e = persistent_grid(k_translate_ws<D, P, G, NC, NST, MBS, double2, false, false, true>,
-                                          NC * 32, smem, &grid_self);
-          if (e != cudaSuccess) return e;
-        }
-        launch_pdl(k_translate_ws<D, P, G, NC, NST, MBS, double2, false, false, true>,
-                   (unsigned)std::min<int64_t>(ntiles, grid_self), NC * 32, smem, Pl->stream, a, frag, L.sched,
-                   ntiles);
-      }
-    } else {
-      launch_pdl(k_translate_ws<D, P, G, NC, NST, MB>, (unsigned)grid, (NC + 1) * 32, smem, Pl->stream, a, frag,
-                 L.sched, ntiles);
-    }
-  } else {
-    constexpr int G = FmaCfg<D, P>::G, NT = FmaCfg<D, P>::NT;
-    const size_t smem = (size_t)G * (1 << D) * PD * sizeof(double2);
-    static bool attr = false;
-    if (!attr) {
-      cudaError_t e = cudaFuncSetAttribute(k_translate_fma<D, P, G, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)smem);
-      if (e != cudaSuccess) return e;
-      attr = true;
-    }
-    const int64_t ntiles = (a.ngroups + G - 1) / G;
-    k_translate_fma<D, P, G, NT><<<(unsigned)ntiles, NT, smem, Pl->stream>>>(a);
+    using C = F32WsCfg<D, P>;
+    const int64_t work = (a.ngroups + C::G - 1) / C::G * a.nrhs;
+    if (a.nrhs > 1) return launch_ws<D, P, C::G, C::NC, C::NST, C::MINB, float2, false, true, false>(Pl, a, L, work);
+    return launch_ws<D, P, C::G, C::NC, C::NST, C::MINB, float2, false, false, false>(Pl, a, L, work);
   }
-  count_launch();
-  return cudaGetLastError();
+  using C = WsCfg<D, P>;
+  const int64_t work = (a.ngroups + C::G - 1) / C::G * a.nrhs;
+  if (a.npeer > 0) return launch_ws<D, P, C::G, C::NC, C::NST, C::MINB, double2, true, false, false>(Pl, a, L, work);
+  if (a.f2) {
+    // two-level launch (2D, G = 4k, unskewed configurations)
+    if constexpr (D == 2 && C::G % 4 == 0 && C::NST < 3) {
+      if (a.nrhs > 1) return launch_ws<D, P, C::G, C::NC, C::NST, C::MINB, double2, false, true, true>(Pl, a, L, work);
+      return launch_ws<D, P, C::G, C::NC, C::NST, C::MINB, double2, false, false, true>(Pl, a, L, work);
+    }
+    return cudaErrorInvalidValue;
+  }
+  if (a.nrhs > 1) return launch_ws<D, P, C::G, C::NC, C::NST, C::MINB, double2, false, true, false>(Pl, a, L, work);
+  return launch_ws<D, P, C::G, C::NC, C::NST, C::MINB, double2, false, false, false>(Pl, a, L, work);
 }
 
 template <int D, int P, int G>
@@ -2288,11 +1546,8 @@ static size_t schedule_bytes_g(const LevelDims& L) {
 
 template <int D, int P>
 static size_t schedule_bytes_t(const sft_plan_s* Pl, const LevelDims& L) {
-  if (Pl->prec == 1)
-    return f32_ffma() ? schedule_bytes_g<D, P, F32Cfg<D, P>::G>(L) : schedule_bytes_g<D, P, F32WsCfg<D, P>::G>(L);
-  const int mode = translate_kernel_choice();
-  if (mode == 0) return schedule_bytes_g<D, P, WsCfg<D, P>::G>(L);
-  return 0;
+  if (Pl->prec == 1) return schedule_bytes_g<D, P, F32WsCfg<D, P>::G>(L);
+  return schedule_bytes_g<D, P, WsCfg<D, P>::G>(L);
 }
 
 template <int D, int P, int G, int PS>
@@ -2336,17 +1591,14 @@ template <int D, int P>
 static cudaError_t launch_schedule_t(const sft_plan_s* Pl, const LevelDims* L, int nlev, unsigned char* const* dst,
                                      cudaStream_t st) {
   if (Pl->prec == 1)
-    return f32_ffma() ? launch_schedule_g<D, P, F32Cfg<D, P>::G, F32<D, P>::PS>(Pl, L, nlev, dst, st)
-                      : launch_schedule_g<D, P, F32WsCfg<D, P>::G, F32<D, P>::PS>(Pl, L, nlev, dst, st);
-  const int mode = translate_kernel_choice();
-  if (mode == 0) return launch_schedule_g<D, P, WsCfg<D, P>::G, Pow<P, D>::v>(Pl, L, nlev, dst, st);
-  return cudaSuccess;
+    return launch_schedule_g<D, P, F32WsCfg<D, P>::G, StrideT<float2, Pow<P, D>::v>::v>(Pl, L, nlev, dst, st);
+  return launch_schedule_g<D, P, WsCfg<D, P>::G, Pow<P, D>::v>(Pl, L, nlev, dst, st);
 }
 
 template <int D, int P>
 static cudaError_t check_schedule_t(const sft_plan_s* Pl, const LevelDims& L, const unsigned char* sched,
                                    int64_t in_pairs, int64_t out_pairs, int* err) {
-  if (translate_kernel_choice() != 0 || Pl->prec != 0 || L.f2) return cudaSuccess;  // (single-level layout only)
+  if (Pl->prec != 0 || L.f2) return cudaSuccess;  // (single-level layout only)
   constexpr int G = WsCfg<D, P>::G;
   TransArgs a = make_args(L, nullptr, nullptr);
   if (a.ngroups <= 0) return cudaSuccess;
@@ -2380,7 +1632,7 @@ cudaError_t launch_schedule(const sft_plan_s* Pl, const LevelDims* L, int nlev, 
 }
 
 bool two_level_supported(const sft_plan_s* Pl) {
-  if (Pl->prec != 0 || Pl->world != 1 || translate_kernel_choice() != 0) return false;
+  if (Pl->prec != 0 || Pl->sharded) return false;
   const char* e = getenv("SFT_F2");
   if (e && e[0] == '0') return false;
   if (Pl->d != 2) return false;

@@ -314,7 +314,7 @@ static cudaError_t sort_pairs(void* temp, size_t& bytes, const KT* kin, KT* kout
 // is only used before sft_plan's counts sync, so consecutive plans of one
 // thread never overlap on it.  SFT_SORT_GRAPH=0 disables (plain CUB call).
 struct SortCache {
-  int64_t n = -1;
+  int64_t n = -1, nx = -1;  // the graph sorts [0, nx) and [nx, n) as two branches: nx is part of the key
   int bits = -1, ksz = 0, nb = -1, L = -1, dev = -1;
   char* scr = nullptr;
   cudaGraphExec_t exec = nullptr;
@@ -367,7 +367,7 @@ static int sort_and_fill(sft_plan_s* P, const double* x_dev, const double* k_dev
   const bool use_graph = sort_graph_enabled() && n >= 4096 && !block_sort;
   int dev = 0;
   CK(cudaGetDevice(&dev));
-  const bool hit = use_graph && C.exec && C.n == n && C.bits == bits && C.ksz == (int)sizeof(KT) &&
+  const bool hit = use_graph && C.exec && C.n == n && C.nx == nx && C.bits == bits && C.ksz == (int)sizeof(KT) &&
                    C.nb == nbx + nbk && C.L == L && C.dev == dev;
   // graph path: X and K sorted as two parallel branches (disjoint halves of the
   // key array, the tree bit is constant in each; each sort is latency-bound, so
@@ -427,11 +427,12 @@ static int sort_and_fill(sft_plan_s* P, const double* x_dev, const double* k_dev
     if constexpr (bs_fits) {
     using BRS = cub::BlockRadixSort<KT, 1024, kBlockSortItems, int32_t, SFT_BS_BITS>;
     const size_t bsm = sizeof(typename BRS::TempStorage);
-    static bool attr = false;
-    if (!attr) {
-      CK(cudaFuncSetAttribute(k_block_sort<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm));
-      attr = true;
-    }
+    static PerDevice<int> attr;  // the shared-memory opt-in, once per device
+    int one = 0;
+    CK(attr.get(&one, [&](int, int* v) {
+      *v = 1;
+      return cudaFuncSetAttribute(k_block_sort<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm);
+    }));
     // (the tree bit above bit d*L is constant within a tree)
     k_block_sort<KT><<<2, 1024, bsm, s>>>(keys_in, idx_in, keys_out, idx_out, nx, nk, bits - 1);
     count_launch();
@@ -469,6 +470,7 @@ static int sort_and_fill(sft_plan_s* P, const double* x_dev, const double* k_dev
       cudaGraphDestroy(g);
       CK(ce);
       C.n = n;
+      C.nx = nx;
       C.bits = bits;
       C.ksz = (int)sizeof(KT);
       C.nb = nbx + nbk;
@@ -514,7 +516,7 @@ static int sort_and_fill(sft_plan_s* P, const double* x_dev, const double* k_dev
 int build_trees(sft_plan_s* P, const double* x_dev, const double* k_dev, std::string* err) {
   cudaStream_t s = P->stream;
   const int d = P->d, L = P->L;
-  const int64_t nx = P->nx, nk = P->nk, n = nx + nk;
+  const int64_t nx = P->nx, nk = P->nk;
   if (L + 1 > kMaxLevels) {
     if (err) *err = "tree depth exceeds kMaxLevels";
     return SFT_E_ARG;

@@ -125,3 +125,35 @@ def test_dist_world2_gloo(name, force):
         assert ok is True, (rank, ok)
     parts = {r[2] for r in res}
     assert len(parts) == 1  # both ranks chose the same (s_K, s_X, m)
+
+
+def _id_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_0801_1524_b200.dist import nccl_id_for
+        a = nccl_id_for()
+        b = nccl_id_for()  # cached: one communicator id per process group
+        q.put((rank, a, a is b))
+    except Exception as e:  # pragma: no cover
+        q.put((rank, repr(e), False))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_nccl_id_broadcast_gloo():
+    """DistPlan(exchange="nccl") plumbing: rank 0 makes the ncclUniqueId with
+    sft_nccl_unique_id (host call, no GPU needed) and torch.distributed
+    broadcasts it once per process group; every rank holds the same 128 bytes."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_id_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert all(isinstance(r[1], bytes) and len(r[1]) == 128 for r in res), res
+    assert res[0][1] == res[1][1]
+    assert all(r[2] for r in res)

@@ -10,6 +10,7 @@ import pytest
 
 import oracle
 import synth
+from helpers import assert_close
 
 pytestmark = pytest.mark.gpu
 
@@ -50,9 +51,9 @@ def test_batch_2d_bitwise_and_parity(name, p, nrhs):
     assert np.array_equal(U.view(np.uint64), S.view(np.uint64))
     assert np.array_equal(U.view(np.uint64), U2.view(np.uint64))
     for r in (0, nrhs - 1):
-        assert oracle.rel_l2(U[r], oracle.butterfly(w.x, w.k, F[r], w.N, p)) <= PARITY
+        assert_close(U[r], oracle.butterfly(w.x, w.k, F[r], w.N, p), PARITY)
     if name == "C0":
-        assert oracle.rel_l2(U[1], oracle.direct(w.x, w.k, F[1], w.N)) <= DIRECT_TOL[p]
+        assert_close(U[1], oracle.direct(w.x, w.k, F[1], w.N), DIRECT_TOL[p])
 
 
 @pytest.mark.parametrize("N,p", [(16, 5), (16, 9), (32, 7)])
@@ -61,7 +62,7 @@ def test_batch_3d(N, p):
     F = _charges(3, len(w.k), 200)
     U, S, _ = _run(w.x, w.k, F, w.N, p)
     assert np.array_equal(U.view(np.uint64), S.view(np.uint64))
-    assert oracle.rel_l2(U[2], oracle.butterfly(w.x, w.k, F[2], w.N, p)) <= PARITY
+    assert_close(U[2], oracle.butterfly(w.x, w.k, F[2], w.N, p), PARITY)
 
 
 def test_batch_host_pointers_and_linearity():
@@ -73,7 +74,7 @@ def test_batch_host_pointers_and_linearity():
     F = np.stack([f, g, f + 2 * g])
     U, S, _ = _run(w.x, w.k, F, w.N, w.p, host=True)
     assert np.array_equal(U.view(np.uint64), S.view(np.uint64))
-    assert oracle.rel_l2(U[2], U[0] + 2 * U[1]) <= 1e-13
+    assert_close(U[2], U[0] + 2 * U[1], 1e-13)
 
 
 def test_batch_dense_leaves():
@@ -87,7 +88,7 @@ def test_batch_dense_leaves():
     F = _charges(3, len(k), 300)
     U, S, _ = _run(x, k, F, N, 9)
     assert np.array_equal(U.view(np.uint64), S.view(np.uint64))
-    assert oracle.rel_l2(U[1], oracle.butterfly(x, k, F[1], N, 9)) <= PARITY
+    assert_close(U[1], oracle.butterfly(x, k, F[1], N, 9), PARITY)
 
 
 def test_batch_fp32_and_adjoint():
@@ -95,13 +96,13 @@ def test_batch_fp32_and_adjoint():
     F = _charges(3, len(w.k), 400)
     U, S, _ = _run(w.x, w.k, F, w.N, 9, precision=1)
     assert np.array_equal(U.view(np.uint64), S.view(np.uint64))
-    assert oracle.rel_l2(U[0], oracle.butterfly(w.x, w.k, F[0], w.N, 9)) <= 2e-5
+    assert_close(U[0], oracle.butterfly(w.x, w.k, F[0], w.N, 9), 2e-5)
     G = _charges(2, len(w.x), 500)
     V, S, _ = _run(w.x, w.k, G, w.N, 9, adjoint=True)
     assert V.shape == (2, len(w.k))
     assert np.array_equal(V.view(np.uint64), S.view(np.uint64))
     vb = np.conj(oracle.butterfly(w.k, w.x, np.conj(G[1]), w.N, 9))
-    assert oracle.rel_l2(V[1], vb) <= PARITY
+    assert_close(V[1], vb, PARITY)
 
 
 def test_batch_errors():

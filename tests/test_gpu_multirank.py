@@ -9,6 +9,7 @@ import pytest
 
 import oracle
 import synth
+from helpers import assert_close
 
 pytestmark = pytest.mark.gpu
 
@@ -97,11 +98,43 @@ def test_multirank_forced_levels(force):
 
 
 def test_multirank_C2_vs_oracle():
+    """C2 at full size sharded over 4 emulated ranks: bitwise equal to the
+    single-GPU result on every target, and within parity of the oracle
+    butterfly on every 4th of the 1024 seeded targets (spread over the whole
+    circle, so every rank's T_X range is covered)."""
     w = synth.make_workload("C2")
     uw, part = emulate(w, 4)
-    tg = w.sample[:256]
+    u1 = single(w)
+    assert np.array_equal(uw.view(np.uint64), u1.view(np.uint64)), f"partition {part[:3]}"
+    tg = w.sample[::4]
     ub = oracle.butterfly(w.x, w.k, w.f, w.N, w.p, targets=tg)
-    assert oracle.rel_l2(uw[tg], ub) <= 1e-10
+    assert_close(uw[tg], ub, 1e-10)
+
+
+@pytest.mark.parametrize("name,force", [("C1", (1, 1, 5)), ("C1", (0, 0, 10)), ("C1", (0, 0, 0)), ("C3s", (1, 1, 2))])
+def test_nccl_sharded_one_rank(name, force):
+    """The in-library NCCL path (opts.nccl_id) on one GPU: world = 1 with an
+    explicit exchange level runs phase 1, the grouped ncclSend/ncclRecv (to
+    itself), phase 2 into the all-gather layout, ncclAllGather and the scatter
+    to user order inside sft_apply -- bitwise equal to the plain apply."""
+    import torch
+    import paper_0801_1524_b200 as sft
+    w = synth.make_workload("C3", N=32, p=5) if name == "C3s" else synth.make_workload(name)
+    L = w.N.bit_length() - 1
+    force = tuple(L if v == 10 else v for v in force)
+    nid = sft.nccl_unique_id()
+    x = torch.from_numpy(w.x).cuda(); k = torch.from_numpy(w.k).cuda(); f = torch.from_numpy(w.f).cuda()
+    try:
+        with sft.Plan(w.dim, w.N, w.p, x, k, rank=0, world=1, split_k=force[0], split_x=force[1],
+                      exchange_level=force[2], nccl_id=nid) as pl:
+            assert tuple(pl.partition()[:3]) == force
+            u = pl.apply(f).cpu().numpy()
+            uh = pl.apply(w.f)  # host in / host out through the same path
+    finally:
+        sft.nccl_release(nid)
+    u1 = single(w)
+    assert np.array_equal(u.view(np.uint64), u1.view(np.uint64))
+    assert np.array_equal(uh.view(np.uint64), u1.view(np.uint64))
 
 
 def emulate_fused(w, world, force=(-1, -1, -1)):

@@ -9,6 +9,7 @@ import pytest
 
 import oracle
 import synth
+from helpers import assert_close
 
 pytestmark = pytest.mark.gpu
 
@@ -44,13 +45,13 @@ def test_parity_2d_small(name, p):
     w = synth.make_workload(name, p=p)
     u, st = gpu_transform(w.x, w.k, w.f, w.N, p)
     ub = oracle.butterfly(w.x, w.k, w.f, w.N, p)
-    assert oracle.rel_l2(u, ub) <= PARITY
+    assert_close(u, ub, PARITY)
     # trees: per-level counts equal the oracle's
     assert list(st["counts_x"]) == list(oracle.tree_counts(w.x, w.N))
     assert list(st["counts_k"]) == list(oracle.tree_counts(w.k, w.N))
     if name == "C0":
         ud = oracle.direct(w.x, w.k, w.f, w.N)
-        assert oracle.rel_l2(u, ud) <= DIRECT_TOL[p]
+        assert_close(u, ud, DIRECT_TOL[p])
 
 
 @pytest.mark.parametrize("N,p", [(16, 5), (16, 7), (16, 9), (32, 7)])
@@ -58,17 +59,17 @@ def test_parity_3d_small(N, p):
     w = synth.make_workload("C3", N=N, p=p)
     u, st = gpu_transform(w.x, w.k, w.f, w.N, p)
     ub = oracle.butterfly(w.x, w.k, w.f, w.N, p)
-    assert oracle.rel_l2(u, ub) <= PARITY
+    assert_close(u, ub, PARITY)
     ud = oracle.direct(w.x, w.k, w.f, w.N, targets=w.sample[:512] if len(w.x) > 512 else None)
     uu = u[w.sample[:512]] if len(w.x) > 512 else u
-    assert oracle.rel_l2(uu, ud) <= DIRECT_TOL[p]
+    assert_close(uu, ud, DIRECT_TOL[p])
 
 
 def test_parity_C1_direct_all_targets():
     w = synth.make_workload("C1")
     u, _ = gpu_transform(w.x, w.k, w.f, w.N, w.p)
     ud = oracle.direct(w.x, w.k, w.f, w.N)
-    assert oracle.rel_l2(u, ud) <= DIRECT_TOL[w.p]
+    assert_close(u, ud, DIRECT_TOL[w.p])
 
 
 def test_parity_C2_full():
@@ -77,25 +78,55 @@ def test_parity_C2_full():
     w = synth.make_workload("C2")
     u, _ = gpu_transform(w.x, w.k, w.f, w.N, w.p)
     ub = oracle.butterfly(w.x, w.k, w.f, w.N, w.p)
-    assert oracle.rel_l2(u, ub) <= PARITY
+    assert_close(u, ub, PARITY)
     ud = oracle.direct(w.x, w.k, w.f, w.N, targets=w.sample)
-    assert oracle.rel_l2(u[w.sample], ud) <= DIRECT_TOL[w.p]
+    assert_close(u[w.sample], ud, DIRECT_TOL[w.p])
 
 
+def spread_targets(n, m, seed):
+    """m targets drawn uniformly from all n (sorted): spread over the whole
+    curve / surface, not a prefix of the sampling order."""
+    return np.sort(np.random.default_rng(seed).choice(n, m, replace=False)).astype(np.int64)
+
+
+@pytest.mark.slow
 def test_parity_C3_full():
+    """C3 at full size (BASELINE.json:10): the direct sum on ALL 131,898
+    targets (the config's error set, DESIGN R12; 1.17e10 long-double terms)
+    and the oracle butterfly on 2048 targets spread over the whole sphere."""
     w = synth.make_workload("C3")
     u, _ = gpu_transform(w.x, w.k, w.f, w.N, w.p)
-    ub = oracle.butterfly(w.x, w.k, w.f, w.N, w.p, targets=w.sample[:2048] if len(w.sample) > 2048 else w.sample)
-    tg = w.sample[:2048] if len(w.sample) > 2048 else w.sample
-    assert oracle.rel_l2(u[tg], ub) <= PARITY
-    ud = oracle.direct(w.x, w.k, w.f, w.N, targets=synth.error_sample(len(w.x), w.seed))
-    assert oracle.rel_l2(u[synth.error_sample(len(w.x), w.seed)], ud) <= DIRECT_TOL[w.p]
+    assert len(w.sample) == len(w.x)  # all targets
+    ud = oracle.direct(w.x, w.k, w.f, w.N)
+    e_d = assert_close(u, ud, DIRECT_TOL[w.p], "C3 vs direct (all targets)")
+    tg = spread_targets(len(w.x), 2048, 33)
+    ub = oracle.butterfly(w.x, w.k, w.f, w.N, w.p, targets=tg)
+    e_b = assert_close(u[tg], ub, PARITY, "C3 vs oracle butterfly (2048 spread targets)")
+    print(f"C3 direct rel_l2/max {e_d[0]:.3e}/{e_d[1]:.3e}; butterfly {e_b[0]:.3e}/{e_b[1]:.3e}")
 
 
-def test_parity_C4_sampled():
-    """C4 at full size in the bench launch configuration: the oracle evaluates
-    256 seeded targets with the charges of one T_K subtree active (all other
-    f_j = 0 on both sides), which skips only zero or unused pairs."""
+@pytest.mark.slow
+def test_parity_C4_full():
+    """C4 at full size with ALL sources active, in the bench launch
+    configuration (BASELINE.json:11): the direct sum on the 1024 seeded targets
+    (the config's error set) and the oracle butterfly on every 4th of them (256
+    targets spread over the whole sphere; the oracle's target restriction skips
+    only pairs that never reach them)."""
+    w = synth.make_workload("C4")
+    u, _ = gpu_transform(w.x, w.k, w.f, w.N, w.p)
+    ud = oracle.direct(w.x, w.k, w.f, w.N, targets=w.sample)
+    e_d = assert_close(u[w.sample], ud, DIRECT_TOL[w.p], "C4 vs direct (1024 seeded targets)")
+    tg = w.sample[::4]
+    ub = oracle.butterfly(w.x, w.k, w.f, w.N, w.p, targets=tg)
+    e_b = assert_close(u[tg], ub, PARITY, "C4 vs oracle butterfly (256 spread targets)")
+    print(f"C4 direct rel_l2/max {e_d[0]:.3e}/{e_d[1]:.3e}; butterfly {e_b[0]:.3e}/{e_b[1]:.3e}")
+
+
+def test_parity_C4_one_subtree():
+    """C4 geometry with the charges of one level-3 T_K subtree active (all
+    other f_j = 0 on both sides): the GPU result against the oracle
+    butterfly on every 4th of the 1024 seeded targets (the oracle's source
+    restriction skips only zero pairs)."""
     w = synth.make_workload("C4")
     leaf = np.minimum(np.floor(w.k).astype(np.int64), w.N - 1)
     sub = leaf >> 6  # level-3 subtree of T_K
@@ -104,11 +135,9 @@ def test_parity_C4_sampled():
     act = key == vals[np.argmax(cnt)]
     f = np.where(act, w.f, 0)
     u, _ = gpu_transform(w.x, w.k, f, w.N, w.p)
-    tg = w.sample[:256]
+    tg = w.sample[1::4]
     ub = oracle.butterfly(w.x, w.k, w.f, w.N, w.p, targets=tg, src_active=act.astype(np.uint8))
-    assert oracle.rel_l2(u[tg], ub) <= PARITY
-    ud = oracle.direct(w.x, w.k[act], f[act], w.N, targets=tg)
-    assert oracle.rel_l2(u[tg], ud) <= DIRECT_TOL[w.p]
+    assert_close(u[tg], ub, PARITY)
 
 
 # ------------------------------------------------------------------ edge cases
@@ -130,7 +159,7 @@ def test_domain_boundaries_and_one_leaf():
     f = rng.normal(size=9) + 1j * rng.normal(size=9)
     u, _ = gpu_transform(x, k, f, N, 7)
     ub = oracle.butterfly(x, k, f, N, 7)
-    assert oracle.rel_l2(u, ub) <= PARITY
+    assert_close(u, ub, PARITY)
 
 
 def test_zero_linear_deterministic_host_device():
@@ -198,10 +227,10 @@ def test_fp32_parity_2d(name, p):
     with sft.Plan(2, w.N, p, x, k, precision=1) as plan:
         u = plan.apply(f).cpu().numpy()
     ub = oracle.butterfly(w.x, w.k, w.f, w.N, p)
-    assert oracle.rel_l2(u, ub) <= FP32_PARITY
+    assert_close(u, ub, FP32_PARITY)
     if name == "C0":
         ud = oracle.direct(w.x, w.k, w.f, w.N)
-        assert oracle.rel_l2(u, ud) <= DIRECT_TOL[p]
+        assert_close(u, ud, DIRECT_TOL[p])
 
 
 @pytest.mark.parametrize("N,p", [(16, 5), (16, 7), (16, 9)])
@@ -213,7 +242,7 @@ def test_fp32_parity_3d(N, p):
     with sft.Plan(3, w.N, p, x, k, precision=1) as plan:
         u = plan.apply(f).cpu().numpy()
     ub = oracle.butterfly(w.x, w.k, w.f, w.N, p)
-    assert oracle.rel_l2(u, ub) <= FP32_PARITY
+    assert_close(u, ub, FP32_PARITY)
 
 
 def test_fp32_c2_sampled_vs_direct():
@@ -226,7 +255,7 @@ def test_fp32_c2_sampled_vs_direct():
         u = plan.apply(f).cpu().numpy()
     tg = w.sample[:1024]
     ud = oracle.direct(w.x[tg], w.k, w.f, w.N)
-    assert oracle.rel_l2(u[tg], ud) <= DIRECT_TOL[9]
+    assert_close(u[tg], ud, DIRECT_TOL[9])
 
 
 def test_dense_leaves_chunked_paths():
@@ -243,7 +272,7 @@ def test_dense_leaves_chunked_paths():
     for p in (5, 9):
         u, _ = gpu_transform(x, k, f, N, p)
         ub = oracle.butterfly(x, k, f, N, p)
-        assert oracle.rel_l2(u, ub) <= PARITY
+        assert_close(u, ub, PARITY)
 
 
 def test_dense_leaves_3d():
@@ -254,7 +283,7 @@ def test_dense_leaves_3d():
     f = rng.normal(size=len(k)) + 1j * rng.normal(size=len(k))
     u, _ = gpu_transform(x, k, f, N, 7)
     ub = oracle.butterfly(x, k, f, N, 7)
-    assert oracle.rel_l2(u, ub) <= PARITY
+    assert_close(u, ub, PARITY)
 
 
 def test_schedule_invariants_checker():
@@ -294,9 +323,9 @@ def test_adjoint(p):
         v = plan.apply(torch.from_numpy(g).cuda()).cpu().numpy()
     assert v.shape == (len(w.k),)
     vb = np.conj(oracle.butterfly(w.k, w.x, np.conj(g), w.N, p))
-    assert oracle.rel_l2(v, vb) <= PARITY
+    assert_close(v, vb, PARITY)
     vd = np.conj(oracle.direct(w.k, w.x, np.conj(g), w.N))
-    assert oracle.rel_l2(v, vd) <= DIRECT_TOL[p]
+    assert_close(v, vd, DIRECT_TOL[p])
     # <A f, g> = <f, A^H g>
     f = w.f
     with sft.Plan(2, w.N, p, torch.from_numpy(w.x).cuda(), torch.from_numpy(w.k).cuda()) as plan:
@@ -329,7 +358,7 @@ def test_sort_graph_cache_reuse_and_sizes():
         u, _ = gpu_transform(x, k, fi, N, p)
         assert np.array_equal(u.view(np.uint64), u0.view(np.uint64))
     x, k = cases[2]
-    assert oracle.rel_l2(first[2], oracle.butterfly(x, k, f[2], N, p)) <= PARITY
+    assert_close(first[2], oracle.butterfly(x, k, f[2], N, p), PARITY)
 
 
 def test_two_level_launches_all_pairs():
@@ -363,7 +392,7 @@ def test_two_level_launches_all_pairs():
     assert "(0, False)" in res["all"][1].splitlines()[-1]
     w = synth.make_workload("C1", N=512, p=9)
     u = res["all"][0][-2 * len(w.x):].view(np.complex128)
-    assert oracle.rel_l2(u, oracle.butterfly(w.x, w.k, w.f, w.N, 9)) <= PARITY
+    assert_close(u, oracle.butterfly(w.x, w.k, w.f, w.N, 9), PARITY)
 
 
 @pytest.mark.parametrize("d,N,n,p", [(2, 64, 3000, 5), (2, 64, 3000, 7), (2, 64, 3000, 9), (2, 256, 20000, 9),
@@ -378,7 +407,7 @@ def test_uniform_random_full_groups(d, N, n, p):
     f = rng.normal(size=len(k)) + 1j * rng.normal(size=len(k))
     u, st = gpu_transform(x, k, f, N, p)
     ub = oracle.butterfly(x, k, f, N, p)
-    assert oracle.rel_l2(u, ub) <= PARITY
+    assert_close(u, ub, PARITY)
     assert list(st["counts_x"]) == list(oracle.tree_counts(x, N))
 
 
@@ -400,6 +429,65 @@ def test_extreme_sizes(d, N, n, p):
     f = rng.normal(size=len(k)) + 1j * rng.normal(size=len(k))
     u, st = gpu_transform(x, k, f, N, p)
     ub = oracle.butterfly(x, k, f, N, p)
-    assert oracle.rel_l2(u, ub) <= PARITY
+    assert_close(u, ub, PARITY)
     assert list(st["counts_x"]) == list(oracle.tree_counts(x, N))
     assert list(st["counts_k"]) == list(oracle.tree_counts(k, N))
+
+
+def test_sort_graph_cache_swapped_sets():
+    """The cached sort graph sorts [0, nx) and [nx, n) as two branches, so two
+    plans with the same n but a different nx -- (x, k) then (k, x), e.g. a
+    forward plan then its adjoint -- must not share it: the third plan below
+    (same sets and sizes as the first, after a plan with the sizes swapped)
+    gives the bits of the first, and the adjoint equals the swapped forward."""
+    torch = _torch()
+    import paper_0801_1524_b200 as sft
+    w = synth.make_workload("C1", N=4096, p=5)  # nx, nk > 16K: the device-sort graph path
+    assert len(w.x) > 16384 and len(w.k) > 16384 and len(w.x) != len(w.k)
+    x = torch.from_numpy(w.x).cuda(); k = torch.from_numpy(w.k).cuda()
+    g = torch.from_numpy(synth.random_charges(len(w.x), 3)).cuda()
+    f = torch.from_numpy(w.f).cuda()
+
+    def fwd(a, b, c):
+        with sft.Plan(2, w.N, 5, a, b) as pl:
+            return pl.apply(c).cpu().numpy()
+
+    u1 = fwd(x, k, f)
+    v1 = fwd(k, x, g)
+    u2 = fwd(x, k, f)
+    v2 = fwd(k, x, g)
+    assert np.array_equal(u1.view(np.uint64), u2.view(np.uint64))
+    assert np.array_equal(v1.view(np.uint64), v2.view(np.uint64))
+    with sft.Plan(2, w.N, 5, x, k, adjoint=True) as pl:  # adjoint right after a forward plan
+        va = pl.apply(torch.conj(g).resolve_conj()).cpu().numpy()
+    assert np.array_equal(np.conj(va).view(np.uint64), v1.view(np.uint64))
+
+
+def test_level_buffer_guard():
+    """Levels whose pair arrays exceed the schedules' 32-bit element offsets
+    (3D N = 256 p = 9 on uniformly filled boxes: ~4096^2 pairs x 729 at level
+    4) are rejected by sft_plan with SFT_E_ARG instead of wrapping."""
+    torch = _torch()
+    import paper_0801_1524_b200 as sft
+    rng = np.random.default_rng(5)
+    x = torch.from_numpy(rng.uniform(0, 256, (60000, 3))).cuda()
+    with pytest.raises(sft.SftError, match="2\\^32"):
+        sft.Plan(3, 256, 9, x, x)
+
+
+def test_host_charges_reusable_after_return():
+    """sft.h: a host f may be modified as soon as sft_apply returns (the call
+    waits for its staging copy), also when u is on the device."""
+    torch = _torch()
+    import paper_0801_1524_b200 as sft
+    w = synth.make_workload("C1")
+    x = torch.from_numpy(w.x).cuda(); k = torch.from_numpy(w.k).cuda()
+    fp = torch.from_numpy(w.f).pin_memory()
+    with sft.Plan(2, w.N, w.p, x, k) as pl:
+        ref = pl.apply(torch.from_numpy(w.f).cuda()).cpu().numpy()
+        u = torch.empty(len(w.x), dtype=torch.complex128, device="cuda")
+        pl.apply(fp, u)
+        fp.fill_(0)  # immediately after return
+        assert np.array_equal(u.cpu().numpy(), ref)
+        with pytest.raises(ValueError):
+            pl.apply(w.f, torch.empty(2 * len(w.x), dtype=torch.complex128, device="cuda")[::2])
