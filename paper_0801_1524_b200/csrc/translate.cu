@@ -31,6 +31,7 @@
 // No floating-point atomics: bitwise reproducible, identical for any world
 // size.
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -142,41 +143,42 @@ __device__ __forceinline__ int64_t out_pair(const LevelArgs& a, const GroupMeta&
 // (s (p-1) = (beta (p-1) + l')/2 is an integer) and the Lagrange basis is a
 // delta there: column l' of RC_beta / RS_beta is zero except at row
 // m = (beta (p-1) + l')/2.  Only the H = (p-1)/2 odd columns per child are
-// dense.  The tensor cores take K = 2H stacked odd elements (k = beta H + i,
-// l' = 2i + 1); the even (delta) columns are added to the accumulators up
-// front with two scalar coefficients per output (DFMA).  p = 9: 2 k-steps
-// instead of 5 (K 20 -> 8).
+// dense.
+//
+// Mirror symmetry: the child-1 grid is the mirror image of the child-0 grid
+// about the parent's centre (node l' of child 1 sits at 1 - node (p-1-l') of
+// child 0, parent node m at 1 - node p-1-m), and the Lagrange basis on the
+// nodes z_m = e^{2 pi i m/(p-1)^2} maps to its conjugate under the mirror, so
+//   RC_1 = J RS_0 J,  RS_1 = J RC_0 J         (J = index reversal)
+// (checked on the host tables to the last bit; tests/test_library_host.py).
+// With y = J x_1, s = x_0 + y, t = x_0 - y and m' = p-1-m, the pass
+//   P = RC_0 x_0 + RS_1 x_1,  Q = RS_0 x_0 - RC_1 x_1
+// becomes, for m < H,
+//   P_m = SP_m + DP_m,  P_m' = SP_m - DP_m,  Q_m = SQ_m + DQ_m,  Q_m' = SQ_m - DQ_m,
+//   SP_m = 1/2 (RC_0[m] + RC_0[m']) . s,   DP_m = 1/2 (RC_0[m] - RC_0[m']) . t,
+//   SQ_m = 1/2 (RS_0[m] + RS_0[m']) . t,   DQ_m = 1/2 (RS_0[m] - RS_0[m']) . s,
+// and at the centre P_H = RC_0[H] . s, Q_H = RS_0[H] . t: half the MACs of
+// the direct form.  On the tensor cores (DMMA m8n8k4, row = fiber, real and
+// imaginary parts of 8 fibers as two A tiles sharing the B fragments) the odd
+// elements of s and of t are one k-step each (K = H <= 4); the s-GEMM's
+// columns are (SP_m, DQ_m) interleaved and the t-GEMM's (DP_m, SQ_m), so lane
+// c of a row holds m = c and forms z_0 = P - iQ, z_1 = P + iQ for m and m'
+// locally.  The centre sits in the same N tile for p = 5, 7 (lane c = H:
+// columns (SP_H, 0) and (0, SQ_H), so the m and m' formulas coincide) and for
+// p = 9 is a DFMA tail (4-lane transpose-reduce).  The even (delta) elements
+// start the accumulators: lane c takes s and t at element 2c.
 template <int P>
-struct MmaShape {
-  static constexpr int H = (P - 1) / 2;           // dense (odd) columns per child
-  // each child's odd elements padded to HP k-slots (p = 7: 3 -> 4), so a child
-  // never straddles a k-step: rows with one live child skip whole k-steps, and
-  // the padding lanes re-read element 1 (a broadcast, no bank conflict)
-  static constexpr int HP = H <= 2 ? 2 : 4;
-  static constexpr int K = 2 * HP;                // stacked (padded) odd child elements
-  static constexpr int NK = (K + 3) / 4;          // k-steps of 4
-  // m = P-1: p = 5 by DFMA with a 4-lane transpose-reduce; p = 9 in a third N
-  // tile on the tensor cores (+50% DMMA on an otherwise idle pipe, ~25 fewer
-  // instructions per super-tile: C2 translate 1.215 -> 1.173 ms; for 3D p = 5
-  // the DFMA tail is faster, 0.895 vs 0.916 ms).  SFT_TAIL_DMMA=0/1 forces.
-#if defined(SFT_TAIL_DMMA)
-  static constexpr bool TAIL = SFT_TAIL_DMMA ? false : (P % 4) == 1;
-#else
-  static constexpr bool TAIL = (P % 4) == 1 && P != 9;
-#endif
-  static constexpr int NM = TAIL ? P - 1 : P;     // m's on the tensor cores
-  static constexpr int NT = (2 * NM + 7) / 8;     // N tiles of 8 (P_m, Q_m interleaved)
-  static constexpr int K0_HI = (HP + 3) / 4;      // k-steps [0, K0_HI) hold child-0 elements
-  static constexpr int K1_LO = HP / 4;            // k-steps [K1_LO, NK) hold child-1 elements
-  // fragment table: B fragments, tail weights, then the delta coefficients
-  // (a0, b0, a1, b1) of m = 4n + lane%4 per N tile and (a1, b1) of the tail
-  static constexpr int OFF_TAIL = NK * NT * 32;
-  static constexpr int OFF_DELTA = OFF_TAIL + (TAIL ? NK * 2 * 32 : 0);
-  static constexpr int OFF_DTAIL = OFF_DELTA + NT * 4 * 32;
-  static constexpr int NFRAG = OFF_DTAIL + (TAIL ? 2 * 32 : 0);
+struct SymShape {
+  static constexpr int H = (P - 1) / 2;   // odd (dense) elements per child = k of the MMA (padded to 4)
+  static constexpr bool TAIL = H >= 4;    // centre column outside the 8-column tile (p = 9)
+  static_assert(H <= 4, "p <= 9");
+  // fragment table (doubles, 32 lanes each): B_s, B_t, delta (s-acc col 0/1, t-acc col 0/1),
+  // tail (s coefficient, t coefficient, s delta, t delta; p = 9)
+  static constexpr int OFF_BS = 0, OFF_BT = 32, OFF_DS = 64, OFF_DT = 128, OFF_TAIL = 192;
+  static constexpr int NFRAG = OFF_TAIL + (TAIL ? 4 * 32 : 0);
 };
 #ifdef SFT_NO_ZEROFILL
-#error "the delta columns read absent children's slots: SFT_NO_ZEROFILL is not supported"
+#error "the consumers read absent children's slots: SFT_NO_ZEROFILL is not supported"
 #endif
 
 // complex element of the level buffers / stages: double2 (FP64) or float2
@@ -208,91 +210,33 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
       : "d"(a), "d"(b));
 }
 
-// measured: C2 translate 1.546 -> 1.457 ms with the table in shared memory,
-// C3 1.026 -> 1.044 ms: 2D only (SFT_TAIL_SMEM overrides)
-#ifndef SFT_TAIL_SMEM
-#define SFT_TAIL_SMEM 2
-#endif
-template <int D>
-struct TailSmem {
-  static constexpr bool v = SFT_TAIL_SMEM == 2 ? D == 2 : SFT_TAIL_SMEM == 1;
-};
-// tail column weights (m = P-1) per (k-step, lane%4) -- (P weight, Q weight);
-// in shared memory (SFT_TAIL_SMEM) they cost one broadcast load per k-step
-// instead of 2*NK registers per thread
-__shared__ double2 s_tail[8][4];
-template <int P, bool TS>
+// Per-lane operator registers of the symmetric pass (lane c = lane % 4)
+template <int P>
 struct LaneOps {
-  using S = MmaShape<P>;
-  double fb[S::NK][S::NT];           // B fragments of the operator (odd columns)
-  double ft[TS ? 1 : S::NK][2];      // tail column (m = P-1): P and Q weights of this lane's k
-  double dl[S::NT][4];               // delta columns of m = 4n + lane%4: (a0, b0, a1, b1)
-  __device__ __forceinline__ double4 delta(int n, int) const {
-    return make_double4(dl[n][0], dl[n][1], dl[n][2], dl[n][3]);
-  }
-  double dt[S::TAIL ? 2 : 1];        // delta column of the tail (lane%4 == 0 only, else 0)
-  // child (0, 1; 2 = padding) and element index of this lane's k in k-step kk
-  __device__ __forceinline__ static int bk(int kk, int lane) {
-    const int k = 4 * kk + (lane & 3);
-    return k < S::K ? k / S::HP : 2;
-  }
-  __device__ __forceinline__ static int lk(int kk, int lane) {
-    const int k = 4 * kk + (lane & 3);
-    return k < S::K && k % S::HP < S::H ? 2 * (k % S::HP) + 1 : 1;  // padding: element 1 (zero B row)
-  }
-  __device__ __forceinline__ double2 tail(int kk, int lane) const {
-    if constexpr (TS) return s_tail[kk][lane & 3];
-    else return make_double2(ft[kk][0], ft[kk][1]);
-  }
+  using S = SymShape<P>;
+  double bs, bt;            // B fragments: s- and t-GEMM, k = c, column lane / 4
+  double ds0, ds1, dt0, dt1;  // delta coefficients of this lane's accumulator columns (even element 2c)
+  double ts, tt, tds, tdt;    // p = 9 centre: odd coefficients of this lane's k, centre deltas (lane 0)
 };
 
-// k-steps [K_LO, K_HI) of one MMA super-tile: A fragments (re and im of one
-// complex element per lane, one 16-byte shared-memory load) times the B
-// fragments held in registers; tail column m = P-1 on DFMA.
-template <int P, int K_LO, int K_HI, int NSUB, typename E, class OPS>
-__device__ __forceinline__ void mma_steps(const OPS& op, const E* const (&x)[NSUB],
-                                          const int (&off)[MmaShape<P>::NK], const bool (&p0)[NSUB],
-                                          const bool (&p1)[NSUB], double (&are)[NSUB][MmaShape<P>::NT][2],
-                                          double (&aim)[NSUB][MmaShape<P>::NT][2], double (&tl)[NSUB][4]) {
-  using S = MmaShape<P>;
-#pragma unroll
-  for (int kk = K_LO; kk < K_HI; ++kk) {
-    double2 av[NSUB];
-#pragma unroll
-    for (int u = 0; u < NSUB; ++u) {
-      // absent children's slots are zero-filled by the producer and the B
-      // rows of padding k are zero: no masking needed
-      av[u] = ElemT<E>::ld(x[u][off[kk]]);
-    }
-    // the accumulators start from the delta columns (consumer_pass)
-#pragma unroll
-    for (int n = 0; n < S::NT; ++n)
-#pragma unroll
-      for (int u = 0; u < NSUB; ++u) {
-        dmma(are[u][n], av[u].x, op.fb[kk][n]);
-        dmma(aim[u][n], av[u].y, op.fb[kk][n]);
-      }
-    if (S::TAIL) {
-      const double2 ft = op.tail(kk, threadIdx.x);
-#pragma unroll
-      for (int u = 0; u < NSUB; ++u) {
-        tl[u][0] = fma(av[u].x, ft.x, tl[u][0]);
-        tl[u][1] = fma(av[u].x, ft.y, tl[u][1]);
-        tl[u][2] = fma(av[u].y, ft.x, tl[u][2]);
-        tl[u][3] = fma(av[u].y, ft.y, tl[u][3]);
-      }
-    }
+template <int P>
+__device__ __forceinline__ void load_lane_ops(LaneOps<P>& op, const double* __restrict__ frag, int lane) {
+  using S = SymShape<P>;
+  op.bs = frag[S::OFF_BS + lane];
+  op.bt = frag[S::OFF_BT + lane];
+  op.ds0 = frag[S::OFF_DS + lane];
+  op.ds1 = frag[S::OFF_DS + 32 + lane];
+  op.dt0 = frag[S::OFF_DT + lane];
+  op.dt1 = frag[S::OFF_DT + 32 + lane];
+  if constexpr (S::TAIL) {
+    op.ts = frag[S::OFF_TAIL + lane];
+    op.tt = frag[S::OFF_TAIL + 32 + lane];
+    op.tds = frag[S::OFF_TAIL + 64 + lane];
+    op.tdt = frag[S::OFF_TAIL + 96 + lane];
+  } else {
+    op.ts = op.tt = op.tds = op.tdt = 0.0;
   }
 }
-
-// One axis pass of the DMMA kernel.  A warp takes super-tiles of 8 fiber
-// tasks: MMA row r (= lane/4) is one fiber, the real parts form one m8n8k4 A
-// tile and the imaginary parts a second one with the same B fragments, so a
-// lane ends up holding re and im of (P_m, Q_m) for its fiber and m = 4n +
-// lane%4 and forms z_0 = P - iQ, z_1 = P + iQ locally.  Rows 2q, 2q+1 take
-// fibers q, q+4 of the super-tile (conflict-free 16-byte shared loads for
-// the unit and p-strided fibers of p = 9).  Outputs go back in place, or to
-// HBM in the last pass.
 
 // ------------------------------------------------------------------------
 // Tile schedule (built once per plan by k_schedule, read by the producer)
@@ -449,28 +393,18 @@ __device__ __forceinline__ void schedule_pass(const LevelArgs& a, const GroupMet
 }
 
 // 2D axis order per group (from its own masks only, so identical for any
-// partition of the work and for single- or two-level launches): the one with
-// fewer MMA k-steps over its fiber rows (rows of a task with one live child
-// skip that child's k-steps).  true = axis 0 first.
+// partition of the work and for single- or two-level launches): the order
+// with fewer fiber tasks over its two passes -- axis 1 first: one task per
+// present beta_0, then one per present alpha_1; axis 0 first: per present
+// beta_1, then per present alpha_0.  true = axis 0 first.
 template <int P>
 __device__ __forceinline__ bool reversed_order(const GroupMeta& m) {
 #ifdef SFT_FIXED_ORDER
   return false;
 #else
   constexpr int D = 2;
-  using S = MmaShape<P>;
-  constexpr int KB = S::NK, K0 = S::K0_HI, K1 = S::NK - S::K1_LO;
-  auto kc = [](uint32_t cls) { return cls == 3 ? KB : (cls == 1 ? K0 : (cls == 2 ? K1 : 0)); };
-  int cf = 0, cr = 0;  // default (axis 1 first) / reversed
-  const uint32_t mB = m.mB, mA = m.mA;
-  const uint32_t b0set = proj_hi<D>(mB, 1), b1set = proj_lo<D>(mB, 1);
-  const int na1 = __popc(proj_lo<D>(mA, 1)), na0 = __popc(proj_hi<D>(mA, 1));
-  for (int v = 0; v < 2; ++v) {
-    if (b0set >> v & 1) cf += kc((mB >> (2 * v)) & 3u);
-    if (b1set >> v & 1) cr += kc((mB >> v & 1u) | ((mB >> (2 + v) & 1u) << 1));
-  }
-  cf += na1 * kc(b0set);
-  cr += na0 * kc(b1set);
+  const int cf = __popc(proj_hi<D>(m.mB, 1)) + __popc(proj_lo<D>(m.mA, 1));
+  const int cr = __popc(proj_lo<D>(m.mB, 1)) + __popc(proj_hi<D>(m.mA, 1));
   return cr < cf;
 #endif
 }
@@ -675,57 +609,61 @@ struct NsubCfg {
   static constexpr int v = (D == 3 && P == 5) ? SFT_NSUB35 : SFT_NSUB_OTHER;
 };
 // Row -> fiber map of a super-tile: chosen per (d, p, axis) by
-// scripts/rfib_search.py, which minimises the modelled shared-memory
-// wavefronts (A fragments, delta columns, in-place stores) of the pass; the
-// default (rows 2q, 2q+1 <- fibers q, q+4) is optimal for 2D p = 9.
+// scripts/rfib_search_sym.py, which minimises the modelled shared-memory
+// wavefronts (A fragments, delta and centre loads, in-place stores) of the
+// symmetric pass; the default (rows 2q, 2q+1 <- fibers q, q+4) is optimal for
+// 2D p = 9, 3D p = 9 and two of the 3D p = 7 axes.
 template <int D, int P, int AX>
 struct RowMap {
   __device__ __forceinline__ static int fiber(int r) {
-    if constexpr (D == 2 && P == 5) return (0x43726150u >> (4 * r)) & 7;   // 0 5 1 6 2 7 3 4
-    else if constexpr (D == 2 && P == 7) return (0x63524170u >> (4 * r)) & 7;  // 0 7 1 4 2 5 3 6
-    else if constexpr (D == 3 && P == 5 && AX == 1) return (0x76432150u >> (4 * r)) & 7;  // 0 5 1 2 3 4 6 7
-    else if constexpr (D == 3 && P == 7 && AX == 1) return (0x74635210u >> (4 * r)) & 7;  // 0 1 2 5 3 6 4 7
-    else if constexpr (D == 3 && P == 7) return (0x63724150u >> (4 * r)) & 7;  // 0 5 1 4 2 7 3 6
+    if constexpr (D == 2 && P == 5) return (0x65437210u >> (4 * r)) & 7;                // 0 1 2 7 3 4 5 6
+    else if constexpr (D == 2 && P == 7) return (0x65432170u >> (4 * r)) & 7;           // 0 7 1 2 3 4 5 6
+    else if constexpr (D == 3 && P == 5 && AX == 0) return (0x63724150u >> (4 * r)) & 7;  // 0 5 1 4 2 7 3 6
+    else if constexpr (D == 3 && P == 5 && AX == 1) return (0x74326150u >> (4 * r)) & 7;  // 0 5 1 6 2 3 4 7
+    else if constexpr ((D == 3 && P == 5 && AX == 2) || (D == 3 && P == 7 && AX == 1)) return r;
     else return (r >> 1) + 4 * (r & 1);
   }
 };
 
+// One axis pass of the consumers (NC warps), symmetric form (see SymShape).
+// A warp takes super-tiles of 8 fiber tasks: MMA row r (= lane/4) is one
+// fiber; lane c = lane%4 loads its fiber's child-0 element 2c+1 and child-1
+// element p-2-2c (so s = x_0 + J x_1 and t = x_0 - J x_1 at odd element 2c+1
+// are one add each: the A fragments of k = c), and the even pair 2c / p-1-2c
+// for the delta columns; 4 DMMA (s and t, real and imaginary parts) give lane
+// c the m = c and m' = p-1-c outputs of both children.  Outputs go back in
+// place, or to HBM (or a peer's buffer) in the last pass.
 // MUL: stage-slot stride of consecutive child slots: 0 = G (slot-major
-// stage), 1 for the second level of a two-level tile (transposed slots)
+// stage), 1 for the second level of a two-level tile (transposed slots).
 template <int D, int P, int G, int NC, int AX, bool LAST, int LIST = AX, typename E = double2, bool FUSED = false,
           int MUL = 0>
 __device__ __forceinline__ void consumer_pass(const TransArgs& a, E* __restrict__ sb,
-                                              const unsigned char* __restrict__ blk,
-                                              const LaneOps<P, TailSmem<D>::v>& op,
+                                              const unsigned char* __restrict__ blk, const LaneOps<P>& op,
                                               int& rot, int64_t ooff = 0) {
-  using S = MmaShape<P>;
+  using S = SymShape<P>;
   using SC = Sched<D, P, G>;
+  using ET = ElemT<E>;
+  constexpr int H = S::H;
   constexpr int NSUB = NsubCfg<D, P>::v;
   constexpr int PF = Pow<P, D>::v / P;
   constexpr int PD = StrideT<E, Pow<P, D>::v>::v;  // slot stride (elements)
-  E* const gout = reinterpret_cast<E*>(a.out) + ooff;  // ooff: RHS offset of a batch
   constexpr int STR = Pow<P, D - 1 - AX>::v;
   constexpr int SH = D - 1 - AX;
+  constexpr int C1 = (1 << SH) * PD * (MUL == 0 ? G : MUL);  // child-1 slot of the pair
+  E* const gout = reinterpret_cast<E*>(a.out) + ooff;  // ooff: RHS offset of a batch
   const int* cnt = SC::cnt(blk) + 3 * LIST;
   const TaskRec* tasks = SC::task(blk, LIST);
   const int ntot = (cnt[0] + cnt[1] + cnt[2]) * PF;
-  const int nst = __shfl_sync(0xffffffffu, (ntot + 7) >> 3, 0);
-  const int lane = threadIdx.x & 31, warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
-  const int r = lane >> 2, c = lane & 3;
-  const int rfib = RowMap<D, P, AX>::fiber(r);  // row -> fiber of the super-tile (bank conflicts)
-  int off[S::NK];
-#pragma unroll
-  for (int kk = 0; kk < S::NK; ++kk)
-    off[kk] = (LaneOps<P, true>::bk(kk, lane) == 1 ? (1 << SH) * PD * (MUL == 0 ? G : MUL) : 0) + LaneOps<P, true>::lk(kk, lane) * STR;
-  // delta columns of this lane's outputs m = 4n + c: child-0 element 2m and
-  // child-1 element 2m - (P-1), clamped into range (their coefficient is 0 there)
-  int doff[S::NT][2];
-#pragma unroll
-  for (int n = 0; n < S::NT; ++n) {
-    const int m = 4 * n + c;
-    doff[n][0] = min(2 * m, P - 1) * STR;
-    doff[n][1] = (1 << SH) * PD * (MUL == 0 ? G : MUL) + min(max(2 * m - (P - 1), 0), P - 1) * STR;  // in range: 0 * finite = 0
-  }
+  const int nst = (ntot + 7) >> 3;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c = lane & 3;
+  const int rfib = RowMap<D, P, AX>::fiber(lane >> 2);  // row -> fiber of the super-tile (bank conflicts)
+  // this lane's element offsets in a fiber (padding k >= H: a valid odd element, zero B row;
+  // delta / outputs of lanes c > H (p = 5): clamped, coefficients 0, no stores)
+  const int o_a0 = min(2 * c + 1, P - 2) * STR, o_a1 = C1 + max(P - 2 - 2 * c, 1) * STR;
+  const int o_d0 = min(2 * c, P - 1) * STR, o_d1 = C1 + max(P - 1 - 2 * c, 0) * STR;
+  const int o_m = min(c, H) * STR, o_mp = max(P - 1 - c, H) * STR;
+  const bool st_m = c <= H, st_mp = c < H;
   // units of NSUB super-tiles go round-robin over the warps, continuing from
   // where the previous pass stopped (rot), so that the extra unit of a pass
   // whose count is not a multiple of NC does not always land on warp 0
@@ -736,8 +674,6 @@ __device__ __forceinline__ void consumer_pass(const TransArgs& a, E* __restrict_
     const E* x[NSUB];
     E* o0[NSUB];
     E* o1[NSUB];
-    bool p0[NSUB], p1[NSUB];
-    int any = 0;
 #pragma unroll
     for (int u = 0; u < NSUB; ++u) {
       const int tau = (st0 + u) * 8 + rfib;
@@ -753,9 +689,6 @@ __device__ __forceinline__ void consumer_pass(const TransArgs& a, E* __restrict_
         d.cls = 0;
         d.o0 = d.o1 = ~0u;
       }
-      p0[u] = d.cls & 1;
-      p1[u] = (d.cls >> 1) & 1;
-      any |= (int)d.cls;
       const uint32_t xo = d.x + (uint32_t)ebase;
       x[u] = sb + xo;
 #ifdef SFT_ABL_NOSTORE  // ablation: no output stores (shared or global)
@@ -777,72 +710,79 @@ __device__ __forceinline__ void consumer_pass(const TransArgs& a, E* __restrict_
         o1[u] = d.o1 != ~0u ? gout + d.o1 + ebase : nullptr;
       } else {
         o0[u] = vrow ? sb + xo : nullptr;
-        o1[u] = vrow ? sb + xo + (1 << SH) * PD * (MUL == 0 ? G : MUL) : nullptr;
+        o1[u] = vrow ? sb + xo + C1 : nullptr;
       }
 #endif
     }
-    // warp-uniform union of the live child classes: k-step range
-    const int cls = __shfl_sync(0xffffffffu, __reduce_or_sync(0xffffffffu, (unsigned)any), 0);
-    double are[NSUB][S::NT][2], aim[NSUB][S::NT][2], tl[NSUB][4];
+    // accumulators: s-GEMM columns (SP_m, DQ_m), t-GEMM columns (DP_m, SQ_m), re / im rows
+    double sre[NSUB][2], sim[NSUB][2], tre[NSUB][2], tim[NSUB][2], tl[NSUB][4];
+    double ar[NSUB][2], ai[NSUB][2];  // odd s / t of this lane's k (re, im)
 #pragma unroll
     for (int u = 0; u < NSUB; ++u) {
-      // accumulators start from the delta (even) columns of the operator
-#pragma unroll
-      for (int n = 0; n < S::NT; ++n) {
-        const double2 x0 = ElemT<E>::ld(x[u][doff[n][0]]), x1 = ElemT<E>::ld(x[u][doff[n][1]]);
-        const double4 dc = op.delta(n, lane);
-        are[u][n][0] = fma(dc.z, x1.x, dc.x * x0.x);
-        are[u][n][1] = fma(dc.w, x1.x, dc.y * x0.x);
-        aim[u][n][0] = fma(dc.z, x1.y, dc.x * x0.y);
-        aim[u][n][1] = fma(dc.w, x1.y, dc.y * x0.y);
-      }
-      if (S::TAIL) {  // m = P-1: child-1 element P-1 only (coefficients non-zero on lane%4 == 0)
-        const double2 x1 = ElemT<E>::ld(x[u][(1 << SH) * PD * (MUL == 0 ? G : MUL) + (P - 1) * STR]);
-        tl[u][0] = op.dt[0] * x1.x;
-        tl[u][1] = op.dt[S::TAIL ? 1 : 0] * x1.x;
-        tl[u][2] = op.dt[0] * x1.y;
-        tl[u][3] = op.dt[S::TAIL ? 1 : 0] * x1.y;
-      } else {
-        tl[u][0] = tl[u][1] = tl[u][2] = tl[u][3] = 0.0;
+      // absent children's slots are zero-filled by the producer: no masking
+      const double2 e0 = ET::ld(x[u][o_d0]), e1 = ET::ld(x[u][o_d1]);
+      const double2 a0 = ET::ld(x[u][o_a0]), a1 = ET::ld(x[u][o_a1]);
+      const double ser = e0.x + e1.x, sei = e0.y + e1.y, ter = e0.x - e1.x, tei = e0.y - e1.y;
+      sre[u][0] = op.ds0 * ser;
+      sre[u][1] = op.ds1 * ser;
+      sim[u][0] = op.ds0 * sei;
+      sim[u][1] = op.ds1 * sei;
+      tre[u][0] = op.dt0 * ter;
+      tre[u][1] = op.dt1 * ter;
+      tim[u][0] = op.dt0 * tei;
+      tim[u][1] = op.dt1 * tei;
+      ar[u][0] = a0.x + a1.x;  // s
+      ai[u][0] = a0.y + a1.y;
+      ar[u][1] = a0.x - a1.x;  // t
+      ai[u][1] = a0.y - a1.y;
+      if constexpr (S::TAIL) {
+        // centre m = H (p = 9): partials of z_0, z_1 over this lane's k, centre delta on lane 0
+        const double2 c0 = ET::ld(x[u][(P - 1) * STR]), c1 = ET::ld(x[u][C1]);
+        const double pr = fma(op.tds, c0.x + c1.x, op.ts * ar[u][0]), pi = fma(op.tds, c0.y + c1.y, op.ts * ai[u][0]);
+        const double qr = fma(op.tdt, c0.x - c1.x, op.tt * ar[u][1]), qi = fma(op.tdt, c0.y - c1.y, op.tt * ai[u][1]);
+        tl[u][0] = pr + qi;
+        tl[u][1] = pi - qr;
+        tl[u][2] = pr - qi;
+        tl[u][3] = pi + qr;
       }
     }
-#ifdef SFT_ABL_NOCOMPUTE  // ablation: no tensor-core work, everything else unchanged
-    if (false)
-#else
-    if (cls == 3)
+#ifndef SFT_ABL_NOCOMPUTE  // ablation: no tensor-core work
+#pragma unroll
+    for (int u = 0; u < NSUB; ++u) {
+      dmma(sre[u], ar[u][0], op.bs);
+      dmma(sim[u], ai[u][0], op.bs);
+      dmma(tre[u], ar[u][1], op.bt);
+      dmma(tim[u], ai[u][1], op.bt);
+    }
 #endif
-      mma_steps<P, 0, S::NK, NSUB, E>(op, x, off, p0, p1, are, aim, tl);
-    else if (cls == 1)
-      mma_steps<P, 0, S::K0_HI, NSUB, E>(op, x, off, p0, p1, are, aim, tl);
-    else if (cls == 2)
-      mma_steps<P, S::K1_LO, S::NK, NSUB, E>(op, x, off, p0, p1, are, aim, tl);
 #pragma unroll
     for (int u = 0; u < NSUB; ++u) {
-#pragma unroll
-      for (int n = 0; n < S::NT; ++n) {
-        const int m = 4 * n + c;
-        if (m < S::NM) {
-          if (o0[u]) o0[u][m * STR] = ElemT<E>::mk(are[u][n][0] + aim[u][n][1], aim[u][n][0] - are[u][n][1]);
-          if (o1[u]) o1[u][m * STR] = ElemT<E>::mk(are[u][n][0] - aim[u][n][1], aim[u][n][0] + are[u][n][1]);
-        }
+      const double pmr = sre[u][0] + tre[u][0], pmi = sim[u][0] + tim[u][0];  // P_m = SP + DP
+      const double ppr = sre[u][0] - tre[u][0], ppi = sim[u][0] - tim[u][0];  // P_m'
+      const double qmr = tre[u][1] + sre[u][1], qmi = tim[u][1] + sim[u][1];  // Q_m = SQ + DQ
+      const double qpr = tre[u][1] - sre[u][1], qpi = tim[u][1] - sim[u][1];  // Q_m'
+      if (st_m) {
+        if (o0[u]) o0[u][o_m] = ET::mk(pmr + qmi, pmi - qmr);  // z_0 = P - iQ
+        if (o1[u]) o1[u][o_m] = ET::mk(pmr - qmi, pmi + qmr);  // z_1 = P + iQ
+      }
+      if (st_mp) {
+        if (o0[u]) o0[u][o_mp] = ET::mk(ppr + qpi, ppi - qpr);
+        if (o1[u]) o1[u][o_mp] = ET::mk(ppr - qpi, ppi + qpr);
       }
     }
-    if (S::TAIL) {
-      // z_0 = (P.re + Q.im, P.im - Q.re), z_1 = (P.re - Q.im, P.im + Q.re) of m = P-1,
-      // partial over this lane's k; transpose-reduce over the 4 lanes of the row
+    if constexpr (S::TAIL) {
+      // transpose-reduce over the 4 lanes of a row: lane c ends with component
+      // c of (z_0.re, z_0.im, z_1.re, z_1.im) at m = H
       const bool odd = c & 1, hi = c & 2;
 #pragma unroll
       for (int u = 0; u < NSUB; ++u) {
-        const double u0 = tl[u][0] + tl[u][3], u1 = tl[u][2] - tl[u][1];
-        const double u2 = tl[u][0] - tl[u][3], u3 = tl[u][2] + tl[u][1];
-        double va = odd ? u1 : u0, vb = odd ? u3 : u2;
-        va += __shfl_xor_sync(0xffffffffu, odd ? u0 : u1, 1);
-        vb += __shfl_xor_sync(0xffffffffu, odd ? u2 : u3, 1);
+        double va = odd ? tl[u][1] : tl[u][0], vb = odd ? tl[u][3] : tl[u][2];
+        va += __shfl_xor_sync(0xffffffffu, odd ? tl[u][0] : tl[u][1], 1);
+        vb += __shfl_xor_sync(0xffffffffu, odd ? tl[u][2] : tl[u][3], 1);
         double w = hi ? vb : va;
         w += __shfl_xor_sync(0xffffffffu, hi ? va : vb, 2);
-        E* o = hi ? o1[u] : o0[u];  // lane c holds component c&1 of z_{c>>1}
-        if (o)
-          reinterpret_cast<typename ElemT<E>::scalar*>(o + (P - 1) * STR)[c & 1] = (typename ElemT<E>::scalar)w;
+        E* o = hi ? o1[u] : o0[u];
+        if (o) reinterpret_cast<typename ET::scalar*>(o + H * STR)[c & 1] = (typename ET::scalar)w;
       }
     }
   }
@@ -884,42 +824,6 @@ __device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
         : "memory");
     if (done) break;
     if (SFT_PRODUCER_SLEEP > 0) __nanosleep(SFT_PRODUCER_SLEEP);
-  }
-}
-
-// the shared tail table, filled by threads 0..3 before the kernel's first __syncthreads
-template <int D, int P>
-__device__ __forceinline__ void fill_tail_smem(const double* __restrict__ frag) {
-  using S = MmaShape<P>;
-  if (TailSmem<D>::v && S::TAIL && threadIdx.x < 4) {
-#pragma unroll
-    for (int kk = 0; kk < S::NK; ++kk)
-      s_tail[kk][threadIdx.x] = make_double2(frag[S::OFF_TAIL + (kk * 2 + 0) * 32 + threadIdx.x],
-                                             frag[S::OFF_TAIL + (kk * 2 + 1) * 32 + threadIdx.x]);
-  }
-}
-
-template <int P, bool TS>
-__device__ __forceinline__ void load_lane_ops(LaneOps<P, TS>& op, const double* __restrict__ frag, int lane) {
-  using S = MmaShape<P>;
-#pragma unroll
-  for (int n = 0; n < S::NT; ++n)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) op.dl[n][j] = frag[S::OFF_DELTA + (n * 4 + j) * 32 + lane];
-  op.dt[0] = S::TAIL ? frag[S::OFF_DTAIL + lane] : 0.0;
-  if (S::TAIL) op.dt[S::TAIL ? 1 : 0] = frag[S::OFF_DTAIL + 32 + lane];
-#pragma unroll
-  for (int kk = 0; kk < S::NK; ++kk) {
-#pragma unroll
-    for (int n = 0; n < S::NT; ++n) op.fb[kk][n] = frag[(kk * S::NT + n) * 32 + lane];
-    if constexpr (!TS) {
-      if (S::TAIL) {
-        op.ft[kk][0] = frag[S::OFF_TAIL + (kk * 2 + 0) * 32 + lane];
-        op.ft[kk][1] = frag[S::OFF_TAIL + (kk * 2 + 1) * 32 + lane];
-      } else {
-        op.ft[kk][0] = op.ft[kk][1] = 0.0;
-      }
-    }
   }
 }
 
@@ -1106,14 +1010,13 @@ __global__ __launch_bounds__((NC + 1) * 32, MINB) void k_translate_ws(TransArgs 
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&p1done[threadIdx.x])), "r"(NC * 32));
   }
   if (threadIdx.x == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  fill_tail_smem<D, P>(frag);
   __syncthreads();
   if (warp == NC) {
     ws_producer<D, P, G, NST, E, PD, BATCH, NB>(a, sched, ntiles, ring, blk, full, empty);
     return;
   }
   // ---------------- consumers ----------------
-  LaneOps<P, TailSmem<D>::v> op;
+  LaneOps<P> op;
   load_lane_ops(op, frag, lane);
   int s = 0, rot = 0;
   uint32_t ph = 0;
@@ -1217,60 +1120,59 @@ __global__ __launch_bounds__((NC + 1) * 32, MINB) void k_translate_ws(TransArgs 
   INSTR_ADD(3, tc0);
 }
 
+// Per-lane operator table of the symmetric pass (SymShape), built from the
+// long-double host tables of beta = 0 (RC_0, RS_0).  Returns {} (an error) if
+// the tables lack the mirror symmetry or the delta structure the kernel's
+// split relies on (never for p = 5, 7, 9).
 template <int P>
-static std::vector<double> mma_fragments() {
-  using S = MmaShape<P>;
+static std::vector<double> sym_fragments() {
+  using S = SymShape<P>;
+  constexpr int H = S::H;
   std::vector<double> V, invD, RC, RS;
   build_tables_host(P, V, invD, &RC, &RS);
   auto rc = [&](int b, int m, int l) { return RC[((size_t)b * P + m) * P + l]; };
   auto rs = [&](int b, int m, int l) { return RS[((size_t)b * P + m) * P + l]; };
-  // full operator entry of stacked element (child b, element l) for output (m, P/Q)
-  auto opv = [&](int b, int l, int m, int pq) -> double {
-    if (pq == 0) return b == 0 ? rc(0, m, l) : rs(1, m, l);
-    return b == 0 ? rs(0, m, l) : -rc(1, m, l);
-  };
-  // tensor-core K index k -> (child k / HP, odd element 2 (k % HP) + 1); padding rows are 0
-  auto bop = [&](int k, int m, int pq) -> double {
-    if (k >= S::K || m >= P || k % S::HP >= S::H) return 0.0;
-    return opv(k / S::HP, 2 * (k % S::HP) + 1, m, pq);
+  // mirror symmetry RC_1 = J RS_0 J, RS_1 = J RC_0 J
+  for (int m = 0; m < P; ++m)
+    for (int l = 0; l < P; ++l)
+      if (std::fabs(rc(1, m, l) - rs(0, P - 1 - m, P - 1 - l)) > 1e-15 ||
+          std::fabs(rs(1, m, l) - rc(0, P - 1 - m, P - 1 - l)) > 1e-15)
+        return {};
+  // column n of the s- / t-GEMM at element l (the 1/2 of the sum/difference folded in)
+  auto col = [&](bool tg, int n, int l) -> double {
+    const int m = n / 2, mp = P - 1 - m;
+    if (m < H) {
+      if (!tg) return n % 2 == 0 ? 0.5 * (rc(0, m, l) + rc(0, mp, l)) : 0.5 * (rs(0, m, l) - rs(0, mp, l));
+      return n % 2 == 0 ? 0.5 * (rc(0, m, l) - rc(0, mp, l)) : 0.5 * (rs(0, m, l) + rs(0, mp, l));
+    }
+    if (m == H && !S::TAIL) return tg ? (n % 2 == 1 ? rs(0, H, l) : 0.0) : (n % 2 == 0 ? rc(0, H, l) : 0.0);
+    return 0.0;
   };
   std::vector<double> fr(S::NFRAG, 0.0);
-  for (int kk = 0; kk < S::NK; ++kk)
-    for (int n = 0; n < S::NT; ++n)
-      for (int lane = 0; lane < 32; ++lane) {
-        const int k = 4 * kk + (lane & 3), col = 8 * n + (lane >> 2);
-        const int m = col / 2, pq = col & 1;
-        fr[(kk * S::NT + n) * 32 + lane] = m < S::NM ? bop(k, m, pq) : 0.0;
-      }
-  if (S::TAIL)
-    for (int kk = 0; kk < S::NK; ++kk)
-      for (int pq = 0; pq < 2; ++pq)
-        for (int lane = 0; lane < 32; ++lane)
-          fr[S::OFF_TAIL + (kk * 2 + pq) * 32 + lane] = bop(4 * kk + (lane & 3), P - 1, pq);
-  // delta (even) columns: output m takes child-0 element 2m and child-1 element
-  // 2m - (P-1) (when in range); every other even-column entry is exactly 0
-  for (int n = 0; n < S::NT; ++n)
-    for (int lane = 0; lane < 32; ++lane) {
-      const int m = 4 * n + (lane & 3);
-      const bool ok = m < S::NM;
-      const int l0 = 2 * m, l1 = 2 * m - (P - 1);
-      const bool v0 = ok && l0 <= P - 1, v1 = ok && l1 >= 0;
-      fr[S::OFF_DELTA + (n * 4 + 0) * 32 + lane] = v0 ? opv(0, l0, m, 0) : 0.0;
-      fr[S::OFF_DELTA + (n * 4 + 1) * 32 + lane] = v0 ? opv(0, l0, m, 1) : 0.0;
-      fr[S::OFF_DELTA + (n * 4 + 2) * 32 + lane] = v1 ? opv(1, l1, m, 0) : 0.0;
-      fr[S::OFF_DELTA + (n * 4 + 3) * 32 + lane] = v1 ? opv(1, l1, m, 1) : 0.0;
+  for (int lane = 0; lane < 32; ++lane) {
+    const int k = lane & 3, n = lane >> 2, c = lane & 3;
+    fr[S::OFF_BS + lane] = k < H ? col(false, n, 2 * k + 1) : 0.0;
+    fr[S::OFF_BT + lane] = k < H ? col(true, n, 2 * k + 1) : 0.0;
+    const bool ev = 2 * c <= P - 1;
+    fr[S::OFF_DS + lane] = ev ? col(false, 2 * c, 2 * c) : 0.0;
+    fr[S::OFF_DS + 32 + lane] = ev ? col(false, 2 * c + 1, 2 * c) : 0.0;
+    fr[S::OFF_DT + lane] = ev ? col(true, 2 * c, 2 * c) : 0.0;
+    fr[S::OFF_DT + 32 + lane] = ev ? col(true, 2 * c + 1, 2 * c) : 0.0;
+    // the split is exact only if lane c's columns have no other even entries
+    for (int i = 0; 2 * i <= P - 1; ++i)
+      if (i != c)
+        for (int nn = 2 * c; nn <= 2 * c + 1; ++nn)
+          if (col(false, nn, 2 * i) != 0.0 || col(true, nn, 2 * i) != 0.0) return {};
+    if (S::TAIL) {
+      fr[S::OFF_TAIL + lane] = k < H ? rc(0, H, 2 * k + 1) : 0.0;
+      fr[S::OFF_TAIL + 32 + lane] = k < H ? rs(0, H, 2 * k + 1) : 0.0;
+      fr[S::OFF_TAIL + 64 + lane] = c == 0 ? rc(0, H, P - 1) : 0.0;
+      fr[S::OFF_TAIL + 96 + lane] = c == 0 ? rs(0, H, P - 1) : 0.0;
     }
+  }
   if (S::TAIL)
-    for (int lane = 0; lane < 32; ++lane) {
-      fr[S::OFF_DTAIL + lane] = (lane & 3) == 0 ? opv(1, P - 1, P - 1, 0) : 0.0;
-      fr[S::OFF_DTAIL + 32 + lane] = (lane & 3) == 0 ? opv(1, P - 1, P - 1, 1) : 0.0;
-    }
-  // the split is exact only if every even-column entry outside the delta is 0
-  for (int b = 0; b < 2; ++b)
-    for (int l = 0; l < P; l += 2)
-      for (int m = 0; m < P; ++m)
-        if (2 * m != b * (P - 1) + l && (rc(b, m, l) != 0.0 || rs(b, m, l) != 0.0))
-          return {};  // (never for p = 5, 7, 9; reported as an error by device_fragments)
+    for (int i = 0; 2 * i < P - 1; ++i)
+      if (rc(0, H, 2 * i) != 0.0 || rs(0, H, 2 * i) != 0.0) return {};
   return fr;
 }
 
@@ -1283,8 +1185,8 @@ static const double* device_fragments(cudaError_t* err) {
   std::lock_guard<std::mutex> lock(mu);
   auto it = cache.find(dev);
   if (it != cache.end()) return it->second;
-  std::vector<double> fr = mma_fragments<P>();
-  if (fr.empty()) {  // the operator tables are not delta-structured: the DMMA split would be wrong
+  std::vector<double> fr = sym_fragments<P>();
+  if (fr.empty()) {  // the operator tables lack the symmetry / delta structure of the split
     *err = cudaErrorInvalidValue;
     return nullptr;
   }
@@ -1474,9 +1376,9 @@ static void launch_pdl(void (*kernel)(KArgs...), unsigned grid, unsigned block, 
 // Resident-CTA grid of a persistent kernel on the current device, with the
 // kernel's dynamic shared-memory opt-in done once per device (a process may
 // plan on several GPUs: nothing here is shared between devices).
+// (cache: one per kernel instantiation -- the caller's static)
 template <class K>
-static cudaError_t persistent_grid(K kernel, int threads, size_t smem, int* grid) {
-  static PerDevice<int> cache;
+static cudaError_t persistent_grid(K kernel, int threads, size_t smem, int* grid, PerDevice<int>& cache) {
   return cache.get(grid, [&](int dev, int* out) {
     cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -1496,8 +1398,9 @@ static cudaError_t launch_ws(const sft_plan_s* Pl, const TransArgs& a, const Lev
   constexpr int PS = StrideT<E, Pow<P, D>::v>::v;
   const size_t smem = (size_t)NST * G * (1 << D) * PS * sizeof(E);
   auto kern = k_translate_ws<D, P, G, NC, NST, MB, E, FUSED, BATCH, F2>;
+  static PerDevice<int> grid_cache;  // this instantiation's grid and smem opt-in, per device
   int grid_max = 0;
-  cudaError_t e = persistent_grid(kern, (NC + 1) * 32, smem, &grid_max);
+  cudaError_t e = persistent_grid(kern, (NC + 1) * 32, smem, &grid_max, grid_cache);
   if (e != cudaSuccess) return e;
   const double* frag = device_fragments<P>(&e);
   if (!frag) return e;
