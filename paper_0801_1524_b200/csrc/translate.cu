@@ -177,9 +177,20 @@ struct SymShape {
   static constexpr int OFF_BS = 0, OFF_BT = 32, OFF_DS = 64, OFF_DT = 128, OFF_TAIL = 192;
   static constexpr int NFRAG = OFF_TAIL + (TAIL ? 4 * 32 : 0);
 };
-#ifdef SFT_NO_ZEROFILL
-#error "the consumers read absent children's slots: SFT_NO_ZEROFILL is not supported"
-#endif
+
+// p = 5 keeps the direct (child-stacked) form: K = 4 = the two odd elements of
+// each child in one k-step, N = (P_m, Q_m) for m = 0..3 in one tile, m = 4 a
+// DFMA tail -- 2 DMMA per super-tile; the symmetric form would need 4 (its
+// s- and t-GEMMs each fill only half a k-step) plus the sum/difference adds.
+template <int P>
+struct UseSym {
+  static constexpr bool v = P >= 7;
+};
+struct DirShape5 {
+  static constexpr int P = 5;
+  // fragment table: B, tail (P, Q weights of this lane's k), delta (a0, b0, a1, b1) of m = lane%4, tail delta
+  static constexpr int OFF_B = 0, OFF_TAIL = 32, OFF_DELTA = 96, OFF_DTAIL = 224, NFRAG = 288;
+};
 
 // complex element of the level buffers / stages: double2 (FP64) or float2
 // (FP32 storage variant; the arithmetic stays FP64 on the tensor cores)
@@ -210,17 +221,92 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
       : "d"(a), "d"(b));
 }
 
+// Stage accesses by 32-bit shared-memory address (explicit ld/st.shared: the
+// row bases are selected between a stage slot and the zero slot, which
+// generic pointers would turn into generic LD/ST).  volatile: never moved
+// across the pass barriers and stage waits (also volatile asm).
+template <typename E>
+__device__ __forceinline__ double2 lds(uint32_t a);
+// How the consumers see absent children (a task's class bit clear):
+// 2 = the row reads the CTA's zero slot (default); 0 = the producer zero-fills
+// their slots (measured on one box: C2 0.975 vs 0.989 ms, C4 36.5 vs 36.8 ms)
+#ifndef SFT_ABSENT
+#define SFT_ABSENT 2
+#endif
+template <>
+__device__ __forceinline__ double2 lds<double2>(uint32_t a) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
+  return v;
+}
+template <>
+__device__ __forceinline__ double2 lds<float2>(uint32_t a) {
+  float x, y;
+  asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(x), "=f"(y) : "r"(a));
+  return make_double2(x, y);
+}
+template <typename E>
+__device__ __forceinline__ void sts(uint32_t a, double re, double im) {
+  if constexpr (sizeof(E) == 16)
+    asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(re), "d"(im) : "memory");
+  else
+    asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(a), "f"((float)re), "f"((float)im) : "memory");
+}
+template <typename E>
+__device__ __forceinline__ void sts1(uint32_t a, double v) {
+  if constexpr (sizeof(E) == 16)
+    asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
+  else
+    asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"((float)v) : "memory");
+}
+
+// One output array of a row: in place in the stage (shared address s) or, in
+// the last pass, in HBM / a peer's buffer (GL, pointer g); ok = false: no store.
+template <typename E, bool GL>
+struct OutRow {
+  E* g;
+  uint32_t s;
+  bool ok;
+  __device__ __forceinline__ void st(int el, double re, double im) const {
+    if (!ok) return;
+    if constexpr (GL) g[el] = ElemT<E>::mk(re, im);
+    else sts<E>(s + el * (int)sizeof(E), re, im);
+  }
+  __device__ __forceinline__ void st1(int el, int comp, double v) const {  // real (0) or imaginary (1) part
+    if (!ok) return;
+    if constexpr (GL) reinterpret_cast<typename ElemT<E>::scalar*>(g + el)[comp] = (typename ElemT<E>::scalar)v;
+    else sts1<E>(s + el * (int)sizeof(E) + comp * (int)sizeof(typename ElemT<E>::scalar), v);
+  }
+};
+
 // Per-lane operator registers of the symmetric pass (lane c = lane % 4)
 template <int P>
 struct LaneOps {
   using S = SymShape<P>;
   double bs, bt;            // B fragments: s- and t-GEMM, k = c, column lane / 4
+                            // (direct form, p = 5: bs = B, bt unused)
   double ds0, ds1, dt0, dt1;  // delta coefficients of this lane's accumulator columns (even element 2c)
+                              // (direct form: a0, b0, a1, b1 of m = c)
   double ts, tt, tds, tdt;    // p = 9 centre: odd coefficients of this lane's k, centre deltas (lane 0)
+                              // (direct form: tail P / Q weights of this lane's k, tail delta on lane 0)
 };
 
 template <int P>
 __device__ __forceinline__ void load_lane_ops(LaneOps<P>& op, const double* __restrict__ frag, int lane) {
+  if constexpr (!UseSym<P>::v) {
+    using S = DirShape5;
+    op.bs = frag[S::OFF_B + lane];
+    op.bt = 0.0;
+    op.ts = frag[S::OFF_TAIL + lane];
+    op.tt = frag[S::OFF_TAIL + 32 + lane];
+    op.ds0 = frag[S::OFF_DELTA + lane];
+    op.ds1 = frag[S::OFF_DELTA + 32 + lane];
+    op.dt0 = frag[S::OFF_DELTA + 64 + lane];
+    op.dt1 = frag[S::OFF_DELTA + 96 + lane];
+    op.tds = frag[S::OFF_DTAIL + lane];
+    op.tdt = frag[S::OFF_DTAIL + 32 + lane];
+    return;
+  }
   using S = SymShape<P>;
   op.bs = frag[S::OFF_BS + lane];
   op.bt = frag[S::OFF_BT + lane];
@@ -587,26 +673,37 @@ __global__ void k_check_schedule(TransArgs a, const unsigned char* __restrict__ 
   if (bad) atomicOr(err, 4);
 }
 
-#ifdef SFT_NSUB
-#define SFT_NSUB35 SFT_NSUB
-#define SFT_NSUB_OTHER SFT_NSUB
-#endif
 #ifndef SFT_ROTATE
 #define SFT_ROTATE 1
+#endif
+// NSUB super-tiles per warp iteration (independent MMA chains interleaved),
+// per (d, p); SFT_NSUB overrides all
+#ifdef SFT_NSUB
+#define SFT_NSUB25 SFT_NSUB
+#define SFT_NSUB27 SFT_NSUB
+#define SFT_NSUB29 SFT_NSUB
+#define SFT_NSUB35 SFT_NSUB
+#define SFT_NSUB37 SFT_NSUB
+#endif
+#ifndef SFT_NSUB25
+#define SFT_NSUB25 1
+#endif
+#ifndef SFT_NSUB27
+#define SFT_NSUB27 1
+#endif
+#ifndef SFT_NSUB29
+#define SFT_NSUB29 1
 #endif
 #ifndef SFT_NSUB35
 #define SFT_NSUB35 2
 #endif
-#ifndef SFT_NSUB_OTHER
-#define SFT_NSUB_OTHER 1
+#ifndef SFT_NSUB37
+#define SFT_NSUB37 1
 #endif
-// One pass of the consumers (NC warps): super-tiles of 8 fiber rows, NSUB
-// super-tiles per warp iteration (independent MMA chains interleaved).
-// Measured (C3 translate, B200): 3D p = 5 1.108 -> 1.023 ms with NSUB = 2; 2D p = 9
-// 1.50 -> 2.37 ms and 3D p = 7 53.2 -> 55.8 ms (register pressure).  SFT_NSUB overrides.
 template <int D, int P>
 struct NsubCfg {
-  static constexpr int v = (D == 3 && P == 5) ? SFT_NSUB35 : SFT_NSUB_OTHER;
+  static constexpr int v = D == 2 ? (P == 5 ? SFT_NSUB25 : P == 7 ? SFT_NSUB27 : SFT_NSUB29)
+                                  : (P == 5 ? SFT_NSUB35 : P == 7 ? SFT_NSUB37 : 1);
 };
 // Row -> fiber map of a super-tile: chosen per (d, p, axis) by
 // scripts/rfib_search_sym.py, which minimises the modelled shared-memory
@@ -616,14 +713,157 @@ struct NsubCfg {
 template <int D, int P, int AX>
 struct RowMap {
   __device__ __forceinline__ static int fiber(int r) {
-    if constexpr (D == 2 && P == 5) return (0x65437210u >> (4 * r)) & 7;                // 0 1 2 7 3 4 5 6
-    else if constexpr (D == 2 && P == 7) return (0x65432170u >> (4 * r)) & 7;           // 0 7 1 2 3 4 5 6
-    else if constexpr (D == 3 && P == 5 && AX == 0) return (0x63724150u >> (4 * r)) & 7;  // 0 5 1 4 2 7 3 6
-    else if constexpr (D == 3 && P == 5 && AX == 1) return (0x74326150u >> (4 * r)) & 7;  // 0 5 1 6 2 3 4 7
-    else if constexpr ((D == 3 && P == 5 && AX == 2) || (D == 3 && P == 7 && AX == 1)) return r;
-    else return (r >> 1) + 4 * (r & 1);
+    if constexpr (UseSym<P>::v) return r;  // symmetric form: rows 2q, 2q+1 <- consecutive fibers
+    else if constexpr (D == 2) return (0x65437210u >> (4 * r)) & 7;                      // 0 1 2 7 3 4 5 6
+    else if constexpr (AX == 0) return (0x63724150u >> (4 * r)) & 7;                      // 0 5 1 4 2 7 3 6
+    else if constexpr (AX == 1) return (0x74326150u >> (4 * r)) & 7;                      // 0 5 1 6 2 3 4 7
+    else return r;
   }
 };
+
+// Super-tile arithmetic of the direct form (p = 5, DirShape5): lane c loads
+// child (c >> 1)'s odd element 2 (c & 1) + 1 (the A fragment of k = c), and
+// for its output m = c child 0's element 2m and child 1's element 2m - (p-1)
+// (the delta columns, coefficients 0 when out of range); 2 DMMA give (P_m,
+// Q_m) of m = c, a 4-lane transpose-reduce the tail m = p-1.
+template <int D, int P, int STR, int C1, int NSUB, typename E, bool GL>
+__device__ __forceinline__ void direct_math(const LaneOps<P>& op, const uint32_t (&xa)[NSUB], const uint32_t (&xb)[NSUB],
+                                            const OutRow<E, GL> (&o0)[NSUB], const OutRow<E, GL> (&o1)[NSUB], int c) {
+  constexpr int ES = sizeof(E);
+  const int o_a = (2 * (c & 1) + 1) * STR * ES;  // of child c >> 1 (byte offsets)
+  const int o_e0 = min(2 * c, P - 1) * STR * ES, o_e1 = max(2 * c - (P - 1), 0) * STR * ES;
+  const int o_t = (P - 1) * STR * ES;  // tail delta: child 1, element p-1
+  double are[NSUB][2], aim[NSUB][2], tl[NSUB][4];
+  double avx[NSUB], avy[NSUB];
+#pragma unroll
+  for (int u = 0; u < NSUB; ++u) {
+    const double2 av = lds<E>(((c >> 1) ? xb[u] : xa[u]) + o_a);
+    const double2 x0 = lds<E>(xa[u] + o_e0), x1 = lds<E>(xb[u] + o_e1);
+    const double2 xt = lds<E>(xb[u] + o_t);
+    are[u][0] = fma(op.dt0, x1.x, op.ds0 * x0.x);
+    are[u][1] = fma(op.dt1, x1.x, op.ds1 * x0.x);
+    aim[u][0] = fma(op.dt0, x1.y, op.ds0 * x0.y);
+    aim[u][1] = fma(op.dt1, x1.y, op.ds1 * x0.y);
+    tl[u][0] = fma(av.x, op.ts, op.tds * xt.x);  // P.re
+    tl[u][1] = fma(av.x, op.tt, op.tdt * xt.x);  // Q.re
+    tl[u][2] = fma(av.y, op.ts, op.tds * xt.y);  // P.im
+    tl[u][3] = fma(av.y, op.tt, op.tdt * xt.y);  // Q.im
+    avx[u] = av.x;
+    avy[u] = av.y;
+  }
+#ifndef SFT_ABL_NOCOMPUTE
+#pragma unroll
+  for (int u = 0; u < NSUB; ++u) {
+    dmma(are[u], avx[u], op.bs);
+    dmma(aim[u], avy[u], op.bs);
+  }
+#endif
+  const bool odd = c & 1, hi = c & 2;
+#pragma unroll
+  for (int u = 0; u < NSUB; ++u) {
+    o0[u].st(c * STR, are[u][0] + aim[u][1], aim[u][0] - are[u][1]);  // z_0 = P - iQ
+    o1[u].st(c * STR, are[u][0] - aim[u][1], aim[u][0] + are[u][1]);  // z_1 = P + iQ
+    // tail m = p-1: (z_0.re, z_0.im, z_1.re, z_1.im) partials, transpose-reduce
+    const double u0 = tl[u][0] + tl[u][3], u1 = tl[u][2] - tl[u][1];
+    const double u2 = tl[u][0] - tl[u][3], u3 = tl[u][2] + tl[u][1];
+    double va = odd ? u1 : u0, vb = odd ? u3 : u2;
+    va += __shfl_xor_sync(0xffffffffu, odd ? u0 : u1, 1);
+    vb += __shfl_xor_sync(0xffffffffu, odd ? u2 : u3, 1);
+    double w = hi ? vb : va;
+    w += __shfl_xor_sync(0xffffffffu, hi ? va : vb, 2);
+    (hi ? o1[u] : o0[u]).st1((P - 1) * STR, c & 1, w);
+  }
+}
+
+// Which row of a 16-byte phase swaps the m / m' store order (see consumer_pass):
+// the even rows where the odd-row swap would put both rows' first stores on the
+// same bank groups (scripts/rfib_model_sym.py: 3D p = 7 axes 1, 2 and 2D p = 7)
+template <int D, int P, int AX>
+struct SwapEven {
+  static constexpr bool v = P == 7 && (D == 2 || AX >= 1);
+};
+
+// Super-tile arithmetic of the symmetric form (p = 7, 9; see SymShape)
+template <int D, int P, int STR, int C1, int NSUB, typename E, bool GL>
+__device__ __forceinline__ void sym_math(const LaneOps<P>& op, const uint32_t (&xa)[NSUB], const uint32_t (&xb)[NSUB],
+                                         const OutRow<E, GL> (&o0)[NSUB], const OutRow<E, GL> (&o1)[NSUB],
+                                         int c, int o_a0, int o_a1, int o_d0, int o_d1, int o_f, int o_s, bool st_f,
+                                         bool st_s, double sg) {
+  using S = SymShape<P>;
+  using ET = ElemT<E>;
+  constexpr int H = S::H;
+  // accumulators: s-GEMM columns (SP_m, DQ_m), t-GEMM columns (DP_m, SQ_m), re / im rows
+  double sre[NSUB][2], sim[NSUB][2], tre[NSUB][2], tim[NSUB][2], tl[NSUB][4];
+  double ar[NSUB][2], ai[NSUB][2];  // odd s / t of this lane's k (re, im)
+#pragma unroll
+  for (int u = 0; u < NSUB; ++u) {
+    constexpr int ES = sizeof(E);
+    const double2 e0 = lds<E>(xa[u] + o_d0 * ES), e1 = lds<E>(xb[u] + o_d1 * ES);
+    const double2 a0 = lds<E>(xa[u] + o_a0 * ES), a1 = lds<E>(xb[u] + o_a1 * ES);
+    const double ser = e0.x + e1.x, sei = e0.y + e1.y, ter = e0.x - e1.x, tei = e0.y - e1.y;
+    sre[u][0] = op.ds0 * ser;
+    sre[u][1] = op.ds1 * ser;
+    sim[u][0] = op.ds0 * sei;
+    sim[u][1] = op.ds1 * sei;
+    tre[u][0] = op.dt0 * ter;
+    tre[u][1] = op.dt1 * ter;
+    tim[u][0] = op.dt0 * tei;
+    tim[u][1] = op.dt1 * tei;
+    ar[u][0] = a0.x + a1.x;  // s
+    ai[u][0] = a0.y + a1.y;
+    ar[u][1] = a0.x - a1.x;  // t
+    ai[u][1] = a0.y - a1.y;
+    if constexpr (S::TAIL) {
+      // centre m = H (p = 9): partials of z_0, z_1 over this lane's k, centre delta on lane 0
+      const double2 c0 = lds<E>(xa[u] + (P - 1) * STR * ES), c1 = lds<E>(xb[u]);
+      const double pr = fma(op.tds, c0.x + c1.x, op.ts * ar[u][0]), pi = fma(op.tds, c0.y + c1.y, op.ts * ai[u][0]);
+      const double qr = fma(op.tdt, c0.x - c1.x, op.tt * ar[u][1]), qi = fma(op.tdt, c0.y - c1.y, op.tt * ai[u][1]);
+      tl[u][0] = pr + qi;
+      tl[u][1] = pi - qr;
+      tl[u][2] = pr - qi;
+      tl[u][3] = pi + qr;
+    }
+  }
+#ifndef SFT_ABL_NOCOMPUTE  // ablation: no tensor-core work
+#pragma unroll
+  for (int u = 0; u < NSUB; ++u) {
+    dmma(sre[u], ar[u][0], op.bs);
+    dmma(sim[u], ai[u][0], op.bs);
+    dmma(tre[u], ar[u][1], op.bt);
+    dmma(tim[u], ai[u][1], op.bt);
+  }
+#endif
+#pragma unroll
+  for (int u = 0; u < NSUB; ++u) {
+    // first store: m (sg = 1) or m' (sg = -1), second: the other one
+    const double pfr = fma(sg, tre[u][0], sre[u][0]), pfi = fma(sg, tim[u][0], sim[u][0]);  // P = SP +- DP
+    const double psr = fma(-sg, tre[u][0], sre[u][0]), psi = fma(-sg, tim[u][0], sim[u][0]);
+    const double qfr = fma(sg, sre[u][1], tre[u][1]), qfi = fma(sg, sim[u][1], tim[u][1]);  // Q = SQ +- DQ
+    const double qsr = fma(-sg, sre[u][1], tre[u][1]), qsi = fma(-sg, sim[u][1], tim[u][1]);
+    if (st_f) {
+      o0[u].st(o_f, pfr + qfi, pfi - qfr);  // z_0 = P - iQ
+      o1[u].st(o_f, pfr - qfi, pfi + qfr);  // z_1 = P + iQ
+    }
+    if (st_s) {
+      o0[u].st(o_s, psr + qsi, psi - qsr);
+      o1[u].st(o_s, psr - qsi, psi + qsr);
+    }
+  }
+  if constexpr (S::TAIL) {
+    // transpose-reduce over the 4 lanes of a row: lane c ends with component
+    // c of (z_0.re, z_0.im, z_1.re, z_1.im) at m = H
+    const bool odd = c & 1, hi = c & 2;
+#pragma unroll
+    for (int u = 0; u < NSUB; ++u) {
+      double va = odd ? tl[u][1] : tl[u][0], vb = odd ? tl[u][3] : tl[u][2];
+      va += __shfl_xor_sync(0xffffffffu, odd ? tl[u][0] : tl[u][1], 1);
+      vb += __shfl_xor_sync(0xffffffffu, odd ? tl[u][2] : tl[u][3], 1);
+      double w = hi ? vb : va;
+      w += __shfl_xor_sync(0xffffffffu, hi ? va : vb, 2);
+      (hi ? o1[u] : o0[u]).st1(H * STR, c & 1, w);
+    }
+  }
+}
 
 // One axis pass of the consumers (NC warps), symmetric form (see SymShape).
 // A warp takes super-tiles of 8 fiber tasks: MMA row r (= lane/4) is one
@@ -639,7 +879,9 @@ template <int D, int P, int G, int NC, int AX, bool LAST, int LIST = AX, typenam
           int MUL = 0>
 __device__ __forceinline__ void consumer_pass(const TransArgs& a, E* __restrict__ sb,
                                               const unsigned char* __restrict__ blk, const LaneOps<P>& op,
-                                              int& rot, int64_t ooff = 0) {
+                                              const E* __restrict__ zs, int& rot, int64_t ooff = 0) {
+  constexpr int ES = sizeof(E);
+  const uint32_t sba = smem_u32(sb), zsa = smem_u32(zs);  // stage and zero slot (shared addresses)
   using S = SymShape<P>;
   using SC = Sched<D, P, G>;
   using ET = ElemT<E>;
@@ -660,10 +902,18 @@ __device__ __forceinline__ void consumer_pass(const TransArgs& a, E* __restrict_
   const int rfib = RowMap<D, P, AX>::fiber(lane >> 2);  // row -> fiber of the super-tile (bank conflicts)
   // this lane's element offsets in a fiber (padding k >= H: a valid odd element, zero B row;
   // delta / outputs of lanes c > H (p = 5): clamped, coefficients 0, no stores)
-  const int o_a0 = min(2 * c + 1, P - 2) * STR, o_a1 = C1 + max(P - 2 - 2 * c, 1) * STR;
-  const int o_d0 = min(2 * c, P - 1) * STR, o_d1 = C1 + max(P - 1 - 2 * c, 0) * STR;
-  const int o_m = min(c, H) * STR, o_mp = max(P - 1 - c, H) * STR;
-  const bool st_m = c <= H, st_mp = c < H;
+  // (child 1 offsets relative to its own slot)
+  const int o_a0 = min(2 * c + 1, P - 2) * STR, o_a1 = max(P - 2 - 2 * c, 1) * STR;
+  const int o_d0 = min(2 * c, P - 1) * STR, o_d1 = max(P - 1 - 2 * c, 0) * STR;
+  // outputs m = c and m' = p-1-c: one row of each 16-byte-access phase
+  // (rows 2q, 2q+1) stores m then m', the other m' then m (role swap, sg =
+  // -1); which row swaps depends on the fiber-address step and STR mod 8
+  // (SwapEven, from scripts/rfib_model_sym.py) -- with it the phase's loads
+  // and stores are bank-conflict free for p = 7 and 3 of 4 instructions for p = 9
+  const bool swp = ((lane >> 2) & 1) ^ SwapEven<D, P, AX>::v;
+  const double sg = swp ? -1.0 : 1.0;
+  const int o_f = (swp ? max(P - 1 - c, H) : min(c, H)) * STR, o_s = (swp ? min(c, H) : max(P - 1 - c, H)) * STR;
+  const bool st_f = c <= H, st_s = c < H;
   // units of NSUB super-tiles go round-robin over the warps, continuing from
   // where the previous pass stopped (rot), so that the extra unit of a pass
   // whose count is not a multiple of NC does not always land on warp 0
@@ -671,9 +921,11 @@ __device__ __forceinline__ void consumer_pass(const TransArgs& a, E* __restrict_
   // (measured: C2 -0.8%, C1 -2%, C3 +2%: 2D only)
   if (SFT_ROTATE && D == 2) rot = (rot + (nst + NSUB - 1) / NSUB) % NC;
   for (int st0 = j0 * NSUB; st0 < nst; st0 += NC * NSUB) {
-    const E* x[NSUB];
-    E* o0[NSUB];
-    E* o1[NSUB];
+    // child slots of the row's pair; an absent child (its task's class bit
+    // clear) reads the CTA's zero slot instead: absent slots are never
+    // zero-filled or read
+    uint32_t xa[NSUB], xb[NSUB];
+    OutRow<E, LAST> o0[NSUB], o1[NSUB];
 #pragma unroll
     for (int u = 0; u < NSUB; ++u) {
       const int tau = (st0 + u) * 8 + rfib;
@@ -690,9 +942,19 @@ __device__ __forceinline__ void consumer_pass(const TransArgs& a, E* __restrict_
         d.o0 = d.o1 = ~0u;
       }
       const uint32_t xo = d.x + (uint32_t)ebase;
-      x[u] = sb + xo;
+#if SFT_ABSENT == 2
+      xa[u] = (d.cls & 1u) ? sba + xo * ES : zsa + ebase * ES;
+      xb[u] = (d.cls & 2u) ? sba + (xo + C1) * ES : zsa + ebase * ES;
+#else  // zero-filled absent slots
+      xa[u] = sba + xo * ES;
+      xb[u] = sba + (xo + C1) * ES;
+#endif
+
+      o0[u].g = o1[u].g = nullptr;
+      o0[u].s = sba + xo * ES;
+      o1[u].s = sba + (xo + C1) * ES;
 #ifdef SFT_ABL_NOSTORE  // ablation: no output stores (shared or global)
-      o0[u] = o1[u] = nullptr;
+      o0[u].ok = o1[u].ok = false;
 #else
       if (LAST && FUSED) {
         // fused exchange: straight into the receiving rank's buffer
@@ -703,88 +965,24 @@ __device__ __forceinline__ void consumer_pass(const TransArgs& a, E* __restrict_
           while (q + 1 < a.npeer && i >= a.peer_seg[q + 1]) ++q;
           return reinterpret_cast<E*>(a.peer[q]) + a.peer_off[q] + (i - a.peer_seg[q]) * PD + ebase;
         };
-        o0[u] = dst(d.o0);
-        o1[u] = dst(d.o1);
+        o0[u].g = dst(d.o0);
+        o1[u].g = dst(d.o1);
+        o0[u].ok = o0[u].g != nullptr;
+        o1[u].ok = o1[u].g != nullptr;
       } else if (LAST) {
-        o0[u] = d.o0 != ~0u ? gout + d.o0 + ebase : nullptr;
-        o1[u] = d.o1 != ~0u ? gout + d.o1 + ebase : nullptr;
+        o0[u].g = gout + d.o0 + ebase;
+        o1[u].g = gout + d.o1 + ebase;
+        o0[u].ok = d.o0 != ~0u;
+        o1[u].ok = d.o1 != ~0u;
       } else {
-        o0[u] = vrow ? sb + xo : nullptr;
-        o1[u] = vrow ? sb + xo + C1 : nullptr;
+        o0[u].ok = o1[u].ok = vrow;
       }
 #endif
     }
-    // accumulators: s-GEMM columns (SP_m, DQ_m), t-GEMM columns (DP_m, SQ_m), re / im rows
-    double sre[NSUB][2], sim[NSUB][2], tre[NSUB][2], tim[NSUB][2], tl[NSUB][4];
-    double ar[NSUB][2], ai[NSUB][2];  // odd s / t of this lane's k (re, im)
-#pragma unroll
-    for (int u = 0; u < NSUB; ++u) {
-      // absent children's slots are zero-filled by the producer: no masking
-      const double2 e0 = ET::ld(x[u][o_d0]), e1 = ET::ld(x[u][o_d1]);
-      const double2 a0 = ET::ld(x[u][o_a0]), a1 = ET::ld(x[u][o_a1]);
-      const double ser = e0.x + e1.x, sei = e0.y + e1.y, ter = e0.x - e1.x, tei = e0.y - e1.y;
-      sre[u][0] = op.ds0 * ser;
-      sre[u][1] = op.ds1 * ser;
-      sim[u][0] = op.ds0 * sei;
-      sim[u][1] = op.ds1 * sei;
-      tre[u][0] = op.dt0 * ter;
-      tre[u][1] = op.dt1 * ter;
-      tim[u][0] = op.dt0 * tei;
-      tim[u][1] = op.dt1 * tei;
-      ar[u][0] = a0.x + a1.x;  // s
-      ai[u][0] = a0.y + a1.y;
-      ar[u][1] = a0.x - a1.x;  // t
-      ai[u][1] = a0.y - a1.y;
-      if constexpr (S::TAIL) {
-        // centre m = H (p = 9): partials of z_0, z_1 over this lane's k, centre delta on lane 0
-        const double2 c0 = ET::ld(x[u][(P - 1) * STR]), c1 = ET::ld(x[u][C1]);
-        const double pr = fma(op.tds, c0.x + c1.x, op.ts * ar[u][0]), pi = fma(op.tds, c0.y + c1.y, op.ts * ai[u][0]);
-        const double qr = fma(op.tdt, c0.x - c1.x, op.tt * ar[u][1]), qi = fma(op.tdt, c0.y - c1.y, op.tt * ai[u][1]);
-        tl[u][0] = pr + qi;
-        tl[u][1] = pi - qr;
-        tl[u][2] = pr - qi;
-        tl[u][3] = pi + qr;
-      }
-    }
-#ifndef SFT_ABL_NOCOMPUTE  // ablation: no tensor-core work
-#pragma unroll
-    for (int u = 0; u < NSUB; ++u) {
-      dmma(sre[u], ar[u][0], op.bs);
-      dmma(sim[u], ai[u][0], op.bs);
-      dmma(tre[u], ar[u][1], op.bt);
-      dmma(tim[u], ai[u][1], op.bt);
-    }
-#endif
-#pragma unroll
-    for (int u = 0; u < NSUB; ++u) {
-      const double pmr = sre[u][0] + tre[u][0], pmi = sim[u][0] + tim[u][0];  // P_m = SP + DP
-      const double ppr = sre[u][0] - tre[u][0], ppi = sim[u][0] - tim[u][0];  // P_m'
-      const double qmr = tre[u][1] + sre[u][1], qmi = tim[u][1] + sim[u][1];  // Q_m = SQ + DQ
-      const double qpr = tre[u][1] - sre[u][1], qpi = tim[u][1] - sim[u][1];  // Q_m'
-      if (st_m) {
-        if (o0[u]) o0[u][o_m] = ET::mk(pmr + qmi, pmi - qmr);  // z_0 = P - iQ
-        if (o1[u]) o1[u][o_m] = ET::mk(pmr - qmi, pmi + qmr);  // z_1 = P + iQ
-      }
-      if (st_mp) {
-        if (o0[u]) o0[u][o_mp] = ET::mk(ppr + qpi, ppi - qpr);
-        if (o1[u]) o1[u][o_mp] = ET::mk(ppr - qpi, ppi + qpr);
-      }
-    }
-    if constexpr (S::TAIL) {
-      // transpose-reduce over the 4 lanes of a row: lane c ends with component
-      // c of (z_0.re, z_0.im, z_1.re, z_1.im) at m = H
-      const bool odd = c & 1, hi = c & 2;
-#pragma unroll
-      for (int u = 0; u < NSUB; ++u) {
-        double va = odd ? tl[u][1] : tl[u][0], vb = odd ? tl[u][3] : tl[u][2];
-        va += __shfl_xor_sync(0xffffffffu, odd ? tl[u][0] : tl[u][1], 1);
-        vb += __shfl_xor_sync(0xffffffffu, odd ? tl[u][2] : tl[u][3], 1);
-        double w = hi ? vb : va;
-        w += __shfl_xor_sync(0xffffffffu, hi ? va : vb, 2);
-        E* o = hi ? o1[u] : o0[u];
-        if (o) reinterpret_cast<typename ET::scalar*>(o + H * STR)[c & 1] = (typename ET::scalar)w;
-      }
-    }
+    if constexpr (!UseSym<P>::v)
+      direct_math<D, P, STR, C1, NSUB, E>(op, xa, xb, o0, o1, c);
+    else
+      sym_math<D, P, STR, C1, NSUB, E>(op, xa, xb, o0, o1, c, o_a0, o_a1, o_d0, o_d1, o_f, o_s, st_f, st_s, sg);
   }
 }
 
@@ -854,11 +1052,14 @@ __device__ __forceinline__ void ws_issue(const TransArgs& a, const unsigned char
   E* sb = ring + s * STAGE;
   // uniform tile: G groups of one B with consecutive A' (the common case) --
   // every child slot's G arrays are contiguous in HBM and in the slot-major
-  // stage, so one bulk copy (or one zero-fill) per child slot
+  // stage, so one bulk copy per present child slot.  Absent children's slots
+  // are not touched: the consumers read only the slots their task's class
+  // marks present.
   const int ng = (int)min((int64_t)G, a.ngroups - tile * G);
   const uint32_t m0 = __shfl_sync(0xffffffffu, gr.y, 0), p0 = __shfl_sync(0xffffffffu, gr.x, 0);
   const bool mine_ok = lane >= G || (gr.y == m0 && gr.x == p0 + (uint32_t)lane);
   const bool uniform = __all_sync(0xffffffffu, mine_ok) && ng == G && m0 != 0u;
+#if SFT_ABSENT == 0
   {
     constexpr int CH = PD * (int)sizeof(E) / 16;  // 16-byte chunks per slot
     if (uniform) {
@@ -868,7 +1069,6 @@ __device__ __forceinline__ void ws_issue(const TransArgs& a, const unsigned char
         for (int q = lane; q < G * CH; q += 32) z[q] = make_float4(0.f, 0.f, 0.f, 0.f);
       }
     } else {
-      // zero the slots of absent children: the consumers read every slot unmasked
       for (int js = 0; js < ng * NS; ++js) {
         const int j = js / NS, c = js % NS;
         const uint32_t mB = __shfl_sync(0xffffffffu, gr.y, j);
@@ -877,9 +1077,12 @@ __device__ __forceinline__ void ws_issue(const TransArgs& a, const unsigned char
         for (int q = lane; q < CH; q += 32) z[q] = make_float4(0.f, 0.f, 0.f, 0.f);
       }
     }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    __syncwarp();
   }
+#endif
+  // the consumers' generic-proxy accesses of this stage (released through
+  // empty[s]) are ordered before the async-proxy writes below
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncwarp();
   if (lane == 0) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&full[s])),
                  "r"(nbytes + (uint32_t)(SC::BLK * NB))
@@ -1000,6 +1203,7 @@ __global__ __launch_bounds__((NC + 1) * 32, MINB) void k_translate_ws(TransArgs 
   constexpr int STAGE = G * NS * PD;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   E* ring = reinterpret_cast<E*>(smem_raw);  // [NST][G][NS][PD]
+  E* const zs = ring + NST * STAGE;          // [PD] zeros: what an absent child slot reads
   constexpr int NB = F2 ? 2 : 1;  // schedule blocks per tile
   __shared__ __align__(128) unsigned char blk[NST][SC::BLK * NB];
   __shared__ __align__(8) uint64_t full[NST], empty[NST], p1done[NST];
@@ -1010,6 +1214,8 @@ __global__ __launch_bounds__((NC + 1) * 32, MINB) void k_translate_ws(TransArgs 
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&p1done[threadIdx.x])), "r"(NC * 32));
   }
   if (threadIdx.x == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  for (int q = threadIdx.x; q < PD * (int)sizeof(E) / 16; q += blockDim.x)
+    reinterpret_cast<float4*>(zs)[q] = make_float4(0.f, 0.f, 0.f, 0.f);
   __syncthreads();
   if (warp == NC) {
     ws_producer<D, P, G, NST, E, PD, BATCH, NB>(a, sched, ntiles, ring, blk, full, empty);
@@ -1024,12 +1230,12 @@ __global__ __launch_bounds__((NC + 1) * 32, MINB) void k_translate_ws(TransArgs 
   // 2D: first passes (list 1: axis 1, list 2: axis 0 for groups in reversed
   // order), then last passes (list 0: axis 0, list 3: axis 1)
   auto first2d = [&](E* sb_, const unsigned char* bk) {
-    consumer_pass<D, P, G, NC, D - 1, false, 1, E>(a, sb_, bk, op, rot, 0);
-    if constexpr (D == 2) consumer_pass<D, P, G, NC, 0, false, 2, E>(a, sb_, bk, op, rot, 0);
+    consumer_pass<D, P, G, NC, D - 1, false, 1, E>(a, sb_, bk, op, zs, rot, 0);
+    if constexpr (D == 2) consumer_pass<D, P, G, NC, 0, false, 2, E>(a, sb_, bk, op, zs, rot, 0);
   };
   auto last2d = [&](E* sb_, const unsigned char* bk, int64_t oo) {
-    consumer_pass<D, P, G, NC, 0, true, 0, E, FUSED>(a, sb_, bk, op, rot, oo);
-    if constexpr (D == 2) consumer_pass<D, P, G, NC, D - 1, true, 3, E, FUSED>(a, sb_, bk, op, rot, oo);
+    consumer_pass<D, P, G, NC, 0, true, 0, E, FUSED>(a, sb_, bk, op, zs, rot, oo);
+    if constexpr (D == 2) consumer_pass<D, P, G, NC, D - 1, true, 3, E, FUSED>(a, sb_, bk, op, zs, rot, oo);
   };
   // work items w = tile * nrhs + r; the output of RHS r goes to out + r * rs
   const int64_t nwork = BATCH ? ntiles * a.nrhs : ntiles;
@@ -1077,17 +1283,17 @@ __global__ __launch_bounds__((NC + 1) * 32, MINB) void k_translate_ws(TransArgs 
         // 1) on the transposed slots, its second pass to HBM
         const unsigned char* bk0 = blk[s];
         const unsigned char* bk1 = blk[s] + SC::BLK;
-        consumer_pass<D, P, G, NC, 1, false, 1, E>(a, sb, bk0, op, rot, 0);
-        consumer_pass<D, P, G, NC, 0, false, 2, E>(a, sb, bk0, op, rot, 0);
+        consumer_pass<D, P, G, NC, 1, false, 1, E>(a, sb, bk0, op, zs, rot, 0);
+        consumer_pass<D, P, G, NC, 0, false, 2, E>(a, sb, bk0, op, zs, rot, 0);
         consumer_sync<NC * 32>();
-        consumer_pass<D, P, G, NC, 0, false, 0, E>(a, sb, bk0, op, rot, 0);
-        consumer_pass<D, P, G, NC, 1, false, 3, E>(a, sb, bk0, op, rot, 0);
+        consumer_pass<D, P, G, NC, 0, false, 0, E>(a, sb, bk0, op, zs, rot, 0);
+        consumer_pass<D, P, G, NC, 1, false, 3, E>(a, sb, bk0, op, zs, rot, 0);
         consumer_sync<NC * 32>();
-        consumer_pass<D, P, G, NC, 1, false, 1, E, false, 1>(a, sb, bk1, op, rot, 0);
-        consumer_pass<D, P, G, NC, 0, false, 2, E, false, 1>(a, sb, bk1, op, rot, 0);
+        consumer_pass<D, P, G, NC, 1, false, 1, E, false, 1>(a, sb, bk1, op, zs, rot, 0);
+        consumer_pass<D, P, G, NC, 0, false, 2, E, false, 1>(a, sb, bk1, op, zs, rot, 0);
         consumer_sync<NC * 32>();
-        consumer_pass<D, P, G, NC, 0, true, 0, E, false, 1>(a, sb, bk1, op, rot, ooff(w));
-        consumer_pass<D, P, G, NC, 1, true, 3, E, false, 1>(a, sb, bk1, op, rot, ooff(w));
+        consumer_pass<D, P, G, NC, 0, true, 0, E, false, 1>(a, sb, bk1, op, zs, rot, ooff(w));
+        consumer_pass<D, P, G, NC, 1, true, 3, E, false, 1>(a, sb, bk1, op, zs, rot, ooff(w));
       } else if constexpr (D == 2) {
         INSTR_T0(t1);
         first2d(sb, blk[s]);
@@ -1099,11 +1305,11 @@ __global__ __launch_bounds__((NC + 1) * 32, MINB) void k_translate_ws(TransArgs 
         last2d(sb, blk[s], ooff(w));
         INSTR_ADD(7, t3);
       } else {
-        consumer_pass<D, P, G, NC, 2, false, 2, E>(a, sb, blk[s], op, rot, 0);
+        consumer_pass<D, P, G, NC, 2, false, 2, E>(a, sb, blk[s], op, zs, rot, 0);
         consumer_sync<NC * 32>();
-        consumer_pass<D, P, G, NC, 1, false, 1, E>(a, sb, blk[s], op, rot, 0);
+        consumer_pass<D, P, G, NC, 1, false, 1, E>(a, sb, blk[s], op, zs, rot, 0);
         consumer_sync<NC * 32>();
-        consumer_pass<D, P, G, NC, 0, true, 0, E, FUSED>(a, sb, blk[s], op, rot, ooff(w));
+        consumer_pass<D, P, G, NC, 0, true, 0, E, FUSED>(a, sb, blk[s], op, zs, rot, ooff(w));
       }
       __syncwarp();
       if (lane == 0)
@@ -1176,6 +1382,46 @@ static std::vector<double> sym_fragments() {
   return fr;
 }
 
+// Per-lane table of the direct form (p = 5): stacked K = (child 0: elements
+// 1, 3; child 1: elements 1, 3), columns (P_m, Q_m) of m = 0..3, tail m = 4.
+// {} if the tables lack the delta structure.
+static std::vector<double> direct_fragments5() {
+  constexpr int P = 5;
+  using S = DirShape5;
+  std::vector<double> V, invD, RC, RS;
+  build_tables_host(P, V, invD, &RC, &RS);
+  auto rc = [&](int b, int m, int l) { return RC[((size_t)b * P + m) * P + l]; };
+  auto rs = [&](int b, int m, int l) { return RS[((size_t)b * P + m) * P + l]; };
+  // operator entry of (child b, element l) for output (m, P/Q):
+  // P = RC_0 x_0 + RS_1 x_1, Q = RS_0 x_0 - RC_1 x_1
+  auto opv = [&](int b, int l, int m, int pq) -> double {
+    if (pq == 0) return b == 0 ? rc(0, m, l) : rs(1, m, l);
+    return b == 0 ? rs(0, m, l) : -rc(1, m, l);
+  };
+  std::vector<double> fr(S::NFRAG, 0.0);
+  for (int lane = 0; lane < 32; ++lane) {
+    const int k = lane & 3, n = lane >> 2, c = lane & 3;
+    const int b = k >> 1, l = 2 * (k & 1) + 1;
+    fr[S::OFF_B + lane] = opv(b, l, n / 2, n % 2);
+    fr[S::OFF_TAIL + lane] = opv(b, l, P - 1, 0);
+    fr[S::OFF_TAIL + 32 + lane] = opv(b, l, P - 1, 1);
+    const int m = c, l0 = 2 * m, l1 = 2 * m - (P - 1);
+    const bool v0 = l0 <= P - 1, v1 = l1 >= 0;
+    fr[S::OFF_DELTA + lane] = v0 ? opv(0, l0, m, 0) : 0.0;
+    fr[S::OFF_DELTA + 32 + lane] = v0 ? opv(0, l0, m, 1) : 0.0;
+    fr[S::OFF_DELTA + 64 + lane] = v1 ? opv(1, l1, m, 0) : 0.0;
+    fr[S::OFF_DELTA + 96 + lane] = v1 ? opv(1, l1, m, 1) : 0.0;
+    fr[S::OFF_DTAIL + lane] = c == 0 ? opv(1, P - 1, P - 1, 0) : 0.0;
+    fr[S::OFF_DTAIL + 32 + lane] = c == 0 ? opv(1, P - 1, P - 1, 1) : 0.0;
+  }
+  // the split is exact only if every even-column entry outside the delta is 0
+  for (int b = 0; b < 2; ++b)
+    for (int l = 0; l < P; l += 2)
+      for (int m = 0; m < P; ++m)
+        if (2 * m != b * (P - 1) + l && (opv(b, l, m, 0) != 0.0 || opv(b, l, m, 1) != 0.0)) return {};
+  return fr;
+}
+
 template <int P>
 static const double* device_fragments(cudaError_t* err) {
   static std::mutex mu;
@@ -1185,7 +1431,7 @@ static const double* device_fragments(cudaError_t* err) {
   std::lock_guard<std::mutex> lock(mu);
   auto it = cache.find(dev);
   if (it != cache.end()) return it->second;
-  std::vector<double> fr = sym_fragments<P>();
+  std::vector<double> fr = UseSym<P>::v ? sym_fragments<P>() : direct_fragments5();
   if (fr.empty()) {  // the operator tables lack the symmetry / delta structure of the split
     *err = cudaErrorInvalidValue;
     return nullptr;
@@ -1396,7 +1642,7 @@ static cudaError_t persistent_grid(K kernel, int threads, size_t smem, int* grid
 template <int D, int P, int G, int NC, int NST, int MB, typename E, bool FUSED, bool BATCH, bool F2>
 static cudaError_t launch_ws(const sft_plan_s* Pl, const TransArgs& a, const LevelDims& L, int64_t work) {
   constexpr int PS = StrideT<E, Pow<P, D>::v>::v;
-  const size_t smem = (size_t)NST * G * (1 << D) * PS * sizeof(E);
+  const size_t smem = (size_t)(NST * G * (1 << D) + 1) * PS * sizeof(E);  // stage ring + zero slot
   auto kern = k_translate_ws<D, P, G, NC, NST, MB, E, FUSED, BATCH, F2>;
   static PerDevice<int> grid_cache;  // this instantiation's grid and smem opt-in, per device
   int grid_max = 0;
