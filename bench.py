@@ -52,6 +52,32 @@ def measured_peaks():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def fp64_peak():
+    """FP64 tensor-core (DMMA m8n8k4) peak measured on this pool's B200 with
+    scripts/fp64_peak.cu (profiles/r1_fp64_peak.json; MEASURED_PEAKS.json has
+    no FP64 entry): 36.85 TF/s at 1.96 GHz.  DFMA reaches 34-39 TF/s on the same
+    datapath (mixed DMMA + DFMA: 32.4 TF/s total)."""
+    path = os.path.join(ROOT, "profiles", "r1_fp64_peak.json")
+    try:
+        for line in open(path):
+            d = json.loads(line)
+            if d.get("test") == "dmma_m8n8k4":
+                return float(d["tflops"]), "measured (profiles/r1_fp64_peak.json, DMMA m8n8k4)"
+    except OSError:
+        pass
+    return 37.2, "nominal (148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz)"
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 # ---------------------------------------------------------------------------
 # clocks sampler (nvidia-smi during the timed region)
 # ---------------------------------------------------------------------------
@@ -241,6 +267,7 @@ def run_ours(args):
             kt.append(plan.last_timing())
         plan.set_timing(False)
         st = plan.stats()
+        work = plan.work()
         # multi-RHS apply (sft_apply_batch): args.nrhs
         # charge vectors through the plan, one launch per step for all of them;
         # skipped when the batch's level buffers would not fit comfortably
@@ -333,7 +360,14 @@ def run_ours(args):
                 traffic = json.load(open(tf)).get("dram_bytes_per_launch")
             n2 = sum(1 for _, f2 in st.get("launches", []) if f2)
             kname = "k_translate_ws (one launch per level" + (f", {n2} two-level launch)" if n2 else ")")
-            roof = {"bound": "hbm", "kernel": kname, "achieved": round(achieved, 1),
+            f64p, f64src = fp64_peak()
+            fl = work["fp64_flops"]
+            fp64 = {"achieved": round(fl / (trans_ms / 1e3) / 1e12, 3), "peak": f64p, "unit": "TFLOP/s",
+                    "frac": round(fl / (trans_ms / 1e3) / 1e12 / f64p, 4), "flops_per_apply": fl,
+                    "supertiles": work["supertiles"], "peak_source": f64src,
+                    "note": "FP64 flops the translation kernels execute (DMMA tiles whole incl. padding, plus "
+                            "DADD/DMUL/DFMA; counted from the tile schedules, sft_plan_work) / translate ms"}
+            roof = {"bound": "hbm", "kernel": kname, "achieved": round(achieved, 1), "fp64": fp64,
                     "peak": hbm_peak, "unit": "GB/s", "frac": round(achieved / hbm_peak, 4), "traffic": traffic,
                     "peak_source": peak_src,
                     "alg_bytes_per_launch": bytes_per_launch, "launches_per_apply": nlaunch,
@@ -392,32 +426,107 @@ def run_ours(args):
     return res, w
 
 
-def cpu_baseline(w, nthreads=0, sample="full", u_gpu=None):
-    """The oracle butterfly (as it stands) on the host cores.  With the GPU's
-    result u_gpu it also returns the accuracy of the GPU run (BASELINE.json's
-    metric includes the relative L2 error vs the direct sum): vs the oracle
-    butterfly on every target and vs the oracle direct sum on the seeded error
-    sample (1024 targets for C2/C4, BASELINE.json:9,11; all targets otherwise)."""
+def cpu_baseline(w, nthreads=0, u_gpu=None):
+    """The oracle (as it stands) on the host cores: the full oracle butterfly
+    (the reported baseline), and the oracle direct sum on the seeded error
+    sample, timed, with T_d -- the direct sum over all n_x targets -- estimated
+    by scaling with n_x / sample size as the paper does (PAPER.md:383-389,
+    "T_d ... estimated").  With the GPU's result u_gpu it also returns the
+    accuracy of the benched run (BASELINE.json's metric includes the relative
+    L2 error vs the direct sum): vs the oracle direct sum on the error sample
+    (1024 seeded targets for C2/C4, BASELINE.json:9,11; all targets otherwise)
+    and vs the oracle butterfly on every target."""
     import oracle
     nth = nthreads or oracle.max_threads()
     t0 = time.perf_counter()
-    if sample != "full":
-        raise ValueError(sample)
     ub = oracle.butterfly(w.x, w.k, w.f, w.N, w.p, nthreads=nth)
     dt = time.perf_counter() - t0
+    tg = w.sample if len(w.x) > 20000 else None
+    t1 = time.perf_counter()
+    ud = oracle.direct(w.x, w.k, w.f, w.N, targets=tg, nthreads=nth)
+    dd = time.perf_counter() - t1
+    t_d = dd * len(w.x) / len(ud)
     out = {"value": round(w.P / dt / 1e6, 6), "unit": "Mpoints/s", "cores": nth, "kind": "oracle",
+           "cpu_model": cpu_model(),
            "sample": f"full {w.name} workload, one oracle butterfly (long double, OpenMP)",
-           "seconds": round(dt, 3)}
+           "seconds": round(dt, 3),
+           "direct": {"targets": int(len(ud)), "seconds": round(dd, 3), "t_d_estimated_s": round(t_d, 2),
+                      "note": "oracle direct sum (long double) on the error sample, T_d scaled by n_x / targets "
+                              "(PAPER.md:386-389)"}}
     acc = None
     if u_gpu is not None:
         tol = {5: 5e-2, 7: 1e-3, 9: 1e-5}[w.p]
-        tg = w.sample if len(w.x) > 20000 else None
-        ud = oracle.direct(w.x, w.k, w.f, w.N, targets=tg, nthreads=nth)
         ug = u_gpu if tg is None else u_gpu[tg]
+        rms = lambda r: float(np.sqrt(np.mean(np.abs(r) ** 2)))  # noqa: E731
         acc = {"rel_l2_vs_direct": float(oracle.rel_l2(ug, ud)),
+               "max_rel_vs_direct": float(np.max(np.abs(ug - ud)) / rms(ud)),
                "direct_targets": int(len(ud)), "direct_tol": tol,
-               "rel_l2_vs_oracle_butterfly": float(oracle.rel_l2(u_gpu, ub)), "parity_tol": 1e-10}
+               "rel_l2_vs_oracle_butterfly": float(oracle.rel_l2(u_gpu, ub)),
+               "max_rel_vs_oracle_butterfly": float(np.max(np.abs(u_gpu - ub)) / rms(ub)), "parity_tol": 1e-10}
     return out, acc
+
+
+def configs_block(steps=5, warmup=3):
+    """Every BASELINE config (C0-C4) on this GPU: plan+apply step and apply
+    time (CUDA events, L2 flushed), translation time and its HBM / FP64
+    roofline fractions, and the relative L2 error vs the oracle direct sum on
+    the seeded error sample (all targets for C0/C1; 1024 seeded targets for
+    C2-C4 -- C3's all-target error is in tests/test_gpu_parity.py)."""
+    import torch
+    import oracle
+    import paper_0801_1524_b200 as sft
+    dev = torch.device("cuda", torch.cuda.current_device())
+    stream = torch.cuda.current_stream(dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    hbm, _ = measured_peaks()
+    f64p, _ = fp64_peak()
+    out = {}
+    for name in ("C0", "C1", "C2", "C3", "C4"):
+        w = synth.make_workload(name)
+        x = torch.from_numpy(w.x).to(dev); k = torch.from_numpy(w.k).to(dev); f = torch.from_numpy(w.f).to(dev)
+        u = torch.empty(len(w.x), dtype=torch.complex128, device=dev)
+
+        def step():
+            with sft.Plan(w.dim, w.N, w.p, x, k, stream=stream) as pl:
+                pl.apply(f, u)
+
+        def timed(fn):
+            ms = []
+            for _ in range(steps):
+                flush.zero_()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream); fn(); b.record(stream)
+                torch.cuda.synchronize(dev)
+                ms.append(a.elapsed_time(b))
+            return float(np.median(ms))
+        for _ in range(warmup):
+            step()
+        step_ms = timed(step)
+        pl = sft.Plan(w.dim, w.N, w.p, x, k, stream=stream)
+        for _ in range(2):
+            pl.apply(f, u)
+        apply_ms = timed(lambda: pl.apply(f, u))
+        pl.set_timing(True)
+        tr = []
+        for _ in range(3):
+            flush.zero_()
+            pl.apply(f, u)
+            torch.cuda.synchronize(dev)
+            tr.append(pl.last_timing()["trans_ms"])
+        trans_ms = float(np.median(tr))
+        wk = pl.work()
+        pl.close()
+        ug = u.cpu().numpy()
+        tg = synth.error_sample(len(w.x), w.seed) if len(w.x) > 20000 else None
+        ud = oracle.direct(w.x, w.k, w.f, w.N, targets=tg)
+        ugs = ug if tg is None else ug[tg]
+        out[name] = {"step_ms": round(step_ms, 4), "mpoints_s": round(w.P / step_ms / 1e3, 3),
+                     "apply_ms": round(apply_ms, 4), "translate_ms": round(trans_ms, 4),
+                     "hbm_frac": round(wk["alg_bytes"] / (trans_ms / 1e3) / 1e9 / hbm, 4),
+                     "fp64_frac": round(wk["fp64_flops"] / (trans_ms / 1e3) / 1e12 / f64p, 4),
+                     "rel_l2_vs_direct": float(oracle.rel_l2(ugs, ud)), "direct_targets": int(len(ud))}
+        del x, k, f, u
+    return out
 
 
 def _pairs(w, targets=None):
@@ -440,7 +549,8 @@ def run_reference(args):
     import oracle
     w = synth.make_workload(args.config)
     nth = oracle.max_threads()
-    tg = w.sample[: args.ref_targets]
+    step = max(1, len(w.sample) // args.ref_targets)
+    tg = w.sample[::step][: args.ref_targets]  # spread over the whole curve / surface
     frac = _pairs(w, tg) / _pairs(w)
 
     def step():
@@ -454,8 +564,10 @@ def run_reference(args):
     dt = (time.perf_counter() - t0) / args.steps
     # full-workload equivalent: the oracle's cost is proportional to the pairs it visits
     value = w.P * frac / dt / 1e6
-    desc = (f"oracle butterfly on {w.name} restricted to {len(tg)} seeded targets (all sources): "
-            f"{frac:.4f} of the pairs; value = P * frac / step time")
+    desc = (f"oracle butterfly on {w.name} restricted to {len(tg)} seeded targets spread over the workload (all "
+            f"sources): {frac:.4f} of the pairs; value = P * frac / step time.  The restricted run is cheaper per "
+            f"pair than the full one (round 1 on C2: 0.0141 vs 0.0067 Mpoints/s for the full oracle in "
+            f"cpu_baseline), so this overstates the oracle ~2x")
     return {
         "impl": "reference",
         "metric": "butterfly SFT Mpoints/s (P=max(nx,nk) per plan+apply step)",
@@ -486,6 +598,7 @@ def main():
     ap.add_argument("--config", default="C2", choices=sorted(CONFIG_DESC))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="skip the per-config block (C0-C4 on this GPU)")
     ap.add_argument("--ref-targets", type=int, default=256)
     ap.add_argument("--exchange", default="nccl", choices=["nccl", "fused", "torch"],
                     help="N > 1: level-m exchange and u all-gather by libsft's own NCCL calls (default), fused into "
@@ -522,6 +635,8 @@ def main():
             res["cpu_baseline"], acc = cpu_baseline(w, u_gpu=res.get("_u"))
             if acc is not None:
                 res["accuracy"] = acc
+        if res["n_gpus"] == 1 and not args.no_cpu_baseline and not args.no_configs:
+            res["configs"] = configs_block()
         res.pop("_u", None)
         print(json.dumps(res), flush=True)
 

@@ -150,6 +150,17 @@ const char* sft_last_error(void);
  *               groups total, translation algorithmic bytes per apply. */
 int sft_plan_stats(sft_plan_t plan, int64_t* counts_x, int64_t* counts_k, int64_t* pairs, double* info);
 
+/* Work model of one sft_apply's translation step (host, caller-allocated [6];
+ * synchronises the plan stream once; diagnostics for the roofline):
+ *   w[0] algorithmic bytes: every pair array written once at its level and
+ *        read once at the next (the level-synchronous schedule)
+ *   w[1] FP64 flops the translation kernels execute (DMMA m8n8k4 tiles
+ *        counted whole, padding included, plus the DADD/DMUL/DFMA of the
+ *        delta columns, sum/difference and tail), from the tile schedules
+ *   w[2] 8-fiber super-tiles, w[3] fiber tasks, w[4] groups (A', B),
+ *   w[5] pairs (A, B) over all levels. */
+int sft_plan_work(sft_plan_t plan, double* w);
+
 /* Translation launches of sft_apply (host, caller-allocated [L] arrays or NULL):
  * *n launches in order; out_level[i] = the level t the launch writes;
  * two_level[i] = 1 if it is a two-level (radix-4) launch computing levels t+1

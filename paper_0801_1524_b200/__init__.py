@@ -99,6 +99,7 @@ def lib():
     L.sft_operator_tables.argtypes = [ctypes.c_int, _c_dp, _c_dp, _c_dp, _c_dp]
     L.sft_launch_count.argtypes = [_c_i64p]
     L.sft_nccl_unique_id.argtypes = [ctypes.c_char_p]
+    L.sft_plan_work.argtypes = [vp, _c_dp]
     L.sft_nccl_release.argtypes = [ctypes.c_char_p]
     _lib = L
     return L
@@ -313,6 +314,12 @@ class Plan:
         _check(lib().sft_translation_launches(self._h, ctypes.byref(nl), lv, f2))
         d.update(launches=[(int(lv[i]), bool(f2[i])) for i in range(nl.value)])
         return d
+
+    def work(self):
+        """sft_plan_work: work model of one apply's translation step."""
+        w = np.zeros(6)
+        _check(lib().sft_plan_work(self._h, w.ctypes.data_as(_c_dp)))
+        return dict(alg_bytes=w[0], fp64_flops=w[1], supertiles=w[2], tasks=w[3], groups=w[4], pairs=w[5])
 
     def set_timing(self, on=True):
         _check(lib().sft_set_timing(self._h, 1 if on else 0))

@@ -1365,6 +1365,39 @@ extern "C" int sft_schedule_bytes(sft_plan_t P, int t, int64_t* bytes, void* dst
   return SFT_OK;
 }
 
+extern "C" int sft_plan_work(sft_plan_t P, double* w) {
+  if (!P || !w) return fail(SFT_E_ARG, "NULL argument");
+  const int L = P->L;
+  const int64_t PD = ipow64(P->p, P->d);
+  double groups = 0, bytes = 0, pairs = 0;
+  for (int t = 0; t < L; ++t) {
+    groups += (double)P->K.counts[t] * P->X.counts[L - t - 1];
+    bytes += (P->prec == 1 ? 8.0 : 16.0) * PD *
+             ((double)P->K.counts[t] * P->X.counts[L - t] + (double)P->K.counts[t + 1] * P->X.counts[L - t - 1]);
+  }
+  for (int t = 0; t <= L; ++t) pairs += (double)P->K.counts[t] * P->X.counts[L - t];
+  double acc[3] = {0, 0, 0};
+  if (P->sched) {
+    std::vector<unsigned char> h;
+    if (P->sched_ready) CKR(cudaStreamWaitEvent(P->stream, P->sched_ready, 0));
+    for (int t = 0; t < L; ++t) {
+      const size_t n = P->sched_off[t + 1] - P->sched_off[t];
+      if (!n) continue;
+      h.resize(n);
+      CKR(cudaMemcpyAsync(h.data(), P->sched + P->sched_off[t], n, cudaMemcpyDeviceToHost, P->stream));
+      CKR(cudaStreamSynchronize(P->stream));
+      schedule_work(P, h.data(), n, acc);
+    }
+  }
+  w[0] = bytes;
+  w[1] = acc[2];
+  w[2] = acc[0];
+  w[3] = acc[1];
+  w[4] = groups;
+  w[5] = pairs;
+  return SFT_OK;
+}
+
 extern "C" int sft_translation_launches(sft_plan_t P, int* n, int* out_level, int* two_level) {
   if (!P || !n) return fail(SFT_E_ARG, "NULL argument");
   const int nl = (int)P->launch_t.size();

@@ -185,6 +185,9 @@ cudaError_t launch_leaf(const sft_plan_s* P, const double2* f, void* out, int64_
 cudaError_t launch_translate(const sft_plan_s* P, const LevelDims& L, const void* in, void* out);
 // two-level launches available for this plan (2D FP64 single-GPU; SFT_F2=0 disables)
 bool two_level_supported(const sft_plan_s* P);
+// work of one translation launch from a host copy of its tile schedule:
+// out[0] += super-tiles, out[1] += fiber tasks, out[2] += executed FP64 flops
+void schedule_work(const sft_plan_s* P, const unsigned char* h, size_t bytes, double* out);
 // tile schedule of one level (sizes and builder; 0 bytes when the kernel needs none)
 size_t schedule_bytes(const sft_plan_s* P, const LevelDims& L);
 // builds the schedules of nlev levels (dims L[i], destination dst[i]) in one launch

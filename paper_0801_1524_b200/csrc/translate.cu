@@ -1780,6 +1780,62 @@ cudaError_t launch_schedule(const sft_plan_s* Pl, const LevelDims* L, int nlev, 
   return cudaSuccess;
 }
 
+// FP64 flops one warp executes per 8-fiber super-tile (DMMA m8n8k4: 512 flops
+// incl. padding; DADD / DMUL: 32, DFMA: 64 per warp instruction), counted
+// from sym_math / direct_math (NSUB = 1 code; NSUB only interleaves):
+//   symmetric p = 7: 4 DMMA, 16 DADD, 8 DMUL, 8 DFMA
+//   symmetric p = 9: 4 DMMA, 27 DADD, 12 DMUL, 12 DFMA (centre tail)
+//   direct    p = 5: 2 DMMA, 11 DADD, 8 DMUL, 8 DFMA (tail)
+static double flops_per_supertile(int p) {
+  if (p == 5) return 2 * 512 + 11 * 32 + 8 * 32 + 8 * 64;
+  if (p == 7) return 4 * 512 + 16 * 32 + 8 * 32 + 8 * 64;
+  return 4 * 512 + 27 * 32 + 12 * 32 + 12 * 64;
+}
+
+template <int D, int P, int G>
+static void schedule_work_g(const unsigned char* h, size_t bytes, int nb, double* out) {
+  using SC = Sched<D, P, G>;
+  constexpr int PF = Pow<P, D>::v / P;
+  const size_t blk = (size_t)SC::BLK;
+  double st = 0, tasks = 0;
+  for (size_t o = 0; o + blk <= bytes; o += blk) {
+    const int* cnt = reinterpret_cast<const int*>(h + o);
+    for (int l = 0; l < SC::NL; ++l) {
+      const int nt = cnt[3 * l] + cnt[3 * l + 1] + cnt[3 * l + 2];
+      tasks += nt;
+      st += (nt * PF + 7) / 8;
+    }
+  }
+  (void)nb;
+  out[0] += st;
+  out[1] += tasks;
+  out[2] += st * flops_per_supertile(P);
+}
+
+// Work of one translation launch from its tile schedule (host copy): out[0]
+// super-tiles, out[1] fiber tasks, out[2] executed FP64 flops (accumulated).
+void schedule_work(const sft_plan_s* Pl, const unsigned char* h, size_t bytes, double* out) {
+  if (Pl->prec == 1) {
+    switch (Pl->d * 10 + Pl->p) {
+      case 25: return schedule_work_g<2, 5, F32WsCfg<2, 5>::G>(h, bytes, 1, out);
+      case 27: return schedule_work_g<2, 7, F32WsCfg<2, 7>::G>(h, bytes, 1, out);
+      case 29: return schedule_work_g<2, 9, F32WsCfg<2, 9>::G>(h, bytes, 1, out);
+      case 35: return schedule_work_g<3, 5, F32WsCfg<3, 5>::G>(h, bytes, 1, out);
+      case 37: return schedule_work_g<3, 7, F32WsCfg<3, 7>::G>(h, bytes, 1, out);
+      case 39: return schedule_work_g<3, 9, F32WsCfg<3, 9>::G>(h, bytes, 1, out);
+    }
+    return;
+  }
+  switch (Pl->d * 10 + Pl->p) {
+    case 25: return schedule_work_g<2, 5, WsCfg<2, 5>::G>(h, bytes, 1, out);
+    case 27: return schedule_work_g<2, 7, WsCfg<2, 7>::G>(h, bytes, 1, out);
+    case 29: return schedule_work_g<2, 9, WsCfg<2, 9>::G>(h, bytes, 1, out);
+    case 35: return schedule_work_g<3, 5, WsCfg<3, 5>::G>(h, bytes, 1, out);
+    case 37: return schedule_work_g<3, 7, WsCfg<3, 7>::G>(h, bytes, 1, out);
+    case 39: return schedule_work_g<3, 9, WsCfg<3, 9>::G>(h, bytes, 1, out);
+  }
+}
+
 bool two_level_supported(const sft_plan_s* Pl) {
   if (Pl->prec != 0 || Pl->sharded) return false;
   const char* e = getenv("SFT_F2");
