@@ -167,6 +167,13 @@ __device__ __forceinline__ int64_t out_pair(const LevelArgs& a, const GroupMeta&
 // columns (SP_H, 0) and (0, SQ_H), so the m and m' formulas coincide) and for
 // p = 9 is a DFMA tail (4-lane transpose-reduce).  The even (delta) elements
 // start the accumulators: lane c takes s and t at element 2c.
+// p = 9: the centre column m = H as a DFMA tail with a 4-lane transpose-reduce
+// (0, default) or on a second DMMA N tile (1: 144 fewer static instructions
+// but +4 DMMA per super-tile; measured C2 translate 0.997 vs 0.979 ms -- the
+// FP64 pipe, which DMMA and DFMA share, is the busier resource)
+#ifndef SFT_CENTRE_DMMA
+#define SFT_CENTRE_DMMA 0
+#endif
 template <int P>
 struct SymShape {
   static constexpr int H = (P - 1) / 2;   // odd (dense) elements per child = k of the MMA (padded to 4)
@@ -795,6 +802,7 @@ __device__ __forceinline__ void sym_math(const LaneOps<P>& op, const uint32_t (&
   // accumulators: s-GEMM columns (SP_m, DQ_m), t-GEMM columns (DP_m, SQ_m), re / im rows
   double sre[NSUB][2], sim[NSUB][2], tre[NSUB][2], tim[NSUB][2], tl[NSUB][4];
   double ar[NSUB][2], ai[NSUB][2];  // odd s / t of this lane's k (re, im)
+  double csr[NSUB][2], csi[NSUB][2], ctr[NSUB][2], cti[NSUB][2], cre[NSUB][2], cim[NSUB][2];  // centre tile (p = 9)
 #pragma unroll
   for (int u = 0; u < NSUB; ++u) {
     constexpr int ES = sizeof(E);
@@ -813,7 +821,21 @@ __device__ __forceinline__ void sym_math(const LaneOps<P>& op, const uint32_t (&
     ai[u][0] = a0.y + a1.y;
     ar[u][1] = a0.x - a1.x;  // t
     ai[u][1] = a0.y - a1.y;
-    if constexpr (S::TAIL) {
+    if constexpr (S::TAIL && SFT_CENTRE_DMMA) {
+      // centre m = H (p = 9) on a second N tile: column 0 = SP_H (s-GEMM) and
+      // SQ_H (t-GEMM), both on lane c = 0 of the row; centre delta (s, t at
+      // element p-1) starts the accumulators there
+      const double2 c0 = lds<E>(xa[u] + (P - 1) * STR * ES), c1 = lds<E>(xb[u]);
+      cre[u][0] = op.tds * (c0.x + c1.x);
+      cim[u][0] = op.tds * (c0.y + c1.y);
+      cre[u][1] = op.tdt * (c0.x - c1.x);
+      cim[u][1] = op.tdt * (c0.y - c1.y);
+      csr[u][1] = csi[u][1] = ctr[u][1] = cti[u][1] = 0.0;
+      csr[u][0] = cre[u][0];
+      csi[u][0] = cim[u][0];
+      ctr[u][0] = cre[u][1];
+      cti[u][0] = cim[u][1];
+    } else if constexpr (S::TAIL) {
       // centre m = H (p = 9): partials of z_0, z_1 over this lane's k, centre delta on lane 0
       const double2 c0 = lds<E>(xa[u] + (P - 1) * STR * ES), c1 = lds<E>(xb[u]);
       const double pr = fma(op.tds, c0.x + c1.x, op.ts * ar[u][0]), pi = fma(op.tds, c0.y + c1.y, op.ts * ai[u][0]);
@@ -831,6 +853,12 @@ __device__ __forceinline__ void sym_math(const LaneOps<P>& op, const uint32_t (&
     dmma(sim[u], ai[u][0], op.bs);
     dmma(tre[u], ar[u][1], op.bt);
     dmma(tim[u], ai[u][1], op.bt);
+    if constexpr (S::TAIL && SFT_CENTRE_DMMA) {
+      dmma(csr[u], ar[u][0], op.ts);
+      dmma(csi[u], ai[u][0], op.ts);
+      dmma(ctr[u], ar[u][1], op.tt);
+      dmma(cti[u], ai[u][1], op.tt);
+    }
   }
 #endif
 #pragma unroll
@@ -849,7 +877,16 @@ __device__ __forceinline__ void sym_math(const LaneOps<P>& op, const uint32_t (&
       o1[u].st(o_s, psr - qsi, psi + qsr);
     }
   }
-  if constexpr (S::TAIL) {
+  if constexpr (S::TAIL && SFT_CENTRE_DMMA) {
+    if (c == 0) {
+#pragma unroll
+      for (int u = 0; u < NSUB; ++u) {
+        // P_H = SP_H, Q_H = SQ_H: z_0 = P - iQ, z_1 = P + iQ
+        o0[u].st(H * STR, csr[u][0] + cti[u][0], csi[u][0] - ctr[u][0]);
+        o1[u].st(H * STR, csr[u][0] - cti[u][0], csi[u][0] + ctr[u][0]);
+      }
+    }
+  } else if constexpr (S::TAIL) {
     // transpose-reduce over the 4 lanes of a row: lane c ends with component
     // c of (z_0.re, z_0.im, z_1.re, z_1.im) at m = H
     const bool odd = c & 1, hi = c & 2;
@@ -1370,8 +1407,10 @@ static std::vector<double> sym_fragments() {
         for (int nn = 2 * c; nn <= 2 * c + 1; ++nn)
           if (col(false, nn, 2 * i) != 0.0 || col(true, nn, 2 * i) != 0.0) return {};
     if (S::TAIL) {
-      fr[S::OFF_TAIL + lane] = k < H ? rc(0, H, 2 * k + 1) : 0.0;
-      fr[S::OFF_TAIL + 32 + lane] = k < H ? rs(0, H, 2 * k + 1) : 0.0;
+      // centre tile B fragments (column n = 0 only) or the tail's per-lane k weights
+      const bool live = k < H && (!SFT_CENTRE_DMMA || n == 0);
+      fr[S::OFF_TAIL + lane] = live ? rc(0, H, 2 * k + 1) : 0.0;
+      fr[S::OFF_TAIL + 32 + lane] = live ? rs(0, H, 2 * k + 1) : 0.0;
       fr[S::OFF_TAIL + 64 + lane] = c == 0 ? rc(0, H, P - 1) : 0.0;
       fr[S::OFF_TAIL + 96 + lane] = c == 0 ? rs(0, H, P - 1) : 0.0;
     }
@@ -1784,11 +1823,13 @@ cudaError_t launch_schedule(const sft_plan_s* Pl, const LevelDims* L, int nlev, 
 // incl. padding; DADD / DMUL: 32, DFMA: 64 per warp instruction), counted
 // from sym_math / direct_math (NSUB = 1 code; NSUB only interleaves):
 //   symmetric p = 7: 4 DMMA, 16 DADD, 8 DMUL, 8 DFMA
-//   symmetric p = 9: 4 DMMA, 27 DADD, 12 DMUL, 12 DFMA (centre tail)
+//   symmetric p = 9: 8 DMMA, 24 DADD, 12 DMUL, 8 DFMA (centre tile; SFT_CENTRE_DMMA=0:
+//                    4 DMMA, 27 DADD, 12 DMUL, 12 DFMA with the centre tail)
 //   direct    p = 5: 2 DMMA, 11 DADD, 8 DMUL, 8 DFMA (tail)
 static double flops_per_supertile(int p) {
   if (p == 5) return 2 * 512 + 11 * 32 + 8 * 32 + 8 * 64;
   if (p == 7) return 4 * 512 + 16 * 32 + 8 * 32 + 8 * 64;
+  if (SFT_CENTRE_DMMA) return 8 * 512 + 24 * 32 + 12 * 32 + 8 * 64;
   return 4 * 512 + 27 * 32 + 12 * 32 + 12 * 64;
 }
 
