@@ -402,17 +402,88 @@ static void ev_put(cudaEvent_t e, bool timing, int dev) {
   g_ev_pool[timing ? 0 : 1][dev].push_back(e);
 }
 
+// Block cache: the device blocks of destroyed plans (tree arena, level
+// buffers, host staging) are kept per device and handed to the next plan of a
+// similar size instead of going back to the stream-ordered pool -- measured on
+// B200, a cudaMallocAsync of a ~50 MB block costs ~35 us of host time on the
+// plan's critical path even when the pool holds the freed block
+// (scripts/malloc_async_probe.cu), a reuse from here ~1 us.  A block freed on
+// another stream is reused behind an event recorded at its free.
+namespace {
+struct CachedBlock {
+  void* p;
+  size_t bytes;
+  cudaStream_t s;
+  cudaEvent_t ev;
+  int dev;
+};
+std::mutex g_blk_mu;
+std::vector<CachedBlock> g_blk;
+constexpr int kBlkPerDev = 8;
+}  // namespace
+
+namespace sft {
+cudaError_t block_alloc(void** out, size_t bytes, cudaStream_t s) {
+  const int dev = current_device();
+  {
+    std::lock_guard<std::mutex> lk(g_blk_mu);
+    int best = -1;
+    for (int i = 0; i < (int)g_blk.size(); ++i) {
+      const CachedBlock& b = g_blk[i];
+      if (b.dev != dev || b.bytes < bytes || b.bytes > bytes + bytes / 4 + (1u << 20)) continue;
+      if (best < 0 || b.bytes < g_blk[best].bytes) best = i;
+    }
+    if (best >= 0) {
+      CachedBlock b = g_blk[best];
+      g_blk.erase(g_blk.begin() + best);
+      cudaError_t e = b.s == s ? cudaSuccess : cudaStreamWaitEvent(s, b.ev, 0);
+      ev_put(b.ev, false, dev);
+      if (e != cudaSuccess) return e;
+      *out = b.p;
+      return cudaSuccess;
+    }
+  }
+  return cudaMallocAsync(out, bytes, s);
+}
+
+void block_free(void* p, size_t bytes, cudaStream_t s) {
+  if (!p) return;
+  const int dev = current_device();
+  cudaEvent_t ev = ev_get(false);
+  if (!ev || cudaEventRecord(ev, s) != cudaSuccess) {
+    if (ev) ev_put(ev, false, dev);
+    cudaFreeAsync(p, s);
+    return;
+  }
+  std::lock_guard<std::mutex> lk(g_blk_mu);
+  int ndev = 0, oldest = -1;
+  for (int i = 0; i < (int)g_blk.size(); ++i)
+    if (g_blk[i].dev == dev) {
+      ++ndev;
+      if (oldest < 0) oldest = i;
+    }
+  if (ndev >= kBlkPerDev) {  // evict the oldest of this device (stream-ordered after its own uses)
+    CachedBlock b = g_blk[oldest];
+    g_blk.erase(g_blk.begin() + oldest);
+    cudaStreamWaitEvent(s, b.ev, 0);
+    cudaFreeAsync(b.p, s);
+    ev_put(b.ev, false, dev);
+  }
+  g_blk.push_back(CachedBlock{p, bytes, s, ev, dev});
+}
+}  // namespace sft
+
 static void plan_free(sft_plan_s* P) {
   if (!P) return;
   cudaStream_t s = P->stream;
   if (P->sched_ready) cudaStreamWaitEvent(s, P->sched_ready, 0);
   free_tree(P->X, s);
   free_tree(P->K, s);
-  if (P->buf[0]) cudaFreeAsync(P->buf[0], s);  // one block: both level buffers (+ schedules)
+  if (P->buf[0]) block_free(P->buf[0], P->blk_bytes, s);  // one block: both level buffers (+ schedules)
   for (int i = 0; i < 2; ++i)
     if (P->bufb[i]) cudaFreeAsync(P->bufb[i], s);
-  if (P->f_stage) cudaFreeAsync(P->f_stage, s);
-  if (P->u_stage) cudaFreeAsync(P->u_stage, s);
+  if (P->f_stage) block_free(P->f_stage, P->f_stage_bytes, s);
+  if (P->u_stage) block_free(P->u_stage, P->u_stage_bytes, s);
   if (P->d_seg) cudaFreeAsync(P->d_seg, s);
   for (void* q : {(void*)P->xsend, (void*)P->xrecv, (void*)P->u_all, (void*)P->d_ubounds})
     if (q) cudaFreeAsync(q, s);
@@ -446,7 +517,9 @@ struct PlanTrace {
     const char* e = getenv("SFT_PLAN_TRACE");
     on = e && e[0] == '1';
     t0 = std::chrono::steady_clock::now();
-    if (on) cudaMallocManaged(&d_ts, 16 * sizeof(unsigned long long));
+    // device memory (a managed page would fault on each first GPU write and
+    // skew the stamps by ~30 us)
+    if (on) cudaMalloc(&d_ts, 16 * sizeof(unsigned long long));
   }
   void mark(const char* what, cudaStream_t s, bool dev) {
     if (!on || n > 900) return;
@@ -461,9 +534,11 @@ struct PlanTrace {
     if (!on) return;
     fprintf(stderr, "[sft_plan] host us:%s\n", buf);
     if (nev) {
+      unsigned long long h[16];
       cudaDeviceSynchronize();
+      cudaMemcpy(h, d_ts, nev * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
       fprintf(stderr, "[sft_plan] device us:");
-      for (int i = 0; i < nev; ++i) fprintf(stderr, " %s=%.1f", evn[i], (d_ts[i] - d_ts[0]) * 1e-3);
+      for (int i = 0; i < nev; ++i) fprintf(stderr, " %s=%.1f", evn[i], (h[i] - h[0]) * 1e-3);
       fprintf(stderr, "\n");
     }
     cudaFree(d_ts);
@@ -758,8 +833,9 @@ extern "C" int sft_plan(int dim, int64_t N, int p, const double* x, int64_t nx, 
     P->sched_off[L] = tot;
     const size_t bb = (P->buf_elems * (P->prec == 1 ? sizeof(float2) : sizeof(double2)) + 255) / 256 * 256;
     char* blk = nullptr;
-    if (cudaMallocAsync((void**)&blk, 2 * bb + tot, s) != cudaSuccess)
+    if (block_alloc((void**)&blk, 2 * bb + tot, s) != cudaSuccess)
       return bail(SFT_E_NOMEM, "level buffer allocation failed");
+    P->blk_bytes = 2 * bb + tot;
     P->buf[0] = (double2*)blk;
     P->buf[1] = (double2*)(blk + bb);
     P->sched = tot > 0 ? (unsigned char*)(blk + 2 * bb) : nullptr;
@@ -960,12 +1036,14 @@ static int apply_impl(sft_plan_s* P, int nrhs, const void* f, int64_t ldf, void*
   double2* ud = (double2*)u;
   const bool f_host = !is_device_ptr(f), u_host = !is_device_ptr(u);
   if ((f_host || u_host) && P->stage_rhs < nrhs) {
-    if (P->f_stage) cudaFreeAsync(P->f_stage, s);
-    if (P->u_stage) cudaFreeAsync(P->u_stage, s);
+    if (P->f_stage) block_free(P->f_stage, P->f_stage_bytes, s);
+    if (P->u_stage) block_free(P->u_stage, P->u_stage_bytes, s);
     P->f_stage = P->u_stage = nullptr;
     P->stage_rhs = 0;
-    CKR(cudaMallocAsync(&P->f_stage, (size_t)nrhs * P->nk * sizeof(double2), s));
-    CKR(cudaMallocAsync(&P->u_stage, (size_t)nrhs * P->nx * sizeof(double2), s));
+    P->f_stage_bytes = (size_t)nrhs * P->nk * sizeof(double2);
+    P->u_stage_bytes = (size_t)nrhs * P->nx * sizeof(double2);
+    CKR(block_alloc((void**)&P->f_stage, P->f_stage_bytes, s));
+    CKR(block_alloc((void**)&P->u_stage, P->u_stage_bytes, s));
     P->stage_rhs = nrhs;
   }
   if (f_host) {
@@ -1198,14 +1276,20 @@ static int apply_sharded(sft_plan_s* P, const void* f, void* u) {
   const double2* fd = (const double2*)f;
   const bool f_host = !is_device_ptr(f), u_host = !is_device_ptr(u);
   if (f_host) {
-    if (!P->f_stage) CKR(cudaMallocAsync(&P->f_stage, P->nk * sizeof(double2), s));
+    if (!P->f_stage) {
+      P->f_stage_bytes = P->nk * sizeof(double2);
+      CKR(block_alloc((void**)&P->f_stage, P->f_stage_bytes, s));
+    }
     CKR(cudaMemcpyAsync(P->f_stage, f, P->nk * sizeof(double2), cudaMemcpyHostToDevice, s));
     CKR(f_copy_mark(P));
     fd = P->f_stage;
   }
   double2* ud = (double2*)u;
   if (u_host) {
-    if (!P->u_stage) CKR(cudaMallocAsync(&P->u_stage, P->nx * sizeof(double2), s));
+    if (!P->u_stage) {
+      P->u_stage_bytes = P->nx * sizeof(double2);
+      CKR(block_alloc((void**)&P->u_stage, P->u_stage_bytes, s));
+    }
     ud = P->u_stage;
   }
   std::string err;
@@ -1233,7 +1317,10 @@ extern "C" int sft_apply_phase1(sft_plan_t P, const void* f, void* sendbuf) {
   cudaStream_t s = P->stream;
   const double2* fd = (const double2*)f;
   if (!is_device_ptr(f)) {
-    if (!P->f_stage) CKR(cudaMallocAsync(&P->f_stage, P->nk * sizeof(double2), s));
+    if (!P->f_stage) {
+      P->f_stage_bytes = P->nk * sizeof(double2);
+      CKR(block_alloc((void**)&P->f_stage, P->f_stage_bytes, s));
+    }
     CKR(cudaMemcpyAsync(P->f_stage, f, P->nk * sizeof(double2), cudaMemcpyHostToDevice, s));
     CKR(f_copy_mark(P));
     fd = P->f_stage;
@@ -1251,7 +1338,10 @@ extern "C" int sft_apply_phase2(sft_plan_t P, const void* recvbuf, void* u) {
   const bool u_host = !is_device_ptr(u);
   double2* ud = (double2*)u;
   if (u_host) {
-    if (!P->u_stage) CKR(cudaMallocAsync(&P->u_stage, P->nx * sizeof(double2), s));
+    if (!P->u_stage) {
+      P->u_stage_bytes = P->nx * sizeof(double2);
+      CKR(block_alloc((void**)&P->u_stage, P->u_stage_bytes, s));
+    }
     ud = P->u_stage;
   }
   if (int rc = phase2_run(P, (const double2*)recvbuf, ud, false)) return rc;

@@ -45,6 +45,7 @@ struct Tree {
   int32_t* perm = nullptr;         // [npts] sorted position -> user index
   double* pts_sorted = nullptr;    // [npts][d]
   void* arena = nullptr;           // one allocation holding every array above (X owns both trees')
+  size_t arena_bytes = 0;
 };
 
 struct DeviceTables {
@@ -94,6 +95,7 @@ struct sft_plan_s {
   // staging for host pointers
   double2* f_stage = nullptr;
   double2* u_stage = nullptr;
+  size_t f_stage_bytes = 0, u_stage_bytes = 0, blk_bytes = 0;  // sizes of the cached blocks (block_free)
   cudaEvent_t f_copied = nullptr;  // recorded after a host f's staging copy (sft_apply waits on it)
   int* d_err = nullptr;
   // multi-GPU
@@ -138,6 +140,10 @@ struct sft_plan_s {
 };
 
 namespace sft {
+
+// api.cu: device blocks of destroyed plans reused by the next plans (per device)
+cudaError_t block_alloc(void** out, size_t bytes, cudaStream_t s);
+void block_free(void* p, size_t bytes, cudaStream_t s);
 
 // tree.cu
 int build_trees(sft_plan_s* P, const double* x_dev, const double* k_dev, std::string* err);

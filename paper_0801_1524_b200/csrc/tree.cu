@@ -572,8 +572,10 @@ int build_trees(sft_plan_s* P, const double* x_dev, const double* k_dev, std::st
     off = align_up(off + 8 * d * npt[t], 256);
   }
   char* arena = nullptr;
-  CK(cudaMallocAsync((void**)&arena, off, s));
+  CK(block_alloc((void**)&arena, off, s));
+  trace_mark("alloc", s, true);
   P->X.arena = arena;
+  P->X.arena_bytes = off;
   P->K.arena = nullptr;
   CK(cudaMemsetAsync(arena + cm_lo, 0, cm_hi - cm_lo, s));
   P->d_err = (int*)(arena + o_errf);  // lives in the arena (freed with the trees)
@@ -628,7 +630,7 @@ int build_trees(sft_plan_s* P, const double* x_dev, const double* k_dev, std::st
 }
 
 void free_tree(Tree& T, cudaStream_t s) {
-  if (T.arena) cudaFreeAsync(T.arena, s);
+  if (T.arena) block_free(T.arena, T.arena_bytes, s);
   T.arena = nullptr;
   T.lev.clear();
   T.first_pt = nullptr;

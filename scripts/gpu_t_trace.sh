@@ -1,0 +1,6 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+timeout 1200 python -m pytest tests -x -q -m "gpu and not slow" -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1
+echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+SFT_PLAN_TRACE=1 timeout 120 python scripts/step_timeline.py C2 > gpurun_out/trace_c2.txt 2>&1
+for c in C2 C1 C0; do timeout 600 python bench.py --config $c --steps 20 --warmup 3 --no-cpu-baseline --nrhs 1 > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err; done
