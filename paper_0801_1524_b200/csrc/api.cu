@@ -599,7 +599,7 @@ extern "C" int sft_plan(int dim, int64_t N, int p, const double* x, int64_t nx, 
   P->prec = o.precision;
   {
     const int64_t pd = ipow64(p, dim);
-    P->pds = (int)(P->prec == 1 ? pd + (pd & 1) : pd);  // FP32: 16-byte multiple per array
+    P->pds = pair_stride((int)pd, P->prec);  // FP32 (and SFT_PAD_EVEN): 16 / 32-byte multiple per array
   }
   P->stream = (cudaStream_t)o.stream;
   P->dev = current_device();

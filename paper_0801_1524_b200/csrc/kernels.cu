@@ -318,7 +318,7 @@ cudaError_t launch_leaf(const sft_plan_s* Pl, const double2* f, void* out, int64
                      Pl->N, Pl->conj, nrhs, ldf, ors, Pl->ffmod && !Pl->conj)));
   } else {
     SFT_DISPATCH(Pl->d, Pl->p,
-                 (k_leaf<D, P, double2, Pow<P, D>::v><<<nb, 128, 0, Pl->stream>>>(
+                 (k_leaf<D, P, double2, StrideT<double2, Pow<P, D>::v>::v><<<nb, 128, 0, Pl->stream>>>(
                      Pl->K.pts_sorted, Pl->K.perm, Pl->K.first_pt, Pl->K.leaf_of, f, Pl->tab->leaf_invD, (double2*)out, b_lo, b_hi,
                      Pl->N, Pl->conj, nrhs, ldf, ors, Pl->ffmod && !Pl->conj)));
   }
@@ -338,7 +338,7 @@ cudaError_t launch_final(const sft_plan_s* Pl, const void* h0, double2* u, int64
                      Pl->conj, nrhs, hrs, ldu, Pl->ffmod && Pl->conj)));
   } else {
     SFT_DISPATCH(Pl->d, Pl->p,
-                 (k_final<D, P, double2, Pow<P, D>::v><<<nb, 128, 0, Pl->stream>>>(
+                 (k_final<D, P, double2, StrideT<double2, Pow<P, D>::v>::v><<<nb, 128, 0, Pl->stream>>>(
                      Pl->X.pts_sorted, sorted_out ? nullptr : Pl->X.perm, Pl->X.leaf_of, (const double2*)h0, u, i_lo, i_hi, a_lo, Pl->N,
                      Pl->conj, nrhs, hrs, ldu, Pl->ffmod && Pl->conj)));
   }

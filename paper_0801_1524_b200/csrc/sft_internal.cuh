@@ -230,6 +230,19 @@ struct Pow<B, 0> {
   static constexpr int v = 1;
 };
 
+// Stride (elements) of one pair array in the level buffers and stages: p^d,
+// rounded up to even for FP32 (16-byte bulk copies) and -- SFT_PAD_EVEN -- for
+// FP64 too (every array starts on a 32-byte sector: no sector is shared by two
+// arrays written by different CTAs)
+#ifndef SFT_PAD_EVEN
+#define SFT_PAD_EVEN 0
+#endif
+template <typename E, int PD>
+struct StrideT {
+  static constexpr int v = (sizeof(E) == 8 || SFT_PAD_EVEN) ? PD + (PD & 1) : PD;
+};
+inline int pair_stride(int pd, int prec) { return (prec == 1 || SFT_PAD_EVEN) ? pd + (pd & 1) : pd; }
+
 #define SFT_DISPATCH(D_, P_, CALL)                                       \
   do {                                                                   \
     if (D_ == 2 && P_ == 5) { constexpr int D = 2, P = 5; CALL; }        \

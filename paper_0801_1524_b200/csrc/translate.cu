@@ -217,10 +217,6 @@ struct ElemT<float2> {
 };
 // pair-array stride (elements) in buffers and stages: FP32 arrays padded to an
 // even count so every array is a multiple of 16 bytes (bulk copies)
-template <typename E, int PD>
-struct StrideT {
-  static constexpr int v = sizeof(E) == 8 ? PD + (PD & 1) : PD;
-};
 
 __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -276,6 +272,14 @@ struct OutRow {
   bool ok;
   __device__ __forceinline__ void st(int el, double re, double im) const {
     if (!ok) return;
+#if defined(SFT_ABL_NOGSTORE) || defined(SFT_ABL_NOSSTORE)  // ablation: values kept live, not stored
+#ifdef SFT_ABL_NOGSTORE
+    if constexpr (GL) { asm volatile("" ::"d"(re), "d"(im)); return; }
+#endif
+#ifdef SFT_ABL_NOSSTORE
+    if constexpr (!GL) { asm volatile("" ::"d"(re), "d"(im)); return; }
+#endif
+#endif
     if constexpr (GL) g[el] = ElemT<E>::mk(re, im);
     else sts<E>(s + el * (int)sizeof(E), re, im);
   }
@@ -653,7 +657,7 @@ template <int D, int P, int G>
 __global__ void k_check_schedule(TransArgs a, const unsigned char* __restrict__ sched, int64_t ntiles,
                                  int64_t in_pairs, int64_t out_pairs, int* err) {
   using SC = Sched<D, P, G>;
-  constexpr int PD = Pow<P, D>::v;
+  constexpr int PD = StrideT<double2, Pow<P, D>::v>::v;  // offsets are in units of the array stride
   constexpr int STAGE = G * (1 << D) * PD;
   const int64_t tile = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (tile >= ntiles) return;
@@ -913,7 +917,7 @@ __device__ __forceinline__ void sym_math(const LaneOps<P>& op, const uint32_t (&
 // MUL: stage-slot stride of consecutive child slots: 0 = G (slot-major
 // stage), 1 for the second level of a two-level tile (transposed slots).
 template <int D, int P, int G, int NC, int AX, bool LAST, int LIST = AX, typename E = double2, bool FUSED = false,
-          int MUL = 0>
+          int MUL = 0, bool STAGED = false>
 __device__ __forceinline__ void consumer_pass(const TransArgs& a, E* __restrict__ sb,
                                               const unsigned char* __restrict__ blk, const LaneOps<P>& op,
                                               const E* __restrict__ zs, int& rot, int64_t ooff = 0) {
@@ -947,7 +951,11 @@ __device__ __forceinline__ void consumer_pass(const TransArgs& a, E* __restrict_
   // -1); which row swaps depends on the fiber-address step and STR mod 8
   // (SwapEven, from scripts/rfib_model_sym.py) -- with it the phase's loads
   // and stores are bank-conflict free for p = 7 and 3 of 4 instructions for p = 9
-  const bool swp = ((lane >> 2) & 1) ^ SwapEven<D, P, AX>::v;
+  // (a last pass storing straight to HBM keeps one order for all rows: rows
+  // 2q, 2q+1 hold consecutive fibers, so one store instruction fills whole
+  // 32-byte sectors -- with the swap every sector would be written in two
+  // 16-byte halves by two instructions, doubling the L1 -> L2 write sectors)
+  const bool swp = !(LAST && !STAGED) && (((lane >> 2) & 1) ^ SwapEven<D, P, AX>::v);
   const double sg = swp ? -1.0 : 1.0;
   const int o_f = (swp ? max(P - 1 - c, H) : min(c, H)) * STR, o_s = (swp ? min(c, H) : max(P - 1 - c, H)) * STR;
   const bool st_f = c <= H, st_s = c < H;
@@ -961,8 +969,11 @@ __device__ __forceinline__ void consumer_pass(const TransArgs& a, E* __restrict_
     // child slots of the row's pair; an absent child (its task's class bit
     // clear) reads the CTA's zero slot instead: absent slots are never
     // zero-filled or read
+    // STAGED: the last pass also writes in place; the tile's outputs then
+    // leave the stage by TMA bulk stores (tma_store_tile)
+    constexpr bool GL = LAST && !STAGED;
     uint32_t xa[NSUB], xb[NSUB];
-    OutRow<E, LAST> o0[NSUB], o1[NSUB];
+    OutRow<E, GL> o0[NSUB], o1[NSUB];
 #pragma unroll
     for (int u = 0; u < NSUB; ++u) {
       const int tau = (st0 + u) * 8 + rfib;
@@ -993,7 +1004,7 @@ __device__ __forceinline__ void consumer_pass(const TransArgs& a, E* __restrict_
 #ifdef SFT_ABL_NOSTORE  // ablation: no output stores (shared or global)
       o0[u].ok = o1[u].ok = false;
 #else
-      if (LAST && FUSED) {
+      if (GL && FUSED) {
         // fused exchange: straight into the receiving rank's buffer
         auto dst = [&](uint32_t off) -> E* {
           if (off == ~0u) return nullptr;
@@ -1006,7 +1017,7 @@ __device__ __forceinline__ void consumer_pass(const TransArgs& a, E* __restrict_
         o1[u].g = dst(d.o1);
         o0[u].ok = o0[u].g != nullptr;
         o1[u].ok = o1[u].g != nullptr;
-      } else if (LAST) {
+      } else if (GL) {
         o0[u].g = gout + d.o0 + ebase;
         o1[u].g = gout + d.o1 + ebase;
         o0[u].ok = d.o0 != ~0u;
@@ -1021,6 +1032,53 @@ __device__ __forceinline__ void consumer_pass(const TransArgs& a, E* __restrict_
     else
       sym_math<D, P, STR, C1, NSUB, E>(op, xa, xb, o0, o1, c, o_a0, o_a1, o_d0, o_d1, o_f, o_s, st_f, st_s, sg);
   }
+  // staged last pass: this thread's stage writes before the async-proxy
+  // (TMA) reads of the bulk stores
+  if constexpr (LAST && STAGED) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// TMA store of a tile whose last pass ran in place (STAGED): every output
+// array (A-child alpha of a group's A', B) is one contiguous p^d array in the
+// stage and in HBM, so one 1-D bulk copy shared -> global each (lanes of one
+// warp issue a task's two outputs each), instead of per-lane 16-byte global
+// stores from registers.  Returns after the copies have read the stage (the
+// caller then releases it to the producer).
+// Measured (B200, same box): C2 translate 1.017 (1) vs 0.953 ms (0), C4 35.4 vs
+// 34.4 ms -- the extra barrier and the serial issue cost more than the per-lane
+// stores, once those fill whole sectors (see consumer_pass); off by default.
+#ifndef SFT_TMA_STORE
+#define SFT_TMA_STORE 0
+#endif
+template <int D, int P, int G, typename E>
+__device__ __forceinline__ void tma_store_tile(const TransArgs& a, const unsigned char* __restrict__ blk, const E* sb,
+                                               int64_t ooff) {
+  using SC = Sched<D, P, G>;
+  constexpr int PS = StrideT<E, Pow<P, D>::v>::v;
+  constexpr uint32_t BYTES = PS * (uint32_t)sizeof(E);
+  const int lane = threadIdx.x & 31;
+  E* const out = reinterpret_cast<E*>(a.out) + ooff;
+  const uint32_t sba = smem_u32(sb);
+  auto bulk = [&](const E* dst, uint32_t src) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src), "r"(BYTES)
+                 : "memory");
+  };
+#pragma unroll
+  for (int li = 0; li < (D == 2 ? 2 : 1); ++li) {
+    // last-pass lists: 0 (axis 0: child slots (1 << (d-1)) G arrays apart), 3 (2D reversed order: axis 1, G apart)
+    const int L = li == 0 ? 0 : 3;
+    const uint32_t C1 = (uint32_t)((li == 0 ? (1 << (D - 1)) : 1) * G * PS);
+    const int* cnt = SC::cnt(blk) + 3 * L;
+    const int n = cnt[0] + cnt[1] + cnt[2];
+    const TaskRec* tk = SC::task(blk, L);
+    for (int t = lane; t < n; t += 32) {
+      const TaskRec r = tk[t];
+      if (r.o0 != ~0u) bulk(out + r.o0, sba + r.x * (uint32_t)sizeof(E));
+      if (r.o1 != ~0u) bulk(out + r.o1, sba + (r.x + C1) * (uint32_t)sizeof(E));
+    }
+  }
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  __syncwarp();
 }
 
 // Optional cycle accounting (-DSFT_INSTR): per-CTA sums of clock64 intervals
@@ -1180,7 +1238,7 @@ __device__ __forceinline__ uint2 ws_group_record(const unsigned char* __restrict
                           : make_uint2(0u, 0u);
 }
 
-template <int D, int P, int G, int NST, typename E = double2, int PS = Pow<P, D>::v, bool BATCH = false, int NB = 1>
+template <int D, int P, int G, int NST, typename E = double2, int PS = StrideT<double2, Pow<P, D>::v>::v, bool BATCH = false, int NB = 1>
 __device__ __forceinline__ void ws_producer(const TransArgs& a, const unsigned char* __restrict__ sched, int64_t ntiles,
                                             E* ring, unsigned char (*blk)[Sched<D, P, G>::BLK * NB], uint64_t* full,
                                             uint64_t* empty) {
@@ -1277,6 +1335,8 @@ __global__ __launch_bounds__((NC + 1) * 32, MINB) void k_translate_ws(TransArgs 
   // work items w = tile * nrhs + r; the output of RHS r goes to out + r * rs
   const int64_t nwork = BATCH ? ntiles * a.nrhs : ntiles;
   auto ooff = [&](int64_t w_) { return BATCH ? (w_ % a.nrhs) * a.rs : (int64_t)0; };
+  // the last pass in place + TMA bulk stores (non-skewed single-level tiles)
+  constexpr bool STAGE_OUT = SFT_TMA_STORE && !FUSED && !F2;
   if constexpr (D == 2 && NST >= 3 && !F2) {
     int64_t tile = blockIdx.x;
     if (tile < nwork) {
@@ -1339,14 +1399,27 @@ __global__ __launch_bounds__((NC + 1) * 32, MINB) void k_translate_ws(TransArgs 
         consumer_sync<NC * 32>();
         INSTR_ADD(6, t2);
         INSTR_T0(t3);
-        last2d(sb, blk[s], ooff(w));
+        if constexpr (STAGE_OUT) {
+          consumer_pass<D, P, G, NC, 0, true, 0, E, false, 0, true>(a, sb, blk[s], op, zs, rot, 0);
+          consumer_pass<D, P, G, NC, D - 1, true, 3, E, false, 0, true>(a, sb, blk[s], op, zs, rot, 0);
+          consumer_sync<NC * 32>();
+          if (warp == 0) tma_store_tile<D, P, G, E>(a, blk[s], sb, ooff(w));
+        } else {
+          last2d(sb, blk[s], ooff(w));
+        }
         INSTR_ADD(7, t3);
       } else {
         consumer_pass<D, P, G, NC, 2, false, 2, E>(a, sb, blk[s], op, zs, rot, 0);
         consumer_sync<NC * 32>();
         consumer_pass<D, P, G, NC, 1, false, 1, E>(a, sb, blk[s], op, zs, rot, 0);
         consumer_sync<NC * 32>();
-        consumer_pass<D, P, G, NC, 0, true, 0, E, FUSED>(a, sb, blk[s], op, zs, rot, ooff(w));
+        if constexpr (STAGE_OUT) {
+          consumer_pass<D, P, G, NC, 0, true, 0, E, false, 0, true>(a, sb, blk[s], op, zs, rot, 0);
+          consumer_sync<NC * 32>();
+          if (warp == 0) tma_store_tile<D, P, G, E>(a, blk[s], sb, ooff(w));
+        } else {
+          consumer_pass<D, P, G, NC, 0, true, 0, E, FUSED>(a, sb, blk[s], op, zs, rot, ooff(w));
+        }
       }
       __syncwarp();
       if (lane == 0)
@@ -1357,6 +1430,8 @@ __global__ __launch_bounds__((NC + 1) * 32, MINB) void k_translate_ws(TransArgs 
       }
     }
   }
+  // bulk stores complete before the CTA exits (the next level reads them)
+  if (warp == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   // fused exchange: make this rank's peer stores visible system-wide before
   // the kernel completes (the caller's cross-rank barrier follows on the stream)
   if (FUSED) __threadfence_system();
@@ -1780,7 +1855,7 @@ static cudaError_t launch_schedule_t(const sft_plan_s* Pl, const LevelDims* L, i
                                      cudaStream_t st) {
   if (Pl->prec == 1)
     return launch_schedule_g<D, P, F32WsCfg<D, P>::G, StrideT<float2, Pow<P, D>::v>::v>(Pl, L, nlev, dst, st);
-  return launch_schedule_g<D, P, WsCfg<D, P>::G, Pow<P, D>::v>(Pl, L, nlev, dst, st);
+  return launch_schedule_g<D, P, WsCfg<D, P>::G, StrideT<double2, Pow<P, D>::v>::v>(Pl, L, nlev, dst, st);
 }
 
 template <int D, int P>
