@@ -87,8 +87,18 @@ __device__ __forceinline__ void leaf_weights(const double* __restrict__ k_sorted
   *rot = make_double2(cs, sn);  // e^{i pi sum_a s_a}, applied to each RHS's charge
 }
 
+// resident 128-thread blocks per SM the register budget is sized for (leaf / final)
+#ifndef SFT_LEAF_MINB2
+#define SFT_LEAF_MINB2 6  // C2 leaf 29.5 -> 26 us (4: 120 registers, 20% warps active)
+#endif
+#ifndef SFT_FINAL_MINB2
+#define SFT_FINAL_MINB2 1
+#endif
+#ifndef SFT_FINAL_MINB3
+#define SFT_FINAL_MINB3 1
+#endif
 template <int D, int P, typename T2, int PS>
-__global__ __launch_bounds__(128, D == 2 ? 4 : 2) void k_leaf(const double* __restrict__ k_sorted,
+__global__ __launch_bounds__(128, D == 2 ? SFT_LEAF_MINB2 : 2) void k_leaf(const double* __restrict__ k_sorted,
                                                               const int32_t* __restrict__ perm,
                                                               const int32_t* __restrict__ first_pt,
                                                               const int32_t* __restrict__ leaf_of,
@@ -186,7 +196,7 @@ __global__ __launch_bounds__(128, D == 2 ? 4 : 2) void k_leaf(const double* __re
 // sum-factorised over the axes; h is read through L1 (the ~3 targets of a
 // leaf share it).
 template <int D, int P, typename T2, int PS>
-__global__ __launch_bounds__(128) void k_final(const double* __restrict__ x_sorted, const int32_t* __restrict__ perm,
+__global__ __launch_bounds__(128, D == 2 ? SFT_FINAL_MINB2 : SFT_FINAL_MINB3) void k_final(const double* __restrict__ x_sorted, const int32_t* __restrict__ perm,
                                                const int32_t* __restrict__ leaf_of,
                                                const T2* __restrict__ h0, double2* __restrict__ u,
                                                int64_t i_lo, int64_t i_hi, int64_t a_lo, int64_t N, int conj,

@@ -26,6 +26,8 @@ with sft.Plan(w.dim, w.N, w.p, x, k, precision=int(os.environ.get('SWEEP_PREC', 
     st = pl.stats()
 tr = float(np.median([t["trans_ms"] for t in ts]))
 ap = float(np.median([t["apply_ms"] for t in ts]))
+lf = float(np.median([t["leaf_ms"] for t in ts]))
+fi = float(np.median([t["final_ms"] for t in ts]))
 print(json.dumps({"lib": os.path.basename(os.environ.get("SFT_LIB", "default")), "cfg": name, "trans_ms": round(tr, 4),
-                  "apply_ms": round(ap, 4), "GBps": round(st["trans_alg_bytes"] / tr / 1e6, 1),
+                  "apply_ms": round(ap, 4), "leaf_ms": round(lf, 4), "final_ms": round(fi, 4), "GBps": round(st["trans_alg_bytes"] / tr / 1e6, 1),
                   "checksum": float(u.abs().sum())}))
