@@ -709,7 +709,7 @@ __global__ void k_check_schedule(TransArgs a, const unsigned char* __restrict__ 
 #define SFT_NSUB29 1
 #endif
 #ifndef SFT_NSUB35
-#define SFT_NSUB35 2
+#define SFT_NSUB35 1
 #endif
 #ifndef SFT_NSUB37
 #define SFT_NSUB37 1
@@ -1636,7 +1636,7 @@ template <> struct WsCfg<2, 9> {
 #define SFT_WS_NST35 2
 #endif
 #ifndef SFT_WS_MINB35
-#define SFT_WS_MINB35 3
+#define SFT_WS_MINB35 4
 #endif
 #ifndef SFT_WS_G37
 #define SFT_WS_G37 1

@@ -96,7 +96,7 @@ def test_batch_fp32_and_adjoint():
     F = _charges(3, len(w.k), 400)
     U, S, _ = _run(w.x, w.k, F, w.N, 9, precision=1)
     assert np.array_equal(U.view(np.uint64), S.view(np.uint64))
-    assert_close(U[0], oracle.butterfly(w.x, w.k, F[0], w.N, 9), 2e-5)
+    assert_close(U[0], oracle.butterfly(w.x, w.k, F[0], w.N, 9), 1.3e-6)  # FP32_PARITY (test_gpu_parity.py)
     G = _charges(2, len(w.x), 500)
     V, S, _ = _run(w.x, w.k, G, w.N, 9, adjoint=True)
     assert V.shape == (2, len(w.k))

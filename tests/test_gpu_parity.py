@@ -209,13 +209,13 @@ def test_errors():
             plan.exchange_counts()  # world == 1
 
 
-# FP32 variant (BASELINE.json:5 "optional FP32 variant"): charges in complex64.
-# Tolerance vs the FP64 oracle butterfly: FP32 rounding (u = 6e-8) of the
-# level charges grows with the L levels and the operator norms (max row sum of
-# |T| ~ 2-3 per axis, partially cancelling); SURVEY.md §8(c) measured ~1e-6;
-# DESIGN.md derives the bar 2e-5.  Against the direct sum the BASELINE
-# tolerances (5e-2 / 1e-3 / 1e-5) apply unchanged.
-FP32_PARITY = 2e-5
+# FP32 variant (BASELINE.json:5 "optional FP32 variant"): level charges in
+# complex64, FP64 arithmetic.  Bar vs the FP64 oracle butterfly: ~3x the worst
+# error measured on these cases (scripts/fp32_errors.py on B200: 9.0e-8 ...
+# 4.3e-7 rel. L2, worst 3D N=16 p=9; max element 1.2e-6 of the RMS), i.e. FP32
+# storage rounding (u = 6e-8) grown over the levels.  Against the direct sum
+# the BASELINE tolerances (5e-2 / 1e-3 / 1e-5) apply unchanged.
+FP32_PARITY = 1.3e-6
 
 
 @pytest.mark.parametrize("name,p", [("C0", 5), ("C0", 7), ("C0", 9), ("C1", 7), ("C1", 9)])
