@@ -196,3 +196,43 @@ def test_partitioner_forced_and_infeasible():
     assert (sk, sx, m) == (2, 3, 5)
     with pytest.raises(sft.SftError):
         sft.choose_partition(L, 2, cx, ck, px, pk, force=(6, 6, 5))  # m < s_K: infeasible
+
+
+@pytest.mark.parametrize("p", [5, 7, 9])
+def test_mirror_symmetry_of_tables(p):
+    """The symmetric translation consumer relies on the child-1
+    operators being the mirror images of the child-0 ones: RC_1 = J RS_0 J and
+    RS_1 = J RC_0 J (J = index reversal) -- the child-1 grid is the mirror of
+    the child-0 grid about the parent's centre and the Lagrange basis on the
+    nodes e^{2 pi i m/(p-1)^2} maps to its conjugate under the mirror."""
+    _, _, RC, RS = sft.operator_tables(p, real=True)
+    J = np.eye(p)[::-1]
+    assert np.max(np.abs(RC[1] - J @ RS[0] @ J)) <= 1e-15
+    assert np.max(np.abs(RS[1] - J @ RC[0] @ J)) <= 1e-15
+
+
+@pytest.mark.parametrize("p", [7, 9])
+def test_symmetric_pass_equals_direct_pass(p):
+    """The sum/difference form of one axis pass (s = x0 + J x1, t = x0 - J x1;
+    SP, DP, SQ, DQ and the centre column) equals the direct form
+    P = RC_0 x0 + RS_1 x1, Q = RS_0 x0 - RC_1 x1 on random complex fibers."""
+    _, _, RC, RS = sft.operator_tables(p, real=True)
+    H = (p - 1) // 2
+    rng = np.random.default_rng(p)
+    for _ in range(4):
+        x0 = rng.normal(size=p) + 1j * rng.normal(size=p)
+        x1 = rng.normal(size=p) + 1j * rng.normal(size=p)
+        P = RC[0] @ x0 + RS[1] @ x1
+        Q = RS[0] @ x0 - RC[1] @ x1
+        s, t = x0 + x1[::-1], x0 - x1[::-1]
+        P2 = np.zeros(p, complex)
+        Q2 = np.zeros(p, complex)
+        for m in range(H):
+            mp = p - 1 - m
+            SP = 0.5 * (RC[0][m] + RC[0][mp]) @ s
+            DP = 0.5 * (RC[0][m] - RC[0][mp]) @ t
+            SQ = 0.5 * (RS[0][m] + RS[0][mp]) @ t
+            DQ = 0.5 * (RS[0][m] - RS[0][mp]) @ s
+            P2[m], P2[mp], Q2[m], Q2[mp] = SP + DP, SP - DP, SQ + DQ, SQ - DQ
+        P2[H], Q2[H] = RC[0][H] @ s, RS[0][H] @ t
+        assert np.max(np.abs(P - P2)) <= 1e-14 and np.max(np.abs(Q - Q2)) <= 1e-14
