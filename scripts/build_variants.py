@@ -31,3 +31,7 @@ if __name__ == "__main__":
     with ThreadPoolExecutor(4) as ex:
         for n in ex.map(one, specs):
             print(n)
+    # the variants' objects are not needed once linked (keep the gpurun snapshot small)
+    import glob
+    for o in glob.glob(os.path.join(ROOT, "paper_0801_1524_b200", "build", "*_*.o")):
+        os.remove(o)

@@ -1,0 +1,8 @@
+# plan-time A/B of sweep_libs variants (scripts/plan_timing.py), interleaved on one box
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+out=gpurun_out/ab_plan.txt; : > $out
+for rep in 1 2; do for c in ${AB_CONFIGS:-C2 C4}; do
+  echo "$c default $(timeout 300 python scripts/plan_timing.py $c 2>&1 | tail -1)" >> $out
+  for f in sweep_libs/lib_SORT*.so; do echo "$c $(basename $f) $(SFT_LIB=$PWD/$f timeout 300 python scripts/plan_timing.py $c 2>&1 | tail -1)" >> $out; done
+done; done
