@@ -719,19 +719,19 @@ struct NsubCfg {
   static constexpr int v = D == 2 ? (P == 5 ? SFT_NSUB25 : P == 7 ? SFT_NSUB27 : SFT_NSUB29)
                                   : (P == 5 ? SFT_NSUB35 : P == 7 ? SFT_NSUB37 : 1);
 };
-// Row -> fiber map of a super-tile: chosen per (d, p, axis) by
-// scripts/rfib_search_sym.py, which minimises the modelled shared-memory
-// wavefronts (A fragments, delta and centre loads, in-place stores) of the
-// symmetric pass; the default (rows 2q, 2q+1 <- fibers q, q+4) is optimal for
-// 2D p = 9, 3D p = 9 and two of the 3D p = 7 axes.
-template <int D, int P, int AX>
+// Row -> fiber map of a super-tile (shared-memory bank conflicts, and whole
+// sectors for the HBM stores of a last pass).  The symmetric form uses the
+// identity with the store-order swap of consumer_pass (scripts/rfib_model_sym.py).
+template <int D, int P, int AX, bool LAST>
 struct RowMap {
   __device__ __forceinline__ static int fiber(int r) {
-    if constexpr (UseSym<P>::v) return r;  // symmetric form: rows 2q, 2q+1 <- consecutive fibers
-    else if constexpr (D == 2) return (0x65437210u >> (4 * r)) & 7;                      // 0 1 2 7 3 4 5 6
-    else if constexpr (AX == 0) return (0x63724150u >> (4 * r)) & 7;                      // 0 5 1 4 2 7 3 6
-    else if constexpr (AX == 1) return (0x74326150u >> (4 * r)) & 7;                      // 0 5 1 6 2 3 4 7
-    else return r;
+    // symmetric form, and any pass storing to HBM: consecutive fibers in rows
+    // 2q, 2q+1 (a store instruction then fills whole 32-byte sectors)
+    if constexpr (UseSym<P>::v || LAST) return r;
+    // direct form (p = 5), in-place passes: scripts/rfib_search_direct.py (slot-major stage, G of WsCfg)
+    else if constexpr (D == 2) return (0x43726150u >> (4 * r)) & 7;                     // 0 5 1 6 2 7 3 4
+    else if constexpr (AX == 1) return (0x76432150u >> (4 * r)) & 7;                    // 0 5 1 2 3 4 6 7
+    else return (0x73625140u >> (4 * r)) & 7;                                           // 0 4 1 5 2 6 3 7
   }
 };
 
@@ -943,7 +943,7 @@ __device__ __forceinline__ void consumer_pass(const TransArgs& a, E* __restrict_
   const int nst = (ntot + 7) >> 3;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int c = lane & 3;
-  const int rfib = RowMap<D, P, AX>::fiber(lane >> 2);  // row -> fiber of the super-tile (bank conflicts)
+  const int rfib = RowMap<D, P, AX, LAST && !STAGED>::fiber(lane >> 2);  // row -> fiber of the super-tile
   // this lane's element offsets in a fiber (padding k >= H: a valid odd element, zero B row;
   // delta / outputs of lanes c > H (p = 5): clamped, coefficients 0, no stores)
   // (child 1 offsets relative to its own slot)
