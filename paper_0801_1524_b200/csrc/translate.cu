@@ -193,6 +193,21 @@ template <int P>
 struct UseSym {
   static constexpr bool v = P >= 7;
 };
+#ifndef SFT_SLOTPAD
+#define SFT_SLOTPAD 0  // 1: measured no gain (C3 0.758 vs 0.756 ms)
+#endif
+// Stage: child slot c of group j at c * SLOT + j * PS elements, SLOT = G * PS +
+// SlotPad.  The direct form reads both children in one instruction (lanes 0, 1:
+// child 0; lanes 2, 3: child 1), so their slots must not be a multiple of 8
+// 16-byte units apart (G * p^d is, e.g. 3D p = 5 with G = 2 on axis 0: 1000):
+// one element of padding per child slot makes the step odd.  The symmetric
+// form loads the two children in separate instructions: no padding.
+// (in elements of the array stride PS: FP64 p^d is odd; the FP32 stride is even
+// and a pad would break the 16-byte alignment of the bulk copies, so none)
+template <int D, int P, int PS>
+struct SlotPad {
+  static constexpr int v = (!UseSym<P>::v && (PS & 1)) ? SFT_SLOTPAD : 0;
+};
 struct DirShape5 {
   static constexpr int P = 5;
   // fragment table: B, tail (P, Q weights of this lane's k), delta (a0, b0, a1, b1) of m = lane%4, tail delta
@@ -415,7 +430,7 @@ __device__ __forceinline__ void schedule_pass(const LevelArgs& a, const GroupMet
         slot0 = v << 1;
       }
       t.x = TR ? (uint32_t)(((lane % NS) * G + ((lane % G) & ~(NS - 1)) + slot0) * PD)
-               : (uint32_t)((slot0 * G + (lane % G)) * PD);
+               : (uint32_t)(slot0 * (G * PD + SlotPad<D, P, PD>::v) + (lane % G) * PD);
       t.cls = cls;
       t.o0 = t.o1 = ~0u;
       if (LAST) {
@@ -443,7 +458,7 @@ __device__ __forceinline__ void schedule_pass(const LevelArgs& a, const GroupMet
         TaskRec t;
         const int sl = (bp << (D - AX)) | as;
         t.x = TR ? (uint32_t)(((lane % NS) * G + ((lane % G) & ~(NS - 1)) + sl) * PD)
-                 : (uint32_t)((sl * G + (lane % G)) * PD);
+                 : (uint32_t)(sl * (G * PD + SlotPad<D, P, PD>::v) + (lane % G) * PD);
         t.cls = cls;
         t.o0 = t.o1 = ~0u;
         if (LAST) {
@@ -658,7 +673,7 @@ __global__ void k_check_schedule(TransArgs a, const unsigned char* __restrict__ 
                                  int64_t in_pairs, int64_t out_pairs, int* err) {
   using SC = Sched<D, P, G>;
   constexpr int PD = StrideT<double2, Pow<P, D>::v>::v;  // offsets are in units of the array stride
-  constexpr int STAGE = G * (1 << D) * PD;
+  constexpr int STAGE = (1 << D) * (G * PD + SlotPad<D, P, PD>::v);
   const int64_t tile = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (tile >= ntiles) return;
   const unsigned char* b = sched + tile * SC::BLK;
@@ -935,7 +950,7 @@ __device__ __forceinline__ void consumer_pass(const TransArgs& a, E* __restrict_
   constexpr int PD = StrideT<E, Pow<P, D>::v>::v;  // slot stride (elements)
   constexpr int STR = Pow<P, D - 1 - AX>::v;
   constexpr int SH = D - 1 - AX;
-  constexpr int C1 = (1 << SH) * PD * (MUL == 0 ? G : MUL);  // child-1 slot of the pair
+  constexpr int C1 = (1 << SH) * (MUL == 0 ? G * PD + SlotPad<D, P, PD>::v : MUL * PD);  // child-1 slot of the pair
   E* const gout = reinterpret_cast<E*>(a.out) + ooff;  // ooff: RHS offset of a batch
   const int* cnt = SC::cnt(blk) + 3 * LIST;
   const TaskRec* tasks = SC::task(blk, LIST);
@@ -1069,7 +1084,7 @@ __device__ __forceinline__ void tma_store_tile(const TransArgs& a, const unsigne
   for (int li = 0; li < (D == 2 ? 2 : 1); ++li) {
     // last-pass lists: 0 (axis 0: child slots (1 << (d-1)) G arrays apart), 3 (2D reversed order: axis 1, G apart)
     const int L = li == 0 ? 0 : 3;
-    const uint32_t C1 = (uint32_t)((li == 0 ? (1 << (D - 1)) : 1) * G * PS);
+    const uint32_t C1 = (uint32_t)((li == 0 ? (1 << (D - 1)) : 1) * (G * PS + SlotPad<D, P, PS>::v));
     const int* cnt = SC::cnt(blk) + 3 * L;
     const int n = cnt[0] + cnt[1] + cnt[2];
     const TaskRec* tk = SC::task(blk, L);
@@ -1140,7 +1155,7 @@ __device__ __forceinline__ void ws_issue(const TransArgs& a, const unsigned char
   using SC = Sched<D, P, G>;
   constexpr int PD = PS;  // stage and HBM arrays have stride PS elements of type E
   constexpr int NS = 1 << D;
-  constexpr int STAGE = G * NS * PD;
+  constexpr int STAGE = NS * (G * PD + SlotPad<D, P, PD>::v);
   const int lane = threadIdx.x & 31;
   const int64_t nr = BATCH ? a.nrhs : 1;
   const E* const ain = reinterpret_cast<const E*>(a.in) + (BATCH ? (w - tile * nr) * a.rs : (int64_t)0);
@@ -1163,7 +1178,7 @@ __device__ __forceinline__ void ws_issue(const TransArgs& a, const unsigned char
     if (uniform) {
       for (int c = 0; c < NS; ++c) {
         if (m0 >> c & 1) continue;
-        float4* z = reinterpret_cast<float4*>(sb + (int64_t)c * G * PD);
+        float4* z = reinterpret_cast<float4*>(sb + (int64_t)c * (G * PD + SlotPad<D, P, PD>::v));
         for (int q = lane; q < G * CH; q += 32) z[q] = make_float4(0.f, 0.f, 0.f, 0.f);
       }
     } else {
@@ -1171,7 +1186,7 @@ __device__ __forceinline__ void ws_issue(const TransArgs& a, const unsigned char
         const int j = js / NS, c = js % NS;
         const uint32_t mB = __shfl_sync(0xffffffffu, gr.y, j);
         if (mB >> c & 1) continue;
-        float4* z = reinterpret_cast<float4*>(sb + ((int64_t)c * G + j) * PD);
+        float4* z = reinterpret_cast<float4*>(sb + (int64_t)c * (G * PD + SlotPad<D, P, PD>::v) + (int64_t)j * PD);
         for (int q = lane; q < CH; q += 32) z[q] = make_float4(0.f, 0.f, 0.f, 0.f);
       }
     }
@@ -1200,7 +1215,7 @@ __device__ __forceinline__ void ws_issue(const TransArgs& a, const unsigned char
 #ifndef SFT_ABL_NOLOAD
       asm volatile(
           "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-              smem_u32(sb + (int64_t)lane * G * PD)),
+              smem_u32(sb + (int64_t)lane * (G * PD + SlotPad<D, P, PD>::v))),
           "l"(ain + pin * PD), "r"((uint32_t)(G * PD * sizeof(E))), "r"(smem_u32(&full[s]))
           : "memory");
 #else
@@ -1221,7 +1236,7 @@ __device__ __forceinline__ void ws_issue(const TransArgs& a, const unsigned char
 #ifndef SFT_ABL_NOLOAD
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_u32(sb + ((int64_t)c * G + lane) * PD)),
+            smem_u32(sb + (int64_t)c * (G * PD + SlotPad<D, P, PD>::v) + (int64_t)lane * PD)),
         "l"(ain + pin * PD), "r"((uint32_t)(PD * sizeof(E))), "r"(smem_u32(&full[s]))
         : "memory");
 #else
@@ -1298,7 +1313,7 @@ __global__ __launch_bounds__((NC + 1) * 32, MINB) void k_translate_ws(TransArgs 
   using SC = Sched<D, P, G>;
   constexpr int PD = StrideT<E, Pow<P, D>::v>::v;  // array stride (elements)
   constexpr int NS = 1 << D;
-  constexpr int STAGE = G * NS * PD;
+  constexpr int STAGE = NS * (G * PD + SlotPad<D, P, PD>::v);
   extern __shared__ __align__(128) unsigned char smem_raw[];
   E* ring = reinterpret_cast<E*>(smem_raw);  // [NST][G][NS][PD]
   E* const zs = ring + NST * STAGE;          // [PD] zeros: what an absent child slot reads
@@ -1759,7 +1774,7 @@ static cudaError_t persistent_grid(K kernel, int threads, size_t smem, int* grid
 template <int D, int P, int G, int NC, int NST, int MB, typename E, bool FUSED, bool BATCH, bool F2>
 static cudaError_t launch_ws(const sft_plan_s* Pl, const TransArgs& a, const LevelDims& L, int64_t work) {
   constexpr int PS = StrideT<E, Pow<P, D>::v>::v;
-  const size_t smem = (size_t)(NST * G * (1 << D) + 1) * PS * sizeof(E);  // stage ring + zero slot
+  const size_t smem = ((size_t)NST * (1 << D) * (G * PS + SlotPad<D, P, PS>::v) + PS) * sizeof(E);  // ring + zero slot
   auto kern = k_translate_ws<D, P, G, NC, NST, MB, E, FUSED, BATCH, F2>;
   static PerDevice<int> grid_cache;  // this instantiation's grid and smem opt-in, per device
   int grid_max = 0;

@@ -1,6 +1,7 @@
 """Row -> fiber map of the direct-form (p = 5) super-tile, per (d, axis, G),
 minimising modelled shared-memory wavefronts, with the slot-major stage
-(child-1 slot (1 << (d-1-axis)) * G * p^d elements after child 0).
+(child-1 slot (1 << (d-1-axis)) * (G * p^d + pad) elements after child 0; pad =
+SlotPad, 1 element).
 
 Access model of direct_math (translate.cu): lane (r, c) loads child (c >> 1)'s
 element 2 (c & 1) + 1 (A fragment), child 0's element min(2c, 4) and child 1's
@@ -20,12 +21,12 @@ def phase(addrs):
     return max((len(v) for v in g.values()), default=0)
 
 
-def cost(D, AX, G, rfib, stores=True):
+def cost(D, AX, G, rfib, stores=True, pad=1):
     P = 5
     PD = P ** D
     STR = P ** (D - 1 - AX)
     PF = PD // P
-    C1 = (1 << (D - 1 - AX)) * PD * G
+    C1 = (1 << (D - 1 - AX)) * (PD * G + pad)  # slot-major stage with SlotPad
     tot = 0
     for f0 in range(0, PF, 8):
         fib = [(f0 + rfib[r]) % PF for r in range(8)]
