@@ -193,6 +193,12 @@ template <int P>
 struct UseSym {
   static constexpr bool v = P >= 7;
 };
+#ifndef SFT_CLASS_SPLIT
+// class-uniform super-tiles skip the absent child's loads; 2D symmetric form
+// only (measured: C2 translate 0.948 -> 0.942 ms; 3D: C3 0.750 -> 0.833, C4
+// 33.8 -> 35.5 ms -- three instantiations of the 3D passes cost more)
+#define SFT_CLASS_SPLIT 1
+#endif
 #ifndef SFT_SLOTPAD
 #define SFT_SLOTPAD 0  // 1: measured no gain (C3 0.758 vs 0.756 ms)
 #endif
@@ -755,7 +761,7 @@ struct RowMap {
 // for its output m = c child 0's element 2m and child 1's element 2m - (p-1)
 // (the delta columns, coefficients 0 when out of range); 2 DMMA give (P_m,
 // Q_m) of m = c, a 4-lane transpose-reduce the tail m = p-1.
-template <int D, int P, int STR, int C1, int NSUB, typename E, bool GL>
+template <int D, int P, int STR, int C1, int NSUB, typename E, bool GL, int PRES>
 __device__ __forceinline__ void direct_math(const LaneOps<P>& op, const uint32_t (&xa)[NSUB], const uint32_t (&xb)[NSUB],
                                             const OutRow<E, GL> (&o0)[NSUB], const OutRow<E, GL> (&o1)[NSUB], int c) {
   constexpr int ES = sizeof(E);
@@ -766,9 +772,14 @@ __device__ __forceinline__ void direct_math(const LaneOps<P>& op, const uint32_t
   double avx[NSUB], avy[NSUB];
 #pragma unroll
   for (int u = 0; u < NSUB; ++u) {
-    const double2 av = lds<E>(((c >> 1) ? xb[u] : xa[u]) + o_a);
-    const double2 x0 = lds<E>(xa[u] + o_e0), x1 = lds<E>(xb[u] + o_e1);
-    const double2 xt = lds<E>(xb[u] + o_t);
+    // PRES (warp-uniform): 1 = no row of the super-tile has child 1, 2 = none
+    // has child 0 -- that child's loads are skipped (zeros); 3 = rows may
+    // lack either (an absent child reads the zero slot)
+    const double2 z = make_double2(0.0, 0.0);
+    const double2 av = (c >> 1) ? (PRES & 2 ? lds<E>(xb[u] + o_a) : z) : (PRES & 1 ? lds<E>(xa[u] + o_a) : z);
+    const double2 x0 = PRES & 1 ? lds<E>(xa[u] + o_e0) : z;
+    const double2 x1 = PRES & 2 ? lds<E>(xb[u] + o_e1) : z;
+    const double2 xt = PRES & 2 ? lds<E>(xb[u] + o_t) : z;
     are[u][0] = fma(op.dt0, x1.x, op.ds0 * x0.x);
     are[u][1] = fma(op.dt1, x1.x, op.ds1 * x0.x);
     aim[u][0] = fma(op.dt0, x1.y, op.ds0 * x0.y);
@@ -813,7 +824,7 @@ struct SwapEven {
 };
 
 // Super-tile arithmetic of the symmetric form (p = 7, 9; see SymShape)
-template <int D, int P, int STR, int C1, int NSUB, typename E, bool GL>
+template <int D, int P, int STR, int C1, int NSUB, typename E, bool GL, int PRES>
 __device__ __forceinline__ void sym_math(const LaneOps<P>& op, const uint32_t (&xa)[NSUB], const uint32_t (&xb)[NSUB],
                                          const OutRow<E, GL> (&o0)[NSUB], const OutRow<E, GL> (&o1)[NSUB],
                                          int c, int o_a0, int o_a1, int o_d0, int o_d1, int o_f, int o_s, bool st_f,
@@ -828,9 +839,25 @@ __device__ __forceinline__ void sym_math(const LaneOps<P>& op, const uint32_t (&
 #pragma unroll
   for (int u = 0; u < NSUB; ++u) {
     constexpr int ES = sizeof(E);
-    const double2 e0 = lds<E>(xa[u] + o_d0 * ES), e1 = lds<E>(xb[u] + o_d1 * ES);
-    const double2 a0 = lds<E>(xa[u] + o_a0 * ES), a1 = lds<E>(xb[u] + o_a1 * ES);
-    const double ser = e0.x + e1.x, sei = e0.y + e1.y, ter = e0.x - e1.x, tei = e0.y - e1.y;
+    // PRES (warp-uniform, see direct_math): s = x0 + Jx1, t = x0 - Jx1 with the
+    // absent child's loads skipped (s = t = x0, or s = -t = Jx1)
+    double2 e0 = make_double2(0.0, 0.0), e1 = e0, a0 = e0, a1 = e0;
+    if constexpr (PRES & 1) {
+      e0 = lds<E>(xa[u] + o_d0 * ES);
+      a0 = lds<E>(xa[u] + o_a0 * ES);
+    }
+    if constexpr (PRES & 2) {
+      e1 = lds<E>(xb[u] + o_d1 * ES);
+      a1 = lds<E>(xb[u] + o_a1 * ES);
+    }
+    double ser, sei, ter, tei;
+    if constexpr (PRES == 3) {
+      ser = e0.x + e1.x; sei = e0.y + e1.y; ter = e0.x - e1.x; tei = e0.y - e1.y;
+    } else if constexpr (PRES == 1) {
+      ser = ter = e0.x; sei = tei = e0.y;
+    } else {
+      ser = e1.x; sei = e1.y; ter = -e1.x; tei = -e1.y;
+    }
     sre[u][0] = op.ds0 * ser;
     sre[u][1] = op.ds1 * ser;
     sim[u][0] = op.ds0 * sei;
@@ -839,15 +866,26 @@ __device__ __forceinline__ void sym_math(const LaneOps<P>& op, const uint32_t (&
     tre[u][1] = op.dt1 * ter;
     tim[u][0] = op.dt0 * tei;
     tim[u][1] = op.dt1 * tei;
-    ar[u][0] = a0.x + a1.x;  // s
-    ai[u][0] = a0.y + a1.y;
-    ar[u][1] = a0.x - a1.x;  // t
-    ai[u][1] = a0.y - a1.y;
+    if constexpr (PRES == 3) {
+      ar[u][0] = a0.x + a1.x;  // s
+      ai[u][0] = a0.y + a1.y;
+      ar[u][1] = a0.x - a1.x;  // t
+      ai[u][1] = a0.y - a1.y;
+    } else if constexpr (PRES == 1) {
+      ar[u][0] = ar[u][1] = a0.x;
+      ai[u][0] = ai[u][1] = a0.y;
+    } else {
+      ar[u][0] = a1.x;
+      ai[u][0] = a1.y;
+      ar[u][1] = -a1.x;
+      ai[u][1] = -a1.y;
+    }
     if constexpr (S::TAIL && SFT_CENTRE_DMMA) {
       // centre m = H (p = 9) on a second N tile: column 0 = SP_H (s-GEMM) and
       // SQ_H (t-GEMM), both on lane c = 0 of the row; centre delta (s, t at
       // element p-1) starts the accumulators there
-      const double2 c0 = lds<E>(xa[u] + (P - 1) * STR * ES), c1 = lds<E>(xb[u]);
+      const double2 c0 = PRES & 1 ? lds<E>(xa[u] + (P - 1) * STR * ES) : make_double2(0.0, 0.0);
+      const double2 c1 = PRES & 2 ? lds<E>(xb[u]) : make_double2(0.0, 0.0);
       cre[u][0] = op.tds * (c0.x + c1.x);
       cim[u][0] = op.tds * (c0.y + c1.y);
       cre[u][1] = op.tdt * (c0.x - c1.x);
@@ -859,7 +897,8 @@ __device__ __forceinline__ void sym_math(const LaneOps<P>& op, const uint32_t (&
       cti[u][0] = cim[u][1];
     } else if constexpr (S::TAIL) {
       // centre m = H (p = 9): partials of z_0, z_1 over this lane's k, centre delta on lane 0
-      const double2 c0 = lds<E>(xa[u] + (P - 1) * STR * ES), c1 = lds<E>(xb[u]);
+      const double2 c0 = PRES & 1 ? lds<E>(xa[u] + (P - 1) * STR * ES) : make_double2(0.0, 0.0);
+      const double2 c1 = PRES & 2 ? lds<E>(xb[u]) : make_double2(0.0, 0.0);
       const double pr = fma(op.tds, c0.x + c1.x, op.ts * ar[u][0]), pi = fma(op.tds, c0.y + c1.y, op.ts * ai[u][0]);
       const double qr = fma(op.tdt, c0.x - c1.x, op.tt * ar[u][1]), qi = fma(op.tdt, c0.y - c1.y, op.tt * ai[u][1]);
       tl[u][0] = pr + qi;
@@ -992,6 +1031,7 @@ __device__ __forceinline__ void consumer_pass(const TransArgs& a, E* __restrict_
     constexpr bool GL = LAST && !STAGED;
     uint32_t xa[NSUB], xb[NSUB];
     OutRow<E, GL> o0[NSUB], o1[NSUB];
+    unsigned orc = 0;  // classes of this lane's rows
 #pragma unroll
     for (int u = 0; u < NSUB; ++u) {
       const int tau = (st0 + u) * 8 + rfib;
@@ -1008,6 +1048,7 @@ __device__ __forceinline__ void consumer_pass(const TransArgs& a, E* __restrict_
         d.o0 = d.o1 = ~0u;
       }
       const uint32_t xo = d.x + (uint32_t)ebase;
+      orc |= d.cls;
 #if SFT_ABSENT == 2
       xa[u] = (d.cls & 1u) ? sba + xo * ES : zsa + ebase * ES;
       xb[u] = (d.cls & 2u) ? sba + (xo + C1) * ES : zsa + ebase * ES;
@@ -1045,10 +1086,22 @@ __device__ __forceinline__ void consumer_pass(const TransArgs& a, E* __restrict_
       }
 #endif
     }
-    if constexpr (!UseSym<P>::v)
-      direct_math<D, P, STR, C1, NSUB, E>(op, xa, xb, o0, o1, c);
-    else
-      sym_math<D, P, STR, C1, NSUB, E>(op, xa, xb, o0, o1, c, o_a0, o_a1, o_d0, o_d1, o_f, o_s, st_f, st_s, sg);
+    // warp-uniform union of the rows' child classes: super-tiles whose rows
+    // all lack one child skip its loads (the task lists are class-sorted, so
+    // most super-tiles are class-uniform)
+    const unsigned pres = (SFT_CLASS_SPLIT && D == 2 && UseSym<P>::v) ? __reduce_or_sync(0xffffffffu, orc) : 3u;
+    if constexpr (!UseSym<P>::v) {
+      if (pres == 1u) direct_math<D, P, STR, C1, NSUB, E, GL, 1>(op, xa, xb, o0, o1, c);
+      else if (pres == 2u) direct_math<D, P, STR, C1, NSUB, E, GL, 2>(op, xa, xb, o0, o1, c);
+      else direct_math<D, P, STR, C1, NSUB, E, GL, 3>(op, xa, xb, o0, o1, c);
+    } else {
+      if (pres == 1u)
+        sym_math<D, P, STR, C1, NSUB, E, GL, 1>(op, xa, xb, o0, o1, c, o_a0, o_a1, o_d0, o_d1, o_f, o_s, st_f, st_s, sg);
+      else if (pres == 2u)
+        sym_math<D, P, STR, C1, NSUB, E, GL, 2>(op, xa, xb, o0, o1, c, o_a0, o_a1, o_d0, o_d1, o_f, o_s, st_f, st_s, sg);
+      else
+        sym_math<D, P, STR, C1, NSUB, E, GL, 3>(op, xa, xb, o0, o1, c, o_a0, o_a1, o_d0, o_d1, o_f, o_s, st_f, st_s, sg);
+    }
   }
   // staged last pass: this thread's stage writes before the async-proxy
   // (TMA) reads of the bulk stores
