@@ -552,6 +552,9 @@ void trace_mark(const char* what, cudaStream_t s, bool dev) {
 }
 }  // namespace sft
 
+// two-level launches by default for plans whose largest level has fewer pairs (see sft_plan)
+constexpr int64_t kF2MaxPairs = 32768;
+
 static int supported_p(int d, int p) { return (d == 2 || d == 3) && (p == 5 || p == 7 || p == 9); }
 
 extern "C" int sft_plan(int dim, int64_t N, int p, const double* x, int64_t nx, const double* k, int64_t nk,
@@ -796,18 +799,19 @@ extern "C" int sft_plan(int dim, int64_t N, int p, const double* x, int64_t nx, 
   P->launch_t.clear();
   P->launch_f2_out.assign(L, 0);
   {
-    // measured (C2, per level pair): the two-level launch wins at the leaf end
-    // (levels 13+12: 0.1125 -> 0.1023 ms) and loses in the middle (e.g. 11+10:
-    // 0.201 -> 0.231 ms: a super-group's 16 stage slots hold ~2 present first-
-    // level groups on these curves), so by default only the first pair is fused;
-    // SFT_F2=all fuses every pair
-    // Default off: with the leaf-end pair fused the translation gains ~8 us on
-    // C2 and the plan loses as much (a second schedule kernel and event on its
-    // critical path), A/B on one box 1.3825 -> 1.3887 ms per step.
-    // SFT_F2=first fuses the leaf-end pair, SFT_F2=all every pair.
+    // Two-level launches halve the per-level latency chain (load, compute,
+    // store, kernel boundary), which is what a small plan's levels cost:
+    // measured (B200, round 2) C0 apply 0.039 -> 0.029 ms, C1 0.075 -> 0.066 ms
+    // with every pair fused.  On large plans a super-group's stage is half
+    // empty (~2 of 4 first-level groups present on curves) and the HBM round
+    // trip they save is not the limiter: C2 0.927 -> 1.311 ms (all), 0.939
+    // (leaf-end pair only).  Default: every pair fused when the largest level
+    // has fewer than kF2MaxPairs pairs, else none; SFT_F2=0|first|all overrides.
     const char* fe = getenv("SFT_F2");
-    const bool f2_all = fe && std::string(fe) == "all";
-    const bool f2 = two_level_supported(P) && fe && (f2_all || std::string(fe) == "first");
+    int64_t max_pairs = 0;
+    for (int tt = 0; tt <= L; ++tt) max_pairs = std::max<int64_t>(max_pairs, P->K.counts[tt] * P->X.counts[L - tt]);
+    const bool f2_all = fe ? std::string(fe) == "all" : max_pairs < kF2MaxPairs;
+    const bool f2 = two_level_supported(P) && (f2_all || (fe && std::string(fe) == "first"));
     int t = L - 1;
     while (t >= 0) {
       if (f2 && t >= 1 && (f2_all || t == L - 1)) {
@@ -847,8 +851,11 @@ extern "C" int sft_plan(int dim, int64_t N, int p, const double* x, int64_t nx, 
       std::vector<unsigned char*> dst;
       // (only when the first launch is a two-level one: its schedule kernel is
       // a separate launch anyway)
-      const int t_first =
-          !P->sharded && !P->launch_t.empty() && P->launch_f2_out[P->launch_t[0]] ? P->launch_t[0] : -1;
+      // (a separate first-launch schedule only pays when the schedules are long)
+      const int t_first = !P->sharded && !P->launch_t.empty() && P->launch_f2_out[P->launch_t[0]] &&
+                                  P->K.counts[L] * P->X.counts[0] >= kF2MaxPairs
+                              ? P->launch_t[0]
+                              : -1;
       for (int t = 0; t < L; ++t) {
         if (t >= 1 && P->launch_f2_out[t - 1]) continue;
         if (t == t_first) continue;

@@ -1860,10 +1860,12 @@ static cudaError_t launch_translate_t(const sft_plan_s* Pl, const LevelDims& L, 
   const int64_t work = (a.ngroups + C::G - 1) / C::G * a.nrhs;
   if (a.npeer > 0) return launch_ws<D, P, C::G, C::NC, C::NST, C::MINB, double2, true, false, false>(Pl, a, L, work);
   if (a.f2) {
-    // two-level launch (2D, G = 4k, unskewed configurations)
-    if constexpr (D == 2 && C::G % 4 == 0 && C::NST < 3) {
-      if (a.nrhs > 1) return launch_ws<D, P, C::G, C::NC, C::NST, C::MINB, double2, false, true, true>(Pl, a, L, work);
-      return launch_ws<D, P, C::G, C::NC, C::NST, C::MINB, double2, false, false, true>(Pl, a, L, work);
+    // two-level launch (2D, G = 4k; the unskewed pipeline, so at most 2 stages
+    // even where single-level launches of that p use the skewed one)
+    if constexpr (D == 2 && C::G % 4 == 0) {
+      constexpr int NST2 = C::NST < 3 ? C::NST : 2;
+      if (a.nrhs > 1) return launch_ws<D, P, C::G, C::NC, NST2, C::MINB, double2, false, true, true>(Pl, a, L, work);
+      return launch_ws<D, P, C::G, C::NC, NST2, C::MINB, double2, false, false, true>(Pl, a, L, work);
     }
     return cudaErrorInvalidValue;
   }
@@ -2029,9 +2031,9 @@ bool two_level_supported(const sft_plan_s* Pl) {
   if (e && e[0] == '0') return false;
   if (Pl->d != 2) return false;
   switch (Pl->p) {
-    case 5: return WsCfg<2, 5>::G % 4 == 0 && WsCfg<2, 5>::NST < 3;
-    case 7: return WsCfg<2, 7>::G % 4 == 0 && WsCfg<2, 7>::NST < 3;
-    case 9: return WsCfg<2, 9>::G % 4 == 0 && WsCfg<2, 9>::NST < 3;
+    case 5: return WsCfg<2, 5>::G % 4 == 0;
+    case 7: return WsCfg<2, 7>::G % 4 == 0;
+    case 9: return WsCfg<2, 9>::G % 4 == 0;
   }
   return false;
 }
