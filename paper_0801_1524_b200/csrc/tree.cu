@@ -87,12 +87,16 @@ __global__ void k_leaf_keys(const double* __restrict__ x, int64_t nx, const doub
 #ifndef SFT_BS_BITS
 #define SFT_BS_BITS 4  // radix digit bits of the block sort
 #endif
+// Items per thread: the smallest instantiation that holds the larger tree
+// (padding items cost a full sort pass each: C1's 10K-point trees take 11 items
+// per thread instead of 16, C0's 643 points 1).
 constexpr int kBlockSortItems = 16;
 constexpr int kBlockSortMax = 1024 * kBlockSortItems;
-template <typename KT>
+template <typename KT, int ITEMS>
 __global__ __launch_bounds__(1024) void k_block_sort(const KT* __restrict__ kin, const int32_t* __restrict__ iin,
                                                      KT* __restrict__ kout, int32_t* __restrict__ iout, int64_t nx,
                                                      int64_t nk, int bits) {
+  constexpr int kBlockSortItems = ITEMS;
   using BRS = cub::BlockRadixSort<KT, 1024, kBlockSortItems, int32_t, SFT_BS_BITS>;
   extern __shared__ __align__(16) unsigned char bs_smem[];
   auto& tmp = *reinterpret_cast<typename BRS::TempStorage*>(bs_smem);
@@ -351,7 +355,8 @@ static int sort_and_fill(sft_plan_s* P, const double* x_dev, const double* k_dev
                          const std::vector<size_t>* o_key, const std::vector<size_t>* o_par,
                          const std::vector<size_t>* o_cm, const std::vector<size_t>* o_cb, const size_t* o_first,
                          const size_t* o_leafof, const size_t* o_perm, const size_t* o_pts, const size_t* o_tot,
-                         const double* const* src, char** scr_out, FillArgs& fa, std::string* err) {
+                         const double* const* src, char** scr_out, size_t* scr_bytes, FillArgs& fa,
+                         std::string* err) {
   cudaStream_t s = P->stream;
   const int d = P->d, L = P->L;
   const int64_t nx = P->nx, nk = P->nk, n = nx + nk;
@@ -363,7 +368,7 @@ static int sort_and_fill(sft_plan_s* P, const double* x_dev, const double* k_dev
   // graph of the device-wide sort (or the plain call, SFT_SORT_GRAPH=0)
   constexpr bool bs_fits =
       sizeof(typename cub::BlockRadixSort<KT, 1024, kBlockSortItems, int32_t, SFT_BS_BITS>::TempStorage) <= 200 * 1024;
-  const bool block_sort = bs_fits && nx <= kBlockSortMax && nk <= kBlockSortMax && n >= 4096 && sort_graph_enabled();
+  const bool block_sort = bs_fits && nx <= kBlockSortMax && nk <= kBlockSortMax && sort_graph_enabled();
   const bool use_graph = sort_graph_enabled() && n >= 4096 && !block_sort;
   int dev = 0;
   CK(cudaGetDevice(&dev));
@@ -409,7 +414,7 @@ static int sort_and_fill(sft_plan_s* P, const double* x_dev, const double* k_dev
     CK(cudaMalloc((void**)&C.scr, so));
     scr = C.scr;
   } else {
-    CK(cudaMallocAsync((void**)&scr, so, s));
+    CK(block_alloc((void**)&scr, so, s));
   }
   trace_mark("scr", s, true);
   KT* keys_in = (KT*)(scr + s_kin);
@@ -425,18 +430,31 @@ static int sort_and_fill(sft_plan_s* P, const double* x_dev, const double* k_dev
   trace_mark("keys", s, true);
   if (block_sort) {
     if constexpr (bs_fits) {
-    using BRS = cub::BlockRadixSort<KT, 1024, kBlockSortItems, int32_t, SFT_BS_BITS>;
-    const size_t bsm = sizeof(typename BRS::TempStorage);
-    static PerDevice<int> attr;  // the shared-memory opt-in, once per device
-    int one = 0;
-    CK(attr.get(&one, [&](int, int* v) {
-      *v = 1;
-      return cudaFuncSetAttribute(k_block_sort<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm);
-    }));
-    // (the tree bit above bit d*L is constant within a tree)
-    k_block_sort<KT><<<2, 1024, bsm, s>>>(keys_in, idx_in, keys_out, idx_out, nx, nk, bits - 1);
-    count_launch();
-    CK(cudaGetLastError());
+      const int64_t nmax = std::max(nx, nk);
+      auto run = [&](auto items) -> cudaError_t {
+        constexpr int IT = decltype(items)::value;
+        using BRS = cub::BlockRadixSort<KT, 1024, IT, int32_t, SFT_BS_BITS>;
+        const size_t bsm = sizeof(typename BRS::TempStorage);
+        static PerDevice<int> attr;  // the shared-memory opt-in, once per device and instantiation
+        int one = 0;
+        cudaError_t e = attr.get(&one, [&](int, int* v) {
+          *v = 1;
+          return cudaFuncSetAttribute(k_block_sort<KT, IT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm);
+        });
+        if (e != cudaSuccess) return e;
+        // (the tree bit above bit d*L is constant within a tree)
+        k_block_sort<KT, IT><<<2, 1024, bsm, s>>>(keys_in, idx_in, keys_out, idx_out, nx, nk, bits - 1);
+        return cudaGetLastError();
+      };
+      cudaError_t e;
+      if (nmax <= 1024) e = run(std::integral_constant<int, 1>());
+      else if (nmax <= 2048) e = run(std::integral_constant<int, 2>());
+      else if (nmax <= 4096) e = run(std::integral_constant<int, 4>());
+      else if (nmax <= 8192) e = run(std::integral_constant<int, 8>());
+      else if (nmax <= 11264) e = run(std::integral_constant<int, 11>());
+      else e = run(std::integral_constant<int, kBlockSortItems>());
+      count_launch();
+      CK(e);
     }
   } else if (!use_graph) {
     CK(cub::DeviceRadixSort::SortPairs(scr + s_cub, cub_bytes, keys_in, keys_out, idx_in, idx_out, (int)n, 0, bits, s));
@@ -510,6 +528,7 @@ static int sort_and_fill(sft_plan_s* P, const double* x_dev, const double* k_dev
   trace_mark("fill", s, true);
 
   *scr_out = use_graph ? nullptr : scr;  // the cached scratch is not the plan's to free
+  *scr_bytes = so;
   return SFT_OK;
 }
 
@@ -583,12 +602,13 @@ int build_trees(sft_plan_s* P, const double* x_dev, const double* k_dev, std::st
 
   // ---- sort + fill (32-bit point keys when d*L+1 <= 32) ----
   char* scr = nullptr;
+  size_t scr_bytes = 0;
   FillArgs fa;
   int rc = (d * L + 1 <= 32)
                ? sort_and_fill<uint32_t>(P, x_dev, k_dev, arena, o_key, o_par, o_cm, o_cb, o_first, o_leafof, o_perm,
-                                         o_pts, o_tot, src, &scr, fa, err)
+                                         o_pts, o_tot, src, &scr, &scr_bytes, fa, err)
                : sort_and_fill<uint64_t>(P, x_dev, k_dev, arena, o_key, o_par, o_cm, o_cb, o_first, o_leafof, o_perm,
-                                         o_pts, o_tot, src, &scr, fa, err);
+                                         o_pts, o_tot, src, &scr, &scr_bytes, fa, err);
   if (rc) return rc;
 
   trace_mark("enq");
@@ -598,7 +618,7 @@ int build_trees(sft_plan_s* P, const double* x_dev, const double* k_dev, std::st
   static thread_local int64_t* h = nullptr;
   if (!h) CK(cudaMallocHost((void**)&h, (2 * kMaxLevels + 1) * sizeof(int64_t)));
   CK(cudaMemcpyAsync(h, arena + o_hdr, (16 * (L + 1) + 8), cudaMemcpyDeviceToHost, s));
-  if (scr) CK(cudaFreeAsync(scr, s));
+  if (scr) block_free(scr, scr_bytes, s);
   CK(cudaStreamSynchronize(s));
   trace_mark("sync");
   const int herr = (int)(h[2 * (L + 1)] & 0xffffffff);
