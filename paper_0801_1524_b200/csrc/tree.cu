@@ -253,6 +253,165 @@ __global__ __launch_bounds__(kBlk) void k_fill(const KT* __restrict__ key, const
   for (int a = 0; a < d; ++a) T.pts_sorted[li * d + a] = T.pts[(int64_t)j * d + a];
 }
 
+// ------------------------------------------------------------------------
+// Small trees (both <= 16K points): the whole build of a tree in one CTA of one
+// launch -- child-mask zeroing, Morton keys, the block radix sort, and the
+// count / fill steps of k_count / k_fill over the tree's sorted positions in
+// chunks of 1024 -- instead of a memset and four launches (small plans are
+// latency-bound: every launch boundary costs microseconds).  Same integer
+// arithmetic as the multi-kernel path, so identical trees.
+// ------------------------------------------------------------------------
+struct SmallTreeArgs {
+  TreeOut t[2];
+  uint32_t* mask[2];     // this tree's child-mask region (zeroed here)
+  int64_t mask_words[2];
+  void* keys[2];         // [n] sorted keys (scratch: predecessors are read across threads)
+  int32_t* idx[2];       // [n] sorted point indices (scratch; !FULL: + the tree's offset, as k_fill reads them)
+  int32_t ioff[2];       // that offset (0 when FULL)
+  int* err[2];           // domain flag of each tree (1 = a coordinate outside [0,N] or non-finite)
+};
+
+// FULL = false: only masks, keys and the sort here (the sorted keys / indices
+// written in the layout of the device-wide sort, totals zeroed); k_count and
+// k_fill follow with one block per 1024 points.  A single CTA walks its chunks
+// one after the other, so the full fusion only pays for small trees.
+template <typename KT, int ITEMS, bool FULL>
+__global__ __launch_bounds__(1024) void k_small_tree(const double* __restrict__ x, int64_t nx,
+                                                     const double* __restrict__ k, int64_t nk, int d, int L, double Nf,
+                                                     int64_t N, SmallTreeArgs A) {
+  using BRS = cub::BlockRadixSort<KT, 1024, ITEMS, int32_t, SFT_BS_BITS>;
+  extern __shared__ __align__(16) unsigned char st_smem[];
+  auto& tmp = *reinterpret_cast<typename BRS::TempStorage*>(st_smem);
+  __shared__ int cnt[ITEMS][kMaxLevels];  // per 1024-position chunk: boxes opened at each level (then its prefix)
+  __shared__ int woff[32][kMaxLevels];
+  __shared__ int errf;
+  const int tree = blockIdx.x;
+  const TreeOut& T = A.t[tree];
+  const int64_t n = tree ? nk : nx;
+  const double* pts = tree ? k : x;
+  KT* const skey = reinterpret_cast<KT*>(A.keys[tree]);
+  int32_t* const sidx = A.idx[tree];
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  for (int64_t q = t; q < A.mask_words[tree]; q += 1024) A.mask[tree][q] = 0u;
+  if (t == 0) errf = 0;
+  for (int q = t; q < ITEMS * kMaxLevels; q += 1024) (&cnt[0][0])[q] = 0;
+  __syncthreads();
+  // Morton keys of this thread's points (blocked), as k_leaf_keys without the tree bit
+  KT kk[ITEMS];
+  int32_t vv[ITEMS];
+  bool bad = false;
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const int64_t j = (int64_t)t * ITEMS + i;
+    if (j < n) {
+      uint64_t c[kMaxDim] = {0, 0, 0};
+#pragma unroll
+      for (int a = 0; a < kMaxDim; ++a) {
+        if (a >= d) break;
+        double y = pts[j * d + a];
+        if (!(y >= 0.0 && y <= Nf)) {
+          bad = true;
+          y = 0.0;
+        }
+        int64_t ci = (int64_t)floor(y);
+        if (ci > N - 1) ci = N - 1;
+        c[a] = (uint64_t)ci;
+      }
+      kk[i] = (KT)(d == 2 ? (spread2(c[0]) << 1) | spread2(c[1])
+                          : (spread3(c[0]) << 2) | (spread3(c[1]) << 1) | spread3(c[2]));
+      vv[i] = (int32_t)j;
+    } else {
+      kk[i] = ~(KT)0;
+      vv[i] = INT32_MAX;
+    }
+  }
+  if (bad) errf = 1;
+  BRS(tmp).SortBlockedToStriped(kk, vv, 0, d * L);  // item i of thread t: sorted position i * 1024 + t
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i)
+    if ((int64_t)i * 1024 + t < n) {
+      skey[(int64_t)i * 1024 + t] = kk[i];
+      sidx[(int64_t)i * 1024 + t] = vv[i] + A.ioff[tree];
+    }
+  if constexpr (!FULL) {
+    if (t <= L) T.totals[t] = 0;  // (k_fill's last block of the tree writes them)
+    __syncthreads();
+    if (t == 0) *A.err[tree] = errf;
+    return;
+  }
+  __syncthreads();
+  const int nch = (int)((n + 1023) / 1024);  // chunks holding points
+  // count: per chunk and level, the boxes its positions open
+#pragma unroll 1
+  for (int c = 0; c < nch; ++c) {
+    const int64_t pos = (int64_t)c * 1024 + t;
+    const int m = pos < n ? open_level(skey, pos, 0, d, L) : L + 1;
+    for (int l = 0; l <= L; ++l) {
+      const unsigned b = __ballot_sync(0xffffffffu, m <= l);
+      if (lane == 0 && b) atomicAdd(&cnt[c][l], __popc(b));
+    }
+  }
+  __syncthreads();
+  if (t <= L) {  // exclusive prefix over the chunks; the tree's box totals
+    int sacc = 0;
+    for (int c = 0; c < ITEMS; ++c) {
+      const int v = cnt[c][t];
+      cnt[c][t] = sacc;
+      sacc += v;
+    }
+    T.totals[t] = sacc;
+  }
+  __syncthreads();
+  // fill, chunk by chunk (k_fill with the chunk prefix as the block base)
+  const unsigned le = (lane == 31) ? 0xffffffffu : ((2u << lane) - 1u);
+#pragma unroll 1
+  for (int c = 0; c < nch; ++c) {
+    const int64_t pos = (int64_t)c * 1024 + t;
+    const bool valid = pos < n;
+    const int m = valid ? open_level(skey, pos, 0, d, L) : L + 1;
+    for (int l = 0; l <= L; ++l) {
+      const unsigned b = __ballot_sync(0xffffffffu, m <= l);
+      if (lane == 0) woff[warp][l] = __popc(b);
+    }
+    __syncthreads();
+    if (t <= L) {
+      int sacc = 0;
+      for (int w = 0; w < 32; ++w) {
+        const int v = woff[w][t];
+        woff[w][t] = sacc;
+        sacc += v;
+      }
+    }
+    __syncthreads();
+    const uint64_t key = valid ? (uint64_t)skey[pos] : 0ull;
+    int bid_prev = -1;
+    for (int l = 0; l <= L; ++l) {
+      const unsigned b = __ballot_sync(0xffffffffu, m <= l);
+      const int bid = cnt[c][l] + woff[warp][l] + __popc(b & le) - 1;
+      if (m <= l) {
+        const uint64_t kl = (key >> (d * (L - l))) & ((1ull << (d * l)) - 1ull);
+        T.key[l][bid] = kl;
+        if (l > 0) {
+          T.parent[l][bid] = bid_prev;
+          atomicOr(&T.child_mask[l - 1][bid_prev], 1u << (uint32_t)(kl & ((1u << d) - 1u)));
+          if (m <= l - 1) T.child_begin[l - 1][bid_prev] = bid;
+        }
+        if (l == L) T.first_pt[bid] = (int32_t)pos;
+      }
+      bid_prev = bid;
+    }
+    if (valid) {
+      if (pos == n - 1) T.first_pt[bid_prev + 1] = (int32_t)n;
+      const int32_t j = sidx[pos];
+      T.perm[pos] = j;
+      T.leaf_of[pos] = bid_prev;
+      for (int a = 0; a < d; ++a) T.pts_sorted[pos * d + a] = pts[(int64_t)j * d + a];
+    }
+    __syncthreads();  // woff is rewritten by the next chunk
+  }
+  if (t == 0) *A.err[tree] = errf;
+}
+
 static inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
 // CUB radix-sort tuning for the tree build: the onesweep digit width (the
@@ -350,6 +509,61 @@ static int64_t level_cap(int64_t n, int d, int l) {
   return std::min<int64_t>(n, int64_t(1) << (d * l));
 }
 
+static bool small_tree_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SFT_SMALL_TREE");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+// both trees built by k_small_tree (one launch, no memset of the child masks)
+template <typename KT>
+static bool small_tree_path(int64_t nx, int64_t nk) {
+  constexpr bool bs_fits =
+      sizeof(typename cub::BlockRadixSort<KT, 1024, kBlockSortItems, int32_t, SFT_BS_BITS>::TempStorage) <= 200 * 1024;
+  return bs_fits && nx <= kBlockSortMax && nk <= kBlockSortMax && sort_graph_enabled() && small_tree_enabled();
+}
+
+// full fusion (count / fill inside the sort CTA) up to this many points per tree
+static int64_t small_full_max() {
+  static int64_t v = -1;
+  if (v < 0) {
+    const char* e = getenv("SFT_SMALL_FULL");
+    v = e ? atoll(e) : 2048;
+  }
+  return v;
+}
+
+template <typename KT, bool FULL>
+static cudaError_t launch_small_tree(const SmallTreeArgs& A, const double* x_dev, int64_t nx, const double* k_dev,
+                                     int64_t nk, int d, int L, int64_t N, cudaStream_t s) {
+  const int64_t nmax = std::max(nx, nk);
+  auto run = [&](auto items) -> cudaError_t {
+    constexpr int IT = decltype(items)::value;
+    using BRS = cub::BlockRadixSort<KT, 1024, IT, int32_t, SFT_BS_BITS>;
+    const size_t bsm = sizeof(typename BRS::TempStorage);
+    static PerDevice<int> attr;  // the shared-memory opt-in, once per device and instantiation
+    int one = 0;
+    cudaError_t e = attr.get(&one, [&](int, int* v) {
+      *v = 1;
+      return cudaFuncSetAttribute(k_small_tree<KT, IT, FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm);
+    });
+    if (e != cudaSuccess) return e;
+    k_small_tree<KT, IT, FULL><<<2, 1024, bsm, s>>>(x_dev, nx, k_dev, nk, d, L, (double)N, N, A);
+    return cudaGetLastError();
+  };
+  cudaError_t e;
+  if (nmax <= 1024) e = run(std::integral_constant<int, 1>());
+  else if (nmax <= 2048) e = run(std::integral_constant<int, 2>());
+  else if (nmax <= 4096) e = run(std::integral_constant<int, 4>());
+  else if (nmax <= 8192) e = run(std::integral_constant<int, 8>());
+  else if (nmax <= 11264) e = run(std::integral_constant<int, 11>());
+  else e = run(std::integral_constant<int, kBlockSortItems>());
+  count_launch();
+  return e;
+}
+
 template <typename KT>
 static int sort_and_fill(sft_plan_s* P, const double* x_dev, const double* k_dev, char* arena,
                          const std::vector<size_t>* o_key, const std::vector<size_t>* o_par,
@@ -372,6 +586,51 @@ static int sort_and_fill(sft_plan_s* P, const double* x_dev, const double* k_dev
   const bool use_graph = sort_graph_enabled() && n >= 4096 && !block_sort;
   int dev = 0;
   CK(cudaGetDevice(&dev));
+  auto fill_out = [&](TreeOut& o, int t) {
+    for (int l = 0; l < kMaxLevels; ++l) {
+      const bool ok = l <= L;
+      o.key[l] = ok ? (uint64_t*)(arena + o_key[t][l]) : nullptr;
+      o.parent[l] = ok ? (int32_t*)(arena + o_par[t][l]) : nullptr;
+      o.child_mask[l] = ok ? (uint32_t*)(arena + o_cm[t][l]) : nullptr;
+      o.child_begin[l] = ok ? (int32_t*)(arena + o_cb[t][l]) : nullptr;
+    }
+    o.first_pt = (int32_t*)(arena + o_first[t]);
+    o.leaf_of = (int32_t*)(arena + o_leafof[t]);
+    o.perm = (int32_t*)(arena + o_perm[t]);
+    o.pts_sorted = (double*)(arena + o_pts[t]);
+    o.pts = src[t];
+    o.totals = (int64_t*)(arena + o_tot[t]);
+  };
+  const int64_t nmax = std::max(nx, nk);
+  const bool small = small_tree_path<KT>(nx, nk);
+  auto small_args = [&](SmallTreeArgs& A) {
+    for (int t = 0; t < 2; ++t) {
+      fill_out(A.t[t], t);
+      A.mask[t] = (uint32_t*)(arena + o_cm[t][0]);
+      A.mask_words[t] = (int64_t)(o_cm[t][L] + 4 * level_cap(t ? nk : nx, d, L) - o_cm[t][0]) / 4;
+      A.err[t] = P->d_err + t;  // the two halves of the header's error word
+    }
+  };
+  if (small && nmax <= small_full_max()) {
+    if constexpr (bs_fits) {
+      const size_t so = align_up(sizeof(KT) * n, 256) + 4 * n;
+      char* scr = nullptr;
+      CK(block_alloc((void**)&scr, so, s));
+      SmallTreeArgs A;
+      small_args(A);
+      for (int t = 0; t < 2; ++t) fa.t[t] = A.t[t];
+      A.keys[0] = scr;
+      A.keys[1] = scr + sizeof(KT) * nx;
+      A.idx[0] = (int32_t*)(scr + align_up(sizeof(KT) * n, 256));
+      A.idx[1] = A.idx[0] + nx;
+      A.ioff[0] = A.ioff[1] = 0;
+      CK((launch_small_tree<KT, true>(A, x_dev, nx, k_dev, nk, d, L, P->N, s)));
+      trace_mark("small_tree", s, true);
+      *scr_out = scr;
+      *scr_bytes = so;
+      return SFT_OK;
+    }
+  }
   const bool hit = use_graph && C.exec && C.n == n && C.nx == nx && C.bits == bits && C.ksz == (int)sizeof(KT) &&
                    C.nb == nbx + nbk && C.L == L && C.dev == dev;
   // graph path: X and K sorted as two parallel branches (disjoint halves of the
@@ -424,11 +683,27 @@ static int sort_and_fill(sft_plan_s* P, const double* x_dev, const double* k_dev
   uint8_t* ml = (uint8_t*)(scr + s_ml);
   int32_t* counts = (int32_t*)(scr + s_cnt);
 
-  k_leaf_keys<KT><<<nblk(n, 256), 256, 0, s>>>(x_dev, nx, k_dev, nk, d, L, (double)P->N, P->N, keys_in, idx_in, P->d_err);
-  count_launch();
-  CK(cudaGetLastError());
+  if (small) {  // masks + keys + block sort in one launch; k_count / k_fill below
+    if constexpr (bs_fits) {
+      SmallTreeArgs A;
+      small_args(A);
+      A.keys[0] = keys_out;
+      A.keys[1] = keys_out + nx;
+      A.idx[0] = idx_out;
+      A.idx[1] = idx_out + nx;
+      A.ioff[0] = 0;
+      A.ioff[1] = (int32_t)nx;
+      CK((launch_small_tree<KT, false>(A, x_dev, nx, k_dev, nk, d, L, P->N, s)));
+    }
+  } else {
+    k_leaf_keys<KT><<<nblk(n, 256), 256, 0, s>>>(x_dev, nx, k_dev, nk, d, L, (double)P->N, P->N, keys_in, idx_in,
+                                                 P->d_err);
+    count_launch();
+    CK(cudaGetLastError());
+  }
   trace_mark("keys", s, true);
-  if (block_sort) {
+  if (small) {
+  } else if (block_sort) {
     if constexpr (bs_fits) {
       const int64_t nmax = std::max(nx, nk);
       auto run = [&](auto items) -> cudaError_t {
@@ -506,22 +781,7 @@ static int sort_and_fill(sft_plan_s* P, const double* x_dev, const double* k_dev
 
   fa.bm = bm;
   fa.nbk = nbk;
-  for (int t = 0; t < 2; ++t) {
-    TreeOut& o = fa.t[t];
-    for (int l = 0; l < kMaxLevels; ++l) {
-      const bool ok = l <= L;
-      o.key[l] = ok ? (uint64_t*)(arena + o_key[t][l]) : nullptr;
-      o.parent[l] = ok ? (int32_t*)(arena + o_par[t][l]) : nullptr;
-      o.child_mask[l] = ok ? (uint32_t*)(arena + o_cm[t][l]) : nullptr;
-      o.child_begin[l] = ok ? (int32_t*)(arena + o_cb[t][l]) : nullptr;
-    }
-    o.first_pt = (int32_t*)(arena + o_first[t]);
-    o.leaf_of = (int32_t*)(arena + o_leafof[t]);
-    o.perm = (int32_t*)(arena + o_perm[t]);
-    o.pts_sorted = (double*)(arena + o_pts[t]);
-    o.pts = src[t];
-    o.totals = (int64_t*)(arena + o_tot[t]);
-  }
+  for (int t = 0; t < 2; ++t) fill_out(fa.t[t], t);
   k_fill<KT><<<nbx + nbk, kBlk, 0, s>>>(keys_out, idx_out, ml, counts, fa, d, L);
   count_launch();
   CK(cudaGetLastError());
@@ -596,7 +856,9 @@ int build_trees(sft_plan_s* P, const double* x_dev, const double* k_dev, std::st
   P->X.arena = arena;
   P->X.arena_bytes = off;
   P->K.arena = nullptr;
-  CK(cudaMemsetAsync(arena + cm_lo, 0, cm_hi - cm_lo, s));
+  // (the small-tree kernel zeroes its masks and writes the whole header itself)
+  const bool small = (d * L + 1 <= 32) ? small_tree_path<uint32_t>(nx, nk) : small_tree_path<uint64_t>(nx, nk);
+  if (!small) CK(cudaMemsetAsync(arena + cm_lo, 0, cm_hi - cm_lo, s));
   P->d_err = (int*)(arena + o_errf);  // lives in the arena (freed with the trees)
   trace_mark("arena", s, true);
 
@@ -621,7 +883,7 @@ int build_trees(sft_plan_s* P, const double* x_dev, const double* k_dev, std::st
   if (scr) block_free(scr, scr_bytes, s);
   CK(cudaStreamSynchronize(s));
   trace_mark("sync");
-  const int herr = (int)(h[2 * (L + 1)] & 0xffffffff);
+  const bool herr = h[2 * (L + 1)] != 0;  // either half (the small-tree path flags each tree)
   if (herr) {
     if (err) *err = "a coordinate is non-finite or outside [0,N]";
     return SFT_E_DOMAIN;

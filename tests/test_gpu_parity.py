@@ -491,3 +491,49 @@ def test_host_charges_reusable_after_return():
         assert np.array_equal(u.cpu().numpy(), ref)
         with pytest.raises(ValueError):
             pl.apply(w.f, torch.empty(2 * len(w.x), dtype=torch.complex128, device="cuda")[::2])
+
+
+_SMALL_TREE_CHILD = r"""
+import sys, numpy as np, torch
+import paper_0801_1524_b200 as sft
+d, N, p, nx, nk, seed, out = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3]), int(sys.argv[4]), int(sys.argv[5]), int(sys.argv[6]), sys.argv[7]
+rng = np.random.default_rng(seed)
+x = torch.from_numpy(rng.uniform(0, N, (nx, d))).cuda()
+k = torch.from_numpy(rng.uniform(0, N, (nk, d))).cuda()
+f = torch.from_numpy(rng.normal(size=nk) + 1j * rng.normal(size=nk)).cuda()
+with sft.Plan(d, N, p, x, k) as plan:
+    u = plan.apply(f).cpu().numpy()
+    st = plan.stats()
+np.savez(out, u=u, cx=np.asarray(st["counts_x"]), ck=np.asarray(st["counts_k"]))
+"""
+
+
+@pytest.mark.parametrize("d,N,p,nx,nk", [(2, 1024, 5, 1024, 1025), (2, 256, 7, 16384, 9000), (3, 64, 5, 2047, 3000),
+                                         (2, 1 << 17, 9, 700, 5000), (2, 64, 5, 1, 16384)])
+def test_small_tree_kernel_equals_multikernel_build(d, N, p, nx, nk, tmp_path):
+    """Trees of <= 16K points are built by one fused kernel (k_small_tree:
+    SFT_SMALL_FULL=16384 forces the full fusion, =0 the sort-only fusion
+    followed by k_count / k_fill); SFT_SMALL_TREE=0 selects the separate keys /
+    block sort / count / fill launches.  All must give the same trees, hence bitwise-equal u -- at chunk
+    boundaries (1024, 1025, 16384 points), 3D, 64-bit keys (N = 2^17) and a
+    one-point tree -- and the fused result must match the oracle."""
+    import os
+    import subprocess
+    import sys
+    outs = []
+    for flag in ("1", "0", "2"):
+        out = str(tmp_path / f"u{flag}.npz")
+        env = dict(os.environ, SFT_SMALL_TREE="0" if flag == "0" else "1", SFT_SMALL_FULL="0" if flag == "2" else "16384")
+        subprocess.run([sys.executable, "-c", _SMALL_TREE_CHILD, str(d), str(N), str(p), str(nx), str(nk), "5", out],
+                       check=True, env=env, cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        outs.append(np.load(out))
+    for o in outs[1:]:
+        assert np.array_equal(outs[0]["u"].view(np.uint64), o["u"].view(np.uint64))
+        assert np.array_equal(outs[0]["cx"], o["cx"]) and np.array_equal(outs[0]["ck"], o["ck"])
+    rng = np.random.default_rng(5)
+    x = rng.uniform(0, N, (nx, d))
+    k = rng.uniform(0, N, (nk, d))
+    f = rng.normal(size=nk) + 1j * rng.normal(size=nk)
+    assert list(outs[0]["cx"]) == list(oracle.tree_counts(x, N))
+    if nx * nk <= 5_000_000:
+        assert_close(outs[0]["u"], oracle.butterfly(x, k, f, N, p), PARITY)
