@@ -20,6 +20,7 @@
 // Level arrays live in one arena sized by the upper bound min(n, 2^(d*l)) per
 // level, so nothing on the device waits for the host; the single sync at the
 // end reads the exact counts (the apply needs them to size grids and buffers).
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
 #include "sft_internal.cuh"
@@ -292,6 +293,14 @@ __global__ __launch_bounds__(1024) void k_small_tree(const double* __restrict__ 
   KT* const skey = reinterpret_cast<KT*>(A.keys[tree]);
   int32_t* const sidx = A.idx[tree];
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+#ifdef SFT_TREE_PROF
+  unsigned long long ts[8];
+  int nts = 0;
+  auto stamp = [&]() { asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts[nts++])); };
+#else
+  auto stamp = [&]() {};
+#endif
+  stamp();
   for (int64_t q = t; q < A.mask_words[tree]; q += 1024) A.mask[tree][q] = 0u;
   if (t == 0) errf = 0;
   for (int q = t; q < ITEMS * kMaxLevels; q += 1024) (&cnt[0][0])[q] = 0;
@@ -326,6 +335,7 @@ __global__ __launch_bounds__(1024) void k_small_tree(const double* __restrict__ 
     }
   }
   if (bad) errf = 1;
+  stamp();
   BRS(tmp).SortBlockedToStriped(kk, vv, 0, d * L);  // item i of thread t: sorted position i * 1024 + t
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i)
@@ -341,6 +351,7 @@ __global__ __launch_bounds__(1024) void k_small_tree(const double* __restrict__ 
   }
   __syncthreads();
   const int nch = (int)((n + 1023) / 1024);  // chunks holding points
+  stamp();
   // count: per chunk and level, the boxes its positions open
 #pragma unroll 1
   for (int c = 0; c < nch; ++c) {
@@ -352,6 +363,7 @@ __global__ __launch_bounds__(1024) void k_small_tree(const double* __restrict__ 
     }
   }
   __syncthreads();
+  stamp();
   if (t <= L) {  // exclusive prefix over the chunks; the tree's box totals
     int sacc = 0;
     for (int c = 0; c < ITEMS; ++c) {
@@ -410,6 +422,274 @@ __global__ __launch_bounds__(1024) void k_small_tree(const double* __restrict__ 
     __syncthreads();  // woff is rewritten by the next chunk
   }
   if (t == 0) *A.err[tree] = errf;
+  stamp();
+#ifdef SFT_TREE_PROF
+  if (t == 0)
+    printf("[small_tree] tree %d n %lld: zero+keys %.2f sort %.2f count %.2f fill %.2f us\n", tree, (long long)n,
+           (ts[1] - ts[0]) * 1e-3, (ts[2] - ts[1]) * 1e-3, (ts[3] - ts[2]) * 1e-3, (ts[4] - ts[3]) * 1e-3);
+#endif
+}
+
+// ------------------------------------------------------------------------
+// Trees of 2K..16K points: one thread-block cluster of CL = 8 CTAs builds a
+// tree in one launch.  The sort is a least-significant-digit
+// radix sort with 8-bit digits whose keys never leave the cluster's shared
+// memory.  CTA r owns the r-th contiguous chunk of the current order.  Per
+// digit pass: CTA r ranks its keys by digit, stably (cub::BlockRadixRankMatch,
+// keys in warp-striped order = chunk order), publishes its 256 digit counts;
+// after a cluster barrier every CTA reads all CTAs' counts over distributed
+// shared memory, so a key's place in the whole tree is
+//   (keys of smaller digits in the tree) + (keys of its digit in earlier CTAs)
+//   + (its rank among its digit in this CTA),
+// and it is stored straight into the owner CTA's buffer (DSMEM store); a
+// second barrier ends the pass.  Stable like the device-wide sort, so the
+// order (and the tree) is identical.  The count and fill steps follow in the
+// cluster on the shared-memory-resident sorted chunk (k_count / k_fill with the
+// chunk's exclusive prefix over the earlier CTAs, read over DSMEM).  (Measured:
+// C1's sort 3 passes ~13 us, count ~4, fill ~7 against ~33 + 4 + 8 for the
+// single-CTA sort and the two launches; the same sort with 16-CTA clusters for
+// C2 / C3-sized trees (up to 12 items per thread, 4 passes) was slower than
+// CUB's onesweep, so those keep the device-wide sort.)
+// ------------------------------------------------------------------------
+constexpr int kTreeCl = 8;  // CTAs per tree (portable cluster size)
+constexpr int kRankBits = 8;
+using ClusterRank = cub::BlockRadixRankMatch<1024, kRankBits, false>;
+
+template <typename KT>
+struct DigitOf {
+  uint32_t shift;
+  __device__ __forceinline__ uint32_t Digit(KT k) const { return (uint32_t)(k >> shift) & ((1u << kRankBits) - 1u); }
+};
+
+__device__ __forceinline__ int open_level_kv(uint64_t key, uint64_t prev, bool first, int d, int L) {
+  if (first) return 0;
+  const uint64_t x = key ^ prev;
+  if (x == 0) return L + 1;
+  return L - (63 - __clzll((long long)x)) / d;
+}
+
+template <typename KT, int ITEMS>
+constexpr size_t cluster_tree_smem() {
+  return (sizeof(typename ClusterRank::TempStorage) + 15) / 16 * 16 + (sizeof(KT) + 4) * ITEMS * 1024;
+}
+
+template <typename KT, int ITEMS, int CL>
+__global__ __launch_bounds__(1024) void k_cluster_tree(const double* __restrict__ x, int64_t nx,
+                                                       const double* __restrict__ k, int64_t nk, int d, int L,
+                                                       double Nf, int64_t N, SmallTreeArgs A) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  constexpr int kTile = ITEMS * 1024;
+  extern __shared__ __align__(16) unsigned char ct_smem[];
+  auto& rtmp = *reinterpret_cast<typename ClusterRank::TempStorage*>(ct_smem);
+  KT* const bkey = reinterpret_cast<KT*>(ct_smem + (sizeof(typename ClusterRank::TempStorage) + 15) / 16 * 16);
+  int32_t* const bidx = reinterpret_cast<int32_t*>(bkey + kTile);  // (sizeof(KT) * kTile is a multiple of 16)
+  __shared__ int s_excl[1 << kRankBits], cnt_s[1 << kRankBits], goff[1 << kRankBits], wsum[8];
+  __shared__ int errf;
+  const int r = (int)cl.block_rank();
+  const int tree = blockIdx.x / CL;
+  const TreeOut& T = A.t[tree];
+  const int64_t n = tree ? nk : nx;
+  const double* pts = tree ? k : x;
+  const int64_t chunk = (n + CL - 1) / CL;
+  const int64_t lo = min((int64_t)r * chunk, n);
+  const int len = (int)(min(lo + chunk, n) - lo);
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+#ifdef SFT_TREE_PROF
+  unsigned long long ts[8];
+  int nts = 0;
+  auto stamp = [&]() { asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts[nts++])); };
+#else
+  auto stamp = [&]() {};
+#endif
+  stamp();
+  for (int64_t q = (int64_t)r * 1024 + t; q < A.mask_words[tree]; q += CL * 1024) A.mask[tree][q] = 0u;
+  if (t == 0) errf = 0;
+  cl.sync();  // rank 0's errf initialised before any CTA posts to it
+  // this CTA's chunk, warp-striped (tile position warp * 32 * ITEMS + i * 32 + lane), Morton keys
+  KT kk[ITEMS];
+  int32_t vv[ITEMS];
+  bool bad = false;
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const int tp = warp * 32 * ITEMS + i * 32 + lane;
+    if (tp < len) {
+      const int64_t g = lo + tp;
+      uint64_t c[kMaxDim] = {0, 0, 0};
+#pragma unroll
+      for (int a = 0; a < kMaxDim; ++a) {
+        if (a >= d) break;
+        double y = pts[g * d + a];
+        if (!(y >= 0.0 && y <= Nf)) {
+          bad = true;
+          y = 0.0;
+        }
+        int64_t ci = (int64_t)floor(y);
+        if (ci > N - 1) ci = N - 1;
+        c[a] = (uint64_t)ci;
+      }
+      kk[i] = (KT)(d == 2 ? (spread2(c[0]) << 1) | spread2(c[1])
+                          : (spread3(c[0]) << 2) | (spread3(c[1]) << 1) | spread3(c[2]));
+      vv[i] = (int32_t)g;
+    } else {
+      kk[i] = ~(KT)0;  // padding: digit 255 in every pass, ranked behind every real key of this CTA
+      vv[i] = -1;
+    }
+  }
+  if (bad) atomicOr(cl.map_shared_rank(&errf, 0), 1);
+  stamp();
+  const int bits = d * L;
+  for (int shift = 0; shift < max(bits, 1); shift += kRankBits) {
+    int rank[ITEMS];
+    int excl[1];
+    const DigitOf<KT> dig{(uint32_t)shift};
+    ClusterRank(rtmp).RankKeys(kk, rank, dig, excl);
+    if (t < (1 << kRankBits)) s_excl[t] = excl[0];
+    __syncthreads();
+    if (t < (1 << kRankBits))
+      cnt_s[t] = (t + 1 < (1 << kRankBits) ? s_excl[t + 1] : kTile) - s_excl[t] -
+                 (t + 1 == (1 << kRankBits) ? kTile - len : 0);
+    cl.sync();  // every CTA's digit counts published; every CTA has its keys in registers
+    int tot = 0, before = 0;
+    if (t < (1 << kRankBits)) {
+#pragma unroll
+      for (int q = 0; q < CL; ++q) {
+        const int c = *cl.map_shared_rank(&cnt_s[t], q);
+        tot += c;
+        before += q < r ? c : 0;
+      }
+    }
+    // exclusive scan of the tree's digit totals over the 256 digits (warps 0..7)
+    int inc = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += v;
+    }
+    if (lane == 31 && warp < 8) wsum[warp] = inc;
+    __syncthreads();
+    if (t < (1 << kRankBits)) {
+      int wpre = 0;
+      for (int w = 0; w < warp; ++w) wpre += wsum[w];
+      goff[t] = wpre + inc - tot + before - s_excl[t];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      if (vv[i] >= 0) {
+        const int64_t g = goff[dig.Digit(kk[i])] + rank[i];
+        const int q = (int)(g / chunk);
+        const int o = (int)(g - (int64_t)q * chunk);
+        *cl.map_shared_rank(bkey + o, q) = kk[i];
+        *cl.map_shared_rank(bidx + o, q) = vv[i];
+      }
+    }
+    cl.sync();  // the pass's keys are in their owners' buffers; no count is read any more
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const int tp = warp * 32 * ITEMS + i * 32 + lane;
+      kk[i] = tp < len ? bkey[tp] : ~(KT)0;
+      vv[i] = tp < len ? bidx[tp] : -1;
+    }
+  }
+  stamp();
+  if (r == 0 && t == 0) *A.err[tree] = errf;  // (every flag was posted before the first pass barrier)
+  {
+    // count / fill on the sorted chunk [lo, lo + len) held in bkey / bidx
+    __shared__ int cnt[ITEMS][kMaxLevels];
+    __shared__ int ctot[kMaxLevels], base[kMaxLevels];
+    __shared__ int woff[32][kMaxLevels];
+    for (int q = t; q < ITEMS * kMaxLevels; q += 1024) (&cnt[0][0])[q] = 0;
+    // the key before this chunk (last of the previous CTA's chunk, full since lo > 0)
+    const uint64_t kprev0 = r > 0 && len > 0 ? (uint64_t)*cl.map_shared_rank(bkey + (chunk - 1), r - 1) : 0ull;
+    __syncthreads();
+    auto ml_at = [&](int j) -> int {
+      if (j >= len) return L + 1;
+      const uint64_t key = bkey[j];
+      const uint64_t prev = j > 0 ? (uint64_t)bkey[j - 1] : kprev0;
+      return open_level_kv(key, prev, lo + j == 0, d, L);
+    };
+    const int nch = (len + 1023) / 1024;
+    for (int c = 0; c < nch; ++c) {
+      const int m = ml_at(c * 1024 + t);
+      for (int l = 0; l <= L; ++l) {
+        const unsigned b = __ballot_sync(0xffffffffu, m <= l);
+        if (lane == 0 && b) atomicAdd(&cnt[c][l], __popc(b));
+      }
+    }
+    __syncthreads();
+    if (t <= L) {
+      int sacc = 0;
+      for (int c = 0; c < ITEMS; ++c) {
+        const int v = cnt[c][t];
+        cnt[c][t] = sacc;
+        sacc += v;
+      }
+      ctot[t] = sacc;
+    }
+    cl.sync();
+    if (t <= L) {
+      int b = 0;
+      for (int q = 0; q < r; ++q) b += *cl.map_shared_rank(&ctot[t], q);
+      base[t] = b;
+      if (r == CL - 1) T.totals[t] = b + ctot[t];
+    }
+    cl.sync();  // (no CTA exits while another still reads its ctot / last key)
+    stamp();
+    const unsigned le = (lane == 31) ? 0xffffffffu : ((2u << lane) - 1u);
+    for (int c = 0; c < nch; ++c) {
+      const int j = c * 1024 + t;
+      const int64_t pos = lo + j;
+      const bool valid = j < len;
+      const int m = ml_at(j);
+      for (int l = 0; l <= L; ++l) {
+        const unsigned b = __ballot_sync(0xffffffffu, m <= l);
+        if (lane == 0) woff[warp][l] = __popc(b);
+      }
+      __syncthreads();
+      if (t <= L) {
+        int sacc = 0;
+        for (int w = 0; w < 32; ++w) {
+          const int v = woff[w][t];
+          woff[w][t] = sacc;
+          sacc += v;
+        }
+      }
+      __syncthreads();
+      const uint64_t key = valid ? (uint64_t)bkey[j] : 0ull;
+      int bid_prev = -1;
+      for (int l = 0; l <= L; ++l) {
+        const unsigned b = __ballot_sync(0xffffffffu, m <= l);
+        const int bid = base[l] + cnt[c][l] + woff[warp][l] + __popc(b & le) - 1;
+        if (m <= l) {
+          const uint64_t kl = (key >> (d * (L - l))) & ((1ull << (d * l)) - 1ull);
+          T.key[l][bid] = kl;
+          if (l > 0) {
+            T.parent[l][bid] = bid_prev;
+            atomicOr(&T.child_mask[l - 1][bid_prev], 1u << (uint32_t)(kl & ((1u << d) - 1u)));
+            if (m <= l - 1) T.child_begin[l - 1][bid_prev] = bid;
+          }
+          if (l == L) T.first_pt[bid] = (int32_t)pos;
+        }
+        bid_prev = bid;
+      }
+      if (valid) {
+        if (pos == n - 1) T.first_pt[bid_prev + 1] = (int32_t)n;
+        const int32_t jj = bidx[j];
+        T.perm[pos] = jj;
+        T.leaf_of[pos] = bid_prev;
+        for (int a = 0; a < d; ++a) T.pts_sorted[pos * d + a] = pts[(int64_t)jj * d + a];
+      }
+      __syncthreads();  // woff is rewritten by the next chunk
+    }
+    stamp();
+#ifdef SFT_TREE_PROF
+    if (t == 0 && (r == 0 || r == CL - 1))
+      printf("[cluster_tree] tree %d rank %d n %lld: zero+keys %.2f sort %.2f count %.2f fill %.2f us\n", tree, r,
+             (long long)n, (ts[1] - ts[0]) * 1e-3, (ts[2] - ts[1]) * 1e-3, (ts[3] - ts[2]) * 1e-3,
+             (ts[4] - ts[3]) * 1e-3);
+#endif
+  }
 }
 
 static inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
@@ -525,6 +805,14 @@ static bool small_tree_path(int64_t nx, int64_t nk) {
   return bs_fits && nx <= kBlockSortMax && nk <= kBlockSortMax && sort_graph_enabled() && small_tree_enabled();
 }
 
+static bool cluster_tree_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SFT_CLUSTER_TREE");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
 // full fusion (count / fill inside the sort CTA) up to this many points per tree
 static int64_t small_full_max() {
   static int64_t v = -1;
@@ -564,6 +852,79 @@ static cudaError_t launch_small_tree(const SmallTreeArgs& A, const double* x_dev
   return e;
 }
 
+// cluster tree build (k_cluster_tree, 8 CTAs per tree): items per thread for
+// trees of nmax points, or 0 when the path does not apply (more than 16K
+// points, disabled, or the cluster cannot be scheduled on this device)
+template <typename KT, int IT>
+static cudaError_t cluster_config(cudaLaunchConfig_t* cfg, cudaLaunchAttribute* at, cudaStream_t s) {
+  const size_t bsm = cluster_tree_smem<KT, IT>();
+  static PerDevice<int> attr;  // the shared-memory opt-in, once per device and instantiation
+  int one = 0;
+  cudaError_t e = attr.get(&one, [&](int, int* v) {
+    *v = 1;
+    return cudaFuncSetAttribute(k_cluster_tree<KT, IT, kTreeCl>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)bsm);
+  });
+  if (e != cudaSuccess) return e;
+  *cfg = cudaLaunchConfig_t{};
+  cfg->gridDim = dim3(2 * kTreeCl);
+  cfg->blockDim = dim3(1024);
+  cfg->dynamicSmemBytes = bsm;
+  cfg->stream = s;
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = kTreeCl;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg->attrs = at;
+  cfg->numAttrs = 1;
+  return cudaSuccess;
+}
+template <typename KT, typename F>
+static cudaError_t cluster_dispatch(int items, F&& f) {
+  if (items == 1) return f(std::integral_constant<int, 1>());
+  if (items == 2) return f(std::integral_constant<int, 2>());
+  return cudaErrorInvalidConfiguration;
+}
+template <typename KT>
+static int cluster_tree_items(int64_t nx, int64_t nk) {
+  if (!cluster_tree_enabled() || !sort_graph_enabled() || !small_tree_enabled()) return 0;
+  const int64_t nmax = std::max(nx, nk);
+  const int items = nmax <= kTreeCl * 1024 ? 1 : nmax <= kTreeCl * 2048 ? 2 : 0;
+  if (!items) return 0;
+  static PerDevice<int> ok[2];  // clusters of this instantiation schedulable on the device
+  int v = 0;
+  cudaError_t e = ok[items - 1].get(&v, [&](int, int* r) {
+    *r = 0;
+    cluster_dispatch<KT>(items, [&](auto it) -> cudaError_t {
+      constexpr int IT = decltype(it)::value;
+      cudaLaunchConfig_t cfg;
+      cudaLaunchAttribute at[1];
+      cudaError_t e3 = cluster_config<KT, IT>(&cfg, at, 0);
+      int nc = 0;
+      if (e3 == cudaSuccess) e3 = cudaOccupancyMaxActiveClusters(&nc, k_cluster_tree<KT, IT, kTreeCl>, &cfg);
+      *r = (e3 == cudaSuccess && nc >= 1) ? 1 : 0;
+      return cudaSuccess;
+    });
+    cudaGetLastError();  // a refused configuration only disables the path
+    return cudaSuccess;
+  });
+  return (e == cudaSuccess && v) ? items : 0;
+}
+template <typename KT>
+static cudaError_t launch_cluster_tree(int items, const SmallTreeArgs& A, const double* x_dev, int64_t nx,
+                                       const double* k_dev, int64_t nk, int d, int L, int64_t N, cudaStream_t s) {
+  cudaError_t e = cluster_dispatch<KT>(items, [&](auto it) -> cudaError_t {
+    constexpr int IT = decltype(it)::value;
+    cudaLaunchConfig_t cfg;
+    cudaLaunchAttribute at[1];
+    cudaError_t e1 = cluster_config<KT, IT>(&cfg, at, s);
+    if (e1 != cudaSuccess) return e1;
+    return cudaLaunchKernelEx(&cfg, k_cluster_tree<KT, IT, kTreeCl>, x_dev, nx, k_dev, nk, d, L, (double)N, N, A);
+  });
+  count_launch();
+  return e;
+}
+
 template <typename KT>
 static int sort_and_fill(sft_plan_s* P, const double* x_dev, const double* k_dev, char* arena,
                          const std::vector<size_t>* o_key, const std::vector<size_t>* o_par,
@@ -582,6 +943,10 @@ static int sort_and_fill(sft_plan_s* P, const double* x_dev, const double* k_dev
   // graph of the device-wide sort (or the plain call, SFT_SORT_GRAPH=0)
   constexpr bool bs_fits =
       sizeof(typename cub::BlockRadixSort<KT, 1024, kBlockSortItems, int32_t, SFT_BS_BITS>::TempStorage) <= 200 * 1024;
+  const int64_t nmax = std::max(nx, nk);
+  const bool small = small_tree_path<KT>(nx, nk);
+  // 2K..16K points: the whole build in one cluster launch (k_cluster_tree)
+  const int citems = (small && nmax <= small_full_max()) ? 0 : cluster_tree_items<KT>(nx, nk);
   const bool block_sort = bs_fits && nx <= kBlockSortMax && nk <= kBlockSortMax && sort_graph_enabled();
   const bool use_graph = sort_graph_enabled() && n >= 4096 && !block_sort;
   int dev = 0;
@@ -601,8 +966,6 @@ static int sort_and_fill(sft_plan_s* P, const double* x_dev, const double* k_dev
     o.pts = src[t];
     o.totals = (int64_t*)(arena + o_tot[t]);
   };
-  const int64_t nmax = std::max(nx, nk);
-  const bool small = small_tree_path<KT>(nx, nk);
   auto small_args = [&](SmallTreeArgs& A) {
     for (int t = 0; t < 2; ++t) {
       fill_out(A.t[t], t);
@@ -611,6 +974,24 @@ static int sort_and_fill(sft_plan_s* P, const double* x_dev, const double* k_dev
       A.err[t] = P->d_err + t;  // the two halves of the header's error word
     }
   };
+  if (citems) {
+    const size_t so = align_up(sizeof(KT) * n, 256) + 4 * n;
+    char* scr = nullptr;
+    CK(block_alloc((void**)&scr, so, s));
+    SmallTreeArgs A;
+    small_args(A);
+    for (int t = 0; t < 2; ++t) fa.t[t] = A.t[t];
+    A.keys[0] = scr;
+    A.keys[1] = scr + sizeof(KT) * nx;
+    A.idx[0] = (int32_t*)(scr + align_up(sizeof(KT) * n, 256));
+    A.idx[1] = A.idx[0] + nx;
+    A.ioff[0] = A.ioff[1] = 0;
+    CK(launch_cluster_tree<KT>(citems, A, x_dev, nx, k_dev, nk, d, L, P->N, s));
+    trace_mark("cluster_tree", s, true);
+    *scr_out = scr;
+    *scr_bytes = so;
+    return SFT_OK;
+  }
   if (small && nmax <= small_full_max()) {
     if constexpr (bs_fits) {
       const size_t so = align_up(sizeof(KT) * n, 256) + 4 * n;
@@ -856,7 +1237,7 @@ int build_trees(sft_plan_s* P, const double* x_dev, const double* k_dev, std::st
   P->X.arena = arena;
   P->X.arena_bytes = off;
   P->K.arena = nullptr;
-  // (the small-tree kernel zeroes its masks and writes the whole header itself)
+  // (the small-tree and cluster kernels zero their masks and write the whole header themselves)
   const bool small = (d * L + 1 <= 32) ? small_tree_path<uint32_t>(nx, nk) : small_tree_path<uint64_t>(nx, nk);
   if (!small) CK(cudaMemsetAsync(arena + cm_lo, 0, cm_hi - cm_lo, s));
   P->d_err = (int*)(arena + o_errf);  // lives in the arena (freed with the trees)

@@ -509,11 +509,15 @@ np.savez(out, u=u, cx=np.asarray(st["counts_x"]), ck=np.asarray(st["counts_k"]))
 
 
 @pytest.mark.parametrize("d,N,p,nx,nk", [(2, 1024, 5, 1024, 1025), (2, 256, 7, 16384, 9000), (3, 64, 5, 2047, 3000),
-                                         (2, 1 << 17, 9, 700, 5000), (2, 64, 5, 1, 16384)])
+                                         (2, 1 << 17, 9, 700, 5000), (2, 64, 5, 1, 16384),
+                                         (2, 4096, 5, 16385, 9000)])
 def test_small_tree_kernel_equals_multikernel_build(d, N, p, nx, nk, tmp_path):
-    """Trees of <= 16K points are built by one fused kernel (k_small_tree:
-    SFT_SMALL_FULL=16384 forces the full fusion, =0 the sort-only fusion
-    followed by k_count / k_fill); SFT_SMALL_TREE=0 selects the separate keys /
+    """Trees of <= 16K points are built in one launch: k_small_tree (one CTA
+    per tree; SFT_SMALL_FULL=16384 forces it for every size) or k_cluster_tree
+    (a cluster of 8 CTAs per tree, LSD radix sort over DSMEM, count and fill
+    in the cluster; SFT_SMALL_FULL=0 forces it).  Above 16K (the last case)
+    every mode takes the device-wide sort.  SFT_CLUSTER_TREE=0 with SFT_SMALL_FULL=0 gives the sort-only
+    fusion followed by k_count / k_fill, SFT_SMALL_TREE=0 the separate keys /
     block sort / count / fill launches.  All must give the same trees, hence bitwise-equal u -- at chunk
     boundaries (1024, 1025, 16384 points), 3D, 64-bit keys (N = 2^17) and a
     one-point tree -- and the fused result must match the oracle."""
@@ -521,9 +525,10 @@ def test_small_tree_kernel_equals_multikernel_build(d, N, p, nx, nk, tmp_path):
     import subprocess
     import sys
     outs = []
-    for flag in ("1", "0", "2"):
+    for flag in ("1", "0", "2", "3"):
         out = str(tmp_path / f"u{flag}.npz")
-        env = dict(os.environ, SFT_SMALL_TREE="0" if flag == "0" else "1", SFT_SMALL_FULL="0" if flag == "2" else "16384")
+        env = dict(os.environ, SFT_SMALL_TREE="0" if flag == "0" else "1", SFT_CLUSTER_TREE="0" if flag == "3" else "1",
+                   SFT_SMALL_FULL="16384" if flag == "1" else "0")
         subprocess.run([sys.executable, "-c", _SMALL_TREE_CHILD, str(d), str(N), str(p), str(nx), str(nk), "5", out],
                        check=True, env=env, cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
         outs.append(np.load(out))
