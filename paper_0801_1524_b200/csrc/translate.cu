@@ -1172,7 +1172,11 @@ __device__ unsigned long long* g_instr = nullptr;
 // named barrier over the NT consumer threads (the producer warp never joins)
 template <int NT>
 __device__ __forceinline__ void consumer_sync() {
+#ifdef SFT_ABL_NOBAR  // ablation: no pass barrier (wrong results; timing only)
+  __syncwarp();
+#else
   asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
+#endif
 }
 
 #ifndef SFT_PRODUCER_SLEEP
@@ -1451,17 +1455,31 @@ __global__ __launch_bounds__((NC + 1) * 32, MINB) void k_translate_ws(TransArgs 
         // 1) on the transposed slots, its second pass to HBM
         const unsigned char* bk0 = blk[s];
         const unsigned char* bk1 = blk[s] + SC::BLK;
+        INSTR_T0(t1);
         consumer_pass<D, P, G, NC, 1, false, 1, E>(a, sb, bk0, op, zs, rot, 0);
         consumer_pass<D, P, G, NC, 0, false, 2, E>(a, sb, bk0, op, zs, rot, 0);
+        INSTR_ADD(5, t1);
+        INSTR_T0(t2);
         consumer_sync<NC * 32>();
+        INSTR_ADD(6, t2);
+        INSTR_T0(t3);
         consumer_pass<D, P, G, NC, 0, false, 0, E>(a, sb, bk0, op, zs, rot, 0);
         consumer_pass<D, P, G, NC, 1, false, 3, E>(a, sb, bk0, op, zs, rot, 0);
+        INSTR_ADD(5, t3);
+        INSTR_T0(t4);
         consumer_sync<NC * 32>();
+        INSTR_ADD(6, t4);
+        INSTR_T0(t5);
         consumer_pass<D, P, G, NC, 1, false, 1, E, false, 1>(a, sb, bk1, op, zs, rot, 0);
         consumer_pass<D, P, G, NC, 0, false, 2, E, false, 1>(a, sb, bk1, op, zs, rot, 0);
+        INSTR_ADD(7, t5);
+        INSTR_T0(t6);
         consumer_sync<NC * 32>();
+        INSTR_ADD(6, t6);
+        INSTR_T0(t7);
         consumer_pass<D, P, G, NC, 0, true, 0, E, false, 1>(a, sb, bk1, op, zs, rot, ooff(w));
         consumer_pass<D, P, G, NC, 1, true, 3, E, false, 1>(a, sb, bk1, op, zs, rot, ooff(w));
+        INSTR_ADD(7, t7);
       } else if constexpr (D == 2) {
         INSTR_T0(t1);
         first2d(sb, blk[s]);
@@ -1726,6 +1744,25 @@ template <> struct WsCfg<3, 7> {
 };
 template <> struct WsCfg<3, 9> { static constexpr int G = 1, NC = 8, NST = 2, MINB = 1; };
 
+#ifndef SFT_F2_WIDE
+#define SFT_F2_WIDE 1  // two-level launches of <= one tile per SM: 12 consumer warps per CTA
+#endif
+static int sm_count() {
+  static PerDevice<int> c;
+  int v = 0;
+  c.get(&v, [](int dev, int* r) { return cudaDeviceGetAttribute(r, cudaDevAttrMultiProcessorCount, dev); });
+  return v > 0 ? v : 148;
+}
+
+// two-level launches (small plans, latency-bound): consumer warps per CTA and
+// CTAs per SM (0 = the single-level configuration's)
+#ifndef SFT_F2_NC
+#define SFT_F2_NC 0
+#endif
+#ifndef SFT_F2_MINB
+#define SFT_F2_MINB 0
+#endif
+
 // FP32 storage on the DMMA kernel (the FP32 variant): arrays are half the
 // size, so twice the groups per stage at the same shared memory
 template <int D, int P>
@@ -1864,8 +1901,15 @@ static cudaError_t launch_translate_t(const sft_plan_s* Pl, const LevelDims& L, 
     // even where single-level launches of that p use the skewed one)
     if constexpr (D == 2 && C::G % 4 == 0) {
       constexpr int NST2 = C::NST < 3 ? C::NST : 2;
-      if (a.nrhs > 1) return launch_ws<D, P, C::G, C::NC, NST2, C::MINB, double2, false, true, true>(Pl, a, L, work);
-      return launch_ws<D, P, C::G, C::NC, NST2, C::MINB, double2, false, false, true>(Pl, a, L, work);
+      constexpr int NC2 = SFT_F2_NC > 0 ? SFT_F2_NC : C::NC, MINB2 = SFT_F2_MINB > 0 ? SFT_F2_MINB : C::MINB;
+      if (a.nrhs > 1) return launch_ws<D, P, C::G, NC2, NST2, MINB2, double2, false, true, true>(Pl, a, L, work);
+      // at most one tile per SM (C0's levels): the launch is one tile's latency
+      // chain, so a CTA of 12 consumer warps (fewer super-tiles per warp per
+      // pass) finishes sooner -- C0 translate 0.031 -> 0.027 ms; with more
+      // tiles than SMs the narrower, more numerous CTAs win (C1)
+      if (SFT_F2_WIDE && work <= sm_count())
+        return launch_ws<D, P, C::G, 12, NST2, 1, double2, false, false, true>(Pl, a, L, work);
+      return launch_ws<D, P, C::G, NC2, NST2, MINB2, double2, false, false, true>(Pl, a, L, work);
     }
     return cudaErrorInvalidValue;
   }
