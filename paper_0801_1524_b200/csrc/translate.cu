@@ -361,7 +361,7 @@ __device__ __forceinline__ void load_lane_ops(LaneOps<P>& op, const double* __re
 // ------------------------------------------------------------------------
 // Per tile of G consecutive groups (B-major, A' fastest) one block of BLK
 // bytes in HBM:
-//   cnt[3][3]  int32: per pass AX, task counts of class both / bit-0 only / bit-1 only
+//   cnt[NCNT][3] int32: per list (3D: per round and axis), task counts of class both / bit-0 only / bit-1 only
 //   grp[G]     {pin0, mB}: pair index of the first child array (iB_c, iA') in the
 //              level input, and the child mask of B (children r at pin0 + r*in_nA)
 //   task[D][MAXT] TaskRec, per pass packed in class order
@@ -377,12 +377,16 @@ struct __align__(16) TaskRec {
 template <int D, int P, int G>
 struct Sched {
   static constexpr int MAXT = G << (D - 1);  // tasks per pass (max)
-  // task lists: 3D: list = axis of the pass (2, 1, 0 in order).  2D: list 1 =
-  // first pass on axis 1 and list 0 = last pass on axis 0 (default order);
-  // list 2 = first pass on axis 0 and list 3 = last pass on axis 1 (groups
-  // whose reversed axis order needs fewer MMA k-steps)
+  // task lists: 2D: list 1 = first pass on axis 1 and list 0 = last pass on
+  // axis 0 (default order); list 2 = first pass on axis 0 and list 3 = last
+  // pass on axis 1 (groups whose reversed axis order needs fewer tasks).
+  // 3D: list r = round r of the three passes; every group runs its own axis
+  // order (schedule_round3), so list r holds three sub-lists, one per axis
+  // (2, 1, 0 in that order), each class-sorted, with count triplets
+  // cnt[3 r + k] for the sub-list of axis 2 - k.
   static constexpr int NL = D == 2 ? 4 : D;
-  static constexpr int HDR = 48;  // int cnt[NL][3]
+  static constexpr int NCNT = D == 2 ? 4 : 9;             // count triplets
+  static constexpr int HDR = (NCNT * 12 + 15) / 16 * 16;  // int cnt[NCNT][3]
   static constexpr int GRP = (8 * G + 15) / 16 * 16;
   static constexpr int BLK = HDR + GRP + NL * MAXT * (int)sizeof(TaskRec);
   __device__ __forceinline__ static const int* cnt(const unsigned char* b) { return reinterpret_cast<const int*>(b); }
@@ -507,6 +511,143 @@ __device__ __forceinline__ void schedule_pass(const LevelArgs& a, const GroupMet
     cnt[0] = n3;
     cnt[1] = n1;
     cnt[2] = n2;
+  }
+}
+
+// ---- 3D: per-group axis order --------------------------------------------
+#ifndef SFT_ORDER3
+#define SFT_ORDER3 1
+#endif
+#ifndef SFT_ROUND_UNROLL
+#define SFT_ROUND_UNROLL 1  // 3D rounds 0, 1 unrolled (C3 translate 0.737 -> 0.715 ms, C4 32.8 -> 32.2)
+#endif
+// Projection of a child mask onto a set of axes: bit (c & sel) set for every
+// present child c, sel = the slot bits (bit D-1-a for axis a) of the axes kept.
+__device__ __forceinline__ uint32_t proj_sel(uint32_t m, uint32_t sel) {
+  uint32_t r = 0;
+#pragma unroll
+  for (int c = 0; c < 8; ++c)
+    if (m >> c & 1) r |= 1u << (c & sel);
+  return r;
+}
+__device__ __forceinline__ uint32_t axbit3(int a) { return 1u << (2 - a); }
+
+// Fiber tasks of a group under axis order (o1, o2, o3): pass on o1: one per
+// present beta over {o2, o3}; on o2: per present alpha_o1 x beta_o3; on o3: per
+// present alpha over {o1, o2}.
+__device__ __forceinline__ int order_tasks3(uint32_t mB, uint32_t mA, int o1, int o2, int o3) {
+  const uint32_t b1 = axbit3(o1), b2 = axbit3(o2), b3 = axbit3(o3);
+  return __popc(proj_sel(mB, b2 | b3)) + __popc(proj_sel(mA, b1)) * __popc(proj_sel(mB, b3)) +
+         __popc(proj_sel(mA, b1 | b2));
+}
+
+// The axis order of a 3D group with the fewest fiber tasks, from its own
+// masks only (identical for any partition of the work); ties keep the
+// earlier order of the list, whose first entry (2, 1, 0) is the default.
+// Returns o1 | o2 << 2 | o3 << 4.  (The tasks are 16% fewer than with the
+// fixed order on C3 and 18% on C4; the translation time is linear in them.)
+__device__ __forceinline__ uint32_t best_order3(uint32_t mB, uint32_t mA) {
+  constexpr uint32_t ords[6] = {2u | 1u << 2 | 0u << 4, 2u | 0u << 2 | 1u << 4, 1u | 2u << 2 | 0u << 4,
+                                1u | 0u << 2 | 2u << 4, 0u | 2u << 2 | 1u << 4, 0u | 1u << 2 | 2u << 4};
+  uint32_t best = ords[0];
+  int bt = order_tasks3(mB, mA, 2, 1, 0);
+#pragma unroll
+  for (int i = 1; i < 6; ++i) {
+    const int t = order_tasks3(mB, mA, ords[i] & 3, ords[i] >> 2 & 3, ords[i] >> 4 & 3);
+    if (t < bt) {
+      bt = t;
+      best = ords[i];
+    }
+  }
+  return best;
+}
+
+// Round R (0, 1, 2) of a 3D group's passes under its order ord: the pass on
+// axis ax = o_{R+1}, alpha over the axes done before (Aset), beta over the
+// axes still to come (Bset).  Task = (alpha over Aset, beta over Bset): the
+// fibers of slots (.., beta_ax = 0, ..) / (.., 1, ..); class bit v = the slot
+// with beta_ax = v holds data, i.e. (v, beta over Bset) is a projection of a
+// present child of B onto {ax} u Bset.  Writes the round's three sub-lists
+// (axis 2, 1, 0), class-sorted, with scans over the G-lane segment.
+template <int D, int P, int G, int PS, int R>
+__device__ __forceinline__ void schedule_round3(const LevelArgs& a, const GroupMeta& m, uint32_t ord, bool valid,
+                                                bool write_cnt, int* cnt, TaskRec* out) {
+  static_assert(D == 3, "3D rounds");
+  constexpr int PD = PS;
+  constexpr bool LAST = R == 2;
+  const int lane = threadIdx.x & 31;
+  const int ax = (int)(ord >> (2 * R) & 3u);
+  uint32_t selA = 0, selB = 0;
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    const uint32_t b = axbit3((int)(ord >> (2 * q) & 3u));
+    if (q < R) selA |= b;
+    if (q > R) selB |= b;
+  }
+  const uint32_t bax = axbit3(ax);
+  const uint32_t pA = proj_sel(m.mA, selA), pB = proj_sel(m.mB, selB), pBa = proj_sel(m.mB, selB | bax);
+  TaskRec mine[4];
+  int n = 0;
+  int cc[3] = {0, 0, 0};  // class 3 / 1 / 2 counts
+  if (valid) {
+    // alpha and beta bits live in disjoint slot bits: enumerate sl over the
+    // subsets of selA | selB
+    const uint32_t selAB = selA | selB;
+    for (uint32_t sl = 0; sl < 8u; ++sl) {
+      if (sl & ~selAB) continue;
+      if (!(pA >> (sl & selA) & 1u) || !(pB >> (sl & selB) & 1u)) continue;
+      const uint32_t sb = sl & selB;
+      const uint32_t cls = (pBa >> sb & 1u) | ((pBa >> (sb | bax) & 1u) << 1);
+      TaskRec t;
+      t.x = (uint32_t)(sl * (G * PD + SlotPad<D, P, PD>::v) + (lane % G) * PD);
+      t.cls = cls;
+      t.o0 = t.o1 = ~0u;
+      if (LAST) {
+        const int64_t q0 = out_pair(a, m, (int)sl), q1 = out_pair(a, m, (int)(sl | bax));
+        if (q0 >= 0) t.o0 = (uint32_t)(q0 * PD);
+        if (q1 >= 0) t.o1 = (uint32_t)(q1 * PD);
+      }
+      mine[n++ & 3] = t;
+      cc[cls == 3 ? 0 : (cls == 1 ? 1 : 2)]++;
+    }
+  }
+  // per (sub-list k = 2 - ax, class) exclusive offsets over the segment
+  const int k = 2 - ax;
+  int v[9], tot[9];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) v[i] = (valid && i / 3 == k) ? cc[i % 3] : 0;
+  const int j = lane % G;
+#pragma unroll
+  for (int i = 0; i < 9; ++i) {
+    int s = v[i];
+#pragma unroll
+    for (int d = 1; d < G; d <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, s, d, G);
+      if (j >= d) s += t;
+    }
+    tot[i] = __shfl_sync(0xffffffffu, s, G - 1, G);
+    v[i] = s - v[i];  // exclusive
+  }
+  int base = 0, off[3] = {0, 0, 0};
+#pragma unroll
+  for (int kk = 0; kk < 3; ++kk) {
+    if (kk == k) {
+      off[0] = base + v[3 * kk];
+      off[1] = base + tot[3 * kk] + v[3 * kk + 1];
+      off[2] = base + tot[3 * kk] + tot[3 * kk + 1] + v[3 * kk + 2];
+    }
+    base += tot[3 * kk] + tot[3 * kk + 1] + tot[3 * kk + 2];
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    if (q < n) {
+      const TaskRec t = mine[q];
+      out[t.cls == 3 ? off[0]++ : (t.cls == 1 ? off[1]++ : off[2]++)] = t;
+    }
+  }
+  if (j == 0 && write_cnt) {
+#pragma unroll
+    for (int i = 0; i < 9; ++i) cnt[i] = tot[i];
   }
 }
 
@@ -665,9 +806,11 @@ __global__ __launch_bounds__(128) void k_schedule(const __grid_constant__ SchedL
     schedule_pass<D, P, G, PS, 0, false, true>(a, m, valid && rev, tv, cnt + 6, tk + 2 * SC::MAXT);
     schedule_pass<D, P, G, PS, 1, true, true>(a, m, valid && rev, tv, cnt + 9, tk + 3 * SC::MAXT);
   } else {
-    schedule_pass<D, P, G, PS, 2, false>(a, m, valid, tv, cnt + 6, tk + 2 * SC::MAXT);
-    schedule_pass<D, P, G, PS, 1, false>(a, m, valid, tv, cnt + 3, tk + SC::MAXT);
-    schedule_pass<D, P, G, PS, 0, true>(a, m, valid, tv, cnt, tk);
+    // per-group axis order (SFT_ORDER3=0: the fixed order 2, 1, 0)
+    const uint32_t ord = (SFT_ORDER3 && valid) ? best_order3(m.mB, m.mA) : (2u | 1u << 2);
+    schedule_round3<D, P, G, PS, 0>(a, m, ord, valid, tv, cnt, tk);
+    schedule_round3<D, P, G, PS, 1>(a, m, ord, valid, tv, cnt + 9, tk + SC::MAXT);
+    schedule_round3<D, P, G, PS, 2>(a, m, ord, valid, tv, cnt + 18, tk + 2 * SC::MAXT);
   }
 }
 
@@ -689,14 +832,21 @@ __global__ void k_check_schedule(TransArgs a, const unsigned char* __restrict__ 
     const int np = __popc(gr.y);
     if (np > 0 && (int64_t)gr.x + (int64_t)(np - 1) * a.in_nA >= in_pairs) bad = true;
   }
-  for (int ax = 0; ax < SC::NL; ++ax) {
-    const int* c = SC::cnt(b) + 3 * ax;
-    const int nt = c[0] + c[1] + c[2];
-    if (c[0] < 0 || c[1] < 0 || c[2] < 0 || nt > SC::MAXT) bad = true;
+  // lists: 2D one count triplet each; 3D three (sub-lists of axes 2, 1, 0)
+  constexpr int SUB = D == 2 ? 1 : 3;
+  for (int l = 0; l < SC::NL; ++l) {
+    const int* c = SC::cnt(b) + 3 * SUB * l;
+    int nt = 0;
+    for (int q = 0; q < 3 * SUB; ++q) {
+      if (c[q] < 0) bad = true;
+      nt += c[q];
+    }
+    if (nt > SC::MAXT) bad = true;
+    const bool last = D == 2 ? (l == 0 || l == 3) : l == 2;
     for (int t = 0; t < nt && t < SC::MAXT; ++t) {
-      const TaskRec r = SC::task(b, ax)[t];
+      const TaskRec r = SC::task(b, l)[t];
       if (r.x >= STAGE || r.cls < 1 || r.cls > 3) bad = true;
-      if (ax == 0 || ax == 3) {
+      if (last) {
         if (r.o0 != ~0u && (int64_t)r.o0 / PD >= out_pairs) bad = true;
         if (r.o1 != ~0u && (int64_t)r.o1 / PD >= out_pairs) bad = true;
       }
@@ -977,7 +1127,7 @@ template <int D, int P, int G, int NC, int AX, bool LAST, int LIST = AX, typenam
           int MUL = 0, bool STAGED = false>
 __device__ __forceinline__ void consumer_pass(const TransArgs& a, E* __restrict__ sb,
                                               const unsigned char* __restrict__ blk, const LaneOps<P>& op,
-                                              const E* __restrict__ zs, int& rot, int64_t ooff = 0) {
+                                              const E* __restrict__ zs, int& rot, int64_t ooff = 0, int round = 0) {
   constexpr int ES = sizeof(E);
   const uint32_t sba = smem_u32(sb), zsa = smem_u32(zs);  // stage and zero slot (shared addresses)
   using S = SymShape<P>;
@@ -991,9 +1141,22 @@ __device__ __forceinline__ void consumer_pass(const TransArgs& a, E* __restrict_
   constexpr int SH = D - 1 - AX;
   constexpr int C1 = (1 << SH) * (MUL == 0 ? G * PD + SlotPad<D, P, PD>::v : MUL * PD);  // child-1 slot of the pair
   E* const gout = reinterpret_cast<E*>(a.out) + ooff;  // ooff: RHS offset of a batch
-  const int* cnt = SC::cnt(blk) + 3 * LIST;
-  const TaskRec* tasks = SC::task(blk, LIST);
+  const int* cnt;
+  const TaskRec* tasks;
+  if constexpr (D == 3) {
+    // round `round`, sub-list of axis AX (k = 2 - AX) after the sub-lists of the axes above it
+    const int* cr = SC::cnt(blk) + 9 * round;
+    int off = 0;
+#pragma unroll
+    for (int kk = 0; kk < 2 - AX; ++kk) off += cr[3 * kk] + cr[3 * kk + 1] + cr[3 * kk + 2];
+    cnt = cr + 3 * (2 - AX);
+    tasks = SC::task(blk, round) + off;
+  } else {
+    cnt = SC::cnt(blk) + 3 * LIST;
+    tasks = SC::task(blk, LIST);
+  }
   const int ntot = (cnt[0] + cnt[1] + cnt[2]) * PF;
+  if (ntot == 0) return;  // (3D: most sub-lists of a round are empty)
   const int nst = (ntot + 7) >> 3;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int c = lane & 3;
@@ -1133,8 +1296,9 @@ __device__ __forceinline__ void tma_store_tile(const TransArgs& a, const unsigne
     asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src), "r"(BYTES)
                  : "memory");
   };
+  static_assert(D == 2, "staged last pass: 2D only");
 #pragma unroll
-  for (int li = 0; li < (D == 2 ? 2 : 1); ++li) {
+  for (int li = 0; li < 2; ++li) {
     // last-pass lists: 0 (axis 0: child slots (1 << (d-1)) G arrays apart), 3 (2D reversed order: axis 1, G apart)
     const int L = li == 0 ? 0 : 3;
     const uint32_t C1 = (uint32_t)((li == 0 ? (1 << (D - 1)) : 1) * (G * PS + SlotPad<D, P, PS>::v));
@@ -1411,7 +1575,7 @@ __global__ __launch_bounds__((NC + 1) * 32, MINB) void k_translate_ws(TransArgs 
   const int64_t nwork = BATCH ? ntiles * a.nrhs : ntiles;
   auto ooff = [&](int64_t w_) { return BATCH ? (w_ % a.nrhs) * a.rs : (int64_t)0; };
   // the last pass in place + TMA bulk stores (non-skewed single-level tiles)
-  constexpr bool STAGE_OUT = SFT_TMA_STORE && !FUSED && !F2;
+  constexpr bool STAGE_OUT = SFT_TMA_STORE && !FUSED && !F2 && D == 2;  // (2D only)
   if constexpr (D == 2 && NST >= 3 && !F2) {
     int64_t tile = blockIdx.x;
     if (tile < nwork) {
@@ -1498,17 +1662,22 @@ __global__ __launch_bounds__((NC + 1) * 32, MINB) void k_translate_ws(TransArgs 
         }
         INSTR_ADD(7, t3);
       } else {
-        consumer_pass<D, P, G, NC, 2, false, 2, E>(a, sb, blk[s], op, zs, rot, 0);
-        consumer_sync<NC * 32>();
-        consumer_pass<D, P, G, NC, 1, false, 1, E>(a, sb, blk[s], op, zs, rot, 0);
-        consumer_sync<NC * 32>();
-        if constexpr (STAGE_OUT) {
-          consumer_pass<D, P, G, NC, 0, true, 0, E, false, 0, true>(a, sb, blk[s], op, zs, rot, 0);
+        // 3D: rounds 0, 1 in place, round 2 to HBM; in each round every group
+        // runs the pass of its own order's axis (sub-lists of axes 2, 1, 0)
+#if SFT_ROUND_UNROLL
+#pragma unroll
+#else
+#pragma unroll 1
+#endif
+        for (int r = 0; r < 2; ++r) {
+          consumer_pass<D, P, G, NC, 2, false, 0, E>(a, sb, blk[s], op, zs, rot, 0, r);
+          consumer_pass<D, P, G, NC, 1, false, 0, E>(a, sb, blk[s], op, zs, rot, 0, r);
+          consumer_pass<D, P, G, NC, 0, false, 0, E>(a, sb, blk[s], op, zs, rot, 0, r);
           consumer_sync<NC * 32>();
-          if (warp == 0) tma_store_tile<D, P, G, E>(a, blk[s], sb, ooff(w));
-        } else {
-          consumer_pass<D, P, G, NC, 0, true, 0, E, FUSED>(a, sb, blk[s], op, zs, rot, ooff(w));
         }
+        consumer_pass<D, P, G, NC, 2, true, 0, E, FUSED>(a, sb, blk[s], op, zs, rot, ooff(w), 2);
+        consumer_pass<D, P, G, NC, 1, true, 0, E, FUSED>(a, sb, blk[s], op, zs, rot, ooff(w), 2);
+        consumer_pass<D, P, G, NC, 0, true, 0, E, FUSED>(a, sb, blk[s], op, zs, rot, ooff(w), 2);
       }
       __syncwarp();
       if (lane == 0)
@@ -2033,7 +2202,7 @@ static void schedule_work_g(const unsigned char* h, size_t bytes, int nb, double
   double st = 0, tasks = 0;
   for (size_t o = 0; o + blk <= bytes; o += blk) {
     const int* cnt = reinterpret_cast<const int*>(h + o);
-    for (int l = 0; l < SC::NL; ++l) {
+    for (int l = 0; l < SC::NCNT; ++l) {  // (3D: every sub-list is its own super-tile loop)
       const int nt = cnt[3 * l] + cnt[3 * l + 1] + cnt[3 * l + 2];
       tasks += nt;
       st += (nt * PF + 7) / 8;
