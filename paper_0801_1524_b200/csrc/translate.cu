@@ -1369,10 +1369,14 @@ __device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
 // schedule block and every present child array.  gr = this lane's group
 // record (first child pair index, child mask) for lane < G.
 // NB: schedule blocks per tile (2 for a two-level tile: one per level)
+// nrec_src / nrec_dst (producer-less kernels): also bulk-copy the group
+// records of the work item that will next use this stage (the tile's stage
+// refill then needs no HBM read of its own), nrec_src = nullptr: none.
 template <int D, int P, int G, int NST, typename E, int PS, bool BATCH, int NB = 1>
 __device__ __forceinline__ void ws_issue(const TransArgs& a, const unsigned char* __restrict__ sched, int64_t w,
                                          int64_t tile, uint2 gr, E* ring,
-                                         unsigned char (*blk)[Sched<D, P, G>::BLK * NB], uint64_t* full, int s) {
+                                         unsigned char (*blk)[Sched<D, P, G>::BLK * NB], uint64_t* full, int s,
+                                         const unsigned char* nrec_src = nullptr, uint32_t nrec_dst = 0) {
   using SC = Sched<D, P, G>;
   constexpr int PD = PS;  // stage and HBM arrays have stride PS elements of type E
   constexpr int NS = 1 << D;
@@ -1419,13 +1423,18 @@ __device__ __forceinline__ void ws_issue(const TransArgs& a, const unsigned char
   __syncwarp();
   if (lane == 0) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&full[s])),
-                 "r"(nbytes + (uint32_t)(SC::BLK * NB))
+                 "r"(nbytes + (uint32_t)(SC::BLK * NB) + (nrec_src ? (uint32_t)SC::GRP : 0u))
                  : "memory");
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
             smem_u32(&blk[s][0])),
         "l"(sched + tile * (SC::BLK * NB)), "r"((uint32_t)(SC::BLK * NB)), "r"(smem_u32(&full[s]))
         : "memory");
+    if (nrec_src)
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(nrec_dst),
+          "l"(nrec_src), "r"((uint32_t)SC::GRP), "r"(smem_u32(&full[s]))
+          : "memory");
   }
   __syncwarp();
   if (uniform) {
@@ -1524,9 +1533,16 @@ __device__ __forceinline__ void ws_producer(const TransArgs& a, const unsigned c
 // 2D with NST >= 3: skewed pipeline, pass 1 of tile i+1 runs before pass 0 of
 // tile i, and pass 0 waits on an mbarrier (p1done) every consumer thread
 // arrives on after its pass-1 rows, so warps do not idle at a pass barrier.
+//
+// PL (producer-less, SFT_PL=1; measured slower, off): no producer warp -- all NC warps consume; warp 0
+// issues the first NST tiles, and afterwards the last consumer warp to finish
+// a tile (smem counter done[s]) refills its stage with the work item NST
+// grid-strides ahead.  The group records that refill needs arrived in the
+// stage bookkeeping (nrec[s]) with the tile's own loads, so it reads no HBM.
+// Same threads per CTA as NC - 1 consumers + a producer, one more consumer.
 template <int D, int P, int G, int NC, int NST, int MINB, typename E = double2, bool FUSED = false,
-          bool BATCH = false, bool F2 = false>
-__global__ __launch_bounds__((NC + 1) * 32, MINB) void k_translate_ws(TransArgs a,
+          bool BATCH = false, bool F2 = false, bool PL = false>
+__global__ __launch_bounds__((NC + (PL ? 0 : 1)) * 32, MINB) void k_translate_ws(TransArgs a,
                                                                                   const double* __restrict__ frag,
                                                                                   const unsigned char* __restrict__ sched,
                                                                                   int64_t ntiles) {
@@ -1541,8 +1557,11 @@ __global__ __launch_bounds__((NC + 1) * 32, MINB) void k_translate_ws(TransArgs 
   constexpr int NB = F2 ? 2 : 1;  // schedule blocks per tile
   __shared__ __align__(128) unsigned char blk[NST][SC::BLK * NB];
   __shared__ __align__(8) uint64_t full[NST], empty[NST], p1done[NST];
+  __shared__ __align__(16) unsigned char nrec[PL ? NST : 1][SC::GRP];  // PL: group records of the stage's next item
+  __shared__ int done[NST];                                            // PL: consumer warps done with the stage
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (threadIdx.x < NST) {
+    done[threadIdx.x] = 0;
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full[threadIdx.x])));
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&empty[threadIdx.x])), "r"(NC));
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&p1done[threadIdx.x])), "r"(NC * 32));
@@ -1551,13 +1570,63 @@ __global__ __launch_bounds__((NC + 1) * 32, MINB) void k_translate_ws(TransArgs 
   for (int q = threadIdx.x; q < PD * (int)sizeof(E) / 16; q += blockDim.x)
     reinterpret_cast<float4*>(zs)[q] = make_float4(0.f, 0.f, 0.f, 0.f);
   __syncthreads();
-  if (warp == NC) {
-    ws_producer<D, P, G, NST, E, PD, BATCH, NB>(a, sched, ntiles, ring, blk, full, empty);
-    return;
+  if constexpr (!PL) {
+    if (warp == NC) {
+      ws_producer<D, P, G, NST, E, PD, BATCH, NB>(a, sched, ntiles, ring, blk, full, empty);
+      return;
+    }
   }
   // ---------------- consumers ----------------
   LaneOps<P> op;
   load_lane_ops(op, frag, lane);
+  const int64_t nr_ = BATCH ? a.nrhs : 1;
+  const int64_t nwork_ = ntiles * nr_;
+  // PL: issue work item w into stage s (one whole warp), with the group
+  // records of item w + NST * grid (the stage's next item) when it exists
+  auto pl_issue = [&](int64_t w, uint2 gr, int st) {
+    const int64_t wn = w + (int64_t)NST * gridDim.x;
+    const unsigned char* nsrc =
+        wn < nwork_ ? sched + (BATCH ? wn / nr_ : wn) * (int64_t)(SC::BLK * NB) + SC::HDR : nullptr;
+    ws_issue<D, P, G, NST, E, PD, BATCH, NB>(a, sched, w, BATCH ? w / nr_ : w, gr, ring, blk, full, st, nsrc,
+                                             smem_u32(&nrec[PL ? st : 0][0]));
+  };
+  if constexpr (PL) {
+    // programmatic dependent launch: the previous level's data is touched only
+    // after it has completed (every thread: any warp may issue a refill)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (warp == 0) {
+      for (int i = 0; i < NST; ++i) {
+        const int64_t w = blockIdx.x + (int64_t)i * gridDim.x;
+        if (w >= nwork_) break;
+        pl_issue(w, ws_group_record<D, P, G, NB>(sched, BATCH ? w / nr_ : w, true), i);
+      }
+    }
+  }
+  // a consumer warp is done with the item w in stage st: PL -- the last warp
+  // to get here refills the stage; otherwise release it to the producer
+  auto release = [&](int64_t w, int st) {
+    __syncwarp();
+    if constexpr (PL) {
+      int last = 0;
+      if (lane == 0) {
+        int old;
+        asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;" : "=r"(old) : "r"(smem_u32(&done[st])) : "memory");
+        last = old == NC - 1;
+        if (last) done[st] = 0;
+      }
+      last = __shfl_sync(0xffffffffu, last, 0);
+      if (last) {
+        const int64_t wn = w + (int64_t)NST * gridDim.x;
+        if (wn < nwork_) {
+          const uint2 gr = lane < G ? reinterpret_cast<const uint2*>(&nrec[PL ? st : 0][0])[lane] : make_uint2(0u, 0u);
+          pl_issue(wn, gr, st);
+        }
+      }
+    } else {
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[st])) : "memory");
+    }
+  };
   int s = 0, rot = 0;
   uint32_t ph = 0;
   INSTR_T0(tc0);
@@ -1602,9 +1671,7 @@ __global__ __launch_bounds__((NC + 1) * 32, MINB) void k_translate_ws(TransArgs 
       INSTR_T0(t3);
       last2d(ring + s * STAGE, blk[s], ooff(tile));
       INSTR_ADD(7, t3);
-      __syncwarp();
-      if (lane == 0)
-        asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[s])) : "memory");
+      release(tile, s);
       s = sn;
       ph = phn;
     }
@@ -1679,9 +1746,7 @@ __global__ __launch_bounds__((NC + 1) * 32, MINB) void k_translate_ws(TransArgs 
         consumer_pass<D, P, G, NC, 1, true, 0, E, FUSED>(a, sb, blk[s], op, zs, rot, ooff(w), 2);
         consumer_pass<D, P, G, NC, 0, true, 0, E, FUSED>(a, sb, blk[s], op, zs, rot, ooff(w), 2);
       }
-      __syncwarp();
-      if (lane == 0)
-        asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[s])) : "memory");
+      release(w, s);
       if (++s == NST) {
         s = 0;
         ph ^= 1u;
@@ -2030,11 +2095,21 @@ static cudaError_t persistent_grid(K kernel, int threads, size_t smem, int* grid
 }
 
 // One persistent launch of k_translate_ws<D, P, G, NC, NST, MB, E, FUSED, BATCH, F2>
+// NC: consumer warps of the producer design; the producer-less kernel (SFT_PL=1)
+// runs NC + 1 consumers in the same (NC + 1) * 32 threads.  Measured slower
+// (C2 translate 0.938 -> 1.042 ms, C3 0.714 -> 0.778, C4 32.0 -> 35.4): the
+// refill work lands on a consumer, and one more warp per pass barrier gets
+// fewer super-tiles each; off.
+#ifndef SFT_PL
+#define SFT_PL 0
+#endif
 template <int D, int P, int G, int NC, int NST, int MB, typename E, bool FUSED, bool BATCH, bool F2>
 static cudaError_t launch_ws(const sft_plan_s* Pl, const TransArgs& a, const LevelDims& L, int64_t work) {
   constexpr int PS = StrideT<E, Pow<P, D>::v>::v;
   const size_t smem = ((size_t)NST * (1 << D) * (G * PS + SlotPad<D, P, PS>::v) + PS) * sizeof(E);  // ring + zero slot
-  auto kern = k_translate_ws<D, P, G, NC, NST, MB, E, FUSED, BATCH, F2>;
+  constexpr bool PLK = SFT_PL != 0;
+  constexpr int NCK = PLK ? NC + 1 : NC;
+  auto kern = k_translate_ws<D, P, G, NCK, NST, MB, E, FUSED, BATCH, F2, PLK>;
   static PerDevice<int> grid_cache;  // this instantiation's grid and smem opt-in, per device
   int grid_max = 0;
   cudaError_t e = persistent_grid(kern, (NC + 1) * 32, smem, &grid_max, grid_cache);
