@@ -120,6 +120,10 @@ __global__ __launch_bounds__(128, D == 2 ? SFT_LEAF_MINB2 : 2) void k_leaf(const
     inv_s[threadIdx.x] = invD[threadIdx.x];
   }
   __syncthreads();
+  // launched with PDL (launch_pdl): the sources, charges and level buffer are
+  // touched only after the previous kernel has completed
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t kw = (int64_t)blockIdx.x * 4 + warp;
   // leaves [lb, le) of this warp: first source in [s0 + W kw, s0 + W (kw+1))
@@ -204,6 +208,9 @@ __global__ __launch_bounds__(128, D == 2 ? SFT_FINAL_MINB2 : SFT_FINAL_MINB3) vo
   constexpr int P1 = P - 1;
   const int64_t j = i_lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (j >= i_hi) return;
+  // launched with PDL (launch_pdl) behind the last translation: the target
+  // side (plan data, complete before that translation started) is set up
+  // while it drains; h is read after griddepcontrol.wait below
   const int64_t lj = (int64_t)leaf_of[j];
   const T2* const hl = h0 + (lj - a_lo) * (int64_t)PS;
   const int64_t pj = perm ? (int64_t)perm[j] : j - i_lo;  // perm == nullptr: sorted output
@@ -231,6 +238,8 @@ __global__ __launch_bounds__(128, D == 2 ? SFT_FINAL_MINB2 : SFT_FINAL_MINB3) vo
   el[0] = make_double2(1.0, 0.0);
 #pragma unroll
   for (int l = 1; l < P; ++l) el[l] = cmul(el[l - 1], z[D - 1]);
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   // the powers are shared by every RHS of a batch (sft_apply_batch)
   for (int rh = 0; rh < nrhs; ++rh) {
   const T2* h = hl + (int64_t)rh * hrs;
@@ -323,14 +332,14 @@ cudaError_t launch_leaf(const sft_plan_s* Pl, const double2* f, void* out, int64
   const unsigned nb = (unsigned)((nw + 3) / 4);
   if (Pl->prec == 1) {
     SFT_DISPATCH(Pl->d, Pl->p,
-                 (k_leaf<D, P, float2, Pow<P, D>::v + (Pow<P, D>::v & 1)><<<nb, 128, 0, Pl->stream>>>(
+                 launch_pdl(k_leaf<D, P, float2, Pow<P, D>::v + (Pow<P, D>::v & 1)>, nb, 128, 0, Pl->stream,
                      Pl->K.pts_sorted, Pl->K.perm, Pl->K.first_pt, Pl->K.leaf_of, f, Pl->tab->leaf_invD, (float2*)out, b_lo, b_hi,
-                     Pl->N, Pl->conj, nrhs, ldf, ors, Pl->ffmod && !Pl->conj)));
+                     Pl->N, Pl->conj, nrhs, ldf, ors, Pl->ffmod && !Pl->conj));
   } else {
     SFT_DISPATCH(Pl->d, Pl->p,
-                 (k_leaf<D, P, double2, StrideT<double2, Pow<P, D>::v>::v><<<nb, 128, 0, Pl->stream>>>(
+                 launch_pdl(k_leaf<D, P, double2, StrideT<double2, Pow<P, D>::v>::v>, nb, 128, 0, Pl->stream,
                      Pl->K.pts_sorted, Pl->K.perm, Pl->K.first_pt, Pl->K.leaf_of, f, Pl->tab->leaf_invD, (double2*)out, b_lo, b_hi,
-                     Pl->N, Pl->conj, nrhs, ldf, ors, Pl->ffmod && !Pl->conj)));
+                     Pl->N, Pl->conj, nrhs, ldf, ors, Pl->ffmod && !Pl->conj));
   }
   count_launch();
   return cudaGetLastError();
@@ -343,14 +352,14 @@ cudaError_t launch_final(const sft_plan_s* Pl, const void* h0, double2* u, int64
   const unsigned nb = (unsigned)((i_hi - i_lo + 127) / 128);
   if (Pl->prec == 1) {
     SFT_DISPATCH(Pl->d, Pl->p,
-                 (k_final<D, P, float2, Pow<P, D>::v + (Pow<P, D>::v & 1)><<<nb, 128, 0, Pl->stream>>>(
+                 launch_pdl(k_final<D, P, float2, Pow<P, D>::v + (Pow<P, D>::v & 1)>, nb, 128, 0, Pl->stream,
                      Pl->X.pts_sorted, sorted_out ? nullptr : Pl->X.perm, Pl->X.leaf_of, (const float2*)h0, u, i_lo, i_hi, a_lo, Pl->N,
-                     Pl->conj, nrhs, hrs, ldu, Pl->ffmod && Pl->conj)));
+                     Pl->conj, nrhs, hrs, ldu, Pl->ffmod && Pl->conj));
   } else {
     SFT_DISPATCH(Pl->d, Pl->p,
-                 (k_final<D, P, double2, StrideT<double2, Pow<P, D>::v>::v><<<nb, 128, 0, Pl->stream>>>(
+                 launch_pdl(k_final<D, P, double2, StrideT<double2, Pow<P, D>::v>::v>, nb, 128, 0, Pl->stream,
                      Pl->X.pts_sorted, sorted_out ? nullptr : Pl->X.perm, Pl->X.leaf_of, (const double2*)h0, u, i_lo, i_hi, a_lo, Pl->N,
-                     Pl->conj, nrhs, hrs, ldu, Pl->ffmod && Pl->conj)));
+                     Pl->conj, nrhs, hrs, ldu, Pl->ffmod && Pl->conj));
   }
   count_launch();
   return cudaGetLastError();

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -290,5 +291,38 @@ void trace_mark(const char* what, cudaStream_t s = nullptr, bool dev = false);  
 // number of kernels this library has launched (own kernels; CUB's internal
 // sort/scan kernels are not counted), for bench.py's gpu_launches
 void count_launch(int n = 1);
+
+// SFT_PDL=0 disables programmatic dependent launch (ablation)
+inline bool pdl_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SFT_PDL");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+// Launch with programmatic stream serialization (PDL): the kernel may start
+// while the previous kernel on the stream drains; it must execute
+// griddepcontrol.wait before touching that kernel's data (or anything an
+// earlier kernel wrote), and every kernel triggers its own dependents
+// (griddepcontrol.launch_dependents) only after that wait, so a dependent's
+// pre-wait prologue never overlaps anything but its direct predecessor.
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kernel)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t st,
+                       Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 
 }  // namespace sft

@@ -1504,6 +1504,7 @@ __device__ __forceinline__ void ws_producer(const TransArgs& a, const unsigned c
   // the previous level's output (our input) and input (our output buffer)
   // are touched only after it has completed
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // (after the wait: see launch_pdl)
   for (int i = 0; w < nwork; ++i) {
     const int64_t wn = w + gridDim.x;
     const int64_t next = BATCH ? wn / nr : wn;
@@ -1579,6 +1580,10 @@ __global__ __launch_bounds__((NC + (PL ? 0 : 1)) * 32, MINB) void k_translate_ws
   // ---------------- consumers ----------------
   LaneOps<P> op;
   load_lane_ops(op, frag, lane);
+  // every thread waits for the previous level before it triggers the next
+  // one's launch (the consumers would wait for the stage anyway)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int64_t nr_ = BATCH ? a.nrhs : 1;
   const int64_t nwork_ = ntiles * nr_;
   // PL: issue work item w into stage s (one whole warp), with the group
@@ -1591,9 +1596,6 @@ __global__ __launch_bounds__((NC + (PL ? 0 : 1)) * 32, MINB) void k_translate_ws
                                              smem_u32(&nrec[PL ? st : 0][0]));
   };
   if constexpr (PL) {
-    // programmatic dependent launch: the previous level's data is touched only
-    // after it has completed (every thread: any warp may issue a refill)
-    asm volatile("griddepcontrol.wait;" ::: "memory");
     if (warp == 0) {
       for (int i = 0; i < NST; ++i) {
         const int64_t w = blockIdx.x + (int64_t)i * gridDim.x;
@@ -2044,35 +2046,6 @@ static TransArgs make_args(const LevelDims& L, const double2* in, double2* out) 
   a.nrhs = L.nrhs;
   a.rs = L.rs;
   return a;
-}
-
-// SFT_PDL=0 disables programmatic dependent launch (ablation)
-static bool pdl_enabled() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("SFT_PDL");
-    v = (e && e[0] == '0') ? 0 : 1;
-  }
-  return v == 1;
-}
-
-// Launch with programmatic stream serialization (PDL): the kernel may start
-// while the previous kernel on the stream drains; it must execute
-// griddepcontrol.wait before touching that kernel's data.
-template <typename... KArgs, typename... Args>
-static void launch_pdl(void (*kernel)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t st,
-                       Args... args) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(block);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
 
 // Resident-CTA grid of a persistent kernel on the current device, with the
