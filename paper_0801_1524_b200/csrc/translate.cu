@@ -189,9 +189,12 @@ struct SymShape {
 // each child in one k-step, N = (P_m, Q_m) for m = 0..3 in one tile, m = 4 a
 // DFMA tail -- 2 DMMA per super-tile; the symmetric form would need 4 (its
 // s- and t-GEMMs each fill only half a k-step) plus the sum/difference adds.
+#ifndef SFT_SYM5
+#define SFT_SYM5 0
+#endif
 template <int P>
 struct UseSym {
-  static constexpr bool v = P >= 7;
+  static constexpr bool v = P >= 7 || (SFT_SYM5 && P == 5);
 };
 #ifndef SFT_CLASS_SPLIT
 // class-uniform super-tiles skip the absent child's loads; 2D symmetric form
@@ -321,6 +324,7 @@ struct LaneOps {
                               // (direct form: a0, b0, a1, b1 of m = c)
   double ts, tt, tds, tdt;    // p = 9 centre: odd coefficients of this lane's k, centre deltas (lane 0)
                               // (direct form: tail P / Q weights of this lane's k, tail delta on lane 0)
+  double b2;                  // direct form, SFT_TAIL5_DMMA: B fragment of the tail tile (columns P_4, Q_4)
 };
 
 template <int P>
@@ -337,6 +341,7 @@ __device__ __forceinline__ void load_lane_ops(LaneOps<P>& op, const double* __re
     op.dt1 = frag[S::OFF_DELTA + 96 + lane];
     op.tds = frag[S::OFF_DTAIL + lane];
     op.tdt = frag[S::OFF_DTAIL + 32 + lane];
+    op.b2 = (lane >> 2) == 0 ? op.ts : (lane >> 2) == 1 ? op.tt : 0.0;  // B[k = lane % 4][n = lane / 4]
     return;
   }
   using S = SymShape<P>;
@@ -354,6 +359,7 @@ __device__ __forceinline__ void load_lane_ops(LaneOps<P>& op, const double* __re
   } else {
     op.ts = op.tt = op.tds = op.tdt = 0.0;
   }
+  op.b2 = 0.0;
 }
 
 // ------------------------------------------------------------------------
@@ -906,6 +912,12 @@ struct RowMap {
   }
 };
 
+// SFT_TAIL5_DMMA=1: the direct form's tail m = p-1 on a second DMMA N tile
+// (columns P_4, Q_4 on lane c = 0 of each row) instead of per-lane partials
+// and a 4-lane transpose-reduce (6 SHFL, selects and adds per super-tile)
+#ifndef SFT_TAIL5_DMMA
+#define SFT_TAIL5_DMMA 1  // C3 translate 0.713 -> 0.684 ms, C2 geometry at p = 5 0.423 -> 0.399; 89 -> 80 registers
+#endif
 // Super-tile arithmetic of the direct form (p = 5, DirShape5): lane c loads
 // child (c >> 1)'s odd element 2 (c & 1) + 1 (the A fragment of k = c), and
 // for its output m = c child 0's element 2m and child 1's element 2m - (p-1)
@@ -934,10 +946,18 @@ __device__ __forceinline__ void direct_math(const LaneOps<P>& op, const uint32_t
     are[u][1] = fma(op.dt1, x1.x, op.ds1 * x0.x);
     aim[u][0] = fma(op.dt0, x1.y, op.ds0 * x0.y);
     aim[u][1] = fma(op.dt1, x1.y, op.ds1 * x0.y);
-    tl[u][0] = fma(av.x, op.ts, op.tds * xt.x);  // P.re
-    tl[u][1] = fma(av.x, op.tt, op.tdt * xt.x);  // Q.re
-    tl[u][2] = fma(av.y, op.ts, op.tds * xt.y);  // P.im
-    tl[u][3] = fma(av.y, op.tt, op.tdt * xt.y);  // Q.im
+    if constexpr (SFT_TAIL5_DMMA) {
+      // tail tile accumulators: (P_4, Q_4) deltas on lane c = 0 (tds, tdt are 0 elsewhere)
+      tl[u][0] = op.tds * xt.x;
+      tl[u][1] = op.tdt * xt.x;
+      tl[u][2] = op.tds * xt.y;
+      tl[u][3] = op.tdt * xt.y;
+    } else {
+      tl[u][0] = fma(av.x, op.ts, op.tds * xt.x);  // P.re
+      tl[u][1] = fma(av.x, op.tt, op.tdt * xt.x);  // Q.re
+      tl[u][2] = fma(av.y, op.ts, op.tds * xt.y);  // P.im
+      tl[u][3] = fma(av.y, op.tt, op.tdt * xt.y);  // Q.im
+    }
     avx[u] = av.x;
     avy[u] = av.y;
   }
@@ -946,6 +966,12 @@ __device__ __forceinline__ void direct_math(const LaneOps<P>& op, const uint32_t
   for (int u = 0; u < NSUB; ++u) {
     dmma(are[u], avx[u], op.bs);
     dmma(aim[u], avy[u], op.bs);
+    if constexpr (SFT_TAIL5_DMMA) {
+      double (&tr)[2] = *reinterpret_cast<double(*)[2]>(&tl[u][0]);
+      double (&ti)[2] = *reinterpret_cast<double(*)[2]>(&tl[u][2]);
+      dmma(tr, avx[u], op.b2);
+      dmma(ti, avy[u], op.b2);
+    }
   }
 #endif
   const bool odd = c & 1, hi = c & 2;
@@ -953,6 +979,14 @@ __device__ __forceinline__ void direct_math(const LaneOps<P>& op, const uint32_t
   for (int u = 0; u < NSUB; ++u) {
     o0[u].st(c * STR, are[u][0] + aim[u][1], aim[u][0] - are[u][1]);  // z_0 = P - iQ
     o1[u].st(c * STR, are[u][0] - aim[u][1], aim[u][0] + are[u][1]);  // z_1 = P + iQ
+    if constexpr (SFT_TAIL5_DMMA) {
+      // lane c = 0: tl = (P_4.re, Q_4.re, P_4.im, Q_4.im)
+      if (c == 0) {
+        o0[u].st((P - 1) * STR, tl[u][0] + tl[u][3], tl[u][2] - tl[u][1]);
+        o1[u].st((P - 1) * STR, tl[u][0] - tl[u][3], tl[u][2] + tl[u][1]);
+      }
+      continue;
+    }
     // tail m = p-1: (z_0.re, z_0.im, z_1.re, z_1.im) partials, transpose-reduce
     const double u0 = tl[u][0] + tl[u][3], u1 = tl[u][2] - tl[u][1];
     const double u2 = tl[u][0] - tl[u][3], u3 = tl[u][2] + tl[u][1];
