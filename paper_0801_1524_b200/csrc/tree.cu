@@ -168,6 +168,30 @@ __global__ __launch_bounds__(kBlk) void k_count(const KT* __restrict__ key, Bloc
   if (threadIdx.x <= L) counts[(int64_t)blockIdx.x * (L + 1) + threadIdx.x] = cnt[threadIdx.x];
 }
 
+// Exclusive prefix, per tree and level, of k_count's per-block box counts
+// (in place), one CTA per (tree, level): k_fill reads its block's offsets
+// directly (summing the earlier blocks in every k_fill block was quadratic in
+// the block count: 170 us of fill at C4's 3.5 M points).
+__global__ __launch_bounds__(kBlk) void k_scan_counts(int32_t* __restrict__ counts, int nbx, int nbk, int L) {
+  using Scan = cub::BlockScan<int, kBlk>;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ int carry;
+  const int tree = blockIdx.x / (L + 1), l = blockIdx.x % (L + 1);
+  const int b0 = tree ? nbx : 0, b1 = tree ? nbx + nbk : nbx;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int c = b0; c < b1; c += kBlk) {
+    const int b = c + threadIdx.x;
+    const int v = b < b1 ? counts[(int64_t)b * (L + 1) + l] : 0;
+    int ex, tot;
+    Scan(tmp).ExclusiveSum(v, ex, tot);
+    if (b < b1) counts[(int64_t)b * (L + 1) + l] = carry + ex;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += tot;
+    __syncthreads();
+  }
+}
+
 struct TreeOut {
   uint64_t* key[kMaxLevels];
   int32_t* child_begin[kMaxLevels];
@@ -198,16 +222,9 @@ __global__ __launch_bounds__(kBlk) void k_fill(const KT* __restrict__ key, const
   A.bm.get(blockIdx.x, tree, ts, lo, hi);
   const TreeOut& T = A.t[tree];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int b_first = tree ? A.bm.nbx : 0;
   const int b_last = tree ? A.bm.nbx + A.nbk - 1 : A.bm.nbx - 1;
-  // exclusive prefix of the level counts over the earlier blocks of this tree
-  if (warp <= L) {
-    int s = 0;
-    for (int b = b_first + lane; b < (int)blockIdx.x; b += 32) s += counts[(int64_t)b * (L + 1) + warp];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) base[warp] = s;
-  }
+  // exclusive prefix of the level counts over the earlier blocks of this tree (k_scan_counts)
+  if (threadIdx.x <= L) base[threadIdx.x] = counts[(int64_t)blockIdx.x * (L + 1) + threadIdx.x];
   const int64_t i = lo + threadIdx.x;
   const int m = i < hi ? (int)ml[i] : L + 1;
   const unsigned le = (lane == 31) ? 0xffffffffu : ((2u << lane) - 1u);
@@ -1156,6 +1173,9 @@ static int sort_and_fill(sft_plan_s* P, const double* x_dev, const double* k_dev
   trace_mark("sort", s, true);
   BlockMap bm{nx, n, nbx};
   k_count<KT><<<nbx + nbk, kBlk, 0, s>>>(keys_out, bm, d, L, ml, counts);
+  count_launch();
+  CK(cudaGetLastError());
+  k_scan_counts<<<2 * (L + 1), kBlk, 0, s>>>(counts, nbx, nbk, L);
   count_launch();
   CK(cudaGetLastError());
   trace_mark("count", s, true);
