@@ -356,7 +356,9 @@ static LevelDims two_level_dims(const sft_plan_s* P, int t) {
 // Dims of the translation launch whose output level is t (two-level or single)
 static LevelDims launch_dims(const sft_plan_s* P, int t) {
   const bool f2 = t < (int)P->launch_f2_out.size() && P->launch_f2_out[t];
-  return f2 ? two_level_dims(P, t) : apply_dims(P, t);
+  LevelDims ld = f2 ? two_level_dims(P, t) : apply_dims(P, t);
+  ld.ctr = P->tctr ? P->tctr + 2 * t : nullptr;
+  return ld;
 }
 
 static LevelDims apply_dims_sched(const sft_plan_s* P, int t) {
@@ -835,14 +837,18 @@ extern "C" int sft_plan(int dim, int64_t N, int p, const double* x, int64_t nx, 
       if (!inner) tot += (schedule_bytes(P, launch_dims(P, t)) + 255) / 256 * 256;
     }
     P->sched_off[L] = tot;
+    // dynamic tile scheduling (SFT_DYN=0: static grid-stride assignment)
+    const char* dyn = getenv("SFT_DYN");
+    const size_t cb = (tot > 0 && !(dyn && dyn[0] == '0')) ? ((size_t)2 * L * sizeof(int) + 255) / 256 * 256 : 0;
     const size_t bb = (P->buf_elems * (P->prec == 1 ? sizeof(float2) : sizeof(double2)) + 255) / 256 * 256;
     char* blk = nullptr;
-    if (block_alloc((void**)&blk, 2 * bb + tot, s) != cudaSuccess)
+    if (block_alloc((void**)&blk, 2 * bb + tot + cb, s) != cudaSuccess)
       return bail(SFT_E_NOMEM, "level buffer allocation failed");
-    P->blk_bytes = 2 * bb + tot;
+    P->blk_bytes = 2 * bb + tot + cb;
     P->buf[0] = (double2*)blk;
     P->buf[1] = (double2*)(blk + bb);
     P->sched = tot > 0 ? (unsigned char*)(blk + 2 * bb) : nullptr;
+    P->tctr = cb > 0 ? (int*)(blk + 2 * bb + tot) : nullptr;
     trace_mark("bufs");
     if (tot > 0) {
       // the first translation launch's schedule first (its own event: the

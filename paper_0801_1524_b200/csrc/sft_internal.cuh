@@ -126,6 +126,7 @@ struct sft_plan_s {
   // tile schedules of the translation launches (one allocation; offsets per launch,
   // for multi-rank plans per level t)
   unsigned char* sched = nullptr;
+  int* tctr = nullptr;  // [L][2] dynamic tile-scheduling counters per translation launch (after the schedules)
   std::vector<size_t> sched_off;
   cudaEvent_t sched_fork = nullptr, sched_ready = nullptr;  // schedule kernel on the side stream
   cudaEvent_t sched_first = nullptr;  // the first translation launch's schedule (world 1)
@@ -183,6 +184,10 @@ struct LevelDims {
   // (elements of the stored type)
   int nrhs = 1;
   int64_t rs = 0;
+  // dynamic tile scheduling counters of this launch ([next item, CTAs done];
+  // zeroed by the plan's schedule kernel, reset by the launch's last CTA), or
+  // nullptr for the static grid-stride assignment
+  int* ctr = nullptr;
 };
 
 // level buffers are void*: complex128 (prec 0) or complex64 (prec 1) pair arrays of stride P->pds

@@ -84,6 +84,10 @@ struct TransArgs : LevelArgs {
   // in + r * rs and writes out + r * rs (elements of the stored type)
   int nrhs;
   int64_t rs;
+  // dynamic tile scheduling: ctr[0] = next work item, ctr[1] = CTAs done
+  // fetching (the last one resets both for the next apply); nullptr = static
+  // grid-stride assignment
+  int* ctr;
 };
 
 struct GroupMeta {
@@ -757,6 +761,7 @@ constexpr int kSchedChunk = 16;  // levels per schedule launch (the struct is on
 struct SchedLevels {
   LevelArgs a[kSchedChunk];
   unsigned char* dst[kSchedChunk];
+  int* ctr[kSchedChunk];  // the launch's tile counters, zeroed here (nullptr: none)
   int64_t tile0[kSchedChunk + 1];
   int nlev;
 };
@@ -770,6 +775,7 @@ __global__ __launch_bounds__(128) void k_schedule(const __grid_constant__ SchedL
   static_assert(G >= 1 && G <= 32 && (G & (G - 1)) == 0, "G must be a power of two");
   constexpr int TPW = 32 / G;  // tiles per warp (G-lane segments)
   const int lane = threadIdx.x & 31;
+  if (blockIdx.x == 0 && threadIdx.x < 2 * S.nlev && S.ctr[threadIdx.x >> 1]) S.ctr[threadIdx.x >> 1][threadIdx.x & 1] = 0;
   const int64_t T = ((int64_t)blockIdx.x * 4 + (threadIdx.x >> 5)) * TPW + lane / G;  // global tile
   const int j = lane % G;
   if (T - lane / G >= S.tile0[S.nlev]) return;  // whole warp out of range
@@ -1410,7 +1416,7 @@ template <int D, int P, int G, int NST, typename E, int PS, bool BATCH, int NB =
 __device__ __forceinline__ void ws_issue(const TransArgs& a, const unsigned char* __restrict__ sched, int64_t w,
                                          int64_t tile, uint2 gr, E* ring,
                                          unsigned char (*blk)[Sched<D, P, G>::BLK * NB], uint64_t* full, int s,
-                                         const unsigned char* nrec_src = nullptr, uint32_t nrec_dst = 0) {
+                                         int64_t* wid, const unsigned char* nrec_src = nullptr, uint32_t nrec_dst = 0) {
   using SC = Sched<D, P, G>;
   constexpr int PD = PS;  // stage and HBM arrays have stride PS elements of type E
   constexpr int NS = 1 << D;
@@ -1456,6 +1462,7 @@ __device__ __forceinline__ void ws_issue(const TransArgs& a, const unsigned char
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   __syncwarp();
   if (lane == 0) {
+    wid[s] = w;  // the consumers read the stage's work item after full[s] (arrive: release)
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&full[s])),
                  "r"(nbytes + (uint32_t)(SC::BLK * NB) + (nrec_src ? (uint32_t)SC::GRP : 0u))
                  : "memory");
@@ -1523,14 +1530,22 @@ __device__ __forceinline__ uint2 ws_group_record(const unsigned char* __restrict
 template <int D, int P, int G, int NST, typename E = double2, int PS = StrideT<double2, Pow<P, D>::v>::v, bool BATCH = false, int NB = 1>
 __device__ __forceinline__ void ws_producer(const TransArgs& a, const unsigned char* __restrict__ sched, int64_t ntiles,
                                             E* ring, unsigned char (*blk)[Sched<D, P, G>::BLK * NB], uint64_t* full,
-                                            uint64_t* empty) {
+                                            uint64_t* empty, int64_t* wid) {
   INSTR_T0(tp0);
   int s = 0;
   uint32_t ph = 0;
   // work items w = tile * nrhs + r (BATCH = false: nrhs = 1, w = tile)
   const int64_t nr = BATCH ? a.nrhs : 1;
   const int64_t nwork = ntiles * nr;
-  int64_t w = blockIdx.x;
+  const int lane = threadIdx.x & 31;
+  // next work item: dynamic (a shared counter, one fetch ahead) or grid-stride
+  auto fetch = [&](int64_t cur) -> int64_t {
+    if (!a.ctr) return cur + gridDim.x;
+    int v = 0;
+    if (lane == 0) v = atomicAdd(&a.ctr[0], 1);
+    return (int64_t)__shfl_sync(0xffffffffu, v, 0);
+  };
+  int64_t w = a.ctr ? fetch(0) : (int64_t)blockIdx.x;
   int64_t tile = BATCH ? w / nr : w;
   uint2 gr = ws_group_record<D, P, G, NB>(sched, tile, w < nwork);
   // programmatic dependent launch: everything above (schedule reads, barrier
@@ -1539,15 +1554,16 @@ __device__ __forceinline__ void ws_producer(const TransArgs& a, const unsigned c
   // are touched only after it has completed
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // (after the wait: see launch_pdl)
-  for (int i = 0; w < nwork; ++i) {
-    const int64_t wn = w + gridDim.x;
+  int i = 0;
+  for (; w < nwork; ++i) {
+    const int64_t wn = fetch(w);
     const int64_t next = BATCH ? wn / nr : wn;
     const uint2 gn = ws_group_record<D, P, G, NB>(sched, next, wn < nwork);
     INSTR_T0(tw0);
     if (i >= NST) mbar_wait_sleep(smem_u32(&empty[s]), ph ^ 1u);
     INSTR_ADD(1, tw0);
     INSTR_T0(tb0);
-    ws_issue<D, P, G, NST, E, PS, BATCH, NB>(a, sched, w, tile, gr, ring, blk, full, s);
+    ws_issue<D, P, G, NST, E, PS, BATCH, NB>(a, sched, w, tile, gr, ring, blk, full, s, wid);
     INSTR_ADD(2, tb0);
     gr = gn;
     w = wn;
@@ -1555,6 +1571,21 @@ __device__ __forceinline__ void ws_producer(const TransArgs& a, const unsigned c
     if (++s == NST) {
       s = 0;
       ph ^= 1u;
+    }
+  }
+  // end of work: a sentinel item (-1) in the next stage of the sequence
+  if (i >= NST) mbar_wait_sleep(smem_u32(&empty[s]), ph ^ 1u);
+  if (lane == 0) {
+    wid[s] = -1;
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full[s])) : "memory");
+    // dynamic scheduling: the last CTA done fetching resets the counters for
+    // the next apply (every CTA's final fetch precedes its increment here)
+    if (a.ctr) {
+      __threadfence();
+      if (atomicAdd(&a.ctr[1], 1) == (int)gridDim.x - 1) {
+        a.ctr[0] = 0;
+        a.ctr[1] = 0;
+      }
     }
   }
   INSTR_ADD(0, tp0);
@@ -1594,6 +1625,7 @@ __global__ __launch_bounds__((NC + (PL ? 0 : 1)) * 32, MINB) void k_translate_ws
   __shared__ __align__(8) uint64_t full[NST], empty[NST], p1done[NST];
   __shared__ __align__(16) unsigned char nrec[PL ? NST : 1][SC::GRP];  // PL: group records of the stage's next item
   __shared__ int done[NST];                                            // PL: consumer warps done with the stage
+  __shared__ int64_t wid[NST];  // work item in each stage (-1: no more work)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (threadIdx.x < NST) {
     done[threadIdx.x] = 0;
@@ -1607,7 +1639,7 @@ __global__ __launch_bounds__((NC + (PL ? 0 : 1)) * 32, MINB) void k_translate_ws
   __syncthreads();
   if constexpr (!PL) {
     if (warp == NC) {
-      ws_producer<D, P, G, NST, E, PD, BATCH, NB>(a, sched, ntiles, ring, blk, full, empty);
+      ws_producer<D, P, G, NST, E, PD, BATCH, NB>(a, sched, ntiles, ring, blk, full, empty, wid);
       return;
     }
   }
@@ -1626,14 +1658,24 @@ __global__ __launch_bounds__((NC + (PL ? 0 : 1)) * 32, MINB) void k_translate_ws
     const int64_t wn = w + (int64_t)NST * gridDim.x;
     const unsigned char* nsrc =
         wn < nwork_ ? sched + (BATCH ? wn / nr_ : wn) * (int64_t)(SC::BLK * NB) + SC::HDR : nullptr;
-    ws_issue<D, P, G, NST, E, PD, BATCH, NB>(a, sched, w, BATCH ? w / nr_ : w, gr, ring, blk, full, st, nsrc,
+    ws_issue<D, P, G, NST, E, PD, BATCH, NB>(a, sched, w, BATCH ? w / nr_ : w, gr, ring, blk, full, st, wid, nsrc,
                                              smem_u32(&nrec[PL ? st : 0][0]));
+  };
+  // PL: no more work for stage st -- the sentinel item
+  auto pl_end = [&](int st) {
+    if (lane == 0) {
+      wid[st] = -1;
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full[st])) : "memory");
+    }
   };
   if constexpr (PL) {
     if (warp == 0) {
       for (int i = 0; i < NST; ++i) {
         const int64_t w = blockIdx.x + (int64_t)i * gridDim.x;
-        if (w >= nwork_) break;
+        if (w >= nwork_) {
+          pl_end(i);
+          break;
+        }
         pl_issue(w, ws_group_record<D, P, G, NB>(sched, BATCH ? w / nr_ : w, true), i);
       }
     }
@@ -1656,6 +1698,8 @@ __global__ __launch_bounds__((NC + (PL ? 0 : 1)) * 32, MINB) void k_translate_ws
         if (wn < nwork_) {
           const uint2 gr = lane < G ? reinterpret_cast<const uint2*>(&nrec[PL ? st : 0][0])[lane] : make_uint2(0u, 0u);
           pl_issue(wn, gr, st);
+        } else {
+          pl_end(st);
         }
       }
     } else {
@@ -1677,25 +1721,26 @@ __global__ __launch_bounds__((NC + (PL ? 0 : 1)) * 32, MINB) void k_translate_ws
     if constexpr (D == 2) consumer_pass<D, P, G, NC, D - 1, true, 3, E, FUSED>(a, sb_, bk, op, zs, rot, oo);
   };
   // work items w = tile * nrhs + r; the output of RHS r goes to out + r * rs
-  const int64_t nwork = BATCH ? ntiles * a.nrhs : ntiles;
   auto ooff = [&](int64_t w_) { return BATCH ? (w_ % a.nrhs) * a.rs : (int64_t)0; };
   // the last pass in place + TMA bulk stores (non-skewed single-level tiles)
   constexpr bool STAGE_OUT = SFT_TMA_STORE && !FUSED && !F2 && D == 2;  // (2D only)
+  // the work item of each stage comes from the producer (wid, after full[s]);
+  // -1 ends the sequence (dynamic or grid-stride assignment alike)
   if constexpr (D == 2 && NST >= 3 && !F2) {
-    int64_t tile = blockIdx.x;
-    if (tile < nwork) {
-      mbar_wait(smem_u32(&full[0]), 0);
+    mbar_wait(smem_u32(&full[0]), 0);
+    int64_t tile = wid[0];
+    if (tile >= 0) {
       first2d(ring, blk[0]);
       asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&p1done[0])) : "memory");
     }
-    for (; tile < nwork; tile += gridDim.x) {
-      const int64_t nt = tile + gridDim.x;
+    while (tile >= 0) {
       const int sn = s + 1 == NST ? 0 : s + 1;
       const uint32_t phn = sn == 0 ? ph ^ 1u : ph;
-      if (nt < nwork) {
-        INSTR_T0(tf0);
-        mbar_wait(smem_u32(&full[sn]), phn);
-        INSTR_ADD(4, tf0);
+      INSTR_T0(tf0);
+      mbar_wait(smem_u32(&full[sn]), phn);
+      INSTR_ADD(4, tf0);
+      const int64_t nt = wid[sn];
+      if (nt >= 0) {
         INSTR_T0(t1);
         first2d(ring + sn * STAGE, blk[sn]);
         asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&p1done[sn])) : "memory");
@@ -1710,12 +1755,15 @@ __global__ __launch_bounds__((NC + (PL ? 0 : 1)) * 32, MINB) void k_translate_ws
       release(tile, s);
       s = sn;
       ph = phn;
+      tile = nt;
     }
   } else {
-    for (int64_t w = blockIdx.x; w < nwork; w += gridDim.x) {
+    for (;;) {
       INSTR_T0(tf0);
       mbar_wait(smem_u32(&full[s]), ph);
       INSTR_ADD(4, tf0);
+      const int64_t w = wid[s];
+      if (w < 0) break;
       E* sb = ring + s * STAGE;
       if constexpr (F2) {
         // two-level tile: first level (block 0) in place, second level (block
@@ -2079,6 +2127,7 @@ static TransArgs make_args(const LevelDims& L, const double2* in, double2* out) 
   a.peer_seg[kMaxPeers] = L.peer_seg[kMaxPeers];
   a.nrhs = L.nrhs;
   a.rs = L.rs;
+  a.ctr = L.ctr;
   return a;
 }
 
@@ -2124,7 +2173,12 @@ static cudaError_t launch_ws(const sft_plan_s* Pl, const TransArgs& a, const Lev
   const double* frag = device_fragments<P>(&e);
   if (!frag) return e;
   const int64_t ntiles = (a.ngroups + G - 1) / G;
-  launch_pdl(kern, (unsigned)std::min<int64_t>(work, grid_max), (NC + 1) * 32, smem, Pl->stream, a, frag, L.sched,
+  // dynamic tile scheduling pays with many items per CTA (C2 translate 0.936 ->
+  // 0.892 ms, C3 0.671 -> 0.632, C4 31.8 -> 30.4); with a few per CTA the
+  // counter's latency is exposed (C1 0.072 -> 0.076): grid-stride there
+  TransArgs ad = a;
+  if (work <= 4 * (int64_t)grid_max) ad.ctr = nullptr;
+  launch_pdl(kern, (unsigned)std::min<int64_t>(work, grid_max), (NC + 1) * 32, smem, Pl->stream, ad, frag, L.sched,
              ntiles);
   count_launch();
   return cudaGetLastError();
@@ -2199,6 +2253,7 @@ static cudaError_t launch_schedule_g(const sft_plan_s* Pl, const LevelDims* L, i
         if (a.ngroups <= 0) continue;
         S.a[S.nlev] = a;
         S.dst[S.nlev] = dst[i];
+        S.ctr[S.nlev] = L[i].ctr;
         S.tile0[S.nlev] = t0;
         t0 += (a.ngroups + G - 1) / G;
         ++S.nlev;
