@@ -24,6 +24,11 @@ KEYS = [
     ("launch__block_size", "block"),
     ("sm__sass_thread_inst_executed_op_dfma_pred_on.sum", "dfma_thread_inst"),
     ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smem_bank_conflicts"),
+    ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "smem_wavefronts"),
+    ("smsp__inst_executed.sum", "warp_instructions"),
+    ("sm__cycles_active.avg", "sm_active_cycles_avg"),
+    ("sm__cycles_active.max", "sm_active_cycles_max"),
+    ("sm__cycles_elapsed.avg", "sm_elapsed_cycles_avg"),
 ]
 
 
