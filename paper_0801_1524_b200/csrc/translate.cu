@@ -1623,6 +1623,7 @@ __global__ __launch_bounds__((NC + (PL ? 0 : 1)) * 32, MINB) void k_translate_ws
   constexpr int NB = F2 ? 2 : 1;  // schedule blocks per tile
   __shared__ __align__(128) unsigned char blk[NST][SC::BLK * NB];
   __shared__ __align__(8) uint64_t full[NST], empty[NST], p1done[NST];
+  __shared__ __align__(8) uint64_t r1done[D == 3 && NST >= 3 ? NST : 1];  // 3D skewed: round 1 of the stage done
   __shared__ __align__(16) unsigned char nrec[PL ? NST : 1][SC::GRP];  // PL: group records of the stage's next item
   __shared__ int done[NST];                                            // PL: consumer warps done with the stage
   __shared__ int64_t wid[NST];  // work item in each stage (-1: no more work)
@@ -1632,6 +1633,8 @@ __global__ __launch_bounds__((NC + (PL ? 0 : 1)) * 32, MINB) void k_translate_ws
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full[threadIdx.x])));
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&empty[threadIdx.x])), "r"(NC));
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&p1done[threadIdx.x])), "r"(NC * 32));
+    if constexpr (D == 3 && NST >= 3)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&r1done[threadIdx.x])), "r"(NC * 32));
   }
   if (threadIdx.x == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   for (int q = threadIdx.x; q < PD * (int)sizeof(E) / 16; q += blockDim.x)
@@ -1726,7 +1729,53 @@ __global__ __launch_bounds__((NC + (PL ? 0 : 1)) * 32, MINB) void k_translate_ws
   constexpr bool STAGE_OUT = SFT_TMA_STORE && !FUSED && !F2 && D == 2;  // (2D only)
   // the work item of each stage comes from the producer (wid, after full[s]);
   // -1 ends the sequence (dynamic or grid-stride assignment alike)
-  if constexpr (D == 2 && NST >= 3 && !F2) {
+  // 3D round r of the tile in stage sb: the axis-2, -1, -0 sub-lists (r < 2 in
+  // place, r = 2 to HBM)
+  auto round3 = [&](E* sb_, const unsigned char* bk, int r, int64_t oo) {
+    if constexpr (D == 3) {
+      if (r < 2) {
+        consumer_pass<D, P, G, NC, 2, false, 0, E>(a, sb_, bk, op, zs, rot, 0, r);
+        consumer_pass<D, P, G, NC, 1, false, 0, E>(a, sb_, bk, op, zs, rot, 0, r);
+        consumer_pass<D, P, G, NC, 0, false, 0, E>(a, sb_, bk, op, zs, rot, 0, r);
+      } else {
+        consumer_pass<D, P, G, NC, 2, true, 0, E, FUSED>(a, sb_, bk, op, zs, rot, oo, 2);
+        consumer_pass<D, P, G, NC, 1, true, 0, E, FUSED>(a, sb_, bk, op, zs, rot, oo, 2);
+        consumer_pass<D, P, G, NC, 0, true, 0, E, FUSED>(a, sb_, bk, op, zs, rot, oo, 2);
+      }
+    }
+  };
+  if constexpr (D == 3 && NST >= 3 && !F2) {
+    // 3D skewed pipeline: per tile i, round 1 of i, round 0 of i+1, round 2
+    // of i -- each round's dependency (the previous round of the same tile, on
+    // every warp: p1done = round 0 done, r1done = round 1 done) is waited on
+    // one round of other work later, so warps do not idle at pass barriers
+    mbar_wait(smem_u32(&full[0]), 0);
+    int64_t tile = wid[0];
+    if (tile >= 0) {
+      round3(ring, blk[0], 0, 0);
+      asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&p1done[0])) : "memory");
+    }
+    while (tile >= 0) {
+      const int sn = s + 1 == NST ? 0 : s + 1;
+      const uint32_t phn = sn == 0 ? ph ^ 1u : ph;
+      E* const sb = ring + s * STAGE;
+      mbar_wait(smem_u32(&p1done[s]), ph);
+      round3(sb, blk[s], 1, 0);
+      asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&r1done[s])) : "memory");
+      mbar_wait(smem_u32(&full[sn]), phn);
+      const int64_t nt = wid[sn];
+      if (nt >= 0) {
+        round3(ring + sn * STAGE, blk[sn], 0, 0);
+        asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&p1done[sn])) : "memory");
+      }
+      mbar_wait(smem_u32(&r1done[s]), ph);
+      round3(sb, blk[s], 2, ooff(tile));
+      release(tile, s);
+      s = sn;
+      ph = phn;
+      tile = nt;
+    }
+  } else if constexpr (D == 2 && NST >= 3 && !F2) {
     mbar_wait(smem_u32(&full[0]), 0);
     int64_t tile = wid[0];
     if (tile >= 0) {

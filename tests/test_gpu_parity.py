@@ -542,3 +542,33 @@ def test_small_tree_kernel_equals_multikernel_build(d, N, p, nx, nk, tmp_path):
     assert list(outs[0]["cx"]) == list(oracle.tree_counts(x, N))
     if nx * nk <= 5_000_000:
         assert_close(outs[0]["u"], oracle.butterfly(x, k, f, N, p), PARITY)
+
+
+@pytest.mark.parametrize("name", ["C2", "C3"])
+def test_dynamic_tile_scheduling(name, monkeypatch):
+    """Dynamic tile scheduling (per-launch work counters, reset by each
+    launch's last CTA) against the static grid-stride assignment: every
+    output is still produced by one thread in a fixed order, so applies are
+    bitwise equal run to run (the counters must be back at zero for the next
+    apply), between the two assignments, and for a batch."""
+    torch = _torch()
+    import paper_0801_1524_b200 as sft
+    w = synth.make_workload(name)
+    xt = torch.from_numpy(w.x).cuda(); kt = torch.from_numpy(w.k).cuda(); ft = torch.from_numpy(w.f).cuda()
+    with sft.Plan(w.dim, w.N, w.p, xt, kt) as plan:
+        runs = [plan.apply(ft).cpu().numpy() for _ in range(3)]
+        g = torch.from_numpy(synth.random_charges(len(w.k), 7)).cuda()
+        ub = plan.apply_batch(torch.stack([ft, g, ft]))
+        ug = plan.apply(g).cpu().numpy()
+    for r in runs[1:]:
+        assert np.array_equal(r, runs[0])
+    ub = ub.cpu().numpy()
+    assert np.array_equal(ub[0], runs[0]) and np.array_equal(ub[2], runs[0]) and np.array_equal(ub[1], ug)
+    monkeypatch.setenv("SFT_DYN", "0")  # read by sft_plan: no counters, grid-stride items
+    with sft.Plan(w.dim, w.N, w.p, xt, kt) as plan:
+        us = plan.apply(ft).cpu().numpy()
+    assert np.array_equal(us, runs[0])
+    # and the transform itself, on a spread sample of targets
+    sel = np.sort(np.random.default_rng(11).choice(len(w.x), 256, replace=False))
+    ub_o = oracle.butterfly(w.x, w.k, w.f, w.N, w.p, targets=sel)
+    assert_close(runs[0][sel], ub_o, PARITY)
