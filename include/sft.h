@@ -170,12 +170,17 @@ int sft_plan_work(sft_plan_t plan, double* w);
 int sft_translation_launches(sft_plan_t plan, int* n, int* out_level, int* two_level);
 
 /* Device time (ms, CUDA events on the plan stream) of the kernels of the last
- * sft_apply when timing was enabled with sft_set_timing(plan, 1):
+ * sft_apply when timing was enabled with sft_set_timing(plan, mode):
  *   t_ms[0] leaf kernel, t_ms[1] sum of translation kernels, t_ms[2] final
  *   kernel, t_ms[3] whole apply; per_level_ms [L] translation level t=0..L-1
  *   (or NULL; a two-level launch is booked on its output level t, level t+1
- *   then reads 0).  Multi-rank plans: after sft_apply_phase2, t_ms[1] is this
- *   rank's translation time of both phases (the other entries are not set). */
+ *   then reads 0).  mode 1: an event after every launch (per-level times; the
+ *   events cut the programmatic-dependent-launch overlap between levels);
+ *   mode 2: events only around the leaf kernel, the whole translation chain
+ *   and the final kernel (t_ms[1] = the chain, per_level_ms all 0).  mode 0:
+ *   off; other modes: SFT_E_ARG.  Multi-rank plans: after sft_apply_phase2,
+ *   t_ms[1] is this rank's translation time of both phases (the other entries
+ *   are not set). */
 int sft_set_timing(sft_plan_t plan, int enable);
 int sft_last_timing(sft_plan_t plan, double* t_ms, double* per_level_ms);
 

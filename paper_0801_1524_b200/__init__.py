@@ -322,7 +322,9 @@ class Plan:
         return dict(alg_bytes=w[0], fp64_flops=w[1], supertiles=w[2], tasks=w[3], groups=w[4], pairs=w[5])
 
     def set_timing(self, on=True):
-        _check(lib().sft_set_timing(self._h, 1 if on else 0))
+        """on: False / True (events around every launch) / 2 (events around the
+        translation chain only: per-level times not recorded)."""
+        _check(lib().sft_set_timing(self._h, int(on) if on in (0, 1, 2) else 1))
 
     def last_timing(self):
         t = np.zeros(4); lv = np.zeros(max(self.L, 1))

@@ -1026,7 +1026,7 @@ static int finish_timing(sft_plan_s* P, int n_levels_first, const std::vector<in
   for (int i = 0; i < nlev; ++i) {
     cudaEventElapsedTime(&ms, P->ev[1 + i], P->ev[2 + i]);
     const int t = tl ? (i < (int)tl->size() ? (*tl)[i] : -1) : n_levels_first - i;
-    if (t >= 0 && t < P->L) P->level_ms[t] = ms;
+    if (P->timing == 1 && t >= 0 && t < P->L) P->level_ms[t] = ms;  // (mode 2: one chain interval)
     trans += ms;
   }
   P->last_ms[1] = trans;
@@ -1122,7 +1122,7 @@ static int apply_impl(sft_plan_s* P, int nrhs, const void* f, int64_t ldf, void*
     ld.nrhs = nrhs;
     ld.rs = rs;
     CKR(launch_translate(P, ld, buf[i & 1], buf[(i + 1) & 1]));
-    tmark(P);
+    if (P->timing != 2 || i == nl - 1) tmark(P);  // mode 2: the chain as one interval (PDL overlap kept)
   }
   // step 4: final evaluation, level 0 buffer [A leaves]
   CKR(launch_final(P, buf[nl & 1], ud, 0, 0, P->nx, nrhs, rs, ldu_dev));
@@ -1522,7 +1522,8 @@ extern "C" int sft_translation_launches(sft_plan_t P, int* n, int* out_level, in
 
 extern "C" int sft_set_timing(sft_plan_t P, int enable) {
   if (!P) return fail(SFT_E_ARG, "NULL plan");
-  P->timing = enable != 0;
+  if (enable < 0 || enable > 2) return fail(SFT_E_ARG, "timing mode must be 0, 1 or 2");
+  P->timing = enable;
   return SFT_OK;
 }
 

@@ -131,7 +131,7 @@ struct sft_plan_s {
   cudaEvent_t sched_fork = nullptr, sched_ready = nullptr;  // schedule kernel on the side stream
   cudaEvent_t sched_first = nullptr;  // the first translation launch's schedule (world 1)
   // timing
-  bool timing = false;
+  int timing = 0;  // sft_set_timing: 0 off, 1 events around every launch, 2 around the translation chain
   cudaEvent_t ev[64];
   int n_ev = 0;
   int ev_created = 0;

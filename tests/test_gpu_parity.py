@@ -557,6 +557,16 @@ def test_dynamic_tile_scheduling(name, monkeypatch):
     xt = torch.from_numpy(w.x).cuda(); kt = torch.from_numpy(w.k).cuda(); ft = torch.from_numpy(w.f).cuda()
     with sft.Plan(w.dim, w.N, w.p, xt, kt) as plan:
         runs = [plan.apply(ft).cpu().numpy() for _ in range(3)]
+        # timing modes: 1 = per launch (per-level times), 2 = the translation chain
+        plan.set_timing(True)
+        plan.apply(ft)
+        t1 = plan.last_timing()
+        plan.set_timing(2)
+        runs.append(plan.apply(ft).cpu().numpy())
+        t2 = plan.last_timing()
+        plan.set_timing(False)
+        assert (t1["level_ms"] > 0).sum() >= 1 and np.all(t2["level_ms"] == 0)
+        assert 0 < t2["trans_ms"] <= t2["apply_ms"] and t2["leaf_ms"] > 0 and t2["final_ms"] > 0
         g = torch.from_numpy(synth.random_charges(len(w.k), 7)).cuda()
         ub = plan.apply_batch(torch.stack([ft, g, ft]))
         ug = plan.apply(g).cpu().numpy()
