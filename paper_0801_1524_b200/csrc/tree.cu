@@ -20,6 +20,7 @@
 // Level arrays live in one arena sized by the upper bound min(n, 2^(d*l)) per
 // level, so nothing on the device waits for the host; the single sync at the
 // end reads the exact counts (the apply needs them to size grids and buffers).
+#include <atomic>
 #include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
@@ -189,6 +190,23 @@ __global__ __launch_bounds__(kBlk) void k_scan_counts(int32_t* __restrict__ coun
     __syncthreads();
     if (threadIdx.x == 0) carry += tot;
     __syncthreads();
+  }
+}
+
+// The plan's box totals and domain flag (nw int64 words) into pinned host
+// memory, then seq in word nw (system-scope fences: the host sees the data
+// before the flag)
+#ifndef SFT_PUBLISH
+#define SFT_PUBLISH 1
+#endif
+__global__ void k_publish(const int64_t* __restrict__ src, int nw, int64_t* dst, int64_t seq) {
+  volatile int64_t* d = dst;
+  for (int i = threadIdx.x; i < nw; i += blockDim.x) d[i] = src[i];
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    d[nw] = seq;
+    __threadfence_system();
   }
 }
 
@@ -1276,13 +1294,38 @@ int build_trees(sft_plan_s* P, const double* x_dev, const double* k_dev, std::st
 
   trace_mark("enq");
   // ---- the one host sync: exact box counts + domain error flag ----
-  // one copy into pinned host memory (a pageable destination would be staged
-  // by the driver: measured ~50 us of device time for the three small copies)
+  // k_publish writes them into pinned host memory (through its UVA address)
+  // followed by a sequence flag the host spins on -- the kernel's completion
+  // is seen a few us sooner than a D2H copy + stream synchronisation (the
+  // host polls the stream now and then: a failed launch cannot hang it)
   static thread_local int64_t* h = nullptr;
-  if (!h) CK(cudaMallocHost((void**)&h, (2 * kMaxLevels + 1) * sizeof(int64_t)));
-  CK(cudaMemcpyAsync(h, arena + o_hdr, (16 * (L + 1) + 8), cudaMemcpyDeviceToHost, s));
+  static thread_local int64_t seq = 0;
+  if (!h) CK(cudaMallocHost((void**)&h, (2 * kMaxLevels + 2) * sizeof(int64_t)));
+  const int nw = 2 * (L + 1) + 1;
+#if !SFT_PUBLISH  // (A/B: D2H copy + stream synchronisation)
+  CK(cudaMemcpyAsync(h, arena + o_hdr, nw * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   if (scr) block_free(scr, scr_bytes, s);
   CK(cudaStreamSynchronize(s));
+  (void)seq;
+#else
+  volatile int64_t* hv = h;
+  hv[nw] = 0;
+  ++seq;
+  k_publish<<<1, 64, 0, s>>>(reinterpret_cast<const int64_t*>(arena + o_hdr), nw, h, seq);
+  count_launch();
+  CK(cudaGetLastError());
+  if (scr) block_free(scr, scr_bytes, s);
+  for (long it = 1; hv[nw] != seq; ++it) {
+    if ((it & 255) == 0) {
+      const cudaError_t q = cudaStreamQuery(s);
+      if (q != cudaErrorNotReady && hv[nw] != seq) {
+        if (err) *err = std::string("tree build: ") + (q == cudaSuccess ? "header not published" : cudaGetErrorString(q));
+        return SFT_E_CUDA;
+      }
+    }
+  }
+  std::atomic_thread_fence(std::memory_order_acquire);
+#endif
   trace_mark("sync");
   const bool herr = h[2 * (L + 1)] != 0;  // either half (the small-tree path flags each tree)
   if (herr) {
