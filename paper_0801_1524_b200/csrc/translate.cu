@@ -902,6 +902,12 @@ struct NsubCfg {
   static constexpr int v = D == 2 ? (P == 5 ? SFT_NSUB25 : P == 7 ? SFT_NSUB27 : SFT_NSUB29)
                                   : (P == 5 ? SFT_NSUB35 : P == 7 ? SFT_NSUB37 : 1);
 };
+// SFT_TAIL5_DMMA=1: the direct form's tail m = p-1 on a second DMMA N tile
+// (columns P_4, Q_4 on lane c = 0 of each row) instead of per-lane partials
+// and a 4-lane transpose-reduce (6 SHFL, selects and adds per super-tile)
+#ifndef SFT_TAIL5_DMMA
+#define SFT_TAIL5_DMMA 1  // C3 translate 0.713 -> 0.684 ms, C2 geometry at p = 5 0.423 -> 0.399; 89 -> 80 registers
+#endif
 // Row -> fiber map of a super-tile (shared-memory bank conflicts, and whole
 // sectors for the HBM stores of a last pass).  The symmetric form uses the
 // identity with the store-order swap of consumer_pass (scripts/rfib_model_sym.py).
@@ -913,17 +919,12 @@ struct RowMap {
     if constexpr (UseSym<P>::v || LAST) return r;
     // direct form (p = 5), in-place passes: scripts/rfib_search_direct.py (slot-major stage, G of WsCfg)
     else if constexpr (D == 2) return (0x43726150u >> (4 * r)) & 7;                     // 0 5 1 6 2 7 3 4
-    else if constexpr (AX == 1) return (0x76432150u >> (4 * r)) & 7;                    // 0 5 1 2 3 4 6 7
+    else if constexpr (AX == 1 || (AX == 0 && SFT_TAIL5_DMMA))
+      return (0x76432150u >> (4 * r)) & 7;  // 0 5 1 2 3 4 6 7 (axis 0: with the merged tail-delta load, G = 1)
     else return (0x73625140u >> (4 * r)) & 7;                                           // 0 4 1 5 2 6 3 7
   }
 };
 
-// SFT_TAIL5_DMMA=1: the direct form's tail m = p-1 on a second DMMA N tile
-// (columns P_4, Q_4 on lane c = 0 of each row) instead of per-lane partials
-// and a 4-lane transpose-reduce (6 SHFL, selects and adds per super-tile)
-#ifndef SFT_TAIL5_DMMA
-#define SFT_TAIL5_DMMA 1  // C3 translate 0.713 -> 0.684 ms, C2 geometry at p = 5 0.423 -> 0.399; 89 -> 80 registers
-#endif
 // Super-tile arithmetic of the direct form (p = 5, DirShape5): lane c loads
 // child (c >> 1)'s odd element 2 (c & 1) + 1 (the A fragment of k = c), and
 // for its output m = c child 0's element 2m and child 1's element 2m - (p-1)
@@ -934,7 +935,10 @@ __device__ __forceinline__ void direct_math(const LaneOps<P>& op, const uint32_t
                                             const OutRow<E, GL> (&o0)[NSUB], const OutRow<E, GL> (&o1)[NSUB], int c) {
   constexpr int ES = sizeof(E);
   const int o_a = (2 * (c & 1) + 1) * STR * ES;  // of child c >> 1 (byte offsets)
-  const int o_e0 = min(2 * c, P - 1) * STR * ES, o_e1 = max(2 * c - (P - 1), 0) * STR * ES;
+  // (DMMA tail: lanes c = 0, 1 have no child-1 delta column, so lane 0's
+  // child-1 load fetches the tail delta, element p-1, instead -- one load less)
+  const int o_e0 = min(2 * c, P - 1) * STR * ES,
+            o_e1 = (SFT_TAIL5_DMMA && c == 0 ? P - 1 : max(2 * c - (P - 1), 0)) * STR * ES;
   const int o_t = (P - 1) * STR * ES;  // tail delta: child 1, element p-1
   double are[NSUB][2], aim[NSUB][2], tl[NSUB][4];
   double avx[NSUB], avy[NSUB];
@@ -947,7 +951,7 @@ __device__ __forceinline__ void direct_math(const LaneOps<P>& op, const uint32_t
     const double2 av = (c >> 1) ? (PRES & 2 ? lds<E>(xb[u] + o_a) : z) : (PRES & 1 ? lds<E>(xa[u] + o_a) : z);
     const double2 x0 = PRES & 1 ? lds<E>(xa[u] + o_e0) : z;
     const double2 x1 = PRES & 2 ? lds<E>(xb[u] + o_e1) : z;
-    const double2 xt = PRES & 2 ? lds<E>(xb[u] + o_t) : z;
+    const double2 xt = SFT_TAIL5_DMMA ? x1 : (PRES & 2 ? lds<E>(xb[u] + o_t) : z);
     are[u][0] = fma(op.dt0, x1.x, op.ds0 * x0.x);
     are[u][1] = fma(op.dt1, x1.x, op.ds1 * x0.x);
     aim[u][0] = fma(op.dt0, x1.y, op.ds0 * x0.y);
