@@ -42,7 +42,16 @@ __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
 // rotated charge f_j e^{i pi sum_a s_a}, into shared memory; then, leaf by
 // leaf, lane = output element: h^{A0 B}_m = sum_j f'_j prod_a r_{m_a}(s_{j,a}).
 // ------------------------------------------------------------------------
-constexpr int kLeafWin = 24;
+// sources per leaf-kernel warp: kLeafWin, or fewer (down to SFT_LEAF_WIN_MIN)
+// when the K sources are too few to give every SM four warps at kLeafWin
+// (small plans are latency-bound: C1 leaf 13.8 -> 12.3 us at 16 vs 24)
+#ifndef SFT_LEAF_WIN
+#define SFT_LEAF_WIN 24
+#endif
+#ifndef SFT_LEAF_WIN_MIN
+#define SFT_LEAF_WIN_MIN 12
+#endif
+constexpr int kLeafWin = SFT_LEAF_WIN;
 
 template <int D, int P>
 __device__ __forceinline__ void leaf_weights(const double* __restrict__ k_sorted, int64_t N, int j, const double* cdq,
@@ -91,21 +100,24 @@ __device__ __forceinline__ void leaf_weights(const double* __restrict__ k_sorted
 #ifndef SFT_LEAF_MINB2
 #define SFT_LEAF_MINB2 6  // C2 leaf 29.5 -> 26 us (4: 120 registers, 20% warps active)
 #endif
+#ifndef SFT_LEAF_MINB3
+#define SFT_LEAF_MINB3 2
+#endif
 #ifndef SFT_FINAL_MINB2
 #define SFT_FINAL_MINB2 1
 #endif
 #ifndef SFT_FINAL_MINB3
-#define SFT_FINAL_MINB3 1
+#define SFT_FINAL_MINB3 4  // C3 final 32.8 -> 30.8 us (1, 2: the same 32.8)
 #endif
 template <int D, int P, typename T2, int PS>
-__global__ __launch_bounds__(128, D == 2 ? SFT_LEAF_MINB2 : 2) void k_leaf(const double* __restrict__ k_sorted,
+__global__ __launch_bounds__(128, D == 2 ? SFT_LEAF_MINB2 : SFT_LEAF_MINB3) void k_leaf(const double* __restrict__ k_sorted,
                                                               const int32_t* __restrict__ perm,
                                                               const int32_t* __restrict__ first_pt,
                                                               const int32_t* __restrict__ leaf_of,
                                                               const double2* __restrict__ f,
                                                               const double* __restrict__ invD, T2* __restrict__ out,
                                                               int64_t b_lo, int64_t b_hi, int64_t N, int conj,
-                                                              int nrhs, int64_t ldf, int64_t ors, int ffmod) {
+                                                              int nrhs, int64_t ldf, int64_t ors, int ffmod, int win) {
   constexpr int PD = Pow<P, D>::v;
   constexpr int NACC = (PD + 31) / 32;
   constexpr int P1 = P - 1;
@@ -128,7 +140,7 @@ __global__ __launch_bounds__(128, D == 2 ? SFT_LEAF_MINB2 : 2) void k_leaf(const
   const int64_t kw = (int64_t)blockIdx.x * 4 + warp;
   // leaves [lb, le) of this warp: first source in [s0 + W kw, s0 + W (kw+1))
   const int32_t s0 = first_pt[b_lo], s1 = first_pt[b_hi];
-  const int64_t w0 = s0 + (int64_t)kLeafWin * kw, w1 = s0 + (int64_t)kLeafWin * (kw + 1);
+  const int64_t w0 = s0 + (int64_t)win * kw, w1 = s0 + (int64_t)win * (kw + 1);
   if (w0 >= s1) return;
   auto lower = [&](int64_t v) {  // first leaf in [b_lo, b_hi] with first_pt >= v (leaf_of: two loads)
     if (v >= s1) return b_hi;
@@ -326,20 +338,25 @@ __global__ void k_zero(double2* p, int64_t n) {
 cudaError_t launch_leaf(const sft_plan_s* Pl, const double2* f, void* out, int64_t b_lo, int64_t b_hi, int nrhs,
                         int64_t ldf, int64_t ors) {
   if (b_hi <= b_lo) return cudaSuccess;
-  // sources of leaves [b_lo, b_hi): one warp per window of kLeafWin sources
+  // sources of leaves [b_lo, b_hi): one warp per window of win sources
   const int64_t ns = b_lo == 0 && b_hi == Pl->K.counts[Pl->L] ? Pl->nk : Pl->k_src_hi - Pl->k_src_lo;
-  const int64_t nw = (ns + kLeafWin - 1) / kLeafWin;
+  static PerDevice<int> nsm_;
+  int nsm = 0;
+  nsm_.get(&nsm, [](int dev, int* r) { return cudaDeviceGetAttribute(r, cudaDevAttrMultiProcessorCount, dev); });
+  if (nsm <= 0) nsm = 148;
+  const int win = (int)std::max<int64_t>(SFT_LEAF_WIN_MIN, std::min<int64_t>(kLeafWin, ns / (4 * (int64_t)nsm)));
+  const int64_t nw = (ns + win - 1) / win;
   const unsigned nb = (unsigned)((nw + 3) / 4);
   if (Pl->prec == 1) {
     SFT_DISPATCH(Pl->d, Pl->p,
                  launch_pdl(k_leaf<D, P, float2, Pow<P, D>::v + (Pow<P, D>::v & 1)>, nb, 128, 0, Pl->stream,
                      Pl->K.pts_sorted, Pl->K.perm, Pl->K.first_pt, Pl->K.leaf_of, f, Pl->tab->leaf_invD, (float2*)out, b_lo, b_hi,
-                     Pl->N, Pl->conj, nrhs, ldf, ors, Pl->ffmod && !Pl->conj));
+                     Pl->N, Pl->conj, nrhs, ldf, ors, Pl->ffmod && !Pl->conj, win));
   } else {
     SFT_DISPATCH(Pl->d, Pl->p,
                  launch_pdl(k_leaf<D, P, double2, StrideT<double2, Pow<P, D>::v>::v>, nb, 128, 0, Pl->stream,
                      Pl->K.pts_sorted, Pl->K.perm, Pl->K.first_pt, Pl->K.leaf_of, f, Pl->tab->leaf_invD, (double2*)out, b_lo, b_hi,
-                     Pl->N, Pl->conj, nrhs, ldf, ors, Pl->ffmod && !Pl->conj));
+                     Pl->N, Pl->conj, nrhs, ldf, ors, Pl->ffmod && !Pl->conj, win));
   }
   count_launch();
   return cudaGetLastError();
