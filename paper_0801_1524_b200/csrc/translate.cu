@@ -206,6 +206,9 @@ struct UseSym {
 // 33.8 -> 35.5 ms -- three instantiations of the 3D passes cost more)
 #define SFT_CLASS_SPLIT 1
 #endif
+#ifndef SFT_CLASS_SPLIT3
+#define SFT_CLASS_SPLIT3 0  // 3D too
+#endif
 #ifndef SFT_SLOTPAD
 #define SFT_SLOTPAD 0  // 1: measured no gain (C3 0.758 vs 0.756 ms)
 #endif
@@ -1296,7 +1299,7 @@ __device__ __forceinline__ void consumer_pass(const TransArgs& a, E* __restrict_
     // warp-uniform union of the rows' child classes: super-tiles whose rows
     // all lack one child skip its loads (the task lists are class-sorted, so
     // most super-tiles are class-uniform)
-    const unsigned pres = (SFT_CLASS_SPLIT && D == 2 && UseSym<P>::v) ? __reduce_or_sync(0xffffffffu, orc) : 3u;
+    const unsigned pres = (SFT_CLASS_SPLIT && ((D == 2 && UseSym<P>::v) || (D == 3 && SFT_CLASS_SPLIT3))) ? __reduce_or_sync(0xffffffffu, orc) : 3u;
     if constexpr (!UseSym<P>::v) {
       if (pres == 1u) direct_math<D, P, STR, C1, NSUB, E, GL, 1>(op, xa, xb, o0, o1, c);
       else if (pres == 2u) direct_math<D, P, STR, C1, NSUB, E, GL, 2>(op, xa, xb, o0, o1, c);

@@ -17,7 +17,7 @@ def parse(spec):
     out = []
     for kv in spec.split(","):
         k, v = kv.split("=")
-        out.append(f"-DSFT_{k}={v}" if k.startswith(("NSUB", "TAIL", "ROTATE", "ABSENT", "CENTRE", "ABL_", "TMA_", "PAD_", "LEAF_", "FINAL_", "SLOTPAD", "CLASS_", "F32", "PRODUCER", "INSTR", "BS_", "SORT_", "TREE_", "CLUSTER_", "F2_", "ORDER3", "ROUND_", "PL", "SYM5", "TAIL5", "PUBLISH", "CNT3")) else f"-DSFT_WS_{k}={v}")
+        out.append(f"-DSFT_{k}={v}" if k.startswith(("NSUB", "TAIL", "ROTATE", "ABSENT", "CENTRE", "ABL_", "TMA_", "PAD_", "LEAF_", "FINAL_", "SLOTPAD", "CLASS_", "F32", "PRODUCER", "INSTR", "BS_", "SORT_", "TREE_", "CLUSTER_", "F2_", "ORDER3", "ROUND_", "PL", "SYM5", "TAIL5", "PUBLISH", "CNT3", "CLASS_SPLIT3")) else f"-DSFT_WS_{k}={v}")
     return out
 
 
