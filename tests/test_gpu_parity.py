@@ -582,3 +582,60 @@ def test_dynamic_tile_scheduling(name, monkeypatch):
     sel = np.sort(np.random.default_rng(11).choice(len(w.x), 256, replace=False))
     ub_o = oracle.butterfly(w.x, w.k, w.f, w.N, w.p, targets=sel)
     assert_close(runs[0][sel], ub_o, PARITY)
+
+
+@pytest.mark.parametrize("name,p", [("C0", 5), ("C1", 7), ("C1", 9), ("C3", 5)])
+def test_user_buffers_guard_bands(name, p):
+    """Out-of-bounds check without a sanitizer: x, k, f and u live inside larger device buffers
+    whose guard bands (NaN / a bit pattern) must be untouched after plan + apply + apply_batch, the
+    inputs themselves must be unchanged, and u must equal the result on plain buffers bit for bit."""
+    import torch
+    import paper_0801_1524_b200 as sft
+    w = synth.make_workload(name, p=p)
+    d, G = w.dim, 4096
+    nx, nk = len(w.x), len(w.k)
+    PAT = 0x7FF8DEADBEEF1234  # a quiet NaN with a payload
+
+    def guard(n):
+        return torch.full((n,), PAT, dtype=torch.int64).cuda().view(torch.float64)
+
+    def banded(a):
+        t = torch.from_numpy(np.ascontiguousarray(a))
+        flat = t.view(torch.float64).reshape(-1) if t.is_complex() else t.reshape(-1)
+        buf = guard(flat.numel() + 2 * G)
+        buf[G:G + flat.numel()] = flat.cuda()
+        return buf, flat.numel()
+
+    bx, sx = banded(w.x)
+    bk, sk = banded(w.k)
+    bf, sf = banded(w.f)
+    bu = guard(2 * nx + 2 * G)
+    F = np.stack([w.f, synth.random_charges(nk, 77)])
+    bF, sF = banded(F)
+    bU = guard(4 * nx + 2 * G)
+    xv = bx[G:G + sx].view(nx, d)
+    kv = bk[G:G + sk].view(nk, d)
+    fv = torch.view_as_complex(bf[G:G + sf].view(nk, 2))
+    uv = torch.view_as_complex(bu[G:G + 2 * nx].view(nx, 2))
+    Fv = torch.view_as_complex(bF[G:G + sF].view(2, nk, 2))
+    Uv = torch.view_as_complex(bU[G:G + 4 * nx].view(2, nx, 2))
+    with sft.Plan(d, w.N, p, xv, kv) as plan:
+        plan.apply(fv, uv)
+        plan.apply_batch(Fv, Uv)
+        torch.cuda.synchronize()
+    with sft.Plan(d, w.N, p, torch.from_numpy(w.x).cuda(), torch.from_numpy(w.k).cuda()) as plan:
+        ref = plan.apply(torch.from_numpy(w.f).cuda())
+        torch.cuda.synchronize()
+
+    def bands_ok(buf, n):
+        b = buf.view(torch.int64)
+        return bool((b[:G] == PAT).all()) and bool((b[G + n:] == PAT).all())
+
+    for buf, n in ((bx, sx), (bk, sk), (bf, sf), (bu, 2 * nx), (bF, sF), (bU, 4 * nx)):
+        assert bands_ok(buf, n)
+    assert torch.equal(xv.cpu(), torch.from_numpy(w.x))
+    assert torch.equal(kv.cpu(), torch.from_numpy(w.k))
+    assert torch.equal(torch.view_as_real(fv).cpu(), torch.view_as_real(torch.from_numpy(w.f)))
+    assert torch.equal(torch.view_as_real(uv).view(torch.int64), torch.view_as_real(ref).view(torch.int64))
+    assert torch.equal(torch.view_as_real(Uv[0]).view(torch.int64), torch.view_as_real(ref).view(torch.int64))
+    assert not torch.isnan(torch.view_as_real(Uv[1])).any()
